@@ -1,0 +1,86 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+Holds none of the method's arithmetic: only random draws with the shapes and value
+distributions of the paper's workloads.  The paper's data
+(ImageNet, speech) is out of scope; PAPER.md:436 (ResNet, batch 32) and PAPER.md:481-483
+(LSTM: batch 64, 50-d input, 5000-way softmax) fix the shapes we imitate.
+
+Chain (reading A10):  x0 ~ N(0,1); W_l ~ N(0, 1/d); b_l ~ N(0, 0.01^2);
+                      gamma_l ~ 1 + N(0, 0.1^2); beta_l ~ N(0, 0.1^2); labels ~ U{0..d-1}.
+LSTM (reading A13):   x_t ~ N(0,1); W_ih, W_hh, b_ih, b_hh ~ U(+-1/sqrt(H)) (PyTorch
+                      default); W_o ~ N(0, 1/H); b_o = 0; labels ~ U{0..C-1}.
+
+Each tensor gets its own child stream of ``np.random.SeedSequence(seed)`` (spawn order is
+fixed), values are drawn in fp64 and rounded to the working dtype on the host; the oracle
+consumes the same rounded values.  For full-size GPU benches (8 GiB of weights) a device
+generator (torch, seeded) is used instead — a different stream, documented as such.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED = 1604_06174
+
+
+def bf16_values(a):
+    """Round fp64 values to the nearest bf16 (RNE); returns float32 carrying bf16 values."""
+    f = np.asarray(a, dtype=np.float32)
+    b = f.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32)
+
+
+def _streams(seed, k):
+    return [np.random.default_rng(s) for s in np.random.SeedSequence(seed).spawn(k)]
+
+
+def chain_inputs(n_layers, batch, width, dtype="f32", seed=SEED):
+    """Returns dict(W [n,d,d] f32 (bf16-valued when dtype='bf16'), b, gamma, beta [n,d] f32,
+    x0 [B,d] f32, labels [B] int32)."""
+    r = _streams(seed, 6)
+    d = width
+    W = r[0].standard_normal((n_layers, d, d)) / np.sqrt(d)
+    b = r[1].standard_normal((n_layers, d)) * 0.01
+    gamma = 1.0 + r[2].standard_normal((n_layers, d)) * 0.1
+    beta = r[3].standard_normal((n_layers, d)) * 0.1
+    x0 = r[4].standard_normal((batch, d))
+    labels = r[5].integers(0, d, size=batch).astype(np.int32)
+    W = bf16_values(W) if dtype == "bf16" else W.astype(np.float32)
+    return dict(W=W, b=b.astype(np.float32), gamma=gamma.astype(np.float32),
+                beta=beta.astype(np.float32), x0=x0.astype(np.float32), labels=labels)
+
+
+def chain_inputs_torch(n_layers, batch, width, dtype="bf16", seed=SEED, device="cuda"):
+    """Device-side generator with the same distributions (a torch.Generator stream, not the
+    NumPy one).  Returns torch tensors; W is bf16 (or f32), the rest f32, labels int32."""
+    import torch
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    d = width
+    wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    W = torch.empty((n_layers, d, d), dtype=wdt, device=device)
+    for l in range(n_layers):  # layer by layer keeps the fp32 temporary small
+        W[l].copy_(torch.randn((d, d), generator=gen, device=device) / d ** 0.5)
+    b = torch.randn((n_layers, d), generator=gen, device=device) * 0.01
+    gamma = 1.0 + torch.randn((n_layers, d), generator=gen, device=device) * 0.1
+    beta = torch.randn((n_layers, d), generator=gen, device=device) * 0.1
+    x0 = torch.randn((batch, d), generator=gen, device=device)
+    labels = torch.randint(0, d, (batch,), generator=gen, device=device, dtype=torch.int32)
+    return dict(W=W, b=b, gamma=gamma, beta=beta, x0=x0, labels=labels)
+
+
+def lstm_inputs(n_layers, steps, batch, hidden, n_in, n_classes, dtype="f32", seed=SEED):
+    r = _streams(seed + 1, 8)
+    H = hidden
+    k = 1.0 / np.sqrt(H)
+    W_ih = [r[0].uniform(-k, k, (4 * H, n_in if l == 0 else H)) for l in range(n_layers)]
+    W_hh = r[1].uniform(-k, k, (n_layers, 4 * H, H))
+    b_ih = r[2].uniform(-k, k, (n_layers, 4 * H))
+    b_hh = r[3].uniform(-k, k, (n_layers, 4 * H))
+    W_o = r[4].standard_normal((n_classes, H)) / np.sqrt(H)
+    x = r[5].standard_normal((steps, batch, n_in))
+    labels = r[6].integers(0, n_classes, size=(steps, batch)).astype(np.int32)
+    cast = bf16_values if dtype == "bf16" else (lambda a: np.asarray(a, np.float32))
+    return dict(W_ih=[cast(w) for w in W_ih], W_hh=cast(W_hh),
+                b=(b_ih + b_hh).astype(np.float32), W_o=cast(W_o),
+                b_o=np.zeros(n_classes, np.float32), x=x.astype(np.float32), labels=labels)

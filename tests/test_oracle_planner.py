@@ -1,0 +1,406 @@
+"""Pins for the oracle planner (CPU).  Every check here compares the oracle with something
+other than itself: the paper's worked examples / closed forms (tests/golden/*.txt, each
+with its derivation), brute force over all checkpoint sets, or invariants that a dropped
+term / wrong index / wrong tie-break would break."""
+import itertools
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import graph as G
+from oracle import planner as P
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rows(name):
+    out = []
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            out.append(line.split())
+    return out
+
+
+# ------------------------------------------------------------------ topo / validate
+def test_topo_worked_examples():
+    # chain -> [0..n]; diamond 0->{1,2}->3 -> [0,1,2,3] (lowest id first)
+    assert G.topo_order(G.unit_chain(8)) == list(range(9))
+    d = G.Graph([G.Node(G.INPUT, [], 1), G.Node(G.RELU, [0], 1), G.Node(G.RELU, [0], 1),
+                 G.Node(G.ADD, [1, 2], 1)], [3])
+    assert G.topo_order(d) == [0, 1, 2, 3]
+    # ids not in dependency order: node 0 consumes node 2
+    r = G.Graph([G.Node(G.RELU, [2], 1), G.Node(G.INPUT, [], 1), G.Node(G.RELU, [1], 1)], [0])
+    assert G.topo_order(r) == [1, 2, 0]
+
+
+def test_validate_diagnostics():
+    assert G.validate(G.Graph([G.Node(G.INPUT, [], 1)], [0])) == []
+    assert (G.CYCLE, 0) in G.validate(G.Graph([G.Node(G.RELU, [0], 1)], [0]))
+    assert (G.ARITY, 0) in G.validate(G.Graph([G.Node(G.FC, [], 1)], [0]))
+    assert (G.DANGLING, 1) in G.validate(G.Graph([G.Node(G.INPUT, [], 1), G.Node(G.RELU, [7], 1)], [1]))
+    assert (G.ZERO_SIZE, 0) in G.validate(G.Graph([G.Node(G.INPUT, [], 0)], [0]))
+
+
+# ------------------------------------------------------------------ Alg. 3
+@pytest.mark.parametrize("row", _rows("alg3_unit_chain.txt"))
+def test_alg3_worked_examples(row):
+    B, x, y, splits = int(row[0]), int(row[1]), int(row[2]), row[3]
+    g = G.unit_chain(8)
+    xx, yy, m = P.alg3(g, B)
+    assert (xx, yy) == (x, y)
+    want = set() if splits == "-" else {int(s) for s in splits.split(",")}
+    assert {v for v in range(1, 9) if m[v] == 0} == want
+
+
+def _alg3_characterisation(g, B, x, y, m):
+    """Independent check of Alg. 3's output from its definition (not a re-run of the loop):
+    walking the topo order, a split is exactly a candidate at which the running sum since
+    the previous split first exceeds B; x sums split sizes, y is the largest segment sum."""
+    C = P.candidates(g)
+    segs, cur, cur_sum = [], [], 0
+    for v in G.topo_order(g):
+        if g.nodes[v].op == G.INPUT:
+            assert m[v] == 0
+            continue
+        cur.append(v)
+        cur_sum += g.nodes[v].out_bytes
+        if m[v] == 0:
+            assert C[v] and cur_sum > B
+            # no earlier candidate of this segment already exceeded B
+            s = 0
+            for w in cur[:-1]:
+                s += g.nodes[w].out_bytes
+                assert not (C[w] and s > B)
+            segs.append(cur_sum)
+            cur, cur_sum = [], 0
+        else:
+            assert m[v] == 1
+    s = 0
+    for w in cur:
+        s += g.nodes[w].out_bytes
+        assert not (C[w] and s > B)
+    assert x == sum(g.nodes[v].out_bytes for v in range(len(g))
+                    if m[v] == 0 and g.nodes[v].op != G.INPUT)
+    assert y == max(segs + [cur_sum] + [0])
+
+
+def test_alg3_random_chains_against_characterisation():
+    rnd = random.Random(3)
+    for _ in range(100):
+        n = rnd.randint(1, 12)
+        g = G.unit_chain(n)
+        for nd in g.nodes:
+            nd.out_bytes = rnd.randint(1, 9)
+        for nd in g.nodes[1:]:
+            if rnd.random() < 0.2:
+                nd.flags |= G.F_NOT_CANDIDATE
+        B = rnd.randint(0, 40)
+        x, y, m = P.alg3(g, B)
+        _alg3_characterisation(g, B, x, y, m)
+
+
+# ------------------------------------------------------------------ sqrt(n) + exact peaks
+@pytest.mark.parametrize("row", _rows("sqrt_peaks.txt"))
+def test_sqrt_and_nockpt_exact_peaks(row):
+    n, k, L, peak_sqrt, extra, peak_none = map(int, row)
+    u = 3 * 5 * 4
+    g = G.chain_graph(n, 3, 5)
+    ps = P.plan(g, P.S_SQRT)
+    pn = P.plan(g, P.S_NONE)
+    assert ps.alloc.exact_peak == peak_sqrt * u + 4
+    assert ps.extra_forward == extra
+    assert sum(1 for v in range(1, n + 1) if ps.m[v] == 0) == k
+    assert pn.alloc.exact_peak == peak_none * u + 4
+    assert pn.extra_forward == 0
+
+
+def test_sqrt_bound_and_sublinear_slope():
+    # Sec. 4.3 "O(2 sqrt n)"; SPEC acceptance 2: peak <= 2 sqrt(n) + 4 units,
+    # log-log slope in [0.4, 0.6]
+    ns = [16, 64, 256, 1024, 4096]
+    peaks = []
+    for n in ns:
+        g = G.unit_chain(n)
+        p = P.plan(g, P.S_SEARCH)
+        assert p.alloc.exact_peak <= 2 * math.sqrt(n) + 4
+        peaks.append(p.alloc.exact_peak)
+    slope = np.polyfit(np.log(ns), np.log(peaks), 1)[0]
+    assert 0.4 <= slope <= 0.6, slope
+
+
+def test_one_extra_forward_bound():
+    # PAPER.md:323 "only requires an additional forward pass": for plans with m <= 1 every
+    # forward node is re-computed at most once
+    rnd = random.Random(5)
+    for _ in range(30):
+        n = rnd.randint(1, 200)
+        g = G.chain_graph(n, 2, 2)
+        for B in (0, rnd.randint(1, 16 * n), 10 ** 9):
+            p = P.plan(g, P.S_BUDGET, budget=B)
+            assert p.extra_forward <= n + 1
+        assert P.plan(g, P.S_SQRT).extra_forward <= n
+
+
+# ------------------------------------------------------------------ App. A search
+def _brute_force_best(g):
+    """min exact peak over every single-level checkpoint set of a chain (2^(n-1) sets)."""
+    n = len(g) - 2
+    best = None
+    for bits in itertools.product((0, 1), repeat=n - 1):
+        m = [0] + list(bits) + [0, 0]
+        p = P.plan(g, P.S_EXPLICIT, m=m)
+        best = p.alloc.exact_peak if best is None else min(best, p.alloc.exact_peak)
+    return best
+
+
+@pytest.mark.parametrize("n", [3, 6, 9, 12])
+def test_search_vs_brute_force(n):
+    g = G.chain_graph(n, 1, 1)
+    p = P.plan(g, P.S_SEARCH)
+    assert len(p.trace) == 8
+    assert p.alloc.exact_peak >= _brute_force_best(g)
+    assert p.alloc.exact_peak <= P.plan(g, P.S_NONE).alloc.exact_peak
+
+
+def test_search_trace_n1024():
+    # reading A3 at n=1024: x0 = 1024 u, y0 = 1 u, B1 = 32 u; grid B_i =
+    # floor(B1 * 2^((2i-5)/10))
+    u = 1
+    g = G.unit_chain(1024, u)
+    p = P.plan(g, P.S_SEARCH)
+    Bs = [r[0] for r in p.trace]
+    assert Bs[:2] == [0, 32]
+    assert Bs[2:] == [22, 25, 29, 34, 39, 45]
+    assert p.trace[0][1:3] == (1024, 1)
+    assert p.alloc.exact_peak == min(r[3] for r in p.trace)
+
+
+# ------------------------------------------------------------------ recursion
+@pytest.mark.parametrize("row", _rows("recursion.txt"))
+def test_recursion_estimate_worked(row):
+    n, k, units, depth = map(int, row)
+    assert P.recursion_estimate(n, k) == (units, depth)
+
+
+def test_recursion_k1_is_ceil_log2():
+    # PAPER.md:373 "if we set k = 1, we get g(n) = log2 n"; ceil(log2 n) = (n-1).bit_length()
+    for n in list(range(1, 5000)) + [2 ** 20 - 1, 2 ** 20, 2 ** 20 + 1]:
+        assert P.recursion_estimate(n, 1)[0] == (n - 1).bit_length()
+
+
+def test_recursive_plan_log_memory():
+    # Sec. 4.4: O(log n) memory at O(n log n) extra forward
+    peaks, extras = [], []
+    for j in range(2, 11):
+        n = 2 ** j
+        p = P.plan(G.chain_graph(n, 1, 1), P.S_RECURSIVE, k=1)
+        peaks.append((p.alloc.exact_peak - 4) // 4)    # units (u = 1*1*4 bytes)
+        extras.append(p.extra_forward)
+        assert p.extra_forward <= n * j
+        assert max(p.m) <= j
+    # memory grows by a bounded number of units per doubling (log), not proportionally
+    diffs = np.diff(peaks)
+    assert diffs.max() <= 1 and peaks[-1] <= 10 + 2
+    # the executed k=1 plan stores <= ceil(log2 n)+1 boundary values at the top level
+    for n in (4, 16, 64):
+        p = P.plan(G.chain_graph(n, 1, 1), P.S_RECURSIVE, k=1)
+        top = sum(1 for v in range(1, n + 1) if p.m[v] == 0)
+        assert top + 1 <= (n - 1).bit_length() + 1
+
+
+def test_recursive_not_a_chain():
+    d = G.Graph([G.Node(G.INPUT, [], 1), G.Node(G.RELU, [0], 1), G.Node(G.RELU, [0], 1),
+                 G.Node(G.ADD, [1, 2], 1)], [3])
+    with pytest.raises(P.PlanError) as e:
+        P.plan(d, P.S_RECURSIVE, k=1)
+    assert e.value.code == P.E_NOT_A_CHAIN
+
+
+# ------------------------------------------------------------------ Alg. 2
+def test_alg2_all_zero_is_plain_gradient_graph():
+    # PAPER.md:238 "When all the mirror counts are set to 0, the algorithm degenerates to
+    # normal gradient graph": n+2 forward + n+1 gradient nodes, no mirrors
+    n = 7
+    g = G.chain_graph(n, 2, 3)
+    gg = P.build_mirrored(g, [0] * len(g))
+    assert len(gg.order) == (n + 2) + (n + 1)
+    assert all(gg.nodes[v].kind != "mirror" for v in gg.order)
+
+
+def test_alg2_fig3_order_and_validity():
+    # Fig. 3: the backward of segment 2 precedes the re-computation of
+    # segment 1; V' is a topological order of G'; k-th mirror's preds are at level <= k
+    g = G.chain_graph(8, 1, 1)
+    m = [0, 1, 1, 1, 0, 1, 1, 1, 0, 0]
+    gg = P.build_mirrored(g, m)
+    pos = {v: i for i, v in enumerate(gg.order)}
+    g_b4 = gg.g[5]                     # gradient of Block_4 (last of segment 2's backward)
+    first_mirror_seg1 = min(pos[v] for v in gg.order
+                            if gg.nodes[v].kind == "mirror" and gg.nodes[v].orig <= 3)
+    assert pos[g_b4] < first_mirror_seg1
+    for v in gg.order:
+        for p in gg.nodes[v].preds:
+            assert pos[p] < pos[v]
+        if gg.nodes[v].kind == "mirror":
+            for p in gg.nodes[v].preds:
+                assert gg.nodes[p].kind in ("fwd", "mirror") and gg.nodes[p].level <= gg.nodes[v].level
+    assert len(set(gg.order)) == len(gg.order)
+
+
+def test_alg2_extra_forward_counts():
+    # all m=0 -> 0; all non-input m=1 -> n (every block once)
+    n = 10
+    g = G.chain_graph(n, 1, 1)
+    assert P.plan(g, P.S_NONE).extra_forward == 0
+    m = [0] + [1] * n + [0]
+    assert P.plan(g, P.S_EXPLICIT, m=m).extra_forward == n
+
+
+def test_alg2_invalid_plan():
+    g = G.chain_graph(3, 1, 1)
+    with pytest.raises(P.PlanError) as e:
+        P.plan(g, P.S_EXPLICIT, m=[1, 0, 0, 0, 0])
+    assert e.value.code == P.E_INVALID_PLAN
+
+
+# ------------------------------------------------------------------ allocator
+def _forward_only(g):
+    gg = P.GradGraph([P.GNode("fwd", nd.op, v, 0, list(nd.preds), nd.out_bytes,
+                              G.OPS[nd.op].fwd_inplace) for v, nd in enumerate(g.nodes)],
+                     G.topo_order(g), list(range(len(g))), {}, {0, len(g) - 1}, {0, len(g) - 1})
+    return gg
+
+
+@pytest.mark.parametrize("n", [2, 5, 64, 4096])
+def test_inference_chain_o1(n):
+    # PAPER.md:185 "from O(n) to nearly O(1)"; in place -> 1 pool tag,
+    # sharing only -> 2 pool tags (ping-pong), for any n.  (Input and output are external.)
+    g = G.unit_chain(n + 1)
+    gg = _forward_only(g)
+    pool = lambda a: sum(1 for t in range(len(a.tag_size)) if not a.tag_external[t])
+    assert pool(P.allocate(gg, P.A_INPLACE | P.A_SHARING)) == 1
+    assert pool(P.allocate(gg, P.A_SHARING)) == 2
+    assert pool(P.allocate(gg, 0)) == n
+
+
+def test_fig1_two_layer_net():
+    # Fig. 1: fullc -> sigmoid -> fullc -> softmax.  "The first
+    # sigmoid transformation is carried out using inplace operation ... which is then reused
+    # by its backward operation.  The storage of the softmax gradient is shared with the
+    # gradient by the first fully connected layer."
+    g = G.Graph([G.Node(G.INPUT, [], 1), G.Node(G.FC, [0], 1), G.Node(G.SIGMOID, [1], 1),
+                 G.Node(G.FC, [2], 1), G.Node(G.SOFTMAX_CE, [3], 1)], [4])
+    p = P.plan(g, P.S_NONE)
+    t = p.alloc.tag_of
+    gg = p.gg
+    assert t[2] == t[1]                               # sigmoid in place over fullc-1
+    assert t[gg.g[2]] == t[2]                         # sigmoid backward reuses it
+    assert t[gg.g[4]] == t[gg.g[1]]                   # softmax grad shares with fullc-1 grad
+    assert len(p.alloc.tag_size) < len(gg.order)
+
+
+def _random_dag(rnd, n):
+    nodes = [G.Node(G.INPUT, [], rnd.randint(1, 4))]
+    for i in range(1, n):
+        if rnd.random() < 0.1:
+            nodes.append(G.Node(G.INPUT, [], rnd.randint(1, 4)))
+            continue
+        op = rnd.choice([G.FC, G.SIGMOID, G.RELU, G.BN, G.IDENTITY, G.ADD, G.MUL])
+        ar = G.OPS[op].arity_min
+        preds = [rnd.randrange(0, i) for _ in range(ar)]
+        size = rnd.randint(1, 4)
+        if G.OPS[op].fwd_inplace == 0 and rnd.random() < 0.7:
+            size = nodes[preds[0]].out_bytes
+        nodes.append(G.Node(op, preds, size))
+    # single loss consuming the last node
+    nodes.append(G.Node(G.SOFTMAX_CE, [n - 1], 1, G.F_NOT_CANDIDATE))
+    return G.Graph(nodes, [len(nodes) - 1])
+
+
+def _simulate_interference(p):
+    """Replay V' symbolically: tag -> node currently held; every read must see its node."""
+    holds = {}
+    for v in p.gg.order:
+        for q in p.gg.nodes[v].preds:
+            assert holds.get(p.alloc.tag_of[q]) == q, (v, q)
+        holds[p.alloc.tag_of[v]] = v
+
+
+def test_allocator_sound_on_random_dags():
+    # SPEC acceptance 5: zero live-value clobbers over 1,000 random DAGs (<= 64 nodes)
+    rnd = random.Random(11)
+    for it in range(1000):
+        g = _random_dag(rnd, rnd.randint(2, 63))
+        assert G.validate(g) == []
+        strat = rnd.choice([P.S_NONE, P.S_SQRT, P.S_BUDGET, P.S_DROP_CHEAP, P.S_EXPLICIT])
+        kw = {}
+        if strat == P.S_BUDGET:
+            kw["budget"] = rnd.randint(0, 40)
+        if strat == P.S_EXPLICIT:
+            kw["m"] = [0 if g.nodes[v].op == G.INPUT else rnd.randint(0, 3) for v in range(len(g))]
+        p = P.plan(g, strat, **kw)
+        _simulate_interference(p)
+        assert p.alloc.exact_peak <= sum(P.plan(g, strat, alloc_flags=0, **kw).alloc.tag_size)
+        noopt = P.plan(g, strat, alloc_flags=0, **kw)
+        assert noopt.alloc.exact_peak == sum(p.gg.nodes[v].out_bytes for v in p.gg.order)
+
+
+def test_offsets_are_aligned_prefix_sums():
+    p = P.plan(G.chain_graph(16, 3, 5), P.S_SQRT)
+    al = p.alloc
+    run = 0
+    for t, sz in enumerate(al.tag_size):
+        if al.tag_external[t]:
+            assert al.offsets[t] == -1
+            continue
+        assert al.offsets[t] % 256 == 0 and al.offsets[t] >= run
+        assert al.offsets[t] - run < 256
+        run = al.offsets[t] + sz
+    assert al.pool_bytes == run
+
+
+def test_sharing_halves_resnet_shaped_chain():
+    # SPEC acceptance 5 / Fig. 5 "factor of two to three": sharing <= 1/2 no-opt
+    # on an FC-BN-ReLU chain of depth >= 32 (ResNet-proportioned stage sizes 8:4:2:1)
+    nodes = [G.Node(G.INPUT, [], 8)]
+    for stage, sz in enumerate((8, 4, 2, 1)):
+        for _ in range(4):
+            for op in (G.FC, G.BN, G.RELU):
+                nodes.append(G.Node(op, [len(nodes) - 1], sz))
+    nodes.append(G.Node(G.SOFTMAX_CE, [len(nodes) - 1], 1, G.F_NOT_CANDIDATE))
+    g = G.Graph(nodes, [len(nodes) - 1])
+    share = P.plan(g, P.S_NONE).alloc.exact_peak
+    noopt = P.plan(g, P.S_NONE, alloc_flags=0).alloc.exact_peak
+    assert share <= noopt / 2
+    drop = P.plan(g, P.S_DROP_CHEAP).alloc.exact_peak
+    assert drop <= share
+
+
+def test_lstm_graph_time_segments():
+    # Time-axis checkpointing of the unrolled LSTM: keep every layer's
+    # state at segment boundaries; the plan stays sublinear in T and gradients of the kept
+    # plan cover every node.
+    L, T = 2, 16
+    g = G.lstm_graph(L, T, 2, 3, 2)
+    assert G.validate(g) == []
+    seg = 4
+    m = [0] * len(g)
+    for v, nd in enumerate(g.nodes):
+        if nd.op in (G.LSTM_GATES, G.LSTM_CELL):
+            m[v] = 1
+    # S^l_t nodes at t % seg == seg-1 are kept
+    t = -1
+    for v, nd in enumerate(g.nodes):
+        if nd.op == G.INPUT:
+            t += 1
+        if nd.op == G.LSTM_CELL and t % seg == seg - 1:
+            m[v] = 0
+    p = P.plan(g, P.S_EXPLICIT, m=m)
+    _simulate_interference(p)
+    none = P.plan(g, P.S_NONE)
+    assert p.alloc.exact_peak < none.alloc.exact_peak
+    assert len(p.gg.g) == sum(1 for nd in g.nodes if nd.op != G.INPUT)
