@@ -1,0 +1,261 @@
+/*
+ * slm.h — C ABI of the B200-native implementation of arXiv 1604.06174,
+ *         "Training Deep Nets with Sublinear Memory Cost" (Chen, Xu, Zhang, Guestrin 2016).
+ *
+ * The library solves the paper's problem statement: given a computation
+ * graph G=(V, pred) and either a mirror plan m or a memory budget B, produce the memory-
+ * optimised gradient graph, its execution order V' and a static memory plan
+ * ("plan(graph, budget)"), then train with it on the GPU ("step(plan, params, batch)").
+ *
+ *   host planner (plain C++, no CUDA):     slm_graph_*, slm_plan_*, slm_recursion_estimate
+ *   device step (sm_100a, hand-written):   slm_model_*, slm_workspace_bytes, slm_step*
+ *   data parallel (NCCL over NVLink):      slm_comm_*
+ *
+ * Conventions (all functions):
+ *   - Every function returns slm_status: SLM_OK (0) or a negative error code; nothing throws
+ *     across the ABI.  slm_last_error() returns a thread-local description of the last error
+ *     (valid until the next call on the same thread).
+ *   - Host objects (graph, plan, model, comm) are owned by the library through create/destroy
+ *     pairs; input arrays are copied, never retained.
+ *   - Array outputs are caller-allocated.  Passing a capacity smaller than needed returns
+ *     SLM_E_BUFFER_TOO_SMALL and writes the needed count to the *n output (cap = 0 queries).
+ *   - Device memory (params, grads, batch, pool, workspace, loss) is always caller-owned.
+ *     slm_step never allocates device memory: the plan is static ("to
+ *     allocate the memory to each node before the execution starts").
+ *   - slm_step is asynchronous on the caller's stream; argument, shape and size errors are
+ *     reported synchronously, device faults surface at the caller's next synchronisation.
+ *   - Plans are immutable and may be shared between threads; a model or comm object is used
+ *     by one thread at a time.
+ */
+#ifndef SLM_H_
+#define SLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t slm_status;
+enum {
+  SLM_OK = 0,
+  SLM_E_ARG = -1,              /* null pointer, bad enum, negative budget, ...            */
+  SLM_E_GRAPH_INVALID = -2,    /* cycle | arity | dangling pred | zero size   */
+  SLM_E_MULTIPLE_ROOTS = -3,   /* gradient graph needs exactly one loss output     */
+  SLM_E_INVALID_PLAN = -4,     /* m(v) > 0 on an Input node, bad length           */
+  SLM_E_NOT_A_CHAIN = -5,      /* recursive plan on a non-chain graph             */
+  SLM_E_DOMAIN = -6,           /* recursion_estimate / recursive plan with n < 1 or k < 1  */
+  SLM_E_DEGENERATE = -7,       /* sum of node sizes is 0                                  */
+  SLM_E_ORDER = -8,            /* internal: execution order is not a permutation           */
+  SLM_E_SHAPE = -9,            /* model dims do not match the graph / plan                */
+  SLM_E_BUFFER_TOO_SMALL = -10,
+  SLM_E_UNSUPPORTED = -11,     /* configuration outside what the sm_100a kernels implement */
+  SLM_E_CUDA = -20,            /* CUDA runtime/driver error (message in slm_last_error)   */
+  SLM_E_NCCL = -21             /* NCCL error or libnccl.so.2 not loadable                  */
+};
+
+const char* slm_last_error(void);
+/* Library version, e.g. "slm 0.1 sm_100a". */
+const char* slm_version(void);
+
+/* ====================================================================== graph
+ * G = (V, pred) of Alg. 2.  Nodes are dense ids 0..n-1, each producing ONE
+ * output of out_bytes bytes ("each node represents an operation").  Weights
+ * and their gradients are not nodes.  Op kinds carry the metadata the paper
+ * asks frameworks to declare: which inputs/outputs the backward reads
+ * (minimum dependencies) and which input an op may overwrite in place.
+ */
+enum {
+  SLM_OP_INPUT = 0,       /* external input (bound to a caller buffer)                       */
+  SLM_OP_BLOCK = 1,       /* residual block x + ReLU(BN(x)) W^T + b; bwd reads its input      */
+  SLM_OP_SOFTMAX_CE = 2,  /* mean softmax cross-entropy loss; bwd reads its input            */
+  SLM_OP_FC = 3,          /* fully connected; bwd reads its input                            */
+  SLM_OP_SIGMOID = 4,     /* bwd reads its output (Fig. 1 sigmoid)         */
+  SLM_OP_RELU = 5,        /* bwd reads its output                                            */
+  SLM_OP_BN = 6,          /* batch-norm (no running stats); bwd reads its input              */
+  SLM_OP_ADD = 7,         /* 2 inputs                                                        */
+  SLM_OP_MUL = 8,         /* 2 inputs; bwd reads both                                        */
+  SLM_OP_IDENTITY = 9,
+  SLM_OP_LSTM_GATES = 10, /* (x_or_lower_state[, prev_state]); bwd reads output and inputs    */
+  SLM_OP_LSTM_CELL = 11,  /* (gates[, prev_state]); bwd reads both inputs                     */
+  SLM_OP_HEAD_CE = 12,    /* per-step softmax head + CE; bwd reads its input                  */
+  SLM_OP_SUM = 13         /* scalar sum of any number of inputs                               */
+};
+enum {
+  SLM_NODE_NOT_CANDIDATE = 1, /* exclude from Alg. 3's candidate set C         */
+  SLM_NODE_PIN = 2,           /* never recycle this node's storage                          */
+  SLM_NODE_REQUEST_GRAD = 4   /* (Input) keep the gradient flowing into this input          */
+};
+
+typedef struct {
+  int32_t op;             /* SLM_OP_*                                                      */
+  int32_t n_preds;
+  const int32_t* preds;   /* n_preds node ids (copied)                                      */
+  int64_t out_bytes;      /* > 0                                                            */
+  int32_t flags;          /* SLM_NODE_*                                                     */
+} slm_node_desc;
+
+enum { SLM_DIAG_CYCLE = 1, SLM_DIAG_ARITY = 2, SLM_DIAG_DANGLING = 3, SLM_DIAG_ZERO_SIZE = 4,
+       SLM_DIAG_BAD_OUTPUT = 5, SLM_DIAG_BAD_OP = 6 };
+typedef struct { int32_t code; int32_t node; } slm_diag;
+
+typedef struct slm_graph slm_graph;
+
+/* Diagnostics are data, not errors: returns SLM_OK with *n_diags = 0 for a valid graph. */
+slm_status slm_graph_validate(const slm_node_desc* nodes, int32_t n, const int32_t* outputs,
+                              int32_t n_out, slm_diag* diags, int32_t cap, int32_t* n_diags);
+/* Validates and copies; SLM_E_GRAPH_INVALID if any diagnostic. */
+slm_status slm_graph_create(const slm_node_desc* nodes, int32_t n, const int32_t* outputs,
+                            int32_t n_out, slm_graph** out);
+/* Residual chain X_0 -> Block_0..Block_{n-1} -> SoftmaxCE (node 0 = Input, node l+1 =
+ * Block_l, node n+1 = loss, 4 bytes, NOT_CANDIDATE).  Node sizes batch*width*4 (fp32 x). */
+slm_status slm_graph_chain(int32_t n_layers, int32_t batch, int32_t width, slm_graph** out);
+/* Unrolled LSTM: per step t an Input X_t (batch*n_in*4), per layer
+ * G^l_t (batch*4H*4) and S^l_t (batch*2H*4), a head H_t (4 bytes); final Sum (the loss). */
+slm_status slm_graph_lstm(int32_t n_layers, int32_t steps, int32_t batch, int32_t hidden,
+                          int32_t n_in, slm_graph** out);
+slm_status slm_graph_size(const slm_graph* g, int32_t* n_nodes);
+/* topological-order(V) of Alg. 2: Kahn, lowest id first among ready nodes. */
+slm_status slm_graph_topo(const slm_graph* g, int32_t* order, int32_t cap, int32_t* n);
+void slm_graph_destroy(slm_graph* g);
+
+/* ====================================================================== plan
+ * Strategies choose the mirror-count function m: V -> N:
+ *   NONE        m = 0 everywhere (ordinary gradient graph)
+ *   SQRT        Sec. 4.3: k = ceil(sqrt n) segments over the candidates
+ *   BUDGET      Alg. 3 with budget_bytes
+ *   SEARCH      App. A grid search over B; trace of 8 evaluated budgets
+ *   RECURSIVE   Sec. 4.4 recursion with k kept results per level; chains
+ *   EXPLICIT    user-set mirror counts ("set the mirror attribute")
+ *   DROP_CHEAP  Sec. 4.2 drop results of low-cost ops
+ * then Alg. 2 builds G' and V' and the Fig. 2 allocator assigns temporal
+ * tags with in-place and sharing.  Readings of silent points: DESIGN.md
+ * A1-A20.  Tags of Input nodes and of the loss are bound to caller buffers (offset -1); all
+ * other tags get 256-byte-aligned offsets in one pool of pool_bytes.  exact_peak = sum of
+ * all tag sizes (unaligned, external tags included) = the paper's "exact memory cost"
+ * (PAPER.md:334, 397).
+ */
+enum { SLM_PLAN_NONE = 0, SLM_PLAN_SQRT = 1, SLM_PLAN_BUDGET = 2, SLM_PLAN_SEARCH = 3,
+       SLM_PLAN_RECURSIVE = 4, SLM_PLAN_EXPLICIT = 5, SLM_PLAN_DROP_CHEAP = 6 };
+enum { SLM_ALLOC_INPLACE = 1, SLM_ALLOC_SHARING = 2 };
+
+typedef struct {
+  int32_t strategy;       /* SLM_PLAN_*                                                    */
+  int32_t k;              /* RECURSIVE: results kept per level (>= 1)                       */
+  int64_t budget_bytes;   /* BUDGET: B >= 0                                                 */
+  const int32_t* m;       /* EXPLICIT: n_nodes mirror counts (copied)                       */
+  int32_t n_m;
+  int32_t alloc_flags;    /* SLM_ALLOC_INPLACE | SLM_ALLOC_SHARING (0 = "no optimization")  */
+  int32_t align;          /* pool offset alignment in bytes, power of two; 0 -> 256         */
+} slm_plan_opts;
+
+typedef struct slm_plan slm_plan;
+slm_status slm_plan_create(const slm_graph* g, const slm_plan_opts* opts, slm_plan** out);
+
+typedef struct {
+  int32_t n_nodes;        /* nodes of G' (forward + all mirrors + gradient nodes)           */
+  int32_t n_order;        /* |V'| (dead mirrors are not in V', reading A7)                  */
+  int32_t n_tags;
+  int32_t n_trace;        /* SEARCH: 8; else 0                                              */
+  int32_t extra_forward;  /* mirror nodes in V' = re-computed forward ops                   */
+  int32_t max_m;
+  int64_t exact_peak;     /* bytes                                                          */
+  int64_t pool_bytes;     /* bytes the caller must provide to slm_step                      */
+  int64_t x, y, budget;   /* Alg. 3 outputs for BUDGET / SEARCH          */
+} slm_plan_info;
+slm_status slm_plan_get_info(const slm_plan* p, slm_plan_info* info);
+/* m over the forward nodes (checkpoint set = {v : m(v) = 0}); cap >= n forward nodes. */
+slm_status slm_plan_mirror(const slm_plan* p, int32_t* m, int32_t cap, int32_t* n);
+
+enum { SLM_KIND_FWD = 0, SLM_KIND_MIRROR = 1, SLM_KIND_GRAD = 2 };
+/* Nodes of G' in CSR form: per node kind, op, orig (forward node it mirrors/differentiates),
+ * level (mirror level), out_bytes, inplace_slot; preds in pred_ptr[i]..pred_ptr[i+1].
+ * cap_nodes >= n_nodes, cap_preds >= total preds (query with cap 0). */
+slm_status slm_plan_nodes(const slm_plan* p, int32_t* kind, int32_t* op, int32_t* orig,
+                          int32_t* level, int64_t* out_bytes, int32_t* inplace_slot,
+                          int32_t* pred_ptr, int32_t cap_nodes, int32_t* preds,
+                          int32_t cap_preds, int32_t* n_preds_total);
+/* V'. */
+slm_status slm_plan_order(const slm_plan* p, int32_t* order, int32_t cap, int32_t* n);
+/* node_tag[n_nodes] (-1 for nodes not in V'); tag_size/tag_offset[n_tags] (offset -1 =
+ * external: bound to an Input buffer or the loss). */
+slm_status slm_plan_tags(const slm_plan* p, int32_t* node_tag, int32_t cap_nodes,
+                         int64_t* tag_size, int64_t* tag_offset, int32_t cap_tags);
+/* App. A trace rows (B, x, y, exact_peak, extra_forward), 5 int64 per row. */
+slm_status slm_plan_trace(const slm_plan* p, int64_t* rows, int32_t cap_rows, int32_t* n);
+void slm_plan_destroy(slm_plan* p);
+
+/* Eq. 2 g(n) = k + g(n/(k+1)) iterated with ceiling division. */
+slm_status slm_recursion_estimate(int64_t n, int64_t k, int64_t* units, int64_t* depth);
+
+/* ====================================================================== device step
+ * The training step of the chain: executes V' on the GPU, writing
+ * every node into its planned pool slot; forward, re-computation (mirrors) and backward
+ * run hand-written sm_100a kernels (tcgen05/TMEM GEMMs fed by TMA in bf16 mode, fp32 FFMA
+ * kernels in f32 mode).  There is no CPU fallback: without an sm_100a device every step
+ * call returns SLM_E_CUDA / SLM_E_UNSUPPORTED.
+ */
+enum { SLM_F32 = 0, SLM_BF16 = 1 };
+enum { SLM_MODEL_CHAIN = 0, SLM_MODEL_LSTM = 1 };
+
+/* Chain parameters, all device pointers, row-major, caller-owned:
+ *   W      [n][d][d]  (out, in)  fp32 (SLM_F32) or bf16 (SLM_BF16)
+ *   b, gamma, beta    [n][d] fp32
+ *   dW     [n][d][d]  same dtype as W (bf16 grads are rounded from fp32 accumulators)
+ *   db, dgamma, dbeta [n][d] fp32
+ * Gradients are overwritten by every step, not accumulated.  batch_global = total batch
+ * over all data-parallel ranks (the loss is the mean over it); 0 means batch. */
+typedef struct {
+  int32_t dtype;
+  int32_t n_layers, batch, width, batch_global;
+  const void* W; const float* b; const float* gamma; const float* beta;
+  void* dW; float* db; float* dgamma; float* dbeta;
+} slm_chain_desc;
+
+typedef struct slm_model slm_model;
+slm_status slm_model_chain(const slm_chain_desc* desc, slm_model** out);
+void slm_model_destroy(slm_model* m);
+/* Options: use_graph = capture the whole step in a CUDA graph (default 1). */
+slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
+/* Per-kernel scratch (bf16 operand copies, BN statistics, loss partials): the paper's
+ * "temporal memory", not part of the feature-map plan. */
+slm_status slm_workspace_bytes(const slm_plan* p, const slm_model* m, size_t* bytes);
+/* Kernels launched by one slm_step of this (plan, model) — for launch accounting. */
+slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* launches);
+
+typedef struct slm_comm slm_comm;
+
+/* step(plan, params, batch) -> loss, grads.
+ *   x0      device [batch][d] fp32 (bound to the Input node's tag)
+ *   labels  device [batch] int32 in [0, d)
+ *   pool    device, >= plan pool_bytes, 256-byte aligned
+ *   ws      device, >= slm_workspace_bytes, 256-byte aligned
+ *   loss    device, 1 float (bound to the loss node's tag)
+ *   stream  cudaStream_t (NULL = legacy default stream)
+ *   comm    NULL for one GPU; else gradients are all-reduced (sum) over the ranks in
+ *           buckets overlapped with the rest of the backward, and loss is the global mean. */
+slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32_t* labels,
+                    void* pool, size_t pool_bytes, void* ws, size_t ws_bytes, float* loss,
+                    void* stream, slm_comm* comm);
+/* The same step with HOST inputs/outputs (the end-to-end path): copies x0_host/labels_host
+ * (pinned host memory recommended) into x0_dev/labels_dev on the stream, runs slm_step and
+ * copies the loss back into *loss_host; synchronises the stream before returning. */
+slm_status slm_step_host(const slm_plan* p, slm_model* m, const float* x0_host,
+                         const int32_t* labels_host, void* x0_dev, int32_t* labels_dev,
+                         void* pool, size_t pool_bytes, void* ws, size_t ws_bytes,
+                         float* loss_dev, float* loss_host, void* stream, slm_comm* comm);
+
+/* ====================================================================== data parallel
+ * One process per GPU.  The caller distributes a 128-byte unique id (e.g. broadcast over a
+ * torch.distributed process group) and each rank calls slm_comm_init.  NCCL is loaded at
+ * run time (libnccl.so.2); bucket_bytes groups per-layer gradients into all-reduce buckets. */
+slm_status slm_comm_unique_id(void* id128);
+slm_status slm_comm_init(int32_t rank, int32_t world, const void* id128, int64_t bucket_bytes,
+                         slm_comm** out);
+void slm_comm_destroy(slm_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLM_H_ */

@@ -1,0 +1,292 @@
+"""B200-native sublinear-memory training (arXiv 1604.06174) — Python binding of libslm.
+
+Thin wrappers over the C ABI (include/slm.h), same names, argument marshalling only:
+
+    g    = Graph.chain(n_layers, batch, width)            # slm_graph_chain
+    plan = Plan(g, "sqrt")                                # slm_plan_create  (plan(graph, budget))
+    mdl  = ChainModel(params, grads, dtype="bf16")        # slm_model_chain
+    loss = mdl.step(plan, x0, labels)                     # slm_step         (step(plan, params, batch))
+
+PyTorch is used only for device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _lib
+from ._lib import check, lib
+
+__all__ = ["Graph", "Plan", "ChainModel", "Comm", "recursion_estimate", "STRATEGY", "OP", "lib"]
+
+STRATEGY = {"none": 0, "sqrt": 1, "budget": 2, "search": 3, "recursive": 4, "explicit": 5,
+            "drop_cheap": 6}
+OP = dict(input=0, block=1, softmax_ce=2, fc=3, sigmoid=4, relu=5, bn=6, add=7, mul=8,
+          identity=9, lstm_gates=10, lstm_cell=11, head_ce=12, sum=13)
+ALLOC_INPLACE, ALLOC_SHARING = 1, 2
+NODE_NOT_CANDIDATE, NODE_PIN, NODE_REQUEST_GRAD = 1, 2, 4
+
+
+def _i32arr(xs):
+    return (C.c_int32 * max(1, len(xs)))(*xs)
+
+
+class Graph:
+    """slm_graph: G = (V, pred)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def chain(cls, n_layers, batch, width):
+        h = C.c_void_p()
+        check(lib.slm_graph_chain(n_layers, batch, width, C.byref(h)), "slm_graph_chain")
+        return cls(h)
+
+    @classmethod
+    def lstm(cls, n_layers, steps, batch, hidden, n_in):
+        h = C.c_void_p()
+        check(lib.slm_graph_lstm(n_layers, steps, batch, hidden, n_in, C.byref(h)), "slm_graph_lstm")
+        return cls(h)
+
+    @staticmethod
+    def _descs(nodes):
+        keep = []
+        arr = (_lib.NodeDesc * max(1, len(nodes)))()
+        for i, (op, preds, size, flags) in enumerate(nodes):
+            p = _i32arr(list(preds))
+            keep.append(p)
+            arr[i] = _lib.NodeDesc(op, len(preds), C.cast(p, _lib.i32p), size, flags)
+        return arr, keep
+
+    @classmethod
+    def from_nodes(cls, nodes, outputs):
+        """nodes: list of (op, preds, out_bytes, flags)."""
+        arr, keep = cls._descs(nodes)
+        outs = _i32arr(outputs)
+        h = C.c_void_p()
+        check(lib.slm_graph_create(arr, len(nodes), outs, len(outputs), C.byref(h)), "slm_graph_create")
+        return cls(h)
+
+    @classmethod
+    def validate(cls, nodes, outputs):
+        arr, keep = cls._descs(nodes)
+        outs = _i32arr(outputs)
+        n = C.c_int32()
+        cap = 4 * len(nodes) + 8
+        diags = (_lib.Diag * cap)()
+        check(lib.slm_graph_validate(arr, len(nodes), outs, len(outputs), diags, cap, C.byref(n)),
+              "slm_graph_validate")
+        return [(diags[i].code, diags[i].node) for i in range(n.value)]
+
+    def __len__(self):
+        n = C.c_int32()
+        check(lib.slm_graph_size(self._h, C.byref(n)))
+        return n.value
+
+    def topo(self):
+        n = len(self)
+        out = (C.c_int32 * max(1, n))()
+        cnt = C.c_int32()
+        check(lib.slm_graph_topo(self._h, out, n, C.byref(cnt)), "slm_graph_topo")
+        return list(out[: cnt.value])
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.slm_graph_destroy(self._h)
+            self._h = None
+
+
+class Plan:
+    """slm_plan: mirror plan m, gradient graph G', V' and the Fig. 2 memory plan."""
+
+    def __init__(self, graph, strategy="sqrt", budget=0, k=1, m=None,
+                 alloc_flags=ALLOC_INPLACE | ALLOC_SHARING, align=256):
+        s = STRATEGY[strategy] if isinstance(strategy, str) else int(strategy)
+        marr = _i32arr(list(m)) if m is not None else None
+        opts = _lib.PlanOpts(s, k, budget, C.cast(marr, _lib.i32p) if marr is not None else None,
+                             len(m) if m is not None else 0, alloc_flags, align)
+        h = C.c_void_p()
+        check(lib.slm_plan_create(graph._h, C.byref(opts), C.byref(h)), "slm_plan_create")
+        self._h = h
+        self.graph = graph
+        info = _lib.PlanInfo()
+        check(lib.slm_plan_get_info(h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in _lib.PlanInfo._fields_}
+
+    def __getattr__(self, k):
+        info = self.__dict__.get("info")
+        if info is not None and k in info:
+            return info[k]
+        raise AttributeError(k)
+
+    @property
+    def m(self):
+        n = len(self.graph)
+        out = (C.c_int32 * max(1, n))()
+        cnt = C.c_int32()
+        check(lib.slm_plan_mirror(self._h, out, n, C.byref(cnt)))
+        return list(out[: cnt.value])
+
+    @property
+    def order(self):
+        n = self.info["n_order"]
+        out = (C.c_int32 * max(1, n))()
+        cnt = C.c_int32()
+        check(lib.slm_plan_order(self._h, out, n, C.byref(cnt)))
+        return list(out[: cnt.value])
+
+    @property
+    def nodes(self):
+        nn = self.info["n_nodes"]
+        tot = C.c_int32()
+        lib.slm_plan_nodes(self._h, None, None, None, None, None, None, None, 0, None, 0, C.byref(tot))
+        arrs = [(C.c_int32 * max(1, nn))() for _ in range(4)]
+        ob = (C.c_int64 * max(1, nn))()
+        ip = (C.c_int32 * max(1, nn))()
+        pp = (C.c_int32 * (nn + 1))()
+        preds = (C.c_int32 * max(1, tot.value))()
+        check(lib.slm_plan_nodes(self._h, *arrs, ob, ip, pp, nn, preds, tot.value, C.byref(tot)))
+        out = []
+        for i in range(nn):
+            out.append(dict(kind=arrs[0][i], op=arrs[1][i], orig=arrs[2][i], level=arrs[3][i],
+                            out_bytes=ob[i], inplace_slot=ip[i], preds=list(preds[pp[i]:pp[i + 1]])))
+        return out
+
+    @property
+    def tags(self):
+        nn, nt = self.info["n_nodes"], self.info["n_tags"]
+        nt_ = (C.c_int32 * max(1, nn))()
+        ts = (C.c_int64 * max(1, nt))()
+        to = (C.c_int64 * max(1, nt))()
+        check(lib.slm_plan_tags(self._h, nt_, nn, ts, to, nt))
+        return list(nt_[:nn]), list(ts[:nt]), list(to[:nt])
+
+    @property
+    def trace(self):
+        n = self.info["n_trace"]
+        rows = (C.c_int64 * max(1, 5 * n))()
+        cnt = C.c_int32()
+        check(lib.slm_plan_trace(self._h, rows, n, C.byref(cnt)))
+        return [tuple(rows[5 * i:5 * i + 5]) for i in range(cnt.value)]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.slm_plan_destroy(self._h)
+            self._h = None
+
+
+def recursion_estimate(n, k):
+    u, d = C.c_int64(), C.c_int64()
+    check(lib.slm_recursion_estimate(n, k, C.byref(u), C.byref(d)), "slm_recursion_estimate")
+    return u.value, d.value
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class Comm:
+    """slm_comm: NCCL communicator built from a unique id broadcast over torch.distributed."""
+
+    def __init__(self, rank, world, pg=None, bucket_bytes=256 << 20):
+        import torch
+        import torch.distributed as dist
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            check(lib.slm_comm_unique_id(uid), "slm_comm_unique_id")
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        if world > 1:
+            obj = [t]
+            dist.broadcast_object_list(obj, src=0, group=pg)
+            t = obj[0]
+        for i in range(128):
+            uid[i] = int(t[i])
+        h = C.c_void_p()
+        check(lib.slm_comm_init(rank, world, uid, bucket_bytes, C.byref(h)), "slm_comm_init")
+        self._h, self.rank, self.world = h, rank, world
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.slm_comm_destroy(self._h)
+            self._h = None
+
+
+class ChainModel:
+    """slm_model for the residual chain.  params/grads: dicts of CUDA tensors
+    W [n,d,d] (bf16 or f32), b/gamma/beta [n,d] f32; dW like W; db/dgamma/dbeta f32."""
+
+    def __init__(self, params, grads, dtype="bf16", batch=None, batch_global=0, **options):
+        W = params["W"]
+        n, d = W.shape[0], W.shape[1]
+        self.params, self.grads = params, grads
+        self.dtype = dtype
+        self.n, self.d = n, d
+        self.batch = batch
+        desc = _lib.ChainDesc(1 if dtype == "bf16" else 0, n, batch, d, batch_global,
+                              _ptr(W), _ptr(params["b"]), _ptr(params["gamma"]), _ptr(params["beta"]),
+                              _ptr(grads["W"]), _ptr(grads["b"]), _ptr(grads["gamma"]), _ptr(grads["beta"]))
+        h = C.c_void_p()
+        check(lib.slm_model_chain(C.byref(desc), C.byref(h)), "slm_model_chain")
+        self._h = h
+        for k, v in options.items():
+            self.set_option(k, v)
+        self._bufs = {}
+
+    def set_option(self, key, value):
+        check(lib.slm_model_set_option(self._h, key.encode(), int(value)), "slm_model_set_option")
+
+    def workspace_bytes(self, plan):
+        n = C.c_size_t()
+        check(lib.slm_workspace_bytes(plan._h, self._h, C.byref(n)), "slm_workspace_bytes")
+        return n.value
+
+    def launches(self, plan):
+        n = C.c_int64()
+        check(lib.slm_step_launches(plan._h, self._h, C.byref(n)))
+        return n.value
+
+    def buffers(self, plan, device="cuda"):
+        """Caller-owned pool (plan.pool_bytes) + workspace + loss scalar, cached per plan."""
+        import torch
+        key = id(plan)
+        if key not in self._bufs:
+            pool = torch.empty(max(256, plan.pool_bytes), dtype=torch.uint8, device=device)
+            ws = torch.empty(self.workspace_bytes(plan), dtype=torch.uint8, device=device)
+            loss = torch.zeros(1, dtype=torch.float32, device=device)
+            self._bufs[key] = (plan, pool, ws, loss)
+        return self._bufs[key][1:]
+
+    def step(self, plan, x0, labels, stream=None, comm=None, bufs=None):
+        """step(plan, params, batch) -> loss (device tensor); grads written into `grads`."""
+        import torch
+        pool, ws, loss = bufs if bufs is not None else self.buffers(plan, x0.device)
+        st = stream if stream is not None else torch.cuda.current_stream(x0.device)
+        check(lib.slm_step(plan._h, self._h, _ptr(x0), _ptr(labels), _ptr(pool), pool.numel(), _ptr(ws),
+                           ws.numel(), _ptr(loss), C.c_void_p(st.cuda_stream),
+                           comm._h if comm is not None else None), "slm_step")
+        return loss
+
+    def step_host(self, plan, x0_host, labels_host, x0_dev, labels_dev, loss_host, stream=None,
+                  comm=None, bufs=None):
+        """End-to-end step from (pinned) host tensors; returns the host loss value."""
+        import torch
+        pool, ws, loss = bufs if bufs is not None else self.buffers(plan, x0_dev.device)
+        st = stream if stream is not None else torch.cuda.current_stream(x0_dev.device)
+        check(lib.slm_step_host(plan._h, self._h, _ptr(x0_host), _ptr(labels_host), _ptr(x0_dev),
+                                _ptr(labels_dev), _ptr(pool), pool.numel(), _ptr(ws), ws.numel(),
+                                _ptr(loss), _ptr(loss_host), C.c_void_p(st.cuda_stream),
+                                comm._h if comm is not None else None), "slm_step_host")
+        return float(loss_host[0])
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.slm_model_destroy(self._h)
+            self._h = None
+
+
+def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None):
+    """Test hook (include/slm_debug.h)."""
+    import torch
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    check(lib.slm_debug_gemm(kind, impl, bn, M, N, K, _ptr(A), _ptr(B), _ptr(out), _ptr(resid),
+                             _ptr(bias), C.c_void_p(st.cuda_stream)), "slm_debug_gemm")

@@ -1,0 +1,58 @@
+"""Builds libslm.so in-tree: host planner (g++) + sm_100a runtime/kernels (nvcc).
+
+The library is the product: `paper_1604_06174_b200._lib` loads it with ctypes and fails
+loudly if it is missing.  nvcc cross-compiles sm_100a without a GPU.
+"""
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "build")
+LIB = os.path.join(PKG, "libslm.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+INC = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+
+
+def _run(cmd):
+    print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC))
+
+
+def up_to_date():
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    deps = sources() + [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
+    return all(os.path.getmtime(f) <= t for f in deps)
+
+
+def build(force=False, verbose_ptxas=False):
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    o = os.path.join(BUILD, "planner.o")
+    _run(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", *INC, "-c", os.path.join(CSRC, "planner.cpp"), "-o", o])
+    objs.append(o)
+    o = os.path.join(BUILD, "runtime.o")
+    flags = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH, *INC]
+    if verbose_ptxas:
+        flags += ["-Xptxas", "-v"]
+    _run([NVCC, *flags, "-c", os.path.join(CSRC, "runtime.cu"), "-o", o])
+    objs.append(o)
+    tmp = LIB + ".tmp"
+    _run([NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-cudart", "static", "-ldl", "-lpthread"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -1,0 +1,263 @@
+// tcgen05 (5th-gen tensor core) GEMM for sm_100a: TMA -> shared memory (128B swizzle) ->
+// tcgen05.mma (kind::f16, bf16 x bf16 -> fp32 accumulator in TMEM) -> tcgen05.ld epilogue.
+//
+//   D[m][n] = sum_k A(m,k) * B(n,k)      tile 128 x BN x 64, K pipelined over STAGES
+//
+// Operands are either K-major (rows of K contiguous: X[rows][K]) or MN-major (X[K][MN]),
+// selected per operand at compile time; that covers the three contractions of a residual
+// block without any transpose copies:
+//   forward      D[f_out][b]  = W[f_out][:] . a[b][:]        A K-major,  B K-major
+//   backward dX  D[f_in][b]   = W[:][f_in] . g[b][:]         A MN-major, B K-major
+//   backward dW  D[f_in][f_out] = a[:][f_in] . g[:][f_out]    A MN-major, B MN-major
+// "swap-AB": the feature dimension is M (one TMEM lane per feature), the batch is N, so the
+// epilogue writes out[n*ld + m] with a warp covering 32 consecutive features (coalesced).
+//
+// Warp roles (128 threads, one CTA per output tile): warp 0 lane 0 = TMA producer and TMEM
+// allocator, warp 1 lane 0 = MMA issuer; afterwards all 4 warps drain TMEM (warp w owns
+// lanes 32w..32w+31).  Barriers: full[s]/empty[s] per stage (TMA <-> MMA), one accumulator
+// barrier (MMA -> epilogue) signalled by tcgen05.commit.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace slmk {
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: thread i of the warp gets lane (base+i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start address, leading and
+// stride byte offsets (16-byte units), version 1 (sm_100), layout SWIZZLE_128B (= 2).
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // version
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor for kind::f16: fp32 accumulate, bf16 A/B, majorness, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------- epilogues
+// Each receives (m, n, acc) for 32 consecutive n of one m per call.
+struct EpiResid {  // forward: out[n*ld+m] = resid[n*ld+m] + acc + bias[m]  (out may alias resid)
+  float* out;
+  const float* resid;
+  const float* bias;
+  long ld;
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+    const float bm = bias[m];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      long o = (long)(n0 + j) * ld + m;
+      out[o] = __fadd_rn(resid[o], __fadd_rn(acc[j], bm));
+    }
+  }
+};
+struct EpiStoreF32 {  // out[n*ld+m] = acc
+  float* out;
+  long ld;
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[(long)(n0 + j) * ld + m] = acc[j];
+  }
+};
+struct EpiStoreBF16 {  // out[n*ld+m] = bf16(acc)
+  __nv_bfloat16* out;
+  long ld;
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[(long)(n0 + j) * ld + m] = __float2bfloat16_rn(acc[j]);
+  }
+};
+
+// ---------------------------------------------------------------- the kernel
+template <int BN, bool A_MN, bool B_MN>
+struct TcCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (STAGE * 4 <= 200 * 1024) ? 4 : 3;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// a_row0/b_row0: row offsets added to the tensor-map coordinates of A / B (e.g. layer l's
+// weight block inside the [n*d, d] weight tensor).
+template <int BN, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(128, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int K, int a_row0, int b_row0, Epi epi) {
+  using C = TcCfg<BN, A_MN, B_MN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accum = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
+  const int nk = K / C::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(accum, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % C::STAGES;
+      if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * C::STAGE;
+      uint8_t* sb = sa + C::A_BYTES;
+      mbar_expect_tx(&full[s], C::STAGE);
+      const int k0 = kb * C::BK;
+      if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
+        tma_load_2d(sa, &tmA, &full[s], m0, a_row0 + k0);
+        tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, a_row0 + k0);
+      } else {     // A stored [M][K]: one box of 64(K) x 128(M)
+        tma_load_2d(sa, &tmA, &full[s], k0, a_row0 + m0);
+      }
+      if (B_MN) {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, b_row0 + k0);
+      } else {
+        tma_load_2d(sb, &tmB, &full[s], k0, b_row0 + n0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===== MMA issuer
+    constexpr uint32_t idesc = make_idesc(C::BM, BN, A_MN, B_MN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % C::STAGES;
+      mbar_wait(&full[s], (kb / C::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * C::STAGE);
+      const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < C::BK / 16; ++kk) {
+        // K-major SW128: +32 B per K=16 inside the 128-B row; SBO = 8 rows * 128 B.
+        // MN-major SW128: +16 rows * 128 B per K=16; LBO = 64-element MN chunk (8 KiB box).
+        uint64_t ad = A_MN ? make_sdesc(sa + kk * 2048, 8192, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
+        uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
+        tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
+      }
+      tc_commit(&empty[s]);
+    }
+    tc_commit(accum);
+  }
+  __syncwarp();
+  // ===== epilogue: TMEM -> registers -> global
+  mbar_wait(accum, 0);
+  tc_fence_after();
+  const int m = m0 + warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    float acc[32];
+    tmem_ld32(trow + c, acc);
+    epi(m, n0 + c, acc);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+}
+
+}  // namespace slmk

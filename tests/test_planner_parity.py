@@ -1,0 +1,155 @@
+"""C++ planner (libslm) vs the independent Python oracle: plans, checkpoint sets, V', tags
+and pool offsets must match byte for byte (north_star; SURVEY 8(c) parity contract)."""
+import random
+
+import pytest
+
+import paper_1604_06174_b200 as slm
+from oracle import graph as G
+from oracle import planner as P
+
+KIND = {"fwd": 0, "mirror": 1, "grad": 2}
+
+
+def _cxx_graph(g):
+    if g.kind == "chain" and "batch" in g.dims:
+        return slm.Graph.chain(g.dims["n_layers"], g.dims["batch"], g.dims["width"])
+    if g.kind == "lstm":
+        d = g.dims
+        return slm.Graph.lstm(d["n_layers"], d["steps"], d["batch"], d["hidden"], d["n_in"])
+    return slm.Graph.from_nodes([(nd.op, nd.preds, nd.out_bytes, nd.flags) for nd in g.nodes], g.outputs)
+
+
+def assert_same_plan(g, strategy, **kw):
+    po = P.plan(g, strategy, **kw)
+    cg = _cxx_graph(g)
+    pc = slm.Plan(cg, strategy, **kw)
+    assert pc.m == po.m
+    assert pc.order == po.gg.order
+    nodes = pc.nodes
+    assert len(nodes) == len(po.gg.nodes)
+    for a, b in zip(nodes, po.gg.nodes):
+        assert (a["kind"], a["op"], a["orig"], a["level"], a["out_bytes"], a["inplace_slot"], a["preds"]) == \
+               (KIND[b.kind], b.op, b.orig, b.level, b.out_bytes, b.inplace_slot, b.preds)
+    node_tag, tsize, toff = pc.tags
+    for v in po.gg.order:
+        assert node_tag[v] == po.alloc.tag_of[v]
+    assert tsize == po.alloc.tag_size
+    assert toff == po.alloc.offsets
+    assert pc.exact_peak == po.alloc.exact_peak
+    assert pc.pool_bytes == po.alloc.pool_bytes
+    assert pc.extra_forward == po.extra_forward
+    assert (pc.x, pc.y, pc.budget) == (po.x, po.y, po.B)
+    assert pc.trace == [tuple(r) for r in po.trace]
+    return pc, po
+
+
+@pytest.mark.parametrize("strategy,kw", [("none", {}), ("sqrt", {}), ("search", {}),
+                                         ("budget", {"budget": 5 * 2048}),
+                                         ("recursive", {"k": 1}), ("recursive", {"k": 3}),
+                                         ("drop_cheap", {})])
+def test_c1_chain(strategy, kw):
+    assert_same_plan(G.chain_graph(16, 8, 64), P.__dict__["S_" + strategy.upper()], **kw)
+
+
+@pytest.mark.parametrize("strategy", [P.S_NONE, P.S_SQRT, P.S_SEARCH])
+def test_c2_chain(strategy):
+    pc, po = assert_same_plan(G.chain_graph(1024, 256, 2048), strategy)
+    if strategy == P.S_SQRT:
+        assert pc.exact_peak == 64 * 256 * 2048 * 4 + 4
+
+
+@pytest.mark.parametrize("strategy,kw", [(P.S_SEARCH, {}), (P.S_RECURSIVE, {"k": 1}),
+                                         (P.S_RECURSIVE, {"k": 2}), (P.S_SQRT, {}),
+                                         (P.S_BUDGET, {"budget": 40 * 2 ** 21})])
+def test_c4_chain_1000(strategy, kw):
+    assert_same_plan(G.chain_graph(1000, 256, 2048), strategy, **kw)
+
+
+def test_c4_resnet_shaped_budget_sweep():
+    # ResNet-shaped 1000-layer chain (4 stages x 250 layers, bottleneck output bytes at batch 32)
+    sizes = [102760448] * 250 + [51380224] * 250 + [25690112] * 250 + [12845056] * 250
+    nodes = [G.Node(G.INPUT, [], sizes[0])]
+    for i, s in enumerate(sizes):
+        nodes.append(G.Node(G.FC, [i], s))
+    nodes.append(G.Node(G.SOFTMAX_CE, [len(sizes)], 4, G.F_NOT_CANDIDATE))
+    g = G.Graph(nodes, [len(nodes) - 1])
+    assert_same_plan(g, P.S_SEARCH)
+    tot = sum(sizes)
+    for i in range(0, 64, 9):
+        B = int(max(sizes) * (tot / max(sizes)) ** (i / 63))
+        assert_same_plan(g, P.S_BUDGET, budget=B)
+
+
+def test_lstm_graph_plan():
+    g = G.lstm_graph(2, 24, 4, 8, 3)
+    m = [0] * len(g)
+    t = -1
+    for v, nd in enumerate(g.nodes):
+        if nd.op == G.INPUT:
+            t += 1
+        if nd.op in (G.LSTM_GATES, G.LSTM_CELL) and not (nd.op == G.LSTM_CELL and t % 5 == 4):
+            m[v] = 1
+    assert_same_plan(g, P.S_EXPLICIT, m=m)
+    assert_same_plan(g, P.S_SEARCH)
+    assert_same_plan(g, P.S_NONE)
+
+
+def _random_dag(rnd, n):
+    nodes = [G.Node(G.INPUT, [], rnd.randint(1, 5) * 64)]
+    for i in range(1, n):
+        if rnd.random() < 0.1:
+            nodes.append(G.Node(G.INPUT, [], rnd.randint(1, 5) * 64))
+            continue
+        op = rnd.choice([G.FC, G.SIGMOID, G.RELU, G.BN, G.IDENTITY, G.ADD, G.MUL, G.BLOCK])
+        preds = [rnd.randrange(0, i) for _ in range(G.OPS[op].arity_min)]
+        size = rnd.randint(1, 5) * 64 + rnd.choice([0, 0, 7])
+        if G.OPS[op].fwd_inplace == 0 and rnd.random() < 0.7:
+            size = nodes[preds[0]].out_bytes
+        flags = G.F_NOT_CANDIDATE if rnd.random() < 0.1 else 0
+        nodes.append(G.Node(op, preds, size, flags))
+    nodes.append(G.Node(G.SOFTMAX_CE, [n - 1], 4, G.F_NOT_CANDIDATE))
+    return G.Graph(nodes, [len(nodes) - 1])
+
+
+def test_random_dags():
+    rnd = random.Random(1234)
+    for it in range(300):
+        g = _random_dag(rnd, rnd.randint(2, 60))
+        s = rnd.choice([P.S_NONE, P.S_SQRT, P.S_BUDGET, P.S_SEARCH, P.S_DROP_CHEAP, P.S_EXPLICIT])
+        kw = {}
+        if s == P.S_BUDGET:
+            kw["budget"] = rnd.randint(0, 3000)
+        if s == P.S_EXPLICIT:
+            kw["m"] = [0 if nd.op == G.INPUT else rnd.randint(0, 3) for nd in g.nodes]
+        flags = rnd.choice([3, 3, 1, 2, 0])
+        assert_same_plan(g, s, alloc_flags=flags, **kw)
+
+
+def test_random_chains_all_strategies():
+    rnd = random.Random(99)
+    for it in range(60):
+        n = rnd.randint(1, 300)
+        g = G.chain_graph(n, rnd.choice([1, 8, 64]), rnd.choice([3, 64]))
+        for s, kw in [(P.S_SQRT, {}), (P.S_SEARCH, {}), (P.S_RECURSIVE, {"k": rnd.randint(1, 4)}),
+                      (P.S_BUDGET, {"budget": rnd.randint(0, 10 ** 6)})]:
+            assert_same_plan(g, s, **kw)
+
+
+def test_validate_and_errors_match():
+    d = [(G.RELU, [0], 1, 0)]
+    assert slm.Graph.validate(d, [0]) == [(G.CYCLE, 0)]
+    assert slm.Graph.validate([(G.FC, [], 1, 0)], [0]) == [(G.ARITY, 0)]
+    assert slm.Graph.validate([(G.INPUT, [], 1, 0), (G.RELU, [7], 1, 0)], [1]) == [(G.DANGLING, 1)]
+    assert slm.Graph.validate([(G.INPUT, [], 0, 0)], [0]) == [(G.ZERO_SIZE, 0)]
+    g = slm.Graph.chain(3, 1, 1)
+    with pytest.raises(slm._lib.SlmError) as e:
+        slm.Plan(g, "explicit", m=[1, 0, 0, 0, 0])
+    assert e.value.code == -4
+    dg = slm.Graph.from_nodes([(G.INPUT, [], 1, 0), (G.RELU, [0], 1, 0), (G.RELU, [0], 1, 0),
+                               (G.ADD, [1, 2], 1, 0)], [3])
+    with pytest.raises(slm._lib.SlmError) as e:
+        slm.Plan(dg, "recursive", k=1)
+    assert e.value.code == -5
+    for n, k in [(1024, 1), (81, 2), (1, 3), (10 ** 12, 1)]:
+        assert slm.recursion_estimate(n, k) == P.recursion_estimate(n, k)
