@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the sqrt(n)-checkpointed training step (arXiv 1604.06174) on B200.
+
+Workload (BASELINE.json configs[1], the config `metric` is quoted on): 1,024-layer residual
+GEMM+BN+ReLU chain, width 2048, batch 256 per GPU, bf16 GEMM operands (fp32 stream),
+sqrt(n) segmentation (k = 32), synthetic seeded data/weights (synth.chain_inputs_torch).
+
+One "step" = one pass of the whole hot path: forward (keeping only segment outputs), loss,
+re-computation of every segment and backward into the planned pool.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--layers n] [--strategy sqrt|none|search|recursive] [--no-baseline]
+
+N > 1: launched by torchrun, one process per GPU, data parallel over the batch (weak
+scaling: 256 samples per rank), gradients all-reduced in buckets with NCCL inside slm_step.
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the reference arm of
+this tier: there is no reference implementation, PAPER.md is the authority).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec + peak activation GB vs n (ckpt vs no-ckpt) at 1/2/4/8 B200"
+UNIT = "samples/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ======================================================================= reference arm
+def run_reference(args):
+    """The CPU oracle as it stands (fp64 NumPy, bf16-operand emulation), timed on this box's
+    host cores on a bounded sample of the same workload, scaled to samples/s of the full
+    n-layer step (cost is linear in n at fixed width/batch)."""
+    import numpy as np
+
+    import synth
+    from oracle import chain as OC
+    from oracle import graph as OG
+    from oracle import planner as OP
+
+    n, B, d = args.layers, args.batch, args.width
+    ns = args.ref_layers
+    inp = synth.chain_inputs(ns, B, d, dtype="bf16")
+    Pm = OC.Params(inp["W"], inp["b"], inp["gamma"], inp["beta"])
+    plan = OP.plan(OG.chain_graph(ns, B, d), OP.S_SQRT)
+    for _ in range(args.warmup if args.impl == "reference" else 1):
+        OC.step_planned(plan, Pm, inp["x0"], inp["labels"], "bf16")
+    ts = []
+    for _ in range(max(1, args.steps if args.impl == "reference" else 1)):
+        t0 = time.perf_counter()
+        OC.step_planned(plan, Pm, inp["x0"], inp["labels"], "bf16")
+        ts.append(time.perf_counter() - t0)
+    t_sample = statistics.median(ts)
+    # a sqrt-plan step runs 4n - k block GEMMs (n forward, n - k re-computed, 2n backward)
+    gemms = lambda L: 4 * L - (math.isqrt(L - 1) + 1)
+    t_full = t_sample * gemms(n) / gemms(ns)
+    value = B / t_full
+    try:
+        import threadpoolctl
+        cores = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()) or os.cpu_count()
+    except Exception:
+        cores = os.cpu_count()
+    sample = (f"oracle step_planned (fp64 NumPy, bf16-operand emulation, sqrt plan) on {ns} of {n} "
+              f"layers at full width {d} / batch {B}, median of {len(ts)}; per-step time scaled by "
+              f"GEMM count (4n-k) to n={n}")
+    return dict(value=value, unit=UNIT, cores=cores, kind="oracle", sample=sample,
+                ms_per_step=t_full * 1e3, sample_s=t_sample)
+
+
+# ======================================================================= our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=1024)
+    ap.add_argument("--width", type=int, default=2048)
+    ap.add_argument("--batch", type=int, default=256, help="per-GPU batch")
+    ap.add_argument("--strategy", default="sqrt")
+    ap.add_argument("--ref-layers", type=int, default=16)
+    ap.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-nockpt", action="store_true", help="skip the non-checkpointed comparison")
+    ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_reference(args)
+        line = dict(metric=METRIC, value=r["value"], unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
+                    scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                    impl="reference",
+                    config=dict(workload=f"chain n={args.layers} d={args.width} B={args.batch} "
+                                         f"sqrt(n) checkpointed step (BASELINE configs[1])",
+                                n_layers=args.layers, width=args.width, batch=args.batch,
+                                strategy="sqrt"),
+                    cpu_baseline=dict(value=r["value"], unit=UNIT, cores=r["cores"], kind="oracle",
+                                      sample=r["sample"]),
+                    e2e=dict(value=r["value"], unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_06174_b200 as slm
+    import synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, B, d = args.layers, args.batch, args.width
+    Bg = B * world
+    inp = synth.chain_inputs_torch(n, B * world, d, dtype="bf16", device=dev)
+    x0 = inp["x0"][rank * B:(rank + 1) * B].contiguous()
+    labels = inp["labels"][rank * B:(rank + 1) * B].contiguous()
+    params = {k: inp[k] for k in ("W", "b", "gamma", "beta")}
+    grads = {k: torch.empty_like(v) for k, v in params.items()}
+    opts = {}
+    if args.bn:
+        f, x, w = (int(v) for v in args.bn.split(","))
+        opts = dict(bn_fwd=f, bn_dx=x, bn_dw=w)
+    model = slm.ChainModel(params, grads, dtype="bf16", batch=B, batch_global=Bg, **opts)
+    comm = slm.Comm(rank, world) if world > 1 else None
+    graph = slm.Graph.chain(n, B, d)
+    stream = torch.cuda.Stream(dev)
+
+    def timed(plan, steps, warmup, with_clocks=False):
+        bufs = model.buffers(plan, dev)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = Clocks(local) if with_clocks else None
+        if clk:
+            clk.__enter__()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(steps):
+                loss = model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        return ms, float(loss.item()), clk.summary() if clk else None
+
+    plan = slm.Plan(graph, args.strategy)
+    torch.cuda.synchronize()
+    base_mem = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    ms, loss, clocks = timed(plan, args.steps, args.warmup, with_clocks=True)
+    act_measured = torch.cuda.max_memory_allocated(dev) - base_mem   # pool + workspace + loss
+    value = Bg / (ms / 1e3)
+    launches = model.launches(plan)
+
+    # ---- roofline of the dominant kernel: per-kernel CUDA events on the launching stream
+    model.set_option("profile_events", 1)
+    bufs = model.buffers(plan, dev)
+    prof_steps = max(1, min(args.steps, 3))
+    with torch.cuda.stream(stream):
+        model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+    torch.cuda.synchronize()
+    model.kernel_times(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(prof_steps):
+            model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    kt = model.kernel_times(reset=True)
+    prof_ms = e0.elapsed_time(e1) / prof_steps
+    model.set_option("profile_events", 0)
+    pk = _peaks()
+    gemm_flop = 2.0 * B * d * d          # every GEMM kind: 2*B*d^2 per launch
+    gemm_ms = sum(kt[k][0] for k in ("gemm_fwd", "gemm_dx", "gemm_dw"))
+    gemm_cnt = sum(kt[k][1] for k in ("gemm_fwd", "gemm_dx", "gemm_dw"))
+    avg_ms = gemm_ms / max(1, gemm_cnt)
+    achieved = gemm_flop / (avg_ms / 1e3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    kernel_share = {k: round(v[0] / max(1e-9, sum(x[0] for x in kt.values())), 4) for k, v in kt.items()}
+    per_kind = {k: {"avg_us": round(1e3 * v[0] / max(1, v[1]), 3), "launches": v[1] // prof_steps}
+                for k, v in kt.items()}
+    roofline = dict(bound="tensor", achieved=round(achieved, 2), peak=peak, unit="TFLOP/s",
+                    frac=round(achieved / peak, 4), traffic=None,
+                    kernel="tc_gemm_kernel (forward, dX, dW GEMMs; 2*B*d^2 FLOP per launch)",
+                    peak_source="MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
+                    if "_fallback" not in pk else "fallback (B200_PROFILING.md)",
+                    per_kind=per_kind, share_of_kernel_time=kernel_share,
+                    step_ms_with_events=round(prof_ms, 3))
+    step_flop = 2.0 * B * d * d * (4 * n - math.isqrt(max(0, n - 1)) - 1 if args.strategy == "sqrt" else 3 * n)
+
+    # ---- non-checkpointed step (the "vs no-ckpt" half of the metric)
+    nock = None
+    if not args.no_nockpt:
+        plan0 = slm.Plan(graph, "none")
+        torch.cuda.synchronize()
+        base0 = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        ms0, loss0, _ = timed(plan0, max(3, args.steps // 2), 3)
+        act0 = torch.cuda.max_memory_allocated(dev) - base0
+        nock = dict(value=Bg / (ms0 / 1e3), ms_per_step=ms0, loss=loss0, plan_exact_peak_gb=plan0.exact_peak / 1e9,
+                    pool_gb=plan0.pool_bytes / 1e9, measured_activation_gb=act0 / 1e9,
+                    bitwise_equal_loss=(loss0 == loss))
+        model._bufs.pop(id(plan0), None)
+        del plan0
+        torch.cuda.empty_cache()
+
+    # ---- end to end: the public API with HOST buffers (pinned), H2D/D2H inside the region
+    x0_h = x0.cpu().pin_memory()
+    y_h = labels.cpu().pin_memory()
+    loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+    x0_d = torch.empty_like(x0)
+    y_d = torch.empty_like(labels)
+    e2e_bufs = model.buffers(plan, dev)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            model.step_host(plan, x0_h, y_h, x0_d, y_d, loss_h, stream=stream, comm=comm, bufs=e2e_bufs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    k2 = max(3, args.steps // 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(k2):
+            model.step_host(plan, x0_h, y_h, x0_d, y_d, loss_h, stream=stream, comm=comm, bufs=e2e_bufs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / k2
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e = dict(value=Bg / (e2e_ms / 1e3), unit=UNIT, ms_per_step=round(e2e_ms, 3),
+               h2d_bytes_per_step=x0.numel() * 4 + labels.numel() * 4, d2h_bytes_per_step=4)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_baseline and world == 1:
+        r = run_reference(args)
+        cpu = dict(value=r["value"], unit=UNIT, cores=r["cores"], kind="oracle", sample=r["sample"])
+
+    line = dict(
+        metric=METRIC, value=round(value, 3), unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=round(ms, 4), higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+        data="synthetic (seeded torch generator; W~N(0,1/d), x0~N(0,1))",
+        config=dict(workload=f"chain n={n} d={d} B={B}/GPU {args.strategy} checkpointed step "
+                             f"(BASELINE configs[1]{' / configs[4] DP' if world > 1 else ''})",
+                    n_layers=n, width=d, batch_per_gpu=B, global_batch=Bg, strategy=args.strategy,
+                    parallelism=f"dp{world}", l2="inputs > L2: 8.6 GB of bf16 weights streamed 4x per step",
+                    segments=math.isqrt(n - 1) + 1 if args.strategy == "sqrt" else None),
+        roofline=roofline,
+        cpu_baseline=cpu,
+        e2e=e2e,
+        gpu_launches=int(launches * args.steps),
+        clocks=clocks,
+        loss=loss,
+        step_tflops=round(step_flop / (ms / 1e3) / 1e12, 2),
+        activation_gb=dict(plan_exact_peak=plan.exact_peak / 1e9, pool=plan.pool_bytes / 1e9,
+                           workspace=model.workspace_bytes(plan) / 1e9, measured=act_measured / 1e9,
+                           extra_forward=plan.extra_forward),
+        nockpt=nock,
+        ckpt_over_nockpt_time=round(ms / nock["ms_per_step"], 4) if nock else None,
+    )
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

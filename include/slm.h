@@ -216,8 +216,20 @@ typedef struct {
 typedef struct slm_model slm_model;
 slm_status slm_model_chain(const slm_chain_desc* desc, slm_model** out);
 void slm_model_destroy(slm_model* m);
-/* Options: use_graph = capture the whole step in a CUDA graph (default 1). */
+/* Options (int64 values):
+ *   use_graph       capture the whole step in a CUDA graph per buffer set (default 1)
+ *   gemm_impl       0 = tcgen05/TMA tensor-core GEMMs (bf16, default), 1 = SIMT FFMA GEMMs
+ *   bn_fwd, bn_dx, bn_dw   N tile of the forward / dX / dW tcgen05 GEMMs (32|64|128|256)
+ *   profile_events  1 = record a CUDA event pair around every kernel of the step, by kind
+ *                   (read with slm_model_kernel_times after the stream is synchronised) */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
+/* Kernel kinds for slm_model_kernel_times. */
+enum { SLM_K_BN_ACT = 0, SLM_K_GEMM_FWD = 1, SLM_K_GEMM_DX = 2, SLM_K_GEMM_DW = 3, SLM_K_BN_BWD = 4,
+       SLM_K_CE = 5, SLM_K_COUNT = 6 };
+/* Sum of event-timed durations (ms) and launch counts per kind since the last reset,
+ * accumulated over every step run with profile_events = 1; reset = 1 clears them. */
+slm_status slm_model_kernel_times(slm_model* m, float* ms, int64_t* count, int32_t n_kinds,
+                                  int32_t reset);
 /* Per-kernel scratch (bf16 operand copies, BN statistics, loss partials): the paper's
  * "temporal memory", not part of the feature-map plan. */
 slm_status slm_workspace_bytes(const slm_plan* p, const slm_model* m, size_t* bytes);

@@ -240,6 +240,14 @@ class ChainModel:
         check(lib.slm_workspace_bytes(plan._h, self._h, C.byref(n)), "slm_workspace_bytes")
         return n.value
 
+    def kernel_times(self, reset=True):
+        """{kind: (total_ms, count)} of the event-timed kernels (option profile_events=1)."""
+        n = len(_lib.K_KINDS)
+        ms = (C.c_float * n)()
+        cnt = (C.c_int64 * n)()
+        check(lib.slm_model_kernel_times(self._h, ms, cnt, n, int(reset)), "slm_model_kernel_times")
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(_lib.K_KINDS)}
+
     def launches(self, plan):
         n = C.c_int64()
         check(lib.slm_step_launches(plan._h, self._h, C.byref(n)))

@@ -100,3 +100,6 @@ def check(code, where=""):
     if code != 0:
         raise SlmError(code, where)
     return code
+
+_sig("slm_model_kernel_times", i32, vp, f32p, i64p, i32, i32)
+K_KINDS = ["bn_act", "gemm_fwd", "gemm_dx", "gemm_dw", "bn_bwd", "ce"]

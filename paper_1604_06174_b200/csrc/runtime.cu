@@ -182,8 +182,33 @@ struct slm_model {
   CUtensorMap mW_K, mW_MN, mA_K, mA_MN, mG_K[2], mG_MN[2];
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
+  // profile_events: (start, end, kind) per kernel, read by slm_model_kernel_times
+  int profile = 0;
+  struct EvPair {
+    cudaEvent_t a, b;
+    int kind;
+  };
+  std::vector<EvPair> ev_live;
+  std::vector<cudaEvent_t> ev_free;
+  double acc_ms[SLM_K_COUNT] = {};
+  int64_t acc_cnt[SLM_K_COUNT] = {};
+  cudaEvent_t get_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
   ~slm_model() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& p : ev_live) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
   }
 };
 
@@ -333,22 +358,41 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
                                                                     ldo, resid, bias);
   };
 
+  // optional per-kernel CUDA events (profile_events), recorded on the launching stream
+  cudaEvent_t ev0 = nullptr;
+  auto pbeg = [&]() {
+    if (m.profile) {
+      ev0 = m.get_event();
+      cudaEventRecord(ev0, st);
+    }
+  };
+  auto pend = [&](int kind) {
+    if (m.profile) {
+      cudaEvent_t e1 = m.get_event();
+      cudaEventRecord(e1, st);
+      m.ev_live.push_back({ev0, e1, kind});
+    }
+  };
+
   for (const Op& o : ops) {
     const int l = o.layer;
     if (o.type == 0 || o.type == 3) {
       // K1: statistics + activation operand of x_l (forward input, or x_l in the backward)
       const float* xin = X(o.type == 0 ? o.in_tag : o.aux_tag);
+      pbeg();
       if (bf16)
         bn_act_kernel<__nv_bfloat16><<<colgrid, blk, 0, st>>>(xin, gam + (size_t)l * d, bet + (size_t)l * d, B,
                                                               d, stats, (__nv_bfloat16*)abuf);
       else
         bn_act_kernel<float><<<colgrid, blk, 0, st>>>(xin, gam + (size_t)l * d, bet + (size_t)l * d, B, d,
                                                       stats, (float*)abuf);
+      pend(SLM_K_BN_ACT);
       ++nl;
     }
     if (o.type == 0) {
       const float* xin = X(o.in_tag);
       float* xout = X(o.out_tag);
+      pbeg();
       if (tc) {
         slmk::EpiResid epi{xout, xin, bvec + (size_t)l * d, d};
         if ((s = launch_tc_bn<slmk::EpiResid, false, false>(m.bn_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0, epi,
@@ -361,18 +405,23 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         simt_gemm((const float*)abuf, (long)d, 1L, (const float*)m.d.W + l * Wl, (long)d, 1L, xout, (long)d,
                   B, d, d, xin, bvec + (size_t)l * d, true);
       }
+      pend(SLM_K_GEMM_FWD);
       ++nl;
     } else if (o.type == 1) {
+      pbeg();
       ce_fwd_kernel<<<B, 256, 0, st>>>(X(o.in_tag), labels, d, rowloss);
       ce_reduce_kernel<<<1, 256, 0, st>>>(rowloss, B, inv_bg, X(o.out_tag));
+      pend(SLM_K_CE);
       nl += 2;
     } else if (o.type == 2) {
       float* dxn = X(o.out_tag);
+      pbeg();
       if (bf16)
         ce_bwd_kernel<__nv_bfloat16><<<B, 256, 0, st>>>(X(o.in_tag), labels, d, inv_bg, dxn, gq[0]);
       else
         ce_bwd_kernel<float><<<B, 256, 0, st>>>(X(o.in_tag), labels, d, inv_bg, dxn, (float*)nullptr);
       colsum_kernel<<<colgrid, blk, 0, st>>>(dxn, B, d, m.d.db + (size_t)(n - 1) * d);
+      pend(SLM_K_CE);
       gpar = 0;
       nl += 2;
     } else {  // type 3: backward of Block_l
@@ -382,28 +431,41 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       if (tc) {
         // da[b][f_in] = sum_k g[b][k] W_l[k][f_in]
         slmk::EpiStoreF32 e1{da, d};
+        pbeg();
         if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false>(m.bn_dx, m.mW_MN, m.mG_K[gpar], d, B, d, l * d,
                                                               0, e1, st)) != SLM_OK)
           return s;
+        pend(SLM_K_GEMM_DX);
         // dW_l[f_out][f_in] = sum_b g[b][f_out] a[b][f_in]
         slmk::EpiStoreBF16 e2{(__nv_bfloat16*)m.d.dW + l * Wl, d};
+        pbeg();
         if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true>(m.bn_dw, m.mA_MN, m.mG_MN[gpar], d, d, B, 0, 0,
                                                               e2, st)) != SLM_OK)
           return s;
+        pend(SLM_K_GEMM_DW);
       } else if (bf16) {
         const __nv_bfloat16* gqp = gq[gpar];
+        pbeg();
         simt_gemm(gqp, (long)d, 1L, (const __nv_bfloat16*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
                   (const float*)nullptr, (const float*)nullptr, false);
+        pend(SLM_K_GEMM_DX);
+        pbeg();
         simt_gemm(gqp, 1L, (long)d, (const __nv_bfloat16*)abuf, 1L, (long)d,
                   (__nv_bfloat16*)m.d.dW + l * Wl, (long)d, d, d, B, (const float*)nullptr,
                   (const float*)nullptr, false);
+        pend(SLM_K_GEMM_DW);
       } else {
+        pbeg();
         simt_gemm(g, (long)d, 1L, (const float*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
                   (const float*)nullptr, (const float*)nullptr, false);
+        pend(SLM_K_GEMM_DX);
+        pbeg();
         simt_gemm(g, 1L, (long)d, (const float*)abuf, 1L, (long)d, (float*)m.d.dW + l * Wl, (long)d, d, d,
                   B, (const float*)nullptr, (const float*)nullptr, false);
+        pend(SLM_K_GEMM_DW);
       }
       float* dbp = l > 0 ? m.d.db + (size_t)(l - 1) * d : nullptr;
+      pbeg();
       if (bf16)
         bn_bwd_kernel<__nv_bfloat16><<<colgrid, blk, 0, st>>>(da, xl, stats, gam + (size_t)l * d,
                                                               bet + (size_t)l * d, g, dxl, B, d,
@@ -413,8 +475,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         bn_bwd_kernel<float><<<colgrid, blk, 0, st>>>(da, xl, stats, gam + (size_t)l * d, bet + (size_t)l * d,
                                                       g, dxl, B, d, m.d.dgamma + (size_t)l * d,
                                                       m.d.dbeta + (size_t)l * d, dbp, (float*)nullptr);
+      pend(SLM_K_BN_BWD);
       gpar ^= 1;
-      nl += 4;
+      nl += 3;
       // data-parallel: all-reduce the bucket [l, bucket_hi] once its last layer is done
       if (comm && comm->world > 1 && (bucket_hi - l + 1 >= bucket_layers || l == 0)) {
         const int lo = l, cnt = bucket_hi - l + 1;
@@ -520,6 +583,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "bn_fwd") m->bn_fwd = (int)value;
   else if (k == "bn_dx") m->bn_dx = (int)value;
   else if (k == "bn_dw") m->bn_dw = (int)value;
+  else if (k == "profile_events") m->profile = (int)value;
   else {
     set_error("unknown option " + k);
     return SLM_E_ARG;
@@ -527,6 +591,33 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   m->graphs.clear();
   m->maps_ws = nullptr;
+  return SLM_OK;
+}
+
+slm_status slm_model_kernel_times(slm_model* m, float* ms, int64_t* count, int32_t n_kinds, int32_t reset) {
+  if (!m) {
+    set_error("null model");
+    return SLM_E_ARG;
+  }
+  for (auto& p : m->ev_live) {
+    CK(cudaEventSynchronize(p.b));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, p.a, p.b));
+    m->acc_ms[p.kind] += t;
+    m->acc_cnt[p.kind] += 1;
+    m->ev_free.push_back(p.a);
+    m->ev_free.push_back(p.b);
+  }
+  m->ev_live.clear();
+  for (int k = 0; k < n_kinds && k < SLM_K_COUNT; ++k) {
+    if (ms) ms[k] = (float)m->acc_ms[k];
+    if (count) count[k] = m->acc_cnt[k];
+  }
+  if (reset)
+    for (int k = 0; k < SLM_K_COUNT; ++k) {
+      m->acc_ms[k] = 0;
+      m->acc_cnt[k] = 0;
+    }
   return SLM_OK;
 }
 
@@ -544,7 +635,7 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   std::vector<Op> ops;
   if ((s = lower(p, &ops)) != SLM_OK) return s;
   int64_t nl = 0;
-  for (auto& o : ops) nl += (o.type == 0) ? 2 : (o.type == 3 ? 5 : 2);
+  for (auto& o : ops) nl += (o.type == 3) ? 4 : 2;
   *launches = nl;
   return SLM_OK;
 }
@@ -583,7 +674,7 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     return SLM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (!m->use_graph || st == nullptr) return enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
+  if (!m->use_graph || st == nullptr || m->profile) return enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
   GraphKey key{p, x0, labels, pool, ws, loss, st, comm};
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {

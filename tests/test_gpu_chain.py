@@ -1,0 +1,171 @@
+"""Device parity of the checkpointed training step through the C ABI (slm_step).
+
+  * GPU vs the fp64 oracle: <= 1e-4 relative (f32, C1) and <= 2e-2 (bf16, against the
+    bf16-operand-emulating oracle) per tensor, ||g_gpu - g_ref|| / ||g_ref|| (reading A12).
+  * checkpointed GPU step == non-checkpointed GPU step, bit for bit, for every strategy.
+  * full C2 size (n=1024, d=2048, B=256): the same bit-exactness plus closed forms.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import chain as OC
+from oracle import graph as OG
+from oracle import planner as OP
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def slm():
+    import paper_1604_06174_b200 as m
+    return m
+
+
+def _dev(inp, dtype):
+    wdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    p = dict(W=torch.tensor(inp["W"]).to(wdt).cuda(), b=torch.tensor(inp["b"]).cuda(),
+             gamma=torch.tensor(inp["gamma"]).cuda(), beta=torch.tensor(inp["beta"]).cuda())
+    g = dict(W=torch.empty_like(p["W"]), b=torch.empty_like(p["b"]), gamma=torch.empty_like(p["gamma"]),
+             beta=torch.empty_like(p["beta"]))
+    return p, g, torch.tensor(inp["x0"]).cuda(), torch.tensor(inp["labels"]).cuda()
+
+
+def _run(slm, n, B, d, dtype, strategy, inp=None, **opt):
+    inp = inp or synth.chain_inputs(n, B, d, dtype=dtype)
+    p, g, x0, y = _dev(inp, dtype)
+    model = slm.ChainModel(p, g, dtype=dtype, batch=B, **opt)
+    plan = slm.Plan(slm.Graph.chain(n, B, d), strategy)
+    loss = model.step(plan, x0, y)
+    torch.cuda.synchronize()
+    return float(loss.item()), {k: v.float().cpu().numpy().astype(np.float64) for k, v in g.items()}, \
+        (model, plan, p, g, x0, y)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _oracle(n, B, d, dtype, inp):
+    Pm = OC.Params(inp["W"], inp["b"], inp["gamma"], inp["beta"])
+    return OC.step_plain(Pm, inp["x0"], inp["labels"], "bf16" if dtype == "bf16" else "f64")
+
+
+@pytest.mark.parametrize("strategy", ["none", "sqrt", "search", "recursive"])
+def test_c1_f32_vs_oracle(slm, strategy):
+    n, B, d = 16, 8, 64
+    inp = synth.chain_inputs(n, B, d, dtype="f32")
+    loss, grads, _ = _run(slm, n, B, d, "f32", strategy, inp)
+    ol, og, _ = _oracle(n, B, d, "f32", inp)
+    assert abs(loss - ol) / abs(ol) <= 1e-4
+    for k in og:
+        assert _rel(grads[k], og[k]) <= 1e-4, (k, _rel(grads[k], og[k]))
+
+
+@pytest.mark.parametrize("n,B,d", [(8, 64, 256), (5, 128, 384), (4, 256, 2048)])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_bf16_vs_oracle(slm, n, B, d, impl):
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=n + B + d)
+    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, gemm_impl=impl)
+    ol, og, _ = _oracle(n, B, d, "bf16", inp)
+    assert abs(loss - ol) / abs(ol) <= 2e-2
+    for k in og:
+        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
+
+
+@pytest.mark.parametrize("dtype,n,B,d", [("f32", 16, 8, 64), ("bf16", 24, 64, 256), ("bf16", 9, 256, 512)])
+def test_ckpt_equals_nockpt_bitwise(slm, dtype, n, B, d):
+    inp = synth.chain_inputs(n, B, d, dtype=dtype, seed=3)
+    ref_loss, ref, _ = _run(slm, n, B, d, dtype, "none", inp)
+    for s in ["sqrt", "search", "recursive"]:
+        loss, grads, _ = _run(slm, n, B, d, dtype, s, inp)
+        assert loss == ref_loss, s
+        for k in ref:
+            assert np.array_equal(grads[k], ref[k]), (s, k)
+
+
+def test_graph_replay_and_no_allocation(slm):
+    n, B, d = 12, 64, 256
+    loss0, g0, (model, plan, p, g, x0, y) = _run(slm, n, B, d, "bf16", "sqrt", use_graph=0)
+    model2 = slm.ChainModel(p, g, dtype="bf16", batch=B, use_graph=1)
+    bufs = model2.buffers(plan)
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):   # eager + capture, then two replays
+            loss = model2.step(plan, x0, y, stream=s, bufs=bufs)
+    torch.cuda.synchronize()
+    assert torch.cuda.max_memory_allocated() == base          # slm_step never allocates
+    assert float(loss.item()) == loss0
+    for k in g0:
+        assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), g0[k])
+
+
+def test_pool_is_plan_sized(slm):
+    n, B, d = 16, 64, 256
+    plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt")
+    u = B * d * 4
+    assert plan.exact_peak == 8 * u + 4                  # tests/golden/sqrt_peaks.txt
+    assert plan.pool_bytes == 7 * u                      # X_0 and the loss are caller buffers
+
+
+@pytest.mark.slow
+def test_c2_full_size_bitwise_and_closed_form(slm):
+    # BASELINE.json configs[1] at full size: n=1024, d=2048, B=256, bf16 — in the bench's launch
+    # configuration (tcgen05 path, CUDA graph)
+    n, B, d = 1024, 256, 2048
+    t = synth.chain_inputs_torch(n, B, d, dtype="bf16", seed=5)
+    p = {k: t[k] for k in ("W", "b", "gamma", "beta")}
+    out = {}
+    for s in ("none", "sqrt"):
+        g = dict(W=torch.empty_like(p["W"]), b=torch.empty_like(p["b"]), gamma=torch.empty_like(p["gamma"]),
+                 beta=torch.empty_like(p["beta"]))
+        model = slm.ChainModel(p, g, dtype="bf16", batch=B)
+        plan = slm.Plan(slm.Graph.chain(n, B, d), s)
+        strm = torch.cuda.Stream()
+        with torch.cuda.stream(strm):
+            loss = model.step(plan, t["x0"], t["labels"], stream=strm)
+            loss = model.step(plan, t["x0"], t["labels"], stream=strm)   # graph replay
+        torch.cuda.synchronize()
+        out[s] = (loss.item(), {k: v.clone() for k, v in g.items()})
+        del model, g
+    assert out["none"][0] == out["sqrt"][0]
+    for k in out["none"][1]:
+        assert torch.equal(out["none"][1][k], out["sqrt"][1][k]), k
+    # property that holds at any size: db_l = sum_b dx_{l+1} and BN backward conserves the
+    # per-feature sum, so db is identical for every layer up to fp32 rounding
+    db = out["sqrt"][1]["b"]
+    assert torch.allclose(db[0], db[-1], rtol=1e-3, atol=1e-6)
+    assert np.isfinite(out["sqrt"][0])
+
+
+@pytest.mark.slow
+def test_c2_width_depth4_vs_oracle(slm):
+    # full width and batch of C2 with 4 layers: the oracle finishes in seconds
+    n, B, d = 4, 256, 2048
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=11)
+    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
+    ol, og, _ = _oracle(n, B, d, "bf16", inp)
+    assert abs(loss - ol) / abs(ol) <= 2e-2
+    for k in og:
+        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
+
+
+def test_zero_weights_closed_form(slm):
+    # W == 0: x_n = x_0 + sum_l b_l and dx_l = dx_n; then dgamma = 0 and db_l is the column sum
+    n, B, d = 6, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16")
+    inp["W"][:] = 0
+    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
+    x = inp["x0"].astype(np.float64) + inp["b"].astype(np.float64).sum(0)
+    e = np.exp(x - x.max(1, keepdims=True))
+    sm = e / e.sum(1, keepdims=True)
+    ref = -np.log(sm[np.arange(B), inp["labels"]]).mean()
+    assert abs(loss - ref) < 1e-5
+    dxn = (sm - np.eye(d)[inp["labels"]]) / B
+    for l in range(n):
+        np.testing.assert_allclose(grads["b"][l], dxn.sum(0), atol=1e-6)
+    assert np.abs(grads["gamma"]).max() == 0.0
