@@ -196,6 +196,24 @@ def step_planned(plan, P: Params, x0, labels, mode="f64", batch_global=None):
     return loss, _stack(grads), dx0, dict(peak_live_bytes=peak, op_evaluations=evals)
 
 
+def relu_margin(P: Params, x0, mode="f64"):
+    """Smallest relative distance of a ReLU input from its decision point 0 over the forward
+    pass: min |u| / (|gamma xhat| + |beta|).  Reading A20: ReLU'(0) = 0 is a discrete
+    decision taken on fp32 u by the device and on fp64 u here; inputs whose margin is
+    within the rounding of the fp32 batch statistics (< 1e-5) would let the two sides take
+    different (equally valid) decisions, so parity tests draw seeds with a larger margin."""
+    x = np.asarray(x0, dtype=np.float64)
+    worst = np.inf
+    for l in range(P.n):
+        mu = x.mean(axis=0)
+        rstd = 1.0 / np.sqrt(((x - mu) ** 2).mean(axis=0) + EPS)
+        gx = P.gamma[l] * (x - mu) * rstd
+        u = gx + P.beta[l]
+        worst = min(worst, float((np.abs(u) / (np.abs(gx) + np.abs(P.beta[l]) + 1e-30)).min()))
+        x = block_forward(x, P, l, mode)
+    return worst
+
+
 def step_dp(P: Params, x0, labels, world, mode="f64"):
     """Data-parallel emulation (reading A14): rank r holds rows [r*Bl, (r+1)*Bl); BN stats
     are local; loss = mean over the global batch; grads = sum over ranks of the locally

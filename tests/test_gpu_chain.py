@@ -10,6 +10,7 @@ import pytest
 import torch
 
 import synth
+from _util import margin_inputs
 from oracle import chain as OC
 from oracle import graph as OG
 from oracle import planner as OP
@@ -55,7 +56,7 @@ def _oracle(n, B, d, dtype, inp):
 @pytest.mark.parametrize("strategy", ["none", "sqrt", "search", "recursive"])
 def test_c1_f32_vs_oracle(slm, strategy):
     n, B, d = 16, 8, 64
-    inp = synth.chain_inputs(n, B, d, dtype="f32")
+    inp = margin_inputs(n, B, d, "f32")
     loss, grads, _ = _run(slm, n, B, d, "f32", strategy, inp)
     ol, og, _ = _oracle(n, B, d, "f32", inp)
     assert abs(loss - ol) / abs(ol) <= 1e-4
@@ -66,7 +67,7 @@ def test_c1_f32_vs_oracle(slm, strategy):
 @pytest.mark.parametrize("n,B,d", [(8, 64, 256), (5, 128, 384), (4, 256, 2048)])
 @pytest.mark.parametrize("impl", [0, 1])
 def test_bf16_vs_oracle(slm, n, B, d, impl):
-    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=n + B + d)
+    inp = margin_inputs(n, B, d, "bf16", seed=n + B + d)
     loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, gemm_impl=impl)
     ol, og, _ = _oracle(n, B, d, "bf16", inp)
     assert abs(loss - ol) / abs(ol) <= 2e-2
@@ -146,7 +147,7 @@ def test_c2_full_size_bitwise_and_closed_form(slm):
 def test_c2_width_depth4_vs_oracle(slm):
     # full width and batch of C2 with 4 layers: the oracle finishes in seconds
     n, B, d = 4, 256, 2048
-    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=11)
+    inp = margin_inputs(n, B, d, "bf16", seed=11)
     loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
     ol, og, _ = _oracle(n, B, d, "bf16", inp)
     assert abs(loss - ol) / abs(ol) <= 2e-2
