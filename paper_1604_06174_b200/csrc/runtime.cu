@@ -112,30 +112,47 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 // ---------------------------------------------------------------- GEMM launchers
 enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
 
-template <int BN, bool AMN, bool BMN, class Epi>
+// Every kernel of the step is launched with programmatic stream serialization (PDL) when
+// `pdl` is set: it may start while its predecessor drains and synchronises on it with
+// griddepcontrol.wait before touching dependent data.
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                     Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+template <int BN, bool AMN, bool BMN, bool PRE, class Epi>
 slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K, int a_row0,
-                     int b_row0, Epi epi, cudaStream_t st) {
+                     int b_row0, Epi epi, cudaStream_t st, bool pdl) {
   using C = slmk::TcCfg<BN, AMN, BMN>;
-  auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, Epi>;
+  auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi>;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  dim3 grid(M / 128, N / BN);
-  kern<<<grid, 128, C::SMEM, st>>>(a, b, K, a_row0, b_row0, epi);
-  CK(cudaGetLastError());
+  CK(launch_k(kern, dim3(M / 128, N / BN), dim3(128), C::SMEM, st, pdl, a, b, K, a_row0, b_row0, epi));
   return SLM_OK;
 }
 
-template <class Epi, bool AMN, bool BMN>
+template <class Epi, bool AMN, bool BMN, bool PRE>
 slm_status launch_tc_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                        int a_row0, int b_row0, Epi epi, cudaStream_t st) {
+                        int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl) {
   switch (bn) {
-    case 32: if (!BMN) return launch_tc<32, AMN, BMN>(a, b, M, N, K, a_row0, b_row0, epi, st); break;
-    case 64: return launch_tc<64, AMN, BMN>(a, b, M, N, K, a_row0, b_row0, epi, st);
-    case 128: return launch_tc<128, AMN, BMN>(a, b, M, N, K, a_row0, b_row0, epi, st);
-    case 256: return launch_tc<256, AMN, BMN>(a, b, M, N, K, a_row0, b_row0, epi, st);
+    case 32: if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, M, N, K, a_row0, b_row0, epi, st, pdl); break;
+    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, M, N, K, a_row0, b_row0, epi, st, pdl);
+    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, M, N, K, a_row0, b_row0, epi, st, pdl);
+    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, M, N, K, a_row0, b_row0, epi, st, pdl);
   }
   set_error("unsupported GEMM N tile " + std::to_string(bn));
   return SLM_E_UNSUPPORTED;
@@ -176,6 +193,7 @@ struct slm_model {
   int kind = SLM_MODEL_CHAIN;
   int use_graph = 1;
   int gemm_impl = 0;      // 0 tcgen05 (bf16), 1 SIMT
+  int pdl = 1;            // programmatic dependent launch between the step's kernels
   int bn_fwd = 64, bn_dx = 64, bn_dw = 128;
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
@@ -344,18 +362,32 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       comm ? (int)std::max<int64_t>(1, std::min<int64_t>(n, comm->bucket_bytes / per_layer)) : 0;
   int ev_i = 0;
 
+  const bool pdl = m.pdl != 0;
   auto simt_gemm = [&](auto* A, long sAm, long sAk, auto* Bp, long sBn, long sBk, auto* out, long ldo,
-                       int M, int N, int K, const float* resid, const float* bias, bool resid_epi) {
+                       int M, int N, int K, const float* resid, const float* bias, bool resid_epi) -> cudaError_t {
     dim3 grid((N + 63) / 64, (M + 63) / 64);
     using TA = std::remove_const_t<std::remove_pointer_t<decltype(A)>>;
     using TB = std::remove_const_t<std::remove_pointer_t<decltype(Bp)>>;
     using TO = std::remove_pointer_t<decltype(out)>;
     if (resid_epi)
-      simt_gemm_kernel<TA, TB, TO, EPI_RESID><<<grid, 256, 0, st>>>(M, N, K, A, sAm, sAk, Bp, sBn, sBk, out,
-                                                                    ldo, resid, bias);
-    else
-      simt_gemm_kernel<TA, TB, TO, EPI_STORE><<<grid, 256, 0, st>>>(M, N, K, A, sAm, sAk, Bp, sBn, sBk, out,
-                                                                    ldo, resid, bias);
+      return launch_k(simt_gemm_kernel<TA, TB, TO, EPI_RESID>, grid, dim3(256), 0, st, pdl, M, N, K, A, sAm, sAk,
+                      Bp, sBn, sBk, out, ldo, resid, bias);
+    return launch_k(simt_gemm_kernel<TA, TB, TO, EPI_STORE>, grid, dim3(256), 0, st, pdl, M, N, K, A, sAm, sAk, Bp,
+                    sBn, sBk, out, ldo, resid, bias);
+  };
+  // batch-norm kernels: register-resident variant when the batch fits (B <= 256)
+  const bool rk = B <= 256;
+  const dim3 rkblk(1024);
+  auto bn_act = [&](const float* xin, int l) -> cudaError_t {
+    const float* ga = gam + (size_t)l * d;
+    const float* be = bet + (size_t)l * d;
+    if (bf16)
+      return rk ? launch_k(bn_act_rk<__nv_bfloat16, 8>, colgrid, rkblk, 0, st, pdl, xin, ga, be, B, d, stats,
+                           (__nv_bfloat16*)abuf)
+                : launch_k(bn_act_kernel<__nv_bfloat16>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats,
+                           (__nv_bfloat16*)abuf);
+    return rk ? launch_k(bn_act_rk<float, 8>, colgrid, rkblk, 0, st, pdl, xin, ga, be, B, d, stats, (float*)abuf)
+              : launch_k(bn_act_kernel<float>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (float*)abuf);
   };
 
   // optional per-kernel CUDA events (profile_events), recorded on the launching stream
@@ -378,14 +410,8 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
     const int l = o.layer;
     if (o.type == 0 || o.type == 3) {
       // K1: statistics + activation operand of x_l (forward input, or x_l in the backward)
-      const float* xin = X(o.type == 0 ? o.in_tag : o.aux_tag);
       pbeg();
-      if (bf16)
-        bn_act_kernel<__nv_bfloat16><<<colgrid, blk, 0, st>>>(xin, gam + (size_t)l * d, bet + (size_t)l * d, B,
-                                                              d, stats, (__nv_bfloat16*)abuf);
-      else
-        bn_act_kernel<float><<<colgrid, blk, 0, st>>>(xin, gam + (size_t)l * d, bet + (size_t)l * d, B, d,
-                                                      stats, (float*)abuf);
+      CK(bn_act(X(o.type == 0 ? o.in_tag : o.aux_tag), l));
       pend(SLM_K_BN_ACT);
       ++nl;
     }
@@ -395,32 +421,34 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       pbeg();
       if (tc) {
         slmk::EpiResid epi{xout, xin, bvec + (size_t)l * d, d};
-        if ((s = launch_tc_bn<slmk::EpiResid, false, false>(m.bn_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0, epi,
-                                                            st)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiResid, false, false, true>(m.bn_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0, epi,
+                                                                  st, pdl)) != SLM_OK)
           return s;
       } else if (bf16) {
-        simt_gemm((const __nv_bfloat16*)abuf, (long)d, 1L, (const __nv_bfloat16*)m.d.W + l * Wl, (long)d, 1L,
-                  xout, (long)d, B, d, d, xin, bvec + (size_t)l * d, true);
+        CK(simt_gemm((const __nv_bfloat16*)abuf, (long)d, 1L, (const __nv_bfloat16*)m.d.W + l * Wl, (long)d, 1L,
+                     xout, (long)d, B, d, d, xin, bvec + (size_t)l * d, true));
       } else {
-        simt_gemm((const float*)abuf, (long)d, 1L, (const float*)m.d.W + l * Wl, (long)d, 1L, xout, (long)d,
-                  B, d, d, xin, bvec + (size_t)l * d, true);
+        CK(simt_gemm((const float*)abuf, (long)d, 1L, (const float*)m.d.W + l * Wl, (long)d, 1L, xout, (long)d,
+                     B, d, d, xin, bvec + (size_t)l * d, true));
       }
       pend(SLM_K_GEMM_FWD);
       ++nl;
     } else if (o.type == 1) {
       pbeg();
-      ce_fwd_kernel<<<B, 256, 0, st>>>(X(o.in_tag), labels, d, rowloss);
-      ce_reduce_kernel<<<1, 256, 0, st>>>(rowloss, B, inv_bg, X(o.out_tag));
+      CK(launch_k(ce_fwd_kernel, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d, rowloss));
+      CK(launch_k(ce_reduce_kernel, dim3(1), blk, 0, st, pdl, (const float*)rowloss, B, inv_bg, X(o.out_tag)));
       pend(SLM_K_CE);
       nl += 2;
     } else if (o.type == 2) {
       float* dxn = X(o.out_tag);
       pbeg();
       if (bf16)
-        ce_bwd_kernel<__nv_bfloat16><<<B, 256, 0, st>>>(X(o.in_tag), labels, d, inv_bg, dxn, gq[0]);
+        CK(launch_k(ce_bwd_kernel<__nv_bfloat16>, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d,
+                    inv_bg, dxn, gq[0]));
       else
-        ce_bwd_kernel<float><<<B, 256, 0, st>>>(X(o.in_tag), labels, d, inv_bg, dxn, (float*)nullptr);
-      colsum_kernel<<<colgrid, blk, 0, st>>>(dxn, B, d, m.d.db + (size_t)(n - 1) * d);
+        CK(launch_k(ce_bwd_kernel<float>, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d, inv_bg,
+                    dxn, (float*)nullptr));
+      CK(launch_k(colsum_kernel, colgrid, blk, 0, st, pdl, (const float*)dxn, B, d, m.d.db + (size_t)(n - 1) * d));
       pend(SLM_K_CE);
       gpar = 0;
       nl += 2;
@@ -432,49 +460,54 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         // da[b][f_in] = sum_k g[b][k] W_l[k][f_in]
         slmk::EpiStoreF32 e1{da, d};
         pbeg();
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false>(m.bn_dx, m.mW_MN, m.mG_K[gpar], d, B, d, l * d,
-                                                              0, e1, st)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(m.bn_dx, m.mW_MN, m.mG_K[gpar], d, B, d, l * d,
+                                                                    0, e1, st, pdl)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX);
         // dW_l[f_out][f_in] = sum_b g[b][f_out] a[b][f_in]
         slmk::EpiStoreBF16 e2{(__nv_bfloat16*)m.d.dW + l * Wl, d};
         pbeg();
-        if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true>(m.bn_dw, m.mA_MN, m.mG_MN[gpar], d, d, B, 0, 0,
-                                                              e2, st)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, m.mA_MN, m.mG_MN[gpar], d, d, B, 0,
+                                                                     0, e2, st, pdl)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DW);
       } else if (bf16) {
         const __nv_bfloat16* gqp = gq[gpar];
         pbeg();
-        simt_gemm(gqp, (long)d, 1L, (const __nv_bfloat16*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
-                  (const float*)nullptr, (const float*)nullptr, false);
+        CK(simt_gemm(gqp, (long)d, 1L, (const __nv_bfloat16*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
+                     (const float*)nullptr, (const float*)nullptr, false));
         pend(SLM_K_GEMM_DX);
         pbeg();
-        simt_gemm(gqp, 1L, (long)d, (const __nv_bfloat16*)abuf, 1L, (long)d,
-                  (__nv_bfloat16*)m.d.dW + l * Wl, (long)d, d, d, B, (const float*)nullptr,
-                  (const float*)nullptr, false);
+        CK(simt_gemm(gqp, 1L, (long)d, (const __nv_bfloat16*)abuf, 1L, (long)d,
+                     (__nv_bfloat16*)m.d.dW + l * Wl, (long)d, d, d, B, (const float*)nullptr,
+                     (const float*)nullptr, false));
         pend(SLM_K_GEMM_DW);
       } else {
         pbeg();
-        simt_gemm(g, (long)d, 1L, (const float*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
-                  (const float*)nullptr, (const float*)nullptr, false);
+        CK(simt_gemm(g, (long)d, 1L, (const float*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
+                     (const float*)nullptr, (const float*)nullptr, false));
         pend(SLM_K_GEMM_DX);
         pbeg();
-        simt_gemm(g, 1L, (long)d, (const float*)abuf, 1L, (long)d, (float*)m.d.dW + l * Wl, (long)d, d, d,
-                  B, (const float*)nullptr, (const float*)nullptr, false);
+        CK(simt_gemm(g, 1L, (long)d, (const float*)abuf, 1L, (long)d, (float*)m.d.dW + l * Wl, (long)d, d, d,
+                     B, (const float*)nullptr, (const float*)nullptr, false));
         pend(SLM_K_GEMM_DW);
       }
       float* dbp = l > 0 ? m.d.db + (size_t)(l - 1) * d : nullptr;
+      const float* ga = gam + (size_t)l * d;
+      const float* be = bet + (size_t)l * d;
+      float* dga = m.d.dgamma + (size_t)l * d;
+      float* dbe = m.d.dbeta + (size_t)l * d;
       pbeg();
       if (bf16)
-        bn_bwd_kernel<__nv_bfloat16><<<colgrid, blk, 0, st>>>(da, xl, stats, gam + (size_t)l * d,
-                                                              bet + (size_t)l * d, g, dxl, B, d,
-                                                              m.d.dgamma + (size_t)l * d,
-                                                              m.d.dbeta + (size_t)l * d, dbp, gq[gpar ^ 1]);
+        CK(rk ? launch_k(bn_bwd_rk<__nv_bfloat16, 8>, colgrid, rkblk, 0, st, pdl, (const float*)da, xl,
+                         (const float*)stats, ga, be, g, dxl, B, d, dga, dbe, dbp, gq[gpar ^ 1])
+              : launch_k(bn_bwd_kernel<__nv_bfloat16>, colgrid, blk, 0, st, pdl, (const float*)da, xl,
+                         (const float*)stats, ga, be, g, dxl, B, d, dga, dbe, dbp, gq[gpar ^ 1]));
       else
-        bn_bwd_kernel<float><<<colgrid, blk, 0, st>>>(da, xl, stats, gam + (size_t)l * d, bet + (size_t)l * d,
-                                                      g, dxl, B, d, m.d.dgamma + (size_t)l * d,
-                                                      m.d.dbeta + (size_t)l * d, dbp, (float*)nullptr);
+        CK(rk ? launch_k(bn_bwd_rk<float, 8>, colgrid, rkblk, 0, st, pdl, (const float*)da, xl, (const float*)stats,
+                         ga, be, g, dxl, B, d, dga, dbe, dbp, (float*)nullptr)
+              : launch_k(bn_bwd_kernel<float>, colgrid, blk, 0, st, pdl, (const float*)da, xl, (const float*)stats,
+                         ga, be, g, dxl, B, d, dga, dbe, dbp, (float*)nullptr));
       pend(SLM_K_BN_BWD);
       gpar ^= 1;
       nl += 3;
@@ -584,6 +617,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "bn_dx") m->bn_dx = (int)value;
   else if (k == "bn_dw") m->bn_dw = (int)value;
   else if (k == "profile_events") m->profile = (int)value;
+  else if (k == "pdl") m->pdl = (int)value;
   else {
     set_error("unknown option " + k);
     return SLM_E_ARG;
@@ -794,15 +828,15 @@ slm_status slm_debug_gemm(int kind, int impl, int bn, int M, int N, int K, const
     if (kind == G_FWD) {  // A = W [M][K], B = act [N][K]; out[n][m] = resid + acc + bias[m]
       if ((s = make_map(&ma, A, K, M, 128)) || (s = make_map(&mb, Bm, K, N, bn))) return s;
       slmk::EpiResid e{(float*)out, resid, bias, M};
-      return launch_tc_bn<slmk::EpiResid, false, false>(bn, ma, mb, M, N, K, 0, 0, e, st);
+      return launch_tc_bn<slmk::EpiResid, false, false, true>(bn, ma, mb, M, N, K, 0, 0, e, st, false);
     } else if (kind == G_DX) {  // A = W [K][M] (MN), B = g [N][K]; out[n][m] fp32
       if ((s = make_map(&ma, A, M, K, 64)) || (s = make_map(&mb, Bm, K, N, bn))) return s;
       slmk::EpiStoreF32 e{(float*)out, M};
-      return launch_tc_bn<slmk::EpiStoreF32, true, false>(bn, ma, mb, M, N, K, 0, 0, e, st);
+      return launch_tc_bn<slmk::EpiStoreF32, true, false, true>(bn, ma, mb, M, N, K, 0, 0, e, st, false);
     } else {  // DW: A = act [K][M] (MN), B = g [K][N] (MN); out[n][m] bf16
       if ((s = make_map(&ma, A, M, K, 64)) || (s = make_map(&mb, Bm, N, K, 64))) return s;
       slmk::EpiStoreBF16 e{(bf*)out, M};
-      return launch_tc_bn<slmk::EpiStoreBF16, true, true>(bn, ma, mb, M, N, K, 0, 0, e, st);
+      return launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(bn, ma, mb, M, N, K, 0, 0, e, st, false);
     }
   }
   dim3 grid((M + 63) / 64, (N + 63) / 64);  // SIMT computes C(n, m) with n as the row

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "kernels_simt.cuh"  // pdl_wait / pdl_launch
+
 namespace slmk {
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -123,11 +125,13 @@ struct EpiResid {  // forward: out[n*ld+m] = resid[n*ld+m] + acc + bias[m]  (out
   long ld;
   __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
     const float bm = bias[m];
+    // all 32 loads first: `out` may alias `resid` (in-place Block), so loads interleaved with
+    // stores would be serialised by the compiler (one memory latency per element)
+    float r[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      long o = (long)(n0 + j) * ld + m;
-      out[o] = __fadd_rn(resid[o], __fadd_rn(acc[j], bm));
-    }
+    for (int j = 0; j < 32; ++j) r[j] = resid[(long)(n0 + j) * ld + m];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[(long)(n0 + j) * ld + m] = __fadd_rn(r[j], __fadd_rn(acc[j], bm));
   }
 };
 struct EpiStoreF32 {  // out[n*ld+m] = acc
@@ -154,14 +158,19 @@ struct TcCfg {
   static constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (STAGE * 4 <= 200 * 1024) ? 4 : 3;
+  // as many stages as fit in ~200 KiB (up to 8): the K loop is latency bound, bytes in
+  // flight per SM set its bandwidth
+  static constexpr int STAGES = (200 * 1024 / STAGE) > 8 ? 8 : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // a_row0/b_row0: row offsets added to the tensor-map coordinates of A / B (e.g. layer l's
 // weight block inside the [n*d, d] weight tensor).
-template <int BN, bool A_MN, bool B_MN, class Epi>
+// PREFETCH_A: A is read-only for the whole step (the weights), so its first pipeline stages are
+// requested before griddepcontrol.wait, i.e. while the previous kernel is still finishing
+// (programmatic dependent launch); B and the epilogue inputs are read only after the wait.
+template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int K, int a_row0, int b_row0, Epi epi) {
@@ -198,28 +207,49 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch();
+
+  auto load_a = [&](int kb, int s) {
+    uint8_t* sa = smem + s * C::STAGE;
+    const int k0 = kb * C::BK;
+    if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
+      tma_load_2d(sa, &tmA, &full[s], m0, a_row0 + k0);
+      tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, a_row0 + k0);
+    } else {     // A stored [M][K]: one box of 64(K) x 128(M)
+      tma_load_2d(sa, &tmA, &full[s], k0, a_row0 + m0);
+    }
+  };
+  auto load_b = [&](int kb, int s) {
+    uint8_t* sb = smem + s * C::STAGE + C::A_BYTES;
+    const int k0 = kb * C::BK;
+    if (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, b_row0 + k0);
+    } else {
+      tma_load_2d(sb, &tmB, &full[s], k0, b_row0 + n0);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     // ===== TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
+    int kb0 = 0;
+    if (PREFETCH_A) {
+      kb0 = nk < C::STAGES ? nk : C::STAGES;
+      for (int kb = 0; kb < kb0; ++kb) {
+        mbar_expect_tx(&full[kb], C::STAGE);
+        load_a(kb, kb);
+      }
+      pdl_wait();
+      for (int kb = 0; kb < kb0; ++kb) load_b(kb, kb);
+    } else {
+      pdl_wait();
+    }
+    for (int kb = kb0; kb < nk; ++kb) {
       const int s = kb % C::STAGES;
       if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-      uint8_t* sa = smem + s * C::STAGE;
-      uint8_t* sb = sa + C::A_BYTES;
       mbar_expect_tx(&full[s], C::STAGE);
-      const int k0 = kb * C::BK;
-      if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
-        tma_load_2d(sa, &tmA, &full[s], m0, a_row0 + k0);
-        tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, a_row0 + k0);
-      } else {     // A stored [M][K]: one box of 64(K) x 128(M)
-        tma_load_2d(sa, &tmA, &full[s], k0, a_row0 + m0);
-      }
-      if (B_MN) {
-#pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, b_row0 + k0);
-      } else {
-        tma_load_2d(sb, &tmB, &full[s], k0, b_row0 + n0);
-      }
+      load_a(kb, s);
+      load_b(kb, s);
     }
   } else if (warp == 1 && lane == 0) {
     // ===== MMA issuer
@@ -244,6 +274,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   __syncwarp();
   // ===== epilogue: TMEM -> registers -> global
+  pdl_wait();
   mbar_wait(accum, 0);
   tc_fence_after();
   const int m = m0 + warp * 32 + lane;
