@@ -149,6 +149,7 @@ def main():
     ap.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-nockpt", action="store_true", help="skip the non-checkpointed comparison")
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
+    ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -195,6 +196,9 @@ def main():
     if args.bn:
         f, x, w = (int(v) for v in args.bn.split(","))
         opts = dict(bn_fwd=f, bn_dx=x, bn_dw=w)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        opts[k] = int(v)
     model = slm.ChainModel(params, grads, dtype="bf16", batch=B, batch_global=Bg, **opts)
     comm = slm.Comm(rank, world) if world > 1 else None
     graph = slm.Graph.chain(n, B, d)

@@ -9,7 +9,11 @@
  *   kind 2 (dW)        out[n][m] = bf16(sum_k A[k][m] B[k][n])
  *                       A bf16 [K][M], B bf16 [K][N], out bf16 [N][M]
  * impl 0 = tcgen05/TMA (bn = N tile: 32|64|128|256; M % 128 == 0, N % bn == 0, K % 64 == 0),
- * impl 1 = SIMT.  All pointers are device pointers; asynchronous on `stream`.
+ * impl 1 = SIMT, impl 2 = tcgen05 data movement only (no MMA), impl 3 = tcgen05 MMA only (no
+ * TMA) — the last two are bandwidth / issue-rate probes with meaningless results.
+ * split = split-K factor of the tcgen05 kernel (K % (64 split) == 0); with split > 1, kinds 0
+ * and 1 write the fp32 partial tiles out[s][n][m] (split x N x M; the caller sums over s, kind 0
+ * then ignores resid/bias).  All pointers are device pointers; asynchronous on `stream`.
  */
 #ifndef SLM_DEBUG_H_
 #define SLM_DEBUG_H_
@@ -17,9 +21,12 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
-slm_status slm_debug_gemm(int kind, int impl, int bn, int M, int N, int K, const void* A,
+slm_status slm_debug_gemm(int kind, int impl, int bn, int split, int M, int N, int K, const void* A,
                           const void* B, void* out, const float* resid, const float* bias,
                           void* stream);
+/* Per-CTA %globaltimer stamps (8 per CTA, phases of tc_gemm_kernel) written to dev_buf
+ * (uint64, >= 8 * CTAs of the next launches); NULL switches the instrumentation off. */
+slm_status slm_debug_timestamps(void* dev_buf);
 #ifdef __cplusplus
 }
 #endif

@@ -292,9 +292,9 @@ class ChainModel:
             self._h = None
 
 
-def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None):
+def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None, split=1):
     """Test hook (include/slm_debug.h)."""
     import torch
     st = stream if stream is not None else torch.cuda.current_stream(A.device)
-    check(lib.slm_debug_gemm(kind, impl, bn, M, N, K, _ptr(A), _ptr(B), _ptr(out), _ptr(resid),
+    check(lib.slm_debug_gemm(kind, impl, bn, split, M, N, K, _ptr(A), _ptr(B), _ptr(out), _ptr(resid),
                              _ptr(bias), C.c_void_p(st.cuda_stream)), "slm_debug_gemm")

@@ -79,7 +79,7 @@ _sig("slm_step_host", i32, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, C.c_size_
 _sig("slm_comm_unique_id", i32, vp)
 _sig("slm_comm_init", i32, i32, i32, vp, i64, C.POINTER(vp))
 _sig("slm_comm_destroy", None, vp)
-_sig("slm_debug_gemm", i32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp)
+_sig("slm_debug_gemm", i32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp)
 
 # names declared in include/slm.h + include/slm_debug.h (checked by tests/test_abi.py)
 EXPORTS = [n for n in dir(lib) if n.startswith("slm_")]
@@ -103,3 +103,4 @@ def check(code, where=""):
 
 _sig("slm_model_kernel_times", i32, vp, f32p, i64p, i32, i32)
 K_KINDS = ["bn_act", "gemm_fwd", "gemm_dx", "gemm_dw", "bn_bwd", "ce"]
+_sig("slm_debug_timestamps", i32, vp)

@@ -1,0 +1,671 @@
+// Executor of V' for the residual chain (included by runtime.cu; not a standalone TU).
+//
+// Every node of V' (Alg. 2's order) writes its value into the pool slot of
+// its temporal tag (Fig. 2).  Two lowerings:
+//
+// * fused (bf16, tcgen05; the product path at B <= 256):
+//     forward/mirror Block_l   [K1 bn_act(x_l) only if a_l is not already resident]
+//                              GEMM  P[s] = W_l a_l^T over K slice s   (split-K, 128 CTAs)
+//                              finalize+K1  x_{l+1} = x_l + (sum_s P[s] + b_l) -> slot,
+//                                           stats/a_{l+1} for the next Block (same kernel code as K1)
+//     grad Block_l             GEMM  P[s] = g_{l+1} W_l over K slice s (dX, split-K)
+//                              bn_bwd  da = sum_s P[s], stats of x_l, a_l, dx_l, dgamma, dbeta,
+//                                      db_{l-1}, bf16 copy of dx_l
+//                              GEMM  dW_l = g_{l+1}^T a_l   on a second stream (off the critical
+//                                      path; joined by events two layers later)
+// * basic (f32 FFMA path, SIMT GEMMs, or B > 256): K1 + GEMM with residual epilogue; K1 + dX +
+//   dW + bn_bwd in the backward.
+//
+// Mirrors re-run exactly the forward kernels with the same launch configuration, and every
+// reduction has a fixed order, so re-computed values are bit-identical.
+
+namespace {
+
+// ---------------------------------------------------------------- launchers
+// Every kernel of the step is launched with programmatic stream serialization (PDL) when
+// `pdl` is set: it may start while its predecessor drains and synchronises on it with
+// griddepcontrol.wait before touching dependent data.
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                     Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
+enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
+
+template <int BN, bool AMN, bool BMN, bool PRE, class Epi>
+slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int M, int N, int K, int split,
+                     int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg) {
+  using C = slmk::TcCfg<BN, AMN, BMN>;
+  auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  if (split < 1 || K % (64 * split) || M % 128 || N % BN) {
+    set_error("GEMM shape not tileable: M % 128, N % BN, K % (64 * split)");
+    return SLM_E_UNSUPPORTED;
+  }
+  CK(launch_k(kern, dim3(M / 128, N / BN, split), dim3(128), C::SMEM, st, pdl, a, b, c, K, a_row0, b_row0, epi, dbg));
+  return SLM_OK;
+}
+
+// c: tensor map of the output for TMA-store epilogues (Epi::kTma), else ignored
+template <class Epi, bool AMN, bool BMN, bool PRE>
+slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                        int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg = 0,
+                        const CUtensorMap* c = nullptr) {
+  const CUtensorMap& cm = c ? *c : a;
+  switch (bn) {
+    case 32:
+      if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+      break;
+    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+  }
+  set_error("unsupported GEMM N tile " + std::to_string(bn));
+  return SLM_E_UNSUPPORTED;
+}
+
+// fp32 2-D tensor [rows][inner], box {128, 32}, no swizzle (epilogue bulk stores)
+slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SLM_E_CUDA;
+  }
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {128, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
+    return SLM_E_CUDA;
+  }
+  return SLM_OK;
+}
+
+// register-resident BN kernels: compile-time rows per warp R = B/32 and split count NS
+template <int R, int NS>
+cudaError_t launch_act_rk(cudaStream_t st, bool pdl, int d, const float* xin, const float* P, unsigned pslice,
+                          const float* bias, float* xout, const float* ga, const float* be, float* stats,
+                          __nv_bfloat16* a) {
+  return launch_k(slmk::bn_act_rk<__nv_bfloat16, R, NS>, dim3(d / slmk::kFeat), dim3(slmk::kThreads), 0, st, pdl, xin,
+                  P, pslice, bias,
+                  xout, ga, be, d, stats, a);
+}
+cudaError_t act_rk(int R, int ns, cudaStream_t st, bool pdl, int d, const float* xin, const float* P,
+                   unsigned pslice, const float* bias, float* xout, const float* ga, const float* be, float* stats,
+                   __nv_bfloat16* a) {
+#define SLM_ACT(R_, NS_) \
+  if (R == R_ && ns == NS_) return launch_act_rk<R_, NS_>(st, pdl, d, xin, P, pslice, bias, xout, ga, be, stats, a);
+#define SLM_ACT_R(R_) SLM_ACT(R_, 0) SLM_ACT(R_, 1) SLM_ACT(R_, 2) SLM_ACT(R_, 4) SLM_ACT(R_, 8)
+  SLM_ACT_R(2) SLM_ACT_R(4) SLM_ACT_R(8)
+#undef SLM_ACT_R
+#undef SLM_ACT
+  return cudaErrorInvalidValue;
+}
+template <int R, int NS>
+cudaError_t launch_bwd_rk(cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice, const float* x,
+                          const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe,
+                          float* dbp, __nv_bfloat16* gq, __nv_bfloat16* a) {
+  return launch_k(slmk::bn_bwd_rk<__nv_bfloat16, __nv_bfloat16, R, NS>, dim3(d / slmk::kFeat), dim3(slmk::kThreads), 0,
+                  st, pdl, P,
+                  pslice, x, ga, be, g, dx, d, dga, dbe, dbp, gq, a);
+}
+cudaError_t bwd_rk(int R, int ns, cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice, const float* x,
+                   const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe, float* dbp,
+                   __nv_bfloat16* gq, __nv_bfloat16* a) {
+#define SLM_BWD(R_, NS_)                                                                                    \
+  if (R == R_ && ns == NS_)                                                                                  \
+    return launch_bwd_rk<R_, NS_>(st, pdl, d, P, pslice, x, ga, be, g, dx, dga, dbe, dbp, gq, a);
+#define SLM_BWD_R(R_) SLM_BWD(R_, 1) SLM_BWD(R_, 2) SLM_BWD(R_, 4) SLM_BWD(R_, 8)
+  SLM_BWD_R(2) SLM_BWD_R(4) SLM_BWD_R(8)
+#undef SLM_BWD_R
+#undef SLM_BWD
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+// ====================================================================== model
+struct slm_comm {
+  nccl_comm_t comm = nullptr;
+  int rank = 0, world = 1;
+  int64_t bucket_bytes = 256ll << 20;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+};
+
+struct Op {
+  int type;      // 0 fwd block, 1 ce fwd, 2 ce bwd, 3 bwd block
+  int layer;
+  int in_tag;    // fwd: x_l ; ce: x_n ; bwd block: g = dx_{l+1}
+  int aux_tag;   // bwd block: x_l
+  int out_tag;
+  int in_node;   // fwd block: the node whose value is x_l
+  int node;      // this node of G'
+};
+
+struct GraphKey {
+  const void* plan;
+  const void *x0, *labels, *pool, *ws, *loss;
+  cudaStream_t stream;
+  const void* comm;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(plan, x0, labels, pool, ws, loss, stream, comm) <
+           std::tie(o.plan, o.x0, o.labels, o.pool, o.ws, o.loss, o.stream, o.comm);
+  }
+};
+
+struct slm_model {
+  slm_chain_desc d{};
+  int kind = SLM_MODEL_CHAIN;
+  int use_graph = 1;
+  int gemm_impl = 0;      // 0 tcgen05 (bf16), 1 SIMT
+  int pdl = 1;            // programmatic dependent launch between the step's kernels
+  int fused = 1;          // fused lowering (split-K partials reduced in the BN kernels)
+  int dw_stream = 1;      // dW GEMMs on a second stream
+  int bn_fwd = 64, bn_dx = 64, bn_dw = 256;  // N tiles (basic lowering; the fused one uses bn = B)
+  int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
+  // tensor maps bound to the current workspace / weights
+  const void* maps_ws = nullptr;
+  int maps_key = -1;
+  CUtensorMap mW_K, mW_MN, mA_K, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int64_t last_launches = 0;
+  cudaStream_t s2 = nullptr;           // second stream (dW)
+  std::vector<cudaEvent_t> sync_ev;    // fork/join events (reused every step)
+  // profile_events: (start, end, kind) per kernel, read by slm_model_kernel_times
+  int profile = 0;
+  struct EvPair {
+    cudaEvent_t a, b;
+    int kind;
+  };
+  std::vector<EvPair> ev_live;
+  std::vector<cudaEvent_t> ev_free;
+  double acc_ms[SLM_K_COUNT] = {};
+  int64_t acc_cnt[SLM_K_COUNT] = {};
+  cudaEvent_t get_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~slm_model() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& p : ev_live) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
+    for (auto e : sync_ev) cudaEventDestroy(e);
+    if (s2) cudaStreamDestroy(s2);
+  }
+};
+
+namespace {
+
+bool tc_ok(const slm_model& m) {
+  const int B = m.d.batch, d = m.d.width;
+  return m.d.dtype == SLM_BF16 && m.gemm_impl == 0 && d % 128 == 0 && B % 64 == 0 && B <= 4096 &&
+         B % m.bn_fwd == 0 && B % m.bn_dx == 0 && d % m.bn_dw == 0;
+}
+// the fused lowering: full batch per GEMM tile (N = B <= 256), split-K partials
+bool fused_ok(const slm_model& m) {
+  const int B = m.d.batch;
+  return tc_ok(m) && m.fused && (B == 64 || B == 128 || B == 256) && m.d.width % 256 == 0;
+}
+// split-K factor: as many K slices as keep <= ~148 CTAs and >= 64 of K per slice
+int auto_split(int M, int K, int req) {
+  if (req > 0) return req;
+  const int tiles = M / 128;
+  int s = 1;
+  // ~64 CTAs: measured best at C2 (split 4: 44.7 ms/step vs 56.1 with split 8 under PDL — the
+  // remaining SMs run the dependent BN kernel's early CTAs and the off-path dW GEMM)
+  while (s < 8 && tiles * s * 2 <= 80 && K % (64 * s * 2) == 0) s *= 2;
+  return s;
+}
+
+struct WsLayout {
+  size_t a, stats, gq[3], ab[2], P, da, rowloss, total;
+  int sk_fwd, sk_dx;
+};
+WsLayout ws_layout(const slm_model& m) {
+  const size_t B = m.d.batch, d = m.d.width;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  WsLayout L{};
+  L.sk_fwd = auto_split((int)d, (int)d, m.sk_fwd);
+  L.sk_dx = auto_split((int)d, (int)d, m.sk_dx);
+  size_t off = 0;
+  L.a = off;
+  off += al(B * d * 4);
+  L.stats = off;
+  off += al(2 * d * 4);
+  for (int i = 0; i < 3; ++i) {
+    L.gq[i] = off;
+    off += al(B * d * 2);
+  }
+  for (int i = 0; i < 2; ++i) {
+    L.ab[i] = off;
+    off += al(B * d * 2);
+  }
+  L.P = off;
+  off += al((size_t)std::max(L.sk_fwd, L.sk_dx) * B * d * 4);
+  L.da = off;
+  off += al(B * d * 4);
+  L.rowloss = off;
+  off += al(B * 4);
+  L.total = off;
+  return L;
+}
+
+slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
+  ops->clear();
+  const int n = p->dims[0];
+  for (int v : p->order) {
+    const int kind = p->kind[v], op = p->op[v], orig = p->orig[v];
+    const int* pr = &p->preds[p->pred_ptr[v]];
+    const int npr = p->pred_ptr[v + 1] - p->pred_ptr[v];
+    if (op == SLM_OP_INPUT) continue;
+    if (kind != SLM_KIND_GRAD) {
+      if (op == SLM_OP_BLOCK)
+        ops->push_back({0, orig - 1, p->node_tag[pr[0]], -1, p->node_tag[v], pr[0], v});
+      else if (op == SLM_OP_SOFTMAX_CE)
+        ops->push_back({1, n, p->node_tag[pr[0]], -1, p->node_tag[v], pr[0], v});
+      else {
+        set_error("unsupported op in chain plan");
+        return SLM_E_UNSUPPORTED;
+      }
+    } else {
+      if (op == SLM_OP_SOFTMAX_CE) {
+        if (npr != 1) return SLM_E_UNSUPPORTED;
+        ops->push_back({2, n, p->node_tag[pr[0]], -1, p->node_tag[v], pr[0], v});
+      } else if (op == SLM_OP_BLOCK) {
+        if (npr != 2) return SLM_E_UNSUPPORTED;
+        ops->push_back({3, orig - 1, p->node_tag[pr[0]], p->node_tag[pr[1]], p->node_tag[v], pr[1], v});
+      } else {
+        set_error("unsupported gradient op in chain plan");
+        return SLM_E_UNSUPPORTED;
+      }
+    }
+  }
+  return SLM_OK;
+}
+
+slm_status bind_maps(slm_model& m, void* ws) {
+  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused;
+  if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
+  const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
+  WsLayout L = ws_layout(m);
+  uint8_t* w = (uint8_t*)ws;
+  const bool fz = fused_ok(m);
+  const uint32_t bnf = fz ? (uint32_t)B : (uint32_t)m.bn_fwd, bnx = fz ? (uint32_t)B : (uint32_t)m.bn_dx;
+  slm_status st;
+  if ((st = make_map(&m.mW_K, m.d.W, d, n * d, 128)) != SLM_OK) return st;
+  if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
+  if ((st = make_map(&m.mA_K, w + L.a, d, B, bnf)) != SLM_OK) return st;
+  if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
+  for (int i = 0; i < 3; ++i) {
+    if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, bnx)) != SLM_OK) return st;
+    if ((st = make_map(&m.mG_MN[i], w + L.gq[i], d, B, 64)) != SLM_OK) return st;
+  }
+  for (int i = 0; i < 2; ++i)
+    if ((st = make_map(&m.mAb_MN[i], w + L.ab[i], d, B, 64)) != SLM_OK) return st;
+  if ((st = make_map_f32(&m.mP, w + L.P, d, (uint64_t)std::max(L.sk_fwd, L.sk_dx) * B)) != SLM_OK) return st;
+  m.maps_ws = ws;
+  m.maps_key = key;
+  return SLM_OK;
+}
+
+slm_status ensure_streams(slm_model& m, int n_layers) {
+  if (!m.s2) CK(cudaStreamCreateWithFlags(&m.s2, cudaStreamNonBlocking));
+  const size_t need = 2 * (size_t)n_layers + 8;
+  while (m.sync_ev.size() < need) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m.sync_ev.push_back(e);
+  }
+  return SLM_OK;
+}
+
+// Enqueue the whole step on `st`; counts kernel launches into *launches.
+slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_t* labels, void* pool, void* ws,
+                   float* loss, cudaStream_t st, slm_comm* comm, int64_t* launches) {
+  using namespace slmk;
+  using bf = __nv_bfloat16;
+  const int B = m.d.batch, d = m.d.width, n = m.d.n_layers;
+  const bool bf16 = m.d.dtype == SLM_BF16;
+  const bool tc = tc_ok(m);
+  const bool fz = fused_ok(m);
+  const int Bg = m.d.batch_global > 0 ? m.d.batch_global : B;
+  const float inv_bg = 1.0f / (float)Bg;
+  const WsLayout L = ws_layout(m);
+  uint8_t* w = (uint8_t*)ws;
+  float* stats = (float*)(w + L.stats);
+  void* abuf = w + L.a;
+  bf* gq[3] = {(bf*)(w + L.gq[0]), (bf*)(w + L.gq[1]), (bf*)(w + L.gq[2])};
+  bf* ab[2] = {(bf*)(w + L.ab[0]), (bf*)(w + L.ab[1])};
+  float* P = (float*)(w + L.P);
+  const long pslice = (long)B * d;
+  float* da = (float*)(w + L.da);
+  float* rowloss = (float*)(w + L.rowloss);
+  const bool pdl = m.pdl != 0;
+  const bool side = fz && m.dw_stream;
+
+  std::vector<Op> ops;
+  slm_status s = lower(p, &ops);
+  if (s != SLM_OK) return s;
+  if (tc && (s = bind_maps(m, ws)) != SLM_OK) return s;
+  if (side && (s = ensure_streams(m, n)) != SLM_OK) return s;
+
+  // tag -> pointer: pool offset, or the caller buffer bound to an external tag
+  std::vector<void*> tp(p->tag_size.size(), nullptr);
+  for (size_t t = 0; t < tp.size(); ++t)
+    if (p->tag_offset[t] >= 0) tp[t] = (uint8_t*)pool + p->tag_offset[t];
+  for (int v = 0; v < p->n_fwd; ++v) {
+    int t = p->node_tag[v];
+    if (t < 0 || p->tag_offset[t] >= 0) continue;
+    if (p->op[v] == SLM_OP_INPUT) tp[t] = const_cast<void*>(x0);
+    else if (p->op[v] == SLM_OP_SOFTMAX_CE) tp[t] = loss;
+  }
+  auto X = [&](int tag) { return (float*)tp[tag]; };
+
+  const size_t Wl = (size_t)d * d;
+  const float* bvec = m.d.b;
+  const float* gam = m.d.gamma;
+  const float* bet = m.d.beta;
+  const dim3 colgrid((d + 31) / 32), blk(256);
+  int64_t nl = 0;
+
+  // optional per-kernel CUDA events (profile_events), recorded on the launching stream
+  cudaEvent_t ev0 = nullptr;
+  auto pbeg = [&](cudaStream_t ss) {
+    if (m.profile) {
+      ev0 = m.get_event();
+      cudaEventRecord(ev0, ss);
+    }
+  };
+  auto pend = [&](int kind, cudaStream_t ss) {
+    if (m.profile) {
+      cudaEvent_t e1 = m.get_event();
+      cudaEventRecord(e1, ss);
+      m.ev_live.push_back({ev0, e1, kind});
+    }
+  };
+
+  auto simt_gemm = [&](auto* A, long sAm, long sAk, auto* Bp, long sBn, long sBk, auto* out, long ldo, int M, int N,
+                       int K, const float* resid, const float* bias, bool resid_epi) -> cudaError_t {
+    dim3 grid((N + 63) / 64, (M + 63) / 64);
+    using TA = std::remove_const_t<std::remove_pointer_t<decltype(A)>>;
+    using TB = std::remove_const_t<std::remove_pointer_t<decltype(Bp)>>;
+    using TO = std::remove_pointer_t<decltype(out)>;
+    if (resid_epi)
+      return launch_k(simt_gemm_kernel<TA, TB, TO, EPI_RESID>, grid, dim3(256), 0, st, pdl, M, N, K, A, sAm, sAk,
+                      Bp, sBn, sBk, out, ldo, resid, bias);
+    return launch_k(simt_gemm_kernel<TA, TB, TO, EPI_STORE>, grid, dim3(256), 0, st, pdl, M, N, K, A, sAm, sAk, Bp,
+                    sBn, sBk, out, ldo, resid, bias);
+  };
+  // K1 (optionally fused with the forward finalize from split-K partials)
+  auto bn_act = [&](const float* xin, const float* Pp, int nsplit, const float* bias, float* xout, int l) -> cudaError_t {
+    const float* ga = l < n ? gam + (size_t)l * d : nullptr;
+    const float* be = l < n ? bet + (size_t)l * d : nullptr;
+    if (fz)
+      return act_rk(B / 32, Pp ? nsplit : 0, st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be, stats,
+                    (bf*)abuf);
+    if (bf16)
+      return launch_k(bn_act_kernel<bf>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (bf*)abuf);
+    return launch_k(bn_act_kernel<float>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (float*)abuf);
+  };
+
+  int abuf_node = -1;     // node whose activation operand a = ReLU(BN(x)) is resident in abuf
+  int kb = 0;             // backward index: the k-th gradient Block node
+  int gcur = 0;           // gq buffer holding the bf16 copy of the current upstream gradient
+  int ev_i = 0;
+  std::vector<int> dw_event(n + 2, -1);   // sync_ev index recorded after dW of backward k
+  // data-parallel buckets: layers [lo, hi] are reduced after layer lo's backward
+  int bucket_hi = n - 1;
+  const int64_t per_layer = (int64_t)Wl * (bf16 ? 2 : 4);
+  const int bucket_layers =
+      comm ? (int)std::max<int64_t>(1, std::min<int64_t>(n, comm->bucket_bytes / per_layer)) : 0;
+  int cev_i = 0;
+
+  for (const Op& o : ops) {
+    const int l = o.layer;
+    if (o.type == 0) {  // ---------------- forward / mirror Block_l
+      const float* xin = X(o.in_tag);
+      float* xout = X(o.out_tag);
+      if (!fz || abuf_node != o.in_node) {
+        pbeg(st);
+        CK(bn_act(xin, nullptr, 0, nullptr, nullptr, l));
+        pend(SLM_K_BN_ACT, st);
+        ++nl;
+      }
+      if (fz) {
+        slmk::EpiPartialTma epi{B};
+        pbeg(st);
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, L.sk_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0,
+                                                                       epi, st, pdl, 0, &m.mP)) != SLM_OK)
+          return s;
+        pend(SLM_K_GEMM_FWD, st);
+        // finalize x_{l+1} and produce a_{l+1} for the next Block (BN of layer l+1)
+        pbeg(st);
+        CK(bn_act(xin, P, L.sk_fwd, bvec + (size_t)l * d, xout, l + 1));
+        pend(SLM_K_BN_ACT, st);
+        abuf_node = o.node;
+        nl += 2;
+      } else {
+        pbeg(st);
+        if (tc) {
+          slmk::EpiResid epi{xout, xin, bvec + (size_t)l * d, d};
+          if ((s = launch_tc_bn<slmk::EpiResid, false, false, true>(m.bn_fwd, 1, m.mW_K, m.mA_K, d, B, d, l * d, 0,
+                                                                    epi, st, pdl)) != SLM_OK)
+            return s;
+        } else if (bf16) {
+          CK(simt_gemm((const bf*)abuf, (long)d, 1L, (const bf*)m.d.W + l * Wl, (long)d, 1L, xout, (long)d, B, d, d,
+                       xin, bvec + (size_t)l * d, true));
+        } else {
+          CK(simt_gemm((const float*)abuf, (long)d, 1L, (const float*)m.d.W + l * Wl, (long)d, 1L, xout, (long)d, B,
+                       d, d, xin, bvec + (size_t)l * d, true));
+        }
+        pend(SLM_K_GEMM_FWD, st);
+        abuf_node = -1;
+        ++nl;
+      }
+    } else if (o.type == 1) {  // ---------------- loss
+      pbeg(st);
+      CK(launch_k(ce_fwd_kernel, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d, rowloss));
+      CK(launch_k(ce_reduce_kernel, dim3(1), blk, 0, st, pdl, (const float*)rowloss, B, inv_bg, X(o.out_tag)));
+      pend(SLM_K_CE, st);
+      nl += 2;
+    } else if (o.type == 2) {  // ---------------- gradient of the loss
+      float* dxn = X(o.out_tag);
+      pbeg(st);
+      if (bf16)
+        CK(launch_k(ce_bwd_kernel<bf>, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d, inv_bg, dxn,
+                    gq[0]));
+      else
+        CK(launch_k(ce_bwd_kernel<float>, dim3(B), blk, 0, st, pdl, (const float*)X(o.in_tag), labels, d, inv_bg,
+                    dxn, (float*)nullptr));
+      CK(launch_k(colsum_kernel, colgrid, blk, 0, st, pdl, (const float*)dxn, B, d, m.d.db + (size_t)(n - 1) * d));
+      pend(SLM_K_CE, st);
+      gcur = 0;
+      nl += 2;
+    } else {  // ---------------- backward of Block_l
+      const float* g = X(o.in_tag);
+      const float* xl = X(o.aux_tag);
+      float* dxl = X(o.out_tag);
+      float* dbp = l > 0 ? m.d.db + (size_t)(l - 1) * d : nullptr;
+      const float* ga = gam + (size_t)l * d;
+      const float* be = bet + (size_t)l * d;
+      float* dga = m.d.dgamma + (size_t)l * d;
+      float* dbe = m.d.dbeta + (size_t)l * d;
+      if (fz) {
+        const int gnext = (gcur + 1) % 3, abi = kb & 1;
+        // dX: P[s] = g_{l+1} W_l over K slice s
+        slmk::EpiPartialTma e1{B};
+        pbeg(st);
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d,
+                                                                      l * d, 0, e1, st, pdl, 0, &m.mP)) != SLM_OK)
+          return s;
+        pend(SLM_K_GEMM_DX, st);
+        // bn_bwd(k) overwrites gq[(k+1)%3] and ab[k%2], last read by dW of backward k-2
+        if (side && kb >= 2 && dw_event[kb - 2] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - 2]], 0));
+        pbeg(st);
+        CK(bwd_rk(B / 32, L.sk_dx, st, pdl, d, (const float*)P, (unsigned)pslice, xl, ga, be, g, dxl, dga, dbe, dbp,
+                  gq[gnext], ab[abi]));
+        pend(SLM_K_BN_BWD, st);
+        // dW_l[f_out][f_in] = sum_b g[b][f_out] a[b][f_in]  (second stream)
+        cudaStream_t sw = st;
+        if (side) {
+          cudaEvent_t ef = m.sync_ev[ev_i++];
+          CK(cudaEventRecord(ef, st));
+          CK(cudaStreamWaitEvent(m.s2, ef, 0));
+          sw = m.s2;
+        }
+        slmk::EpiStoreBF16 e2{(bf*)m.d.dW + l * Wl, d};
+        pbeg(sw);
+        if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, 1, m.mAb_MN[abi], m.mG_MN[gcur], d, d,
+                                                                     B, 0, 0, e2, sw, pdl && !side)) != SLM_OK)
+          return s;
+        pend(SLM_K_GEMM_DW, sw);
+        if (side) {
+          dw_event[kb] = ev_i;
+          CK(cudaEventRecord(m.sync_ev[ev_i++], m.s2));
+        }
+        gcur = gnext;
+        nl += 3;
+      } else {
+        pbeg(st);
+        CK(bn_act(xl, nullptr, 0, nullptr, nullptr, l));
+        pend(SLM_K_BN_ACT, st);
+        if (tc) {
+          slmk::EpiStoreF32 e1{da, d};
+          pbeg(st);
+          if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(m.bn_dx, 1, m.mW_MN, m.mG_K[gcur], d, B, d,
+                                                                      l * d, 0, e1, st, pdl)) != SLM_OK)
+            return s;
+          pend(SLM_K_GEMM_DX, st);
+          slmk::EpiStoreBF16 e2{(bf*)m.d.dW + l * Wl, d};
+          pbeg(st);
+          if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, 1, m.mA_MN, m.mG_MN[gcur], d, d, B,
+                                                                       0, 0, e2, st, pdl)) != SLM_OK)
+            return s;
+          pend(SLM_K_GEMM_DW, st);
+        } else if (bf16) {
+          const bf* gqp = gq[gcur];
+          pbeg(st);
+          CK(simt_gemm(gqp, (long)d, 1L, (const bf*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
+                       (const float*)nullptr, (const float*)nullptr, false));
+          pend(SLM_K_GEMM_DX, st);
+          pbeg(st);
+          CK(simt_gemm(gqp, 1L, (long)d, (const bf*)abuf, 1L, (long)d, (bf*)m.d.dW + l * Wl, (long)d, d, d, B,
+                       (const float*)nullptr, (const float*)nullptr, false));
+          pend(SLM_K_GEMM_DW, st);
+        } else {
+          pbeg(st);
+          CK(simt_gemm(g, (long)d, 1L, (const float*)m.d.W + l * Wl, 1L, (long)d, da, (long)d, B, d, d,
+                       (const float*)nullptr, (const float*)nullptr, false));
+          pend(SLM_K_GEMM_DX, st);
+          pbeg(st);
+          CK(simt_gemm(g, 1L, (long)d, (const float*)abuf, 1L, (long)d, (float*)m.d.dW + l * Wl, (long)d, d, d, B,
+                       (const float*)nullptr, (const float*)nullptr, false));
+          pend(SLM_K_GEMM_DW, st);
+        }
+        pbeg(st);
+        if (bf16)
+          CK(launch_k(bn_bwd_kernel<bf>, colgrid, blk, 0, st, pdl, (const float*)da, xl, (const float*)stats, ga, be,
+                      g, dxl, B, d, dga, dbe, dbp, gq[(gcur + 1) % 3]));
+        else
+          CK(launch_k(bn_bwd_kernel<float>, colgrid, blk, 0, st, pdl, (const float*)da, xl, (const float*)stats, ga,
+                      be, g, dxl, B, d, dga, dbe, dbp, (float*)nullptr));
+        pend(SLM_K_BN_BWD, st);
+        gcur = (gcur + 1) % 3;
+        abuf_node = -1;
+        nl += 4;
+      }
+      // data-parallel: all-reduce the bucket [l, bucket_hi] once its last layer is done
+      if (comm && comm->world > 1 && (bucket_hi - l + 1 >= bucket_layers || l == 0)) {
+        const int lo = l, cnt = bucket_hi - l + 1;
+        cudaEvent_t ev = comm->events[cev_i++ % comm->events.size()];
+        CK(cudaEventRecord(ev, side ? m.s2 : st));
+        CK(cudaStreamWaitEvent(comm->stream, ev, 0));
+        cudaEvent_t ev1 = comm->events[cev_i++ % comm->events.size()];
+        CK(cudaEventRecord(ev1, st));
+        CK(cudaStreamWaitEvent(comm->stream, ev1, 0));
+        g_nccl.GroupStart();
+        int r = 0;
+        r |= g_nccl.AllReduce((uint8_t*)m.d.dW + (size_t)lo * per_layer, (uint8_t*)m.d.dW + (size_t)lo * per_layer,
+                              (size_t)cnt * Wl, bf16 ? NCCL_BF16 : NCCL_FLOAT32, NCCL_SUM, comm->comm, comm->stream);
+        r |= g_nccl.AllReduce(m.d.dgamma + (size_t)lo * d, m.d.dgamma + (size_t)lo * d, (size_t)cnt * d,
+                              NCCL_FLOAT32, NCCL_SUM, comm->comm, comm->stream);
+        r |= g_nccl.AllReduce(m.d.dbeta + (size_t)lo * d, m.d.dbeta + (size_t)lo * d, (size_t)cnt * d, NCCL_FLOAT32,
+                              NCCL_SUM, comm->comm, comm->stream);
+        g_nccl.GroupEnd();
+        if (r) {
+          set_error("ncclAllReduce failed");
+          return SLM_E_NCCL;
+        }
+        bucket_hi = l - 1;
+      }
+      ++kb;
+    }
+  }
+  // join the dW stream
+  if (side && kb > 0 && dw_event[kb - 1] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - 1]], 0));
+  if (comm && comm->world > 1) {
+    // db (all layers; db_0 is final after the last backward) and the loss, then join
+    cudaEvent_t ev = comm->events[cev_i++ % comm->events.size()];
+    CK(cudaEventRecord(ev, st));
+    CK(cudaStreamWaitEvent(comm->stream, ev, 0));
+    g_nccl.GroupStart();
+    int r = 0;
+    r |= g_nccl.AllReduce(m.d.db, m.d.db, (size_t)n * d, NCCL_FLOAT32, NCCL_SUM, comm->comm, comm->stream);
+    r |= g_nccl.AllReduce(loss, loss, 1, NCCL_FLOAT32, NCCL_SUM, comm->comm, comm->stream);
+    g_nccl.GroupEnd();
+    if (r) {
+      set_error("ncclAllReduce failed");
+      return SLM_E_NCCL;
+    }
+    cudaEvent_t ev2 = comm->events[cev_i++ % comm->events.size()];
+    CK(cudaEventRecord(ev2, comm->stream));
+    CK(cudaStreamWaitEvent(st, ev2, 0));
+  }
+  CK(cudaGetLastError());
+  if (launches) *launches = nl;
+  return SLM_OK;
+}
+
+slm_status check_plan_model(const slm_plan* p, const slm_model* m) {
+  if (!p || !m) {
+    set_error("null plan/model");
+    return SLM_E_ARG;
+  }
+  if (p->graph_kind != SLM_MODEL_CHAIN || p->dims[0] != m->d.n_layers || p->dims[1] != m->d.batch ||
+      p->dims[2] != m->d.width) {
+    set_error("plan was not built for this chain's dims (use slm_graph_chain)");
+    return SLM_E_SHAPE;
+  }
+  return SLM_OK;
+}
+
+}  // namespace

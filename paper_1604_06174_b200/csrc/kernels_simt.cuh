@@ -155,121 +155,6 @@ __global__ void __launch_bounds__(256) bn_bwd_kernel(
   if (db_prev) db_prev[f] = S3;
 }
 
-// ------------------------------------------------------------------ register-resident variants
-// For B <= 32*R: one CTA = 32 features x 32 warps, warp w owns rows w, w+32, ... (R of them)
-// held in registers, so x / da / g are read from memory exactly once with all R loads in
-// flight per thread (the loops above are load-latency bound).  Same per-feature reduction
-// order on every call: per-thread serial over its rows, then the 32 warp partials in order.
-template <int R>
-__device__ __forceinline__ float cta_feature_sum(float v, float (*red)[33], int w, int lane) {
-  red[w][lane] = v;
-  __syncthreads();
-  float t = 0.f;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) t = __fadd_rn(t, red[i][lane]);
-  __syncthreads();
-  return t;
-}
-
-template <class T, int R>
-__global__ void __launch_bounds__(1024) bn_act_rk(const float* __restrict__ x, const float* __restrict__ gamma,
-                                                  const float* __restrict__ beta, int B, int d,
-                                                  float* __restrict__ stats, T* __restrict__ a) {
-  __shared__ float red[32][33];
-  pdl_wait();
-  pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  const bool ok = f < d;
-  float v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int b = w + 32 * i;
-    v[i] = (ok && b < B) ? x[(size_t)b * d + f] : 0.f;
-  }
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (w + 32 * i < B) s = __fadd_rn(s, v[i]);
-  const float mu = __fdiv_rn(cta_feature_sum<R>(s, red, w, lane), (float)B);
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (w + 32 * i < B) {
-      const float c = __fsub_rn(v[i], mu);
-      q = __fmaf_rn(c, c, q);
-    }
-  const float var = __fdiv_rn(cta_feature_sum<R>(q, red, w, lane), (float)B);
-  const float rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, kEps)));
-  if (!ok) return;
-  if (w == 0) {
-    stats[f] = mu;
-    stats[d + f] = rstd;
-  }
-  const float g = gamma[f], bt = beta[f];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int b = w + 32 * i;
-    if (b < B) a[(size_t)b * d + f] = from_f32<T>(fmaxf(bn_u(bn_xhat(v[i], mu, rstd), g, bt), 0.f));
-  }
-}
-
-template <class GQ, int R>
-__global__ void __launch_bounds__(1024) bn_bwd_rk(
-    const float* __restrict__ da, const float* __restrict__ x, const float* __restrict__ stats,
-    const float* __restrict__ gamma, const float* __restrict__ beta, const float* g, float* dx, int B, int d,
-    float* __restrict__ dgamma, float* __restrict__ dbeta, float* __restrict__ db_prev, GQ* __restrict__ gq) {
-  __shared__ float red[32][33];
-  pdl_wait();
-  pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  const bool ok = f < d;
-  const float mu = ok ? stats[f] : 0.f, rstd = ok ? stats[d + f] : 0.f;
-  const float ga = ok ? gamma[f] : 0.f, bt = ok ? beta[f] : 0.f;
-  float xh[R], du[R], gv[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int b = w + 32 * i;
-    const bool in = ok && b < B;
-    const size_t j = (size_t)b * d + f;
-    const float xv = in ? x[j] : 0.f;
-    const float dav = in ? da[j] : 0.f;
-    gv[i] = in ? g[j] : 0.f;
-    xh[i] = bn_xhat(xv, mu, rstd);
-    du[i] = (in && bn_u(xh[i], ga, bt) > 0.f) ? dav : 0.f;
-  }
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (w + 32 * i < B) {
-      s1 = __fadd_rn(s1, du[i]);
-      s2 = __fmaf_rn(du[i], xh[i], s2);
-    }
-  const float S1 = cta_feature_sum<R>(s1, red, w, lane);
-  const float S2 = cta_feature_sum<R>(s2, red, w, lane);
-  const float invB = __frcp_rn((float)B);
-  const float m1 = __fmul_rn(S1, invB), m2 = __fmul_rn(S2, invB);
-  const float k = __fmul_rn(ga, rstd);
-  float s3 = 0.f;
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int b = w + 32 * i;
-    if (ok && b < B) {
-      const size_t j = (size_t)b * d + f;
-      const float v = __fadd_rn(gv[i], __fmul_rn(k, __fsub_rn(__fsub_rn(du[i], m1), __fmul_rn(xh[i], m2))));
-      dx[j] = v;
-      s3 = __fadd_rn(s3, v);
-      if (gq) gq[j] = from_f32<GQ>(v);
-    }
-  }
-  const float S3 = cta_feature_sum<R>(s3, red, w, lane);
-  if (!ok || w != 0) return;
-  dgamma[f] = S2;
-  dbeta[f] = S1;
-  if (db_prev) db_prev[f] = S3;
-}
-
 // ------------------------------------------------------------------ column sum (db_{n-1})
 __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ g, int B, int d,
                                                      float* __restrict__ out) {

@@ -47,6 +47,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -117,13 +120,14 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool 
 }
 
 // ---------------------------------------------------------------- epilogues
-// Each receives (m, n, acc) for 32 consecutive n of one m per call.
-struct EpiResid {  // forward: out[n*ld+m] = resid[n*ld+m] + acc + bias[m]  (out may alias resid)
+// Each receives (m, n0, acc[32], ks): rows m, columns n0..n0+31 of the tile, K slice ks.
+struct EpiResid {  // forward, no split: out[n*ld+m] = resid[n*ld+m] + acc + bias[m]  (out may alias resid)
+  static constexpr bool kTma = false;
   float* out;
   const float* resid;
   const float* bias;
   long ld;
-  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int) const {
     const float bm = bias[m];
     // all 32 loads first: `out` may alias `resid` (in-place Block), so loads interleaved with
     // stores would be serialised by the compiler (one memory latency per element)
@@ -135,20 +139,44 @@ struct EpiResid {  // forward: out[n*ld+m] = resid[n*ld+m] + acc + bias[m]  (out
   }
 };
 struct EpiStoreF32 {  // out[n*ld+m] = acc
+  static constexpr bool kTma = false;
   float* out;
   long ld;
-  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int) const {
 #pragma unroll
     for (int j = 0; j < 32; ++j) out[(long)(n0 + j) * ld + m] = acc[j];
   }
 };
 struct EpiStoreBF16 {  // out[n*ld+m] = bf16(acc)
+  static constexpr bool kTma = false;
   __nv_bfloat16* out;
   long ld;
-  __device__ __forceinline__ void operator()(int m, int n0, const float* acc) const {
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int) const {
 #pragma unroll
     for (int j = 0; j < 32; ++j) out[(long)(n0 + j) * ld + m] = __float2bfloat16_rn(acc[j]);
   }
+};
+// split-K partial of slice ks: P[ks][n][m] (fp32, coalesced: a warp writes 32 consecutive m).
+// The consumer (bn_act_rk / bn_bwd_rk) sums the slices in the fixed order 0..SK-1.
+struct EpiPartial {
+  static constexpr bool kTma = false;
+  float* P;
+  long ld;      // = M
+  long slice;   // = N * M
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int ks) const {
+    float* p = P + (long)ks * slice + m;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) p[(long)(n0 + j) * ld] = acc[j];
+  }
+};
+
+// the same partials written by TMA bulk tensor stores from a smem staging box (tmC maps P
+// as [slices * N rows][M] fp32, box {128, 32}); row of (ks, n) = ks * N + n
+struct EpiPartialTma {
+  static constexpr bool kTma = true;
+  int n_rows;   // = N
+  __device__ __forceinline__ int row0(int ks) const { return ks * n_rows; }
+  __device__ __forceinline__ void operator()(int, int, const float*, int) const {}
 };
 
 // ---------------------------------------------------------------- the kernel
@@ -165,15 +193,34 @@ struct TcCfg {
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// debug instrumentation: per-CTA %globaltimer stamps at 8 phase points (null = off)
+__device__ unsigned long long* g_slm_ts = nullptr;
+__device__ __forceinline__ void ts_mark(int phase) {
+  unsigned long long* p = g_slm_ts;
+  if (p != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    p[cta * 8 + phase] = t;
+  }
+}
+
 // a_row0/b_row0: row offsets added to the tensor-map coordinates of A / B (e.g. layer l's
 // weight block inside the [n*d, d] weight tensor).
 // PREFETCH_A: A is read-only for the whole step (the weights), so its first pipeline stages are
 // requested before griddepcontrol.wait, i.e. while the previous kernel is still finishing
 // (programmatic dependent launch); B and the epilogue inputs are read only after the wait.
+// Split-K: gridDim.z = number of K slices; CTA z accumulates K range [z*K/Z, (z+1)*K/Z) and
+// hands its fp32 partial to the epilogue with ks = z (EpiPartial).  Measured on B200 the
+// per-SM operand ingest (~64-70 B/clk via TMA, and SS-mode tcgen05 operand reads at a
+// similar rate) bounds these skinny GEMMs, so K is split until each SM ingests ~192 KiB;
+// the partials are summed by the BN kernel that consumes the GEMM output anyway
+// (distributed-shared-memory reduction was measured ~16 KB/us per SM: too slow).
 template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int K, int a_row0, int b_row0, Epi epi) {
+                   const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg) {
+  ts_mark(0);
   using C = TcCfg<BN, A_MN, B_MN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -184,7 +231,9 @@ __global__ void __launch_bounds__(128, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * C::BM, n0 = blockIdx.y * BN;
-  const int nk = K / C::BK;
+  const int ks = (int)blockIdx.z;
+  const int nk = K / C::BK / (int)gridDim.z;
+  const int kbase = ks * nk * C::BK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -207,11 +256,11 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_launch();
+  ts_mark(1);
 
   auto load_a = [&](int kb, int s) {
     uint8_t* sa = smem + s * C::STAGE;
-    const int k0 = kb * C::BK;
+    const int k0 = kbase + kb * C::BK;
     if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
       tma_load_2d(sa, &tmA, &full[s], m0, a_row0 + k0);
       tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, a_row0 + k0);
@@ -221,7 +270,7 @@ __global__ void __launch_bounds__(128, 1)
   };
   auto load_b = [&](int kb, int s) {
     uint8_t* sb = smem + s * C::STAGE + C::A_BYTES;
-    const int k0 = kb * C::BK;
+    const int k0 = kbase + kb * C::BK;
     if (B_MN) {
 #pragma unroll
       for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, b_row0 + k0);
@@ -230,7 +279,15 @@ __global__ void __launch_bounds__(128, 1)
     }
   };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && (dbg & 2)) {
+    // debug probe: MMA issue rate only (no TMA, operands are whatever is in smem)
+    pdl_wait();
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % C::STAGES;
+      if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+      mbar_arrive(&full[s]);
+    }
+  } else if (warp == 0 && lane == 0) {
     // ===== TMA producer
     int kb0 = 0;
     if (PREFETCH_A) {
@@ -260,6 +317,10 @@ __global__ void __launch_bounds__(128, 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * C::STAGE);
       const uint32_t sb = sa + C::A_BYTES;
+      if (dbg & 1) {  // debug probe: data movement only, no MMA
+        mbar_arrive(&empty[s]);
+        continue;
+      }
 #pragma unroll
       for (int kk = 0; kk < C::BK / 16; ++kk) {
         // K-major SW128: +32 B per K=16 inside the 128-B row; SBO = 8 rows * 128 B.
@@ -270,21 +331,59 @@ __global__ void __launch_bounds__(128, 1)
       }
       tc_commit(&empty[s]);
     }
-    tc_commit(accum);
+    if (dbg & 1)
+      mbar_arrive(accum);
+    else
+      tc_commit(accum);
   }
   __syncwarp();
   // ===== epilogue: TMEM -> registers -> global
   pdl_wait();
   mbar_wait(accum, 0);
   tc_fence_after();
-  const int m = m0 + warp * 32 + lane;
+  // let the dependent kernel launch only now (its CTAs would otherwise sit on this kernel's SMs
+  // waiting in griddepcontrol.wait for the whole main loop; measured: early trigger is slower)
+  pdl_launch();
+  ts_mark(2);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const int m = m0 + warp * 32 + lane;
+  if constexpr (Epi::kTma) {
+    // fp32 tile -> smem box [32 n][128 m] (a warp writes 128 contiguous bytes: conflict-free)
+    // -> cp.async.bulk.tensor store, double-buffered; the pipeline smem is free after the MMAs.
+    float* stage = reinterpret_cast<float*>(smem);
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 32) {
-    float acc[32];
-    tmem_ld32(trow + c, acc);
-    epi(m, n0 + c, acc);
+    for (int c = 0; c < BN; c += 32) {
+      const int buf = (c >> 5) & 1;
+      if (c >= 64) {  // the store issued two chunks ago must have read this buffer
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+      }
+      float acc[32];
+      tmem_ld32(trow + c, acc);
+      float* sp = stage + buf * 4096 + warp * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sp[j * 128] = acc[j];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&tmC)),
+            "r"(smem_u32(stage + buf * 4096)), "r"(m0), "r"(epi.row0(ks) + n0 + c)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float acc[32];
+      tmem_ld32(trow + c, acc);
+      epi(m, n0 + c, acc, ks);
+    }
   }
+  ts_mark(7);
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
