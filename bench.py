@@ -243,41 +243,56 @@ def main():
     value = Bg / (ms / 1e3)
     launches = model.launches(plan)
 
-    # ---- roofline of the dominant kernel: per-kernel CUDA events on the launching stream
-    model.set_option("profile_events", 1)
+    # ---- roofline of the dominant kernel (the tcgen05 GEMMs), measured live on the device clock:
+    # every GEMM launch of the step stamps %globaltimer at start/end of each CTA (profile_ts), in
+    # the same CUDA-graph launch configuration as the timed region; span = latest end - earliest
+    # start over the launch's CTAs (the event pair of a single graph node cannot be recorded
+    # without breaking the graph's programmatic dependent launches).
+    n_gemm = 3 * n + plan.extra_forward
+    ts = torch.zeros(n_gemm * 1024 * 2, dtype=torch.int64, device=dev)
+    model.set_option("profile_ts", n_gemm)
+    model.set_option("profile_ts_buffer", ts.data_ptr())
     bufs = model.buffers(plan, dev)
     prof_steps = max(1, min(args.steps, 3))
     with torch.cuda.stream(stream):
+        model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)     # eager + capture
         model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
     torch.cuda.synchronize()
     model.kernel_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(prof_steps):
+    prof_ms = 0.0
+    for _ in range(prof_steps):
+        e0.record(stream)
+        with torch.cuda.stream(stream):
             model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
-    e1.record(stream)
-    torch.cuda.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        prof_ms += e0.elapsed_time(e1) / prof_steps
+        kt = model.kernel_times(reset=False)
     kt = model.kernel_times(reset=True)
-    prof_ms = e0.elapsed_time(e1) / prof_steps
-    model.set_option("profile_events", 0)
+    model.set_option("profile_ts", 0)
     pk = _peaks()
     gemm_flop = 2.0 * B * d * d          # every GEMM kind: 2*B*d^2 per launch
-    gemm_ms = sum(kt[k][0] for k in ("gemm_fwd", "gemm_dx", "gemm_dw"))
-    gemm_cnt = sum(kt[k][1] for k in ("gemm_fwd", "gemm_dx", "gemm_dw"))
+    kinds = ("gemm_fwd", "gemm_dx", "gemm_dw")
+    gemm_ms = sum(kt[k][0] for k in kinds)
+    gemm_cnt = sum(kt[k][1] for k in kinds)
     avg_ms = gemm_ms / max(1, gemm_cnt)
     achieved = gemm_flop / (avg_ms / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    kernel_share = {k: round(v[0] / max(1e-9, sum(x[0] for x in kt.values())), 4) for k, v in kt.items()}
-    per_kind = {k: {"avg_us": round(1e3 * v[0] / max(1, v[1]), 3), "launches": v[1] // prof_steps}
-                for k, v in kt.items()}
+    per_kind = {k: {"avg_us": round(1e3 * kt[k][0] / max(1, kt[k][1]), 3),
+                    "launches_per_step": kt[k][1] // prof_steps,
+                    "tflops": round(gemm_flop / (kt[k][0] / max(1, kt[k][1]) / 1e3) / 1e12, 1) if kt[k][1] else None}
+                for k in kinds}
+    crit_ms = (kt["gemm_fwd"][0] + kt["gemm_dx"][0]) / prof_steps   # dW runs on a second stream
     roofline = dict(bound="tensor", achieved=round(achieved, 2), peak=peak, unit="TFLOP/s",
                     frac=round(achieved / peak, 4), traffic=None,
                     kernel="tc_gemm_kernel (forward, dX, dW GEMMs; 2*B*d^2 FLOP per launch)",
                     peak_source="MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                     if "_fallback" not in pk else "fallback (B200_PROFILING.md)",
-                    per_kind=per_kind, share_of_kernel_time=kernel_share,
-                    step_ms_with_events=round(prof_ms, 3))
+                    timing="device clock per launch (%globaltimer, CTA min start .. max end) inside the graph",
+                    per_kind=per_kind,
+                    gemm_share_of_step=round(crit_ms / prof_ms, 4) if prof_ms else None,
+                    step_ms_instrumented=round(prof_ms, 3))
     step_flop = 2.0 * B * d * d * (4 * n - math.isqrt(max(0, n - 1)) - 1 if args.strategy == "sqrt" else 3 * n)
 
     # ---- non-checkpointed step (the "vs no-ckpt" half of the metric)

@@ -221,7 +221,13 @@ void slm_model_destroy(slm_model* m);
  *   gemm_impl       0 = tcgen05/TMA tensor-core GEMMs (bf16, default), 1 = SIMT FFMA GEMMs
  *   bn_fwd, bn_dx, bn_dw   N tile of the forward / dX / dW tcgen05 GEMMs (32|64|128|256)
  *   profile_events  1 = record a CUDA event pair around every kernel of the step, by kind
- *                   (read with slm_model_kernel_times after the stream is synchronised) */
+ *                   (read with slm_model_kernel_times after the stream is synchronised)
+ *   profile_ts      N > 0: the first N tcgen05 GEMM launches of a step record the device clock
+ *                   (%globaltimer) at start and end of every CTA into profile_ts_buffer
+ *                   (caller-owned, zeroed device buffer of N*1024*2 uint64, passed as an int64
+ *                   pointer value); slm_model_kernel_times then adds each launch's span
+ *                   (latest end - earliest start) to its GEMM kind.  Works inside the CUDA graph.
+ *   fused, dw_stream, pdl, sk_fwd, sk_dx   lowering switches */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
 /* Kernel kinds for slm_model_kernel_times. */
 enum { SLM_K_BN_ACT = 0, SLM_K_GEMM_FWD = 1, SLM_K_GEMM_DX = 2, SLM_K_GEMM_DW = 3, SLM_K_BN_BWD = 4,

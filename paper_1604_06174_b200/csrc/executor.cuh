@@ -191,6 +191,12 @@ struct slm_model {
   int64_t last_launches = 0;
   cudaStream_t s2 = nullptr;           // second stream (dW)
   std::vector<cudaEvent_t> sync_ev;    // fork/join events (reused every step)
+  // profile_ts: device-clock (%globaltimer) start/end of every CTA of the first profile_ts GEMM
+  // launches of a step, in the caller's buffer ts_buf ([slot][1024][2] uint64, zeroed)
+  int profile_ts = 0;
+  void* ts_buf = nullptr;
+  std::vector<int> ts_kind;
+  int ts_used = 0;
   // profile_events: (start, end, kind) per kernel, read by slm_model_kernel_times
   int profile = 0;
   struct EvPair {
@@ -437,6 +443,13 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
     return launch_k(bn_act_kernel<float>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (float*)abuf);
   };
 
+  int ts_slot = 0;
+  if (m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) m.ts_kind.resize(m.profile_ts);
+  auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock GEMM timing
+    if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
+    m.ts_kind[ts_slot] = kind;
+    return (++ts_slot) << 8;
+  };
   int abuf_node = -1;     // node whose activation operand a = ReLU(BN(x)) is resident in abuf
   int kb = 0;             // backward index: the k-th gradient Block node
   int gcur = 0;           // gq buffer holding the bf16 copy of the current upstream gradient
@@ -464,7 +477,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         slmk::EpiPartialTma epi{B};
         pbeg(st);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, L.sk_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0,
-                                                                       epi, st, pdl, 0, &m.mP)) != SLM_OK)
+                                                                       epi, st, pdl, gdbg(SLM_K_GEMM_FWD), &m.mP)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_FWD, st);
         // finalize x_{l+1} and produce a_{l+1} for the next Block (BN of layer l+1)
@@ -525,7 +538,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         slmk::EpiPartialTma e1{B};
         pbeg(st);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d,
-                                                                      l * d, 0, e1, st, pdl, 0, &m.mP)) != SLM_OK)
+                                                                      l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX), &m.mP)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX, st);
         // bn_bwd(k) overwrites gq[(k+1)%3] and ab[k%2], last read by dW of backward k-2
@@ -545,7 +558,8 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         slmk::EpiStoreBF16 e2{(bf*)m.d.dW + l * Wl, d};
         pbeg(sw);
         if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, 1, m.mAb_MN[abi], m.mG_MN[gcur], d, d,
-                                                                     B, 0, 0, e2, sw, pdl && !side)) != SLM_OK)
+                                                                     B, 0, 0, e2, sw, pdl && !side,
+                                                                     gdbg(SLM_K_GEMM_DW))) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DW, sw);
         if (side) {
@@ -652,6 +666,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   }
   CK(cudaGetLastError());
   if (launches) *launches = nl;
+  m.ts_used = ts_slot;
   return SLM_OK;
 }
 

@@ -161,6 +161,12 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "sk_dx") m->sk_dx = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
+  else if (k == "profile_ts") m->profile_ts = (int)value;
+  else if (k == "profile_ts_buffer") {
+    m->ts_buf = reinterpret_cast<void*>(value);
+    unsigned long long* p = (unsigned long long*)m->ts_buf;
+    CK(cudaMemcpyToSymbol(slmk::g_slm_ts, &p, sizeof(p)));
+  }
   else if (k == "profile_events") m->profile = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
   else {
@@ -188,6 +194,26 @@ slm_status slm_model_kernel_times(slm_model* m, float* ms, int64_t* count, int32
     m->ev_free.push_back(p.b);
   }
   m->ev_live.clear();
+  // device-clock GEMM spans of the last step (profile_ts): max end - min start over the CTAs
+  if (m->profile_ts > 0 && m->ts_buf && m->ts_used > 0) {
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h((size_t)m->ts_used * 1024 * 2);
+    CK(cudaMemcpy(h.data(), m->ts_buf, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int s = 0; s < m->ts_used; ++s) {
+      unsigned long long t0 = ~0ull, t1 = 0;
+      for (int c = 0; c < 1024; ++c) {
+        unsigned long long a = h[((size_t)s * 1024 + c) * 2], b = h[((size_t)s * 1024 + c) * 2 + 1];
+        if (a == 0 || b == 0) continue;
+        t0 = std::min(t0, a);
+        t1 = std::max(t1, b);
+      }
+      if (t1 > t0 && t0 != ~0ull) {
+        m->acc_ms[m->ts_kind[s]] += (double)(t1 - t0) * 1e-6;
+        m->acc_cnt[m->ts_kind[s]] += 1;
+      }
+    }
+    CK(cudaMemset(m->ts_buf, 0, h.size() * 8));
+  }
   for (int k = 0; k < n_kinds && k < SLM_K_COUNT; ++k) {
     if (ms) ms[k] = (float)m->acc_ms[k];
     if (count) count[k] = m->acc_cnt[k];

@@ -194,14 +194,22 @@ struct TcCfg {
 };
 
 // debug instrumentation: per-CTA %globaltimer stamps at 8 phase points (null = off)
+// Two layouts: dbg >> 8 == 0: [cta][8 phases] (micro-benchmarks); dbg >> 8 == slot + 1: the
+// launch's start (phase 0) and end (phase 7) per CTA at [slot][1024 CTAs][2] — used to time
+// every GEMM of a real step on the device clock (profile_ts option of the model).
 __device__ unsigned long long* g_slm_ts = nullptr;
-__device__ __forceinline__ void ts_mark(int phase) {
+__device__ __forceinline__ void ts_mark(int phase, int dbg) {
   unsigned long long* p = g_slm_ts;
   if (p != nullptr && threadIdx.x == 0) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int slot = (dbg >> 8) - 1;
+    if (slot >= 0 && phase != 0 && phase != 7) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    p[cta * 8 + phase] = t;
+    if (slot >= 0)
+      p[((size_t)slot * 1024 + cta) * 2 + (phase == 7)] = t;
+    else
+      p[cta * 8 + phase] = t;
   }
 }
 
@@ -220,7 +228,7 @@ template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg) {
-  ts_mark(0);
+  ts_mark(0, dbg);
   using C = TcCfg<BN, A_MN, B_MN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  ts_mark(1);
+  ts_mark(1, dbg);
 
   auto load_a = [&](int kb, int s) {
     uint8_t* sa = smem + s * C::STAGE;
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(128, 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * C::STAGE);
       const uint32_t sb = sa + C::A_BYTES;
-      if (dbg & 1) {  // debug probe: data movement only, no MMA
+      if (dbg & 1) {  // debug probe: data movement only, no MMA (bits 0-1 only; bits 8+ = ts slot)
         mbar_arrive(&empty[s]);
         continue;
       }
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(128, 1)
   // let the dependent kernel launch only now (its CTAs would otherwise sit on this kernel's SMs
   // waiting in griddepcontrol.wait for the whole main loop; measured: early trigger is slower)
   pdl_launch();
-  ts_mark(2);
+  ts_mark(2, dbg);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const int m = m0 + warp * 32 + lane;
   if constexpr (Epi::kTma) {
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(128, 1)
       epi(m, n0 + c, acc, ks);
     }
   }
-  ts_mark(7);
+  ts_mark(7, dbg);
   tc_fence_before();
   __syncthreads();
   if (warp == 0)

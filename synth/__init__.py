@@ -70,17 +70,25 @@ def chain_inputs_torch(n_layers, batch, width, dtype="bf16", seed=SEED, device="
 
 
 def lstm_inputs(n_layers, steps, batch, hidden, n_in, n_classes, dtype="f32", seed=SEED):
+    """Unrolled LSTM inputs in the C-ABI layout: W[l] = [W_ih | W_hh] as [4H, Kin_l + H] with
+    Kin_0 = n_in padded up to a multiple of 64 (zero columns), b[l] = b_ih + b_hh [4H],
+    W_o [C, H], b_o [C] (zeros), x [T, B, n_in], labels [T, B]."""
     r = _streams(seed + 1, 8)
     H = hidden
     k = 1.0 / np.sqrt(H)
-    W_ih = [r[0].uniform(-k, k, (4 * H, n_in if l == 0 else H)) for l in range(n_layers)]
-    W_hh = r[1].uniform(-k, k, (n_layers, 4 * H, H))
-    b_ih = r[2].uniform(-k, k, (n_layers, 4 * H))
-    b_hh = r[3].uniform(-k, k, (n_layers, 4 * H))
+    kin0 = -(-n_in // 64) * 64
+    W = []
+    for l in range(n_layers):
+        kin = kin0 if l == 0 else H
+        w = np.zeros((4 * H, kin + H))
+        w[:, : (n_in if l == 0 else H)] = r[0].uniform(-k, k, (4 * H, n_in if l == 0 else H))
+        w[:, kin:] = r[1].uniform(-k, k, (4 * H, H))
+        W.append(w)
+    b = r[2].uniform(-k, k, (n_layers, 4 * H)) + r[3].uniform(-k, k, (n_layers, 4 * H))
     W_o = r[4].standard_normal((n_classes, H)) / np.sqrt(H)
     x = r[5].standard_normal((steps, batch, n_in))
     labels = r[6].integers(0, n_classes, size=(steps, batch)).astype(np.int32)
     cast = bf16_values if dtype == "bf16" else (lambda a: np.asarray(a, np.float32))
-    return dict(W_ih=[cast(w) for w in W_ih], W_hh=cast(W_hh),
-                b=(b_ih + b_hh).astype(np.float32), W_o=cast(W_o),
-                b_o=np.zeros(n_classes, np.float32), x=x.astype(np.float32), labels=labels)
+    return dict(W=[cast(w) for w in W], b=b.astype(np.float32), W_o=cast(W_o),
+                b_o=np.zeros(n_classes, np.float32), x=x.astype(np.float32), labels=labels,
+                n_in=n_in)
