@@ -215,6 +215,27 @@ typedef struct {
 
 typedef struct slm_model slm_model;
 slm_status slm_model_chain(const slm_chain_desc* desc, slm_model** out);
+
+/* Unrolled multi-layer LSTM (reading A13: gate order i, f, g, o; h_0 = c_0 = 0;
+ * a softmax head after the top layer at every step; loss = sum_t sum_b CE / (T B)).
+ * All device pointers, caller-owned; bf16 GEMM operands only (reading A11):
+ *   W     bf16, layer 0 [4H][Kin0 + H] then layers 1.. [4H][2H], each = [W_ih | W_hh] (out, in);
+ *         Kin0 = round_up(n_in, 128), the padding columns are ignored (they multiply zeros)
+ *   b     fp32 [L][4H] (= b_ih + b_hh)
+ *   W_o   bf16 [Cp][H], Cp = round_up(n_classes, 128); rows >= n_classes are never read
+ *         into the loss (their logits are masked) but must be finite
+ *   b_o   fp32 [Cp]
+ *   dW, db, dW_o, db_o   fp32, same layouts; overwritten by every step (the per-step weight
+ *         gradients are summed over time inside the step).
+ * Constraints of the tcgen05 path: batch in {64, 128, 256}, hidden % 128 == 0.
+ * Step inputs: x0 = x fp32 [T][B][n_in], labels int32 [T][B] in [0, n_classes).
+ * The LSTM runs replicas-only across GPUs (comm must be NULL). */
+typedef struct {
+  int32_t n_layers, steps, batch, hidden, n_in, n_classes;
+  const void* W; const float* b; const void* W_o; const float* b_o;
+  float* dW; float* db; float* dW_o; float* db_o;
+} slm_lstm_desc;
+slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out);
 void slm_model_destroy(slm_model* m);
 /* Options (int64 values):
  *   use_graph       capture the whole step in a CUDA graph per buffer set (default 1)
@@ -245,8 +266,8 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
 typedef struct slm_comm slm_comm;
 
 /* step(plan, params, batch) -> loss, grads.
- *   x0      device [batch][d] fp32 (bound to the Input node's tag)
- *   labels  device [batch] int32 in [0, d)
+ *   x0      device [batch][d] fp32 (bound to the Input node's tag); LSTM: [T][B][n_in]
+ *   labels  device [batch] int32 in [0, d); LSTM: [T][B] in [0, n_classes)
  *   pool    device, >= plan pool_bytes, 256-byte aligned
  *   ws      device, >= slm_workspace_bytes, 256-byte aligned
  *   loss    device, 1 float (bound to the loss node's tag)

@@ -6,7 +6,7 @@ input of each timestamp is a continuous 50 dimension vector and the output is so
 h_0 = c_0 = 0, a softmax head at every step, loss = mean over (t, b).
 
 Parameter layout (shared with the device path's C ABI, a layout only — no code is shared):
-  W[l]   [4H, Kin_l + H]  = [W_ih | W_hh], Kin_0 = the input width padded to a multiple of 64
+  W[l]   [4H, Kin_l + H]  = [W_ih | W_hh], Kin_0 = the input width padded to a multiple of 128
                            (padding columns multiply zero-padded inputs), Kin_l = H for l > 0
   b[l]   [4H]             = b_ih + b_hh
   W_o    [C, H], b_o [C]  the per-step softmax head

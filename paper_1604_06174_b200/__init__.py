@@ -211,22 +211,10 @@ class Comm:
             self._h = None
 
 
-class ChainModel:
-    """slm_model for the residual chain.  params/grads: dicts of CUDA tensors
-    W [n,d,d] (bf16 or f32), b/gamma/beta [n,d] f32; dW like W; db/dgamma/dbeta f32."""
+class _Model:
+    """Common slm_model methods (include/slm.h "device step")."""
 
-    def __init__(self, params, grads, dtype="bf16", batch=None, batch_global=0, **options):
-        W = params["W"]
-        n, d = W.shape[0], W.shape[1]
-        self.params, self.grads = params, grads
-        self.dtype = dtype
-        self.n, self.d = n, d
-        self.batch = batch
-        desc = _lib.ChainDesc(1 if dtype == "bf16" else 0, n, batch, d, batch_global,
-                              _ptr(W), _ptr(params["b"]), _ptr(params["gamma"]), _ptr(params["beta"]),
-                              _ptr(grads["W"]), _ptr(grads["b"]), _ptr(grads["gamma"]), _ptr(grads["beta"]))
-        h = C.c_void_p()
-        check(lib.slm_model_chain(C.byref(desc), C.byref(h)), "slm_model_chain")
+    def _init(self, h, options):
         self._h = h
         for k, v in options.items():
             self.set_option(k, v)
@@ -290,6 +278,49 @@ class ChainModel:
         if getattr(self, "_h", None):
             lib.slm_model_destroy(self._h)
             self._h = None
+
+
+class ChainModel(_Model):
+    """slm_model for the residual chain.  params/grads: dicts of CUDA tensors
+    W [n,d,d] (bf16 or f32), b/gamma/beta [n,d] f32; dW like W; db/dgamma/dbeta f32."""
+
+    def __init__(self, params, grads, dtype="bf16", batch=None, batch_global=0, **options):
+        W = params["W"]
+        n, d = W.shape[0], W.shape[1]
+        self.params, self.grads = params, grads
+        self.dtype = dtype
+        self.n, self.d = n, d
+        self.batch = batch
+        desc = _lib.ChainDesc(1 if dtype == "bf16" else 0, n, batch, d, batch_global,
+                              _ptr(W), _ptr(params["b"]), _ptr(params["gamma"]), _ptr(params["beta"]),
+                              _ptr(grads["W"]), _ptr(grads["b"]), _ptr(grads["gamma"]), _ptr(grads["beta"]))
+        h = C.c_void_p()
+        check(lib.slm_model_chain(C.byref(desc), C.byref(h)), "slm_model_chain")
+        self._init(h, options)
+
+
+class LstmModel(_Model):
+    """slm_model for the unrolled LSTM (include/slm.h slm_lstm_desc).  params: dict of CUDA
+    tensors W (flat bf16: layer 0 [4H, Kin0+H] then [4H, 2H] per layer), b [L, 4H] f32,
+    W_o bf16 [Cp, H], b_o f32 [Cp]; grads: the same keys in fp32."""
+
+    def __init__(self, params, grads, n_layers, steps, batch, hidden, n_in, n_classes, **options):
+        self.params, self.grads = params, grads
+        self.L, self.T, self.B, self.H, self.I, self.C = n_layers, steps, batch, hidden, n_in, n_classes
+        desc = _lib.LstmDesc(n_layers, steps, batch, hidden, n_in, n_classes,
+                             _ptr(params["W"]), _ptr(params["b"]), _ptr(params["W_o"]), _ptr(params["b_o"]),
+                             _ptr(grads["W"]), _ptr(grads["b"]), _ptr(grads["W_o"]), _ptr(grads["b_o"]))
+        h = C.c_void_p()
+        check(lib.slm_model_lstm(C.byref(desc), C.byref(h)), "slm_model_lstm")
+        self._init(h, options)
+
+    @staticmethod
+    def kin0(n_in):
+        return -(-n_in // 128) * 128
+
+    @staticmethod
+    def cpad(n_classes):
+        return -(-n_classes // 128) * 128
 
 
 def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None, split=1):

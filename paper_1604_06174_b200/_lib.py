@@ -44,6 +44,12 @@ class ChainDesc(C.Structure):
                 ("dW", vp), ("db", vp), ("dgamma", vp), ("dbeta", vp)]
 
 
+class LstmDesc(C.Structure):
+    _fields_ = [("n_layers", i32), ("steps", i32), ("batch", i32), ("hidden", i32), ("n_in", i32),
+                ("n_classes", i32), ("W", vp), ("b", vp), ("W_o", vp), ("b_o", vp),
+                ("dW", vp), ("db", vp), ("dW_o", vp), ("db_o", vp)]
+
+
 def _sig(name, res, *args):
     f = getattr(lib, name)
     f.restype = res
@@ -70,6 +76,7 @@ _sig("slm_plan_trace", i32, vp, i64p, i32, i32p)
 _sig("slm_plan_destroy", None, vp)
 _sig("slm_recursion_estimate", i32, i64, i64, i64p, i64p)
 _sig("slm_model_chain", i32, C.POINTER(ChainDesc), C.POINTER(vp))
+_sig("slm_model_lstm", i32, C.POINTER(LstmDesc), C.POINTER(vp))
 _sig("slm_model_destroy", None, vp)
 _sig("slm_model_set_option", i32, vp, C.c_char_p, i64)
 _sig("slm_workspace_bytes", i32, vp, vp, C.POINTER(C.c_size_t))

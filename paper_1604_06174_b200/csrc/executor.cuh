@@ -173,8 +173,23 @@ struct GraphKey {
   }
 };
 
+// LSTM executor state (executor_lstm.cuh): tensor maps bound to the weights / workspace and
+// the Sum node's pool-offset table
+struct LstmMaps {
+  std::vector<CUtensorMap> wK, wMN;   // per layer W_l K-major / MN-major
+  CUtensorMap woK, woMN, dpK, dpMN, hopK, hopMN, dlK, dlMN;
+  const void* ws = nullptr;
+};
+struct slm_lstm_state {
+  LstmMaps maps;
+  const void* offs_ws = nullptr;
+  const void* offs_plan = nullptr;
+};
+
 struct slm_model {
   slm_chain_desc d{};
+  slm_lstm_desc ld{};
+  slm_lstm_state lst;
   int kind = SLM_MODEL_CHAIN;
   int use_graph = 1;
   int gemm_impl = 0;      // 0 tcgen05 (bf16), 1 SIMT
@@ -674,6 +689,15 @@ slm_status check_plan_model(const slm_plan* p, const slm_model* m) {
   if (!p || !m) {
     set_error("null plan/model");
     return SLM_E_ARG;
+  }
+  if (m->kind == SLM_MODEL_LSTM) {
+    const slm_lstm_desc& d = m->ld;
+    if (p->graph_kind != SLM_MODEL_LSTM || p->dims[0] != d.n_layers || p->dims[1] != d.steps ||
+        p->dims[2] != d.batch || p->dims[3] != d.hidden || p->dims[4] != d.n_in) {
+      set_error("plan was not built for this LSTM's dims (use slm_graph_lstm)");
+      return SLM_E_SHAPE;
+    }
+    return SLM_OK;
   }
   if (p->graph_kind != SLM_MODEL_CHAIN || p->dims[0] != m->d.n_layers || p->dims[1] != m->d.batch ||
       p->dims[2] != m->d.width) {

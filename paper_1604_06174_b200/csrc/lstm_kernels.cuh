@@ -1,0 +1,201 @@
+// SIMT kernels of the unrolled-LSTM step (sm_100a).  The dense contractions (gates, head
+// logits, input/recurrent gradients, weight gradients) run on the tcgen05 GEMM; these kernels
+// do the element-wise cell math, operand packing and the softmax head (PAPER.md:480-485,
+// reading A13: PyTorch gate order i, f, g, o; h_0 = c_0 = 0).
+//
+// Value layouts (fp32, row-major over the batch):
+//   G^l_t  [B][4H]  gate activations (i, f, g, o)
+//   S^l_t  [B][2H]  (h | c)
+//   gradient node of v: gradients w.r.t. v's inputs, concatenated in pred order (reading A17)
+#pragma once
+#include "kernels_simt.cuh"
+
+namespace slmk {
+
+__device__ __forceinline__ float sigm(float x) { return __frcp_rn(__fadd_rn(1.f, expf(-x))); }
+
+// op[b][0:Kin] = x (width xw, zero padded to Kin, source row stride xs), op[b][Kin:Kin+H] = h_prev
+// (h part of S_{t-1}: row stride 2H; null = zeros).  bf16 GEMM operand [B][Kin+H].
+__global__ void __launch_bounds__(256) lstm_pack_kernel(const float* __restrict__ x, int xw, int xs, int Kin,
+                                                        const float* __restrict__ sprev, int H, int B,
+                                                        __nv_bfloat16* __restrict__ op) {
+  pdl_wait();
+  const int K = Kin + H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * K; i += gridDim.x * blockDim.x) {
+    const int b = i / K, k = i % K;
+    float v;
+    if (k < Kin)
+      v = k < xw ? x[(size_t)b * xs + k] : 0.f;
+    else
+      v = sprev ? sprev[(size_t)b * 2 * H + (k - Kin)] : 0.f;
+    op[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// S = (h, c): c = f c_prev + i g, h = o tanh(c)   (sprev null: c_prev = 0)
+__global__ void __launch_bounds__(256) lstm_cell_fwd_kernel(const float* __restrict__ act,
+                                                            const float* __restrict__ sprev, int H, int B,
+                                                            float* __restrict__ s) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, j = i % H;
+    const float* a = act + (size_t)b * 4 * H;
+    const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
+    const float c = __fadd_rn(__fmul_rn(a[H + j], cp), __fmul_rn(a[j], a[2 * H + j]));
+    s[(size_t)b * 2 * H + j] = __fmul_rn(a[3 * H + j], tanhf(c));
+    s[(size_t)b * 2 * H + H + j] = c;
+  }
+}
+
+// Back through S: dS = sum of up to 3 successor slices (dh | dc), each [B][2H] with row stride
+// ld_k (null = absent), added in the fixed order 0, 1, 2.  Output rows (pred order, reading
+// A17): [4H d(acts) | 2H (0 | dc_prev)] when the cell has a predecessor state, else [4H].
+__global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restrict__ d0, int ld0,
+                                                            const float* __restrict__ d1, int ld1,
+                                                            const float* __restrict__ d2, int ld2,
+                                                            const float* __restrict__ act,
+                                                            const float* __restrict__ sprev, int H, int B,
+                                                            float* __restrict__ out) {
+  pdl_wait();
+  const size_t RW = (size_t)4 * H + (sprev ? 2 * H : 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, j = i % H;
+    float dh = 0.f, dc = 0.f;
+    if (d0) { dh = __fadd_rn(dh, d0[(size_t)b * ld0 + j]); dc = __fadd_rn(dc, d0[(size_t)b * ld0 + H + j]); }
+    if (d1) { dh = __fadd_rn(dh, d1[(size_t)b * ld1 + j]); dc = __fadd_rn(dc, d1[(size_t)b * ld1 + H + j]); }
+    if (d2) { dh = __fadd_rn(dh, d2[(size_t)b * ld2 + j]); dc = __fadd_rn(dc, d2[(size_t)b * ld2 + H + j]); }
+    const float* a = act + (size_t)b * 4 * H;
+    const float ig = a[j], fg = a[H + j], gg = a[2 * H + j], og = a[3 * H + j];
+    const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
+    const float c = __fadd_rn(__fmul_rn(fg, cp), __fmul_rn(ig, gg));
+    const float tc = tanhf(c);
+    const float dct = __fadd_rn(dc, __fmul_rn(__fmul_rn(dh, og), __fsub_rn(1.f, __fmul_rn(tc, tc))));
+    float* da = out + (size_t)b * RW;
+    da[j] = __fmul_rn(dct, gg);
+    da[H + j] = __fmul_rn(dct, cp);
+    da[2 * H + j] = __fmul_rn(dct, ig);
+    da[3 * H + j] = __fmul_rn(dh, tc);
+    if (sprev) {
+      da[4 * H + j] = 0.f;
+      da[4 * H + H + j] = __fmul_rn(dct, fg);
+    }
+  }
+}
+
+// d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> bf16 operand [B][4H]
+// (d(acts) rows have stride ldd: the 4H slot of the cell gradient node)
+__global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
+                                                        const float* __restrict__ act, int H, int B,
+                                                        __nv_bfloat16* __restrict__ dpre, float* __restrict__ dpre_f) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * 4 * H; i += gridDim.x * blockDim.x) {
+    const int b = i / (4 * H), j = i % (4 * H);
+    const float a = act[i], da = dact[(size_t)b * ldd + j];
+    const float dv = (j >= 2 * H && j < 3 * H) ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a)))
+                                                : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
+    dpre[i] = __float2bfloat16_rn(dv);
+    dpre_f[i] = dv;
+  }
+}
+
+// Gradient w.r.t. the gates node's inputs from the dX GEMM output gx [B][Kin+H]:
+//   x part:  width xw (the input's true width; for a lower-layer state: (dh | 0), width 2H)
+//   S part:  (dh_prev | 0), width 2H, only when has_prev
+__global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __restrict__ gx, int Kin, int H, int B,
+                                                                int xw_true, int x_is_state, int has_prev,
+                                                                float* __restrict__ out) {
+  pdl_wait();
+  const int K = Kin + H;
+  const int xw = x_is_state ? 2 * H : xw_true;
+  const int W = xw + (has_prev ? 2 * H : 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * W; i += gridDim.x * blockDim.x) {
+    const int b = i / W, k = i % W;
+    float v;
+    if (k < xw) {
+      v = (x_is_state ? (k < H) : true) ? gx[(size_t)b * K + k] : 0.f;
+    } else {
+      const int kk = k - xw;
+      v = kk < H ? gx[(size_t)b * K + Kin + kk] : 0.f;
+    }
+    out[i] = v;
+  }
+}
+
+// h operand of the head: bf16 [B][H] from S^{L-1}_t
+__global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict__ s, int H, int B,
+                                                         __nv_bfloat16* __restrict__ hop) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x)
+    hop[i] = __float2bfloat16_rn(s[(size_t)(i / H) * 2 * H + i % H]);
+}
+
+// One block per row of logits [B][Cp] (C real classes, bias b_o added here): row loss =
+// logsumexp - logit[y]; grad (when dlog != null) = (softmax - onehot) * scale as bf16 + fp32
+// (classes >= C: 0).  The row is biased in place so both passes read the same values.
+__global__ void __launch_bounds__(256) lstm_head_ce_kernel(float* __restrict__ logits, const float* __restrict__ bo,
+                                                           const int* __restrict__ y, int C, int Cp, float scale,
+                                                           float* __restrict__ rowloss, __nv_bfloat16* __restrict__ dlog,
+                                                           float* __restrict__ dlog_f) {
+  __shared__ float sh[32];
+  pdl_wait();
+  float* lr = logits + (size_t)blockIdx.x * Cp;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float v = __fadd_rn(lr[c], bo[c]);
+    lr[c] = v;
+    mx = fmaxf(mx, v);
+  }
+  mx = block_reduce_max(mx, sh);   // (block_reduce_* synchronise the block: the biased row is visible)
+  float s = 0.f;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) s = __fadd_rn(s, expf(__fsub_rn(lr[c], mx)));
+  s = block_reduce_sum(s, sh);
+  const int yy = y[blockIdx.x];
+  if (threadIdx.x == 0 && rowloss) rowloss[blockIdx.x] = __fsub_rn(__fadd_rn(logf(s), mx), lr[yy]);
+  if (!dlog) return;
+  const float inv = __frcp_rn(s);
+  for (int c = threadIdx.x; c < Cp; c += blockDim.x) {
+    float v = 0.f;
+    if (c < C) v = __fmul_rn(__fsub_rn(__fmul_rn(expf(__fsub_rn(lr[c], mx)), inv), c == yy ? 1.f : 0.f), scale);
+    dlog[(size_t)blockIdx.x * Cp + c] = __float2bfloat16_rn(v);
+    dlog_f[(size_t)blockIdx.x * Cp + c] = v;
+  }
+}
+
+// out = sum_b rowloss[b] * scale (single block, fixed order)
+__global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restrict__ rowloss, int B, float scale,
+                                                          float* __restrict__ out) {
+  __shared__ float sh[32];
+  pdl_wait();
+  float s = 0.f;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) s = __fadd_rn(s, rowloss[b]);
+  s = block_reduce_sum(s, sh);
+  if (threadIdx.x == 0) *out = __fmul_rn(s, scale);
+}
+
+// loss = sum over the step losses (pool offsets table, in time order) — the Sum node
+__global__ void __launch_bounds__(32) lstm_sum_kernel(const uint8_t* __restrict__ pool, const long* __restrict__ offs,
+                                                      int T, float* __restrict__ out) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  float s = 0.f;
+  for (int t = 0; t < T; ++t) s = __fadd_rn(s, *reinterpret_cast<const float*>(pool + offs[t]));
+  *out = s;
+}
+
+__global__ void __launch_bounds__(256) fill_kernel(float* __restrict__ p, int n, float v) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
+// acc[j] += sum_b g[b][j]  (column sums accumulated into a gradient, fixed order)
+__global__ void __launch_bounds__(256) colsum_acc_kernel(const float* __restrict__ g, int B, int n,
+                                                         float* __restrict__ acc) {
+  pdl_wait();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float s = 0.f;
+  for (int b = 0; b < B; ++b) s = __fadd_rn(s, g[(size_t)b * n + j]);
+  acc[j] = __fadd_rn(acc[j], s);
+}
+
+}  // namespace slmk

@@ -113,6 +113,8 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 }  // namespace
 
 #include "executor.cuh"
+#include "lstm_kernels.cuh"
+#include "executor_lstm.cuh"
 
 extern "C" {
 
@@ -140,6 +142,29 @@ slm_status slm_model_chain(const slm_chain_desc* desc, slm_model** out) {
   m->bn_fwd = B >= 64 ? 64 : 32;
   m->bn_dx = m->bn_fwd;
   m->bn_dw = desc->width % 256 == 0 ? 256 : 128;
+  *out = m;
+  return SLM_OK;
+}
+
+slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out) {
+  if (!desc || !out) {
+    set_error("null argument");
+    return SLM_E_ARG;
+  }
+  *out = nullptr;
+  const slm_lstm_desc& d = *desc;
+  if (d.n_layers <= 0 || d.steps <= 0 || d.n_in <= 0 || d.n_classes <= 0 ||
+      !(d.batch == 64 || d.batch == 128 || d.batch == 256) || d.hidden <= 0 || d.hidden % 128) {
+    set_error("bad lstm dims (batch in {64,128,256}, hidden % 128 == 0)");
+    return SLM_E_ARG;
+  }
+  if (!d.W || !d.b || !d.W_o || !d.b_o || !d.dW || !d.db || !d.dW_o || !d.db_o) {
+    set_error("null parameter/gradient pointer");
+    return SLM_E_ARG;
+  }
+  auto* m = new slm_model();
+  m->kind = SLM_MODEL_LSTM;
+  m->ld = d;
   *out = m;
   return SLM_OK;
 }
@@ -176,6 +201,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   m->graphs.clear();
   m->maps_ws = nullptr;
+  m->lst.maps.ws = nullptr;
   return SLM_OK;
 }
 
@@ -230,13 +256,17 @@ slm_status slm_workspace_bytes(const slm_plan* p, const slm_model* m, size_t* by
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (!bytes) return SLM_E_ARG;
-  *bytes = ws_layout(*m).total;
+  *bytes = m->kind == SLM_MODEL_LSTM ? lstm_ws_layout(m->ld).total : ws_layout(*m).total;
   return SLM_OK;
 }
 
 slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* launches) {
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
+  if (m->kind == SLM_MODEL_LSTM) {
+    *launches = lstm_launches(p);
+    return SLM_OK;
+  }
   std::vector<Op> ops;
   if ((s = lower(p, &ops)) != SLM_OK) return s;
   // mirrors enqueue(): the fused lowering skips K1 when the operand is already resident
@@ -270,7 +300,8 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("null device buffer");
     return SLM_E_ARG;
   }
-  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < ws_layout(*m).total) {
+  const bool is_lstm = m->kind == SLM_MODEL_LSTM;
+  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < (is_lstm ? lstm_ws_layout(m->ld).total : ws_layout(*m).total)) {
     set_error("pool or workspace smaller than required");
     return SLM_E_BUFFER_TOO_SMALL;
   }
@@ -287,25 +318,33 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("slm kernels are built for sm_100a only");
     return SLM_E_UNSUPPORTED;
   }
-  if (m->d.dtype == SLM_BF16 && m->gemm_impl == 0 && !tc_ok(*m)) {
+  if (is_lstm && comm) {
+    set_error("the LSTM step runs replicas-only (comm must be NULL)");
+    return SLM_E_UNSUPPORTED;
+  }
+  if (!is_lstm && m->d.dtype == SLM_BF16 && m->gemm_impl == 0 && !tc_ok(*m)) {
     set_error("bf16 tcgen05 path needs width % 128 == 0 and batch % 64 == 0 (or gemm_impl=1)");
     return SLM_E_UNSUPPORTED;
   }
-  if (comm && comm->world > 1 && m->d.batch_global <= 0) {
+  if (!is_lstm && comm && comm->world > 1 && m->d.batch_global <= 0) {
     set_error("data parallel step needs batch_global");
     return SLM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (!m->use_graph || st == nullptr || m->profile) return enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
+  auto run = [&]() {
+    return is_lstm ? enqueue_lstm(p, m->ld, m->lst, x0, labels, pool, ws, loss, st, m->pdl != 0, &m->last_launches)
+                   : enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
+  };
+  if (!m->use_graph || st == nullptr || m->profile) return run();
   GraphKey key{p, x0, labels, pool, ws, loss, st, comm};
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {
     // the first call runs eagerly (sets kernel attributes, tensor maps) then captures
-    s = enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
+    s = run();
     if (s != SLM_OK) return s;
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    s = enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
+    s = run();
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (s != SLM_OK) return s;
     if (e != cudaSuccess) {
@@ -336,9 +375,16 @@ slm_status slm_step_host(const slm_plan* p, slm_model* m, const float* x0_host, 
     return SLM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t B = m->d.batch, d = m->d.width;
-  CK(cudaMemcpyAsync(x0_dev, x0_host, B * d * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(labels_dev, labels_host, B * 4, cudaMemcpyHostToDevice, st));
+  size_t xb, lb;
+  if (m->kind == SLM_MODEL_LSTM) {
+    xb = (size_t)m->ld.steps * m->ld.batch * m->ld.n_in * 4;
+    lb = (size_t)m->ld.steps * m->ld.batch * 4;
+  } else {
+    xb = (size_t)m->d.batch * m->d.width * 4;
+    lb = (size_t)m->d.batch * 4;
+  }
+  CK(cudaMemcpyAsync(x0_dev, x0_host, xb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(labels_dev, labels_host, lb, cudaMemcpyHostToDevice, st));
   s = slm_step(p, m, x0_dev, labels_dev, pool, pool_bytes, ws, ws_bytes, loss_dev, stream, comm);
   if (s != SLM_OK) return s;
   CK(cudaMemcpyAsync(loss_host, loss_dev, 4, cudaMemcpyDeviceToHost, st));

@@ -1,0 +1,111 @@
+"""Device parity of the unrolled-LSTM training step (C3) through the C ABI (slm_step).
+
+  * GPU vs the bf16-operand-emulating fp64 oracle (oracle.lstm.step_plain): loss and every
+    gradient within 2e-2 relative norm (reading A12).
+  * checkpointed GPU step == non-checkpointed GPU step, bit for bit, for the generic
+    strategies and the time-segment plan of PAPER.md:486-490.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import graph as OG
+from oracle import lstm as OL
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def slm():
+    import paper_1604_06174_b200 as m
+    return m
+
+
+def _dev(inp, L, H, C):
+    """synth.lstm_inputs (bf16-valued) -> device tensors in the slm_lstm_desc layout."""
+    Cp = -(-C // 128) * 128
+    W = torch.cat([torch.tensor(w).reshape(-1) for w in inp["W"]]).to(torch.bfloat16).cuda()
+    Wo = torch.zeros(Cp, H)
+    Wo[:C] = torch.tensor(inp["W_o"])
+    bo = torch.zeros(Cp)
+    bo[:C] = torch.tensor(inp["b_o"])
+    p = dict(W=W, b=torch.tensor(inp["b"]).cuda(), W_o=Wo.to(torch.bfloat16).cuda(), b_o=bo.cuda())
+    g = dict(W=torch.empty(W.numel(), device="cuda"), b=torch.empty_like(p["b"]),
+             W_o=torch.empty(Cp, H, device="cuda"), b_o=torch.empty(Cp, device="cuda"))
+    return p, g, torch.tensor(inp["x"]).cuda(), torch.tensor(inp["labels"]).cuda()
+
+
+def _run(slm, cfg, inp, strategy="none", m=None, **opt):
+    L, T, B, H, I, C = cfg
+    p, g, x, y = _dev(inp, L, H, C)
+    model = slm.LstmModel(p, g, L, T, B, H, I, C, **opt)
+    plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "explicit" if m is not None else strategy, m=m)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        loss = model.step(plan, x, y, stream=s)
+        loss = model.step(plan, x, y, stream=s)   # graph replay (first call is eager + capture)
+    torch.cuda.synchronize()
+    out = {k: v.cpu().numpy().astype(np.float64) for k, v in g.items()}
+    return float(loss.item()), out, plan
+
+
+def _split_w(flat, inp):
+    out, o = [], 0
+    for w in inp["W"]:
+        out.append(flat[o:o + w.size].reshape(w.shape))
+        o += w.size
+    return out
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+CFGS = [(2, 6, 64, 128, 50, 300), (1, 3, 128, 256, 50, 129), (3, 4, 64, 128, 200, 500)]
+
+
+@pytest.mark.parametrize("cfg", CFGS)
+def test_lstm_vs_oracle(slm, cfg):
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=sum(cfg))
+    loss, g, _ = _run(slm, cfg, inp, "sqrt")
+    P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
+    ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
+    assert abs(loss - ol) / abs(ol) <= 2e-2, (loss, ol)
+    for l, w in enumerate(_split_w(g["W"], inp)):
+        assert _rel(w, og["W"][l]) <= 2e-2, ("W", l, _rel(w, og["W"][l]))
+    b = g["b"]
+    for l in range(L):
+        assert _rel(b[l], og["b"][l]) <= 2e-2, ("b", l)
+    assert _rel(g["W_o"][:C], og["W_o"]) <= 2e-2, _rel(g["W_o"][:C], og["W_o"])
+    assert _rel(g["b_o"][:C], og["b_o"]) <= 2e-2
+    assert not np.any(g["W_o"][C:]) and not np.any(g["b_o"][C:])   # padded classes get no gradient
+
+
+def test_lstm_ckpt_equals_nockpt_bitwise(slm):
+    cfg = (2, 8, 64, 128, 50, 300)
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=7)
+    ref_loss, ref, _ = _run(slm, cfg, inp, "none")
+    og = OG.lstm_graph(L, T, B, H, I)
+    runs = {s: _run(slm, cfg, inp, s) for s in ("sqrt", "search", "drop_cheap")}
+    for seg in (2, 4):
+        runs[f"seg{seg}"] = _run(slm, cfg, inp, m=OL.time_segment_plan(og, seg))
+    for s, (loss, g, plan) in runs.items():
+        assert loss == ref_loss, s
+        for k in ref:
+            assert np.array_equal(g[k], ref[k]), (s, k)
+    # the time-segment plan re-computes and saves memory
+    assert runs["seg4"][2].extra_forward > 0
+
+
+def test_lstm_launch_count(slm):
+    cfg = (2, 4, 64, 128, 50, 300)
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16")
+    p, g, x, y = _dev(inp, L, H, C)
+    model = slm.LstmModel(p, g, L, T, B, H, I, C, use_graph=0)
+    plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "none")
+    # forward: T*(L*(2+1) + 4) + 1; backward: 1 + T*(6 + L*(1+6))
+    assert model.launches(plan) == T * (3 * L + 4) + 1 + 1 + T * (6 + 7 * L)
