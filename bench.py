@@ -134,6 +134,260 @@ def run_reference(args):
                 ms_per_step=t_full * 1e3, sample_s=t_sample)
 
 
+# ======================================================================= LSTM (configs[2])
+def lstm_gemm_flops(plan, L, T, B, H, I, C):
+    """Algorithmic GEMM FLOPs of one step of `plan` on the LSTM graph, by kind: every gates
+    node run (forward or mirror) is one 2*B*4H*K_l GEMM; its gradient node two more (dX, dW);
+    a head run is 2*B*Cp*H, its gradient node re-computes the logits and adds dX and dW."""
+    per_t = 2 * L + 2
+    Cp = -(-C // 128) * 128
+    K0 = -(-I // 128) * 128 + H
+    fl = dict(gemm_fwd=0.0, gemm_dx=0.0, gemm_dw=0.0)
+    nodes = plan.nodes
+    for v in plan.order:
+        nd = nodes[v]
+        op, o = nd["op"], nd["orig"]
+        if op == 10:   # gates
+            l = (o % per_t - 1) // 2
+            f = 2.0 * B * 4 * H * (K0 if l == 0 else 2 * H)
+            if nd["kind"] == 2:
+                fl["gemm_dx"] += f
+                fl["gemm_dw"] += f
+            else:
+                fl["gemm_fwd"] += f
+        elif op == 12:  # head
+            f = 2.0 * B * Cp * H
+            fl["gemm_fwd"] += f
+            if nd["kind"] == 2:
+                fl["gemm_dx"] += f
+                fl["gemm_dw"] += f
+    return fl
+
+
+def lstm_inputs_dev(L, T, B, H, I, C, dev):
+    import torch
+
+    import synth
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16")
+    Cp = -(-C // 128) * 128
+    W = torch.cat([torch.from_numpy(w).reshape(-1) for w in inp["W"]]).to(torch.bfloat16).to(dev)
+    Wo = torch.zeros(Cp, H)
+    Wo[:C] = torch.from_numpy(inp["W_o"])
+    bo = torch.zeros(Cp)
+    p = dict(W=W, b=torch.from_numpy(inp["b"]).to(dev), W_o=Wo.to(torch.bfloat16).to(dev), b_o=bo.to(dev))
+    g = dict(W=torch.empty(W.numel(), device=dev), b=torch.empty_like(p["b"]),
+             W_o=torch.empty(Cp, H, device=dev), b_o=torch.empty(Cp, device=dev))
+    return p, g, torch.from_numpy(inp["x"]).to(dev), torch.from_numpy(inp["labels"]).to(dev)
+
+
+def run_reference_lstm(args):
+    """The CPU oracle (oracle.lstm.step_planned, fp64 NumPy with bf16-operand emulation) on the
+    first --ref-steps time steps of the same LSTM, time-segment plan; scaled linearly to T."""
+    import numpy as np
+
+    import synth
+    from oracle import graph as OG
+    from oracle import lstm as OL
+    from oracle import planner as OP
+    L, T, B, H, I, C = args.lstm_layers, args.unroll, args.batch, args.hidden, args.n_in, args.classes
+    Ts = min(T, args.ref_steps)
+    inp = synth.lstm_inputs(L, Ts, B, H, I, C, dtype="bf16")
+    P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
+    g = OG.lstm_graph(L, Ts, B, H, I)
+    plan = OP.plan(g, OP.S_EXPLICIT, m=OL.time_segment_plan(g, min(args.seg, Ts)))
+    ts = []
+    for _ in range(max(1, args.steps if args.impl == "reference" else 1)):
+        t0 = time.perf_counter()
+        OL.step_planned(plan, P, inp["x"], inp["labels"], "bf16")
+        ts.append(time.perf_counter() - t0)
+    t_full = statistics.median(ts) * T / Ts
+    try:
+        import threadpoolctl
+        cores = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()) or os.cpu_count()
+    except Exception:
+        cores = os.cpu_count()
+    sample = (f"oracle lstm.step_planned (fp64 NumPy, bf16-operand emulation, time-segment plan) on the first "
+              f"{Ts} of {T} steps at full L={L} H={H} B={B} C={C}, median of {len(ts)}; scaled linearly to T={T}")
+    return dict(value=B / t_full, unit=UNIT, cores=cores, kind="oracle", sample=sample, ms_per_step=t_full * 1e3)
+
+
+def lstm_workload(args):
+    return (f"LSTM L={args.lstm_layers} H={args.hidden} T={args.unroll} B={args.batch} n_in={args.n_in} "
+            f"C={args.classes}, checkpoint every {args.seg} steps (BASELINE configs[2])")
+
+
+def run_lstm(args):
+    import torch
+
+    import paper_1604_06174_b200 as slm
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # replicas only (DESIGN.md): every rank runs its own independent problem, no collective
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L, T, B, H, I, C = args.lstm_layers, args.unroll, args.batch, args.hidden, args.n_in, args.classes
+    p, g, x, y = lstm_inputs_dev(L, T, B, H, I, C, dev)
+    opts = {}
+    for kv in args.opt:
+        k, v = kv.split("=")
+        opts[k] = int(v)
+    model = slm.LstmModel(p, g, L, T, B, H, I, C, **opts)
+    graph = slm.Graph.lstm(L, T, B, H, I)
+    stream = torch.cuda.Stream(dev)
+
+    def timed(plan, steps, warmup, with_clocks=False):
+        bufs = model.buffers(plan, dev)
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                model.step(plan, x, y, stream=stream, bufs=bufs)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk = Clocks(local) if with_clocks else None
+        if clk:
+            clk.__enter__()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(steps):
+                loss = model.step(plan, x, y, stream=stream, bufs=bufs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = t.item()
+        return ms, float(loss.item()), clk.summary() if clk else None
+
+    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg))
+    torch.cuda.synchronize()
+    base_mem = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    ms, loss, clocks = timed(plan, args.steps, args.warmup, with_clocks=True)
+    act_measured = torch.cuda.max_memory_allocated(dev) - base_mem
+    value = B * world / (ms / 1e3)
+    launches = model.launches(plan)
+
+    # GEMM roofline on the device clock (every GEMM launch of one step, profile_ts)
+    fl = lstm_gemm_flops(plan, L, T, B, H, I, C)
+    n_gemm = 0
+    nodes = plan.nodes
+    for v in plan.order:
+        op, kind = nodes[v]["op"], nodes[v]["kind"]
+        if op == 10:
+            n_gemm += 2 if kind == 2 else 1
+        elif op == 12:
+            n_gemm += 3 if kind == 2 else 1
+    tsb = torch.zeros(n_gemm * 1024 * 2, dtype=torch.int64, device=dev)
+    model.set_option("profile_ts", n_gemm)
+    model.set_option("profile_ts_buffer", tsb.data_ptr())
+    bufs = model.buffers(plan, dev)
+    with torch.cuda.stream(stream):
+        model.step(plan, x, y, stream=stream, bufs=bufs)
+        model.step(plan, x, y, stream=stream, bufs=bufs)
+    torch.cuda.synchronize()
+    model.kernel_times(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        model.step(plan, x, y, stream=stream, bufs=bufs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prof_ms = e0.elapsed_time(e1)
+    kt = model.kernel_times(reset=True)
+    model.set_option("profile_ts", 0)
+    del tsb
+    pk = _peaks()
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    kinds = ("gemm_fwd", "gemm_dx", "gemm_dw")
+    gemm_ms = sum(kt[k][0] for k in kinds)
+    achieved = sum(fl.values()) / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
+    per_kind = {k: {"launches_per_step": kt[k][1], "avg_us": round(1e3 * kt[k][0] / max(1, kt[k][1]), 3),
+                    "tflops": round(fl[k] / (kt[k][0] / 1e3) / 1e12, 1) if kt[k][0] else None} for k in kinds}
+    roofline = dict(bound="tensor", achieved=round(achieved, 2) if achieved else None, peak=peak, unit="TFLOP/s",
+                    frac=round(achieved / peak, 4) if achieved else None, traffic=None,
+                    kernel="tc_gemm_kernel (gates / head / dX / dW GEMMs, N = batch = 64)",
+                    flop_per_step={k: fl[k] for k in kinds},
+                    timing="device clock per launch (%globaltimer) inside the graph; achieved = "
+                           "algorithmic GEMM FLOPs of the step / summed launch spans",
+                    per_kind=per_kind, gemm_share_of_step=round(gemm_ms / prof_ms, 4) if prof_ms else None,
+                    step_ms_instrumented=round(prof_ms, 3))
+
+    nock = None
+    if not args.no_nockpt:
+        plan0 = slm.Plan(graph, "none")
+        model._bufs.pop(id(plan), None)
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        base0 = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        ms0, loss0, _ = timed(plan0, max(3, args.steps // 2), 3)
+        act0 = torch.cuda.max_memory_allocated(dev) - base0
+        nock = dict(value=B * world / (ms0 / 1e3), ms_per_step=ms0, loss=loss0,
+                    plan_exact_peak_gb=plan0.exact_peak / 1e9, pool_gb=plan0.pool_bytes / 1e9,
+                    measured_activation_gb=act0 / 1e9, bitwise_equal_loss=(loss0 == loss))
+        model._bufs.pop(id(plan0), None)
+        del plan0
+        torch.cuda.empty_cache()
+
+    # end to end through slm_step_host
+    x_h = x.cpu().pin_memory()
+    y_h = y.cpu().pin_memory()
+    loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+    x_d, y_d = torch.empty_like(x), torch.empty_like(y)
+    eb = model.buffers(plan, dev)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            model.step_host(plan, x_h, y_h, x_d, y_d, loss_h, stream=stream, bufs=eb)
+    torch.cuda.synchronize()
+    k2 = max(3, args.steps // 2)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(k2):
+            model.step_host(plan, x_h, y_h, x_d, y_d, loss_h, stream=stream, bufs=eb)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / k2
+    e2e = dict(value=B * world / (e2e_ms / 1e3), unit=UNIT, ms_per_step=round(e2e_ms, 3),
+               h2d_bytes_per_step=x.numel() * 4 + y.numel() * 4, d2h_bytes_per_step=4)
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_baseline and world == 1:
+        r = run_reference_lstm(args)
+        cpu = dict(value=r["value"], unit=UNIT, cores=r["cores"], kind="oracle", sample=r["sample"])
+    line = dict(
+        metric=METRIC, value=round(value, 3), unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+        data="synthetic (seeded NumPy, synth.lstm_inputs: PyTorch-default uniform LSTM init, x~N(0,1))",
+        config=dict(workload=lstm_workload(args), n_layers=L, hidden=H, unroll=T, batch=B, n_in=I, classes=C,
+                    segment=args.seg, parallelism=f"replicas{world}" if world > 1 else "single",
+                    l2="inputs > L2: 33 MB of bf16 weights + 24 GB of no-ckpt activations; the ckpt step re-reads "
+                       "W every time step (L2-resident by design)"),
+        roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches * args.steps), clocks=clocks,
+        loss=loss,
+        activation_gb=dict(plan_exact_peak=plan.exact_peak / 1e9, pool=plan.pool_bytes / 1e9,
+                           workspace=model.workspace_bytes(plan) / 1e9, measured=act_measured / 1e9,
+                           extra_forward=plan.extra_forward),
+        nockpt=nock, ckpt_over_nockpt_time=round(ms / nock["ms_per_step"], 4) if nock else None)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 # ======================================================================= our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -150,8 +404,33 @@ def main():
     ap.add_argument("--no-nockpt", action="store_true", help="skip the non-checkpointed comparison")
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
+    ap.add_argument("--model", default="chain", choices=["chain", "lstm"],
+                    help="chain = configs[1] (default, the metric's config); lstm = configs[2]")
+    ap.add_argument("--lstm-layers", type=int, default=4)
+    ap.add_argument("--unroll", type=int, default=4096)
+    ap.add_argument("--hidden", type=int, default=1024)
+    ap.add_argument("--n-in", type=int, default=50)
+    ap.add_argument("--classes", type=int, default=5000)
+    ap.add_argument("--seg", type=int, default=64, help="LSTM checkpoint interval (time steps)")
+    ap.add_argument("--ref-steps", type=int, default=4, help="LSTM time steps the CPU oracle runs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.model == "lstm":
+        if args.batch == 256:
+            args.batch = 64
+        if args.impl == "reference":
+            if int(os.environ.get("RANK", "0")) != 0:
+                return
+            r = run_reference_lstm(args)
+            print(json.dumps(dict(
+                metric=METRIC, value=r["value"], unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+                config=dict(workload=lstm_workload(args)),
+                cpu_baseline=dict(value=r["value"], unit=UNIT, cores=r["cores"], kind="oracle", sample=r["sample"]),
+                e2e=dict(value=r["value"], unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))), flush=True)
+            return
+        return run_lstm(args)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -115,6 +115,12 @@ slm_status slm_graph_chain(int32_t n_layers, int32_t batch, int32_t width, slm_g
  * G^l_t (batch*4H*4) and S^l_t (batch*2H*4), a head H_t (4 bytes); final Sum (the loss). */
 slm_status slm_graph_lstm(int32_t n_layers, int32_t steps, int32_t batch, int32_t hidden,
                           int32_t n_in, slm_graph** out);
+/* Time-segment mirror counts for a graph built by slm_graph_lstm (the LSTM
+ * is checkpointed along time): m[v] = 1 for every gates/cell node except the cell states
+ * S^l_t at segment ends (t % seg == seg - 1), which are kept; 0 elsewhere.  Feed the result
+ * to slm_plan_create with strategy SLM_STRATEGY_EXPLICIT.  m has room for n_nodes entries;
+ * SLM_E_ARG when seg < 1 or the graph is not an LSTM graph. */
+slm_status slm_lstm_segment_mirrors(const slm_graph* g, int32_t seg, int32_t* m, int32_t n_nodes);
 slm_status slm_graph_size(const slm_graph* g, int32_t* n_nodes);
 /* topological-order(V) of Alg. 2: Kahn, lowest id first among ready nodes. */
 slm_status slm_graph_topo(const slm_graph* g, int32_t* order, int32_t cap, int32_t* n);

@@ -16,7 +16,7 @@ import ctypes as C
 from . import _lib
 from ._lib import check, lib
 
-__all__ = ["Graph", "Plan", "ChainModel", "Comm", "recursion_estimate", "STRATEGY", "OP", "lib"]
+__all__ = ["Graph", "Plan", "ChainModel", "LstmModel", "Comm", "recursion_estimate", "STRATEGY", "OP", "lib"]
 
 STRATEGY = {"none": 0, "sqrt": 1, "budget": 2, "search": 3, "recursive": 4, "explicit": 5,
             "drop_cheap": 6}
@@ -47,6 +47,13 @@ class Graph:
         h = C.c_void_p()
         check(lib.slm_graph_lstm(n_layers, steps, batch, hidden, n_in, C.byref(h)), "slm_graph_lstm")
         return cls(h)
+
+    def lstm_segment_mirrors(self, seg):
+        """Time-segment mirror counts (slm_lstm_segment_mirrors) for Plan(..., 'explicit', m=...)."""
+        n = len(self)
+        arr = (C.c_int32 * max(1, n))()
+        check(lib.slm_lstm_segment_mirrors(self._h, seg, arr, n), "slm_lstm_segment_mirrors")
+        return list(arr)[:n]
 
     @staticmethod
     def _descs(nodes):

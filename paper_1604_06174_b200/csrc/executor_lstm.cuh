@@ -87,10 +87,19 @@ struct LstmNode {
   int t, l;     // time, layer (-1 for X_t, L for H_t / Sum)
 };
 
-slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_state& S, const void* xin,
-                        const int32_t* labels, void* pool, void* ws, float* loss, cudaStream_t st, bool pdl,
-                        int64_t* launches) {
+slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const int32_t* labels, void* pool,
+                        void* ws, float* loss, cudaStream_t st, int64_t* launches) {
   using namespace slmk;
+  const slm_lstm_desc& d = m.ld;
+  slm_lstm_state& S = m.lst;
+  const bool pdl = m.pdl != 0;
+  int ts_slot = 0;
+  if (m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) m.ts_kind.resize(m.profile_ts);
+  auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock GEMM timing
+    if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
+    m.ts_kind[ts_slot] = kind;
+    return (++ts_slot) << 8;
+  };
   using bf = __nv_bfloat16;
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
   const int Cp = lstm_cpad(C), K0 = lstm_kin0(I);
@@ -172,7 +181,7 @@ slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_stat
                     H, B, op));
         slmk::EpiLstmGates e{V(v), d.b + (size_t)l * 4 * H, H};
         if ((s = launch_tc_bn<slmk::EpiLstmGates, false, false, true>(B, 1, S.maps.wK[l], opK[l], 4 * H, B, Kin + H,
-                                                                      0, 0, e, st, pdl)) != SLM_OK)
+                                                                      0, 0, e, st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
           return s;
         nl += 2;
       } else if (opk == SLM_OP_LSTM_CELL) {
@@ -183,7 +192,7 @@ slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_stat
         CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]), H, B, hop));
         slmk::EpiStoreF32 e{logits, Cp};
         if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(B, 1, S.maps.woK, S.maps.hopK, Cp, B, H, 0, 0, e,
-                                                                     st, pdl)) != SLM_OK)
+                                                                     st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, logits, d.b_o, labels + (size_t)t * B,
                     C, Cp, scale, rowloss, (bf*)nullptr, (float*)nullptr));
@@ -206,21 +215,21 @@ slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_stat
         CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, sL, H, B, hop));
         slmk::EpiStoreF32 e{logits, Cp};
         if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(B, 1, S.maps.woK, S.maps.hopK, Cp, B, H, 0, 0, e,
-                                                                     st, pdl)) != SLM_OK)
+                                                                     st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, logits, d.b_o, labels + (size_t)t * B,
                     C, Cp, scale, (float*)nullptr, dlog_bf, dlog_f));
         // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  -> gx (fp32 [B][H]) then (dh | 0) into the node
         slmk::EpiStoreF32 e2{V(v), 2 * H};
         if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(B, 1, S.maps.woMN, S.maps.dlK, H, B, Cp, 0, 0, e2,
-                                                                    st, pdl)) != SLM_OK)
+                                                                    st, pdl, gdbg(SLM_K_GEMM_DX))) != SLM_OK)
           return s;
         // zero the dc half of (dh | dc)
         CK(cudaMemset2DAsync(V(v) + H, (size_t)2 * H * 4, 0, (size_t)H * 4, B, st));
         // dW_o[c][h] += sum_b dlog[b][c] h[b][h]   (D[m=h][n=c], K = B)
         slmk::EpiAccF32 e3{d.dW_o, H};
         if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(128, 1, S.maps.hopMN, S.maps.dlMN, H, Cp, B, 0, 0,
-                                                                  e3, st, pdl)) != SLM_OK)
+                                                                  e3, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
           return s;
         CK(launch_k(colsum_acc_kernel, dim3((Cp + 255) / 256), eb, 0, st, pdl, (const float*)dlog_f, B, Cp, d.db_o));
         nl += 6;
@@ -270,14 +279,14 @@ slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_stat
         // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H
         slmk::EpiStoreF32 e{gx, Kin + H};
         if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(B, 1, S.maps.wMN[l], S.maps.dpK, Kin + H, B, 4 * H,
-                                                                    0, 0, e, st, pdl)) != SLM_OK)
+                                                                    0, 0, e, st, pdl, gdbg(SLM_K_GEMM_DX))) != SLM_OK)
           return s;
         CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)gx, Kin, H, B, I, l > 0 ? 1 : 0,
                     has_prev ? 1 : 0, V(v)));
         // dW_l[n = gate][m = k_in] += sum_b op[b][k_in] d_pre[b][gate]
         slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), Kin + H};
         if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(128, 1, opMN[l], S.maps.dpMN, Kin + H, 4 * H, B, 0,
-                                                                  0, e2, st, pdl)) != SLM_OK)
+                                                                  0, e2, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
           return s;
         CK(launch_k(colsum_acc_kernel, dim3((4 * H + 255) / 256), eb, 0, st, pdl, (const float*)dpre_f, B, 4 * H,
                     d.db + (size_t)l * 4 * H));
@@ -289,6 +298,7 @@ slm_status enqueue_lstm(const slm_plan* p, const slm_lstm_desc& d, slm_lstm_stat
     }
   }
   CK(cudaGetLastError());
+  m.ts_used = ts_slot;
   if (launches) *launches = nl;
   return SLM_OK;
 }

@@ -729,6 +729,23 @@ slm_status slm_graph_lstm(int32_t L, int32_t T, int32_t B, int32_t H, int32_t I,
   return SLM_OK;
 }
 
+slm_status slm_lstm_segment_mirrors(const slm_graph* g, int32_t seg, int32_t* m, int32_t n_nodes) {
+  if (!g || !m || seg < 1 || g->kind != SLM_MODEL_LSTM || n_nodes < (int32_t)g->nodes.size()) {
+    set_error("slm_lstm_segment_mirrors: bad arguments");
+    return SLM_E_ARG;
+  }
+  int t = -1;
+  for (size_t v = 0; v < g->nodes.size(); ++v) {
+    const int op = g->nodes[v].op;
+    if (op == SLM_OP_INPUT) ++t;
+    int mv = 0;
+    if (op == SLM_OP_LSTM_GATES) mv = 1;
+    else if (op == SLM_OP_LSTM_CELL) mv = (t % seg == seg - 1) ? 0 : 1;
+    m[v] = mv;
+  }
+  return SLM_OK;
+}
+
 slm_status slm_graph_size(const slm_graph* g, int32_t* n) {
   if (!g || !n) {
     set_error("null argument");

@@ -332,7 +332,7 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
   }
   cudaStream_t st = (cudaStream_t)stream;
   auto run = [&]() {
-    return is_lstm ? enqueue_lstm(p, m->ld, m->lst, x0, labels, pool, ws, loss, st, m->pdl != 0, &m->last_launches)
+    return is_lstm ? enqueue_lstm(p, *m, x0, labels, pool, ws, loss, st, &m->last_launches)
                    : enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
   };
   if (!m->use_graph || st == nullptr || m->profile) return run();

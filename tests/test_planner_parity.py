@@ -95,6 +95,15 @@ def test_lstm_graph_plan():
     assert_same_plan(g, P.S_NONE)
 
 
+@pytest.mark.parametrize("L,T,seg", [(2, 24, 5), (4, 64, 8), (1, 7, 1), (3, 10, 64)])
+def test_lstm_segment_mirrors(L, T, seg):
+    from oracle.lstm import time_segment_plan
+    dg = slm.Graph.lstm(L, T, 64, 128, 50)
+    assert dg.lstm_segment_mirrors(seg) == time_segment_plan(G.lstm_graph(L, T, 64, 128, 50), seg)
+    with pytest.raises(slm.SlmError if hasattr(slm, "SlmError") else Exception):
+        slm.Graph.chain(4, 8, 64).lstm_segment_mirrors(seg)
+
+
 def _random_dag(rnd, n):
     nodes = [G.Node(G.INPUT, [], rnd.randint(1, 5) * 64)]
     for i in range(1, n):
