@@ -196,6 +196,15 @@ class Comm:
     """slm_comm: NCCL communicator built from a unique id broadcast over torch.distributed."""
 
     def __init__(self, rank, world, pg=None, bucket_bytes=256 << 20):
+        uid = self.broadcast_unique_id(rank, world, pg)
+        h = C.c_void_p()
+        check(lib.slm_comm_init(rank, world, uid, bucket_bytes, C.byref(h)), "slm_comm_init")
+        self._h, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def broadcast_unique_id(rank, world, pg=None):
+        """Rank 0 draws the 128-byte NCCL unique id (slm_comm_unique_id); it is broadcast over
+        the torch.distributed group (any backend, e.g. gloo) to every rank."""
         import torch
         import torch.distributed as dist
         uid = (C.c_uint8 * 128)()
@@ -208,9 +217,7 @@ class Comm:
             t = obj[0]
         for i in range(128):
             uid[i] = int(t[i])
-        h = C.c_void_p()
-        check(lib.slm_comm_init(rank, world, uid, bucket_bytes, C.byref(h)), "slm_comm_init")
-        self._h, self.rank, self.world = h, rank, world
+        return uid
 
     def __del__(self):
         if getattr(self, "_h", None):
