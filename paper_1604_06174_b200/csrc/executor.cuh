@@ -176,8 +176,10 @@ struct GraphKey {
 // LSTM executor state (executor_lstm.cuh): tensor maps bound to the weights / workspace and
 // the Sum node's pool-offset table
 struct LstmMaps {
-  std::vector<CUtensorMap> wK, wMN;   // per layer W_l K-major / MN-major
-  CUtensorMap woK, woMN, dpK, dpMN, hopK, hopMN, dlK, dlMN;
+  // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
+  // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
+  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX;
+  CUtensorMap woK, woMN, hopK, hopRK, hopRMN, dlRK, dlRMN, pG, pL, pH;
   const void* ws = nullptr;
 };
 struct slm_lstm_state {

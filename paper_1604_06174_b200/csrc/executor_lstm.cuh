@@ -2,85 +2,132 @@
 //
 // Node semantics (graph: oracle.graph.lstm_graph / slm_graph_lstm, time-major ids):
 //   X_t      Input [B][n_in]                 bound to x + t*B*n_in (caller buffer)
-//   G^l_t    gates  [B][4H] = act([x | h_{t-1}] W_l^T + b_l)        pack + tcgen05 GEMM
-//   S^l_t    cell   [B][2H] = (h, c)                                SIMT
-//   H_t      head   scalar  = sum_b CE(h W_o^T + b_o, y_t) / (T B)  tcgen05 GEMM + SIMT
+//   G^l_t    gates  [B][4H] = act([x | h_{t-1}] W_l^T + b_l)
+//   S^l_t    cell   [B][2H] = (h, c)
+//   H_t      head   scalar  = sum_b CE(h W_o^T + b_o, y_t) / (T B)
 //   Sum      loss   scalar  (caller buffer)
-// and one gradient node per non-Input node holding d(inputs) concatenated in pred order;
-// weight gradients accumulate in place across time steps with fp32
-// read-modify-write GEMM epilogues.  Re-computed (mirror) nodes run the same kernels with the
-// same configuration, so the checkpointed step is bit-identical to the plain one.
+// and one gradient node per non-Input node holding d(inputs) concatenated in pred order (A17).
+//
+// Lowering:
+//   gates (fwd/mirror)  pack [x | h] bf16 -> tcgen05 GEMM, split-K fp32 partials (N = B = 64
+//                       would leave 32 of 148 SMs busy) -> lstm_gates_cell_kernel (partials +
+//                       bias + activations -> G; fused with the cell S when S^l_t is the next
+//                       node of V', which it is in forward and recompute order)
+//   head  (fwd)         pack h -> logits GEMM (split-K) -> softmax-CE rows -> row sum
+//   grad head           pack h -> logits GEMM -> CE + dlogits -> dh GEMM (split-K) -> (dh | 0)
+//   grad cell           sum of successor slices -> d(acts) | (0 | dc_prev)
+//   grad gates          d_pre (+ db) -> dX GEMM (split-K) -> scatter into d(inputs)
+//   weight gradients    the GEMM operands of each step are kept in a per-layer ring of CH time
+//                       steps; once per chunk (in time order, independent of the plan)
+//                       dW_l += opᵀ d_pre runs as ONE GEMM with K = B * CH (PAPER.md:488-489
+//                       "in-place accumulation"), instead of CH GEMMs with K = B.
+// Re-computed (mirror) nodes run the same kernels with the same configuration and every
+// reduction has a fixed order, so the checkpointed step is bit-identical to the plain one.
 
 namespace {
 
+constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
+
 struct LstmWs {
-  size_t op, dpre_bf, dpre_f, gx, logits, dlog_bf, dlog_f, hop, rowloss, offs, total;
+  size_t op, hop, P, logits, dlog_f, rowloss, offs, hopR, dlR, total;
+  std::vector<size_t> opR, dpR;   // per layer rings
 };
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
 inline int lstm_cpad(int C) { return (C + 127) / 128 * 128; }
+inline int lstm_K(const slm_lstm_desc& d, int l) { return (l == 0 ? lstm_kin0(d.n_in) : d.hidden) + d.hidden; }
+
+// split-K factor: the largest s dividing K/64 with mtiles * s <= 148 (one wave)
+inline int lstm_sk(int mtiles, int K) {
+  const int kb = K / 64;
+  int best = 1;
+  for (int s = 1; s <= kb; ++s)
+    if (kb % s == 0 && mtiles * s <= 148) best = s;
+  return best;
+}
+struct LstmSplits {
+  int g0, g1, x0, x1, lg, hd;   // gates (layer 0 / l > 0), dX (layer 0 / l > 0), logits, head dX
+};
+LstmSplits lstm_splits(const slm_lstm_desc& d) {
+  const int H = d.hidden, Cp = lstm_cpad(d.n_classes);
+  const int K0 = lstm_K(d, 0), K1 = 2 * H;
+  return {lstm_sk(4 * H / 128, K0), lstm_sk(4 * H / 128, K1), lstm_sk(K0 / 128, 4 * H), lstm_sk(K1 / 128, 4 * H),
+          lstm_sk(Cp / 128, H), lstm_sk(H / 128, Cp)};
+}
 
 LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t B = d.batch, H = d.hidden, T = d.steps;
-  const size_t Kmax = std::max<size_t>(lstm_kin0(d.n_in), H) + H, Cp = lstm_cpad(d.n_classes);
+  const size_t B = d.batch, H = d.hidden, T = d.steps, CH = kLstmChunk;
+  const size_t K0 = lstm_K(d, 0), Kmax = std::max<size_t>(K0, 2 * H), Cp = lstm_cpad(d.n_classes);
+  const LstmSplits sp = lstm_splits(d);
+  const size_t pbytes = std::max({(size_t)std::max(sp.g0, sp.g1) * B * 4 * H, (size_t)sp.x0 * B * K0,
+                                  (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
   size_t off = 0;
   L.op = off;       off += al(B * Kmax * 2);
-  L.dpre_bf = off;  off += al(B * 4 * H * 2);
-  L.dpre_f = off;   off += al(B * 4 * H * 4);
-  L.gx = off;       off += al(B * Kmax * 4);
-  L.logits = off;   off += al(B * Cp * 4);
-  L.dlog_bf = off;  off += al(B * Cp * 2);
-  L.dlog_f = off;   off += al(B * Cp * 4);
   L.hop = off;      off += al(B * H * 2);
+  L.P = off;        off += al(pbytes);
+  L.logits = off;   off += al(B * Cp * 4);
+  L.dlog_f = off;   off += al(B * Cp * 4);
   L.rowloss = off;  off += al(B * 4);
   L.offs = off;     off += al(T * 8);
+  L.hopR = off;     off += al(CH * B * H * 2);
+  L.dlR = off;      off += al(CH * B * Cp * 2);
+  for (int l = 0; l < d.n_layers; ++l) {
+    L.opR.push_back(off);
+    off += al(CH * B * lstm_K(d, l) * 2);
+    L.dpR.push_back(off);
+    off += al(CH * B * 4 * H * 2);
+  }
   L.total = off;
   return L;
 }
 
-
 size_t lstm_w_offset(const slm_lstm_desc& d, int l) {   // elements
-  const size_t H = d.hidden, k0 = lstm_kin0(d.n_in) + H;
+  const size_t H = d.hidden, k0 = lstm_K(d, 0);
   return l == 0 ? 0 : 4 * H * k0 + (size_t)(l - 1) * 4 * H * 2 * H;
 }
 
 slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
   if (M.ws == ws) return SLM_OK;
-  const uint64_t B = d.batch, H = d.hidden, Cp = lstm_cpad(d.n_classes);
+  const uint64_t B = d.batch, H = d.hidden, Cp = lstm_cpad(d.n_classes), CH = kLstmChunk;
   const LstmWs L = lstm_ws_layout(d);
+  const LstmSplits sp = lstm_splits(d);
   uint8_t* w = (uint8_t*)ws;
   const __nv_bfloat16* W = (const __nv_bfloat16*)d.W;
-  M.wK.resize(d.n_layers);
-  M.wMN.resize(d.n_layers);
+  const int nl = d.n_layers;
+  M.wK.resize(nl);
+  M.wMN.resize(nl);
+  M.opK.resize(nl);
+  M.opRMN.resize(nl);
+  M.dpRK.resize(nl);
+  M.dpRMN.resize(nl);
+  M.pX.resize(nl);
+  M.opRK.resize(nl);
   slm_status st;
-  for (int l = 0; l < d.n_layers; ++l) {
-    const uint64_t K = (l == 0 ? lstm_kin0(d.n_in) : H) + H;
+  for (int l = 0; l < nl; ++l) {
+    const uint64_t K = lstm_K(d, l);
     if ((st = make_map(&M.wK[l], W + lstm_w_offset(d, l), K, 4 * H, 128)) != SLM_OK) return st;
     if ((st = make_map(&M.wMN[l], W + lstm_w_offset(d, l), K, 4 * H, 64)) != SLM_OK) return st;
+    if ((st = make_map(&M.opK[l], w + L.op, K, B, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map(&M.opRK[l], w + L.opR[l], K, CH * B, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
+    if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
+    if ((st = make_map_f32(&M.pX[l], w + L.P, K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
   }
   if ((st = make_map(&M.woK, d.W_o, H, Cp, 128)) != SLM_OK) return st;
   if ((st = make_map(&M.woMN, d.W_o, H, Cp, 64)) != SLM_OK) return st;
-  const uint64_t K0 = lstm_kin0(d.n_in) + H;
-  // operand [B][K]: the GEMM's B operand (K-major, box rows = B) and the dW's A (MN-major)
-  if ((st = make_map(&M.dpK, w + L.dpre_bf, 4 * H, B, (uint32_t)B)) != SLM_OK) return st;
-  if ((st = make_map(&M.dpMN, w + L.dpre_bf, 4 * H, B, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.hopK, w + L.hop, H, B, (uint32_t)B)) != SLM_OK) return st;
-  if ((st = make_map(&M.hopMN, w + L.hop, H, B, 64)) != SLM_OK) return st;
-  if ((st = make_map(&M.dlK, w + L.dlog_bf, Cp, B, (uint32_t)B)) != SLM_OK) return st;
-  if ((st = make_map(&M.dlMN, w + L.dlog_bf, Cp, B, 64)) != SLM_OK) return st;
+  if ((st = make_map(&M.hopRK, w + L.hopR, H, CH * B, (uint32_t)B)) != SLM_OK) return st;
+  if ((st = make_map(&M.hopRMN, w + L.hopR, H, CH * B, 64)) != SLM_OK) return st;
+  if ((st = make_map(&M.dlRK, w + L.dlR, Cp, CH * B, (uint32_t)B)) != SLM_OK) return st;
+  if ((st = make_map(&M.dlRMN, w + L.dlR, Cp, CH * B, 64)) != SLM_OK) return st;
+  if ((st = make_map_f32(&M.pG, w + L.P, 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK) return st;
+  if ((st = make_map_f32(&M.pL, w + L.P, Cp, (uint64_t)sp.lg * B)) != SLM_OK) return st;
+  if ((st = make_map_f32(&M.pH, w + L.P, H, (uint64_t)sp.hd * B)) != SLM_OK) return st;
   M.ws = ws;
   return SLM_OK;
-}
-
-// the operand buffer is [B][K_l] with a per-layer K: encode its maps per call (host only)
-slm_status lstm_op_maps(const slm_lstm_desc& d, void* ws, int l, CUtensorMap* k, CUtensorMap* mn) {
-  const uint64_t B = d.batch, H = d.hidden, K = (l == 0 ? lstm_kin0(d.n_in) : H) + H;
-  uint8_t* w = (uint8_t*)ws + lstm_ws_layout(d).op;
-  slm_status st;
-  if ((st = make_map(k, w, K, B, (uint32_t)B)) != SLM_OK) return st;
-  return make_map(mn, w, K, B, 64);
 }
 
 struct LstmNode {
@@ -90,6 +137,7 @@ struct LstmNode {
 slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const int32_t* labels, void* pool,
                         void* ws, float* loss, cudaStream_t st, int64_t* launches) {
   using namespace slmk;
+  using bf = __nv_bfloat16;
   const slm_lstm_desc& d = m.ld;
   slm_lstm_state& S = m.lst;
   const bool pdl = m.pdl != 0;
@@ -100,27 +148,24 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     m.ts_kind[ts_slot] = kind;
     return (++ts_slot) << 8;
   };
-  using bf = __nv_bfloat16;
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
-  const int Cp = lstm_cpad(C), K0 = lstm_kin0(I);
+  const int Cp = lstm_cpad(C), K0 = lstm_kin0(I), CH = kLstmChunk;
   const LstmWs W = lstm_ws_layout(d);
+  const LstmSplits sp = lstm_splits(d);
   uint8_t* w = (uint8_t*)ws;
   bf* op = (bf*)(w + W.op);
-  bf* dpre_bf = (bf*)(w + W.dpre_bf);
-  float* dpre_f = (float*)(w + W.dpre_f);
-  float* gx = (float*)(w + W.gx);
-  float* logits = (float*)(w + W.logits);
-  bf* dlog_bf = (bf*)(w + W.dlog_bf);
-  float* dlog_f = (float*)(w + W.dlog_f);
   bf* hop = (bf*)(w + W.hop);
+  float* P = (float*)(w + W.P);
+  float* logits = (float*)(w + W.logits);
+  float* dlog_f = (float*)(w + W.dlog_f);
   float* rowloss = (float*)(w + W.rowloss);
   long* offs = (long*)(w + W.offs);
+  bf* hopR = (bf*)(w + W.hopR);
+  bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
   slm_status s;
   if ((s = lstm_bind_maps(d, S.maps, ws)) != SLM_OK) return s;
-  std::vector<CUtensorMap> opK(L), opMN(L);
-  for (int l = 0; l < L; ++l)
-    if ((s = lstm_op_maps(d, ws, l, &opK[l], &opMN[l])) != SLM_OK) return s;
+  const LstmMaps& M = S.maps;
 
   const int N = p->n_fwd;
   const int per_t = 2 * L + 2;
@@ -144,28 +189,28 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto V = [&](int node) -> float* { return node < 0 ? nullptr : (float*)tp[p->node_tag[node]]; };
   const int* pred = p->preds.data();
   auto preds_of = [&](int v) { return std::make_pair(pred + p->pred_ptr[v], p->pred_ptr[v + 1] - p->pred_ptr[v]); };
-  // the Sum node's inputs: pool offsets of the H_t values, uploaded once per workspace
-  {
+  // the Sum node's inputs: pool offsets of the H_t values, uploaded once per (workspace, plan)
+  if (S.offs_ws != ws || S.offs_plan != (const void*)p) {
     std::vector<long> h_offs(T, 0);
     for (int t = 0; t < T; ++t) h_offs[t] = p->tag_offset[p->node_tag[t * per_t + per_t - 1]];
-    if (S.offs_ws != ws || S.offs_plan != (const void*)p) {
-      CK(cudaMemcpy(offs, h_offs.data(), T * 8, cudaMemcpyHostToDevice));
-      S.offs_ws = ws;
-      S.offs_plan = p;
-    }
+    CK(cudaMemcpy(offs, h_offs.data(), T * 8, cudaMemcpyHostToDevice));
+    S.offs_ws = ws;
+    S.offs_plan = p;
   }
   const dim3 eg(592), eb(256);
   int64_t nl = 0;
   // gradients are overwritten by every step: zero the in-place accumulators first
-  {
-    size_t wsz = lstm_w_offset(d, L);
-    CK(cudaMemsetAsync(d.dW, 0, wsz * 4, st));
-    CK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
-    CK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
-    CK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
-  }
+  CK(cudaMemsetAsync(d.dW, 0, lstm_w_offset(d, L) * 4, st));
+  CK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
+  CK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
+  CK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
+  // weight-gradient chunk of time t: slot in the ring and whether t closes the chunk (the
+  // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
+  auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
 
-  for (int v : p->order) {
+  const std::vector<int>& order = p->order;
+  for (size_t oi = 0; oi < order.size(); ++oi) {
+    const int v = order[oi];
     const int kind = p->kind[v], opk = p->op[v], orig = p->orig[v];
     auto pp = preds_of(v);
     const LstmNode ni = info(orig);
@@ -176,26 +221,40 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const bool lower_state = l > 0;
         const float* x = V(pp.first[0]);
         const float* sprev = pp.second > 1 ? V(pp.first[1]) : nullptr;
-        const int Kin = l == 0 ? K0 : H;
+        const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
         CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
                     H, B, op));
-        slmk::EpiLstmGates e{V(v), d.b + (size_t)l * 4 * H, H};
-        if ((s = launch_tc_bn<slmk::EpiLstmGates, false, false, true>(B, 1, S.maps.wK[l], opK[l], 4 * H, B, Kin + H,
-                                                                      0, 0, e, st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+        slmk::EpiPartialTma e{B};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[l], 4 * H, B, Kin + H, 0, 0,
+                                                                       e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pG)) != SLM_OK)
           return s;
-        nl += 2;
+        // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
+        float* s_out = nullptr;
+        const float* s_prev = nullptr;
+        if (oi + 1 < order.size()) {
+          const int u = order[oi + 1];
+          auto pu = preds_of(u);
+          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu.first[0] == v) {
+            s_out = V(u);
+            s_prev = pu.second > 1 ? V(pu.first[1]) : nullptr;
+            ++oi;
+          }
+        }
+        CK(launch_k(lstm_gates_cell_kernel, eg, eb, 0, st, pdl, (const float*)P, sk, d.b + (size_t)l * 4 * H, H, B, V(v),
+                    s_prev, s_out));
+        nl += 3;
       } else if (opk == SLM_OP_LSTM_CELL) {
         CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]),
                     (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
         CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]), H, B, hop));
-        slmk::EpiStoreF32 e{logits, Cp};
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(B, 1, S.maps.woK, S.maps.hopK, Cp, B, H, 0, 0, e,
-                                                                     st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+        slmk::EpiPartialTma e{B};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, st,
+                                                                       pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, logits, d.b_o, labels + (size_t)t * B,
-                    C, Cp, scale, rowloss, (bf*)nullptr, (float*)nullptr));
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+                    labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr));
         CK(launch_k(lstm_rowsum_kernel, dim3(1), eb, 0, st, pdl, (const float*)rowloss, B, scale, V(v)));
         nl += 4;
       } else if (opk == SLM_OP_SUM) {
@@ -206,33 +265,36 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         return SLM_E_UNSUPPORTED;
       }
     } else {
+      const int slot = t % CH;
+      const bool flush = slot == 0;
       if (opk == SLM_OP_SUM) {
         CK(launch_k(fill_kernel, dim3(1), eb, 0, st, pdl, V(v), T, 1.0f));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits, dlogits, dh = dlog W_o, dW_o += ...
+        // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits (the head reads only its input, A6)
         const float* sL = V(pp.first[pp.second - 1]);
-        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, sL, H, B, hop));
-        slmk::EpiStoreF32 e{logits, Cp};
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(B, 1, S.maps.woK, S.maps.hopK, Cp, B, H, 0, 0, e,
-                                                                     st, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, sL, H, B, hopR + (size_t)slot * B * H));
+        slmk::EpiPartialTma e{B};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
+                                                                       e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, logits, d.b_o, labels + (size_t)t * B,
-                    C, Cp, scale, (float*)nullptr, dlog_bf, dlog_f));
-        // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  -> gx (fp32 [B][H]) then (dh | 0) into the node
-        slmk::EpiStoreF32 e2{V(v), 2 * H};
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(B, 1, S.maps.woMN, S.maps.dlK, H, B, Cp, 0, 0, e2,
-                                                                    st, pdl, gdbg(SLM_K_GEMM_DX))) != SLM_OK)
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+                    labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f));
+        // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  (split-K partials) -> (dh | 0)
+        slmk::EpiPartialTma e2{B};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
+                                                                      e2, st, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
           return s;
-        // zero the dc half of (dh | dc)
-        CK(cudaMemset2DAsync(V(v) + H, (size_t)2 * H * 4, 0, (size_t)H * 4, B, st));
-        // dW_o[c][h] += sum_b dlog[b][c] h[b][h]   (D[m=h][n=c], K = B)
-        slmk::EpiAccF32 e3{d.dW_o, H};
-        if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(128, 1, S.maps.hopMN, S.maps.dlMN, H, Cp, B, 0, 0,
-                                                                  e3, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-          return s;
+        CK(launch_k(lstm_head_dh_kernel, eg, eb, 0, st, pdl, (const float*)P, sp.hd, H, B, V(v)));
         CK(launch_k(colsum_acc_kernel, dim3((Cp + 255) / 256), eb, 0, st, pdl, (const float*)dlog_f, B, Cp, d.db_o));
         nl += 6;
+        if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
+          slmk::EpiAccF32 e3{d.dW_o, H};
+          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp, chunk_rows(t), 0,
+                                                                    0, e3, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+            return s;
+          ++nl;
+        }
       } else if (opk == SLM_OP_LSTM_CELL) {
         // successor slices (order: layer above / head, next-step gates, next-step cell)
         const float* sl[3] = {nullptr, nullptr, nullptr};
@@ -247,16 +309,11 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         };
         const int sv = orig;
         const int above = l + 1 < L ? sv + 1 : t * per_t + per_t - 1;   // G^{l+1}_t or H_t
-        {
-          const int wa = (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H;   // row width of g[above]
-          slice(above, 0, wa);
-        }
+        slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
         if (t + 1 < T) {
-          const int gn = sv + per_t - 1;      // G^l_{t+1}
           const int xw = l == 0 ? I : 2 * H;
-          slice(gn, xw, xw + 2 * H);
-          const int sn = sv + per_t;          // S^l_{t+1}
-          slice(sn, 4 * H, 4 * H + 2 * H);
+          slice(sv + per_t - 1, xw, xw + 2 * H);   // G^l_{t+1}
+          slice(sv + per_t, 4 * H, 4 * H + 2 * H);  // S^l_{t+1}
         }
         const float* act = V(pp.first[pp.second - (t > 0 ? 2 : 1)]);
         const float* sprev = t > 0 ? V(pp.first[pp.second - 1]) : nullptr;
@@ -271,26 +328,30 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const float* act = V(pp.first[pp.second - nf - 1]);
         const float* x = V(pp.first[pp.second - nf]);
         const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
-        const int Kin = l == 0 ? K0 : H;
-        // d(acts) rows of g[S] are [4H | 2H] wide when the cell has a predecessor
+        const int Kin = l == 0 ? K0 : H, K = Kin + H, skx = l == 0 ? sp.x0 : sp.x1;
+        bf* opS = (bf*)(w + W.opR[l]) + (size_t)slot * B * K;
+        bf* dpS = (bf*)(w + W.dpR[l]) + (size_t)slot * B * 4 * H;
         const int drow = 4 * H + (has_prev ? 2 * H : 0);
-        CK(launch_k(lstm_dpre_kernel, eg, eb, 0, st, pdl, dact, drow, act, H, B, dpre_bf, dpre_f));
-        CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, sprev, H, B, op));
-        // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H
-        slmk::EpiStoreF32 e{gx, Kin + H};
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, true, false, true>(B, 1, S.maps.wMN[l], S.maps.dpK, Kin + H, B, 4 * H,
-                                                                    0, 0, e, st, pdl, gdbg(SLM_K_GEMM_DX))) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)gx, Kin, H, B, I, l > 0 ? 1 : 0,
-                    has_prev ? 1 : 0, V(v)));
-        // dW_l[n = gate][m = k_in] += sum_b op[b][k_in] d_pre[b][gate]
-        slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), Kin + H};
-        if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(128, 1, opMN[l], S.maps.dpMN, Kin + H, 4 * H, B, 0,
-                                                                  0, e2, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-          return s;
-        CK(launch_k(colsum_acc_kernel, dim3((4 * H + 255) / 256), eb, 0, st, pdl, (const float*)dpre_f, B, 4 * H,
+        CK(launch_k(lstm_dpre_kernel, dim3(4 * H / 32), eb, 0, st, pdl, dact, drow, act, H, B, dpS,
                     d.db + (size_t)l * 4 * H));
-        nl += 6;
+        CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, sprev, H, B, opS));
+        // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
+        slmk::EpiPartialTma e{B};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
+                                                                      slot * B, e, st, pdl, gdbg(SLM_K_GEMM_DX),
+                                                                      &M.pX[l])) != SLM_OK)
+          return s;
+        CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)P, skx, Kin, H, B, I, l > 0 ? 1 : 0,
+                    has_prev ? 1 : 0, V(v)));
+        nl += 4;
+        if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
+          slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
+          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l], M.dpRMN[l], K, 4 * H,
+                                                                    chunk_rows(t), 0, 0, e2, st, pdl,
+                                                                    gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+            return s;
+          ++nl;
+        }
       } else {
         set_error("unsupported gradient op in lstm plan");
         return SLM_E_UNSUPPORTED;
@@ -304,15 +365,31 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
 }
 
 // kernels enqueue_lstm launches for this plan (the memsets are not counted)
-int64_t lstm_launches(const slm_plan* p) {
+int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
   int64_t nl = 0;
-  for (int v : p->order) {
-    const int opk = p->op[v];
+  const int per_t = 2 * d.n_layers + 2, N = p->n_fwd;
+  const std::vector<int>& order = p->order;
+  for (size_t oi = 0; oi < order.size(); ++oi) {
+    const int v = order[oi], opk = p->op[v], kind = p->kind[v];
     if (opk == SLM_OP_INPUT) continue;
-    if (p->kind[v] != SLM_KIND_GRAD)
-      nl += opk == SLM_OP_LSTM_GATES ? 2 : opk == SLM_OP_HEAD_CE ? 4 : 1;
-    else
-      nl += opk == SLM_OP_HEAD_CE ? 6 : opk == SLM_OP_LSTM_GATES ? 6 : 1;
+    const int o = p->orig[v];
+    const int t = o == N - 1 ? d.steps - 1 : o / per_t;
+    if (kind != SLM_KIND_GRAD) {
+      if (opk == SLM_OP_LSTM_GATES) {
+        nl += 3;
+        if (oi + 1 < order.size()) {
+          const int u = order[oi + 1];
+          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) ++oi;
+        }
+      } else {
+        nl += opk == SLM_OP_HEAD_CE ? 4 : 1;
+      }
+    } else {
+      const bool flush = t % kLstmChunk == 0;
+      if (opk == SLM_OP_HEAD_CE) nl += 6 + flush;
+      else if (opk == SLM_OP_LSTM_GATES) nl += 4 + flush;
+      else nl += 1;
+    }
   }
   return nl;
 }

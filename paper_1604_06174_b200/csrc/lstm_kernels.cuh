@@ -82,40 +82,107 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restr
   }
 }
 
-// d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> bf16 operand [B][4H]
-// (d(acts) rows have stride ldd: the 4H slot of the cell gradient node)
+// d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> bf16 GEMM operand [B][4H]
+// (a slot of the per-layer time-chunk ring), and db += sum_b d_pre (fixed order: 8 row groups
+// summed in smem in group order).  d(acts) rows have stride ldd.  Block = 32 columns x 8 row
+// groups; grid = 4H / 32.
 __global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
                                                         const float* __restrict__ act, int H, int B,
-                                                        __nv_bfloat16* __restrict__ dpre, float* __restrict__ dpre_f) {
+                                                        __nv_bfloat16* __restrict__ dpre, float* __restrict__ db) {
+  __shared__ float red[8][33];
   pdl_wait();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * 4 * H; i += gridDim.x * blockDim.x) {
-    const int b = i / (4 * H), j = i % (4 * H);
-    const float a = act[i], da = dact[(size_t)b * ldd + j];
-    const float dv = (j >= 2 * H && j < 3 * H) ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a)))
-                                                : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
-    dpre[i] = __float2bfloat16_rn(dv);
-    dpre_f[i] = dv;
+  const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + c;
+  const int G4 = 4 * H;
+  const bool tanh_gate = j >= 2 * H && j < 3 * H;
+  float sum = 0.f;
+  for (int b = rg; b < B; b += 8) {
+    const float a = act[(size_t)b * G4 + j], da = dact[(size_t)b * ldd + j];
+    const float dv = tanh_gate ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a)))
+                               : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
+    dpre[(size_t)b * G4 + j] = __float2bfloat16_rn(dv);
+    sum = __fadd_rn(sum, dv);
+  }
+  red[rg][c] = sum;
+  __syncthreads();
+  if (rg == 0) {
+    float t = red[0][c];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t = __fadd_rn(t, red[r][c]);
+    db[j] = __fadd_rn(db[j], t);
   }
 }
 
-// Gradient w.r.t. the gates node's inputs from the dX GEMM output gx [B][Kin+H]:
+// G = act(sum_s P[s] + b) from the split-K partials P [sk][B][4H] (fixed slice order), and —
+// when s_out is given — the fused cell S = (h, c) = (o tanh(c), f c_prev + i g) (same
+// arithmetic as lstm_cell_fwd_kernel, so fused and separate runs are bit-identical).
+__global__ void __launch_bounds__(256) lstm_gates_cell_kernel(const float* __restrict__ P, int sk,
+                                                              const float* __restrict__ bias, int H, int B,
+                                                              float* __restrict__ g_out,
+                                                              const float* __restrict__ sprev,
+                                                              float* __restrict__ s_out) {
+  pdl_wait();
+  const size_t slice = (size_t)B * 4 * H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, j = i % H;
+    float a[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const size_t e = (size_t)b * 4 * H + q * H + j;
+      float acc = P[e];
+      for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, P[s * slice + e]);
+      const float pre = __fadd_rn(acc, bias[q * H + j]);
+      a[q] = q == 2 ? tanhf(pre) : __frcp_rn(__fadd_rn(1.f, expf(-pre)));
+      g_out[e] = a[q];
+    }
+    if (s_out) {
+      const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
+      const float c = __fadd_rn(__fmul_rn(a[1], cp), __fmul_rn(a[0], a[2]));
+      s_out[(size_t)b * 2 * H + j] = __fmul_rn(a[3], tanhf(c));
+      s_out[(size_t)b * 2 * H + H + j] = c;
+    }
+  }
+}
+
+// (dh | 0) of the head gradient node from the split-K partials of dlogits W_o, P [sk][B][H]
+__global__ void __launch_bounds__(256) lstm_head_dh_kernel(const float* __restrict__ P, int sk, int H, int B,
+                                                           float* __restrict__ out) {
+  pdl_wait();
+  const size_t slice = (size_t)B * H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, j = i % H;
+    float acc = P[i];
+    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, P[s * slice + i]);
+    out[(size_t)b * 2 * H + j] = acc;
+    out[(size_t)b * 2 * H + H + j] = 0.f;
+  }
+}
+
+// Gradient w.r.t. the gates node's inputs from the dX GEMM's split-K partials
+// gx [sk][B][Kin+H] (summed in slice order):
 //   x part:  width xw (the input's true width; for a lower-layer state: (dh | 0), width 2H)
 //   S part:  (dh_prev | 0), width 2H, only when has_prev
-__global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __restrict__ gx, int Kin, int H, int B,
-                                                                int xw_true, int x_is_state, int has_prev,
+__global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __restrict__ gx, int sk, int Kin, int H,
+                                                                int B, int xw_true, int x_is_state, int has_prev,
                                                                 float* __restrict__ out) {
   pdl_wait();
   const int K = Kin + H;
+  const size_t slice = (size_t)B * K;
+  auto part = [&](size_t e) {
+    float acc = gx[e];
+    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, gx[s * slice + e]);
+    return acc;
+  };
   const int xw = x_is_state ? 2 * H : xw_true;
   const int W = xw + (has_prev ? 2 * H : 0);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * W; i += gridDim.x * blockDim.x) {
     const int b = i / W, k = i % W;
     float v;
     if (k < xw) {
-      v = (x_is_state ? (k < H) : true) ? gx[(size_t)b * K + k] : 0.f;
+      v = (x_is_state ? (k < H) : true) ? part((size_t)b * K + k) : 0.f;
     } else {
       const int kk = k - xw;
-      v = kk < H ? gx[(size_t)b * K + Kin + kk] : 0.f;
+      v = kk < H ? part((size_t)b * K + Kin + kk) : 0.f;
     }
     out[i] = v;
   }
@@ -129,23 +196,29 @@ __global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict
     hop[i] = __float2bfloat16_rn(s[(size_t)(i / H) * 2 * H + i % H]);
 }
 
-// One block per row of logits [B][Cp] (C real classes, bias b_o added here): row loss =
-// logsumexp - logit[y]; grad (when dlog != null) = (softmax - onehot) * scale as bf16 + fp32
-// (classes >= C: 0).  The row is biased in place so both passes read the same values.
-__global__ void __launch_bounds__(256) lstm_head_ce_kernel(float* __restrict__ logits, const float* __restrict__ bo,
-                                                           const int* __restrict__ y, int C, int Cp, float scale,
+// One block per row b: logits = sum_s P[s][b][:] + b_o (split-K partials [sk][B][Cp], slice
+// order), written to the row buffer `logits`; row loss = logsumexp - logit[y] over the C real
+// classes; grad (when dlog != null) = (softmax - onehot) * scale as bf16 (the GEMM operand,
+// a ring slot) + fp32 (for db_o), classes >= C: 0.
+__global__ void __launch_bounds__(256) lstm_head_ce_kernel(const float* __restrict__ P, int sk,
+                                                           float* __restrict__ logits, const float* __restrict__ bo,
+                                                           const int* __restrict__ y, int C, int Cp, int B, float scale,
                                                            float* __restrict__ rowloss, __nv_bfloat16* __restrict__ dlog,
                                                            float* __restrict__ dlog_f) {
   __shared__ float sh[32];
   pdl_wait();
+  const size_t slice = (size_t)B * Cp;
   float* lr = logits + (size_t)blockIdx.x * Cp;
+  const float* pr = P + (size_t)blockIdx.x * Cp;
   float mx = -INFINITY;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    const float v = __fadd_rn(lr[c], bo[c]);
+    float acc = pr[c];
+    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, pr[s * slice + c]);
+    const float v = __fadd_rn(acc, bo[c]);
     lr[c] = v;
     mx = fmaxf(mx, v);
   }
-  mx = block_reduce_max(mx, sh);   // (block_reduce_* synchronise the block: the biased row is visible)
+  mx = block_reduce_max(mx, sh);   // (block_reduce_* synchronise the block: the row is visible)
   float s = 0.f;
   for (int c = threadIdx.x; c < C; c += blockDim.x) s = __fadd_rn(s, expf(__fsub_rn(lr[c], mx)));
   s = block_reduce_sum(s, sh);

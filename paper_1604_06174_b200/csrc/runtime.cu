@@ -264,7 +264,7 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (m->kind == SLM_MODEL_LSTM) {
-    *launches = lstm_launches(p);
+    *launches = lstm_launches(p, m->ld);
     return SLM_OK;
   }
   std::vector<Op> ops;

@@ -10,7 +10,6 @@ import pytest
 import torch
 
 import synth
-from oracle import graph as OG
 from oracle import lstm as OL
 
 pytestmark = pytest.mark.gpu
@@ -62,7 +61,8 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-CFGS = [(2, 6, 64, 128, 50, 300), (1, 3, 128, 256, 50, 129), (3, 4, 64, 128, 200, 500)]
+# (L, T, B, H, I, C); T = 37 spans two weight-gradient chunks (32 + a ragged 5)
+CFGS = [(2, 6, 64, 128, 50, 300), (1, 3, 128, 256, 50, 129), (3, 4, 64, 128, 200, 500), (1, 37, 64, 128, 50, 129)]
 
 
 @pytest.mark.parametrize("cfg", CFGS)
@@ -83,15 +83,14 @@ def test_lstm_vs_oracle(slm, cfg):
     assert not np.any(g["W_o"][C:]) and not np.any(g["b_o"][C:])   # padded classes get no gradient
 
 
-def test_lstm_ckpt_equals_nockpt_bitwise(slm):
-    cfg = (2, 8, 64, 128, 50, 300)
+@pytest.mark.parametrize("cfg", [(2, 8, 64, 128, 50, 300), (1, 40, 64, 128, 50, 129)])
+def test_lstm_ckpt_equals_nockpt_bitwise(slm, cfg):
     L, T, B, H, I, C = cfg
     inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=7)
     ref_loss, ref, _ = _run(slm, cfg, inp, "none")
-    og = OG.lstm_graph(L, T, B, H, I)
     runs = {s: _run(slm, cfg, inp, s) for s in ("sqrt", "search", "drop_cheap")}
     for seg in (2, 4):
-        runs[f"seg{seg}"] = _run(slm, cfg, inp, m=OL.time_segment_plan(og, seg))
+        runs[f"seg{seg}"] = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(seg))
     for s, (loss, g, plan) in runs.items():
         assert loss == ref_loss, s
         for k in ref:
@@ -107,5 +106,7 @@ def test_lstm_launch_count(slm):
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, use_graph=0)
     plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "none")
-    # forward: T*(L*(2+1) + 4) + 1; backward: 1 + T*(6 + L*(1+6))
-    assert model.launches(plan) == T * (3 * L + 4) + 1 + 1 + T * (6 + 7 * L)
+    # forward: per t, per layer pack + GEMM + fused gates/cell, head 4; Sum 1.
+    # backward: fill 1; per t head 6, per layer cell 1 + gates 4; one weight-gradient GEMM per
+    # layer and one for the head per 32-step chunk (T = 4: one chunk)
+    assert model.launches(plan) == T * (3 * L + 4) + 1 + 1 + T * (6 + 5 * L) + (L + 1)
