@@ -10,7 +10,8 @@
  *                       A bf16 [K][M], B bf16 [K][N], out bf16 [N][M]
  * impl 0 = tcgen05/TMA (bn = N tile: 32|64|128|256; M % 128 == 0, N % bn == 0, K % 64 == 0),
  * impl 1 = SIMT, impl 2 = tcgen05 data movement only (no MMA), impl 3 = tcgen05 MMA only (no
- * TMA) — the last two are bandwidth / issue-rate probes with meaningless results.
+ * TMA) — the last two are bandwidth / issue-rate probes with meaningless results —, impl 4 =
+ * tcgen05 CTA pair (cta_group::2, clusters of 2 along M: M % 256 == 0, bn in {128, 256}).
  * split = split-K factor of the tcgen05 kernel (K % (64 split) == 0); with split > 1, kinds 0
  * and 1 write the fp32 partial tiles out[s][n][m] (split x N x M; the caller sums over s, kind 0
  * then ignores resid/bias).  All pointers are device pointers; asynchronous on `stream`.

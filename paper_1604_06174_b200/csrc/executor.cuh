@@ -26,47 +26,73 @@ namespace {
 // `pdl` is set: it may start while its predecessor drains and synchronises on it with
 // griddepcontrol.wait before touching dependent data.
 template <class... KArgs, class... Args>
-cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
-                     Args... args) {
+cudaError_t launch_kc(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                      int cluster_x, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster_x > 1) {   // thread-block cluster (CTA pairs of the cta_group::2 GEMM)
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster_x;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                     Args... args) {
+  return launch_kc(k, grid, block, smem, st, pdl, 1, args...);
 }
 
 enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
 
-template <int BN, bool AMN, bool BMN, bool PRE, class Epi>
+template <int BN, bool AMN, bool BMN, bool PRE, class Epi, int CG = 1>
 slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int M, int N, int K, int split,
                      int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg) {
-  using C = slmk::TcCfg<BN, AMN, BMN>;
-  auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi>;
+  using C = slmk::TcCfg<BN, AMN, BMN, CG>;
+  auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi, CG>;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  if (split < 1 || K % (64 * split) || M % 128 || N % BN) {
-    set_error("GEMM shape not tileable: M % 128, N % BN, K % (64 * split)");
+  if (split < 1 || K % (64 * split) || M % (128 * CG) || N % BN) {
+    set_error("GEMM shape not tileable: M % (128 * cta_group), N % BN, K % (64 * split)");
     return SLM_E_UNSUPPORTED;
   }
-  CK(launch_k(kern, dim3(M / 128, N / BN, split), dim3(128), C::SMEM, st, pdl, a, b, c, K, a_row0, b_row0, epi, dbg));
+  CK(launch_kc(kern, dim3(M / 128, N / BN, split), dim3(128), C::SMEM, st, pdl, CG, a, b, c, K, a_row0, b_row0, epi,
+               dbg));
   return SLM_OK;
 }
 
-// c: tensor map of the output for TMA-store epilogues (Epi::kTma), else ignored
+// c: tensor map of the output for TMA-store epilogues (Epi::kTma), else ignored.
+// cg = 2: CTA-pair GEMM (cta_group::2); a K-major B map must then have box rows bn / 2.
 template <class Epi, bool AMN, bool BMN, bool PRE>
 slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                         int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg = 0,
-                        const CUtensorMap* c = nullptr) {
+                        const CUtensorMap* c = nullptr, int cg = 1) {
   const CUtensorMap& cm = c ? *c : a;
+  if (cg == 2) {
+    switch (bn) {
+      case 128: return launch_tc<128, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+      case 256: return launch_tc<256, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+    }
+    set_error("unsupported CTA-pair GEMM N tile " + std::to_string(bn));
+    return SLM_E_UNSUPPORTED;
+  }
   switch (bn) {
     case 32:
       if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
@@ -635,7 +661,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         nl += 4;
       }
       // data-parallel: all-reduce the bucket [l, bucket_hi] once its last layer is done
-      if (comm && comm->world > 1 && (bucket_hi - l + 1 >= bucket_layers || l == 0)) {
+      if (comm && (bucket_hi - l + 1 >= bucket_layers || l == 0)) {   // (world 1: identity, same path)
         const int lo = l, cnt = bucket_hi - l + 1;
         cudaEvent_t ev = comm->events[cev_i++ % comm->events.size()];
         CK(cudaEventRecord(ev, side ? m.s2 : st));
@@ -663,7 +689,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   }
   // join the dW stream
   if (side && kb > 0 && dw_event[kb - 1] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - 1]], 0));
-  if (comm && comm->world > 1) {
+  if (comm) {
     // db (all layers; db_0 is final after the last backward) and the loss, then join
     cudaEvent_t ev = comm->events[cev_i++ % comm->events.size()];
     CK(cudaEventRecord(ev, st));

@@ -464,32 +464,36 @@ slm_status slm_debug_gemm(int kind, int impl, int bn, int split, int M, int N, i
   using bf = __nv_bfloat16;
   if (impl == 0 || impl >= 2) {
     const int dbg = impl == 2 ? 1 : (impl == 3 ? 2 : 0);   // 2: data movement only, 3: MMA only
+    const int cg = impl == 4 ? 2 : 1;                       // 4: CTA-pair (cta_group::2) tcgen05
+    const uint32_t bbox = (uint32_t)(bn / cg);              // K-major B box rows
     CUtensorMap ma, mb;
     slm_status s;
     if (kind == G_FWD && split == 1) {  // A = W [M][K], B = act [N][K]; out[n][m] = resid + acc + bias[m]
-      if ((s = make_map(&ma, A, K, M, 128)) || (s = make_map(&mb, Bm, K, N, bn))) return s;
+      if ((s = make_map(&ma, A, K, M, 128)) || (s = make_map(&mb, Bm, K, N, bbox))) return s;
       slmk::EpiResid e{(float*)out, resid, bias, M};
-      return launch_tc_bn<slmk::EpiResid, false, false, true>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg);
+      return launch_tc_bn<slmk::EpiResid, false, false, true>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg,
+                                                              nullptr, cg);
     } else if (kind == G_FWD) {  // split-K partials: out[s][n][m] (fp32, split x N x M)
       CUtensorMap mc;
-      if ((s = make_map(&ma, A, K, M, 128)) || (s = make_map(&mb, Bm, K, N, bn)) ||
+      if ((s = make_map(&ma, A, K, M, 128)) || (s = make_map(&mb, Bm, K, N, bbox)) ||
           (s = make_map_f32(&mc, out, M, (uint64_t)split * N)))
         return s;
       slmk::EpiPartialTma e{N};
       return launch_tc_bn<slmk::EpiPartialTma, false, false, true>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg,
-                                                                   &mc);
+                                                                   &mc, cg);
     } else if (kind == G_DX) {  // A = W [K][M] (MN), B = g [N][K]; out[s][n][m] fp32 (split partials)
       CUtensorMap mc;
-      if ((s = make_map(&ma, A, M, K, 64)) || (s = make_map(&mb, Bm, K, N, bn)) ||
+      if ((s = make_map(&ma, A, M, K, 64)) || (s = make_map(&mb, Bm, K, N, bbox)) ||
           (s = make_map_f32(&mc, out, M, (uint64_t)split * N)))
         return s;
       slmk::EpiPartialTma e{N};
       return launch_tc_bn<slmk::EpiPartialTma, true, false, true>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg,
-                                                                  &mc);
+                                                                  &mc, cg);
     } else {  // DW: A = act [K][M] (MN), B = g [K][N] (MN); out[n][m] bf16
       if ((s = make_map(&ma, A, M, K, 64)) || (s = make_map(&mb, Bm, N, K, 64))) return s;
       slmk::EpiStoreBF16 e{(bf*)out, M};
-      return launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg);
+      return launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(bn, split, ma, mb, M, N, K, 0, 0, e, st, false, dbg,
+                                                                 nullptr, cg);
     }
   }
   dim3 grid((M + 63) / 64, (N + 63) / 64);  // SIMT computes C(n, m) with n as the row

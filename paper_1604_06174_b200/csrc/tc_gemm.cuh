@@ -84,6 +84,43 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- CTA pair (cta_group::2): two SMs of a TPC execute one M=256 MMA; each CTA stages its
+// own 128 rows of A and half of the N columns of B, the leader (rank 0) issues the MMAs.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load into this CTA's smem whose completion is counted on the LEADER CTA's mbarrier (the
+// same smem offset with the peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the mbarrier at this smem offset in every CTA of `mask` once the leader's MMAs retire
+__device__ __forceinline__ void tc_commit2(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // 32 lanes x 32 consecutive 32-bit columns: thread i of the warp gets lane (base+i).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
@@ -211,11 +248,12 @@ struct EpiPartialTma {
 };
 
 // ---------------------------------------------------------------- the kernel
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG = 1>
 struct TcCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;   // 16 KiB
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int A_BYTES = BM * BK * 2;   // 16 KiB (this CTA's 128 rows of A)
+  static constexpr int BNC = BN / CG;           // columns of B staged by this CTA
+  static constexpr int B_BYTES = BNC * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // as many stages as fit in ~200 KiB (up to 8): the K loop is latency bound, bytes in
   // flight per SM set its bandwidth
@@ -255,12 +293,19 @@ __device__ __forceinline__ void ts_mark(int phase, int dbg) {
 // similar rate) bounds these skinny GEMMs, so K is split until each SM ingests ~192 KiB;
 // the partials are summed by the BN kernel that consumes the GEMM output anyway
 // (distributed-shared-memory reduction was measured ~16 KB/us per SM: too slow).
-template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi>
+// CG = 2: CTA pair (launched as clusters of 2 along x): CTAs 2c and 2c+1 compute the 256 x BN
+// tile of rows [256c, 256c+256) with one cta_group::2 MMA per K step; each stages its own
+// 128 rows of A and BN/2 columns of B (so per-SM operand ingest drops from (128+BN)*64*2 to
+// (128+BN/2)*64*2 bytes per K step), the leader issues the MMAs and multicasts the commits.
+template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi, int CG = 1>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg) {
   ts_mark(0, dbg);
-  using C = TcCfg<BN, A_MN, B_MN>;
+  using C = TcCfg<BN, A_MN, B_MN, CG>;
+  uint32_t rank = 0;
+  if constexpr (CG == 2) rank = cluster_ctarank();
+  const bool leader = rank == 0;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
@@ -286,39 +331,58 @@ __global__ void __launch_bounds__(128, 1)
       fence_barrier_init();
     }
     __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();   // the peer's barriers are initialised before use
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   ts_mark(1, dbg);
 
+  auto tma = [&](void* dst, const CUtensorMap* map, int s, int c0, int c1) {
+    if constexpr (CG == 2)
+      tma_load_2d_cg2(dst, map, &full[s], c0, c1);
+    else
+      tma_load_2d(dst, map, &full[s], c0, c1);
+  };
   auto load_a = [&](int kb, int s) {
     uint8_t* sa = smem + s * C::STAGE;
     const int k0 = kbase + kb * C::BK;
     if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
-      tma_load_2d(sa, &tmA, &full[s], m0, a_row0 + k0);
-      tma_load_2d(sa + 8192, &tmA, &full[s], m0 + 64, a_row0 + k0);
+      tma(sa, &tmA, s, m0, a_row0 + k0);
+      tma(sa + 8192, &tmA, s, m0 + 64, a_row0 + k0);
     } else {     // A stored [M][K]: one box of 64(K) x 128(M)
-      tma_load_2d(sa, &tmA, &full[s], k0, a_row0 + m0);
+      tma(sa, &tmA, s, k0, a_row0 + m0);
     }
   };
+  const int nb0 = n0 + (int)rank * C::BNC;   // first B column staged by this CTA
   auto load_b = [&](int kb, int s) {
     uint8_t* sb = smem + s * C::STAGE + C::A_BYTES;
     const int k0 = kbase + kb * C::BK;
     if (B_MN) {
 #pragma unroll
-      for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[s], n0 + 64 * j, b_row0 + k0);
-    } else {
-      tma_load_2d(sb, &tmB, &full[s], k0, b_row0 + n0);
+      for (int j = 0; j < C::BNC / 64; ++j) tma(sb + j * 8192, &tmB, s, nb0 + 64 * j, b_row0 + k0);
+    } else {     // box rows = BN / CG
+      tma(sb, &tmB, s, k0, b_row0 + nb0);
     }
   };
+  // the leader's full barrier counts both CTAs' bytes; only it arrives (expect_tx)
+  auto expect = [&](int s) {
+    if (leader) mbar_expect_tx(&full[s], CG * C::STAGE);
+  };
 
-  if (warp == 0 && lane == 0 && (dbg & 2)) {
+  if (CG == 1 && warp == 0 && lane == 0 && (dbg & 2)) {
     // debug probe: MMA issue rate only (no TMA, operands are whatever is in smem)
     pdl_wait();
     for (int kb = 0; kb < nk; ++kb) {
@@ -332,7 +396,7 @@ __global__ void __launch_bounds__(128, 1)
     if (PREFETCH_A) {
       kb0 = nk < C::STAGES ? nk : C::STAGES;
       for (int kb = 0; kb < kb0; ++kb) {
-        mbar_expect_tx(&full[kb], C::STAGE);
+        expect(kb);
         load_a(kb, kb);
       }
       pdl_wait();
@@ -343,20 +407,20 @@ __global__ void __launch_bounds__(128, 1)
     for (int kb = kb0; kb < nk; ++kb) {
       const int s = kb % C::STAGES;
       if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-      mbar_expect_tx(&full[s], C::STAGE);
+      expect(s);
       load_a(kb, s);
       load_b(kb, s);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ===== MMA issuer
-    constexpr uint32_t idesc = make_idesc(C::BM, BN, A_MN, B_MN);
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ===== MMA issuer (the leader of a CTA pair issues for both)
+    constexpr uint32_t idesc = make_idesc(C::BM * CG, BN, A_MN, B_MN);
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % C::STAGES;
       mbar_wait(&full[s], (kb / C::STAGES) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * C::STAGE);
       const uint32_t sb = sa + C::A_BYTES;
-      if (dbg & 1) {  // debug probe: data movement only, no MMA (bits 0-1 only; bits 8+ = ts slot)
+      if (CG == 1 && (dbg & 1)) {  // debug probe: data movement only, no MMA (bits 0-1 only; bits 8+ = ts slot)
         mbar_arrive(&empty[s]);
         continue;
       }
@@ -366,11 +430,19 @@ __global__ void __launch_bounds__(128, 1)
         // MN-major SW128: +16 rows * 128 B per K=16; LBO = 64-element MN chunk (8 KiB box).
         uint64_t ad = A_MN ? make_sdesc(sa + kk * 2048, 8192, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
         uint64_t bd = B_MN ? make_sdesc(sb + kk * 2048, 8192, 1024) : make_sdesc(sb + kk * 32, 16, 1024);
-        tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
+        if constexpr (CG == 2)
+          tc_mma2(tmem, ad, bd, idesc, (kb | kk) != 0);
+        else
+          tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
       }
-      tc_commit(&empty[s]);
+      if constexpr (CG == 2)
+        tc_commit2(&empty[s], 3);
+      else
+        tc_commit(&empty[s]);
     }
-    if (dbg & 1)
+    if constexpr (CG == 2)
+      tc_commit2(accum, 3);
+    else if (dbg & 1)
       mbar_arrive(accum);
     else
       tc_commit(accum);
@@ -425,8 +497,14 @@ __global__ void __launch_bounds__(128, 1)
   ts_mark(7, dbg);
   tc_fence_before();
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  if constexpr (CG == 2) {
+    cluster_sync();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  } else {
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
 }
 
 }  // namespace slmk

@@ -17,13 +17,13 @@ def bench(kind, impl, bn, split=1, M=2048, N=256, K=2048, nw=48, reps=96, check=
     if kind == 0:      # A = W [M][K], B = act [N][K]
         As = [torch.randn(M, K, device=dev).bfloat16() for _ in range(nw)]
         B = torch.randn(N, K, device=dev).bfloat16()
-        out = torch.empty(N, M, device=dev)
+        out = torch.empty(split, N, M, device=dev)
         resid = torch.randn(N, M, device=dev)
         bias = torch.randn(M, device=dev)
     elif kind == 1:    # A = W [K][M], B = g [N][K]
         As = [torch.randn(K, M, device=dev).bfloat16() for _ in range(nw)]
         B = torch.randn(N, K, device=dev).bfloat16()
-        out = torch.empty(N, M, device=dev)
+        out = torch.empty(split, N, M, device=dev)
         resid = bias = None
     else:              # dW: A = act [K][M], B = g [K][N], out [N][M]
         M, N, K = 2048, 2048, 256
@@ -37,16 +37,17 @@ def bench(kind, impl, bn, split=1, M=2048, N=256, K=2048, nw=48, reps=96, check=
             slm.debug_gemm(kind, impl, bn, M, N, K, As[i], B, out, resid, bias, stream=s, split=split)
     torch.cuda.synchronize()
     err = None
-    if check and impl == 0:
+    if check and impl in (0, 4):
         # correctness of this configuration against torch (fp32 reference)
         i = 1
         if kind == 0:
-            ref = resid + B.float() @ As[i].float().T + bias
+            ref = B.float() @ As[i].float().T + (resid + bias if split == 1 else 0)
         elif kind == 1:
             ref = B.float() @ As[i].float()
         else:
             ref = B.float().T @ As[i].float()
-        err = ((out.float() - ref).norm() / ref.norm()).item()
+        o = out.float().sum(0) if kind < 2 else out.float()
+        err = ((o - ref).norm() / ref.norm()).item()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for i in range(reps):

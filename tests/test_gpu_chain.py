@@ -170,3 +170,23 @@ def test_zero_weights_closed_form(slm):
     for l in range(n):
         np.testing.assert_allclose(grads["b"][l], dxn.sum(0), atol=1e-6)
     assert np.abs(grads["gamma"]).max() == 0.0
+
+
+def test_comm_world1_equals_no_comm(slm):
+    """The data-parallel path (NCCL communicator, bucketed all-reduce on the comm stream,
+    batch_global scaling) at world size 1 must reproduce the single-GPU step bit for bit."""
+    n, B, d = 12, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=4)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
+    p, g, x0, y = _dev(inp, "bf16")
+    model = slm.ChainModel(p, g, dtype="bf16", batch=B, batch_global=B)
+    plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt")
+    comm = slm.Comm(0, 1, bucket_bytes=2 * d * d * 2)   # several buckets
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            loss = model.step(plan, x0, y, stream=s, comm=comm)
+    torch.cuda.synchronize()
+    assert float(loss.item()) == ref_loss
+    for k in ref:
+        assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), k
