@@ -29,8 +29,8 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t op, hop, P, logits, dlog_f, rowloss, offs, hopR, dlR, total;
-  std::vector<size_t> opR, dpR;   // per layer rings
+  size_t hop, P, logits, dlog_f, rowloss, offs, hopR, dlR, total;
+  std::vector<size_t> opL, opR, dpR;   // per layer: forward operand [B][K_l], backward rings
 };
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
@@ -64,7 +64,6 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
                                   (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
   size_t off = 0;
-  L.op = off;       off += al(B * Kmax * 2);
   L.hop = off;      off += al(B * H * 2);
   L.P = off;        off += al(pbytes);
   L.logits = off;   off += al(B * Cp * 4);
@@ -74,6 +73,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
   L.hopR = off;     off += al(CH * B * H * 2);
   L.dlR = off;      off += al(CH * B * Cp * 2);
   for (int l = 0; l < d.n_layers; ++l) {
+    L.opL.push_back(off);
+    off += al(B * lstm_K(d, l) * 2);
     L.opR.push_back(off);
     off += al(CH * B * lstm_K(d, l) * 2);
     L.dpR.push_back(off);
@@ -109,7 +110,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
     const uint64_t K = lstm_K(d, l);
     if ((st = make_map(&M.wK[l], W + lstm_w_offset(d, l), K, 4 * H, 128)) != SLM_OK) return st;
     if ((st = make_map(&M.wMN[l], W + lstm_w_offset(d, l), K, 4 * H, 64)) != SLM_OK) return st;
-    if ((st = make_map(&M.opK[l], w + L.op, K, B, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map(&M.opK[l], w + L.opL[l], K, B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.opRK[l], w + L.opR[l], K, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
@@ -134,6 +135,31 @@ struct LstmNode {
   int t, l;     // time, layer (-1 for X_t, L for H_t / Sum)
 };
 
+// Which V' node's value currently sits (as bf16) in each forward GEMM operand: the x and h
+// halves of layer l's operand [x | h_{t-1}] and the head operand.  Cell-state kernels write
+// their h (and, at layer 0, the next input) straight into the operands of their consumers;
+// a gates / head node re-packs only when its operand does not already hold its inputs.
+// kZeros marks the all-zero h of t = 0.  Used identically by enqueue_lstm and lstm_launches.
+struct OperandTracker {
+  static constexpr int kZeros = -2;
+  std::vector<int> wx, wh;
+  int whead = -1;
+  explicit OperandTracker(int L) : wx(L, -1), wh(L, -1) {}
+  bool gates_needs_pack(int l, int xnode, int hnode) const { return wx[l] != xnode || wh[l] != hnode; }
+  void packed(int l, int xnode, int hnode) {
+    wx[l] = xnode;
+    wh[l] = hnode;
+  }
+  // cell state node u = S^l_t produced: h -> layer l's h half (t+1 < T), layer l+1's x half
+  // or the head operand; layer 0 also writes x_{t+1} (Input node xnext_node)
+  void cell(int u, int l, int t, int L, int T, int xnext_node) {
+    if (t + 1 < T) wh[l] = u;
+    if (l + 1 < L) wx[l + 1] = u;
+    else whead = u;
+    if (l == 0 && t + 1 < T) wx[0] = xnext_node;
+  }
+};
+
 slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const int32_t* labels, void* pool,
                         void* ws, float* loss, cudaStream_t st, int64_t* launches) {
   using namespace slmk;
@@ -153,7 +179,6 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const LstmWs W = lstm_ws_layout(d);
   const LstmSplits sp = lstm_splits(d);
   uint8_t* w = (uint8_t*)ws;
-  bf* op = (bf*)(w + W.op);
   bf* hop = (bf*)(w + W.hop);
   float* P = (float*)(w + W.P);
   float* logits = (float*)(w + W.logits);
@@ -208,6 +233,28 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
 
+  OperandTracker trk(L);
+  auto opl = [&](int l) { return (bf*)(w + W.opL[l]); };
+  // the operand side outputs of the kernel producing S^l_t (V' node u)
+  auto op_out = [&](int u, int l, int t) {
+    slmk::OpOut o{};
+    if (t + 1 < T) {
+      o.h_self = opl(l) + (l == 0 ? K0 : H);
+      o.ld_self = lstm_K(d, l);
+    }
+    o.h_up = l + 1 < L ? opl(l + 1) : hop;
+    o.ld_up = l + 1 < L ? lstm_K(d, l + 1) : H;
+    if (l == 0 && t + 1 < T) {
+      o.xnext = (const float*)((const uint8_t*)xin + (size_t)(t + 1) * B * I * 4);
+      o.I = I;
+      o.Kin0 = K0;
+      o.x0 = opl(0);
+      o.ld0 = lstm_K(d, 0);
+    }
+    trk.cell(u, l, t, L, T, (t + 1) * per_t);
+    return o;
+  };
+
   const std::vector<int>& order = p->order;
   for (size_t oi = 0; oi < order.size(); ++oi) {
     const int v = order[oi];
@@ -222,8 +269,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const float* x = V(pp.first[0]);
         const float* sprev = pp.second > 1 ? V(pp.first[1]) : nullptr;
         const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
-        CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
-                    H, B, op));
+        const int xn = pp.first[0], hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
+        if (trk.gates_needs_pack(l, xn, hn)) {
+          CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
+                      H, B, opl(l)));
+          trk.packed(l, xn, hn);
+          ++nl;
+        }
         slmk::EpiPartialTma e{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[l], 4 * H, B, Kin + H, 0, 0,
                                                                        e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pG)) != SLM_OK)
@@ -231,32 +283,38 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
         float* s_out = nullptr;
         const float* s_prev = nullptr;
+        slmk::OpOut oo{};
         if (oi + 1 < order.size()) {
           const int u = order[oi + 1];
           auto pu = preds_of(u);
           if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu.first[0] == v) {
             s_out = V(u);
             s_prev = pu.second > 1 ? V(pu.first[1]) : nullptr;
+            oo = op_out(u, l, t);
             ++oi;
           }
         }
         CK(launch_k(lstm_gates_cell_kernel, eg, eb, 0, st, pdl, (const float*)P, sk, d.b + (size_t)l * 4 * H, H, B, V(v),
-                    s_prev, s_out));
-        nl += 3;
+                    s_prev, s_out, oo));
+        nl += 2;
       } else if (opk == SLM_OP_LSTM_CELL) {
         CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]),
-                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v)));
+                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]), H, B, hop));
+        if (trk.whead != pp.first[0]) {
+          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]), H, B, hop));
+          trk.whead = pp.first[0];
+          ++nl;
+        }
         slmk::EpiPartialTma e{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, st,
                                                                        pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
                     labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr));
         CK(launch_k(lstm_rowsum_kernel, dim3(1), eb, 0, st, pdl, (const float*)rowloss, B, scale, V(v)));
-        nl += 4;
+        nl += 3;
       } else if (opk == SLM_OP_SUM) {
         CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, st, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
         ++nl;
@@ -278,7 +336,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
                                                                        e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), eb, 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
                     labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f));
         // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  (split-K partials) -> (dh | 0)
         slmk::EpiPartialTma e2{B};
@@ -286,7 +344,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                                                                       e2, st, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_dh_kernel, eg, eb, 0, st, pdl, (const float*)P, sp.hd, H, B, V(v)));
-        CK(launch_k(colsum_acc_kernel, dim3((Cp + 255) / 256), eb, 0, st, pdl, (const float*)dlog_f, B, Cp, d.db_o));
+        CK(launch_k(colsum_acc_kernel, dim3((Cp + 31) / 32), dim3(512), 0, st, pdl, (const float*)dlog_f, B, Cp,
+                    d.db_o));
         nl += 6;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};
@@ -332,7 +391,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         bf* opS = (bf*)(w + W.opR[l]) + (size_t)slot * B * K;
         bf* dpS = (bf*)(w + W.dpR[l]) + (size_t)slot * B * 4 * H;
         const int drow = 4 * H + (has_prev ? 2 * H : 0);
-        CK(launch_k(lstm_dpre_kernel, dim3(4 * H / 32), eb, 0, st, pdl, dact, drow, act, H, B, dpS,
+        CK(launch_k(lstm_dpre_kernel, dim3(4 * H / 32), dim3(512), 0, st, pdl, dact, drow, act, H, B, dpS,
                     d.db + (size_t)l * 4 * H));
         CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, sprev, H, B, opS));
         // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
@@ -364,25 +423,49 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   return SLM_OK;
 }
 
-// kernels enqueue_lstm launches for this plan (the memsets are not counted)
+// kernels enqueue_lstm launches for this plan (the memsets are not counted); mirrors its
+// fusion and operand-residency decisions
 int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
   int64_t nl = 0;
-  const int per_t = 2 * d.n_layers + 2, N = p->n_fwd;
+  const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, N = p->n_fwd;
+  OperandTracker trk(L);
+  auto tl = [&](int o) {
+    if (o == N - 1) return std::make_pair(T - 1, L);
+    return std::make_pair(o / per_t, (o % per_t - 1) / 2);
+  };
   const std::vector<int>& order = p->order;
   for (size_t oi = 0; oi < order.size(); ++oi) {
     const int v = order[oi], opk = p->op[v], kind = p->kind[v];
     if (opk == SLM_OP_INPUT) continue;
-    const int o = p->orig[v];
-    const int t = o == N - 1 ? d.steps - 1 : o / per_t;
+    const auto [t, l] = tl(p->orig[v]);
+    const int* pr = p->preds.data() + p->pred_ptr[v];
+    const int np = p->pred_ptr[v + 1] - p->pred_ptr[v];
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
-        nl += 3;
+        const int xn = pr[0], hn = np > 1 ? pr[1] : OperandTracker::kZeros;
+        if (trk.gates_needs_pack(l, xn, hn)) {
+          ++nl;
+          trk.packed(l, xn, hn);
+        }
+        nl += 2;
         if (oi + 1 < order.size()) {
           const int u = order[oi + 1];
-          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) ++oi;
+          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) {
+            trk.cell(u, l, t, L, T, (t + 1) * per_t);
+            ++oi;
+          }
         }
+      } else if (opk == SLM_OP_LSTM_CELL) {
+        trk.cell(v, l, t, L, T, (t + 1) * per_t);
+        ++nl;
+      } else if (opk == SLM_OP_HEAD_CE) {
+        if (trk.whead != pr[0]) {
+          ++nl;
+          trk.whead = pr[0];
+        }
+        nl += 3;
       } else {
-        nl += opk == SLM_OP_HEAD_CE ? 4 : 1;
+        ++nl;
       }
     } else {
       const bool flush = t % kLstmChunk == 0;

@@ -12,6 +12,45 @@
 
 namespace slmk {
 
+// 1 = every LSTM SIMT kernel signals griddepcontrol.launch_dependents right after its own
+// griddepcontrol.wait, so the next kernel of the chain is scheduled (and runs its prologue)
+// while this one works; the dependent still waits for this grid's completion before reading
+// its outputs (option lstm_early_trigger, default 1).
+__constant__ int c_lstm_trigger = 1;
+__device__ __forceinline__ void lstm_entry() {
+  pdl_wait();
+  if (c_lstm_trigger) pdl_launch();
+}
+
+// bf16 GEMM-operand side outputs of a cell-state kernel (S^l_t = (h, c)): the executor keeps
+// the next consumers' operands resident instead of re-packing them (executor_lstm.cuh):
+//   h_self  -> h part of layer l's operand (read by G^l_{t+1}),      row stride ld_self
+//   h_up    -> x part of layer l+1's operand, or the head operand,   row stride ld_up
+//   xnext   -> (layer 0) the next step's input x_{t+1} [B][I] fp32, written zero-padded to
+//              Kin0 columns into x0 (row stride ld0)
+struct OpOut {
+  __nv_bfloat16* h_self;
+  int ld_self;
+  __nv_bfloat16* h_up;
+  int ld_up;
+  const float* xnext;
+  int I, Kin0;
+  __nv_bfloat16* x0;
+  int ld0;
+};
+__device__ __forceinline__ void op_out_h(const OpOut& o, int b, int j, float h) {
+  const __nv_bfloat16 hb = __float2bfloat16_rn(h);
+  if (o.h_self) o.h_self[(size_t)b * o.ld_self + j] = hb;
+  if (o.h_up) o.h_up[(size_t)b * o.ld_up + j] = hb;
+}
+__device__ __forceinline__ void op_out_x(const OpOut& o, int B) {
+  if (!o.xnext) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * o.Kin0; i += gridDim.x * blockDim.x) {
+    const int b = i / o.Kin0, k = i % o.Kin0;
+    o.x0[(size_t)b * o.ld0 + k] = __float2bfloat16_rn(k < o.I ? o.xnext[(size_t)b * o.I + k] : 0.f);
+  }
+}
+
 __device__ __forceinline__ float sigm(float x) { return __frcp_rn(__fadd_rn(1.f, expf(-x))); }
 
 // op[b][0:Kin] = x (width xw, zero padded to Kin, source row stride xs), op[b][Kin:Kin+H] = h_prev
@@ -19,7 +58,7 @@ __device__ __forceinline__ float sigm(float x) { return __frcp_rn(__fadd_rn(1.f,
 __global__ void __launch_bounds__(256) lstm_pack_kernel(const float* __restrict__ x, int xw, int xs, int Kin,
                                                         const float* __restrict__ sprev, int H, int B,
                                                         __nv_bfloat16* __restrict__ op) {
-  pdl_wait();
+  lstm_entry();
   const int K = Kin + H;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * K; i += gridDim.x * blockDim.x) {
     const int b = i / K, k = i % K;
@@ -35,16 +74,19 @@ __global__ void __launch_bounds__(256) lstm_pack_kernel(const float* __restrict_
 // S = (h, c): c = f c_prev + i g, h = o tanh(c)   (sprev null: c_prev = 0)
 __global__ void __launch_bounds__(256) lstm_cell_fwd_kernel(const float* __restrict__ act,
                                                             const float* __restrict__ sprev, int H, int B,
-                                                            float* __restrict__ s) {
-  pdl_wait();
+                                                            float* __restrict__ s, OpOut oo) {
+  lstm_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
     const float* a = act + (size_t)b * 4 * H;
     const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
     const float c = __fadd_rn(__fmul_rn(a[H + j], cp), __fmul_rn(a[j], a[2 * H + j]));
-    s[(size_t)b * 2 * H + j] = __fmul_rn(a[3 * H + j], tanhf(c));
+    const float h = __fmul_rn(a[3 * H + j], tanhf(c));
+    s[(size_t)b * 2 * H + j] = h;
     s[(size_t)b * 2 * H + H + j] = c;
+    op_out_h(oo, b, j, h);
   }
+  op_out_x(oo, B);
 }
 
 // Back through S: dS = sum of up to 3 successor slices (dh | dc), each [B][2H] with row stride
@@ -56,7 +98,7 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restr
                                                             const float* __restrict__ act,
                                                             const float* __restrict__ sprev, int H, int B,
                                                             float* __restrict__ out) {
-  pdl_wait();
+  lstm_entry();
   const size_t RW = (size_t)4 * H + (sprev ? 2 * H : 0);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
@@ -83,20 +125,21 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restr
 }
 
 // d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> bf16 GEMM operand [B][4H]
-// (a slot of the per-layer time-chunk ring), and db += sum_b d_pre (fixed order: 8 row groups
-// summed in smem in group order).  d(acts) rows have stride ldd.  Block = 32 columns x 8 row
-// groups; grid = 4H / 32.
-__global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
+// (a slot of the per-layer time-chunk ring), and db += sum_b d_pre (fixed order: 16 row groups
+// b = rg (mod 16), summed in smem in group order).  d(acts) rows have stride ldd.  Block = 32
+// columns x 16 row groups; grid = 4H / 32.
+constexpr int kColGroups = 16;
+__global__ void __launch_bounds__(512) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
                                                         const float* __restrict__ act, int H, int B,
                                                         __nv_bfloat16* __restrict__ dpre, float* __restrict__ db) {
-  __shared__ float red[8][33];
-  pdl_wait();
+  __shared__ float red[kColGroups][33];
+  lstm_entry();
   const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + c;
   const int G4 = 4 * H;
   const bool tanh_gate = j >= 2 * H && j < 3 * H;
   float sum = 0.f;
-  for (int b = rg; b < B; b += 8) {
+  for (int b = rg; b < B; b += kColGroups) {
     const float a = act[(size_t)b * G4 + j], da = dact[(size_t)b * ldd + j];
     const float dv = tanh_gate ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a)))
                                : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
@@ -108,7 +151,7 @@ __global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict_
   if (rg == 0) {
     float t = red[0][c];
 #pragma unroll
-    for (int r = 1; r < 8; ++r) t = __fadd_rn(t, red[r][c]);
+    for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
     db[j] = __fadd_rn(db[j], t);
   }
 }
@@ -120,8 +163,8 @@ __global__ void __launch_bounds__(256) lstm_gates_cell_kernel(const float* __res
                                                               const float* __restrict__ bias, int H, int B,
                                                               float* __restrict__ g_out,
                                                               const float* __restrict__ sprev,
-                                                              float* __restrict__ s_out) {
-  pdl_wait();
+                                                              float* __restrict__ s_out, OpOut oo) {
+  lstm_entry();
   const size_t slice = (size_t)B * 4 * H;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
@@ -138,16 +181,19 @@ __global__ void __launch_bounds__(256) lstm_gates_cell_kernel(const float* __res
     if (s_out) {
       const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
       const float c = __fadd_rn(__fmul_rn(a[1], cp), __fmul_rn(a[0], a[2]));
-      s_out[(size_t)b * 2 * H + j] = __fmul_rn(a[3], tanhf(c));
+      const float h = __fmul_rn(a[3], tanhf(c));
+      s_out[(size_t)b * 2 * H + j] = h;
       s_out[(size_t)b * 2 * H + H + j] = c;
+      op_out_h(oo, b, j, h);
     }
   }
+  if (s_out) op_out_x(oo, B);
 }
 
 // (dh | 0) of the head gradient node from the split-K partials of dlogits W_o, P [sk][B][H]
 __global__ void __launch_bounds__(256) lstm_head_dh_kernel(const float* __restrict__ P, int sk, int H, int B,
                                                            float* __restrict__ out) {
-  pdl_wait();
+  lstm_entry();
   const size_t slice = (size_t)B * H;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
@@ -165,7 +211,7 @@ __global__ void __launch_bounds__(256) lstm_head_dh_kernel(const float* __restri
 __global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __restrict__ gx, int sk, int Kin, int H,
                                                                 int B, int xw_true, int x_is_state, int has_prev,
                                                                 float* __restrict__ out) {
-  pdl_wait();
+  lstm_entry();
   const int K = Kin + H;
   const size_t slice = (size_t)B * K;
   auto part = [&](size_t e) {
@@ -191,7 +237,7 @@ __global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __r
 // h operand of the head: bf16 [B][H] from S^{L-1}_t
 __global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict__ s, int H, int B,
                                                          __nv_bfloat16* __restrict__ hop) {
-  pdl_wait();
+  lstm_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x)
     hop[i] = __float2bfloat16_rn(s[(size_t)(i / H) * 2 * H + i % H]);
 }
@@ -200,13 +246,13 @@ __global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict
 // order), written to the row buffer `logits`; row loss = logsumexp - logit[y] over the C real
 // classes; grad (when dlog != null) = (softmax - onehot) * scale as bf16 (the GEMM operand,
 // a ring slot) + fp32 (for db_o), classes >= C: 0.
-__global__ void __launch_bounds__(256) lstm_head_ce_kernel(const float* __restrict__ P, int sk,
+__global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restrict__ P, int sk,
                                                            float* __restrict__ logits, const float* __restrict__ bo,
                                                            const int* __restrict__ y, int C, int Cp, int B, float scale,
                                                            float* __restrict__ rowloss, __nv_bfloat16* __restrict__ dlog,
                                                            float* __restrict__ dlog_f) {
   __shared__ float sh[32];
-  pdl_wait();
+  lstm_entry();
   const size_t slice = (size_t)B * Cp;
   float* lr = logits + (size_t)blockIdx.x * Cp;
   const float* pr = P + (size_t)blockIdx.x * Cp;
@@ -238,7 +284,7 @@ __global__ void __launch_bounds__(256) lstm_head_ce_kernel(const float* __restri
 __global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restrict__ rowloss, int B, float scale,
                                                           float* __restrict__ out) {
   __shared__ float sh[32];
-  pdl_wait();
+  lstm_entry();
   float s = 0.f;
   for (int b = threadIdx.x; b < B; b += blockDim.x) s = __fadd_rn(s, rowloss[b]);
   s = block_reduce_sum(s, sh);
@@ -248,7 +294,7 @@ __global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restric
 // loss = sum over the step losses (pool offsets table, in time order) — the Sum node
 __global__ void __launch_bounds__(32) lstm_sum_kernel(const uint8_t* __restrict__ pool, const long* __restrict__ offs,
                                                       int T, float* __restrict__ out) {
-  pdl_wait();
+  lstm_entry();
   if (threadIdx.x != 0) return;
   float s = 0.f;
   for (int t = 0; t < T; ++t) s = __fadd_rn(s, *reinterpret_cast<const float*>(pool + offs[t]));
@@ -256,19 +302,29 @@ __global__ void __launch_bounds__(32) lstm_sum_kernel(const uint8_t* __restrict_
 }
 
 __global__ void __launch_bounds__(256) fill_kernel(float* __restrict__ p, int n, float v) {
-  pdl_wait();
+  lstm_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
 }
 
-// acc[j] += sum_b g[b][j]  (column sums accumulated into a gradient, fixed order)
-__global__ void __launch_bounds__(256) colsum_acc_kernel(const float* __restrict__ g, int B, int n,
+// acc[j] += sum_b g[b][j]  (column sums accumulated into a gradient; fixed order: 16 row
+// groups b = rg (mod 16), then the groups in order).  Block = 32 columns x 16 groups.
+__global__ void __launch_bounds__(512) colsum_acc_kernel(const float* __restrict__ g, int B, int n,
                                                          float* __restrict__ acc) {
-  pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  float s = 0.f;
-  for (int b = 0; b < B; ++b) s = __fadd_rn(s, g[(size_t)b * n + j]);
-  acc[j] = __fadd_rn(acc[j], s);
+  __shared__ float red[kColGroups][33];
+  lstm_entry();
+  const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + c;
+  float sum = 0.f;
+  if (j < n)
+    for (int b = rg; b < B; b += kColGroups) sum = __fadd_rn(sum, g[(size_t)b * n + j]);
+  red[rg][c] = sum;
+  __syncthreads();
+  if (rg == 0 && j < n) {
+    float t = red[0][c];
+#pragma unroll
+    for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
+    acc[j] = __fadd_rn(acc[j], t);
+  }
 }
 
 }  // namespace slmk

@@ -194,6 +194,10 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   }
   else if (k == "profile_events") m->profile = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
+  else if (k == "lstm_early_trigger") {
+    const int v = (int)value;
+    CK(cudaMemcpyToSymbol(slmk::c_lstm_trigger, &v, sizeof(v)));
+  }
   else {
     set_error("unknown option " + k);
     return SLM_E_ARG;
