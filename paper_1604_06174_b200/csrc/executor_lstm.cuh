@@ -29,8 +29,8 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t hop, P, logits, dlog_f, rowloss, offs, hopR, dlR, total;
-  std::vector<size_t> opL, opR, dpR;   // per layer: forward operand [B][K_l], backward rings
+  size_t hop, P, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, total;
+  std::vector<size_t> opL, opR, dpR, dpF;   // per layer: forward operand [B][K_l], backward rings
 };
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
@@ -70,6 +70,7 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
   L.dlog_f = off;   off += al(B * Cp * 4);
   L.rowloss = off;  off += al(B * 4);
   L.offs = off;     off += al(T * 8);
+  L.cnt = off;      off += 256;
   L.hopR = off;     off += al(CH * B * H * 2);
   L.dlR = off;      off += al(CH * B * Cp * 2);
   for (int l = 0; l < d.n_layers; ++l) {
@@ -79,6 +80,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
     off += al(CH * B * lstm_K(d, l) * 2);
     L.dpR.push_back(off);
     off += al(CH * B * 4 * H * 2);
+    L.dpF.push_back(off);
+    off += al(CH * B * 4 * H * 4);
   }
   L.total = off;
   return L;
@@ -185,6 +188,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   float* dlog_f = (float*)(w + W.dlog_f);
   float* rowloss = (float*)(w + W.rowloss);
   long* offs = (long*)(w + W.offs);
+  unsigned* cnt = (unsigned*)(w + W.cnt);
   bf* hopR = (bf*)(w + W.hopR);
   bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
@@ -229,6 +233,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   CK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
   CK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
   CK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
+  CK(cudaMemsetAsync(cnt, 0, 256, st));
   // weight-gradient chunk of time t: slot in the ring and whether t closes the chunk (the
   // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
@@ -312,9 +317,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                                                                        pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
-                    labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr));
-        CK(launch_k(lstm_rowsum_kernel, dim3(1), eb, 0, st, pdl, (const float*)rowloss, B, scale, V(v)));
-        nl += 3;
+                    labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr, cnt, V(v)));
+        nl += 2;
       } else if (opk == SLM_OP_SUM) {
         CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, st, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
         ++nl;
@@ -337,16 +341,16 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                                                                        e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
-                    labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f));
+                    labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f,
+                    (unsigned*)nullptr, (float*)nullptr));
         // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  (split-K partials) -> (dh | 0)
         slmk::EpiPartialTma e2{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
                                                                       e2, st, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_dh_kernel, eg, eb, 0, st, pdl, (const float*)P, sp.hd, H, B, V(v)));
-        CK(launch_k(colsum_acc_kernel, dim3((Cp + 31) / 32), dim3(512), 0, st, pdl, (const float*)dlog_f, B, Cp,
-                    d.db_o));
-        nl += 6;
+        CK(launch_k(lstm_head_dh_colsum_kernel, dim3(std::max((Cp + 31) / 32, 128)), dim3(512), 0, st, pdl,
+                    (const float*)P, sp.hd, H, B, V(v), (const float*)dlog_f, Cp, d.db_o));
+        nl += 5;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};
           if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp, chunk_rows(t), 0,
@@ -354,62 +358,88 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             return s;
           ++nl;
         }
-      } else if (opk == SLM_OP_LSTM_CELL) {
-        // successor slices (order: layer above / head, next-step gates, next-step cell)
-        const float* sl[3] = {nullptr, nullptr, nullptr};
-        int ld[3] = {0, 0, 0};
-        int k = 0;
-        auto slice = [&](int succ_fwd, int offset_floats, int row_width) {
-          const int gs = p->gnode[succ_fwd];
-          if (gs < 0) return;
-          sl[k] = V(gs) + offset_floats;
-          ld[k] = row_width;
-          ++k;
-        };
-        const int sv = orig;
-        const int above = l + 1 < L ? sv + 1 : t * per_t + per_t - 1;   // G^{l+1}_t or H_t
-        slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
-        if (t + 1 < T) {
-          const int xw = l == 0 ? I : 2 * H;
-          slice(sv + per_t - 1, xw, xw + 2 * H);   // G^l_{t+1}
-          slice(sv + per_t, 4 * H, 4 * H + 2 * H);  // S^l_{t+1}
-        }
-        const float* act = V(pp.first[pp.second - (t > 0 ? 2 : 1)]);
-        const float* sprev = t > 0 ? V(pp.first[pp.second - 1]) : nullptr;
-        CK(launch_k(lstm_cell_bwd_kernel, eg, eb, 0, st, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev, H,
-                    B, V(v)));
-        ++nl;
-      } else if (opk == SLM_OP_LSTM_GATES) {
-        // preds = [g[S^l_t], a[G], a[x], a[S_{t-1}]?]
+      } else if (opk == SLM_OP_LSTM_CELL || opk == SLM_OP_LSTM_GATES) {
+        // g[S^l_t]: successor slices (order: layer above / head, next-step gates, next-step cell);
+        // g[G^l_t]: preds = [g[S^l_t], a[G], a[x], a[S_{t-1}]?]
         const bool has_prev = t > 0;
-        const int nf = has_prev ? 2 : 1;
-        const float* dact = V(pp.first[0]);   // slot 0 of g[S^l_t] = d(acts), row width 4H (+2H)
-        const float* act = V(pp.first[pp.second - nf - 1]);
-        const float* x = V(pp.first[pp.second - nf]);
-        const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
         const int Kin = l == 0 ? K0 : H, K = Kin + H, skx = l == 0 ? sp.x0 : sp.x1;
         bf* opS = (bf*)(w + W.opR[l]) + (size_t)slot * B * K;
         bf* dpS = (bf*)(w + W.dpR[l]) + (size_t)slot * B * 4 * H;
-        const int drow = 4 * H + (has_prev ? 2 * H : 0);
-        CK(launch_k(lstm_dpre_kernel, dim3(4 * H / 32), dim3(512), 0, st, pdl, dact, drow, act, H, B, dpS,
-                    d.db + (size_t)l * 4 * H));
-        CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, sprev, H, B, opS));
-        // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
-        slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
-                                                                      slot * B, e, st, pdl, gdbg(SLM_K_GEMM_DX),
-                                                                      &M.pX[l])) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)P, skx, Kin, H, B, I, l > 0 ? 1 : 0,
-                    has_prev ? 1 : 0, V(v)));
-        nl += 4;
-        if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
-          slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
-          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l], M.dpRMN[l], K, 4 * H,
-                                                                    chunk_rows(t), 0, 0, e2, st, pdl,
-                                                                    gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-            return s;
+        float* dpFS = (float*)(w + W.dpF[l]) + (size_t)slot * B * 4 * H;
+        int vg = -1;   // the gates gradient node handled by this iteration
+        if (opk == SLM_OP_LSTM_CELL) {
+          const float* sl[3] = {nullptr, nullptr, nullptr};
+          int ld[3] = {0, 0, 0};
+          int k = 0;
+          auto slice = [&](int succ_fwd, int offset_floats, int row_width) {
+            const int gs = p->gnode[succ_fwd];
+            if (gs < 0) return;
+            sl[k] = V(gs) + offset_floats;
+            ld[k] = row_width;
+            ++k;
+          };
+          const int sv = orig;
+          const int above = l + 1 < L ? sv + 1 : t * per_t + per_t - 1;   // G^{l+1}_t or H_t
+          slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
+          if (t + 1 < T) {
+            const int xw = l == 0 ? I : 2 * H;
+            slice(sv + per_t - 1, xw, xw + 2 * H);   // G^l_{t+1}
+            slice(sv + per_t, 4 * H, 4 * H + 2 * H);  // S^l_{t+1}
+          }
+          const float* act = V(pp.first[pp.second - (t > 0 ? 2 : 1)]);
+          const float* sprev = t > 0 ? V(pp.first[pp.second - 1]) : nullptr;
+          // fuse with g[G^l_t]'s element-wise part when V' runs it next
+          if (oi + 1 < order.size()) {
+            const int u = order[oi + 1];
+            auto pu = preds_of(u);
+            if (p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && pu.first[0] == v) {
+              const int nf = has_prev ? 2 : 1;
+              const float* x = V(pu.first[pu.second - nf]);
+              CK(launch_k(lstm_cell_bwd_dpre_kernel, eg, eb, 0, st, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
+                          sprev, H, B, V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
+              ++nl;
+              vg = u;
+              ++oi;
+            }
+          }
+          if (vg < 0) {
+            CK(launch_k(lstm_cell_bwd_kernel, eg, eb, 0, st, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
+                        H, B, V(v)));
+            ++nl;
+          }
+        } else {
+          vg = v;
+          const int nf = has_prev ? 2 : 1;
+          const float* dact = V(pp.first[0]);   // slot 0 of g[S^l_t] = d(acts), row width 4H (+2H)
+          const float* act = V(pp.first[pp.second - nf - 1]);
+          const float* x = V(pp.first[pp.second - nf]);
+          const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
+          const int drow = 4 * H + (has_prev ? 2 * H : 0);
+          CK(launch_k(lstm_dpre_kernel, eg, eb, 0, st, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
+                      l > 0 ? 2 * H : I, Kin, sprev, opS));
           ++nl;
+        }
+        if (vg >= 0) {
+          // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
+          slmk::EpiPartialTma e{B};
+          if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
+                                                                        slot * B, e, st, pdl, gdbg(SLM_K_GEMM_DX),
+                                                                        &M.pX[l])) != SLM_OK)
+            return s;
+          CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)P, skx, Kin, H, B, I, l > 0 ? 1 : 0,
+                      has_prev ? 1 : 0, V(vg)));
+          nl += 2;
+          if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
+            slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
+            if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l],
+                                                                      M.dpRMN[l], K, 4 * H, chunk_rows(t), 0, 0, e2,
+                                                                      st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+              return s;
+            // db_l += column sums of the chunk's fp32 d_pre rows (time order, plan-independent)
+            CK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, st, pdl, (const float*)(w + W.dpF[l]),
+                        chunk_rows(t), 4 * H, d.db + (size_t)l * 4 * H));
+            nl += 2;
+          }
         }
       } else {
         set_error("unsupported gradient op in lstm plan");
@@ -463,15 +493,27 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
           ++nl;
           trk.whead = pr[0];
         }
-        nl += 3;
+        nl += 2;
       } else {
         ++nl;
       }
     } else {
       const bool flush = t % kLstmChunk == 0;
-      if (opk == SLM_OP_HEAD_CE) nl += 6 + flush;
-      else if (opk == SLM_OP_LSTM_GATES) nl += 4 + flush;
-      else nl += 1;
+      if (opk == SLM_OP_HEAD_CE) {
+        nl += 5 + flush;
+      } else if (opk == SLM_OP_LSTM_GATES) {
+        nl += 3 + 2 * flush;   // d_pre/pack, dX GEMM, scatter (+ dW GEMM and db column sums)
+      } else if (opk == SLM_OP_LSTM_CELL) {
+        const int u = oi + 1 < order.size() ? order[oi + 1] : -1;
+        if (u >= 0 && p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && p->preds[p->pred_ptr[u]] == v) {
+          nl += 3 + 2 * flush;   // fused cell/d_pre/pack + dX GEMM + scatter
+          ++oi;
+        } else {
+          nl += 1;
+        }
+      } else {
+        nl += 1;
+      }
     }
   }
   return nl;

@@ -124,36 +124,30 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restr
   }
 }
 
-// d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> bf16 GEMM operand [B][4H]
-// (a slot of the per-layer time-chunk ring), and db += sum_b d_pre (fixed order: 16 row groups
-// b = rg (mod 16), summed in smem in group order).  d(acts) rows have stride ldd.  Block = 32
-// columns x 16 row groups; grid = 4H / 32.
 constexpr int kColGroups = 16;
-__global__ void __launch_bounds__(512) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
+// (declared before use by the fused kernels)
+__device__ __forceinline__ float dpre_of(int q, float da, float a);
+__device__ __forceinline__ void pack_op(const float* __restrict__ x, int xw, int xs, int Kin,
+                                       const float* __restrict__ sprev, int H, int B, __nv_bfloat16* __restrict__ op);
+
+// d_pre = d(acts) * act'  (sigmoid for i, f, o; tanh for g) -> the time-chunk rings (bf16 GEMM
+// operand + fp32 for db); d(acts) rows have stride ldd.  Then the dW operand [x | h_{t-1}]
+// into its ring slot.  (The unfused form of lstm_cell_bwd_dpre_kernel's second half.)
+__global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict__ dact, int ldd,
                                                         const float* __restrict__ act, int H, int B,
-                                                        __nv_bfloat16* __restrict__ dpre, float* __restrict__ db) {
-  __shared__ float red[kColGroups][33];
+                                                        __nv_bfloat16* __restrict__ dpre, float* __restrict__ dpre_f,
+                                                        const float* __restrict__ x, int xw, int xs, int Kin,
+                                                        const float* __restrict__ sprev,
+                                                        __nv_bfloat16* __restrict__ op) {
   lstm_entry();
-  const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + c;
   const int G4 = 4 * H;
-  const bool tanh_gate = j >= 2 * H && j < 3 * H;
-  float sum = 0.f;
-  for (int b = rg; b < B; b += kColGroups) {
-    const float a = act[(size_t)b * G4 + j], da = dact[(size_t)b * ldd + j];
-    const float dv = tanh_gate ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a)))
-                               : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
-    dpre[(size_t)b * G4 + j] = __float2bfloat16_rn(dv);
-    sum = __fadd_rn(sum, dv);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * G4; i += gridDim.x * blockDim.x) {
+    const int b = i / G4, jj = i % G4;
+    const float dv = dpre_of(jj / H, dact[(size_t)b * ldd + jj], act[i]);
+    dpre[i] = __float2bfloat16_rn(dv);
+    dpre_f[i] = dv;
   }
-  red[rg][c] = sum;
-  __syncthreads();
-  if (rg == 0) {
-    float t = red[0][c];
-#pragma unroll
-    for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
-    db[j] = __fadd_rn(db[j], t);
-  }
+  pack_op(x, xw, xs, Kin, sprev, H, B, op);
 }
 
 // G = act(sum_s P[s] + b) from the split-K partials P [sk][B][4H] (fixed slice order), and —
@@ -204,6 +198,99 @@ __global__ void __launch_bounds__(256) lstm_head_dh_kernel(const float* __restri
   }
 }
 
+__device__ __forceinline__ float dpre_of(int q, float da, float a) {   // d_pre = d(act) * act'
+  return q == 2 ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a))) : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
+}
+// [x | h_{t-1}] bf16 operand (lstm_pack_kernel's values), grid-stride over all threads
+__device__ __forceinline__ void pack_op(const float* __restrict__ x, int xw, int xs, int Kin,
+                                       const float* __restrict__ sprev, int H, int B, __nv_bfloat16* __restrict__ op) {
+  const int K = Kin + H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * K; i += gridDim.x * blockDim.x) {
+    const int b = i / K, k = i % K;
+    float v;
+    if (k < Kin)
+      v = k < xw ? x[(size_t)b * xs + k] : 0.f;
+    else
+      v = sprev ? sprev[(size_t)b * 2 * H + (k - Kin)] : 0.f;
+    op[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// Fused backward of S^l_t and the element-wise part of G^l_t's backward (used when V' runs
+// g[G^l_t] right after g[S^l_t]): lstm_cell_bwd_kernel's arithmetic writing g[S], d_pre of the
+// four gates into the time-chunk rings (bf16 GEMM operand + fp32 for db), and the dW operand
+// [x | h_{t-1}] into its ring slot.  Thread per (b, j), grid-stride.
+__global__ void __launch_bounds__(256) lstm_cell_bwd_dpre_kernel(
+    const float* __restrict__ d0, int ld0, const float* __restrict__ d1, int ld1, const float* __restrict__ d2,
+    int ld2, const float* __restrict__ act, const float* __restrict__ sprev, int H, int B, float* __restrict__ out,
+    __nv_bfloat16* __restrict__ dpre, float* __restrict__ dpre_f, const float* __restrict__ x, int xw, int xs,
+    int Kin, __nv_bfloat16* __restrict__ op) {
+  lstm_entry();
+  const size_t RW = (size_t)4 * H + (sprev ? 2 * H : 0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, j = i % H;
+    float dh = 0.f, dc = 0.f;
+    if (d0) { dh = __fadd_rn(dh, d0[(size_t)b * ld0 + j]); dc = __fadd_rn(dc, d0[(size_t)b * ld0 + H + j]); }
+    if (d1) { dh = __fadd_rn(dh, d1[(size_t)b * ld1 + j]); dc = __fadd_rn(dc, d1[(size_t)b * ld1 + H + j]); }
+    if (d2) { dh = __fadd_rn(dh, d2[(size_t)b * ld2 + j]); dc = __fadd_rn(dc, d2[(size_t)b * ld2 + H + j]); }
+    const float* a = act + (size_t)b * 4 * H;
+    const float ig = a[j], fg = a[H + j], gg = a[2 * H + j], og = a[3 * H + j];
+    const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
+    const float cc = __fadd_rn(__fmul_rn(fg, cp), __fmul_rn(ig, gg));
+    const float tc = tanhf(cc);
+    const float dct = __fadd_rn(dc, __fmul_rn(__fmul_rn(dh, og), __fsub_rn(1.f, __fmul_rn(tc, tc))));
+    const float da[4] = {__fmul_rn(dct, gg), __fmul_rn(dct, cp), __fmul_rn(dct, ig), __fmul_rn(dh, tc)};
+    const float av[4] = {ig, fg, gg, og};
+    float* o = out + (size_t)b * RW;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      o[q * H + j] = da[q];
+      const float dv = dpre_of(q, da[q], av[q]);
+      dpre[(size_t)b * 4 * H + q * H + j] = __float2bfloat16_rn(dv);
+      dpre_f[(size_t)b * 4 * H + q * H + j] = dv;
+    }
+    if (sprev) {
+      o[4 * H + j] = 0.f;
+      o[4 * H + H + j] = __fmul_rn(dct, fg);
+    }
+  }
+  pack_op(x, xw, xs, Kin, sprev, H, B, op);
+}
+
+// (dh | 0) of the head gradient node from the split-K partials P [sk][B][H] and, in blocks
+// 0 .. ceil(Cp/32)-1, db_o += column sums of dlog_f [B][Cp] (colsum_acc_kernel's order).
+// Block = 512 threads.
+__global__ void __launch_bounds__(512) lstm_head_dh_colsum_kernel(const float* __restrict__ P, int sk, int H, int B,
+                                                                  float* __restrict__ out,
+                                                                  const float* __restrict__ g, int n,
+                                                                  float* __restrict__ acc) {
+  __shared__ float red[kColGroups][33];
+  lstm_entry();
+  if ((int)blockIdx.x * 32 < n) {
+    const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + c;
+    float sum = 0.f;
+    if (j < n)
+      for (int b = rg; b < B; b += kColGroups) sum = __fadd_rn(sum, g[(size_t)b * n + j]);
+    red[rg][c] = sum;
+    __syncthreads();
+    if (rg == 0 && j < n) {
+      float t = red[0][c];
+#pragma unroll
+      for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
+      acc[j] = __fadd_rn(acc[j], t);
+    }
+  }
+  const size_t slice = (size_t)B * H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
+    const int b = i / H, jj = i % H;
+    float a = P[i];
+    for (int s = 1; s < sk; ++s) a = __fadd_rn(a, P[s * slice + i]);
+    out[(size_t)b * 2 * H + jj] = a;
+    out[(size_t)b * 2 * H + H + jj] = 0.f;
+  }
+}
+
 // Gradient w.r.t. the gates node's inputs from the dX GEMM's split-K partials
 // gx [sk][B][Kin+H] (summed in slice order):
 //   x part:  width xw (the input's true width; for a lower-layer state: (dh | 0), width 2H)
@@ -246,11 +333,14 @@ __global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict
 // order), written to the row buffer `logits`; row loss = logsumexp - logit[y] over the C real
 // classes; grad (when dlog != null) = (softmax - onehot) * scale as bf16 (the GEMM operand,
 // a ring slot) + fp32 (for db_o), classes >= C: 0.
+// With rowloss != null the last block to finish (counter `done`, reset by it) also writes
+// loss_out = sum_b rowloss[b] * scale in row order (lstm_rowsum_kernel's arithmetic).
 __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restrict__ P, int sk,
                                                            float* __restrict__ logits, const float* __restrict__ bo,
                                                            const int* __restrict__ y, int C, int Cp, int B, float scale,
                                                            float* __restrict__ rowloss, __nv_bfloat16* __restrict__ dlog,
-                                                           float* __restrict__ dlog_f) {
+                                                           float* __restrict__ dlog_f, unsigned* __restrict__ done,
+                                                           float* __restrict__ loss_out) {
   __shared__ float sh[32];
   lstm_entry();
   const size_t slice = (size_t)B * Cp;
@@ -269,6 +359,26 @@ __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restr
   for (int c = threadIdx.x; c < C; c += blockDim.x) s = __fadd_rn(s, expf(__fsub_rn(lr[c], mx)));
   s = block_reduce_sum(s, sh);
   const int yy = y[blockIdx.x];
+  if (rowloss && done) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      rowloss[blockIdx.x] = __fsub_rn(__fadd_rn(logf(s), mx), lr[yy]);
+      __threadfence();
+      last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      float t = 0.f;
+      for (int b = threadIdx.x; b < B; b += blockDim.x) t = __fadd_rn(t, ((volatile float*)rowloss)[b]);
+      t = block_reduce_sum(t, sh);
+      if (threadIdx.x == 0) {
+        *loss_out = __fmul_rn(t, scale);
+        *done = 0u;
+      }
+    }
+    return;
+  }
   if (threadIdx.x == 0 && rowloss) rowloss[blockIdx.x] = __fsub_rn(__fadd_rn(logf(s), mx), lr[yy]);
   if (!dlog) return;
   const float inv = __frcp_rn(s);

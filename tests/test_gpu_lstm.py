@@ -106,8 +106,9 @@ def test_lstm_launch_count(slm):
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, use_graph=0)
     plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "none")
-    # forward: per t, per layer GEMM + fused gates/cell, head GEMM + CE + row sum; the operands
-    # are packed only at t = 0 (afterwards the cell kernels write them); Sum 1.
-    # backward: fill 1; per t head 6, per layer cell 1 + gates 4; one weight-gradient GEMM per
-    # layer and one for the head per 32-step chunk (T = 4: one chunk)
-    assert model.launches(plan) == T * (2 * L + 3) + L + 1 + 1 + T * (6 + 5 * L) + (L + 1)
+    # forward: per t, per layer GEMM + fused gates/cell, head GEMM + CE (row sum fused); the
+    # operands are packed only at t = 0 (afterwards the cell kernels write them); Sum 1.
+    # backward: fill 1; per t head 5 (pack, logits GEMM, CE, dh GEMM, dh + db_o), per layer 3
+    # (fused cell / d_pre / pack, dX GEMM, scatter); per 32-step chunk one weight-gradient GEMM
+    # + db column sum per layer and one GEMM for the head (T = 4: one chunk)
+    assert model.launches(plan) == T * (2 * L + 2) + L + 1 + 1 + T * (5 + 3 * L) + (2 * L + 1)
