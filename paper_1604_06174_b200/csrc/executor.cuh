@@ -226,6 +226,8 @@ struct slm_model {
   int dw_stream = 1;      // dW GEMMs on a second stream
   int bn_fwd = 64, bn_dx = 64, bn_dw = 256;  // N tiles (basic lowering; the fused one uses bn = B)
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
+  int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
+  int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
@@ -284,10 +286,13 @@ bool fused_ok(const slm_model& m) {
   const int B = m.d.batch;
   return tc_ok(m) && m.fused && (B == 64 || B == 128 || B == 256) && m.d.width % 256 == 0;
 }
+// N tile of the fused GEMMs: 128 (measured best at C2: 43.7 ms/step vs 45.1 with the full
+// batch of 256 per tile; profiles/README.md sweep), or the batch when smaller
+int fused_n(const slm_model& m) { return m.fused_bn > 0 ? m.fused_bn : std::min(m.d.batch, 128); }
 // split-K factor: as many K slices as keep <= ~148 CTAs and >= 64 of K per slice
-int auto_split(int M, int K, int req) {
+int auto_split(int M, int K, int req, int n_tiles = 1) {
   if (req > 0) return req;
-  const int tiles = M / 128;
+  const int tiles = M / 128 * n_tiles;
   int s = 1;
   // ~64 CTAs: measured best at C2 (split 4: 44.7 ms/step vs 56.1 with split 8 under PDL — the
   // remaining SMs run the dependent BN kernel's early CTAs and the off-path dW GEMM)
@@ -303,8 +308,9 @@ WsLayout ws_layout(const slm_model& m) {
   const size_t B = m.d.batch, d = m.d.width;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   WsLayout L{};
-  L.sk_fwd = auto_split((int)d, (int)d, m.sk_fwd);
-  L.sk_dx = auto_split((int)d, (int)d, m.sk_dx);
+  const int nt = fused_ok(m) ? (int)B / fused_n(m) : 1;
+  L.sk_fwd = auto_split((int)d, (int)d, m.sk_fwd, nt);
+  L.sk_dx = auto_split((int)d, (int)d, m.sk_dx, nt);
   size_t off = 0;
   L.a = off;
   off += al(B * d * 4);
@@ -362,13 +368,15 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 }
 
 slm_status bind_maps(slm_model& m, void* ws) {
-  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused;
+  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
   uint8_t* w = (uint8_t*)ws;
   const bool fz = fused_ok(m);
-  const uint32_t bnf = fz ? (uint32_t)B : (uint32_t)m.bn_fwd, bnx = fz ? (uint32_t)B : (uint32_t)m.bn_dx;
+  // fused: N tile fused_n() (K-major B box rows = tile / cta group)
+  const uint32_t fb = (uint32_t)(fused_n(m) / (m.cta_pair ? 2 : 1));
+  const uint32_t bnf = fz ? fb : (uint32_t)m.bn_fwd, bnx = fz ? fb : (uint32_t)m.bn_dx;
   slm_status st;
   if ((st = make_map(&m.mW_K, m.d.W, d, n * d, 128)) != SLM_OK) return st;
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
@@ -519,8 +527,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       if (fz) {
         slmk::EpiPartialTma epi{B};
         pbeg(st);
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, L.sk_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0,
-                                                                       epi, st, pdl, gdbg(SLM_K_GEMM_FWD), &m.mP)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(fused_n(m), L.sk_fwd, m.mW_K, m.mA_K, d, B, d,
+                                                                       l * d, 0, epi, st, pdl, gdbg(SLM_K_GEMM_FWD),
+                                                                       &m.mP, m.cta_pair ? 2 : 1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_FWD, st);
         // finalize x_{l+1} and produce a_{l+1} for the next Block (BN of layer l+1)
@@ -580,8 +589,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         // dX: P[s] = g_{l+1} W_l over K slice s
         slmk::EpiPartialTma e1{B};
         pbeg(st);
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d,
-                                                                      l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX), &m.mP)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(fused_n(m), L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B,
+                                                                      d, l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX),
+                                                                      &m.mP, m.cta_pair ? 2 : 1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX, st);
         // bn_bwd(k) overwrites gq[(k+1)%3] and ab[k%2], last read by dW of backward k-2

@@ -184,6 +184,8 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "bn_dw") m->bn_dw = (int)value;
   else if (k == "sk_fwd") m->sk_fwd = (int)value;
   else if (k == "sk_dx") m->sk_dx = (int)value;
+  else if (k == "fused_bn") m->fused_bn = (int)value;
+  else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "profile_ts") m->profile_ts = (int)value;
