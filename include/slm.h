@@ -254,7 +254,12 @@ void slm_model_destroy(slm_model* m);
  *                   (caller-owned, zeroed device buffer of N*1024*2 uint64, passed as an int64
  *                   pointer value); slm_model_kernel_times then adds each launch's span
  *                   (latest end - earliest start) to its GEMM kind.  Works inside the CUDA graph.
- *   fused, dw_stream, pdl, sk_fwd, sk_dx   lowering switches */
+ *   fused, dw_stream, pdl   lowering switches of the chain
+ *   sk_fwd, sk_dx   split-K of the fused forward / dX GEMMs (0 = auto, ~64 CTAs)
+ *   fused_bn        N tile of the fused GEMMs (0 = min(batch, 128))
+ *   cta_pair        1 = fused GEMMs as CTA pairs (tcgen05 cta_group::2, clusters of 2)
+ *   lstm_early_trigger  1 (default) = LSTM element-wise kernels release their dependent launch
+ *                   (griddepcontrol.launch_dependents) right after their own dependency wait */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
 /* Kernel kinds for slm_model_kernel_times. */
 enum { SLM_K_BN_ACT = 0, SLM_K_GEMM_FWD = 1, SLM_K_GEMM_DX = 2, SLM_K_GEMM_DW = 3, SLM_K_BN_BWD = 4,
