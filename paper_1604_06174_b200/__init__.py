@@ -98,7 +98,7 @@ class Graph:
         return list(out[: cnt.value])
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.slm_graph_destroy(self._h)
             self._h = None
 
@@ -177,7 +177,7 @@ class Plan:
         return [tuple(rows[5 * i:5 * i + 5]) for i in range(cnt.value)]
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.slm_plan_destroy(self._h)
             self._h = None
 
@@ -220,7 +220,7 @@ class Comm:
         return uid
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.slm_comm_destroy(self._h)
             self._h = None
 
@@ -289,7 +289,7 @@ class _Model:
         return float(loss_host[0])
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.slm_model_destroy(self._h)
             self._h = None
 

@@ -315,6 +315,10 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("pool and workspace must be 256-byte aligned");
     return SLM_E_ARG;
   }
+  if (is_lstm && comm) {
+    set_error("the LSTM step runs replicas-only (comm must be NULL)");
+    return SLM_E_UNSUPPORTED;
+  }
   int dev = 0;
   CK(cudaGetDevice(&dev));
   int major = 0, minor = 0;
@@ -322,10 +326,6 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
   CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
   if (major != 10 || minor != 0) {
     set_error("slm kernels are built for sm_100a only");
-    return SLM_E_UNSUPPORTED;
-  }
-  if (is_lstm && comm) {
-    set_error("the LSTM step runs replicas-only (comm must be NULL)");
     return SLM_E_UNSUPPORTED;
   }
   if (!is_lstm && m->d.dtype == SLM_BF16 && m->gemm_impl == 0 && !tc_ok(*m)) {

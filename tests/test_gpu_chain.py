@@ -190,3 +190,55 @@ def test_comm_world1_equals_no_comm(slm):
     assert float(loss.item()) == ref_loss
     for k in ref:
         assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), k
+
+
+@pytest.mark.parametrize("dtype,n,B,d", [("f32", 1, 8, 64), ("f32", 2, 5, 48), ("f32", 3, 33, 80),
+                                         ("bf16", 1, 64, 256), ("bf16", 2, 64, 128), ("bf16", 3, 128, 384)])
+def test_edge_sizes_vs_oracle(slm, dtype, n, B, d):
+    """Degenerate and ragged shapes: a single block, batch/width that are not tile multiples
+    (f32 SIMT path), width not a multiple of 256 (bf16 basic lowering)."""
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    inp = margin_inputs(n, B, d, dtype, seed=n * 100 + B + d)
+    for strategy in ("none", "sqrt"):
+        loss, grads, _ = _run(slm, n, B, d, dtype, strategy, inp)
+        ol, og, _ = _oracle(n, B, d, dtype, inp)
+        assert abs(loss - ol) / abs(ol) <= tol
+        for k in og:
+            assert _rel(grads[k], og[k]) <= tol, (strategy, k, _rel(grads[k], og[k]))
+
+
+@pytest.mark.parametrize("strategy,kw", [("budget", {"budget": 3 * 64 * 256 * 4}), ("recursive", {"k": 2}),
+                                         ("recursive", {"k": 3}), ("drop_cheap", {})])
+def test_other_plans_bitwise(slm, strategy, kw):
+    n, B, d = 20, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=9)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+    p, g, x0, y = _dev(inp, "bf16")
+    model = slm.ChainModel(p, g, dtype="bf16", batch=B)
+    plan = slm.Plan(slm.Graph.chain(n, B, d), strategy, **kw)
+    loss = model.step(plan, x0, y)
+    torch.cuda.synchronize()
+    assert float(loss.item()) == ref_loss
+    for k in ref:
+        assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), k
+
+
+def test_cta_pair_and_tile_options_bitwise(slm):
+    """The fused lowering's GEMM variants: CTA pairs keep the accumulation order (bitwise equal
+    to the default); other N tiles / split-K factors re-associate the fp32 partial sums (close
+    to the default); every variant keeps checkpointed == non-checkpointed bit for bit."""
+    n, B, d = 10, 256, 512
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=21)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+    for opt in (dict(cta_pair=1), dict(fused_bn=256, sk_fwd=4, sk_dx=4), dict(cta_pair=1, fused_bn=256)):
+        l0, g0, _ = _run(slm, n, B, d, "bf16", "none", inp, **opt)
+        l1, g1, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, **opt)
+        assert l0 == l1, opt
+        for k in ref:
+            assert np.array_equal(g0[k], g1[k]), (opt, k)
+            if opt == dict(cta_pair=1):
+                assert np.array_equal(g0[k], ref[k]), (opt, k)
+            else:
+                assert _rel(g0[k], ref[k]) <= 2e-2, (opt, k, _rel(g0[k], ref[k]))   # bf16 dW rounding
+        if opt == dict(cta_pair=1):
+            assert l0 == ref_loss

@@ -112,3 +112,21 @@ def test_lstm_launch_count(slm):
     # (fused cell / d_pre / pack, dX GEMM, scatter); per 32-step chunk one weight-gradient GEMM
     # + db column sum per layer and one GEMM for the head (T = 4: one chunk)
     assert model.launches(plan) == T * (2 * L + 2) + L + 1 + 1 + T * (5 + 3 * L) + (2 * L + 1)
+
+
+@pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
+def test_lstm_edge_sizes(slm, cfg):
+    """T = 1 (no recurrence), batch 256 with a 7-wide input, a 33-step unroll (chunk + 1)."""
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=T + B)
+    loss, g, _ = _run(slm, cfg, inp, "sqrt")
+    P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
+    ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
+    assert abs(loss - ol) / abs(ol) <= 2e-2
+    for l, w in enumerate(_split_w(g["W"], inp)):
+        assert _rel(w, og["W"][l]) <= 2e-2, ("W", l)
+    assert _rel(g["W_o"][:C], og["W_o"]) <= 2e-2
+    loss0, g0, _ = _run(slm, cfg, inp, "none")
+    assert loss0 == loss
+    for k in g0:
+        assert np.array_equal(g0[k], g[k]), k
