@@ -259,7 +259,10 @@ void slm_model_destroy(slm_model* m);
  *   fused_bn        N tile of the fused GEMMs (0 = min(batch, 128))
  *   cta_pair        1 = fused GEMMs as CTA pairs (tcgen05 cta_group::2, clusters of 2)
  *   lstm_early_trigger  1 (default) = LSTM element-wise kernels release their dependent launch
- *                   (griddepcontrol.launch_dependents) right after their own dependency wait */
+ *                   (griddepcontrol.launch_dependents) right after their own dependency wait
+ *   lstm_streams    1 (default) = LSTM layer wavefront: one stream per layer + one for the head,
+ *                   ordered by per-buffer last-writer / reader events (0 = the caller's stream)
+ *   lstm_sk         split-K of the LSTM gates GEMMs (default 2, 0 = one wave of CTAs) */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
 /* Kernel kinds for slm_model_kernel_times. */
 enum { SLM_K_BN_ACT = 0, SLM_K_GEMM_FWD = 1, SLM_K_GEMM_DX = 2, SLM_K_GEMM_DW = 3, SLM_K_BN_BWD = 4,

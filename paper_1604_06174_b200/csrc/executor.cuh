@@ -204,14 +204,26 @@ struct GraphKey {
 struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
-  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX;
-  CUtensorMap woK, woMN, hopK, hopRK, hopRMN, dlRK, dlRMN, pG, pL, pH;
+  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG;   // pX / pG over layer l's partials
+  CUtensorMap woK, woMN, hopK, hopRK, hopRMN, dlRK, dlRMN, pL, pH;            // pL / pH over the head's
   const void* ws = nullptr;
 };
 struct slm_lstm_state {
   LstmMaps maps;
   const void* offs_ws = nullptr;
   const void* offs_plan = nullptr;
+  // layer-wavefront execution (option lstm_streams): one stream per layer + one for the head,
+  // a ring of events per stream, fork/join events
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> join;
+  ~slm_lstm_state() {
+    for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : join) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+    for (auto x : streams) cudaStreamDestroy(x);
+  }
 };
 
 struct slm_model {
@@ -228,6 +240,8 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
+  int lstm_sk = 2;                            // LSTM: split-K of the gates GEMMs (0 = auto; 2 measured best with the wavefront)
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;

@@ -29,7 +29,8 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t hop, P, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, total;
+  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, total;
+  std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
   std::vector<size_t> opL, opR, dpR, dpF;   // per layer: forward operand [B][K_l], backward rings
 };
 
@@ -48,24 +49,38 @@ inline int lstm_sk(int mtiles, int K) {
 struct LstmSplits {
   int g0, g1, x0, x1, lg, hd;   // gates (layer 0 / l > 0), dX (layer 0 / l > 0), logits, head dX
 };
-LstmSplits lstm_splits(const slm_lstm_desc& d) {
+LstmSplits lstm_splits(const slm_lstm_desc& d, int gates_sk = 0) {
   const int H = d.hidden, Cp = lstm_cpad(d.n_classes);
   const int K0 = lstm_K(d, 0), K1 = 2 * H;
-  return {lstm_sk(4 * H / 128, K0), lstm_sk(4 * H / 128, K1), lstm_sk(K0 / 128, 4 * H), lstm_sk(K1 / 128, 4 * H),
-          lstm_sk(Cp / 128, H), lstm_sk(H / 128, Cp)};
+  LstmSplits s{lstm_sk(4 * H / 128, K0), lstm_sk(4 * H / 128, K1), lstm_sk(K0 / 128, 4 * H), lstm_sk(K1 / 128, 4 * H),
+               lstm_sk(Cp / 128, H), lstm_sk(H / 128, Cp)};
+  if (gates_sk > 0) {   // the largest divisor of K/64 not above the request
+    auto fit = [&](int K) {
+      int b = 1;
+      for (int q = 1; q <= gates_sk; ++q)
+        if ((K / 64) % q == 0) b = q;
+      return b;
+    };
+    s.g0 = fit(K0);
+    s.g1 = fit(K1);
+  }
+  return s;
 }
 
-LstmWs lstm_ws_layout(const slm_lstm_desc& d) {
+LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t B = d.batch, H = d.hidden, T = d.steps, CH = kLstmChunk;
   const size_t K0 = lstm_K(d, 0), Kmax = std::max<size_t>(K0, 2 * H), Cp = lstm_cpad(d.n_classes);
-  const LstmSplits sp = lstm_splits(d);
+  const LstmSplits sp = lstm_splits(d, gates_sk);
   const size_t pbytes = std::max({(size_t)std::max(sp.g0, sp.g1) * B * 4 * H, (size_t)sp.x0 * B * K0,
                                   (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
   size_t off = 0;
   L.hop = off;      off += al(B * H * 2);
-  L.P = off;        off += al(pbytes);
+  for (int i = 0; i <= d.n_layers; ++i) {
+    L.P.push_back(off);
+    off += al(pbytes);
+  }
   L.logits = off;   off += al(B * Cp * 4);
   L.dlog_f = off;   off += al(B * Cp * 4);
   L.rowloss = off;  off += al(B * 4);
@@ -92,11 +107,11 @@ size_t lstm_w_offset(const slm_lstm_desc& d, int l) {   // elements
   return l == 0 ? 0 : 4 * H * k0 + (size_t)(l - 1) * 4 * H * 2 * H;
 }
 
-slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
+slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gates_sk) {
   if (M.ws == ws) return SLM_OK;
   const uint64_t B = d.batch, H = d.hidden, Cp = lstm_cpad(d.n_classes), CH = kLstmChunk;
-  const LstmWs L = lstm_ws_layout(d);
-  const LstmSplits sp = lstm_splits(d);
+  const LstmWs L = lstm_ws_layout(d, gates_sk);
+  const LstmSplits sp = lstm_splits(d, gates_sk);
   uint8_t* w = (uint8_t*)ws;
   const __nv_bfloat16* W = (const __nv_bfloat16*)d.W;
   const int nl = d.n_layers;
@@ -107,6 +122,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
   M.dpRK.resize(nl);
   M.dpRMN.resize(nl);
   M.pX.resize(nl);
+  M.pG.resize(nl);
   M.opRK.resize(nl);
   slm_status st;
   for (int l = 0; l < nl; ++l) {
@@ -118,7 +134,8 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
     if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
-    if ((st = make_map_f32(&M.pX[l], w + L.P, K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
+    if ((st = make_map_f32(&M.pX[l], w + L.P[l], K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
+    if ((st = make_map_f32(&M.pG[l], w + L.P[l], 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK) return st;
   }
   if ((st = make_map(&M.woK, d.W_o, H, Cp, 128)) != SLM_OK) return st;
   if ((st = make_map(&M.woMN, d.W_o, H, Cp, 64)) != SLM_OK) return st;
@@ -127,9 +144,8 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws) {
   if ((st = make_map(&M.hopRMN, w + L.hopR, H, CH * B, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRK, w + L.dlR, Cp, CH * B, (uint32_t)B)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRMN, w + L.dlR, Cp, CH * B, 64)) != SLM_OK) return st;
-  if ((st = make_map_f32(&M.pG, w + L.P, 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK) return st;
-  if ((st = make_map_f32(&M.pL, w + L.P, Cp, (uint64_t)sp.lg * B)) != SLM_OK) return st;
-  if ((st = make_map_f32(&M.pH, w + L.P, H, (uint64_t)sp.hd * B)) != SLM_OK) return st;
+  if ((st = make_map_f32(&M.pL, w + L.P[nl], Cp, (uint64_t)sp.lg * B)) != SLM_OK) return st;
+  if ((st = make_map_f32(&M.pH, w + L.P[nl], H, (uint64_t)sp.hd * B)) != SLM_OK) return st;
   M.ws = ws;
   return SLM_OK;
 }
@@ -179,11 +195,11 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   };
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
   const int Cp = lstm_cpad(C), K0 = lstm_kin0(I), CH = kLstmChunk;
-  const LstmWs W = lstm_ws_layout(d);
-  const LstmSplits sp = lstm_splits(d);
+  const LstmWs W = lstm_ws_layout(d, m.lstm_sk);
+  const LstmSplits sp = lstm_splits(d, m.lstm_sk);
   uint8_t* w = (uint8_t*)ws;
   bf* hop = (bf*)(w + W.hop);
-  float* P = (float*)(w + W.P);
+  auto Pb = [&](int i) { return (const float*)(w + W.P[i]); };   // split-K partials of stream i
   float* logits = (float*)(w + W.logits);
   float* dlog_f = (float*)(w + W.dlog_f);
   float* rowloss = (float*)(w + W.rowloss);
@@ -193,7 +209,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
   slm_status s;
-  if ((s = lstm_bind_maps(d, S.maps, ws)) != SLM_OK) return s;
+  if ((s = lstm_bind_maps(d, S.maps, ws, m.lstm_sk)) != SLM_OK) return s;
   const LstmMaps& M = S.maps;
 
   const int N = p->n_fwd;
@@ -260,6 +276,71 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     return o;
   };
 
+  // ---- layer wavefront (option lstm_streams): every launch unit runs on the stream of its
+  // layer (the head and the loss on stream L); happens-before edges come from tracking, per
+  // resource (pool tag, forward operand half), the last writer and the latest reader on each
+  // stream, so concurrent units never touch a buffer out of V' order.  Event rings per stream:
+  // re-recording an event only makes a later wait more conservative (same stream, later work).
+  const bool msm = m.lstm_streams != 0 && st != nullptr;
+  const int NSTR = L + 1;
+  constexpr int kRing = 64;
+  const int ntag = (int)p->tag_size.size();
+  auto OPX = [&](int l) { return ntag + 2 * l; };
+  auto OPH = [&](int l) { return ntag + 2 * l + 1; };
+  const int HOP = ntag + 2 * L;
+  std::vector<int> rd, wr;
+  std::vector<int> res_w, res_r;   // [resource] last writer event; [resource][stream] latest reader
+  std::vector<int> ring(NSTR, 0), waits;
+  if (msm) {
+    while ((int)S.streams.size() < NSTR) {
+      cudaStream_t x;
+      CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+      S.streams.push_back(x);
+    }
+    while ((int)S.ev.size() < NSTR * kRing) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      S.ev.push_back(e);
+    }
+    while ((int)S.join.size() < NSTR) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      S.join.push_back(e);
+    }
+    if (!S.fork) CK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
+    res_w.assign(HOP + 1, -1);
+    res_r.assign((size_t)(HOP + 1) * NSTR, -1);
+    CK(cudaEventRecord(S.fork, st));
+    for (int i = 0; i < NSTR; ++i) CK(cudaStreamWaitEvent(S.streams[i], S.fork, 0));
+  }
+  auto unit_begin = [&](int sid, cudaStream_t* out) -> slm_status {
+    waits.clear();
+    for (int r : rd)
+      if (res_w[r] >= 0) waits.push_back(res_w[r]);
+    for (int r : wr) {
+      if (res_w[r] >= 0) waits.push_back(res_w[r]);
+      for (int i = 0; i < NSTR; ++i)
+        if (res_r[(size_t)r * NSTR + i] >= 0) waits.push_back(res_r[(size_t)r * NSTR + i]);
+    }
+    std::sort(waits.begin(), waits.end());
+    waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
+    for (int e : waits)
+      if (e / kRing != sid) CK(cudaStreamWaitEvent(S.streams[sid], S.ev[e], 0));
+    *out = S.streams[sid];
+    return SLM_OK;
+  };
+  auto unit_end = [&](int sid) -> slm_status {
+    const int e = sid * kRing + ring[sid];
+    ring[sid] = (ring[sid] + 1) % kRing;
+    CK(cudaEventRecord(S.ev[e], S.streams[sid]));
+    for (int r : rd) res_r[(size_t)r * NSTR + sid] = e;
+    for (int r : wr) {
+      res_w[r] = e;
+      for (int i = 0; i < NSTR; ++i) res_r[(size_t)r * NSTR + i] = -1;
+    }
+    return SLM_OK;
+  };
+
   const std::vector<int>& order = p->order;
   for (size_t oi = 0; oi < order.size(); ++oi) {
     const int v = order[oi];
@@ -268,6 +349,51 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     const LstmNode ni = info(orig);
     const int t = ni.t, l = ni.l;
     if (opk == SLM_OP_INPUT) continue;
+    // ---- the launch unit: this node, plus the next one when the two are fused
+    const int sid = (opk == SLM_OP_LSTM_GATES || opk == SLM_OP_LSTM_CELL) ? l : L;
+    int partner = -1;
+    if (oi + 1 < order.size()) {
+      const int u = order[oi + 1];
+      const bool pu0 = p->pred_ptr[u + 1] > p->pred_ptr[u] && p->preds[p->pred_ptr[u]] == v;
+      if (kind != SLM_KIND_GRAD && opk == SLM_OP_LSTM_GATES && p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu0)
+        partner = u;
+      if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL && p->op[u] == SLM_OP_LSTM_GATES &&
+          p->kind[u] == SLM_KIND_GRAD && pu0)
+        partner = u;
+    }
+    rd.clear();
+    wr.clear();
+    for (int node : {v, partner}) {
+      if (node < 0) continue;
+      auto pn = preds_of(node);
+      for (int i = 0; i < pn.second; ++i)
+        if (pn.first[i] != v) rd.push_back(p->node_tag[pn.first[i]]);
+      wr.push_back(p->node_tag[node]);
+    }
+    auto cell_writes = [&]() {
+      if (t + 1 < T) wr.push_back(OPH(l));
+      wr.push_back(l + 1 < L ? OPX(l + 1) : HOP);
+      if (l == 0 && t + 1 < T) wr.push_back(OPX(0));
+    };
+    if (kind != SLM_KIND_GRAD) {
+      if (opk == SLM_OP_LSTM_GATES) {
+        const int hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
+        if (trk.gates_needs_pack(l, pp.first[0], hn)) {
+          wr.push_back(OPX(l));
+          wr.push_back(OPH(l));
+        } else {
+          rd.push_back(OPX(l));
+          rd.push_back(OPH(l));
+        }
+        if (partner >= 0) cell_writes();
+      } else if (opk == SLM_OP_LSTM_CELL) {
+        cell_writes();
+      } else if (opk == SLM_OP_HEAD_CE) {
+        (trk.whead != pp.first[0] ? wr : rd).push_back(HOP);
+      }
+    }
+    cudaStream_t cs = st;
+    if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
         const bool lower_state = l > 0;
@@ -276,14 +402,14 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
         const int xn = pp.first[0], hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
         if (trk.gates_needs_pack(l, xn, hn)) {
-          CK(launch_k(lstm_pack_kernel, eg, eb, 0, st, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
+          CK(launch_k(lstm_pack_kernel, eg, eb, 0, cs, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
                       H, B, opl(l)));
           trk.packed(l, xn, hn);
           ++nl;
         }
         slmk::EpiPartialTma e{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[l], 4 * H, B, Kin + H, 0, 0,
-                                                                       e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pG)) != SLM_OK)
+                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pG[l])) != SLM_OK)
           return s;
         // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
         float* s_out = nullptr;
@@ -299,16 +425,16 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             ++oi;
           }
         }
-        CK(launch_k(lstm_gates_cell_kernel, eg, eb, 0, st, pdl, (const float*)P, sk, d.b + (size_t)l * 4 * H, H, B, V(v),
+        CK(launch_k(lstm_gates_cell_kernel, eg, eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H, H, B, V(v),
                     s_prev, s_out, oo));
         nl += 2;
       } else if (opk == SLM_OP_LSTM_CELL) {
-        CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]),
+        CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]),
                     (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
         if (trk.whead != pp.first[0]) {
-          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, (const float*)V(pp.first[0]), H, B, hop));
+          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]), H, B, hop));
           trk.whead = pp.first[0];
           ++nl;
         }
@@ -316,11 +442,11 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, st,
                                                                        pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
                     labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr, cnt, V(v)));
         nl += 2;
       } else if (opk == SLM_OP_SUM) {
-        CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, st, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
+        CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
         ++nl;
       } else {
         set_error("unsupported op in lstm plan");
@@ -330,31 +456,31 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       const int slot = t % CH;
       const bool flush = slot == 0;
       if (opk == SLM_OP_SUM) {
-        CK(launch_k(fill_kernel, dim3(1), eb, 0, st, pdl, V(v), T, 1.0f));
+        CK(launch_k(fill_kernel, dim3(1), eb, 0, cs, pdl, V(v), T, 1.0f));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
         // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits (the head reads only its input, A6)
         const float* sL = V(pp.first[pp.second - 1]);
-        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, st, pdl, sL, H, B, hopR + (size_t)slot * B * H));
+        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, sL, H, B, hopR + (size_t)slot * B * H));
         slmk::EpiPartialTma e{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
-                                                                       e, st, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
+                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, st, pdl, (const float*)P, sp.lg, logits, d.b_o,
+        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
                     labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f,
                     (unsigned*)nullptr, (float*)nullptr));
         // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  (split-K partials) -> (dh | 0)
         slmk::EpiPartialTma e2{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
-                                                                      e2, st, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
+                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_dh_colsum_kernel, dim3(std::max((Cp + 31) / 32, 128)), dim3(512), 0, st, pdl,
-                    (const float*)P, sp.hd, H, B, V(v), (const float*)dlog_f, Cp, d.db_o));
+        CK(launch_k(lstm_head_dh_colsum_kernel, dim3(std::max((Cp + 31) / 32, 128)), dim3(512), 0, cs, pdl,
+                    Pb(sid), sp.hd, H, B, V(v), (const float*)dlog_f, Cp, d.db_o));
         nl += 5;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};
           if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp, chunk_rows(t), 0,
-                                                                    0, e3, st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+                                                                    0, e3, cs, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
             return s;
           ++nl;
         }
@@ -395,7 +521,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             if (p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && pu.first[0] == v) {
               const int nf = has_prev ? 2 : 1;
               const float* x = V(pu.first[pu.second - nf]);
-              CK(launch_k(lstm_cell_bwd_dpre_kernel, eg, eb, 0, st, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
+              CK(launch_k(lstm_cell_bwd_dpre_kernel, eg, eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
                           sprev, H, B, V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
               ++nl;
               vg = u;
@@ -403,7 +529,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             }
           }
           if (vg < 0) {
-            CK(launch_k(lstm_cell_bwd_kernel, eg, eb, 0, st, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
+            CK(launch_k(lstm_cell_bwd_kernel, eg, eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
                         H, B, V(v)));
             ++nl;
           }
@@ -415,7 +541,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           const float* x = V(pp.first[pp.second - nf]);
           const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
           const int drow = 4 * H + (has_prev ? 2 * H : 0);
-          CK(launch_k(lstm_dpre_kernel, eg, eb, 0, st, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
+          CK(launch_k(lstm_dpre_kernel, eg, eb, 0, cs, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
                       l > 0 ? 2 * H : I, Kin, sprev, opS));
           ++nl;
         }
@@ -423,20 +549,20 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
           slmk::EpiPartialTma e{B};
           if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
-                                                                        slot * B, e, st, pdl, gdbg(SLM_K_GEMM_DX),
+                                                                        slot * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX),
                                                                         &M.pX[l])) != SLM_OK)
             return s;
-          CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, st, pdl, (const float*)P, skx, Kin, H, B, I, l > 0 ? 1 : 0,
+          CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, cs, pdl, Pb(sid), skx, Kin, H, B, I, l > 0 ? 1 : 0,
                       has_prev ? 1 : 0, V(vg)));
           nl += 2;
           if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
             slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
             if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l],
                                                                       M.dpRMN[l], K, 4 * H, chunk_rows(t), 0, 0, e2,
-                                                                      st, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+                                                                      cs, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
               return s;
             // db_l += column sums of the chunk's fp32 d_pre rows (time order, plan-independent)
-            CK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, st, pdl, (const float*)(w + W.dpF[l]),
+            CK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, cs, pdl, (const float*)(w + W.dpF[l]),
                         chunk_rows(t), 4 * H, d.db + (size_t)l * 4 * H));
             nl += 2;
           }
@@ -445,6 +571,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         set_error("unsupported gradient op in lstm plan");
         return SLM_E_UNSUPPORTED;
       }
+    }
+    if (msm && (s = unit_end(sid)) != SLM_OK) return s;
+  }
+  if (msm) {   // join every stream back into the caller's
+    for (int i = 0; i < NSTR; ++i) {
+      CK(cudaEventRecord(S.join[i], S.streams[i]));
+      CK(cudaStreamWaitEvent(st, S.join[i], 0));
     }
   }
   CK(cudaGetLastError());
