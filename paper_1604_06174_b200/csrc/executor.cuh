@@ -219,7 +219,8 @@ struct slm_lstm_state {
   cudaEvent_t fork = nullptr;
   std::vector<cudaEvent_t> join;
   ~slm_lstm_state() {
-    for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
     for (auto e : join) cudaEventDestroy(e);
     if (fork) cudaEventDestroy(fork);
     for (auto x : streams) cudaStreamDestroy(x);

@@ -279,29 +279,30 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   // ---- layer wavefront (option lstm_streams): every launch unit runs on the stream of its
   // layer (the head and the loss on stream L); happens-before edges come from tracking, per
   // resource (pool tag, forward operand half), the last writer and the latest reader on each
-  // stream, so concurrent units never touch a buffer out of V' order.  Event rings per stream:
-  // re-recording an event only makes a later wait more conservative (same stream, later work).
+  // stream, so concurrent units never touch a buffer out of V' order.  A dependency is a
+  // (stream, unit sequence number); it is skipped when the waiting stream is already ordered
+  // after that unit (same stream, or an earlier wait on a later unit of that stream).  Events
+  // live in a per-stream ring large enough to hold a step's units; a re-recorded slot only
+  // makes a (very old) wait more conservative, never wrong.
   const bool msm = m.lstm_streams != 0 && st != nullptr;
   const int NSTR = L + 1;
-  constexpr int kRing = 64;
+  constexpr int kRing = 16384;
   const int ntag = (int)p->tag_size.size();
   auto OPX = [&](int l) { return ntag + 2 * l; };
   auto OPH = [&](int l) { return ntag + 2 * l + 1; };
   const int HOP = ntag + 2 * L;
   std::vector<int> rd, wr;
-  std::vector<int> res_w, res_r;   // [resource] last writer event; [resource][stream] latest reader
-  std::vector<int> ring(NSTR, 0), waits;
+  // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
+  std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
+  std::vector<long> seqn(NSTR, 0), waits;
+  std::vector<long> known((size_t)NSTR * NSTR, -1);   // [a][s]: latest seq of s stream a is ordered after
   if (msm) {
     while ((int)S.streams.size() < NSTR) {
       cudaStream_t x;
       CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
       S.streams.push_back(x);
     }
-    while ((int)S.ev.size() < NSTR * kRing) {
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      S.ev.push_back(e);
-    }
+    if ((int)S.ev.size() < NSTR * kRing) S.ev.resize((size_t)NSTR * kRing, nullptr);
     while ((int)S.join.size() < NSTR) {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -310,9 +311,11 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     if (!S.fork) CK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
     res_w.assign(HOP + 1, -1);
     res_r.assign((size_t)(HOP + 1) * NSTR, -1);
+    // events are created lazily up to the ring size
     CK(cudaEventRecord(S.fork, st));
     for (int i = 0; i < NSTR; ++i) CK(cudaStreamWaitEvent(S.streams[i], S.fork, 0));
   }
+  auto evt = [&](long u) -> cudaEvent_t& { return S.ev[(size_t)(u % NSTR) * kRing + (size_t)((u / NSTR) % kRing)]; };
   auto unit_begin = [&](int sid, cudaStream_t* out) -> slm_status {
     waits.clear();
     for (int r : rd)
@@ -322,20 +325,25 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       for (int i = 0; i < NSTR; ++i)
         if (res_r[(size_t)r * NSTR + i] >= 0) waits.push_back(res_r[(size_t)r * NSTR + i]);
     }
-    std::sort(waits.begin(), waits.end());
-    waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
-    for (int e : waits)
-      if (e / kRing != sid) CK(cudaStreamWaitEvent(S.streams[sid], S.ev[e], 0));
+    // per source stream only the latest unit matters
+    std::vector<long> need(NSTR, -1);
+    for (long u : waits) need[u % NSTR] = std::max(need[u % NSTR], u / NSTR);
+    for (int s2 = 0; s2 < NSTR; ++s2) {
+      if (s2 == sid || need[s2] < 0 || known[(size_t)sid * NSTR + s2] >= need[s2]) continue;
+      CK(cudaStreamWaitEvent(S.streams[sid], evt(need[s2] * NSTR + s2), 0));
+      known[(size_t)sid * NSTR + s2] = need[s2];
+    }
     *out = S.streams[sid];
     return SLM_OK;
   };
   auto unit_end = [&](int sid) -> slm_status {
-    const int e = sid * kRing + ring[sid];
-    ring[sid] = (ring[sid] + 1) % kRing;
-    CK(cudaEventRecord(S.ev[e], S.streams[sid]));
-    for (int r : rd) res_r[(size_t)r * NSTR + sid] = e;
+    const long u = seqn[sid]++ * NSTR + sid;
+    cudaEvent_t& e = evt(u);
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, S.streams[sid]));
+    for (int r : rd) res_r[(size_t)r * NSTR + sid] = u;
     for (int r : wr) {
-      res_w[r] = e;
+      res_w[r] = u;
       for (int i = 0; i < NSTR; ++i) res_r[(size_t)r * NSTR + i] = -1;
     }
     return SLM_OK;
@@ -439,7 +447,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           ++nl;
         }
         slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, st,
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, cs,
                                                                        pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,

@@ -130,3 +130,21 @@ def test_lstm_edge_sizes(slm, cfg):
     assert loss0 == loss
     for k in g0:
         assert np.array_equal(g0[k], g[k]), k
+
+
+@pytest.mark.parametrize("cfg", [(1, 2, 256, 128, 7, 128), (3, 9, 64, 128, 50, 300)])
+def test_lstm_wavefront_matches_single_stream(slm, cfg):
+    """Race detection for the layer wavefront (lstm_streams=1): repeated steps must reproduce
+    the single-stream step bit for bit (a missing happens-before edge shows up as a changed
+    loss or gradient, e.g. a head reading a stale operand)."""
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=5)
+    ref_loss, ref, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
+                            lstm_streams=0)
+    for rep in range(4):
+        for pdl in (1, 0):
+            loss, g, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
+                              lstm_streams=1, pdl=pdl)
+            assert loss == ref_loss, (rep, pdl)
+            for k in ref:
+                assert np.array_equal(g[k], ref[k]), (rep, pdl, k)
