@@ -268,7 +268,10 @@ def run_lstm(args):
             ms = t.item()
         return ms, float(loss.item()), clk.summary() if clk else None
 
-    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg))
+    # grouped sharing (reading A22): tags never cross layers -> less memory and no false
+    # cross-layer dependencies for the layer wavefront
+    AF = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_GROUPED
+    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg), alloc_flags=AF)
     torch.cuda.synchronize()
     base_mem = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
@@ -324,7 +327,7 @@ def run_lstm(args):
 
     nock = None
     if not args.no_nockpt:
-        plan0 = slm.Plan(graph, "none")
+        plan0 = slm.Plan(graph, "none", alloc_flags=AF)
         model._bufs.pop(id(plan), None)
         torch.cuda.empty_cache()
         torch.cuda.synchronize()

@@ -144,7 +144,11 @@ void slm_graph_destroy(slm_graph* g);
  */
 enum { SLM_PLAN_NONE = 0, SLM_PLAN_SQRT = 1, SLM_PLAN_BUDGET = 2, SLM_PLAN_SEARCH = 3,
        SLM_PLAN_RECURSIVE = 4, SLM_PLAN_EXPLICIT = 5, SLM_PLAN_DROP_CHEAP = 6 };
-enum { SLM_ALLOC_INPLACE = 1, SLM_ALLOC_SHARING = 2 };
+/* SLM_ALLOC_GROUPED (with SHARING): a freed tag is reused only by a node of the same allocation
+ * group (slm_graph_lstm: the layer of a gates/cell node, L for the head and the loss; every
+ * other builder: one group), so the plan never makes work of two layers share memory and the
+ * layer wavefront keeps its concurrency (reading A22; an extension, not the paper). */
+enum { SLM_ALLOC_INPLACE = 1, SLM_ALLOC_SHARING = 2, SLM_ALLOC_GROUPED = 4 };
 
 typedef struct {
   int32_t strategy;       /* SLM_PLAN_*                                                    */

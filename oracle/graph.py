@@ -85,6 +85,7 @@ class Node:
     preds: list
     out_bytes: int
     flags: int = 0
+    group: int = 0     # allocation group (A_GROUPED, reading A22): the LSTM layer
 
 
 @dataclass
@@ -224,15 +225,15 @@ def lstm_graph(n_layers: int, steps: int, batch: int, hidden: int, n_in: int,
         for l in range(n_layers):
             gid = len(nodes)
             preds = [below] + ([s_prev[l]] if s_prev[l] is not None else [])
-            nodes.append(Node(LSTM_GATES, preds, batch * 4 * hidden * elem_bytes))
+            nodes.append(Node(LSTM_GATES, preds, batch * 4 * hidden * elem_bytes, group=l))
             sid = len(nodes)
             preds = [gid] + ([s_prev[l]] if s_prev[l] is not None else [])
-            nodes.append(Node(LSTM_CELL, preds, batch * 2 * hidden * elem_bytes))
+            nodes.append(Node(LSTM_CELL, preds, batch * 2 * hidden * elem_bytes, group=l))
             s_prev[l] = sid
             below = sid
         heads.append(len(nodes))
-        nodes.append(Node(HEAD_CE, [below], 4, F_NOT_CANDIDATE))
-    nodes.append(Node(SUM, heads, 4, F_NOT_CANDIDATE))
+        nodes.append(Node(HEAD_CE, [below], 4, F_NOT_CANDIDATE, group=n_layers))
+    nodes.append(Node(SUM, heads, 4, F_NOT_CANDIDATE, group=n_layers))
     return Graph(nodes, [len(nodes) - 1], kind="lstm",
                  dims=dict(n_layers=n_layers, steps=steps, batch=batch, hidden=hidden,
                            n_in=n_in))

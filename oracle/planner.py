@@ -24,7 +24,7 @@ from .graph import (OPS, INPUT, F_NOT_CANDIDATE, F_PIN, F_REQUEST_GRAD, Graph,
 # strategies (values mirrored independently in include/slm.h)
 S_NONE, S_SQRT, S_BUDGET, S_SEARCH, S_RECURSIVE, S_EXPLICIT, S_DROP_CHEAP = range(7)
 # allocator switches (the paper's compared strategies)
-A_INPLACE, A_SHARING = 1, 2
+A_INPLACE, A_SHARING, A_GROUPED = 1, 2, 4
 
 # App. A grid, reading A3: 6 geometric points 2^((2i-5)/10), i=0..5, spanning [B/sqrt2, sqrt2 B]
 GRID = (0.7071067811865476, 0.8122523963562356, 0.9330329915368074,
@@ -277,15 +277,20 @@ class Allocation:
     exact_peak: int
 
 
-def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256) -> Allocation:
+def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256, groups=None) -> Allocation:
     """Fig. 2 over V' with reading A8:
     counter = pending consumers; (1) in place iff the op declares a slot, that input's
     counter is 1, sizes are equal and the input is not pinned; (2) else the smallest free
     tag with size >= request (ties: lowest tag id); (3) else a fresh tag of exactly that
     size; (4) only then decrement input counters and release tags that reach 0.  Nodes
     with no consumers are released right after they run.  Pinned tags never recycle.
-    Offsets: reading A9."""
+    Offsets: reading A9.  A_GROUPED (reading A22, an extension): step (2) only considers free
+    tags created by a node of the same allocation group (groups[orig])."""
     nodes = gg.nodes
+
+    def grp(v):
+        return groups[nodes[v].orig] if (flags & A_GROUPED) and groups is not None else 0
+    tag_group = []
     cnt = {}
     for v in gg.order:
         cnt.setdefault(v, 0)
@@ -299,6 +304,7 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256) -> Allocatio
             t = len(tag_size)
             tag_size.append(nd.out_bytes)
             tag_ext.append(True)
+            tag_group.append(grp(v))
         else:
             s = nd.inplace_slot
             if (flags & A_INPLACE) and 0 <= s < len(nd.preds):
@@ -309,7 +315,7 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256) -> Allocatio
             if t is None and (flags & A_SHARING):
                 best = None
                 for f in free:
-                    if tag_size[f] >= nd.out_bytes:
+                    if tag_size[f] >= nd.out_bytes and tag_group[f] == grp(v):
                         if best is None or (tag_size[f], f) < (tag_size[best], best):
                             best = f
                 if best is not None:
@@ -319,6 +325,7 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256) -> Allocatio
                 t = len(tag_size)
                 tag_size.append(nd.out_bytes)
                 tag_ext.append(False)
+                tag_group.append(grp(v))
         tag_of[v] = t
         for u in nd.preds:
             cnt[u] -= 1
@@ -352,7 +359,7 @@ class Plan:
 
 def _make(g, m, topo, flags, align):
     gg = build_mirrored(g, m, topo)
-    al = allocate(gg, flags, align)
+    al = allocate(gg, flags, align, [nd.group for nd in g.nodes])
     return Plan(list(m), gg, al, extra_forward(gg))
 
 

@@ -14,6 +14,7 @@
 #include <functional>
 #include <new>
 #include <queue>
+#include <map>
 #include <set>
 #include <string>
 #include <unordered_set>
@@ -385,8 +386,11 @@ struct Alloc {
 };
 
 // Fig. 2, reading A8; offsets reading A9.
-void allocate(const Built& b, int flags, int64_t align, Alloc* out) {
+void allocate(const Built& b, int flags, int64_t align, Alloc* out, const std::vector<int>& group) {
   const auto& nodes = b.nodes;
+  const bool grouped = (flags & SLM_ALLOC_GROUPED) != 0;
+  auto grp = [&](int v) { return grouped ? group[nodes[v].orig] : 0; };
+  std::vector<int> tag_group;
   std::vector<int> cnt(nodes.size(), 0);
   for (int v : b.order)
     for (int p : nodes[v].preds) cnt[p]++;
@@ -396,7 +400,9 @@ void allocate(const Built& b, int flags, int64_t align, Alloc* out) {
   auto& tag_ext = out->tag_ext;
   tag_size.clear();
   tag_ext.clear();
-  std::set<std::pair<int64_t, int>> free_tags;  // (size, id): smallest fit, lowest id
+  // free tags per allocation group: (size, id) -> smallest fit, lowest id
+  std::map<int, std::set<std::pair<int64_t, int>>> free_by_group;
+  auto release = [&](int tag) { free_by_group[tag_group[tag]].insert({tag_size[tag], tag}); };
   for (int v : b.order) {
     const GN& nd = nodes[v];
     int t = -1;
@@ -404,6 +410,7 @@ void allocate(const Built& b, int flags, int64_t align, Alloc* out) {
       t = (int)tag_size.size();
       tag_size.push_back(nd.out_bytes);
       tag_ext.push_back(1);
+      tag_group.push_back(grp(v));
     } else {
       int s = nd.inplace_slot;
       if ((flags & SLM_ALLOC_INPLACE) && s >= 0 && s < (int)nd.preds.size()) {
@@ -411,6 +418,7 @@ void allocate(const Built& b, int flags, int64_t align, Alloc* out) {
         if (cnt[u] == 1 && nodes[u].out_bytes == nd.out_bytes && !b.pinned[u]) t = tag_of[u];
       }
       if (t < 0 && (flags & SLM_ALLOC_SHARING)) {
+        auto& free_tags = free_by_group[grp(v)];
         auto it = free_tags.lower_bound({nd.out_bytes, -1});
         if (it != free_tags.end()) {
           t = it->second;
@@ -421,14 +429,14 @@ void allocate(const Built& b, int flags, int64_t align, Alloc* out) {
         t = (int)tag_size.size();
         tag_size.push_back(nd.out_bytes);
         tag_ext.push_back(0);
+        tag_group.push_back(grp(v));
       }
     }
     tag_of[v] = t;
     for (int u : nd.preds) {
-      if (--cnt[u] == 0 && !b.pinned[u] && tag_of[u] != t)
-        free_tags.insert({tag_size[tag_of[u]], tag_of[u]});
+      if (--cnt[u] == 0 && !b.pinned[u] && tag_of[u] != t) release(tag_of[u]);
     }
-    if (cnt[v] == 0 && !b.pinned[v]) free_tags.insert({tag_size[t], t});
+    if (cnt[v] == 0 && !b.pinned[v]) release(t);
   }
   out->tag_offset.assign(tag_size.size(), -1);
   int64_t run = 0, peak = 0;
@@ -459,7 +467,9 @@ slm_status evaluate(const slm_graph& g, const std::vector<int>& topo, std::vecto
   e->m = std::move(m);
   slm_status st = build_mirrored(g, e->m, topo, &e->b);
   if (st != SLM_OK) return st;
-  allocate(e->b, flags, align, &e->al);
+  std::vector<int> group(g.nodes.size());
+  for (size_t v = 0; v < g.nodes.size(); ++v) group[v] = g.nodes[v].group;
+  allocate(e->b, flags, align, &e->al, group);
   return SLM_OK;
 }
 
@@ -709,18 +719,18 @@ slm_status slm_graph_lstm(int32_t L, int32_t T, int32_t B, int32_t H, int32_t I,
       int gid = (int)g->nodes.size();
       std::vector<int> pg{below};
       if (s_prev[l] >= 0) pg.push_back(s_prev[l]);
-      g->nodes.push_back({SLM_OP_LSTM_GATES, pg, (int64_t)B * 4 * H * 4, 0});
+      g->nodes.push_back({SLM_OP_LSTM_GATES, pg, (int64_t)B * 4 * H * 4, 0, l});
       int sid = (int)g->nodes.size();
       std::vector<int> ps{gid};
       if (s_prev[l] >= 0) ps.push_back(s_prev[l]);
-      g->nodes.push_back({SLM_OP_LSTM_CELL, ps, (int64_t)B * 2 * H * 4, 0});
+      g->nodes.push_back({SLM_OP_LSTM_CELL, ps, (int64_t)B * 2 * H * 4, 0, l});
       s_prev[l] = sid;
       below = sid;
     }
     heads.push_back((int)g->nodes.size());
-    g->nodes.push_back({SLM_OP_HEAD_CE, {below}, 4, SLM_NODE_NOT_CANDIDATE});
+    g->nodes.push_back({SLM_OP_HEAD_CE, {below}, 4, SLM_NODE_NOT_CANDIDATE, L});
   }
-  g->nodes.push_back({SLM_OP_SUM, heads, 4, SLM_NODE_NOT_CANDIDATE});
+  g->nodes.push_back({SLM_OP_SUM, heads, 4, SLM_NODE_NOT_CANDIDATE, L});
   g->outputs = {(int)g->nodes.size() - 1};
   g->kind = SLM_MODEL_LSTM;
   int d[5] = {L, T, B, H, I};

@@ -27,6 +27,7 @@ struct Node {
   std::vector<int> preds;
   int64_t out_bytes;
   int flags;
+  int group = 0;   // allocation group (SLM_ALLOC_GROUPED): the LSTM builder uses the layer
 };
 
 void set_error(const std::string& msg);

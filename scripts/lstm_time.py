@@ -12,7 +12,9 @@ L, T, B, H, I, C = 4, int(os.environ.get("T", 4096)), 64, 1024, 50, 5000
 dev = torch.device("cuda", 0)
 p, g, x, y = bench.lstm_inputs_dev(L, T, B, H, I, C, dev)
 graph = slm.Graph.lstm(L, T, B, H, I)
-plans = {"seg64": slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(64)), "none": slm.Plan(graph, "none")}
+AF = int(os.environ.get("ALLOC", 7))
+plans = {"seg64": slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(64), alloc_flags=AF),
+         "none": slm.Plan(graph, "none", alloc_flags=AF)}
 for optstr in sys.argv[1:] or ["lstm_streams=1"]:
     opts = dict(kv.split("=") for kv in optstr.split(","))
     model = slm.LstmModel(p, g, L, T, B, H, I, C, **{k: int(v) for k, v in opts.items()})

@@ -35,11 +35,12 @@ def _dev(inp, L, H, C):
     return p, g, torch.tensor(inp["x"]).cuda(), torch.tensor(inp["labels"]).cuda()
 
 
-def _run(slm, cfg, inp, strategy="none", m=None, **opt):
+def _run(slm, cfg, inp, strategy="none", m=None, alloc_flags=3, **opt):
     L, T, B, H, I, C = cfg
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, **opt)
-    plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "explicit" if m is not None else strategy, m=m)
+    plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "explicit" if m is not None else strategy, m=m,
+                    alloc_flags=alloc_flags)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         loss = model.step(plan, x, y, stream=s)
@@ -142,9 +143,9 @@ def test_lstm_wavefront_matches_single_stream(slm, cfg):
     ref_loss, ref, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
                             lstm_streams=0)
     for rep in range(4):
-        for pdl in (1, 0):
+        for pdl, af in ((1, 3), (0, 3), (1, 7)):
             loss, g, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
-                              lstm_streams=1, pdl=pdl)
-            assert loss == ref_loss, (rep, pdl)
+                              alloc_flags=af, lstm_streams=1, pdl=pdl)
+            assert loss == ref_loss, (rep, pdl, af)
             for k in ref:
-                assert np.array_equal(g[k], ref[k]), (rep, pdl, k)
+                assert np.array_equal(g[k], ref[k]), (rep, pdl, af, k)

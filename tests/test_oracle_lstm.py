@@ -86,15 +86,16 @@ def test_lstm_finite_differences():
 
 @pytest.mark.parametrize("plan_kind", ["none", "seg2", "seg3", "sqrt", "search"])
 @pytest.mark.parametrize("mode", ["f64", "bf16"])
-def test_lstm_plan_invariance_bitwise(plan_kind, mode):
+@pytest.mark.parametrize("flags", [P.A_INPLACE | P.A_SHARING, P.A_INPLACE | P.A_SHARING | P.A_GROUPED])
+def test_lstm_plan_invariance_bitwise(plan_kind, mode, flags):
     L, T, B, H, I, C = 2, 6, 3, 4, 3, 5
     Pm, inp = _params(L, T, B, H, I, C, dtype="bf16" if mode == "bf16" else "f32", seed=2)
     loss, g = OL.step_plain(Pm, inp["x"], inp["labels"], mode)
     gr = G.lstm_graph(L, T, B, H, Pm.kin(0))
     if plan_kind.startswith("seg"):
-        p = P.plan(gr, P.S_EXPLICIT, m=OL.time_segment_plan(gr, int(plan_kind[3:])))
+        p = P.plan(gr, P.S_EXPLICIT, m=OL.time_segment_plan(gr, int(plan_kind[3:])), alloc_flags=flags)
     else:
-        p = P.plan(gr, {"none": P.S_NONE, "sqrt": P.S_SQRT, "search": P.S_SEARCH}[plan_kind])
+        p = P.plan(gr, {"none": P.S_NONE, "sqrt": P.S_SQRT, "search": P.S_SEARCH}[plan_kind], alloc_flags=flags)
     l2, g2 = OL.step_planned(p, Pm, inp["x"], inp["labels"], mode)
     assert loss == l2
     assert np.array_equal(g["W_o"], g2["W_o"]) and np.array_equal(g["b_o"], g2["b_o"])
@@ -110,3 +111,19 @@ def test_lstm_time_segments_save_memory():
     none = P.plan(gr, P.S_NONE).alloc.exact_peak
     seg = P.plan(gr, P.S_EXPLICIT, m=OL.time_segment_plan(gr, 8)).alloc.exact_peak
     assert seg * 4 < none, (seg, none)
+
+
+def test_grouped_allocation_invariants():
+    """Reading A22: with A_GROUPED every tag is only ever used by nodes of one allocation group
+    (the LSTM layer, or the head); on a single-group graph it is the plain Fig. 2 allocator."""
+    gr = G.lstm_graph(3, 10, 4, 8, 3)
+    p = P.plan(gr, P.S_EXPLICIT, m=OL.time_segment_plan(gr, 3),
+               alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUPED)
+    users = {}
+    for v in p.gg.order:
+        users.setdefault(p.alloc.tag_of[v], set()).add(gr.nodes[p.gg.nodes[v].orig].group)
+    assert all(len(s) == 1 for s in users.values())
+    ch = G.chain_graph(40, 8, 64)
+    a = P.plan(ch, P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING).alloc
+    b = P.plan(ch, P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUPED).alloc
+    assert a.tag_of == b.tag_of and a.offsets == b.offsets

@@ -93,6 +93,13 @@ def test_lstm_graph_plan():
     assert_same_plan(g, P.S_EXPLICIT, m=m)
     assert_same_plan(g, P.S_SEARCH)
     assert_same_plan(g, P.S_NONE)
+    grouped = P.A_INPLACE | P.A_SHARING | P.A_GROUPED
+    assert_same_plan(g, P.S_EXPLICIT, m=m, alloc_flags=grouped)
+    assert_same_plan(g, P.S_SEARCH, alloc_flags=grouped)
+    assert_same_plan(g, P.S_SQRT, alloc_flags=grouped)
+    assert_same_plan(G.lstm_graph(4, 64, 64, 1024, 50), P.S_EXPLICIT,
+                     m=[1 if (nd.op in (G.LSTM_GATES, G.LSTM_CELL)) else 0 for nd in G.lstm_graph(4, 64, 64, 1024, 50).nodes],
+                     alloc_flags=grouped)
 
 
 @pytest.mark.parametrize("L,T,seg", [(2, 24, 5), (4, 64, 8), (1, 7, 1), (3, 10, 64)])
