@@ -190,7 +190,14 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
-  else if (k == "profile_ts") m->profile_ts = (int)value;
+  else if (k == "profile_ts") {
+    m->profile_ts = (int)value;
+    if (value <= 0) {   // detach the device-clock buffer: the caller may free it now
+      m->ts_buf = nullptr;
+      unsigned long long* z = nullptr;
+      CK(cudaMemcpyToSymbol(slmk::g_slm_ts, &z, sizeof(z)));
+    }
+  }
   else if (k == "profile_ts_buffer") {
     m->ts_buf = reinterpret_cast<void*>(value);
     unsigned long long* p = (unsigned long long*)m->ts_buf;
@@ -471,7 +478,7 @@ slm_status slm_debug_gemm(int kind, int impl, int bn, int split, int M, int N, i
   cudaStream_t st = (cudaStream_t)stream;
   using bf = __nv_bfloat16;
   if (impl == 0 || impl >= 2) {
-    const int dbg = impl == 2 ? 1 : (impl == 3 ? 2 : 0);   // 2: data movement only, 3: MMA only
+    const int dbg = (impl == 2 ? 1 : (impl == 3 ? 2 : 0)) | 4;   // 2: data movement only, 3: MMA only; 4: phase stamps
     const int cg = impl == 4 ? 2 : 1;                       // 4: CTA-pair (cta_group::2) tcgen05
     const uint32_t bbox = (uint32_t)(bn / cg);              // K-major B box rows
     CUtensorMap ma, mb;

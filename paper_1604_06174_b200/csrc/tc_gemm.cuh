@@ -263,7 +263,7 @@ struct TcCfg {
 };
 
 // debug instrumentation: per-CTA %globaltimer stamps at 8 phase points (null = off)
-// Two layouts: dbg >> 8 == 0: [cta][8 phases] (micro-benchmarks); dbg >> 8 == slot + 1: the
+// Two layouts: dbg bit 2 (debug hook only): [cta][8 phases] (micro-benchmarks); dbg >> 8 == slot + 1: the
 // launch's start (phase 0) and end (phase 7) per CTA at [slot][1024 CTAs][2] — used to time
 // every GEMM of a real step on the device clock (profile_ts option of the model).
 __device__ unsigned long long* g_slm_ts = nullptr;
@@ -272,6 +272,7 @@ __device__ __forceinline__ void ts_mark(int phase, int dbg) {
   if (p != nullptr && threadIdx.x == 0) {
     const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int slot = (dbg >> 8) - 1;
+    if (slot < 0 && !(dbg & 4)) return;   // per-CTA phase mode only from the debug hook (bit 2)
     if (slot >= 0 && phase != 0 && phase != 7) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
