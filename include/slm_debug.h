@@ -28,6 +28,10 @@ slm_status slm_debug_gemm(int kind, int impl, int bn, int split, int M, int N, i
 /* Per-CTA %globaltimer stamps (8 per CTA, phases of tc_gemm_kernel) written to dev_buf
  * (uint64, >= 8 * CTAs of the next launches); NULL switches the instrumentation off. */
 slm_status slm_debug_timestamps(void* dev_buf);
+/* Metadata of the GEMM launches stamped by the last step run with profile_ts (test hook):
+ * per slot the kernel kind (SLM_K_*) and an executor tag (LSTM: stream * 4 + {0 fwd, 1 mirror,
+ * 2 grad}); *n = number of stamped launches; cap = 0 queries n. */
+slm_status slm_debug_ts_meta(const slm_model* m, int32_t* kind, int32_t* aux, int32_t cap, int32_t* n);
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,7 @@ _sig("slm_plan_destroy", None, vp)
 _sig("slm_recursion_estimate", i32, i64, i64, i64p, i64p)
 _sig("slm_model_chain", i32, C.POINTER(ChainDesc), C.POINTER(vp))
 _sig("slm_model_lstm", i32, C.POINTER(LstmDesc), C.POINTER(vp))
+_sig("slm_debug_ts_meta", i32, vp, i32p, i32p, i32, i32p)
 _sig("slm_lstm_segment_mirrors", i32, vp, i32, i32p, i32)
 _sig("slm_model_destroy", None, vp)
 _sig("slm_model_set_option", i32, vp, C.c_char_p, i64)

@@ -204,8 +204,8 @@ struct GraphKey {
 struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
-  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG;   // pX / pG over layer l's partials
-  CUtensorMap woK, woMN, hopK, hopRK, hopRMN, dlRK, dlRMN, pL, pH;            // pL / pH over the head's
+  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm;   // partials of layer l's streams
+  CUtensorMap woK, woMN, hopK2[2], hopRK, hopRMN, dlRK, dlRMN, pL, pH;            // pL / pH over the head's
   const void* ws = nullptr;
 };
 struct slm_lstm_state {
@@ -256,6 +256,8 @@ struct slm_model {
   int profile_ts = 0;
   void* ts_buf = nullptr;
   std::vector<int> ts_kind;
+  std::vector<int> ts_aux;    // per slot: the LSTM stream of the launch (slm_debug_ts_meta)
+  int ts_cur_aux = 0;
   int ts_used = 0;
   // profile_events: (start, end, kind) per kernel, read by slm_model_kernel_times
   int profile = 0;

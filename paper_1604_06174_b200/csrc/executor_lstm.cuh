@@ -76,8 +76,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
                                   (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
   size_t off = 0;
-  L.hop = off;      off += al(B * H * 2);
-  for (int i = 0; i <= d.n_layers; ++i) {
+  L.hop = off;      off += 2 * al(B * H * 2);   // time-parity double buffer
+  for (int i = 0; i <= 2 * d.n_layers; ++i) {   // layers, head, mirror streams
     L.P.push_back(off);
     off += al(pbytes);
   }
@@ -90,7 +90,7 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
   L.dlR = off;      off += al(CH * B * Cp * 2);
   for (int l = 0; l < d.n_layers; ++l) {
     L.opL.push_back(off);
-    off += al(B * lstm_K(d, l) * 2);
+    off += 2 * al(B * lstm_K(d, l) * 2);   // time-parity double buffer
     L.opR.push_back(off);
     off += al(CH * B * lstm_K(d, l) * 2);
     L.dpR.push_back(off);
@@ -117,29 +117,38 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   const int nl = d.n_layers;
   M.wK.resize(nl);
   M.wMN.resize(nl);
-  M.opK.resize(nl);
+  M.opK.resize(2 * nl);
   M.opRMN.resize(nl);
   M.dpRK.resize(nl);
   M.dpRMN.resize(nl);
   M.pX.resize(nl);
   M.pG.resize(nl);
+  M.pGm.resize(nl);
   M.opRK.resize(nl);
   slm_status st;
   for (int l = 0; l < nl; ++l) {
     const uint64_t K = lstm_K(d, l);
     if ((st = make_map(&M.wK[l], W + lstm_w_offset(d, l), K, 4 * H, 128)) != SLM_OK) return st;
     if ((st = make_map(&M.wMN[l], W + lstm_w_offset(d, l), K, 4 * H, 64)) != SLM_OK) return st;
-    if ((st = make_map(&M.opK[l], w + L.opL[l], K, B, (uint32_t)B)) != SLM_OK) return st;
+    for (int par = 0; par < 2; ++par)
+      if ((st = make_map(&M.opK[2 * l + par], w + L.opL[l] + par * ((B * K * 2 + 255) / 256 * 256), K, B,
+                         (uint32_t)B)) != SLM_OK)
+        return st;
     if ((st = make_map(&M.opRK[l], w + L.opR[l], K, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pX[l], w + L.P[l], K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pG[l], w + L.P[l], 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK) return st;
+    if ((st = make_map_f32(&M.pGm[l], w + L.P[nl + 1 + l], 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK)
+      return st;
   }
   if ((st = make_map(&M.woK, d.W_o, H, Cp, 128)) != SLM_OK) return st;
   if ((st = make_map(&M.woMN, d.W_o, H, Cp, 64)) != SLM_OK) return st;
-  if ((st = make_map(&M.hopK, w + L.hop, H, B, (uint32_t)B)) != SLM_OK) return st;
+  for (int par = 0; par < 2; ++par)
+    if ((st = make_map(&M.hopK2[par], w + L.hop + par * ((B * H * 2 + 255) / 256 * 256), H, B, (uint32_t)B)) !=
+        SLM_OK)
+      return st;
   if ((st = make_map(&M.hopRK, w + L.hopR, H, CH * B, (uint32_t)B)) != SLM_OK) return st;
   if ((st = make_map(&M.hopRMN, w + L.hopR, H, CH * B, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRK, w + L.dlR, Cp, CH * B, (uint32_t)B)) != SLM_OK) return st;
@@ -159,23 +168,27 @@ struct LstmNode {
 // their h (and, at layer 0, the next input) straight into the operands of their consumers;
 // a gates / head node re-packs only when its operand does not already hold its inputs.
 // kZeros marks the all-zero h of t = 0.  Used identically by enqueue_lstm and lstm_launches.
+// Operands are double-buffered by time parity (G^l_t reads buffer t % 2), so a producer for
+// step t+1 never waits for the consumer of step t.
 struct OperandTracker {
   static constexpr int kZeros = -2;
-  std::vector<int> wx, wh;
-  int whead = -1;
-  explicit OperandTracker(int L) : wx(L, -1), wh(L, -1) {}
-  bool gates_needs_pack(int l, int xnode, int hnode) const { return wx[l] != xnode || wh[l] != hnode; }
-  void packed(int l, int xnode, int hnode) {
-    wx[l] = xnode;
-    wh[l] = hnode;
+  std::vector<int> wx, wh;   // [2 l + parity]
+  int whead[2] = {-1, -1};
+  explicit OperandTracker(int L) : wx(2 * L, -1), wh(2 * L, -1) {}
+  bool gates_needs_pack(int l, int t, int xnode, int hnode) const {
+    return wx[2 * l + t % 2] != xnode || wh[2 * l + t % 2] != hnode;
   }
-  // cell state node u = S^l_t produced: h -> layer l's h half (t+1 < T), layer l+1's x half
-  // or the head operand; layer 0 also writes x_{t+1} (Input node xnext_node)
+  void packed(int l, int t, int xnode, int hnode) {
+    wx[2 * l + t % 2] = xnode;
+    wh[2 * l + t % 2] = hnode;
+  }
+  // cell state node u = S^l_t produced: h -> layer l's h half for t+1, layer l+1's x half
+  // (step t) or the head operand (step t); layer 0 also writes x_{t+1} (Input node xnext_node)
   void cell(int u, int l, int t, int L, int T, int xnext_node) {
-    if (t + 1 < T) wh[l] = u;
-    if (l + 1 < L) wx[l + 1] = u;
-    else whead = u;
-    if (l == 0 && t + 1 < T) wx[0] = xnext_node;
+    if (t + 1 < T) wh[2 * l + (t + 1) % 2] = u;
+    if (l + 1 < L) wx[2 * (l + 1) + t % 2] = u;
+    else whead[t % 2] = u;
+    if (l == 0 && t + 1 < T) wx[(t + 1) % 2] = xnext_node;
   }
 };
 
@@ -187,10 +200,14 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   slm_lstm_state& S = m.lst;
   const bool pdl = m.pdl != 0;
   int ts_slot = 0;
-  if (m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) m.ts_kind.resize(m.profile_ts);
+  if (m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) {
+    m.ts_kind.resize(m.profile_ts);
+    m.ts_aux.resize(m.profile_ts);
+  }
   auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock GEMM timing
     if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
     m.ts_kind[ts_slot] = kind;
+    m.ts_aux[ts_slot] = m.ts_cur_aux;
     return (++ts_slot) << 8;
   };
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
@@ -198,7 +215,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const LstmWs W = lstm_ws_layout(d, m.lstm_sk);
   const LstmSplits sp = lstm_splits(d, m.lstm_sk);
   uint8_t* w = (uint8_t*)ws;
-  bf* hop = (bf*)(w + W.hop);
+  auto hopb = [&](int par) { return (bf*)(w + W.hop + par * (((size_t)B * H * 2 + 255) / 256 * 256)); };
   auto Pb = [&](int i) { return (const float*)(w + W.P[i]); };   // split-K partials of stream i
   float* logits = (float*)(w + W.logits);
   float* dlog_f = (float*)(w + W.dlog_f);
@@ -255,21 +272,23 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
 
   OperandTracker trk(L);
-  auto opl = [&](int l) { return (bf*)(w + W.opL[l]); };
+  auto opl = [&](int l, int par) {
+    return (bf*)(w + W.opL[l] + par * (((size_t)B * lstm_K(d, l) * 2 + 255) / 256 * 256));
+  };
   // the operand side outputs of the kernel producing S^l_t (V' node u)
   auto op_out = [&](int u, int l, int t) {
     slmk::OpOut o{};
     if (t + 1 < T) {
-      o.h_self = opl(l) + (l == 0 ? K0 : H);
+      o.h_self = opl(l, (t + 1) % 2) + (l == 0 ? K0 : H);
       o.ld_self = lstm_K(d, l);
     }
-    o.h_up = l + 1 < L ? opl(l + 1) : hop;
+    o.h_up = l + 1 < L ? opl(l + 1, t % 2) : hopb(t % 2);
     o.ld_up = l + 1 < L ? lstm_K(d, l + 1) : H;
     if (l == 0 && t + 1 < T) {
       o.xnext = (const float*)((const uint8_t*)xin + (size_t)(t + 1) * B * I * 4);
       o.I = I;
       o.Kin0 = K0;
-      o.x0 = opl(0);
+      o.x0 = opl(0, (t + 1) % 2);
       o.ld0 = lstm_K(d, 0);
     }
     trk.cell(u, l, t, L, T, (t + 1) * per_t);
@@ -285,12 +304,15 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   // live in a per-stream ring large enough to hold a step's units; a re-recorded slot only
   // makes a (very old) wait more conservative, never wrong.
   const bool msm = m.lstm_streams != 0 && st != nullptr;
-  const int NSTR = L + 1;
+  // lstm_streams = 2: re-computed (mirror) units get streams of their own (L+1+l), so the
+  // recompute of segment j-1 can overlap the backward of segment j
+  const int NSTR = m.lstm_streams >= 2 ? 2 * L + 1 : L + 1;
   constexpr int kRing = 16384;
   const int ntag = (int)p->tag_size.size();
-  auto OPX = [&](int l) { return ntag + 2 * l; };
-  auto OPH = [&](int l) { return ntag + 2 * l + 1; };
-  const int HOP = ntag + 2 * L;
+  auto OPX = [&](int l, int par) { return ntag + 4 * l + par; };
+  auto OPH = [&](int l, int par) { return ntag + 4 * l + 2 + par; };
+  auto HOPR = [&](int par) { return ntag + 4 * L + par; };
+  const int HOP = ntag + 4 * L + 1;   // the highest resource id
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -358,7 +380,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     const int t = ni.t, l = ni.l;
     if (opk == SLM_OP_INPUT) continue;
     // ---- the launch unit: this node, plus the next one when the two are fused
-    const int sid = (opk == SLM_OP_LSTM_GATES || opk == SLM_OP_LSTM_CELL) ? l : L;
+    const bool lay = opk == SLM_OP_LSTM_GATES || opk == SLM_OP_LSTM_CELL;
+    const int sid = !lay ? L : (kind == SLM_KIND_MIRROR && NSTR > L + 1 ? L + 1 + l : l);
     int partner = -1;
     if (oi + 1 < order.size()) {
       const int u = order[oi + 1];
@@ -379,29 +402,30 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       wr.push_back(p->node_tag[node]);
     }
     auto cell_writes = [&]() {
-      if (t + 1 < T) wr.push_back(OPH(l));
-      wr.push_back(l + 1 < L ? OPX(l + 1) : HOP);
-      if (l == 0 && t + 1 < T) wr.push_back(OPX(0));
+      if (t + 1 < T) wr.push_back(OPH(l, (t + 1) % 2));
+      wr.push_back(l + 1 < L ? OPX(l + 1, t % 2) : HOPR(t % 2));
+      if (l == 0 && t + 1 < T) wr.push_back(OPX(0, (t + 1) % 2));
     };
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
         const int hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, pp.first[0], hn)) {
-          wr.push_back(OPX(l));
-          wr.push_back(OPH(l));
+        if (trk.gates_needs_pack(l, t, pp.first[0], hn)) {
+          wr.push_back(OPX(l, t % 2));
+          wr.push_back(OPH(l, t % 2));
         } else {
-          rd.push_back(OPX(l));
-          rd.push_back(OPH(l));
+          rd.push_back(OPX(l, t % 2));
+          rd.push_back(OPH(l, t % 2));
         }
         if (partner >= 0) cell_writes();
       } else if (opk == SLM_OP_LSTM_CELL) {
         cell_writes();
       } else if (opk == SLM_OP_HEAD_CE) {
-        (trk.whead != pp.first[0] ? wr : rd).push_back(HOP);
+        (trk.whead[t % 2] != pp.first[0] ? wr : rd).push_back(HOPR(t % 2));
       }
     }
     cudaStream_t cs = st;
     if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
+    m.ts_cur_aux = sid * 4 + (kind == SLM_KIND_GRAD ? 2 : kind == SLM_KIND_MIRROR ? 1 : 0);
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
         const bool lower_state = l > 0;
@@ -409,15 +433,17 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const float* sprev = pp.second > 1 ? V(pp.first[1]) : nullptr;
         const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
         const int xn = pp.first[0], hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, xn, hn)) {
+        if (trk.gates_needs_pack(l, t, xn, hn)) {
           CK(launch_k(lstm_pack_kernel, eg, eb, 0, cs, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
-                      H, B, opl(l)));
-          trk.packed(l, xn, hn);
+                      H, B, opl(l, t % 2)));
+          trk.packed(l, t, xn, hn);
           ++nl;
         }
         slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[l], 4 * H, B, Kin + H, 0, 0,
-                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pG[l])) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[2 * l + t % 2], 4 * H, B,
+                                                                       Kin + H, 0, 0,
+                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD),
+                                                                       sid > L ? &M.pGm[l] : &M.pG[l])) != SLM_OK)
           return s;
         // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
         float* s_out = nullptr;
@@ -441,13 +467,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                     (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        if (trk.whead != pp.first[0]) {
-          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]), H, B, hop));
-          trk.whead = pp.first[0];
+        if (trk.whead[t % 2] != pp.first[0]) {
+          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]), H, B, hopb(t % 2)));
+          trk.whead[t % 2] = pp.first[0];
           ++nl;
         }
         slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK, Cp, B, H, 0, 0, e, cs,
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK2[t % 2], Cp, B, H, 0, 0, e, cs,
                                                                        pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
           return s;
         CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
@@ -614,9 +640,9 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
         const int xn = pr[0], hn = np > 1 ? pr[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, xn, hn)) {
+        if (trk.gates_needs_pack(l, t, xn, hn)) {
           ++nl;
-          trk.packed(l, xn, hn);
+          trk.packed(l, t, xn, hn);
         }
         nl += 2;
         if (oi + 1 < order.size()) {
@@ -630,9 +656,9 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
         trk.cell(v, l, t, L, T, (t + 1) * per_t);
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        if (trk.whead != pr[0]) {
+        if (trk.whead[t % 2] != pr[0]) {
           ++nl;
-          trk.whead = pr[0];
+          trk.whead[t % 2] = pr[0];
         }
         nl += 2;
       } else {

@@ -465,6 +465,17 @@ void slm_comm_destroy(slm_comm* c) {
 }
 
 // ---------------------------------------------------------------- test hooks
+slm_status slm_debug_ts_meta(const slm_model* m, int32_t* kind, int32_t* aux, int32_t cap, int32_t* n) {
+  if (!m || !n) return SLM_E_ARG;
+  *n = m->ts_used;
+  if (cap < m->ts_used) return cap == 0 ? SLM_OK : SLM_E_BUFFER_TOO_SMALL;
+  for (int i = 0; i < m->ts_used; ++i) {
+    if (kind) kind[i] = m->ts_kind[i];
+    if (aux) aux[i] = i < (int)m->ts_aux.size() ? m->ts_aux[i] : 0;
+  }
+  return SLM_OK;
+}
+
 slm_status slm_debug_timestamps(void* dev_buf) {
   unsigned long long* p = (unsigned long long*)dev_buf;
   CK(cudaMemcpyToSymbol(slmk::g_slm_ts, &p, sizeof(p)));

@@ -143,9 +143,9 @@ def test_lstm_wavefront_matches_single_stream(slm, cfg):
     ref_loss, ref, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
                             lstm_streams=0)
     for rep in range(4):
-        for pdl, af in ((1, 3), (0, 3), (1, 7)):
+        for pdl, af, ns in ((1, 3, 1), (0, 3, 1), (1, 7, 1), (1, 7, 2), (0, 3, 2)):
             loss, g, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
-                              alloc_flags=af, lstm_streams=1, pdl=pdl)
+                              alloc_flags=af, lstm_streams=ns, pdl=pdl)
             assert loss == ref_loss, (rep, pdl, af)
             for k in ref:
                 assert np.array_equal(g[k], ref[k]), (rep, pdl, af, k)
