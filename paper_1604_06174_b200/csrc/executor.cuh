@@ -61,7 +61,7 @@ enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
 
 template <int BN, bool AMN, bool BMN, bool PRE, class Epi, int CG = 1>
 slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int M, int N, int K, int split,
-                     int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg) {
+                     int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg, int pf_row0 = -1) {
   using C = slmk::TcCfg<BN, AMN, BMN, CG>;
   auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi, CG>;
   static bool attr = false;
@@ -74,7 +74,7 @@ slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
     return SLM_E_UNSUPPORTED;
   }
   CK(launch_kc(kern, dim3(M / 128, N / BN, split), dim3(128), C::SMEM, st, pdl, CG, a, b, c, K, a_row0, b_row0, epi,
-               dbg));
+               dbg, pf_row0));
   return SLM_OK;
 }
 
@@ -83,23 +83,25 @@ slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
 template <class Epi, bool AMN, bool BMN, bool PRE>
 slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                         int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg = 0,
-                        const CUtensorMap* c = nullptr, int cg = 1) {
+                        const CUtensorMap* c = nullptr, int cg = 1, int pf = -1) {
   const CUtensorMap& cm = c ? *c : a;
   if (cg == 2) {
     switch (bn) {
-      case 128: return launch_tc<128, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
-      case 256: return launch_tc<256, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+      case 128:
+        return launch_tc<128, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+      case 256:
+        return launch_tc<256, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
     }
     set_error("unsupported CTA-pair GEMM N tile " + std::to_string(bn));
     return SLM_E_UNSUPPORTED;
   }
   switch (bn) {
     case 32:
-      if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+      if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
       break;
-    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
-    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
-    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg);
+    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
   }
   set_error("unsupported GEMM N tile " + std::to_string(bn));
   return SLM_E_UNSUPPORTED;
@@ -242,6 +244,7 @@ struct slm_model {
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
   int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
+  int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
   int lstm_sk = 2;                            // LSTM: split-K of the gates GEMMs (0 = auto; 2 measured best with the wavefront)
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
@@ -544,9 +547,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       if (fz) {
         slmk::EpiPartialTma epi{B};
         pbeg(st);
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(fused_n(m), L.sk_fwd, m.mW_K, m.mA_K, d, B, d,
-                                                                       l * d, 0, epi, st, pdl, gdbg(SLM_K_GEMM_FWD),
-                                                                       &m.mP, m.cta_pair ? 2 : 1)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(
+                 fused_n(m), L.sk_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0, epi, st, pdl, gdbg(SLM_K_GEMM_FWD), &m.mP,
+                 m.cta_pair ? 2 : 1, m.l2_prefetch && l + 1 < n ? (l + 1) * d : -1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_FWD, st);
         // finalize x_{l+1} and produce a_{l+1} for the next Block (BN of layer l+1)
@@ -606,9 +609,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         // dX: P[s] = g_{l+1} W_l over K slice s
         slmk::EpiPartialTma e1{B};
         pbeg(st);
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(fused_n(m), L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B,
-                                                                      d, l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX),
-                                                                      &m.mP, m.cta_pair ? 2 : 1)) != SLM_OK)
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(
+                 fused_n(m), L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d, l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX), &m.mP,
+                 m.cta_pair ? 2 : 1, m.l2_prefetch && l > 0 ? (l - 1) * d : -1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX, st);
         // bn_bwd(k) overwrites gq[(k+1)%3] and ab[k%2], last read by dW of backward k-2

@@ -61,6 +61,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// bulk prefetch of one tensor-map box into L2 (no smem, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -301,7 +307,8 @@ __device__ __forceinline__ void ts_mark(int phase, int dbg) {
 template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi, int CG = 1>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg) {
+                   const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg,
+                   int pf_row0) {
   ts_mark(0, dbg);
   using C = TcCfg<BN, A_MN, B_MN, CG>;
   uint32_t rank = 0;
@@ -350,6 +357,19 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   ts_mark(1, dbg);
+  // pf_row0 >= 0: pull this CTA's A tile of the NEXT GEMM of the chain (the next layer's
+  // weights, rows a_row0 -> pf_row0) into L2 while this one runs
+  if (pf_row0 >= 0 && warp == 2 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int k0 = kbase + kb * C::BK;
+      if (A_MN) {
+        tma_prefetch_l2(&tmA, m0, pf_row0 + k0);
+        tma_prefetch_l2(&tmA, m0 + 64, pf_row0 + k0);
+      } else {
+        tma_prefetch_l2(&tmA, k0, pf_row0 + m0);
+      }
+    }
+  }
 
   auto tma = [&](void* dst, const CUtensorMap* map, int s, int c0, int c1) {
     if constexpr (CG == 2)

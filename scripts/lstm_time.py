@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_1604_06174_b200 as slm  # noqa: E402
 
-L, T, B, H, I, C = 4, int(os.environ.get("T", 4096)), 64, 1024, 50, 5000
+L, T, B, H, I, C = 4, int(os.environ.get("T", 4096)), 64, 1024, 50, int(os.environ.get("C", 5000))
 dev = torch.device("cuda", 0)
 p, g, x, y = bench.lstm_inputs_dev(L, T, B, H, I, C, dev)
 graph = slm.Graph.lstm(L, T, B, H, I)
