@@ -29,7 +29,7 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, total;
+  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
   std::vector<size_t> opL, opR, dpR, dpF;   // per layer: forward operand [B][K_l], backward rings
 };
@@ -87,6 +87,9 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
   L.offs = off;     off += al(T * 8);
   L.cnt = off;      off += 256;
   L.hopR = off;     off += al(CH * B * H * 2);
+  L.hf = off;       off += 2 * al(CH * B * H * 2);   // forward head operands, chunk-parity double buffer
+  L.logitsF = off;  off += al(CH * B * Cp * 4);
+  L.rowlossF = off; off += al(CH * B * 4);
   L.dlR = off;      off += al(CH * B * Cp * 2);
   for (int l = 0; l < d.n_layers; ++l) {
     L.opL.push_back(off);
@@ -150,6 +153,11 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
         SLM_OK)
       return st;
   if ((st = make_map(&M.hopRK, w + L.hopR, H, CH * B, (uint32_t)B)) != SLM_OK) return st;
+  for (int par = 0; par < 2; ++par)
+    for (int bi = 0; bi < 2; ++bi)
+      if ((st = make_map(&M.hfK[par][bi], w + L.hf + par * ((CH * B * H * 2 + 255) / 256 * 256), H, CH * B,
+                         bi ? 256u : 64u)) != SLM_OK)
+        return st;
   if ((st = make_map(&M.hopRMN, w + L.hopR, H, CH * B, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRK, w + L.dlR, Cp, CH * B, (uint32_t)B)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRMN, w + L.dlR, Cp, CH * B, 64)) != SLM_OK) return st;
@@ -275,14 +283,19 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto opl = [&](int l, int par) {
     return (bf*)(w + W.opL[l] + par * (((size_t)B * lstm_K(d, l) * 2 + 255) / 256 * 256));
   };
-  // the operand side outputs of the kernel producing S^l_t (V' node u)
-  auto op_out = [&](int u, int l, int t) {
+  // forward head operands: a ring of CH steps per chunk parity, consumed by one batched head
+  auto hfb = [&](int t) {
+    return (bf*)(w + W.hf + ((t / CH) % 2) * (((size_t)CH * B * H * 2 + 255) / 256 * 256)) + (size_t)(t % CH) * B * H;
+  };
+  // the operand side outputs of the kernel producing S^l_t (V' node u); the top layer's h
+  // goes to the forward head ring only for forward (not re-computed) states
+  auto op_out = [&](int u, int l, int t, int knd) {
     slmk::OpOut o{};
     if (t + 1 < T) {
       o.h_self = opl(l, (t + 1) % 2) + (l == 0 ? K0 : H);
       o.ld_self = lstm_K(d, l);
     }
-    o.h_up = l + 1 < L ? opl(l + 1, t % 2) : hopb(t % 2);
+    o.h_up = l + 1 < L ? opl(l + 1, t % 2) : (knd == SLM_KIND_FWD ? hfb(t) : nullptr);
     o.ld_up = l + 1 < L ? lstm_K(d, l + 1) : H;
     if (l == 0 && t + 1 < T) {
       o.xnext = (const float*)((const uint8_t*)xin + (size_t)(t + 1) * B * I * 4);
@@ -311,7 +324,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const int ntag = (int)p->tag_size.size();
   auto OPX = [&](int l, int par) { return ntag + 4 * l + par; };
   auto OPH = [&](int l, int par) { return ntag + 4 * l + 2 + par; };
-  auto HOPR = [&](int par) { return ntag + 4 * L + par; };
+  auto HFR = [&](int par) { return ntag + 4 * L + par; };   // forward head ring, chunk parity
   const int HOP = ntag + 4 * L + 1;   // the highest resource id
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
@@ -403,7 +416,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     }
     auto cell_writes = [&]() {
       if (t + 1 < T) wr.push_back(OPH(l, (t + 1) % 2));
-      wr.push_back(l + 1 < L ? OPX(l + 1, t % 2) : HOPR(t % 2));
+      if (l + 1 < L) wr.push_back(OPX(l + 1, t % 2));
+      else if (kind == SLM_KIND_FWD) wr.push_back(HFR((t / CH) % 2));
       if (l == 0 && t + 1 < T) wr.push_back(OPX(0, (t + 1) % 2));
     };
     if (kind != SLM_KIND_GRAD) {
@@ -420,7 +434,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       } else if (opk == SLM_OP_LSTM_CELL) {
         cell_writes();
       } else if (opk == SLM_OP_HEAD_CE) {
-        (trk.whead[t % 2] != pp.first[0] ? wr : rd).push_back(HOPR(t % 2));
+        // one batched unit per chunk of forward heads, at the chunk's last step
+        wr.clear();
+        rd.clear();
+        if (t % CH == CH - 1 || t == T - 1) {
+          rd.push_back(HFR((t / CH) % 2));
+          for (int t2 = t - t % CH; t2 <= t; ++t2) wr.push_back(p->node_tag[t2 * per_t + per_t - 1]);
+        }
       }
     }
     cudaStream_t cs = st;
@@ -455,7 +475,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu.first[0] == v) {
             s_out = V(u);
             s_prev = pu.second > 1 ? V(pu.first[1]) : nullptr;
-            oo = op_out(u, l, t);
+            oo = op_out(u, l, t, kind);
             ++oi;
           }
         }
@@ -464,21 +484,28 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         nl += 2;
       } else if (opk == SLM_OP_LSTM_CELL) {
         CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]),
-                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t)));
+                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t, kind)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        if (trk.whead[t % 2] != pp.first[0]) {
-          CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]), H, B, hopb(t % 2)));
-          trk.whead[t % 2] = pp.first[0];
-          ++nl;
+        // batched forward heads of steps t0..t (the chunk ends here): logits for n*B rows in one
+        // GEMM, the softmax-CE rows, then the per-step losses into the H_t tags
+        if (t % CH == CH - 1 || t == T - 1) {
+          const int t0 = t - t % CH, n = t - t0 + 1, N = n * B, bi = N % 256 == 0 ? 1 : 0;
+          float* lgF = (float*)(w + W.logitsF);
+          float* rlF = (float*)(w + W.rowlossF);
+          slmk::EpiStoreF32 e{lgF, Cp};
+          if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bi ? 256 : 64, 1, M.woK, M.hfK[(t / CH) % 2][bi],
+                                                                       Cp, N, H, 0, 0, e, cs, pdl,
+                                                                       gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+            return s;
+          CK(launch_k(lstm_head_ce_kernel, dim3(N), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
+                      labels + (size_t)t0 * B, C, Cp, N, scale, rlF, (bf*)nullptr, (float*)nullptr, (unsigned*)nullptr,
+                      (float*)nullptr));
+          slmk::StepOut so{};
+          for (int i = 0; i < n; ++i) so.p[i] = V((t0 + i) * per_t + per_t - 1);
+          CK(launch_k(lstm_step_loss_kernel, dim3(n), dim3(1024), 0, cs, pdl, (const float*)rlF, B, scale, so));
+          nl += 3;
         }
-        slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopK2[t % 2], Cp, B, H, 0, 0, e, cs,
-                                                                       pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
-                    labels + (size_t)t * B, C, Cp, B, scale, rowloss, (bf*)nullptr, (float*)nullptr, cnt, V(v)));
-        nl += 2;
       } else if (opk == SLM_OP_SUM) {
         CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
         ++nl;
@@ -656,11 +683,7 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
         trk.cell(v, l, t, L, T, (t + 1) * per_t);
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        if (trk.whead[t % 2] != pr[0]) {
-          ++nl;
-          trk.whead[t % 2] = pr[0];
-        }
-        nl += 2;
+        if (t % kLstmChunk == kLstmChunk - 1 || t == T - 1) nl += 3;   // batched forward heads
       } else {
         ++nl;
       }

@@ -390,6 +390,21 @@ __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restr
   }
 }
 
+// Per-step losses of a batch of head steps: block i writes *out.p[i] = sum_b rowloss[i B + b] *
+// scale (block_reduce_sum order, 1024 threads).
+struct StepOut {
+  float* p[32];
+};
+__global__ void __launch_bounds__(1024) lstm_step_loss_kernel(const float* __restrict__ rowloss, int B, float scale,
+                                                              StepOut out) {
+  __shared__ float sh[32];
+  lstm_entry();
+  float t = 0.f;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) t = __fadd_rn(t, rowloss[(size_t)blockIdx.x * B + b]);
+  t = block_reduce_sum(t, sh);
+  if (threadIdx.x == 0) *out.p[blockIdx.x] = __fmul_rn(t, scale);
+}
+
 // out = sum_b rowloss[b] * scale (single block, fixed order)
 __global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restrict__ rowloss, int B, float scale,
                                                           float* __restrict__ out) {

@@ -107,12 +107,13 @@ def test_lstm_launch_count(slm):
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, use_graph=0)
     plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "none")
-    # forward: per t, per layer GEMM + fused gates/cell, head GEMM + CE (row sum fused); the
-    # operands are packed only at t = 0 (afterwards the cell kernels write them); Sum 1.
+    # forward: per t, per layer GEMM + fused gates/cell; the operands are packed only at t = 0
+    # (afterwards the cell kernels write them); the heads run batched per 32-step chunk
+    # (logits GEMM, CE rows, per-step losses); Sum 1.
     # backward: fill 1; per t head 5 (pack, logits GEMM, CE, dh GEMM, dh + db_o), per layer 3
     # (fused cell / d_pre / pack, dX GEMM, scatter); per 32-step chunk one weight-gradient GEMM
     # + db column sum per layer and one GEMM for the head (T = 4: one chunk)
-    assert model.launches(plan) == T * (2 * L + 2) + L + 1 + 1 + T * (5 + 3 * L) + (2 * L + 1)
+    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + T * (5 + 3 * L) + (2 * L + 1)
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
