@@ -29,7 +29,7 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, total;
+  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, dhR, PH, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
   std::vector<size_t> opL, opR, dpR, dpF;   // per layer: forward operand [B][K_l], backward rings
 };
@@ -52,8 +52,16 @@ struct LstmSplits {
 LstmSplits lstm_splits(const slm_lstm_desc& d, int gates_sk = 0) {
   const int H = d.hidden, Cp = lstm_cpad(d.n_classes);
   const int K0 = lstm_K(d, 0), K1 = 2 * H;
+  // head: logits without split-K, dh with at most 4 K slices -- the per-step and the batched
+  // (32-step) head backward use the same K slicing, so their values are bit-identical
+  auto upto = [](int K, int q) {
+    int b = 1;
+    for (int x = 1; x <= q; ++x)
+      if ((K / 64) % x == 0) b = x;
+    return b;
+  };
   LstmSplits s{lstm_sk(4 * H / 128, K0), lstm_sk(4 * H / 128, K1), lstm_sk(K0 / 128, 4 * H), lstm_sk(K1 / 128, 4 * H),
-               lstm_sk(Cp / 128, H), lstm_sk(H / 128, Cp)};
+               1, upto(Cp, 4)};
   if (gates_sk > 0) {   // the largest divisor of K/64 not above the request
     auto fit = [&](int K) {
       int b = 1;
@@ -82,7 +90,7 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
     off += al(pbytes);
   }
   L.logits = off;   off += al(B * Cp * 4);
-  L.dlog_f = off;   off += al(B * Cp * 4);
+  L.dlog_f = off;   off += al(CH * B * Cp * 4);
   L.rowloss = off;  off += al(B * 4);
   L.offs = off;     off += al(T * 8);
   L.cnt = off;      off += 256;
@@ -90,6 +98,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
   L.hf = off;       off += 2 * al(CH * B * H * 2);   // forward head operands, chunk-parity double buffer
   L.logitsF = off;  off += al(CH * B * Cp * 4);
   L.rowlossF = off; off += al(CH * B * 4);
+  L.dhR = off;      off += 2 * al(CH * B * 2 * H * 4);          // (dh | 0) of batched head steps, chunk parity
+  L.PH = off;       off += al((size_t)sp.hd * CH * B * H * 4);  // split-K partials of the batched dh GEMM
   L.dlR = off;      off += al(CH * B * Cp * 2);
   for (int l = 0; l < d.n_layers; ++l) {
     L.opL.push_back(off);
@@ -158,6 +168,11 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
       if ((st = make_map(&M.hfK[par][bi], w + L.hf + par * ((CH * B * H * 2 + 255) / 256 * 256), H, CH * B,
                          bi ? 256u : 64u)) != SLM_OK)
         return st;
+  for (int bi = 0; bi < 3; ++bi) {   // batched head backward: N tiles 64 / 128 / 256
+    if ((st = make_map(&M.hopRKb[bi], w + L.hopR, H, CH * B, 64u << bi)) != SLM_OK) return st;
+    if ((st = make_map(&M.dlRKb[bi], w + L.dlR, Cp, CH * B, 64u << bi)) != SLM_OK) return st;
+  }
+  if ((st = make_map_f32(&M.pHB, w + L.PH, H, (uint64_t)sp.hd * CH * B)) != SLM_OK) return st;
   if ((st = make_map(&M.hopRMN, w + L.hopR, H, CH * B, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRK, w + L.dlR, Cp, CH * B, (uint32_t)B)) != SLM_OK) return st;
   if ((st = make_map(&M.dlRMN, w + L.dlR, Cp, CH * B, 64)) != SLM_OK) return st;
@@ -324,8 +339,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const int ntag = (int)p->tag_size.size();
   auto OPX = [&](int l, int par) { return ntag + 4 * l + par; };
   auto OPH = [&](int l, int par) { return ntag + 4 * l + 2 + par; };
-  auto HFR = [&](int par) { return ntag + 4 * L + par; };   // forward head ring, chunk parity
-  const int HOP = ntag + 4 * L + 1;   // the highest resource id
+  auto HFR = [&](int par) { return ntag + 4 * L + par; };       // forward head ring, chunk parity
+  auto DHR = [&](int par) { return ntag + 4 * L + 2 + par; };   // batched (dh | 0) ring, chunk parity
+  const int HOP = ntag + 4 * L + 3;   // the highest resource id
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -382,6 +398,30 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       for (int i = 0; i < NSTR; ++i) res_r[(size_t)r * NSTR + i] = -1;
     }
     return SLM_OK;
+  };
+
+  // which V' node's value each pool tag holds (host view of V' order), for the batched head
+  // backward: a chunk of g[H_t] runs as one unit when every a[S^{L-1}_t] it reads is resident
+  std::vector<int> owner(p->tag_size.size(), -1);
+  std::vector<char> hb_batched(T, 0);
+  auto dh_ring = [&](int t) {
+    return (float*)(w + W.dhR + ((t / CH) % 2) * (((size_t)CH * B * 2 * H * 4 + 255) / 256 * 256)) +
+           (size_t)(t % CH) * B * 2 * H;
+  };
+  auto head_state = [&](int t) {   // the V' node a[S^{L-1}_t] the head gradient of step t reads
+    const int gh = p->gnode[t * per_t + per_t - 1];
+    if (gh < 0) return -1;
+    return p->preds[p->pred_ptr[gh + 1] - 1];
+  };
+  // the lowest step t_lo >= the chunk start such that every head input of t_lo..t is resident
+  auto ready_from = [&](int t) {
+    int lo = t + 1;
+    for (int t2 = t; t2 >= t - t % CH; --t2) {
+      const int a = head_state(t2);
+      if (a < 0 || owner[p->node_tag[a]] != a) break;
+      lo = t2;
+    }
+    return lo;
   };
 
   const std::vector<int>& order = p->order;
@@ -443,6 +483,21 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         }
       }
     }
+    bool hb_now = false;   // this g[H_t] runs the batched head backward of steps hb_lo..t
+    int hb_lo = t;
+    if (kind == SLM_KIND_GRAD && opk == SLM_OP_HEAD_CE && !hb_batched[t]) {
+      hb_lo = ready_from(t);
+      if (hb_lo < t) {
+        hb_now = true;
+        rd.clear();
+        wr.clear();
+        for (int t2 = hb_lo; t2 <= t; ++t2) rd.push_back(p->node_tag[head_state(t2)]);
+        wr.push_back(DHR((t / CH) % 2));
+      }
+    }
+    if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL && l == L - 1 && hb_batched[t]) rd.push_back(DHR((t / CH) % 2));
+    const bool skip_unit = kind == SLM_KIND_GRAD && opk == SLM_OP_HEAD_CE && hb_batched[t];
+    if (skip_unit) continue;
     cudaStream_t cs = st;
     if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
     m.ts_cur_aux = sid * 4 + (kind == SLM_KIND_GRAD ? 2 : kind == SLM_KIND_MIRROR ? 1 : 0);
@@ -519,6 +574,39 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       if (opk == SLM_OP_SUM) {
         CK(launch_k(fill_kernel, dim3(1), eb, 0, cs, pdl, V(v), T, 1.0f));
         ++nl;
+      } else if (opk == SLM_OP_HEAD_CE && hb_now) {
+        // batched head backward of steps t0..t: h operands, logits GEMM (N = n B), CE rows ->
+        // d logits (bf16 ring + fp32), dh GEMM (same K slicing as the per-step path), (dh | 0)
+        // into the chunk's dh ring + db_o (per step, descending), dW_o for the chunk
+        const int t0 = hb_lo, n = t - t0 + 1, N = n * B, r0 = (t0 % CH) * B;   // ring rows of t0
+        const int bi = N % 256 == 0 ? 2 : N % 128 == 0 ? 1 : 0, bnb = 64 << bi;
+        slmk::StepIn in{};
+        for (int i = 0; i < n; ++i) in.p[i] = V(head_state(t0 + i));
+        CK(launch_k(lstm_hpack_multi_kernel, eg, eb, 0, cs, pdl, in, n, H, B, hopR + (size_t)r0 * H));
+        float* lgF = (float*)(w + W.logitsF);
+        slmk::EpiStoreF32 e{lgF, Cp};
+        if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bnb, 1, M.woK, M.hopRKb[bi], Cp, N, H, 0, r0, e, cs,
+                                                                     pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+          return s;
+        CK(launch_k(lstm_head_ce_kernel, dim3(N), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
+                    labels + (size_t)t0 * B, C, Cp, N, scale, (float*)nullptr, dlR + (size_t)r0 * Cp, dlog_f,
+                    (unsigned*)nullptr, (float*)nullptr));
+        slmk::EpiPartialTma e2{N};
+        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(bnb, sp.hd, M.woMN, M.dlRKb[bi], H, N, Cp, 0, r0,
+                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pHB)) != SLM_OK)
+          return s;
+        CK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl,
+                    (const float*)(w + W.PH), sp.hd, H, N, dh_ring(t0), (const float*)dlog_f, Cp, B, n, d.db_o));
+        nl += 5;
+        if (t0 % CH == 0) {   // the chunk is complete: dW_o over all its rows
+          slmk::EpiAccF32 e3{d.dW_o, H};
+          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp,
+                                                                    chunk_rows(t0), 0, 0, e3, cs, pdl,
+                                                                    gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+            return s;
+          ++nl;
+        }
+        for (int t2 = t0; t2 <= t; ++t2) hb_batched[t2] = 1;
       } else if (opk == SLM_OP_HEAD_CE) {
         // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits (the head reads only its input, A6)
         const float* sL = V(pp.first[pp.second - 1]);
@@ -535,8 +623,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
                                                                       e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
           return s;
-        CK(launch_k(lstm_head_dh_colsum_kernel, dim3(std::max((Cp + 31) / 32, 128)), dim3(512), 0, cs, pdl,
-                    Pb(sid), sp.hd, H, B, V(v), (const float*)dlog_f, Cp, d.db_o));
+        CK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl, Pb(sid),
+                    sp.hd, H, B, V(v), (const float*)dlog_f, Cp, B, 1, d.db_o));
         nl += 5;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};
@@ -567,7 +655,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           };
           const int sv = orig;
           const int above = l + 1 < L ? sv + 1 : t * per_t + per_t - 1;   // G^{l+1}_t or H_t
-          slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
+          if (l + 1 == L && hb_batched[t]) {   // the head gradient of this step came from the batched unit
+            sl[k] = dh_ring(t);
+            ld[k] = 2 * H;
+            ++k;
+          } else {
+            slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
+          }
           if (t + 1 < T) {
             const int xw = l == 0 ? I : 2 * H;
             slice(sv + per_t - 1, xw, xw + 2 * H);   // G^l_{t+1}
@@ -634,6 +728,10 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       }
     }
     if (msm && (s = unit_end(sid)) != SLM_OK) return s;
+    for (int node : {v, partner})
+      if (node >= 0) owner[p->node_tag[node]] = node;
+    if (kind != SLM_KIND_GRAD && opk == SLM_OP_HEAD_CE && (t % CH == CH - 1 || t == T - 1))
+      for (int t2 = t - t % CH; t2 <= t; ++t2) owner[p->node_tag[t2 * per_t + per_t - 1]] = t2 * per_t + per_t - 1;
   }
   if (msm) {   // join every stream back into the caller's
     for (int i = 0; i < NSTR; ++i) {
@@ -651,11 +749,17 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
 // fusion and operand-residency decisions
 int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
   int64_t nl = 0;
-  const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, N = p->n_fwd;
+  const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, N = p->n_fwd, CH = kLstmChunk;
   OperandTracker trk(L);
   auto tl = [&](int o) {
     if (o == N - 1) return std::make_pair(T - 1, L);
     return std::make_pair(o / per_t, (o % per_t - 1) / 2);
+  };
+  std::vector<int> owner(p->tag_size.size(), -1);
+  std::vector<char> hb_batched(T, 0);
+  auto head_state = [&](int t) {
+    const int gh = p->gnode[t * per_t + per_t - 1];
+    return gh < 0 ? -1 : p->preds[p->pred_ptr[gh + 1] - 1];
   };
   const std::vector<int>& order = p->order;
   for (size_t oi = 0; oi < order.size(); ++oi) {
@@ -664,6 +768,7 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
     const auto [t, l] = tl(p->orig[v]);
     const int* pr = p->preds.data() + p->pred_ptr[v];
     const int np = p->pred_ptr[v + 1] - p->pred_ptr[v];
+    int partner = -1;
     if (kind != SLM_KIND_GRAD) {
       if (opk == SLM_OP_LSTM_GATES) {
         const int xn = pr[0], hn = np > 1 ? pr[1] : OperandTracker::kZeros;
@@ -676,6 +781,7 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
           const int u = order[oi + 1];
           if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) {
             trk.cell(u, l, t, L, T, (t + 1) * per_t);
+            partner = u;
             ++oi;
           }
         }
@@ -683,20 +789,36 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
         trk.cell(v, l, t, L, T, (t + 1) * per_t);
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
-        if (t % kLstmChunk == kLstmChunk - 1 || t == T - 1) nl += 3;   // batched forward heads
+        if (t % CH == CH - 1 || t == T - 1) {   // batched forward heads
+          nl += 3;
+          for (int t2 = t - t % CH; t2 <= t; ++t2) owner[p->node_tag[t2 * per_t + per_t - 1]] = t2 * per_t + per_t - 1;
+        }
       } else {
         ++nl;
       }
     } else {
-      const bool flush = t % kLstmChunk == 0;
+      const bool flush = t % CH == 0;
       if (opk == SLM_OP_HEAD_CE) {
-        nl += 5 + flush;
+        if (hb_batched[t]) continue;
+        int lo = t + 1;
+        for (int t2 = t; t2 >= t - t % CH; --t2) {
+          const int a = head_state(t2);
+          if (a < 0 || owner[p->node_tag[a]] != a) break;
+          lo = t2;
+        }
+        if (lo < t) {   // batched head backward of steps lo..t
+          nl += 5 + (lo % CH == 0);
+          for (int t2 = lo; t2 <= t; ++t2) hb_batched[t2] = 1;
+        } else {
+          nl += 5 + flush;
+        }
       } else if (opk == SLM_OP_LSTM_GATES) {
         nl += 3 + 2 * flush;   // d_pre/pack, dX GEMM, scatter (+ dW GEMM and db column sums)
       } else if (opk == SLM_OP_LSTM_CELL) {
         const int u = oi + 1 < order.size() ? order[oi + 1] : -1;
         if (u >= 0 && p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && p->preds[p->pred_ptr[u]] == v) {
           nl += 3 + 2 * flush;   // fused cell/d_pre/pack + dX GEMM + scatter
+          partner = u;
           ++oi;
         } else {
           nl += 1;
@@ -705,6 +827,8 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
         nl += 1;
       }
     }
+    for (int node : {v, partner})
+      if (node >= 0) owner[p->node_tag[node]] = node;
   }
   return nl;
 }

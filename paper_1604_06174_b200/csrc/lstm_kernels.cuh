@@ -329,6 +329,61 @@ __global__ void __launch_bounds__(256) lstm_hpack_kernel(const float* __restrict
     hop[i] = __float2bfloat16_rn(s[(size_t)(i / H) * 2 * H + i % H]);
 }
 
+// h operands of a batch of steps: out rows [i B + b] = bf16(h of in.p[i] (a [B][2H] state))
+struct StepIn {
+  const float* p[32];
+};
+__global__ void __launch_bounds__(256) lstm_hpack_multi_kernel(StepIn in, int n, int H, int B,
+                                                               __nv_bfloat16* __restrict__ out) {
+  lstm_entry();
+  const size_t per = (size_t)B * H;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (size_t)n * per;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int st = (int)(i / per);
+    const size_t r = i % per;
+    out[i] = __float2bfloat16_rn(in.p[st][(r / H) * 2 * H + r % H]);
+  }
+}
+
+// Head backward finish for nsteps steps of B rows: (dh | 0) rows from the dh GEMM's split-K
+// partials P [sk][N][H] (N = nsteps B rows, row stride 2H in out), and, in blocks
+// 0 .. ceil(Cp/32)-1, db_o += the column sums of dlog_f step by step in descending step order
+// (each step: rows b = rg (mod 16) per group, groups in order) -- the same arithmetic as one
+// launch per step in the backward's descending time order.  Block = 512 threads.
+__global__ void __launch_bounds__(512) lstm_head_bwd_finish_kernel(const float* __restrict__ P, int sk, int H, int N,
+                                                                   float* __restrict__ out,
+                                                                   const float* __restrict__ g, int Cp, int B,
+                                                                   int nsteps, float* __restrict__ acc) {
+  __shared__ float red[kColGroups][33];
+  lstm_entry();
+  if ((int)blockIdx.x * 32 < Cp) {
+    const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + c;
+    for (int i = nsteps - 1; i >= 0; --i) {
+      float sum = 0.f;
+      if (j < Cp)
+        for (int b = rg; b < B; b += kColGroups) sum = __fadd_rn(sum, g[((size_t)i * B + b) * Cp + j]);
+      red[rg][c] = sum;
+      __syncthreads();
+      if (rg == 0 && j < Cp) {
+        float t = red[0][c];
+#pragma unroll
+        for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
+        acc[j] = __fadd_rn(acc[j], t);
+      }
+      __syncthreads();
+    }
+  }
+  const size_t slice = (size_t)N * H;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slice; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i / H, jj = i % H;
+    float a = P[i];
+    for (int s2 = 1; s2 < sk; ++s2) a = __fadd_rn(a, P[s2 * slice + i]);
+    out[row * 2 * H + jj] = a;
+    out[row * 2 * H + H + jj] = 0.f;
+  }
+}
+
 // One block per row b: logits = sum_s P[s][b][:] + b_o (split-K partials [sk][B][Cp], slice
 // order), written to the row buffer `logits`; row loss = logsumexp - logit[y] over the C real
 // classes; grad (when dlog != null) = (softmax - onehot) * scale as bf16 (the GEMM operand,

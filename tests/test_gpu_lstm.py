@@ -110,10 +110,10 @@ def test_lstm_launch_count(slm):
     # forward: per t, per layer GEMM + fused gates/cell; the operands are packed only at t = 0
     # (afterwards the cell kernels write them); the heads run batched per 32-step chunk
     # (logits GEMM, CE rows, per-step losses); Sum 1.
-    # backward: fill 1; per t head 5 (pack, logits GEMM, CE, dh GEMM, dh + db_o), per layer 3
-    # (fused cell / d_pre / pack, dX GEMM, scatter); per 32-step chunk one weight-gradient GEMM
-    # + db column sum per layer and one GEMM for the head (T = 4: one chunk)
-    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + T * (5 + 3 * L) + (2 * L + 1)
+    # backward: fill 1; the head gradients batched per 32-step chunk (pack, logits GEMM, CE,
+    # dh GEMM, dh + db_o, dW_o GEMM); per t and layer 3 (fused cell / d_pre / pack, dX GEMM,
+    # scatter); per chunk one weight-gradient GEMM + db column sum per layer (T = 4: one chunk)
+    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + 6 + T * 3 * L + 2 * L
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
