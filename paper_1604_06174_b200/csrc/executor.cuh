@@ -244,6 +244,7 @@ struct slm_model {
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
   int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
+  int lstm_grid = 1;                          // LSTM element-wise grids sized to the work
   int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
   int lstm_sk = 2;                            // LSTM: split-K of the gates GEMMs (0 = auto; 2 measured best with the wavefront)
   // tensor maps bound to the current workspace / weights

@@ -283,6 +283,12 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     S.offs_plan = p;
   }
   const dim3 eg(592), eb(256);
+  // element-wise grids sized to the work (one element per thread, at most 4 CTAs per SM) so
+  // the kernels of concurrent layer streams share the SMs (option lstm_grid = 0: 592 CTAs)
+  auto gsz = [&](size_t n) {
+    if (!m.lstm_grid) return eg;
+    return dim3((unsigned)std::max<size_t>(1, std::min<size_t>(592, (n + 255) / 256)));
+  };
   int64_t nl = 0;
   // gradients are overwritten by every step: zero the in-place accumulators first
   CK(cudaMemsetAsync(d.dW, 0, lstm_w_offset(d, L) * 4, st));
@@ -509,7 +515,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
         const int xn = pp.first[0], hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
         if (trk.gates_needs_pack(l, t, xn, hn)) {
-          CK(launch_k(lstm_pack_kernel, eg, eb, 0, cs, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
+          CK(launch_k(lstm_pack_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
                       H, B, opl(l, t % 2)));
           trk.packed(l, t, xn, hn);
           ++nl;
@@ -534,11 +540,11 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             ++oi;
           }
         }
-        CK(launch_k(lstm_gates_cell_kernel, eg, eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H, H, B, V(v),
+        CK(launch_k(lstm_gates_cell_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H, H, B, V(v),
                     s_prev, s_out, oo));
         nl += 2;
       } else if (opk == SLM_OP_LSTM_CELL) {
-        CK(launch_k(lstm_cell_fwd_kernel, eg, eb, 0, cs, pdl, (const float*)V(pp.first[0]),
+        CK(launch_k(lstm_cell_fwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, (const float*)V(pp.first[0]),
                     (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t, kind)));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE) {
@@ -582,7 +588,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const int bi = N % 256 == 0 ? 2 : N % 128 == 0 ? 1 : 0, bnb = 64 << bi;
         slmk::StepIn in{};
         for (int i = 0; i < n; ++i) in.p[i] = V(head_state(t0 + i));
-        CK(launch_k(lstm_hpack_multi_kernel, eg, eb, 0, cs, pdl, in, n, H, B, hopR + (size_t)r0 * H));
+        CK(launch_k(lstm_hpack_multi_kernel, gsz((size_t)n * B * H), eb, 0, cs, pdl, in, n, H, B, hopR + (size_t)r0 * H));
         float* lgF = (float*)(w + W.logitsF);
         slmk::EpiStoreF32 e{lgF, Cp};
         if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bnb, 1, M.woK, M.hopRKb[bi], Cp, N, H, 0, r0, e, cs,
@@ -610,7 +616,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       } else if (opk == SLM_OP_HEAD_CE) {
         // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits (the head reads only its input, A6)
         const float* sL = V(pp.first[pp.second - 1]);
-        CK(launch_k(lstm_hpack_kernel, eg, eb, 0, cs, pdl, sL, H, B, hopR + (size_t)slot * B * H));
+        CK(launch_k(lstm_hpack_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, sL, H, B, hopR + (size_t)slot * B * H));
         slmk::EpiPartialTma e{B};
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
                                                                        e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
@@ -676,7 +682,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             if (p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && pu.first[0] == v) {
               const int nf = has_prev ? 2 : 1;
               const float* x = V(pu.first[pu.second - nf]);
-              CK(launch_k(lstm_cell_bwd_dpre_kernel, eg, eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
+              CK(launch_k(lstm_cell_bwd_dpre_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
                           sprev, H, B, V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
               ++nl;
               vg = u;
@@ -684,7 +690,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             }
           }
           if (vg < 0) {
-            CK(launch_k(lstm_cell_bwd_kernel, eg, eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
+            CK(launch_k(lstm_cell_bwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
                         H, B, V(v)));
             ++nl;
           }
@@ -696,7 +702,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           const float* x = V(pp.first[pp.second - nf]);
           const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
           const int drow = 4 * H + (has_prev ? 2 * H : 0);
-          CK(launch_k(lstm_dpre_kernel, eg, eb, 0, cs, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
+          CK(launch_k(lstm_dpre_kernel, gsz((size_t)B * 4 * H), eb, 0, cs, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
                       l > 0 ? 2 * H : I, Kin, sprev, opS));
           ++nl;
         }
@@ -707,7 +713,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                                                                         slot * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX),
                                                                         &M.pX[l])) != SLM_OK)
             return s;
-          CK(launch_k(lstm_gate_scatter_kernel, eg, eb, 0, cs, pdl, Pb(sid), skx, Kin, H, B, I, l > 0 ? 1 : 0,
+          CK(launch_k(lstm_gate_scatter_kernel, gsz((size_t)B * (Kin + 3 * H)), eb, 0, cs, pdl, Pb(sid), skx, Kin, H, B, I, l > 0 ? 1 : 0,
                       has_prev ? 1 : 0, V(vg)));
           nl += 2;
           if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
