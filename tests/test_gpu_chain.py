@@ -242,3 +242,22 @@ def test_cta_pair_and_tile_options_bitwise(slm):
                 assert _rel(g0[k], ref[k]) <= 2e-2, (opt, k, _rel(g0[k], ref[k]))   # bf16 dW rounding
         if opt == dict(cta_pair=1):
             assert l0 == ref_loss
+
+
+def test_sgd_training_reduces_loss(slm):
+    """End to end: the checkpointed step's gradients train the chain (plain SGD on the device
+    parameters; the same batch) -- the loss falls monotonically over a few steps."""
+    n, B, d = 16, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=31)
+    p, g, x0, y = _dev(inp, "bf16")
+    model = slm.ChainModel(p, g, dtype="bf16", batch=B)
+    plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt")
+    losses = []
+    for _ in range(6):
+        losses.append(float(model.step(plan, x0, y).item()))
+        with torch.no_grad():
+            W32 = p["W"].float() - 0.5 * g["W"].float()
+            p["W"].copy_(W32.to(torch.bfloat16))
+            for k in ("b", "gamma", "beta"):
+                p[k].sub_(0.5 * g[k])
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses

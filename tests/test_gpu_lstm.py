@@ -150,3 +150,21 @@ def test_lstm_wavefront_matches_single_stream(slm, cfg):
             assert loss == ref_loss, (rep, pdl, af)
             for k in ref:
                 assert np.array_equal(g[k], ref[k]), (rep, pdl, af, k)
+
+
+def test_lstm_sgd_training_reduces_loss(slm):
+    L, T, B, H, I, C = 2, 16, 64, 128, 50, 200
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=13)
+    p, g, x, y = _dev(inp, L, H, C)
+    model = slm.LstmModel(p, g, L, T, B, H, I, C)
+    graph = slm.Graph.lstm(L, T, B, H, I)
+    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(4), alloc_flags=7)
+    losses = []
+    for _ in range(6):
+        losses.append(float(model.step(plan, x, y).item()))
+        with torch.no_grad():
+            for k in ("W", "W_o"):
+                p[k].copy_((p[k].float() - 2.0 * g[k]).to(torch.bfloat16))
+            for k in ("b", "b_o"):
+                p[k].sub_(2.0 * g[k])
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses
