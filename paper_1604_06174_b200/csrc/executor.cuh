@@ -206,7 +206,7 @@ struct GraphKey {
 struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
-  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm;   // partials of layer l's streams
+  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
   CUtensorMap woK, woMN, hopK2[2], hopRK, hopRMN, dlRK, dlRMN, pL, pH, hfK[2][2], hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
   const void* ws = nullptr;
 };

@@ -31,7 +31,7 @@ constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 struct LstmWs {
   size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, dhR, PH, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
-  std::vector<size_t> opL, opR, dpR, dpF;   // per layer: forward operand [B][K_l], backward rings
+  std::vector<size_t> opL, opR, dpR, dpF, PX;   // per layer: forward operand, backward rings, dX partials
 };
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
@@ -110,6 +110,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
     off += al(CH * B * 4 * H * 2);
     L.dpF.push_back(off);
     off += al(CH * B * 4 * H * 4);
+    L.PX.push_back(off);   // dX partials [sk][B][K_l], double-buffered by time parity
+    off += 2 * al((size_t)(l == 0 ? sp.x0 : sp.x1) * B * lstm_K(d, l) * 4);
   }
   L.total = off;
   return L;
@@ -137,6 +139,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   M.pX.resize(nl);
   M.pG.resize(nl);
   M.pGm.resize(nl);
+  M.pXd.resize(2 * nl);
   M.opRK.resize(nl);
   slm_status st;
   for (int l = 0; l < nl; ++l) {
@@ -152,6 +155,12 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pX[l], w + L.P[l], K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
+    for (int par = 0; par < 2; ++par) {
+      const size_t bytes = ((size_t)(l == 0 ? sp.x0 : sp.x1) * B * K * 4 + 255) / 256 * 256;
+      if ((st = make_map_f32(&M.pXd[2 * l + par], w + L.PX[l] + par * bytes, K,
+                             (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK)
+        return st;
+    }
     if ((st = make_map_f32(&M.pG[l], w + L.P[l], 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pGm[l], w + L.P[nl + 1 + l], 4 * H, (uint64_t)std::max(sp.g0, sp.g1) * B)) != SLM_OK)
       return st;
@@ -347,7 +356,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto OPH = [&](int l, int par) { return ntag + 4 * l + 2 + par; };
   auto HFR = [&](int par) { return ntag + 4 * L + par; };       // forward head ring, chunk parity
   auto DHR = [&](int par) { return ntag + 4 * L + 2 + par; };   // batched (dh | 0) ring, chunk parity
-  const int HOP = ntag + 4 * L + 3;   // the highest resource id
+  auto PXR = [&](int l, int par) { return ntag + 4 * L + 4 + 2 * l + par; };   // dX partials of layer l
+  const int HOP = ntag + 6 * L + 3;   // the highest resource id
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -502,6 +512,12 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       }
     }
     if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL && l == L - 1 && hb_batched[t]) rd.push_back(DHR((t / CH) % 2));
+    if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL) {   // reads dX partials of its gates successors
+      if (l + 1 < L) rd.push_back(PXR(l + 1, t % 2));
+      if (t + 1 < T) rd.push_back(PXR(l, (t + 1) % 2));
+    }
+    if (kind == SLM_KIND_GRAD && (opk == SLM_OP_LSTM_GATES || (opk == SLM_OP_LSTM_CELL && partner >= 0)))
+      wr.push_back(PXR(l, t % 2));
     const bool skip_unit = kind == SLM_KIND_GRAD && opk == SLM_OP_HEAD_CE && hb_batched[t];
     if (skip_unit) continue;
     cudaStream_t cs = st;
@@ -649,29 +665,30 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         float* dpFS = (float*)(w + W.dpF[l]) + (size_t)slot * B * 4 * H;
         int vg = -1;   // the gates gradient node handled by this iteration
         if (opk == SLM_OP_LSTM_CELL) {
-          const float* sl[3] = {nullptr, nullptr, nullptr};
-          int ld[3] = {0, 0, 0};
+          // successor contributions, in ascending successor id (A17): the gates node above (its
+          // dX partials, x columns) or the head, the next step's gates (dX partials, h
+          // columns), the next step's cell (its gradient node, (0 | dc) slot)
+          slmk::GradSrcs src{};
           int k = 0;
-          auto slice = [&](int succ_fwd, int offset_floats, int row_width) {
-            const int gs = p->gnode[succ_fwd];
-            if (gs < 0) return;
-            sl[k] = V(gs) + offset_floats;
-            ld[k] = row_width;
-            ++k;
+          auto pxs = [&](int ll, int tt, int col) {   // layer ll's dX partials of step tt
+            const int sk2 = ll == 0 ? sp.x0 : sp.x1, K2 = lstm_K(d, ll);
+            const size_t bytes = ((size_t)sk2 * B * K2 * 4 + 255) / 256 * 256;
+            src.s[k++] = slmk::GradSrc{(const float*)(w + W.PX[ll] + (tt % 2) * bytes) + col, K2, sk2, -1,
+                                       (long)B * K2};
           };
           const int sv = orig;
-          const int above = l + 1 < L ? sv + 1 : t * per_t + per_t - 1;   // G^{l+1}_t or H_t
-          if (l + 1 == L && hb_batched[t]) {   // the head gradient of this step came from the batched unit
-            sl[k] = dh_ring(t);
-            ld[k] = 2 * H;
-            ++k;
+          if (l + 1 < L) {
+            if (p->gnode[sv + 1] >= 0) pxs(l + 1, t, 0);                    // G^{l+1}_t
+          } else if (hb_batched[t]) {
+            src.s[k++] = slmk::GradSrc{dh_ring(t), 2 * H, 1, H, 0};          // batched head gradient
           } else {
-            slice(above, 0, (l + 1 < L) ? (2 * H + 2 * H * (t > 0)) : 2 * H);
+            const int gs = p->gnode[t * per_t + per_t - 1];                  // H_t
+            if (gs >= 0) src.s[k++] = slmk::GradSrc{V(gs), 2 * H, 1, H, 0};
           }
           if (t + 1 < T) {
-            const int xw = l == 0 ? I : 2 * H;
-            slice(sv + per_t - 1, xw, xw + 2 * H);   // G^l_{t+1}
-            slice(sv + per_t, 4 * H, 4 * H + 2 * H);  // S^l_{t+1}
+            if (p->gnode[sv + per_t - 1] >= 0) pxs(l, t + 1, l == 0 ? K0 : H);   // G^l_{t+1}
+            const int gs = p->gnode[sv + per_t];                                 // S^l_{t+1}
+            if (gs >= 0) src.s[k++] = slmk::GradSrc{V(gs) + 4 * H, 6 * H, 1, H, 0};
           }
           const float* act = V(pp.first[pp.second - (t > 0 ? 2 : 1)]);
           const float* sprev = t > 0 ? V(pp.first[pp.second - 1]) : nullptr;
@@ -682,16 +699,15 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             if (p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && pu.first[0] == v) {
               const int nf = has_prev ? 2 : 1;
               const float* x = V(pu.first[pu.second - nf]);
-              CK(launch_k(lstm_cell_bwd_dpre_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act,
-                          sprev, H, B, V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
+              CK(launch_k(lstm_cell_bwd_dpre_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, src, act, sprev, H, B,
+                          V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
               ++nl;
               vg = u;
               ++oi;
             }
           }
           if (vg < 0) {
-            CK(launch_k(lstm_cell_bwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, sl[0], ld[0], sl[1], ld[1], sl[2], ld[2], act, sprev,
-                        H, B, V(v)));
+            CK(launch_k(lstm_cell_bwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, src, act, sprev, H, B, V(v)));
             ++nl;
           }
         } else {
@@ -707,15 +723,14 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           ++nl;
         }
         if (vg >= 0) {
-          // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials
+          // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials kept (time-parity
+          // double buffer) and read in place by the two cell gradients that consume them
           slmk::EpiPartialTma e{B};
           if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
                                                                         slot * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX),
-                                                                        &M.pX[l])) != SLM_OK)
+                                                                        &M.pXd[2 * l + t % 2])) != SLM_OK)
             return s;
-          CK(launch_k(lstm_gate_scatter_kernel, gsz((size_t)B * (Kin + 3 * H)), eb, 0, cs, pdl, Pb(sid), skx, Kin, H, B, I, l > 0 ? 1 : 0,
-                      has_prev ? 1 : 0, V(vg)));
-          nl += 2;
+          ++nl;
           if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
             slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
             if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l],
@@ -819,11 +834,11 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
           nl += 5 + flush;
         }
       } else if (opk == SLM_OP_LSTM_GATES) {
-        nl += 3 + 2 * flush;   // d_pre/pack, dX GEMM, scatter (+ dW GEMM and db column sums)
+        nl += 2 + 2 * flush;   // d_pre/pack, dX GEMM (+ dW GEMM and db column sums)
       } else if (opk == SLM_OP_LSTM_CELL) {
         const int u = oi + 1 < order.size() ? order[oi + 1] : -1;
         if (u >= 0 && p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && p->preds[p->pred_ptr[u]] == v) {
-          nl += 3 + 2 * flush;   // fused cell/d_pre/pack + dX GEMM + scatter
+          nl += 2 + 2 * flush;   // fused cell/d_pre/pack + dX GEMM
           partner = u;
           ++oi;
         } else {

@@ -92,10 +92,28 @@ __global__ void __launch_bounds__(256) lstm_cell_fwd_kernel(const float* __restr
 // Back through S: dS = sum of up to 3 successor slices (dh | dc), each [B][2H] with row stride
 // ld_k (null = absent), added in the fixed order 0, 1, 2.  Output rows (pred order, reading
 // A17): [4H d(acts) | 2H (0 | dc_prev)] when the cell has a predecessor state, else [4H].
-__global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restrict__ d0, int ld0,
-                                                            const float* __restrict__ d1, int ld1,
-                                                            const float* __restrict__ d2, int ld2,
-                                                            const float* __restrict__ act,
+// A successor's contribution to dS^l_t = (dh | dc): rows of stride ld; dh = the sum of sk
+// split-K slices (sstride apart, slice order) -- the dX GEMM partials of a gates gradient are
+// read in place, never materialised -- and dc at column offset c_off (c_off < 0: no c part,
+// adds 0).  p == null: no such successor.
+struct GradSrc {
+  const float* p;
+  int ld, sk, c_off;
+  long sstride;
+};
+struct GradSrcs {
+  GradSrc s[3];
+};
+__device__ __forceinline__ void add_src(const GradSrc& g, int b, int j, float& dh, float& dc) {
+  if (!g.p) return;
+  const float* q = g.p + (size_t)b * g.ld + j;
+  float v = q[0];
+  for (int k = 1; k < g.sk; ++k) v = __fadd_rn(v, q[(size_t)k * g.sstride]);
+  dh = __fadd_rn(dh, v);
+  dc = __fadd_rn(dc, g.c_off >= 0 ? q[g.c_off] : 0.f);
+}
+
+__global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(GradSrcs src, const float* __restrict__ act,
                                                             const float* __restrict__ sprev, int H, int B,
                                                             float* __restrict__ out) {
   lstm_entry();
@@ -103,9 +121,8 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_kernel(const float* __restr
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
     float dh = 0.f, dc = 0.f;
-    if (d0) { dh = __fadd_rn(dh, d0[(size_t)b * ld0 + j]); dc = __fadd_rn(dc, d0[(size_t)b * ld0 + H + j]); }
-    if (d1) { dh = __fadd_rn(dh, d1[(size_t)b * ld1 + j]); dc = __fadd_rn(dc, d1[(size_t)b * ld1 + H + j]); }
-    if (d2) { dh = __fadd_rn(dh, d2[(size_t)b * ld2 + j]); dc = __fadd_rn(dc, d2[(size_t)b * ld2 + H + j]); }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) add_src(src.s[k], b, j, dh, dc);
     const float* a = act + (size_t)b * 4 * H;
     const float ig = a[j], fg = a[H + j], gg = a[2 * H + j], og = a[3 * H + j];
     const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
@@ -221,8 +238,7 @@ __device__ __forceinline__ void pack_op(const float* __restrict__ x, int xw, int
 // four gates into the time-chunk rings (bf16 GEMM operand + fp32 for db), and the dW operand
 // [x | h_{t-1}] into its ring slot.  Thread per (b, j), grid-stride.
 __global__ void __launch_bounds__(256) lstm_cell_bwd_dpre_kernel(
-    const float* __restrict__ d0, int ld0, const float* __restrict__ d1, int ld1, const float* __restrict__ d2,
-    int ld2, const float* __restrict__ act, const float* __restrict__ sprev, int H, int B, float* __restrict__ out,
+    GradSrcs src, const float* __restrict__ act, const float* __restrict__ sprev, int H, int B, float* __restrict__ out,
     __nv_bfloat16* __restrict__ dpre, float* __restrict__ dpre_f, const float* __restrict__ x, int xw, int xs,
     int Kin, __nv_bfloat16* __restrict__ op) {
   lstm_entry();
@@ -230,9 +246,8 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_dpre_kernel(
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
     float dh = 0.f, dc = 0.f;
-    if (d0) { dh = __fadd_rn(dh, d0[(size_t)b * ld0 + j]); dc = __fadd_rn(dc, d0[(size_t)b * ld0 + H + j]); }
-    if (d1) { dh = __fadd_rn(dh, d1[(size_t)b * ld1 + j]); dc = __fadd_rn(dc, d1[(size_t)b * ld1 + H + j]); }
-    if (d2) { dh = __fadd_rn(dh, d2[(size_t)b * ld2 + j]); dc = __fadd_rn(dc, d2[(size_t)b * ld2 + H + j]); }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) add_src(src.s[k], b, j, dh, dc);
     const float* a = act + (size_t)b * 4 * H;
     const float ig = a[j], fg = a[H + j], gg = a[2 * H + j], og = a[3 * H + j];
     const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;

@@ -111,9 +111,10 @@ def test_lstm_launch_count(slm):
     # (afterwards the cell kernels write them); the heads run batched per 32-step chunk
     # (logits GEMM, CE rows, per-step losses); Sum 1.
     # backward: fill 1; the head gradients batched per 32-step chunk (pack, logits GEMM, CE,
-    # dh GEMM, dh + db_o, dW_o GEMM); per t and layer 3 (fused cell / d_pre / pack, dX GEMM,
-    # scatter); per chunk one weight-gradient GEMM + db column sum per layer (T = 4: one chunk)
-    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + 6 + T * 3 * L + 2 * L
+    # dh GEMM, dh + db_o, dW_o GEMM); per t and layer 2 (fused cell / d_pre / pack, dX GEMM whose
+    # partials the next cell gradients read in place); per chunk one weight-gradient GEMM + db
+    # column sum per layer (T = 4: one chunk)
+    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + 6 + T * 2 * L + 2 * L
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
