@@ -67,3 +67,21 @@ for tt, d in ev:
     last = tt
 tot = acc.sum()
 print("GEMMs in flight (fraction of time):", {i: round(acc[i] / tot, 3) for i in range(8) if acc[i] > 0})
+# phases: forward (kind 0), recompute (1), backward (2): first start .. last end and GEMM busy union
+for kd, name in ((0, "forward"), (1, "recompute"), (2, "backward")):
+    sel = aux % 4 == kd
+    if not sel.any():
+        continue
+    ss, ee = s_us[sel], e_us[sel]
+    order = np.argsort(ss)
+    busy, cur_s, cur_e = 0.0, None, None
+    for i in order:
+        if cur_e is None or ss[i] > cur_e:
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = ss[i], ee[i]
+        else:
+            cur_e = max(cur_e, ee[i])
+    busy += cur_e - cur_s
+    print(f"{name:9s}: {sel.sum():6d} GEMMs, first {ss.min() / 1e3:8.2f} ms  last end {ee.max() / 1e3:8.2f} ms  "
+          f"GEMM-busy union {busy / 1e3:8.2f} ms")
