@@ -18,4 +18,4 @@ timeout -s KILL 900 $NCU --set full --clock-control none --import-source on -k r
   -s 300 -c 8 -o gpurun_out/${TAG}_full -f \
   python bench.py --layers 64 --steps 1 --warmup 3 --no-baseline --no-nockpt > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/${TAG}_ncu_full.log
-tail -2 gpurun_out/${TAG}_bench.txt gpurun_out/${TAG}_ncu_bench.log gpurun_out/${TAG}_ncu_full.log | cut -c1-400
+tail -n 2 gpurun_out/${TAG}_bench.txt gpurun_out/${TAG}_ncu_bench.log gpurun_out/${TAG}_ncu_full.log | cut -c1-400
