@@ -552,6 +552,23 @@ def main():
         prof_ms += e0.elapsed_time(e1) / prof_steps
         kt = model.kernel_times(reset=False)
     kt = model.kernel_times(reset=True)
+    # the same launches with the start stamp taken after each CTA's dependency wait (excludes
+    # the time a launch overlaps its predecessor under programmatic dependent launch)
+    model.set_option("profile_ts", n_gemm)
+    model.set_option("profile_ts_buffer", ts.data_ptr())
+    model.set_option("profile_ts_dep", 1)
+    with torch.cuda.stream(stream):
+        model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)     # eager + capture
+        model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+    torch.cuda.synchronize()
+    model.kernel_times(reset=True)
+    for _ in range(prof_steps):
+        with torch.cuda.stream(stream):
+            model.step(plan, x0, labels, stream=stream, comm=comm, bufs=bufs)
+        torch.cuda.synchronize()
+        model.kernel_times(reset=False)
+    kt_dep = model.kernel_times(reset=True)
+    model.set_option("profile_ts_dep", 0)
     model.set_option("profile_ts", 0)
     pk = _peaks()
     gemm_flop = 2.0 * B * d * d          # every GEMM kind: 2*B*d^2 per launch
@@ -566,12 +583,20 @@ def main():
                     "tflops": round(gemm_flop / (kt[k][0] / max(1, kt[k][1]) / 1e3) / 1e12, 1) if kt[k][1] else None}
                 for k in kinds}
     crit_ms = (kt["gemm_fwd"][0] + kt["gemm_dx"][0]) / prof_steps   # dW runs on a second stream
+    dep_ms = sum(kt_dep[k][0] for k in kinds)
+    dep_cnt = sum(kt_dep[k][1] for k in kinds)
+    achieved_dep = gemm_flop / (dep_ms / max(1, dep_cnt) / 1e3) / 1e12 if dep_ms else None
     roofline = dict(bound="tensor", achieved=round(achieved, 2), peak=peak, unit="TFLOP/s",
                     frac=round(achieved / peak, 4), traffic=None,
+                    achieved_after_dependency=round(achieved_dep, 2) if achieved_dep else None,
+                    frac_after_dependency=round(achieved_dep / peak, 4) if achieved_dep else None,
+                    avg_us_after_dependency={k: round(1e3 * kt_dep[k][0] / max(1, kt_dep[k][1]), 3) for k in kinds},
                     kernel="tc_gemm_kernel (forward, dX, dW GEMMs; 2*B*d^2 FLOP per launch)",
                     peak_source="MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                     if "_fallback" not in pk else "fallback (B200_PROFILING.md)",
-                    timing="device clock per launch (%globaltimer, CTA min start .. max end) inside the graph",
+                    timing="device clock per launch (%globaltimer, CTA min start .. max end) inside the graph; "
+                           "frac uses the span from launch, *_after_dependency from each CTA's return from "
+                           "griddepcontrol.wait (excludes the PDL overlap with the predecessor)",
                     per_kind=per_kind,
                     gemm_share_of_step=round(crit_ms / prof_ms, 4) if prof_ms else None,
                     step_ms_instrumented=round(prof_ms, 3))

@@ -258,6 +258,7 @@ struct slm_model {
   // profile_ts: device-clock (%globaltimer) start/end of every CTA of the first profile_ts GEMM
   // launches of a step, in the caller's buffer ts_buf ([slot][1024][2] uint64, zeroed)
   int profile_ts = 0;
+  int profile_ts_dep = 0;   // 1: stamp the start after the dependency wait (ts_dep)
   void* ts_buf = nullptr;
   std::vector<int> ts_kind;
   std::vector<int> ts_aux;    // per slot: the LSTM stream of the launch (slm_debug_ts_meta)
@@ -520,7 +521,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock GEMM timing
     if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
     m.ts_kind[ts_slot] = kind;
-    return (++ts_slot) << 8;
+    return ((++ts_slot) << 8) | (m.profile_ts_dep ? 8 : 0);
   };
   int abuf_node = -1;     // node whose activation operand a = ReLU(BN(x)) is resident in abuf
   int kb = 0;             // backward index: the k-th gradient Block node

@@ -240,7 +240,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
     m.ts_kind[ts_slot] = kind;
     m.ts_aux[ts_slot] = m.ts_cur_aux;
-    return (++ts_slot) << 8;
+    return ((++ts_slot) << 8) | (m.profile_ts_dep ? 8 : 0);
   };
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
   const int Cp = lstm_cpad(C), K0 = lstm_kin0(I), CH = kLstmChunk;

@@ -206,6 +206,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
     CK(cudaMemcpyToSymbol(slmk::g_slm_ts, &p, sizeof(p)));
   }
   else if (k == "profile_events") m->profile = (int)value;
+  else if (k == "profile_ts_dep") m->profile_ts_dep = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
   else if (k == "lstm_early_trigger") {
     const int v = (int)value;

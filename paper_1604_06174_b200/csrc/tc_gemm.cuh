@@ -289,6 +289,19 @@ __device__ __forceinline__ void ts_mark(int phase, int dbg) {
   }
 }
 
+// profile mode "after dependency" (dbg bit 3): the launch's start stamp is replaced by the
+// moment this CTA's producer returns from griddepcontrol.wait (its inputs are ready), so the
+// span excludes time spent overlapping the predecessor under programmatic dependent launch
+__device__ __forceinline__ void ts_dep(int dbg) {
+  unsigned long long* p = g_slm_ts;
+  const int slot = (dbg >> 8) - 1;
+  if (p == nullptr || slot < 0) return;
+  const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p[((size_t)slot * 1024 + cta) * 2] = t;
+}
+
 // a_row0/b_row0: row offsets added to the tensor-map coordinates of A / B (e.g. layer l's
 // weight block inside the [n*d, d] weight tensor).
 // PREFETCH_A: A is read-only for the whole step (the weights), so its first pipeline stages are
@@ -421,9 +434,11 @@ __global__ void __launch_bounds__(128, 1)
         load_a(kb, kb);
       }
       pdl_wait();
+      if (dbg & 8) ts_dep(dbg);
       for (int kb = 0; kb < kb0; ++kb) load_b(kb, kb);
     } else {
       pdl_wait();
+      if (dbg & 8) ts_dep(dbg);
     }
     for (int kb = kb0; kb < nk; ++kb) {
       const int s = kb % C::STAGES;
