@@ -212,8 +212,6 @@ struct LstmMaps {
 };
 struct slm_lstm_state {
   LstmMaps maps;
-  const void* offs_ws = nullptr;
-  const void* offs_plan = nullptr;
   // layer-wavefront execution (option lstm_streams): one stream per layer + one for the head,
   // a ring of events per stream, fork/join events
   std::vector<cudaStream_t> streams;

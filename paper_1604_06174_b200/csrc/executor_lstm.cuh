@@ -92,7 +92,7 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
   L.logits = off;   off += al(B * Cp * 4);
   L.dlog_f = off;   off += al(CH * B * Cp * 4);
   L.rowloss = off;  off += al(B * 4);
-  L.offs = off;     off += al(T * 8);
+  L.offs = off;     off += al(T * 4);   // per-step losses (loss_t)
   L.cnt = off;      off += 256;
   L.hopR = off;     off += al(CH * B * H * 2);
   L.hf = off;       off += 2 * al(CH * B * H * 2);   // forward head operands, chunk-parity double buffer
@@ -252,7 +252,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   float* logits = (float*)(w + W.logits);
   float* dlog_f = (float*)(w + W.dlog_f);
   float* rowloss = (float*)(w + W.rowloss);
-  long* offs = (long*)(w + W.offs);
+  float* loss_t = (float*)(w + W.offs);
   unsigned* cnt = (unsigned*)(w + W.cnt);
   bf* hopR = (bf*)(w + W.hopR);
   bf* dlR = (bf*)(w + W.dlR);
@@ -283,14 +283,6 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto V = [&](int node) -> float* { return node < 0 ? nullptr : (float*)tp[p->node_tag[node]]; };
   const int* pred = p->preds.data();
   auto preds_of = [&](int v) { return std::make_pair(pred + p->pred_ptr[v], p->pred_ptr[v + 1] - p->pred_ptr[v]); };
-  // the Sum node's inputs: pool offsets of the H_t values, uploaded once per (workspace, plan)
-  if (S.offs_ws != ws || S.offs_plan != (const void*)p) {
-    std::vector<long> h_offs(T, 0);
-    for (int t = 0; t < T; ++t) h_offs[t] = p->tag_offset[p->node_tag[t * per_t + per_t - 1]];
-    CK(cudaMemcpy(offs, h_offs.data(), T * 8, cudaMemcpyHostToDevice));
-    S.offs_ws = ws;
-    S.offs_plan = p;
-  }
   const dim3 eg(592), eb(256);
   // element-wise grids sized to the work (one element per thread, at most 4 CTAs per SM) so
   // the kernels of concurrent layer streams share the SMs (option lstm_grid = 0: 592 CTAs)
@@ -580,11 +572,12 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
                       (float*)nullptr));
           slmk::StepOut so{};
           for (int i = 0; i < n; ++i) so.p[i] = V((t0 + i) * per_t + per_t - 1);
-          CK(launch_k(lstm_step_loss_kernel, dim3(n), dim3(1024), 0, cs, pdl, (const float*)rlF, B, scale, so));
+          CK(launch_k(lstm_step_loss_kernel, dim3(n), dim3(1024), 0, cs, pdl, (const float*)rlF, B, scale, so,
+                      loss_t + t0));
           nl += 3;
         }
       } else if (opk == SLM_OP_SUM) {
-        CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const uint8_t*)pool, (const long*)offs, T, V(v)));
+        CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const float*)loss_t, T, V(v)));
         ++nl;
       } else {
         set_error("unsupported op in lstm plan");

@@ -465,14 +465,19 @@ __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restr
 struct StepOut {
   float* p[32];
 };
+// (also into loss_t[i]: the per-step losses in time order, read by the Sum node)
 __global__ void __launch_bounds__(1024) lstm_step_loss_kernel(const float* __restrict__ rowloss, int B, float scale,
-                                                              StepOut out) {
+                                                              StepOut out, float* __restrict__ loss_t) {
   __shared__ float sh[32];
   lstm_entry();
   float t = 0.f;
   for (int b = threadIdx.x; b < B; b += blockDim.x) t = __fadd_rn(t, rowloss[(size_t)blockIdx.x * B + b]);
   t = block_reduce_sum(t, sh);
-  if (threadIdx.x == 0) *out.p[blockIdx.x] = __fmul_rn(t, scale);
+  if (threadIdx.x == 0) {
+    const float v = __fmul_rn(t, scale);
+    *out.p[blockIdx.x] = v;
+    loss_t[blockIdx.x] = v;
+  }
 }
 
 // out = sum_b rowloss[b] * scale (single block, fixed order)
@@ -487,12 +492,13 @@ __global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restric
 }
 
 // loss = sum over the step losses (pool offsets table, in time order) — the Sum node
-__global__ void __launch_bounds__(32) lstm_sum_kernel(const uint8_t* __restrict__ pool, const long* __restrict__ offs,
-                                                      int T, float* __restrict__ out) {
+// loss = sum over the step losses in time order -- the Sum node (the H_t values, as written
+// next to their tags by lstm_step_loss_kernel into loss_t)
+__global__ void __launch_bounds__(32) lstm_sum_kernel(const float* __restrict__ loss_t, int T, float* __restrict__ out) {
   lstm_entry();
   if (threadIdx.x != 0) return;
   float s = 0.f;
-  for (int t = 0; t < T; ++t) s = __fadd_rn(s, *reinterpret_cast<const float*>(pool + offs[t]));
+  for (int t = 0; t < T; ++t) s = __fadd_rn(s, loss_t[t]);
   *out = s;
 }
 

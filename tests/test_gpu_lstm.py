@@ -169,3 +169,30 @@ def test_lstm_sgd_training_reduces_loss(slm):
             for k in ("b", "b_o"):
                 p[k].sub_(2.0 * g[k])
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
+
+
+def test_lstm_alternating_plans_share_buffers(slm):
+    """Two plans stepped alternately on the same model and the same pool / workspace: every
+    captured graph must keep reproducing its own step (no per-plan state left in the buffers)."""
+    cfg = (2, 8, 64, 128, 50, 300)
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=17)
+    p, g, x, y = _dev(inp, L, H, C)
+    model = slm.LstmModel(p, g, L, T, B, H, I, C)
+    graph = slm.Graph.lstm(L, T, B, H, I)
+    pa = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(2), alloc_flags=7)
+    pb = slm.Plan(graph, "none", alloc_flags=7)
+    nbytes = max(pa.pool_bytes, pb.pool_bytes)
+    pool = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(model.workspace_bytes(pa), dtype=torch.uint8, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    s = torch.cuda.Stream()
+    out = []
+    with torch.cuda.stream(s):
+        for plan in (pa, pb, pa, pb, pa):
+            model.step(plan, x, y, stream=s, bufs=(pool, ws, loss))
+            torch.cuda.synchronize()
+            out.append((float(loss.item()), g["W"].clone()))
+    for a, b in zip(out, out[1:]):
+        assert a[0] == b[0]
+        assert torch.equal(a[1], b[1])
