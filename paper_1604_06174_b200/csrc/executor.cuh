@@ -207,7 +207,7 @@ struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
   std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
-  CUtensorMap woK, woMN, hopK2[2], hopRK, hopRMN, dlRK, dlRMN, pL, pH, hfK[2][2], hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
+  CUtensorMap woK, woMN, hopRK, hopRMN, dlRK, dlRMN, pL, pH, hfK[2][2], hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
   const void* ws = nullptr;
 };
 struct slm_lstm_state {
@@ -252,6 +252,9 @@ struct slm_model {
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
   cudaStream_t s2 = nullptr;           // second stream (dW)
+  cudaStream_t s1 = nullptr;           // high-priority critical-path stream (option prio)
+  cudaEvent_t prio_ev[2] = {nullptr, nullptr};
+  int prio = 0;                        // 1: critical path on s1 (highest priority), dW on s2 (lowest)
   std::vector<cudaEvent_t> sync_ev;    // fork/join events (reused every step)
   // profile_ts: device-clock (%globaltimer) start/end of every CTA of the first profile_ts GEMM
   // launches of a step, in the caller's buffer ts_buf ([slot][1024][2] uint64, zeroed)
@@ -291,6 +294,9 @@ struct slm_model {
     for (auto e : ev_free) cudaEventDestroy(e);
     for (auto e : sync_ev) cudaEventDestroy(e);
     if (s2) cudaStreamDestroy(s2);
+    if (s1) cudaStreamDestroy(s1);
+    for (auto e : prio_ev)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -415,7 +421,15 @@ slm_status bind_maps(slm_model& m, void* ws) {
 }
 
 slm_status ensure_streams(slm_model& m, int n_layers) {
-  if (!m.s2) CK(cudaStreamCreateWithFlags(&m.s2, cudaStreamNonBlocking));
+  if (!m.s2) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&m.s2, cudaStreamNonBlocking, m.prio ? lo : 0));
+    if (m.prio) {
+      CK(cudaStreamCreateWithPriority(&m.s1, cudaStreamNonBlocking, hi));
+      for (auto& e : m.prio_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+  }
   const size_t need = 2 * (size_t)n_layers + 8;
   while (m.sync_ev.size() < need) {
     cudaEvent_t e;
@@ -454,6 +468,14 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   if (s != SLM_OK) return s;
   if (tc && (s = bind_maps(m, ws)) != SLM_OK) return s;
   if (side && (s = ensure_streams(m, n)) != SLM_OK) return s;
+  // option prio: the critical path runs on a high-priority internal stream forked from the caller's
+  cudaStream_t caller = st;
+  const bool use_s1 = side && m.prio && m.s1 != nullptr && st != nullptr;
+  if (use_s1) {
+    CK(cudaEventRecord(m.prio_ev[0], caller));
+    CK(cudaStreamWaitEvent(m.s1, m.prio_ev[0], 0));
+    st = m.s1;
+  }
 
   // tag -> pointer: pool offset, or the caller buffer bound to an external tag
   std::vector<void*> tp(p->tag_size.size(), nullptr);
@@ -736,6 +758,10 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
     cudaEvent_t ev2 = comm->events[cev_i++ % comm->events.size()];
     CK(cudaEventRecord(ev2, comm->stream));
     CK(cudaStreamWaitEvent(st, ev2, 0));
+  }
+  if (use_s1) {   // join the critical-path stream back into the caller's
+    CK(cudaEventRecord(m.prio_ev[1], st));
+    CK(cudaStreamWaitEvent(caller, m.prio_ev[1], 0));
   }
   CK(cudaGetLastError());
   if (launches) *launches = nl;

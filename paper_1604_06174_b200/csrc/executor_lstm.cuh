@@ -29,7 +29,7 @@ namespace {
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t hop, logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, dhR, PH, total;
+  size_t logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, dhR, PH, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
   std::vector<size_t> opL, opR, dpR, dpF, PX;   // per layer: forward operand, backward rings, dX partials
 };
@@ -84,7 +84,6 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
                                   (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
   size_t off = 0;
-  L.hop = off;      off += 2 * al(B * H * 2);   // time-parity double buffer
   for (int i = 0; i <= 2 * d.n_layers; ++i) {   // layers, head, mirror streams
     L.P.push_back(off);
     off += al(pbytes);
@@ -167,10 +166,6 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   }
   if ((st = make_map(&M.woK, d.W_o, H, Cp, 128)) != SLM_OK) return st;
   if ((st = make_map(&M.woMN, d.W_o, H, Cp, 64)) != SLM_OK) return st;
-  for (int par = 0; par < 2; ++par)
-    if ((st = make_map(&M.hopK2[par], w + L.hop + par * ((B * H * 2 + 255) / 256 * 256), H, B, (uint32_t)B)) !=
-        SLM_OK)
-      return st;
   if ((st = make_map(&M.hopRK, w + L.hopR, H, CH * B, (uint32_t)B)) != SLM_OK) return st;
   for (int par = 0; par < 2; ++par)
     for (int bi = 0; bi < 2; ++bi)
@@ -205,7 +200,6 @@ struct LstmNode {
 struct OperandTracker {
   static constexpr int kZeros = -2;
   std::vector<int> wx, wh;   // [2 l + parity]
-  int whead[2] = {-1, -1};
   explicit OperandTracker(int L) : wx(2 * L, -1), wh(2 * L, -1) {}
   bool gates_needs_pack(int l, int t, int xnode, int hnode) const {
     return wx[2 * l + t % 2] != xnode || wh[2 * l + t % 2] != hnode;
@@ -219,7 +213,6 @@ struct OperandTracker {
   void cell(int u, int l, int t, int L, int T, int xnext_node) {
     if (t + 1 < T) wh[2 * l + (t + 1) % 2] = u;
     if (l + 1 < L) wx[2 * (l + 1) + t % 2] = u;
-    else whead[t % 2] = u;
     if (l == 0 && t + 1 < T) wx[(t + 1) % 2] = xnext_node;
   }
 };
@@ -247,13 +240,10 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const LstmWs W = lstm_ws_layout(d, m.lstm_sk);
   const LstmSplits sp = lstm_splits(d, m.lstm_sk);
   uint8_t* w = (uint8_t*)ws;
-  auto hopb = [&](int par) { return (bf*)(w + W.hop + par * (((size_t)B * H * 2 + 255) / 256 * 256)); };
   auto Pb = [&](int i) { return (const float*)(w + W.P[i]); };   // split-K partials of stream i
   float* logits = (float*)(w + W.logits);
   float* dlog_f = (float*)(w + W.dlog_f);
-  float* rowloss = (float*)(w + W.rowloss);
   float* loss_t = (float*)(w + W.offs);
-  unsigned* cnt = (unsigned*)(w + W.cnt);
   bf* hopR = (bf*)(w + W.hopR);
   bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
@@ -296,7 +286,6 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   CK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
   CK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
   CK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
-  CK(cudaMemsetAsync(cnt, 0, 256, st));
   // weight-gradient chunk of time t: slot in the ring and whether t closes the chunk (the
   // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };

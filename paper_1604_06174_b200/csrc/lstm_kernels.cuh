@@ -51,7 +51,6 @@ __device__ __forceinline__ void op_out_x(const OpOut& o, int B) {
   }
 }
 
-__device__ __forceinline__ float sigm(float x) { return __frcp_rn(__fadd_rn(1.f, expf(-x))); }
 
 // op[b][0:Kin] = x (width xw, zero padded to Kin, source row stride xs), op[b][Kin:Kin+H] = h_prev
 // (h part of S_{t-1}: row stride 2H; null = zeros).  bf16 GEMM operand [B][Kin+H].
@@ -201,20 +200,6 @@ __global__ void __launch_bounds__(256) lstm_gates_cell_kernel(const float* __res
   if (s_out) op_out_x(oo, B);
 }
 
-// (dh | 0) of the head gradient node from the split-K partials of dlogits W_o, P [sk][B][H]
-__global__ void __launch_bounds__(256) lstm_head_dh_kernel(const float* __restrict__ P, int sk, int H, int B,
-                                                           float* __restrict__ out) {
-  lstm_entry();
-  const size_t slice = (size_t)B * H;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
-    const int b = i / H, j = i % H;
-    float acc = P[i];
-    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, P[s * slice + i]);
-    out[(size_t)b * 2 * H + j] = acc;
-    out[(size_t)b * 2 * H + H + j] = 0.f;
-  }
-}
-
 __device__ __forceinline__ float dpre_of(int q, float da, float a) {   // d_pre = d(act) * act'
   return q == 2 ? __fmul_rn(da, __fsub_rn(1.f, __fmul_rn(a, a))) : __fmul_rn(da, __fmul_rn(a, __fsub_rn(1.f, a)));
 }
@@ -270,70 +255,6 @@ __global__ void __launch_bounds__(256) lstm_cell_bwd_dpre_kernel(
     }
   }
   pack_op(x, xw, xs, Kin, sprev, H, B, op);
-}
-
-// (dh | 0) of the head gradient node from the split-K partials P [sk][B][H] and, in blocks
-// 0 .. ceil(Cp/32)-1, db_o += column sums of dlog_f [B][Cp] (colsum_acc_kernel's order).
-// Block = 512 threads.
-__global__ void __launch_bounds__(512) lstm_head_dh_colsum_kernel(const float* __restrict__ P, int sk, int H, int B,
-                                                                  float* __restrict__ out,
-                                                                  const float* __restrict__ g, int n,
-                                                                  float* __restrict__ acc) {
-  __shared__ float red[kColGroups][33];
-  lstm_entry();
-  if ((int)blockIdx.x * 32 < n) {
-    const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
-    const int j = blockIdx.x * 32 + c;
-    float sum = 0.f;
-    if (j < n)
-      for (int b = rg; b < B; b += kColGroups) sum = __fadd_rn(sum, g[(size_t)b * n + j]);
-    red[rg][c] = sum;
-    __syncthreads();
-    if (rg == 0 && j < n) {
-      float t = red[0][c];
-#pragma unroll
-      for (int r = 1; r < kColGroups; ++r) t = __fadd_rn(t, red[r][c]);
-      acc[j] = __fadd_rn(acc[j], t);
-    }
-  }
-  const size_t slice = (size_t)B * H;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
-    const int b = i / H, jj = i % H;
-    float a = P[i];
-    for (int s = 1; s < sk; ++s) a = __fadd_rn(a, P[s * slice + i]);
-    out[(size_t)b * 2 * H + jj] = a;
-    out[(size_t)b * 2 * H + H + jj] = 0.f;
-  }
-}
-
-// Gradient w.r.t. the gates node's inputs from the dX GEMM's split-K partials
-// gx [sk][B][Kin+H] (summed in slice order):
-//   x part:  width xw (the input's true width; for a lower-layer state: (dh | 0), width 2H)
-//   S part:  (dh_prev | 0), width 2H, only when has_prev
-__global__ void __launch_bounds__(256) lstm_gate_scatter_kernel(const float* __restrict__ gx, int sk, int Kin, int H,
-                                                                int B, int xw_true, int x_is_state, int has_prev,
-                                                                float* __restrict__ out) {
-  lstm_entry();
-  const int K = Kin + H;
-  const size_t slice = (size_t)B * K;
-  auto part = [&](size_t e) {
-    float acc = gx[e];
-    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, gx[s * slice + e]);
-    return acc;
-  };
-  const int xw = x_is_state ? 2 * H : xw_true;
-  const int W = xw + (has_prev ? 2 * H : 0);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * W; i += gridDim.x * blockDim.x) {
-    const int b = i / W, k = i % W;
-    float v;
-    if (k < xw) {
-      v = (x_is_state ? (k < H) : true) ? part((size_t)b * K + k) : 0.f;
-    } else {
-      const int kk = k - xw;
-      v = kk < H ? part((size_t)b * K + Kin + kk) : 0.f;
-    }
-    out[i] = v;
-  }
 }
 
 // h operand of the head: bf16 [B][H] from S^{L-1}_t
@@ -404,7 +325,7 @@ __global__ void __launch_bounds__(512) lstm_head_bwd_finish_kernel(const float* 
 // classes; grad (when dlog != null) = (softmax - onehot) * scale as bf16 (the GEMM operand,
 // a ring slot) + fp32 (for db_o), classes >= C: 0.
 // With rowloss != null the last block to finish (counter `done`, reset by it) also writes
-// loss_out = sum_b rowloss[b] * scale in row order (lstm_rowsum_kernel's arithmetic).
+// loss_out = sum_b rowloss[b] * scale in row order.
 __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restrict__ P, int sk,
                                                            float* __restrict__ logits, const float* __restrict__ bo,
                                                            const int* __restrict__ y, int C, int Cp, int B, float scale,
@@ -478,17 +399,6 @@ __global__ void __launch_bounds__(1024) lstm_step_loss_kernel(const float* __res
     *out.p[blockIdx.x] = v;
     loss_t[blockIdx.x] = v;
   }
-}
-
-// out = sum_b rowloss[b] * scale (single block, fixed order)
-__global__ void __launch_bounds__(256) lstm_rowsum_kernel(const float* __restrict__ rowloss, int B, float scale,
-                                                          float* __restrict__ out) {
-  __shared__ float sh[32];
-  lstm_entry();
-  float s = 0.f;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) s = __fadd_rn(s, rowloss[b]);
-  s = block_reduce_sum(s, sh);
-  if (threadIdx.x == 0) *out = __fmul_rn(s, scale);
 }
 
 // loss = sum over the step losses (pool offsets table, in time order) — the Sum node

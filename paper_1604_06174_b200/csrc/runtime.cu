@@ -188,6 +188,13 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
   else if (k == "l2_prefetch") m->l2_prefetch = (int)value;
   else if (k == "lstm_grid") m->lstm_grid = (int)value;
+  else if (k == "prio") {
+    if (m->s2) {
+      set_error("option prio must be set before the first step");
+      return SLM_E_ARG;
+    }
+    m->prio = (int)value;
+  }
   else if (k == "lstm_sk") m->lstm_sk = (int)value;
   else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;

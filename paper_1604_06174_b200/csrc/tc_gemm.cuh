@@ -214,22 +214,6 @@ struct EpiPartial {
 };
 
 // LSTM gates: out[n*4H + m] = act_m(acc + b[m]), sigmoid for the i, f, o blocks, tanh for g
-struct EpiLstmGates {
-  static constexpr bool kTma = false;
-  float* out;
-  const float* bias;
-  int H;
-  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int) const {
-    const float bm = bias[m];
-    const bool is_g = m >= 2 * H && m < 3 * H;
-    const long ld = 4L * H;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float p = __fadd_rn(acc[j], bm);
-      out[(long)(n0 + j) * ld + m] = is_g ? tanhf(p) : __frcp_rn(__fadd_rn(1.f, expf(-p)));
-    }
-  }
-};
 // gradient accumulation in place across time steps: out[n*ld+m] += acc
 struct EpiAccF32 {
   static constexpr bool kTma = false;
