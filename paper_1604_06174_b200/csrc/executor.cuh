@@ -244,7 +244,8 @@ struct slm_model {
   int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
   int lstm_grid = 1;                          // LSTM element-wise grids sized to the work
   int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
-  int lstm_sk = 2;                            // LSTM: split-K of the gates GEMMs (0 = auto; 2 measured best with the wavefront)
+  int lstm_sk = 1;                            // LSTM: split-K of the gates GEMMs (0 = auto; 1 measured best with the wavefront)
+  int lstm_skx = 4;                           // LSTM: split-K of the dX GEMMs (0 = auto; 4 measured best with the wavefront)
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;

@@ -49,7 +49,7 @@ inline int lstm_sk(int mtiles, int K) {
 struct LstmSplits {
   int g0, g1, x0, x1, lg, hd;   // gates (layer 0 / l > 0), dX (layer 0 / l > 0), logits, head dX
 };
-LstmSplits lstm_splits(const slm_lstm_desc& d, int gates_sk = 0) {
+LstmSplits lstm_splits(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
   const int H = d.hidden, Cp = lstm_cpad(d.n_classes);
   const int K0 = lstm_K(d, 0), K1 = 2 * H;
   // head: logits without split-K, dh with at most 4 K slices -- the per-step and the batched
@@ -72,14 +72,18 @@ LstmSplits lstm_splits(const slm_lstm_desc& d, int gates_sk = 0) {
     s.g0 = fit(K0);
     s.g1 = fit(K1);
   }
+  if (dx_sk > 0) {
+    s.x0 = upto(4 * H, dx_sk);
+    s.x1 = upto(4 * H, dx_sk);
+  }
   return s;
 }
 
-LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0) {
+LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t B = d.batch, H = d.hidden, T = d.steps, CH = kLstmChunk;
   const size_t K0 = lstm_K(d, 0), Kmax = std::max<size_t>(K0, 2 * H), Cp = lstm_cpad(d.n_classes);
-  const LstmSplits sp = lstm_splits(d, gates_sk);
+  const LstmSplits sp = lstm_splits(d, gates_sk, dx_sk);
   const size_t pbytes = std::max({(size_t)std::max(sp.g0, sp.g1) * B * 4 * H, (size_t)sp.x0 * B * K0,
                                   (size_t)sp.x1 * B * 2 * H, (size_t)sp.lg * B * Cp, (size_t)sp.hd * B * H}) * 4;
   LstmWs L{};
@@ -121,11 +125,11 @@ size_t lstm_w_offset(const slm_lstm_desc& d, int l) {   // elements
   return l == 0 ? 0 : 4 * H * k0 + (size_t)(l - 1) * 4 * H * 2 * H;
 }
 
-slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gates_sk) {
+slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gates_sk, int dx_sk) {
   if (M.ws == ws) return SLM_OK;
   const uint64_t B = d.batch, H = d.hidden, Cp = lstm_cpad(d.n_classes), CH = kLstmChunk;
-  const LstmWs L = lstm_ws_layout(d, gates_sk);
-  const LstmSplits sp = lstm_splits(d, gates_sk);
+  const LstmWs L = lstm_ws_layout(d, gates_sk, dx_sk);
+  const LstmSplits sp = lstm_splits(d, gates_sk, dx_sk);
   uint8_t* w = (uint8_t*)ws;
   const __nv_bfloat16* W = (const __nv_bfloat16*)d.W;
   const int nl = d.n_layers;
@@ -237,8 +241,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   };
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
   const int Cp = lstm_cpad(C), K0 = lstm_kin0(I), CH = kLstmChunk;
-  const LstmWs W = lstm_ws_layout(d, m.lstm_sk);
-  const LstmSplits sp = lstm_splits(d, m.lstm_sk);
+  const LstmWs W = lstm_ws_layout(d, m.lstm_sk, m.lstm_skx);
+  const LstmSplits sp = lstm_splits(d, m.lstm_sk, m.lstm_skx);
   uint8_t* w = (uint8_t*)ws;
   auto Pb = [&](int i) { return (const float*)(w + W.P[i]); };   // split-K partials of stream i
   float* logits = (float*)(w + W.logits);
@@ -248,7 +252,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
   slm_status s;
-  if ((s = lstm_bind_maps(d, S.maps, ws, m.lstm_sk)) != SLM_OK) return s;
+  if ((s = lstm_bind_maps(d, S.maps, ws, m.lstm_sk, m.lstm_skx)) != SLM_OK) return s;
   const LstmMaps& M = S.maps;
 
   const int N = p->n_fwd;

@@ -196,6 +196,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
     m->prio = (int)value;
   }
   else if (k == "lstm_sk") m->lstm_sk = (int)value;
+  else if (k == "lstm_skx") m->lstm_skx = (int)value;
   else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
@@ -281,7 +282,7 @@ slm_status slm_workspace_bytes(const slm_plan* p, const slm_model* m, size_t* by
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (!bytes) return SLM_E_ARG;
-  *bytes = m->kind == SLM_MODEL_LSTM ? lstm_ws_layout(m->ld, m->lstm_sk).total : ws_layout(*m).total;
+  *bytes = m->kind == SLM_MODEL_LSTM ? lstm_ws_layout(m->ld, m->lstm_sk, m->lstm_skx).total : ws_layout(*m).total;
   return SLM_OK;
 }
 
@@ -326,7 +327,7 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     return SLM_E_ARG;
   }
   const bool is_lstm = m->kind == SLM_MODEL_LSTM;
-  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < (is_lstm ? lstm_ws_layout(m->ld, m->lstm_sk).total : ws_layout(*m).total)) {
+  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < (is_lstm ? lstm_ws_layout(m->ld, m->lstm_sk, m->lstm_skx).total : ws_layout(*m).total)) {
     set_error("pool or workspace smaller than required");
     return SLM_E_BUFFER_TOO_SMALL;
   }
