@@ -206,7 +206,7 @@ struct GraphKey {
 struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
-  std::vector<CUtensorMap> wK, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
+  std::vector<CUtensorMap> wK, wK32, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
   CUtensorMap woK, woMN, hopRK, hopRMN, dlRK, dlRMN, pL, pH, hfK[2][2], hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
   const void* ws = nullptr;
 };
@@ -245,6 +245,7 @@ struct slm_model {
   int lstm_grid = 1;                          // LSTM element-wise grids sized to the work
   int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
   int lstm_sk = 1;                            // LSTM: split-K of the gates GEMMs (0 = auto; 1 measured best with the wavefront)
+  int lstm_fuse_cell = 0;                     // LSTM: gates + cell in the GEMM epilogue (needs lstm_sk = 1; measured slower)
   int lstm_skx = 4;                           // LSTM: split-K of the dX GEMMs (0 = auto; 4 measured best with the wavefront)
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;

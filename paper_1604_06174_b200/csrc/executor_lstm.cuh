@@ -135,6 +135,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   const int nl = d.n_layers;
   M.wK.resize(nl);
   M.wMN.resize(nl);
+  M.wK32.resize(nl);
   M.opK.resize(2 * nl);
   M.opRMN.resize(nl);
   M.dpRK.resize(nl);
@@ -148,6 +149,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   for (int l = 0; l < nl; ++l) {
     const uint64_t K = lstm_K(d, l);
     if ((st = make_map(&M.wK[l], W + lstm_w_offset(d, l), K, 4 * H, 128)) != SLM_OK) return st;
+    if ((st = make_map(&M.wK32[l], W + lstm_w_offset(d, l), K, 4 * H, 32)) != SLM_OK) return st;
     if ((st = make_map(&M.wMN[l], W + lstm_w_offset(d, l), K, 4 * H, 64)) != SLM_OK) return st;
     for (int par = 0; par < 2; ++par)
       if ((st = make_map(&M.opK[2 * l + par], w + L.opL[l] + par * ((B * K * 2 + 255) / 256 * 256), K, B,
@@ -521,12 +523,6 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           trk.packed(l, t, xn, hn);
           ++nl;
         }
-        slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sk, M.wK[l], M.opK[2 * l + t % 2], 4 * H, B,
-                                                                       Kin + H, 0, 0,
-                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD),
-                                                                       sid > L ? &M.pGm[l] : &M.pG[l])) != SLM_OK)
-          return s;
         // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
         float* s_out = nullptr;
         const float* s_prev = nullptr;
@@ -541,9 +537,23 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             ++oi;
           }
         }
-        CK(launch_k(lstm_gates_cell_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H, H, B, V(v),
-                    s_prev, s_out, oo));
-        nl += 2;
+        if (sk == 1 && m.lstm_fuse_cell) {   // one kernel: GEMM with the activations and the cell in its epilogue
+          slmk::EpiGatesCell e{V(v), s_out, s_prev, d.b + (size_t)l * 4 * H, H, B, oo};
+          if ((s = launch_tc_bn<slmk::EpiGatesCell, false, false, true>(B, 1, M.wK32[l], M.opK[2 * l + t % 2], 4 * H, B,
+                                                                        Kin + H, 0, 0, e, cs, pdl,
+                                                                        gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+            return s;
+          nl += 1;
+        } else {
+          slmk::EpiPartialTma e{B};
+          if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(
+                   B, sk, M.wK[l], M.opK[2 * l + t % 2], 4 * H, B, Kin + H, 0, 0, e, cs, pdl, gdbg(SLM_K_GEMM_FWD),
+                   sid > L ? &M.pGm[l] : &M.pG[l])) != SLM_OK)
+            return s;
+          CK(launch_k(lstm_gates_cell_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H,
+                      H, B, V(v), s_prev, s_out, oo));
+          nl += 2;
+        }
       } else if (opk == SLM_OP_LSTM_CELL) {
         CK(launch_k(lstm_cell_fwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, (const float*)V(pp.first[0]),
                     (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t, kind)));
@@ -754,7 +764,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
 
 // kernels enqueue_lstm launches for this plan (the memsets are not counted); mirrors its
 // fusion and operand-residency decisions
-int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
+int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d, int gates_sk, int fuse_cell) {
   int64_t nl = 0;
   const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, N = p->n_fwd, CH = kLstmChunk;
   OperandTracker trk(L);
@@ -764,6 +774,7 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
   };
   std::vector<int> owner(p->tag_size.size(), -1);
   std::vector<char> hb_batched(T, 0);
+  const LstmSplits sp = lstm_splits(d, gates_sk);
   auto head_state = [&](int t) {
     const int gh = p->gnode[t * per_t + per_t - 1];
     return gh < 0 ? -1 : p->preds[p->pred_ptr[gh + 1] - 1];
@@ -783,7 +794,7 @@ int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d) {
           ++nl;
           trk.packed(l, t, xn, hn);
         }
-        nl += 2;
+        nl += ((l == 0 ? sp.g0 : sp.g1) == 1 && fuse_cell) ? 1 : 2;   // GEMM with the cell epilogue, or + gates/cell kernel
         if (oi + 1 < order.size()) {
           const int u = order[oi + 1];
           if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) {

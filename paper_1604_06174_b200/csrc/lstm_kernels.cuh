@@ -88,6 +88,56 @@ __global__ void __launch_bounds__(256) lstm_cell_fwd_kernel(const float* __restr
   op_out_x(oo, B);
 }
 
+// tcgen05 GEMM epilogue of a gates node computed without split-K (tc_gemm.cuh, EpiCell): the
+// CTA's tile holds gate q = warp of 32 hidden units (TMEM lane = unit) for BN batch columns;
+// each warp activates its gate (pre = acc + b, sigmoid / tanh) and writes G, the four gates
+// meet in shared memory, and -- when the cell S^l_t is fused (s_out) -- the CTA computes
+// c = f c_prev + i g, h = o tanh c for its units and writes S and the operand side outputs.
+// The arithmetic is lstm_gates_cell_kernel's with one K slice, so both give identical bits.
+struct EpiGatesCell {
+  static constexpr bool kTma = false;
+  static constexpr bool kCell = true;
+  float* g_out;
+  float* s_out;
+  const float* sprev;
+  const float* bias;
+  int H, B;
+  OpOut oo;
+  __device__ __forceinline__ void operator()(int, int, const float*, int) const {}
+  template <int BN>
+  __device__ __forceinline__ void cell(uint32_t trow, int m0, int n0, int warp, int lane, float* sm) const {
+    constexpr int LD = BN + 1;   // padded rows: conflict-free in both passes
+    const int q = warp, j = (m0 >> 2) + lane;
+    const float bq = bias[q * H + j];
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float acc[32];
+      tmem_ld32(trow + c, acc);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const float pre = __fadd_rn(acc[jj], bq);
+        const float a = q == 2 ? tanhf(pre) : __frcp_rn(__fadd_rn(1.f, expf(-pre)));
+        g_out[(size_t)(n0 + c + jj) * 4 * H + q * H + j] = a;
+        sm[(q * 32 + lane) * LD + c + jj] = a;
+      }
+    }
+    __syncthreads();
+    if (!s_out) return;
+    for (int idx = threadIdx.x; idx < 32 * BN; idx += blockDim.x) {
+      const int u = idx % 32, nl = idx / 32, n = n0 + nl, ju = (m0 >> 2) + u;
+      const float ig = sm[u * LD + nl], fg = sm[(32 + u) * LD + nl], gg = sm[(64 + u) * LD + nl],
+                  og = sm[(96 + u) * LD + nl];
+      const float cp = sprev ? sprev[(size_t)n * 2 * H + H + ju] : 0.f;
+      const float cc = __fadd_rn(__fmul_rn(fg, cp), __fmul_rn(ig, gg));
+      const float h = __fmul_rn(og, tanhf(cc));
+      s_out[(size_t)n * 2 * H + ju] = h;
+      s_out[(size_t)n * 2 * H + H + ju] = cc;
+      op_out_h(oo, n, ju, h);
+    }
+    op_out_x(oo, B);
+  }
+};
+
 // Back through S: dS = sum of up to 3 successor slices (dh | dc), each [B][2H] with row stride
 // ld_k (null = absent), added in the fixed order 0, 1, 2.  Output rows (pred order, reading
 // A17): [4H d(acts) | 2H (0 | dc_prev)] when the cell has a predecessor state, else [4H].

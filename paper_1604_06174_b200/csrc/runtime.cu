@@ -197,6 +197,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   }
   else if (k == "lstm_sk") m->lstm_sk = (int)value;
   else if (k == "lstm_skx") m->lstm_skx = (int)value;
+  else if (k == "lstm_fuse_cell") m->lstm_fuse_cell = (int)value;
   else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
@@ -290,7 +291,7 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (m->kind == SLM_MODEL_LSTM) {
-    *launches = lstm_launches(p, m->ld);
+    *launches = lstm_launches(p, m->ld, m->lstm_sk, m->lstm_fuse_cell);
     return SLM_OK;
   }
   std::vector<Op> ops;
