@@ -148,7 +148,9 @@ enum { SLM_PLAN_NONE = 0, SLM_PLAN_SQRT = 1, SLM_PLAN_BUDGET = 2, SLM_PLAN_SEARC
  * group (slm_graph_lstm: the layer of a gates/cell node, L for the head and the loss; every
  * other builder: one group), so the plan never makes work of two layers share memory and the
  * layer wavefront keeps its concurrency (reading A22; an extension, not the paper). */
-enum { SLM_ALLOC_INPLACE = 1, SLM_ALLOC_SHARING = 2, SLM_ALLOC_GROUPED = 4 };
+/* SLM_ALLOC_GROUP_MIRRORS: re-computed (mirror) nodes and the other nodes never share a tag, so
+ * the recompute of one segment does not wait for the backward of the next (A22). */
+enum { SLM_ALLOC_INPLACE = 1, SLM_ALLOC_SHARING = 2, SLM_ALLOC_GROUPED = 4, SLM_ALLOC_GROUP_MIRRORS = 8 };
 
 typedef struct {
   int32_t strategy;       /* SLM_PLAN_*                                                    */

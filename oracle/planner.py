@@ -24,7 +24,7 @@ from .graph import (OPS, INPUT, F_NOT_CANDIDATE, F_PIN, F_REQUEST_GRAD, Graph,
 # strategies (values mirrored independently in include/slm.h)
 S_NONE, S_SQRT, S_BUDGET, S_SEARCH, S_RECURSIVE, S_EXPLICIT, S_DROP_CHEAP = range(7)
 # allocator switches (the paper's compared strategies)
-A_INPLACE, A_SHARING, A_GROUPED = 1, 2, 4
+A_INPLACE, A_SHARING, A_GROUPED, A_GROUP_MIRRORS = 1, 2, 4, 8
 
 # App. A grid, reading A3: 6 geometric points 2^((2i-5)/10), i=0..5, spanning [B/sqrt2, sqrt2 B]
 GRID = (0.7071067811865476, 0.8122523963562356, 0.9330329915368074,
@@ -285,11 +285,13 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256, groups=None)
     size; (4) only then decrement input counters and release tags that reach 0.  Nodes
     with no consumers are released right after they run.  Pinned tags never recycle.
     Offsets: reading A9.  A_GROUPED (reading A22, an extension): step (2) only considers free
-    tags created by a node of the same allocation group (groups[orig])."""
+    tags created by a node of the same allocation group (groups[orig]); A_GROUP_MIRRORS further
+    separates mirror nodes from the others."""
     nodes = gg.nodes
 
     def grp(v):
-        return groups[nodes[v].orig] if (flags & A_GROUPED) and groups is not None else 0
+        g = groups[nodes[v].orig] if (flags & A_GROUPED) and groups is not None else 0
+        return 2 * g + (nodes[v].kind == "mirror") if flags & A_GROUP_MIRRORS else g
     tag_group = []
     cnt = {}
     for v in gg.order:

@@ -388,8 +388,11 @@ struct Alloc {
 // Fig. 2, reading A8; offsets reading A9.
 void allocate(const Built& b, int flags, int64_t align, Alloc* out, const std::vector<int>& group) {
   const auto& nodes = b.nodes;
-  const bool grouped = (flags & SLM_ALLOC_GROUPED) != 0;
-  auto grp = [&](int v) { return grouped ? group[nodes[v].orig] : 0; };
+  const bool grouped = (flags & SLM_ALLOC_GROUPED) != 0, by_kind = (flags & SLM_ALLOC_GROUP_MIRRORS) != 0;
+  auto grp = [&](int v) {
+    const int g = grouped ? group[nodes[v].orig] : 0;
+    return by_kind ? 2 * g + (nodes[v].kind == SLM_KIND_MIRROR ? 1 : 0) : g;
+  };
   std::vector<int> tag_group;
   std::vector<int> cnt(nodes.size(), 0);
   for (int v : b.order)

@@ -86,7 +86,8 @@ def test_lstm_finite_differences():
 
 @pytest.mark.parametrize("plan_kind", ["none", "seg2", "seg3", "sqrt", "search"])
 @pytest.mark.parametrize("mode", ["f64", "bf16"])
-@pytest.mark.parametrize("flags", [P.A_INPLACE | P.A_SHARING, P.A_INPLACE | P.A_SHARING | P.A_GROUPED])
+@pytest.mark.parametrize("flags", [P.A_INPLACE | P.A_SHARING, P.A_INPLACE | P.A_SHARING | P.A_GROUPED,
+                                   P.A_INPLACE | P.A_SHARING | P.A_GROUPED | P.A_GROUP_MIRRORS])
 def test_lstm_plan_invariance_bitwise(plan_kind, mode, flags):
     L, T, B, H, I, C = 2, 6, 3, 4, 3, 5
     Pm, inp = _params(L, T, B, H, I, C, dtype="bf16" if mode == "bf16" else "f32", seed=2)
@@ -123,6 +124,12 @@ def test_grouped_allocation_invariants():
     for v in p.gg.order:
         users.setdefault(p.alloc.tag_of[v], set()).add(gr.nodes[p.gg.nodes[v].orig].group)
     assert all(len(s) == 1 for s in users.values())
+    p2 = P.plan(gr, P.S_EXPLICIT, m=OL.time_segment_plan(gr, 3),
+                alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUPED | P.A_GROUP_MIRRORS)
+    kinds = {}
+    for v in p2.gg.order:
+        kinds.setdefault(p2.alloc.tag_of[v], set()).add(p2.gg.nodes[v].kind == "mirror")
+    assert all(len(s) == 1 for s in kinds.values())    # mirrors never share with other nodes
     ch = G.chain_graph(40, 8, 64)
     a = P.plan(ch, P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING).alloc
     b = P.plan(ch, P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUPED).alloc

@@ -95,6 +95,8 @@ def test_lstm_graph_plan():
     assert_same_plan(g, P.S_NONE)
     grouped = P.A_INPLACE | P.A_SHARING | P.A_GROUPED
     assert_same_plan(g, P.S_EXPLICIT, m=m, alloc_flags=grouped)
+    assert_same_plan(g, P.S_EXPLICIT, m=m, alloc_flags=grouped | P.A_GROUP_MIRRORS)
+    assert_same_plan(G.chain_graph(40, 8, 64), P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUP_MIRRORS)
     assert_same_plan(g, P.S_SEARCH, alloc_flags=grouped)
     assert_same_plan(g, P.S_SQRT, alloc_flags=grouped)
     assert_same_plan(G.lstm_graph(4, 64, 64, 1024, 50), P.S_EXPLICIT,
