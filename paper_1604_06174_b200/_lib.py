@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libslm.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1604_06174_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: run `python paper_1604_06174_b200/build.py` "
                       "(or __graft_entry__.build()); there is no non-native fallback")
 lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
 
