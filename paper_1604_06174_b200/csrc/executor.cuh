@@ -107,6 +107,32 @@ slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorM
   return SLM_E_UNSUPPORTED;
 }
 
+// persistent forward run (fwd_persist.cuh): B in {64, 128, 256}, S in {4, 8, 16}
+template <int B_, int S_>
+slm_status launch_fwd_seg_t(const CUtensorMap& w, const CUtensorMap& a, const slmk::FwdSegArgs& A, int grid,
+                            cudaStream_t st, bool pdl) {
+  using C = slmk::FwdSegCfg<B_, S_>;
+  auto kern = slmk::fwd_seg_kernel<B_, S_>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CK(launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, st, pdl, w, a, A));
+  return SLM_OK;
+}
+slm_status launch_fwd_seg(int B, int S, const CUtensorMap& w, const CUtensorMap& a, const slmk::FwdSegArgs& A,
+                          int grid, cudaStream_t st, bool pdl) {
+#define SLM_FS(B_, S_) \
+  if (B == B_ && S == S_) return launch_fwd_seg_t<B_, S_>(w, a, A, grid, st, pdl);
+#define SLM_FS_B(B_) SLM_FS(B_, 4) SLM_FS(B_, 8) SLM_FS(B_, 16)
+  SLM_FS_B(64) SLM_FS_B(128) SLM_FS_B(256)
+#undef SLM_FS_B
+#undef SLM_FS
+  set_error("unsupported persistent forward configuration");
+  return SLM_E_UNSUPPORTED;
+}
+
 // fp32 2-D tensor [rows][inner], box {128, 32}, no swizzle (epilogue bulk stores)
 slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows) {
   EncodeTiledFn enc = get_encode();
@@ -241,6 +267,9 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int persist_dbg = 0;                        // persistent kernel phase stamps (scripts/persist_phases.py)
+  int persist = 0;                            // runs of forward / mirror Blocks as one persistent kernel (fwd_persist.cuh;
+                                              // measured slower at C2: 47.4 / 50.9 ms/step vs 43.2)
   int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
   int lstm_grid = 1;                          // LSTM element-wise grids sized to the work
   int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
@@ -250,7 +279,7 @@ struct slm_model {
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
-  CUtensorMap mW_K, mW_MN, mA_K, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
+  CUtensorMap mW_K, mW_MN, mA_K, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
   cudaStream_t s2 = nullptr;           // second stream (dW)
@@ -328,9 +357,23 @@ int auto_split(int M, int K, int req, int n_tiles = 1) {
   return s;
 }
 
+// split-K factor S of the persistent forward kernel (fwd_persist.cuh), 0 = not applicable:
+// the largest S with (d / 128) x S CTAs <= one per SM, a K slice of 64..256 (all of it resident
+// in shared memory)
+int persist_split(const slm_model& m) {
+  if (!m.persist || !fused_ok(m)) return 0;
+  const int d = m.d.width, tiles = d / 128;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int s : {16, 8, 4})
+    if (tiles * s <= sms && d % (s * 64) == 0 && d / s >= 64 && d / s <= 256) return s;
+  return 0;
+}
+
 struct WsLayout {
-  size_t a, stats, gq[3], ab[2], P, da, rowloss, total;
-  int sk_fwd, sk_dx;
+  size_t a, stats, gq[3], ab[2], P, da, rowloss, bar, total;
+  int sk_fwd, sk_dx, sk_persist;
 };
 WsLayout ws_layout(const slm_model& m) {
   const size_t B = m.d.batch, d = m.d.width;
@@ -339,6 +382,7 @@ WsLayout ws_layout(const slm_model& m) {
   const int nt = fused_ok(m) ? (int)B / fused_n(m) : 1;
   L.sk_fwd = auto_split((int)d, (int)d, m.sk_fwd, nt);
   L.sk_dx = auto_split((int)d, (int)d, m.sk_dx, nt);
+  L.sk_persist = persist_split(m);
   size_t off = 0;
   L.a = off;
   off += al(B * d * 4);
@@ -353,11 +397,13 @@ WsLayout ws_layout(const slm_model& m) {
     off += al(B * d * 2);
   }
   L.P = off;
-  off += al((size_t)std::max(L.sk_fwd, L.sk_dx) * B * d * 4);
+  off += al((size_t)std::max({L.sk_fwd, L.sk_dx, L.sk_persist}) * B * d * 4);
   L.da = off;
   off += al(B * d * 4);
   L.rowloss = off;
   off += al(B * 4);
+  L.bar = off;
+  off += 128 * 128;
   L.total = off;
   return L;
 }
@@ -396,7 +442,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 }
 
 slm_status bind_maps(slm_model& m, void* ws) {
-  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003;
+  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -409,6 +455,7 @@ slm_status bind_maps(slm_model& m, void* ws) {
   if ((st = make_map(&m.mW_K, m.d.W, d, n * d, 128)) != SLM_OK) return st;
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
   if ((st = make_map(&m.mA_K, w + L.a, d, B, bnf)) != SLM_OK) return st;
+  if (fz && (st = make_map(&m.mA_Kf, w + L.a, d, B, (uint32_t)B)) != SLM_OK) return st;
   if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
   for (int i = 0; i < 3; ++i) {
     if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, bnx)) != SLM_OK) return st;
@@ -416,7 +463,8 @@ slm_status bind_maps(slm_model& m, void* ws) {
   }
   for (int i = 0; i < 2; ++i)
     if ((st = make_map(&m.mAb_MN[i], w + L.ab[i], d, B, 64)) != SLM_OK) return st;
-  if ((st = make_map_f32(&m.mP, w + L.P, d, (uint64_t)std::max(L.sk_fwd, L.sk_dx) * B)) != SLM_OK) return st;
+  if ((st = make_map_f32(&m.mP, w + L.P, d, (uint64_t)std::max({L.sk_fwd, L.sk_dx, L.sk_persist}) * B)) != SLM_OK)
+    return st;
   m.maps_ws = ws;
   m.maps_key = key;
   return SLM_OK;
@@ -557,7 +605,14 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       comm ? (int)std::max<int64_t>(1, std::min<int64_t>(n, comm->bucket_bytes / per_layer)) : 0;
   int cev_i = 0;
 
-  for (const Op& o : ops) {
+  // persistent forward runs: grid-barrier counter, zeroed once per step (monotonic within it)
+  const int PS = L.sk_persist;
+  unsigned* bar = (unsigned*)(w + L.bar);
+  unsigned bar_count = 0;
+  if (PS > 0) CK(cudaMemsetAsync(bar, 0, 128 * 128, st));
+
+  for (size_t oi = 0; oi < ops.size(); ++oi) {
+    const Op& o = ops[oi];
     const int l = o.layer;
     if (o.type == 0) {  // ---------------- forward / mirror Block_l
       const float* xin = X(o.in_tag);
@@ -568,7 +623,41 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         pend(SLM_K_BN_ACT, st);
         ++nl;
       }
-      if (fz) {
+      if (PS > 0) {
+        // the run of chained forward / mirror Blocks starting here (each reads the previous one's
+        // output), up to kSegMax per launch
+        slmk::FwdSegArgs A{};
+        A.n = n;
+        A.d = d;
+        A.bar = bar;
+        A.P = P;
+        A.bias = bvec;
+        A.gamma = gam;
+        A.beta = bet;
+        A.stats = stats;
+        A.a = (bf*)abuf;
+        A.phase_dbg = m.persist_dbg;
+        int cnt = 0;
+        size_t oj = oi;
+        for (;;) {
+          const Op& q = ops[oj];
+          A.L[cnt++] = {X(q.in_tag), X(q.out_tag), q.layer, gdbg(SLM_K_GEMM_FWD)};
+          if (cnt == slmk::kSegMax || oj + 1 >= ops.size()) break;
+          const Op& nx = ops[oj + 1];
+          if (nx.type != 0 || nx.in_node != q.node) break;
+          ++oj;
+        }
+        A.nl = cnt;
+        const int grid = d / 128 * PS;
+        A.lay_base = bar_count;
+        bar_count += (unsigned)cnt;
+        pbeg(st);
+        if ((s = launch_fwd_seg(B, PS, m.mW_K, m.mA_Kf, A, grid, st, pdl)) != SLM_OK) return s;
+        pend(SLM_K_GEMM_FWD, st);
+        abuf_node = ops[oj].node;
+        oi = oj;
+        ++nl;
+      } else if (fz) {
         slmk::EpiPartialTma epi{B};
         pbeg(st);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(

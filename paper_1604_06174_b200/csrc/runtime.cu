@@ -29,6 +29,7 @@
 #include "bn_kernels.cuh"
 #include "slm_internal.h"
 #include "tc_gemm.cuh"
+#include "fwd_persist.cuh"
 
 using namespace slm;
 
@@ -200,6 +201,8 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "lstm_fuse_cell") m->lstm_fuse_cell = (int)value;
   else if (k == "cta_pair") m->cta_pair = (int)value;
   else if (k == "fused") m->fused = (int)value;
+  else if (k == "persist") m->persist = (int)value;
+  else if (k == "persist_dbg") m->persist_dbg = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "profile_ts") {
     m->profile_ts = (int)value;

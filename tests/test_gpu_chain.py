@@ -261,3 +261,29 @@ def test_sgd_training_reduces_loss(slm):
             for k in ("b", "gamma", "beta"):
                 p[k].sub_(0.5 * g[k])
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
+
+
+@pytest.mark.parametrize("n,B,d", [(9, 64, 256), (7, 128, 1024), (6, 256, 2048), (70, 64, 512)])
+def test_persistent_forward_option(slm, n, B, d):
+    """Option persist=1 (fwd_persist.cuh: runs of forward / mirror Blocks as one persistent
+    kernel with split-K S = 4 / 16 / 8 / 8 at these widths; n = 70 spans two launches of <= 64
+    Blocks): within the bf16 tolerance of the fp64 oracle at the small size (ReLU-margin inputs,
+    reading A20) and of the default two-kernel lowering at all sizes, and checkpointed ==
+    non-checkpointed bit for bit for every strategy (mirrors re-run the same kernel)."""
+    small = n * B * d <= 200_000
+    inp = margin_inputs(n, B, d, "bf16") if small else synth.chain_inputs(n, B, d, dtype="bf16", seed=5)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, persist=1)
+    if small:
+        ol, og, _ = _oracle(n, B, d, "bf16", inp)
+        assert abs(ref_loss - ol) <= 2e-2 * abs(ol)
+        for k in og:
+            assert _rel(ref[k], og[k]) <= 2e-2, (k, _rel(ref[k], og[k]))
+    dl, dg, _ = _run(slm, n, B, d, "bf16", "none", inp, persist=0)
+    assert abs(ref_loss - dl) <= 2e-2 * abs(dl)
+    for k in dg:
+        assert _rel(ref[k], dg[k]) <= 2e-2, (k, _rel(ref[k], dg[k]))
+    for strategy in ("sqrt", "search", "recursive"):
+        l1, g1, _ = _run(slm, n, B, d, "bf16", strategy, inp, persist=1)
+        assert l1 == ref_loss, strategy
+        for k in ref:
+            assert np.array_equal(g1[k], ref[k]), (strategy, k)
