@@ -24,7 +24,7 @@ from .graph import (OPS, INPUT, F_NOT_CANDIDATE, F_PIN, F_REQUEST_GRAD, Graph,
 # strategies (values mirrored independently in include/slm.h)
 S_NONE, S_SQRT, S_BUDGET, S_SEARCH, S_RECURSIVE, S_EXPLICIT, S_DROP_CHEAP = range(7)
 # allocator switches (the paper's compared strategies)
-A_INPLACE, A_SHARING, A_GROUPED, A_GROUP_MIRRORS = 1, 2, 4, 8
+A_INPLACE, A_SHARING, A_GROUPED, A_GROUP_MIRRORS, A_MIRROR_PARITY = 1, 2, 4, 8, 16
 
 # App. A grid, reading A3: 6 geometric points 2^((2i-5)/10), i=0..5, spanning [B/sqrt2, sqrt2 B]
 GRID = (0.7071067811865476, 0.8122523963562356, 0.9330329915368074,
@@ -286,12 +286,27 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256, groups=None)
     with no consumers are released right after they run.  Pinned tags never recycle.
     Offsets: reading A9.  A_GROUPED (reading A22, an extension): step (2) only considers free
     tags created by a node of the same allocation group (groups[orig]); A_GROUP_MIRRORS further
-    separates mirror nodes from the others."""
+    separates mirror nodes from the others; A_MIRROR_PARITY (reading A24) separates them too and
+    lets a mirror reuse only tags of mirrors whose run (maximal sequence of consecutive mirrors
+    in V') has the same parity."""
     nodes = gg.nodes
+    mpar = {}
+    if flags & A_MIRROR_PARITY:
+        run, prev = -1, False
+        for v in gg.order:
+            im = nodes[v].kind == "mirror"
+            if im and not prev:
+                run += 1
+            if im:
+                mpar[v] = run % 2
+            prev = im
 
     def grp(v):
         g = groups[nodes[v].orig] if (flags & A_GROUPED) and groups is not None else 0
-        return 2 * g + (nodes[v].kind == "mirror") if flags & A_GROUP_MIRRORS else g
+        im = nodes[v].kind == "mirror"
+        if flags & A_MIRROR_PARITY:
+            return 3 * g + (1 + mpar[v] if im else 0)
+        return 2 * g + im if flags & A_GROUP_MIRRORS else g
     tag_group = []
     cnt = {}
     for v in gg.order:

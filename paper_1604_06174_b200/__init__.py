@@ -22,7 +22,7 @@ STRATEGY = {"none": 0, "sqrt": 1, "budget": 2, "search": 3, "recursive": 4, "exp
             "drop_cheap": 6}
 OP = dict(input=0, block=1, softmax_ce=2, fc=3, sigmoid=4, relu=5, bn=6, add=7, mul=8,
           identity=9, lstm_gates=10, lstm_cell=11, head_ce=12, sum=13)
-ALLOC_INPLACE, ALLOC_SHARING, ALLOC_GROUPED, ALLOC_GROUP_MIRRORS = 1, 2, 4, 8
+ALLOC_INPLACE, ALLOC_SHARING, ALLOC_GROUPED, ALLOC_GROUP_MIRRORS, ALLOC_MIRROR_PARITY = 1, 2, 4, 8, 16
 NODE_NOT_CANDIDATE, NODE_PIN, NODE_REQUEST_GRAD = 1, 2, 4
 
 

@@ -389,9 +389,24 @@ struct Alloc {
 void allocate(const Built& b, int flags, int64_t align, Alloc* out, const std::vector<int>& group) {
   const auto& nodes = b.nodes;
   const bool grouped = (flags & SLM_ALLOC_GROUPED) != 0, by_kind = (flags & SLM_ALLOC_GROUP_MIRRORS) != 0;
+  const bool parity = (flags & SLM_ALLOC_MIRROR_PARITY) != 0;
+  // MIRROR_PARITY: parity of the mirror run (maximal run of consecutive mirrors in V') of each mirror
+  std::vector<int> mpar(nodes.size(), 0);
+  if (parity) {
+    int run = -1;
+    bool prev = false;
+    for (int v : b.order) {
+      const bool im = nodes[v].kind == SLM_KIND_MIRROR;
+      if (im && !prev) ++run;
+      if (im) mpar[v] = run & 1;
+      prev = im;
+    }
+  }
   auto grp = [&](int v) {
     const int g = grouped ? group[nodes[v].orig] : 0;
-    return by_kind ? 2 * g + (nodes[v].kind == SLM_KIND_MIRROR ? 1 : 0) : g;
+    const bool im = nodes[v].kind == SLM_KIND_MIRROR;
+    if (parity) return 3 * g + (im ? 1 + mpar[v] : 0);
+    return by_kind ? 2 * g + (im ? 1 : 0) : g;
   };
   std::vector<int> tag_group;
   std::vector<int> cnt(nodes.size(), 0);

@@ -404,3 +404,77 @@ def test_lstm_graph_time_segments():
     none = P.plan(g, P.S_NONE)
     assert p.alloc.exact_peak < none.alloc.exact_peak
     assert len(p.gg.g) == sum(1 for nd in g.nodes if nd.op != G.INPUT)
+
+
+def _mirror_runs(p):
+    """V' after its first mirror, split into alternating maximal runs: M_0 N_0 M_1 N_1 ...
+    (M = mirrors, N = everything else); returns (prefix, [(M_r, N_r)])."""
+    order, nodes = p.gg.order, p.gg.nodes
+    first = next((i for i, v in enumerate(order) if nodes[v].kind == "mirror"), len(order))
+    runs, i = [], first
+    while i < len(order):
+        m = []
+        while i < len(order) and nodes[order[i]].kind == "mirror":
+            m.append(order[i])
+            i += 1
+        nn = []
+        while i < len(order) and nodes[order[i]].kind != "mirror":
+            nn.append(order[i])
+            i += 1
+        runs.append((m, nn))
+    return order[:first], runs
+
+
+def _concurrent_schedule(p, rnd):
+    """One random execution order of the executor's two-stream schedule (reading A24):
+    M_r may run as soon as M_{r-1} and N_{r-2} are done, so it interleaves with N_{r-1}."""
+    pre, runs = _mirror_runs(p)
+    out = list(pre)
+    if runs:
+        out += runs[0][0]
+    for r in range(1, len(runs) + 1):
+        a = list(runs[r - 1][1])
+        b = list(runs[r][0]) if r < len(runs) else []
+        while a or b:
+            src = a if (a and (not b or rnd.random() < 0.5)) else b
+            out.append(src.pop(0))
+    return out
+
+
+def _replay(p, order):
+    holds = {}
+    for v in order:
+        for q in p.gg.nodes[v].preds:
+            assert holds.get(p.alloc.tag_of[q]) == q, (v, q)
+        holds[p.alloc.tag_of[v]] = v
+
+
+@pytest.mark.parametrize("n", [16, 40, 100, 257])
+def test_mirror_parity_concurrent_recompute_is_sound(n):
+    """A_MIRROR_PARITY (reading A24): the recompute of segment j-1 may run concurrently with the
+    backward of segment j.  Pinned by brute force: 200 random interleavings of every M_r with
+    N_{r-1} replay V' without a single clobbered read; the plain allocator fails that replay
+    (so the flag is what makes it sound), and for the sqrt plan the price is at most one extra
+    segment of mirrors."""
+    rnd = random.Random(n)
+    g = G.chain_graph(n, 8, 64)
+    u = 8 * 64 * 4
+    fl = P.A_INPLACE | P.A_SHARING
+    for strat in (P.S_SQRT, P.S_SEARCH):
+        p = P.plan(g, strat, alloc_flags=fl | P.A_MIRROR_PARITY)
+        _simulate_interference(p)
+        for _ in range(200):
+            _replay(p, _concurrent_schedule(p, rnd))
+        base = P.plan(g, strat, alloc_flags=fl)
+        if strat == P.S_SQRT:   # same m; one more segment of mirrors (App. A search re-optimises m)
+            L = max(len(m) for m, _ in _mirror_runs(base)[1])
+            assert base.alloc.exact_peak <= p.alloc.exact_peak <= base.alloc.exact_peak + L * u
+        assert p.alloc.exact_peak < P.plan(g, strat, alloc_flags=0).alloc.exact_peak
+    p = P.plan(g, P.S_SQRT, alloc_flags=fl)
+    bad = 0
+    for _ in range(50):
+        try:
+            _replay(p, _concurrent_schedule(p, rnd))
+        except AssertionError:
+            bad += 1
+    assert bad > 0

@@ -97,6 +97,10 @@ def test_lstm_graph_plan():
     assert_same_plan(g, P.S_EXPLICIT, m=m, alloc_flags=grouped)
     assert_same_plan(g, P.S_EXPLICIT, m=m, alloc_flags=grouped | P.A_GROUP_MIRRORS)
     assert_same_plan(G.chain_graph(40, 8, 64), P.S_SQRT, alloc_flags=P.A_INPLACE | P.A_SHARING | P.A_GROUP_MIRRORS)
+    par = P.A_INPLACE | P.A_SHARING | P.A_MIRROR_PARITY
+    for strat, kw in ((P.S_SQRT, {}), (P.S_SEARCH, {}), (P.S_RECURSIVE, dict(k=1)), (P.S_RECURSIVE, dict(k=2))):
+        assert_same_plan(G.chain_graph(40, 8, 64), strat, alloc_flags=par, **kw)
+    assert_same_plan(g, P.S_SQRT, alloc_flags=grouped | P.A_MIRROR_PARITY)
     assert_same_plan(g, P.S_SEARCH, alloc_flags=grouped)
     assert_same_plan(g, P.S_SQRT, alloc_flags=grouped)
     assert_same_plan(G.lstm_graph(4, 64, 64, 1024, 50), P.S_EXPLICIT,
@@ -140,7 +144,7 @@ def test_random_dags():
             kw["budget"] = rnd.randint(0, 3000)
         if s == P.S_EXPLICIT:
             kw["m"] = [0 if nd.op == G.INPUT else rnd.randint(0, 3) for nd in g.nodes]
-        flags = rnd.choice([3, 3, 1, 2, 0])
+        flags = rnd.choice([3, 3, 1, 2, 0, 19])
         assert_same_plan(g, s, alloc_flags=flags, **kw)
 
 
