@@ -406,6 +406,8 @@ def main():
     ap.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-nockpt", action="store_true", help="skip the non-checkpointed comparison")
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
+    ap.add_argument("--mirror-parity", type=int, default=1,
+                    help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
     ap.add_argument("--model", default="chain", choices=["chain", "lstm"],
                     help="chain = configs[1] (default, the metric's config); lstm = configs[2]")
@@ -516,11 +518,15 @@ def main():
             ms = t.item()
         return ms, float(loss.item()), clk.summary() if clk else None
 
-    plan = slm.Plan(graph, args.strategy)
+    # SLM_ALLOC_MIRROR_PARITY (reading A24): mirrors of consecutive segments use disjoint pool
+    # slots, so each segment's recompute runs concurrently with the next segment's backward
+    chain_af = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | (slm.ALLOC_MIRROR_PARITY if args.mirror_parity else 0)
+    plan = slm.Plan(graph, args.strategy, alloc_flags=chain_af)
     torch.cuda.synchronize()
     base_mem = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
     ms, loss, clocks = timed(plan, args.steps, args.warmup, with_clocks=True)
+    overlapped = bool(model.get_option("last_overlap"))
     act_measured = torch.cuda.max_memory_allocated(dev) - base_mem   # pool + workspace + loss
     value = Bg / (ms / 1e3)
     launches = model.launches(plan)
@@ -666,7 +672,9 @@ def main():
                              f"(BASELINE configs[1]{' / configs[4] DP' if world > 1 else ''})",
                     n_layers=n, width=d, batch_per_gpu=B, global_batch=Bg, strategy=args.strategy,
                     parallelism=f"dp{world}", l2="inputs > L2: 8.6 GB of bf16 weights streamed 4x per step",
-                    segments=math.isqrt(n - 1) + 1 if args.strategy == "sqrt" else None),
+                    segments=math.isqrt(n - 1) + 1 if args.strategy == "sqrt" else None,
+                    recompute="concurrent with the next segment's backward (SLM_ALLOC_MIRROR_PARITY plan)"
+                    if overlapped else "sequential (V' order)"),
         roofline=roofline,
         cpu_baseline=cpu,
         e2e=e2e,

@@ -270,12 +270,21 @@ void slm_model_destroy(slm_model* m);
  *   sk_fwd, sk_dx   split-K of the fused forward / dX GEMMs (0 = auto, ~64 CTAs)
  *   fused_bn        N tile of the fused GEMMs (0 = min(batch, 128))
  *   cta_pair        1 = fused GEMMs as CTA pairs (tcgen05 cta_group::2, clusters of 2)
+ *   overlap         1 (default) = chain: each segment's recompute on its own stream, concurrent
+ *                   with the backward of the next segment, when the plan makes that sound
+ *                   (SLM_ALLOC_MIRROR_PARITY plans); other plans run sequentially
+ *   persist         1 = chain: runs of forward / mirror Blocks as one persistent kernel
+ *                   (default 0: measured slower at the bench configuration)
  *   lstm_early_trigger  1 (default) = LSTM element-wise kernels release their dependent launch
  *                   (griddepcontrol.launch_dependents) right after their own dependency wait
  *   lstm_streams    1 (default) = LSTM layer wavefront: one stream per layer + one for the head,
  *                   ordered by per-buffer last-writer / reader events (0 = the caller's stream)
  *   lstm_sk         split-K of the LSTM gates GEMMs (default 2, 0 = one wave of CTAs) */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
+/* Reads an option back, or the read-only state "last_overlap" (1 = the last enqueued chain step
+ * ran its segment recomputes on the recompute stream, concurrently with the backward; option
+ * overlap + a plan that allows it).  SLM_E_ARG for unknown keys. */
+slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* value);
 /* Kernel kinds for slm_model_kernel_times. */
 enum { SLM_K_BN_ACT = 0, SLM_K_GEMM_FWD = 1, SLM_K_GEMM_DX = 2, SLM_K_GEMM_DW = 3, SLM_K_BN_BWD = 4,
        SLM_K_CE = 5, SLM_K_COUNT = 6 };

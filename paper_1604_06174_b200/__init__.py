@@ -237,6 +237,11 @@ class _Model:
     def set_option(self, key, value):
         check(lib.slm_model_set_option(self._h, key.encode(), int(value)), "slm_model_set_option")
 
+    def get_option(self, key):
+        v = C.c_int64()
+        check(lib.slm_model_get_option(self._h, key.encode(), C.byref(v)), "slm_model_get_option")
+        return v.value
+
     def workspace_bytes(self, plan):
         n = C.c_size_t()
         check(lib.slm_workspace_bytes(plan._h, self._h, C.byref(n)), "slm_workspace_bytes")

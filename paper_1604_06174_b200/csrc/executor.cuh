@@ -267,6 +267,8 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int overlap = 1;                            // segment recompute on its own stream, concurrent with the backward of
+                                              // the next segment, when the plan allows it (SLM_ALLOC_MIRROR_PARITY)
   int persist_dbg = 0;                        // persistent kernel phase stamps (scripts/persist_phases.py)
   int persist = 0;                            // runs of forward / mirror Blocks as one persistent kernel (fwd_persist.cuh;
                                               // measured slower at C2: 47.4 / 50.9 ms/step vs 43.2)
@@ -279,10 +281,13 @@ struct slm_model {
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
-  CUtensorMap mW_K, mW_MN, mA_K, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
+  CUtensorMap mW_K, mW_MN, mA_K, mA_K3, mP3, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
+  bool last_overlap = false;           // the last enqueued step ran its recompute on s3
   cudaStream_t s2 = nullptr;           // second stream (dW)
+  cudaStream_t s3 = nullptr;           // recompute stream (option overlap)
+  std::vector<cudaEvent_t> ov_ev;      // its fork/join events
   cudaStream_t s1 = nullptr;           // high-priority critical-path stream (option prio)
   cudaEvent_t prio_ev[2] = {nullptr, nullptr};
   int prio = 0;                        // 1: critical path on s1 (highest priority), dW on s2 (lowest)
@@ -325,6 +330,8 @@ struct slm_model {
     for (auto e : ev_free) cudaEventDestroy(e);
     for (auto e : sync_ev) cudaEventDestroy(e);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
+    for (auto e : ov_ev) cudaEventDestroy(e);
     if (s1) cudaStreamDestroy(s1);
     for (auto e : prio_ev)
       if (e) cudaEventDestroy(e);
@@ -372,7 +379,7 @@ int persist_split(const slm_model& m) {
 }
 
 struct WsLayout {
-  size_t a, stats, gq[3], ab[2], P, da, rowloss, bar, total;
+  size_t a, stats, gq[3], ab[2], P, da, rowloss, bar, a3, stats3, P3, total;
   int sk_fwd, sk_dx, sk_persist;
 };
 WsLayout ws_layout(const slm_model& m) {
@@ -404,6 +411,14 @@ WsLayout ws_layout(const slm_model& m) {
   off += al(B * 4);
   L.bar = off;
   off += 128 * 128;
+  // the recompute stream's own operand / statistics / partial buffers (option overlap)
+  const bool ovw = fused_ok(m) && m.overlap;
+  L.a3 = off;
+  off += ovw ? al(B * d * 4) : 0;
+  L.stats3 = off;
+  off += ovw ? al(2 * d * 4) : 0;
+  L.P3 = off;
+  off += ovw ? al((size_t)L.sk_fwd * B * d * 4) : 0;
   L.total = off;
   return L;
 }
@@ -442,7 +457,8 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 }
 
 slm_status bind_maps(slm_model& m, void* ws) {
-  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3;
+  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3 +
+                  m.overlap * 5;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -456,6 +472,10 @@ slm_status bind_maps(slm_model& m, void* ws) {
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
   if ((st = make_map(&m.mA_K, w + L.a, d, B, bnf)) != SLM_OK) return st;
   if (fz && (st = make_map(&m.mA_Kf, w + L.a, d, B, (uint32_t)B)) != SLM_OK) return st;
+  if (fz && m.overlap) {
+    if ((st = make_map(&m.mA_K3, w + L.a3, d, B, bnf)) != SLM_OK) return st;
+    if ((st = make_map_f32(&m.mP3, w + L.P3, d, (uint64_t)L.sk_fwd * B)) != SLM_OK) return st;
+  }
   if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
   for (int i = 0; i < 3; ++i) {
     if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, bnx)) != SLM_OK) return st;
@@ -480,6 +500,7 @@ slm_status ensure_streams(slm_model& m, int n_layers) {
       for (auto& e : m.prio_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
   }
+  if (m.overlap && !m.s3) CK(cudaStreamCreateWithFlags(&m.s3, cudaStreamNonBlocking));
   const size_t need = 2 * (size_t)n_layers + 8;
   while (m.sync_ev.size() < need) {
     cudaEvent_t e;
@@ -575,12 +596,13 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
                     sBn, sBk, out, ldo, resid, bias);
   };
   // K1 (optionally fused with the forward finalize from split-K partials)
-  auto bn_act = [&](const float* xin, const float* Pp, int nsplit, const float* bias, float* xout, int l) -> cudaError_t {
+  auto bn_act = [&](const float* xin, const float* Pp, int nsplit, const float* bias, float* xout, int l,
+                    cudaStream_t fs = nullptr, void* fa = nullptr, float* fstats = nullptr) -> cudaError_t {
     const float* ga = l < n ? gam + (size_t)l * d : nullptr;
     const float* be = l < n ? bet + (size_t)l * d : nullptr;
     if (fz)
-      return act_rk(B / 32, Pp ? nsplit : 0, st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be, stats,
-                    (bf*)abuf);
+      return act_rk(B / 32, Pp ? nsplit : 0, fs ? fs : st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be,
+                    fstats ? fstats : stats, (bf*)(fa ? fa : abuf));
     if (bf16)
       return launch_k(bn_act_kernel<bf>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (bf*)abuf);
     return launch_k(bn_act_kernel<float>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (float*)abuf);
@@ -611,16 +633,83 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   unsigned bar_count = 0;
   if (PS > 0) CK(cudaMemsetAsync(bar, 0, 128 * 128, st));
 
+  // ---- option overlap (reading A24): after the first mirror, V' alternates mirror runs M_r and
+  // gradient runs N_r.  M_r runs on s3 as soon as M_{r-1} and N_{r-2} are done, i.e. concurrently
+  // with N_{r-1}; N_r waits for M_r.  Enabled only when the plan makes that sound: no tag written
+  // by M_r is touched by N_{r-1}, no tag written by N_{r-1} is read by M_r (SLM_ALLOC_MIRROR_PARITY
+  // plans satisfy it; other plans run sequentially as before).
+  std::vector<int> run_of(ops.size(), -1);
+  std::vector<char> is_m(ops.size(), 0);
+  bool ov = false;
+  int n_runs = 0;
+  if (fz && side && m.overlap && PS == 0 && m.s3) {
+    size_t i = 0;
+    auto mir = [&](size_t k) { return ops[k].type == 0 && p->kind[ops[k].node] == SLM_KIND_MIRROR; };
+    while (i < ops.size() && !mir(i)) ++i;
+    int r = -1;
+    bool prev = false;
+    for (; i < ops.size(); ++i) {
+      const bool im = mir(i);
+      if (im && !prev) ++r;
+      run_of[i] = r;
+      is_m[i] = im;
+      prev = im;
+    }
+    n_runs = r + 1;
+    std::vector<std::set<int>> mw(n_runs), mr(n_runs), nw(n_runs), nrd(n_runs);
+    for (size_t k = 0; k < ops.size(); ++k) {
+      if (run_of[k] < 0) continue;
+      const int q = run_of[k];
+      (is_m[k] ? mw : nw)[q].insert(ops[k].out_tag);
+      (is_m[k] ? mr : nrd)[q].insert(ops[k].in_tag);
+      if (ops[k].aux_tag >= 0) (is_m[k] ? mr : nrd)[q].insert(ops[k].aux_tag);
+    }
+    ov = n_runs > 1;
+    for (int q = 1; q < n_runs && ov; ++q) {
+      for (int t : mw[q])
+        if (nw[q - 1].count(t) || nrd[q - 1].count(t)) ov = false;
+      for (int t : nw[q - 1])
+        if (mr[q].count(t)) ov = false;
+    }
+    while (ov && m.ov_ev.size() < (size_t)(2 * n_runs + 2)) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      m.ov_ev.push_back(e);
+    }
+  }
+  m.last_overlap = ov;
+  int abuf3_node = -1;   // abuf_node of the recompute stream's operand buffer
+  float* stats3 = (float*)(w + L.stats3);
+  void* abuf3 = w + L.a3;
+  float* P3 = (float*)(w + L.P3);
+
   for (size_t oi = 0; oi < ops.size(); ++oi) {
     const Op& o = ops[oi];
     const int l = o.layer;
+    if (ov && run_of[oi] >= 0 && (oi == 0 || run_of[oi - 1] != run_of[oi] || is_m[oi - 1] != is_m[oi])) {
+      const int r = run_of[oi];
+      if (is_m[oi]) {            // start of M_r on s3: st holds everything through N_{r-1}
+        CK(cudaEventRecord(m.ov_ev[2 * r], st));   // E_N[r-1] (r = 0: the forward prefix)
+        if (r == 0) CK(cudaStreamWaitEvent(m.s3, m.ov_ev[0], 0));
+        if (r >= 2) CK(cudaStreamWaitEvent(m.s3, m.ov_ev[2 * (r - 1)], 0));   // E_N[r-2]
+      } else {                   // start of N_r on st: M_r done
+        CK(cudaEventRecord(m.ov_ev[2 * r + 1], m.s3));
+        CK(cudaStreamWaitEvent(st, m.ov_ev[2 * r + 1], 0));
+      }
+    }
     if (o.type == 0) {  // ---------------- forward / mirror Block_l
       const float* xin = X(o.in_tag);
       float* xout = X(o.out_tag);
-      if (!fz || abuf_node != o.in_node) {
-        pbeg(st);
-        CK(bn_act(xin, nullptr, 0, nullptr, nullptr, l));
-        pend(SLM_K_BN_ACT, st);
+      const bool on3 = ov && is_m[oi];
+      cudaStream_t fs = on3 ? m.s3 : st;
+      void* fa = on3 ? abuf3 : abuf;
+      float* fstats = on3 ? stats3 : stats;
+      float* fP = on3 ? P3 : P;
+      int& fnode = on3 ? abuf3_node : abuf_node;
+      if (!fz || fnode != o.in_node) {
+        pbeg(fs);
+        CK(bn_act(xin, nullptr, 0, nullptr, nullptr, l, fs, fa, fstats));
+        pend(SLM_K_BN_ACT, fs);
         ++nl;
       }
       if (PS > 0) {
@@ -659,17 +748,18 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         ++nl;
       } else if (fz) {
         slmk::EpiPartialTma epi{B};
-        pbeg(st);
+        pbeg(fs);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(
-                 fused_n(m), L.sk_fwd, m.mW_K, m.mA_K, d, B, d, l * d, 0, epi, st, pdl, gdbg(SLM_K_GEMM_FWD), &m.mP,
-                 m.cta_pair ? 2 : 1, m.l2_prefetch && l + 1 < n ? (l + 1) * d : -1)) != SLM_OK)
+                 fused_n(m), L.sk_fwd, m.mW_K, on3 ? m.mA_K3 : m.mA_K, d, B, d, l * d, 0, epi, fs, pdl,
+                 gdbg(SLM_K_GEMM_FWD), on3 ? &m.mP3 : &m.mP, m.cta_pair ? 2 : 1,
+                 m.l2_prefetch && l + 1 < n ? (l + 1) * d : -1)) != SLM_OK)
           return s;
-        pend(SLM_K_GEMM_FWD, st);
+        pend(SLM_K_GEMM_FWD, fs);
         // finalize x_{l+1} and produce a_{l+1} for the next Block (BN of layer l+1)
-        pbeg(st);
-        CK(bn_act(xin, P, L.sk_fwd, bvec + (size_t)l * d, xout, l + 1));
-        pend(SLM_K_BN_ACT, st);
-        abuf_node = o.node;
+        pbeg(fs);
+        CK(bn_act(xin, fP, L.sk_fwd, bvec + (size_t)l * d, xout, l + 1, fs, fa, fstats));
+        pend(SLM_K_BN_ACT, fs);
+        fnode = o.node;
         nl += 2;
       } else {
         pbeg(st);

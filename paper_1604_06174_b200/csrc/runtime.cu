@@ -20,6 +20,7 @@
 #include <type_traits>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -172,6 +173,24 @@ slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out) {
 
 void slm_model_destroy(slm_model* m) { delete m; }
 
+slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* value) {
+  if (!m || !key || !value) {
+    set_error("null argument");
+    return SLM_E_ARG;
+  }
+  const std::string k(key);
+  if (k == "last_overlap") *value = m->last_overlap ? 1 : 0;
+  else if (k == "overlap") *value = m->overlap;
+  else if (k == "persist") *value = m->persist;
+  else if (k == "fused") *value = m->fused;
+  else if (k == "use_graph") *value = m->use_graph;
+  else {
+    set_error("unknown or write-only option: " + k);
+    return SLM_E_ARG;
+  }
+  return SLM_OK;
+}
+
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   if (!m || !key) {
     set_error("null argument");
@@ -203,6 +222,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "fused") m->fused = (int)value;
   else if (k == "persist") m->persist = (int)value;
   else if (k == "persist_dbg") m->persist_dbg = (int)value;
+  else if (k == "overlap") m->overlap = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "profile_ts") {
     m->profile_ts = (int)value;
