@@ -133,6 +133,27 @@ slm_status launch_fwd_seg(int B, int S, const CUtensorMap& w, const CUtensorMap&
   return SLM_E_UNSUPPORTED;
 }
 
+// bf16 2-D tensor [rows][inner], box {128, 32}, no swizzle (dW epilogue bulk stores)
+slm_status make_map_bf16_store(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SLM_E_CUDA;
+  }
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {128, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (bf16 store) failed: " + std::to_string((int)r));
+    return SLM_E_CUDA;
+  }
+  return SLM_OK;
+}
+
 // fp32 2-D tensor [rows][inner], box {128, 32}, no swizzle (epilogue bulk stores)
 slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows) {
   EncodeTiledFn enc = get_encode();
@@ -267,6 +288,8 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int dw_tma = 1;                             // dW epilogue: bf16 TMA bulk stores (0 = per-thread stores)
+  int s3_prio = 0;                            // priority of the recompute stream above the lowest (set before the first step)
   int overlap = 1;                            // segment recompute on its own stream, concurrent with the backward of
                                               // the next segment, when the plan allows it (SLM_ALLOC_MIRROR_PARITY)
   int persist_dbg = 0;                        // persistent kernel phase stamps (scripts/persist_phases.py)
@@ -281,7 +304,7 @@ struct slm_model {
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
-  CUtensorMap mW_K, mW_MN, mA_K, mA_K3, mP3, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
+  CUtensorMap mW_K, mW_MN, mA_K, mA_K3, mP3, mdW_st, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
   bool last_overlap = false;           // the last enqueued step ran its recompute on s3
@@ -458,7 +481,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 
 slm_status bind_maps(slm_model& m, void* ws) {
   const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3 +
-                  m.overlap * 5;
+                  m.overlap * 5 + m.dw_tma * 11;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -472,6 +495,7 @@ slm_status bind_maps(slm_model& m, void* ws) {
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
   if ((st = make_map(&m.mA_K, w + L.a, d, B, bnf)) != SLM_OK) return st;
   if (fz && (st = make_map(&m.mA_Kf, w + L.a, d, B, (uint32_t)B)) != SLM_OK) return st;
+  if (fz && m.dw_tma && (st = make_map_bf16_store(&m.mdW_st, m.d.dW, d, n * d)) != SLM_OK) return st;
   if (fz && m.overlap) {
     if ((st = make_map(&m.mA_K3, w + L.a3, d, B, bnf)) != SLM_OK) return st;
     if ((st = make_map_f32(&m.mP3, w + L.P3, d, (uint64_t)L.sk_fwd * B)) != SLM_OK) return st;
@@ -500,7 +524,12 @@ slm_status ensure_streams(slm_model& m, int n_layers) {
       for (auto& e : m.prio_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
   }
-  if (m.overlap && !m.s3) CK(cudaStreamCreateWithFlags(&m.s3, cudaStreamNonBlocking));
+  if (m.overlap && !m.s3) {
+    // s3_prio = k > 0: the recompute stream k levels above the lowest priority
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&m.s3, cudaStreamNonBlocking, std::max(hi, lo - m.s3_prio)));
+  }
   const size_t need = 2 * (size_t)n_layers + 8;
   while (m.sync_ev.size() < need) {
     cudaEvent_t e;
@@ -831,12 +860,20 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
           CK(cudaStreamWaitEvent(m.s2, ef, 0));
           sw = m.s2;
         }
-        slmk::EpiStoreBF16 e2{(bf*)m.d.dW + l * Wl, d};
         pbeg(sw);
-        if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, 1, m.mAb_MN[abi], m.mG_MN[gcur], d, d,
-                                                                     B, 0, 0, e2, sw, pdl && !side,
-                                                                     gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-          return s;
+        if (m.dw_tma) {
+          slmk::EpiStoreBF16Tma e2{l * d};
+          if ((s = launch_tc_bn<slmk::EpiStoreBF16Tma, true, true, false>(m.bn_dw, 1, m.mAb_MN[abi], m.mG_MN[gcur], d,
+                                                                          d, B, 0, 0, e2, sw, pdl && !side,
+                                                                          gdbg(SLM_K_GEMM_DW), &m.mdW_st)) != SLM_OK)
+            return s;
+        } else {
+          slmk::EpiStoreBF16 e2{(bf*)m.d.dW + l * Wl, d};
+          if ((s = launch_tc_bn<slmk::EpiStoreBF16, true, true, false>(m.bn_dw, 1, m.mAb_MN[abi], m.mG_MN[gcur], d,
+                                                                       d, B, 0, 0, e2, sw, pdl && !side,
+                                                                       gdbg(SLM_K_GEMM_DW))) != SLM_OK)
+            return s;
+        }
         pend(SLM_K_GEMM_DW, sw);
         if (side) {
           dw_event[kb] = ev_i;

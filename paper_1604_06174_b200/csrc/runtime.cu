@@ -223,6 +223,14 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "persist") m->persist = (int)value;
   else if (k == "persist_dbg") m->persist_dbg = (int)value;
   else if (k == "overlap") m->overlap = (int)value;
+  else if (k == "dw_tma") m->dw_tma = (int)value;
+  else if (k == "s3_prio") {
+    if (m->s3) {
+      set_error("option s3_prio must be set before the first step");
+      return SLM_E_ARG;
+    }
+    m->s3_prio = (int)value;
+  }
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "profile_ts") {
     m->profile_ts = (int)value;

@@ -239,6 +239,20 @@ struct EpiPartialTma {
   __device__ __forceinline__ void operator()(int, int, const float*, int) const {}
 };
 
+// dW: bf16(acc) written by TMA bulk tensor stores from a smem staging box (tmC maps the output as
+// [rows][M] bf16, box {128, 32}); row of column n = row_base + n (layer l's block of dW)
+struct EpiStoreBF16Tma {
+  static constexpr bool kTma = true;
+  static constexpr bool kHalf = true;
+  int row_base;
+  __device__ __forceinline__ int row0(int) const { return row_base; }
+  __device__ __forceinline__ void operator()(int, int, const float*, int) const {}
+};
+template <class E, class = void>
+struct EpiHalf : std::false_type {};
+template <class E>
+struct EpiHalf<E, std::void_t<decltype(E::kHalf)>> : std::bool_constant<E::kHalf> {};
+
 // Epilogues with kCell = true (the LSTM gates + cell epilogue, lstm_kernels.cuh) load A as four
 // 32-row boxes, rows q*H + m0/4 .. +32 of gate q (one tile = 32 hidden units x 4 gates), and
 // run their own cell(...) epilogue with the whole CTA.
@@ -494,9 +508,11 @@ __global__ void __launch_bounds__(128, 1)
   if constexpr (EpiCell<Epi>::value) {
     epi.template cell<BN>(trow, m0, n0, warp, lane, reinterpret_cast<float*>(smem));
   } else if constexpr (Epi::kTma) {
-    // fp32 tile -> smem box [32 n][128 m] (a warp writes 128 contiguous bytes: conflict-free)
-    // -> cp.async.bulk.tensor store, double-buffered; the pipeline smem is free after the MMAs.
-    float* stage = reinterpret_cast<float*>(smem);
+    // fp32 (or bf16, EpiHalf) tile -> smem box [32 n][128 m] (a warp writes 128 (64) contiguous
+    // bytes: conflict-free) -> cp.async.bulk.tensor store, double-buffered; the pipeline smem is
+    // free after the MMAs.
+    constexpr bool HALF = EpiHalf<Epi>::value;
+    constexpr int BUF_BYTES = 32 * 128 * (HALF ? 2 : 4);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       const int buf = (c >> 5) & 1;
@@ -506,16 +522,23 @@ __global__ void __launch_bounds__(128, 1)
       }
       float acc[32];
       tmem_ld32(trow + c, acc);
-      float* sp = stage + buf * 4096 + warp * 32 + lane;
+      uint8_t* sbuf = smem + buf * BUF_BYTES;
+      if constexpr (HALF) {
+        __nv_bfloat16* sp = reinterpret_cast<__nv_bfloat16*>(sbuf) + warp * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) sp[j * 128] = acc[j];
+        for (int j = 0; j < 32; ++j) sp[j * 128] = __float2bfloat16_rn(acc[j]);
+      } else {
+        float* sp = reinterpret_cast<float*>(sbuf) + warp * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sp[j * 128] = acc[j];
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (threadIdx.x == 0) {
         asm volatile(
             "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                 reinterpret_cast<uint64_t>(&tmC)),
-            "r"(smem_u32(stage + buf * 4096)), "r"(m0), "r"(epi.row0(ks) + n0 + c)
+            "r"(smem_u32(sbuf)), "r"(m0), "r"(epi.row0(ks) + n0 + c)
             : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }

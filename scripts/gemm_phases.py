@@ -18,10 +18,15 @@ def run(kind, bn, split, K=2048, impl=0, M=2048, N=256):
         B = torch.randn(N, K, device=dev).bfloat16()
         out = torch.empty(split, N, M, device=dev)
         resid, bias = torch.randn(N, M, device=dev), torch.randn(M, device=dev)
-    else:
+    elif kind == 1:
         A = torch.randn(K, M, device=dev).bfloat16()
         B = torch.randn(N, K, device=dev).bfloat16()
         out = torch.empty(split, N, M, device=dev)
+        resid = bias = None
+    else:   # dW: A = act [K][M], B = g [K][N] (both MN-major), out bf16 [N][M]
+        A = torch.randn(K, M, device=dev).bfloat16()
+        B = torch.randn(K, N, device=dev).bfloat16()
+        out = torch.empty(N, M, device=dev).bfloat16()
         resid = bias = None
     ncta = (M // 128) * (N // bn) * split
     ts = torch.zeros(ncta * 8, dtype=torch.int64, device=dev)
