@@ -270,7 +270,7 @@ def run_lstm(args):
 
     # grouped sharing (reading A22): tags never cross layers -> less memory and no false
     # cross-layer dependencies for the layer wavefront
-    AF = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_GROUPED
+    AF = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_GROUPED | (slm.ALLOC_MIRROR_PARITY if args.lstm_parity else 0)
     plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg), alloc_flags=AF)
     torch.cuda.synchronize()
     base_mem = torch.cuda.memory_allocated(dev)
@@ -408,6 +408,8 @@ def main():
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
     ap.add_argument("--mirror-parity", type=int, default=1,
                     help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
+    ap.add_argument("--lstm-parity", type=int, default=0,
+                    help="LSTM plan with SLM_ALLOC_MIRROR_PARITY (with --opt lstm_streams=2: recompute on its own streams)")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
     ap.add_argument("--model", default="chain", choices=["chain", "lstm"],
                     help="chain = configs[1] (default, the metric's config); lstm = configs[2]")

@@ -218,6 +218,8 @@ cudaError_t bwd_rk(int R, int ns, cudaStream_t st, bool pdl, int d, const float*
 
 }  // namespace
 
+constexpr int kMaxLag = 8;
+
 // ====================================================================== model
 struct slm_comm {
   nccl_comm_t comm = nullptr;
@@ -288,6 +290,7 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int dw_lag = 2;                             // dW ring depth: layers the dW stream may lag the dX chain (2..8)
   int dw_tma = 1;                             // dW epilogue: bf16 TMA bulk stores (0 = per-thread stores)
   int s3_prio = 0;                            // priority of the recompute stream above the lowest (set before the first step)
   int overlap = 1;                            // segment recompute on its own stream, concurrent with the backward of
@@ -304,7 +307,7 @@ struct slm_model {
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
-  CUtensorMap mW_K, mW_MN, mA_K, mA_K3, mP3, mdW_st, mA_Kf, mA_MN, mG_K[3], mG_MN[3], mAb_MN[2], mP;
+  CUtensorMap mW_K, mW_MN, mA_K, mA_K3, mP3, mdW_st, mA_Kf, mA_MN, mG_K[kMaxLag + 1], mG_MN[kMaxLag + 1], mAb_MN[kMaxLag], mP;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
   bool last_overlap = false;           // the last enqueued step ran its recompute on s3
@@ -401,8 +404,14 @@ int persist_split(const slm_model& m) {
   return 0;
 }
 
+// dW lag ring (fused lowering): the dW GEMM of backward k reads ab[k % NA] and gq[k % NG]; bn_bwd of
+// backward k overwrites gq[(k+1) % NG] and ab[k % NA], so it waits for dW of backward k - NA
+// (NG = NA + 1): NA layers of slack between the dX chain and the dW stream (option dw_lag)
+int dw_na(const slm_model& m) { return std::max(2, std::min(kMaxLag, m.dw_lag)); }
+int dw_ng(const slm_model& m) { return dw_na(m) + 1; }
+
 struct WsLayout {
-  size_t a, stats, gq[3], ab[2], P, da, rowloss, bar, a3, stats3, P3, total;
+  size_t a, stats, gq[kMaxLag + 1], ab[kMaxLag], P, da, rowloss, bar, a3, stats3, P3, total;
   int sk_fwd, sk_dx, sk_persist;
 };
 WsLayout ws_layout(const slm_model& m) {
@@ -418,11 +427,11 @@ WsLayout ws_layout(const slm_model& m) {
   off += al(B * d * 4);
   L.stats = off;
   off += al(2 * d * 4);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < dw_ng(m); ++i) {
     L.gq[i] = off;
     off += al(B * d * 2);
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < dw_na(m); ++i) {
     L.ab[i] = off;
     off += al(B * d * 2);
   }
@@ -481,7 +490,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 
 slm_status bind_maps(slm_model& m, void* ws) {
   const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3 +
-                  m.overlap * 5 + m.dw_tma * 11;
+                  m.overlap * 5 + m.dw_tma * 11 + m.dw_lag * 13;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -501,11 +510,11 @@ slm_status bind_maps(slm_model& m, void* ws) {
     if ((st = make_map_f32(&m.mP3, w + L.P3, d, (uint64_t)L.sk_fwd * B)) != SLM_OK) return st;
   }
   if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < dw_ng(m); ++i) {
     if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, bnx)) != SLM_OK) return st;
     if ((st = make_map(&m.mG_MN[i], w + L.gq[i], d, B, 64)) != SLM_OK) return st;
   }
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < dw_na(m); ++i)
     if ((st = make_map(&m.mAb_MN[i], w + L.ab[i], d, B, 64)) != SLM_OK) return st;
   if ((st = make_map_f32(&m.mP, w + L.P, d, (uint64_t)std::max({L.sk_fwd, L.sk_dx, L.sk_persist}) * B)) != SLM_OK)
     return st;
@@ -554,8 +563,11 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   uint8_t* w = (uint8_t*)ws;
   float* stats = (float*)(w + L.stats);
   void* abuf = w + L.a;
-  bf* gq[3] = {(bf*)(w + L.gq[0]), (bf*)(w + L.gq[1]), (bf*)(w + L.gq[2])};
-  bf* ab[2] = {(bf*)(w + L.ab[0]), (bf*)(w + L.ab[1])};
+  const int NA = dw_na(m), NG = dw_ng(m);
+  bf* gq[kMaxLag + 1];
+  bf* ab[kMaxLag];
+  for (int i = 0; i < NG; ++i) gq[i] = (bf*)(w + L.gq[i]);
+  for (int i = 0; i < NA; ++i) ab[i] = (bf*)(w + L.ab[i]);
   float* P = (float*)(w + L.P);
   const long pslice = (long)B * d;
   float* da = (float*)(w + L.da);
@@ -837,7 +849,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       float* dga = m.d.dgamma + (size_t)l * d;
       float* dbe = m.d.dbeta + (size_t)l * d;
       if (fz) {
-        const int gnext = (gcur + 1) % 3, abi = kb & 1;
+        const int gnext = (gcur + 1) % NG, abi = kb % NA;
         // dX: P[s] = g_{l+1} W_l over K slice s
         slmk::EpiPartialTma e1{B};
         pbeg(st);
@@ -846,8 +858,8 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
                  m.cta_pair ? 2 : 1, m.l2_prefetch && l > 0 ? (l - 1) * d : -1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX, st);
-        // bn_bwd(k) overwrites gq[(k+1)%3] and ab[k%2], last read by dW of backward k-2
-        if (side && kb >= 2 && dw_event[kb - 2] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - 2]], 0));
+        // bn_bwd(k) overwrites gq[(k+1)%NG] and ab[k%NA], last read by dW of backward k-NA
+        if (side && kb >= NA && dw_event[kb - NA] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - NA]], 0));
         pbeg(st);
         CK(bwd_rk(B / 32, L.sk_dx, st, pdl, d, (const float*)P, (unsigned)pslice, xl, ga, be, g, dxl, dga, dbe, dbp,
                   gq[gnext], ab[abi]));

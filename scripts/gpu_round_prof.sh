@@ -9,6 +9,7 @@ TAG=${1:-r1}
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout -s KILL 900 python bench.py > gpurun_out/${TAG}_bench.txt 2>&1
+timeout -s KILL 900 python bench.py --model lstm --steps 3 > gpurun_out/${TAG}_bench_lstm.txt 2>&1
 echo "bench rc=$?" >> gpurun_out/${TAG}_bench.txt
 timeout -s KILL 1500 $NCU --metrics gpu__time_duration.sum --clock-control none -s 31000 -c 10200 --csv \
   --log-file gpurun_out/${TAG}_launches.csv \

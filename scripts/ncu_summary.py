@@ -32,7 +32,11 @@ for r in data:
         if i is None or not r[i]:
             vals.append("-")
             continue
-        v = float(r[i].replace(",", ""))
+        try:
+            v = float(r[i].replace(",", ""))
+        except ValueError:
+            vals.append("-")
+            continue
         u = units[i]
         if key == "gpu__time_duration.sum" and u == "us":
             sc = 1

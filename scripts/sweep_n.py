@@ -64,9 +64,12 @@ def main():
         g = {k: torch.empty_like(v) for k, v in p.items()}
         model = slm.ChainModel(p, g, dtype="bf16", batch=B)
         graph = slm.Graph.chain(n, B, D)
-        plans = [("none", slm.Plan(graph, "none")), ("sqrt", slm.Plan(graph, "sqrt"))]
+        par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+        plans = [("none", slm.Plan(graph, "none")), ("sqrt", slm.Plan(graph, "sqrt")),
+                 ("sqrt + A24 (overlapped recompute)", slm.Plan(graph, "sqrt", alloc_flags=par))]
         if n == 1024:
-            plans += [("search (App. A)", slm.Plan(graph, "search")),
+            plans += [("search (App. A) + A24", slm.Plan(graph, "search", alloc_flags=par)),
+                      ("search (App. A)", slm.Plan(graph, "search")),
                       ("recursive k=1", slm.Plan(graph, "recursive", k=1)),
                       ("recursive k=2", slm.Plan(graph, "recursive", k=2))]
             u = B * D * 4

@@ -315,3 +315,21 @@ def test_overlapped_recompute_bitwise(slm, n, B, d):
     torch.cuda.synchronize()
     assert model.get_option("last_overlap") == 0
     assert float(loss.item()) == ref_loss
+
+
+def test_dw_lag_ring_bitwise(slm):
+    """Option dw_lag (ring of NA bf16 dW operands): only the schedule changes, so any depth gives
+    the default step's bits, with and without the overlapped recompute."""
+    n, B, d = 24, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=9)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+    for lag in (3, 5, 8):
+        p, g, x0, y = _dev(inp, "bf16")
+        model = slm.ChainModel(p, g, dtype="bf16", batch=B, dw_lag=lag)
+        for af in (3, par):
+            loss = model.step(slm.Plan(slm.Graph.chain(n, B, d), "sqrt", alloc_flags=af), x0, y)
+            torch.cuda.synchronize()
+            assert float(loss.item()) == ref_loss, (lag, af)
+            for k in ref:
+                assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (lag, af, k)

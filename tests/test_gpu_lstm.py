@@ -146,7 +146,7 @@ def test_lstm_wavefront_matches_single_stream(slm, cfg):
     ref_loss, ref, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
                             lstm_streams=0)
     for rep in range(4):
-        for pdl, af, ns in ((1, 3, 1), (0, 3, 1), (1, 7, 1), (1, 7, 2), (0, 3, 2)):
+        for pdl, af, ns in ((1, 3, 1), (0, 3, 1), (1, 7, 1), (1, 7, 2), (0, 3, 2), (1, 23, 2), (0, 19, 2)):
             loss, g, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(3),
                               alloc_flags=af, lstm_streams=ns, pdl=pdl)
             assert loss == ref_loss, (rep, pdl, af)
