@@ -292,14 +292,23 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256, groups=None)
     nodes = gg.nodes
     mpar = {}
     if flags & A_MIRROR_PARITY:
-        run, prev = -1, False
-        for v in gg.order:
-            im = nodes[v].kind == "mirror"
-            if im and not prev:
-                run += 1
-            if im:
-                mpar[v] = run % 2
-            prev = im
+        # recompute phase of each mirror (reading A24): a maximal run of consecutive mirrors in V'
+        # joins the latest phase one of its mirrors reads a mirror of; otherwise it starts a new one
+        phase, n_phase, order, i = {}, 0, gg.order, 0
+        while i < len(order):
+            if nodes[order[i]].kind != "mirror":
+                i += 1
+                continue
+            j = i
+            while j < len(order) and nodes[order[j]].kind == "mirror":
+                j += 1
+            ph = max((phase[u] for k in range(i, j) for u in nodes[order[k]].preds if u in phase), default=-1)
+            if ph < 0:
+                ph, n_phase = n_phase, n_phase + 1
+            for k in range(i, j):
+                phase[order[k]] = ph
+                mpar[order[k]] = ph % 2
+            i = j
 
     def grp(v):
         g = groups[nodes[v].orig] if (flags & A_GROUPED) and groups is not None else 0

@@ -390,16 +390,32 @@ void allocate(const Built& b, int flags, int64_t align, Alloc* out, const std::v
   const auto& nodes = b.nodes;
   const bool grouped = (flags & SLM_ALLOC_GROUPED) != 0, by_kind = (flags & SLM_ALLOC_GROUP_MIRRORS) != 0;
   const bool parity = (flags & SLM_ALLOC_MIRROR_PARITY) != 0;
-  // MIRROR_PARITY: parity of the mirror run (maximal run of consecutive mirrors in V') of each mirror
+  // MIRROR_PARITY (reading A24): recompute phase of each mirror.  A maximal run of consecutive
+  // mirrors in V' joins the latest phase one of its mirrors reads a mirror of (it continues that
+  // segment's re-computation); a run that reads no earlier mirror starts a new phase.  The tag
+  // group of a mirror is the parity of its phase.
   std::vector<int> mpar(nodes.size(), 0);
   if (parity) {
-    int run = -1;
-    bool prev = false;
-    for (int v : b.order) {
-      const bool im = nodes[v].kind == SLM_KIND_MIRROR;
-      if (im && !prev) ++run;
-      if (im) mpar[v] = run & 1;
-      prev = im;
+    std::vector<int> phase(nodes.size(), -1);
+    int n_phase = 0;
+    const auto& ord = b.order;
+    for (size_t i = 0; i < ord.size();) {
+      if (nodes[ord[i]].kind != SLM_KIND_MIRROR) {
+        ++i;
+        continue;
+      }
+      size_t j = i;
+      while (j < ord.size() && nodes[ord[j]].kind == SLM_KIND_MIRROR) ++j;
+      int ph = -1;
+      for (size_t k = i; k < j; ++k)
+        for (int u : nodes[ord[k]].preds)
+          if (nodes[u].kind == SLM_KIND_MIRROR && phase[u] >= 0) ph = std::max(ph, phase[u]);
+      if (ph < 0) ph = n_phase++;
+      for (size_t k = i; k < j; ++k) {
+        phase[ord[k]] = ph;
+        mpar[ord[k]] = ph & 1;
+      }
+      i = j;
     }
   }
   auto grp = [&](int v) {
