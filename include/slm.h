@@ -150,8 +150,9 @@ enum { SLM_PLAN_NONE = 0, SLM_PLAN_SQRT = 1, SLM_PLAN_BUDGET = 2, SLM_PLAN_SEARC
  * layer wavefront keeps its concurrency (reading A22; an extension, not the paper). */
 /* SLM_ALLOC_GROUP_MIRRORS: re-computed (mirror) nodes and the other nodes never share a tag, so
  * the recompute of one segment does not wait for the backward of the next (A22). */
-/* SLM_ALLOC_MIRROR_PARITY: like GROUP_MIRRORS, and a mirror reuses only tags of mirrors whose run
- * (maximal sequence of consecutive mirrors in V') has the same parity, so the recompute of segment
+/* SLM_ALLOC_MIRROR_PARITY: like GROUP_MIRRORS, and a mirror reuses only tags of mirrors whose
+ * recompute phase has the same parity (a maximal run of consecutive mirrors in V' continues the
+ * latest phase it reads a mirror of, else starts a new one), so the recompute of segment
  * j-1 writes memory disjoint from everything the backward of segment j reads or writes: the
  * executor runs the two concurrently (reading A24; an extension, not the paper).
  * Costs one more segment of mirrors (still O(sqrt n) for the sqrt plan). */

@@ -287,8 +287,7 @@ def allocate(gg: GradGraph, flags=A_INPLACE | A_SHARING, align=256, groups=None)
     Offsets: reading A9.  A_GROUPED (reading A22, an extension): step (2) only considers free
     tags created by a node of the same allocation group (groups[orig]); A_GROUP_MIRRORS further
     separates mirror nodes from the others; A_MIRROR_PARITY (reading A24) separates them too and
-    lets a mirror reuse only tags of mirrors whose run (maximal sequence of consecutive mirrors
-    in V') has the same parity."""
+    lets a mirror reuse only tags of mirrors whose recompute phase has the same parity."""
     nodes = gg.nodes
     mpar = {}
     if flags & A_MIRROR_PARITY:
