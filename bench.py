@@ -408,7 +408,7 @@ def main():
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
     ap.add_argument("--mirror-parity", type=int, default=1,
                     help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
-    ap.add_argument("--lstm-parity", type=int, default=0,
+    ap.add_argument("--lstm-parity", type=int, default=1,
                     help="LSTM plan with SLM_ALLOC_MIRROR_PARITY (with --opt lstm_streams=2: recompute on its own streams)")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
     ap.add_argument("--model", default="chain", choices=["chain", "lstm"],

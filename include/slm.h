@@ -278,8 +278,11 @@ void slm_model_destroy(slm_model* m);
  *                   (default 0: measured slower at the bench configuration)
  *   lstm_early_trigger  1 (default) = LSTM element-wise kernels release their dependent launch
  *                   (griddepcontrol.launch_dependents) right after their own dependency wait
- *   lstm_streams    1 (default) = LSTM layer wavefront: one stream per layer + one for the head,
- *                   ordered by per-buffer last-writer / reader events (0 = the caller's stream)
+ *   lstm_streams    1 = LSTM layer wavefront: one stream per layer + one for the head, ordered
+ *                   by per-buffer last-writer / reader events (0 = the caller's stream);
+ *                   2 (default) = plus one stream per layer for re-computed (mirror) units, so
+ *                   with a SLM_ALLOC_MIRROR_PARITY plan the recompute of a time segment runs
+ *                   concurrently with the backward of the next one
  *   lstm_sk         split-K of the LSTM gates GEMMs (default 2, 0 = one wave of CTAs) */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
 /* Reads an option back, or the read-only state "last_overlap" (1 = the last enqueued chain step

@@ -298,7 +298,7 @@ struct slm_model {
   int persist_dbg = 0;                        // persistent kernel phase stamps (scripts/persist_phases.py)
   int persist = 0;                            // runs of forward / mirror Blocks as one persistent kernel (fwd_persist.cuh;
                                               // measured slower at C2: 47.4 / 50.9 ms/step vs 43.2)
-  int lstm_streams = 1;                       // LSTM: layer wavefront over L+1 streams
+  int lstm_streams = 2;                       // LSTM: layer wavefront over L+1 streams (2: + L mirror streams)
   int lstm_grid = 1;                          // LSTM element-wise grids sized to the work
   int l2_prefetch = 0;                        // chain GEMMs pull the next layer's W tile into L2 (measured: no gain)
   int lstm_sk = 1;                            // LSTM: split-K of the gates GEMMs (0 = auto; 1 measured best with the wavefront)
