@@ -376,7 +376,7 @@ def run_lstm(args):
         ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
         data="synthetic (seeded NumPy, synth.lstm_inputs: PyTorch-default uniform LSTM init, x~N(0,1))",
         config=dict(workload=lstm_workload(args), n_layers=L, hidden=H, unroll=T, batch=B, n_in=I, classes=C,
-                    segment=args.seg, parallelism=f"replicas{world}" if world > 1 else "single",
+                    segment=args.seg, recompute="concurrent with the next segment's backward (A24 plan, mirror streams)" if args.lstm_parity else "sequential", parallelism=f"replicas{world}" if world > 1 else "single",
                     l2="inputs > L2: 33 MB of bf16 weights + 24 GB of no-ckpt activations; the ckpt step re-reads "
                        "W every time step (L2-resident by design)"),
         roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches * args.steps), clocks=clocks,
