@@ -478,3 +478,37 @@ def test_mirror_parity_concurrent_recompute_is_sound(n):
         except AssertionError:
             bad += 1
     assert bad > 0
+
+
+def test_mirror_parity_lstm_segments_disjoint():
+    """A24 on the LSTM's time-segment plan: V' interleaves one-node mirror runs with the head
+    gradients inside a segment's re-computation, so a plain run parity would give consecutive
+    segments the same tags.  The recompute-phase rule must keep the mirror tags of every two
+    consecutive time segments (identified here by the mirrored node's time step, independently
+    of the rule) disjoint, while the plain grouped plan shares them."""
+    L, T, seg = 2, 24, 6
+    g = G.lstm_graph(L, T, 2, 3, 2)
+    m = [0] * len(g)
+    step_of, t = {}, -1
+    for v, nd in enumerate(g.nodes):
+        if nd.op == G.INPUT:
+            t += 1
+        step_of[v] = t
+        if nd.op in (G.LSTM_GATES, G.LSTM_CELL) and not (nd.op == G.LSTM_CELL and t % seg == seg - 1):
+            m[v] = 1
+
+    def seg_tags(p):
+        out = {}
+        for v in p.gg.order:
+            nd = p.gg.nodes[v]
+            if nd.kind == "mirror":
+                out.setdefault(step_of[nd.orig] // seg, set()).add(p.alloc.tag_of[v])
+        return out
+
+    fl = P.A_INPLACE | P.A_SHARING
+    st = seg_tags(P.plan(g, P.S_EXPLICIT, m=m, alloc_flags=fl | P.A_MIRROR_PARITY))
+    assert len(st) == T // seg
+    for j in range(1, T // seg):
+        assert not (st[j] & st[j - 1]), j
+    plain = seg_tags(P.plan(g, P.S_EXPLICIT, m=m, alloc_flags=fl | P.A_GROUP_MIRRORS))
+    assert any(plain[j] & plain[j - 1] for j in range(1, T // seg))
