@@ -107,6 +107,34 @@ slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorM
   return SLM_E_UNSUPPORTED;
 }
 
+// forward Block as one cluster kernel (blk_cluster.cuh), split-K SK in {2, 4}
+template <int SK>
+slm_status launch_blk_cl_t(const CUtensorMap& w, const CUtensorMap& a, int d, int l, int n, const float* xin,
+                           float* xout, const float* bias, const float* gam, const float* bet, float* stats,
+                           __nv_bfloat16* aout, cudaStream_t st, bool pdl, int dbg) {
+  using C = slmk::BlkClCfg<SK>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(slmk::blk_fwd_cl_kernel<SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CK(launch_kc(slmk::blk_fwd_cl_kernel<SK>, dim3(d / 128 * C::CL), dim3(C::THREADS), C::SMEM, st, pdl, C::CL, w, a, d,
+               l, n, xin, xout, bias, gam, bet, stats, aout, dbg));
+  return SLM_OK;
+}
+slm_status launch_blk_cl(int sk, const CUtensorMap& w, const CUtensorMap& a, int d, int l, int n, const float* xin,
+                         float* xout, const float* bias, const float* gam, const float* bet, float* stats,
+                         __nv_bfloat16* aout, cudaStream_t st, bool pdl, int dbg) {
+  (void)sk;
+  return launch_blk_cl_t<2>(w, a, d, l, n, xin, xout, bias, gam, bet, stats, aout, st, pdl, dbg);
+}
+cudaError_t launch_bn_act_cl(int sk, const float* x, const float* gam, const float* bet, int d, float* stats,
+                             __nv_bfloat16* a, cudaStream_t st, bool pdl) {
+  (void)sk;
+  return launch_k(slmk::bn_act_cl_kernel<2>, dim3(d / slmk::BlkClCfg<2>::FK), dim3(256), 0, st, pdl, x, gam, bet, d,
+                  stats, a);
+}
+
 // persistent forward run (fwd_persist.cuh): B in {64, 128, 256}, S in {4, 8, 16}
 template <int B_, int S_>
 slm_status launch_fwd_seg_t(const CUtensorMap& w, const CUtensorMap& a, const slmk::FwdSegArgs& A, int grid,
@@ -290,6 +318,8 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int blk_cluster = 0;                        // forward Block as one cluster kernel (blk_cluster.cuh; B = 256;
+                                              // measured 35.2 vs 35.3 ms/step at C2: within noise, default off)
   int dw_lag = 2;                             // dW ring depth: layers the dW stream may lag the dX chain (2..8)
   int dw_tma = 1;                             // dW epilogue: bf16 TMA bulk stores (0 = per-thread stores)
   int s3_prio = 0;                            // priority of the recompute stream above the lowest (set before the first step)
@@ -490,7 +520,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 
 slm_status bind_maps(slm_model& m, void* ws) {
   const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3 +
-                  m.overlap * 5 + m.dw_tma * 11 + m.dw_lag * 13;
+                  m.overlap * 5 + m.dw_tma * 11 + m.dw_lag * 13 + m.blk_cluster * 17;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -747,12 +777,28 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
       float* fstats = on3 ? stats3 : stats;
       float* fP = on3 ? P3 : P;
       int& fnode = on3 ? abuf3_node : abuf_node;
+      // split-K 2 only: SK = 4 (clusters of 8) measured 19.7 us per Block at C2 and did not match the
+      // default lowering at d = 2048 (test_cluster_block_option); not dispatched
+      const int csk = 2;
+      const bool clk = fz && m.blk_cluster && B == 256 && PS == 0 && fused_n(m) == 128 && !m.cta_pair;
       if (!fz || fnode != o.in_node) {
         pbeg(fs);
-        CK(bn_act(xin, nullptr, 0, nullptr, nullptr, l, fs, fa, fstats));
+        if (clk)
+          CK(launch_bn_act_cl(csk, xin, gam + (size_t)l * d, bet + (size_t)l * d, d, fstats, (bf*)fa, fs, pdl));
+        else
+          CK(bn_act(xin, nullptr, 0, nullptr, nullptr, l, fs, fa, fstats));
         pend(SLM_K_BN_ACT, fs);
         ++nl;
       }
+      if (clk) {
+        pbeg(fs);
+        if ((s = launch_blk_cl(csk, m.mW_K, on3 ? m.mA_K3 : m.mA_K, d, l, n, xin, xout, bvec, gam, bet, fstats, (bf*)fa,
+                               fs, pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
+          return s;
+        pend(SLM_K_GEMM_FWD, fs);
+        fnode = o.node;
+        ++nl;
+      } else
       if (PS > 0) {
         // the run of chained forward / mirror Blocks starting here (each reads the previous one's
         // output), up to kSegMax per launch

@@ -31,6 +31,7 @@
 #include "slm_internal.h"
 #include "tc_gemm.cuh"
 #include "fwd_persist.cuh"
+#include "blk_cluster.cuh"
 
 using namespace slm;
 
@@ -225,6 +226,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "overlap") m->overlap = (int)value;
   else if (k == "dw_tma") m->dw_tma = (int)value;
   else if (k == "dw_lag") m->dw_lag = (int)value;
+  else if (k == "blk_cluster") m->blk_cluster = (int)value;
   else if (k == "s3_prio") {
     if (m->s3) {
       set_error("option s3_prio must be set before the first step");

@@ -333,3 +333,37 @@ def test_dw_lag_ring_bitwise(slm):
             assert float(loss.item()) == ref_loss, (lag, af)
             for k in ref:
                 assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (lag, af, k)
+
+
+@pytest.mark.parametrize("sk,n,d", [(2, 4, 256), (2, 10, 512), (2, 4, 2048)])
+def test_cluster_block_option(slm, sk, n, d):
+    """Option blk_cluster = SK (blk_cluster.cuh: the forward Block as one kernel, split-K SK
+    partials reduced over DSMEM inside a 2 SK-CTA cluster, batch statistics exchanged between
+    the batch halves): within the bf16 tolerance of the oracle (small sizes, ReLU-margin inputs)
+    and of the default lowering (n = 10, like the tile options), and checkpointed ==
+    non-checkpointed bit for bit for every strategy and with the overlapped recompute (the K1
+    before a mirror run reproduces the kernel's statistics)."""
+    B = 256
+    small = n * B * d <= 300_000
+    inp = margin_inputs(n, B, d, "bf16") if small else synth.chain_inputs(n, B, d, dtype="bf16", seed=21)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, blk_cluster=sk)
+    if small:
+        ol, og, _ = _oracle(n, B, d, "bf16", inp)
+        assert abs(ref_loss - ol) <= 2e-2 * abs(ol)
+        for k in og:
+            assert _rel(ref[k], og[k]) <= 2e-2, (k, _rel(ref[k], og[k]))
+    elif n <= 10:
+        dl, dg, _ = _run(slm, n, B, d, "bf16", "none", inp)
+        assert abs(ref_loss - dl) <= 2e-2 * abs(dl)
+        for k in dg:
+            assert _rel(ref[k], dg[k]) <= 2e-2, (k, _rel(ref[k], dg[k]))
+    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+    for strategy, af in (("sqrt", 3), ("search", 3), ("recursive", 3), ("sqrt", par)):
+        p, g, x0, y = _dev(inp, "bf16")
+        model = slm.ChainModel(p, g, dtype="bf16", batch=B, blk_cluster=sk)
+        for _ in range(2):
+            loss = model.step(slm.Plan(slm.Graph.chain(n, B, d), strategy, alloc_flags=af), x0, y)
+            torch.cuda.synchronize()
+            assert float(loss.item()) == ref_loss, (strategy, af)
+            for k in ref:
+                assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (strategy, af, k)
