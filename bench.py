@@ -451,10 +451,10 @@ def main():
                     warmup=args.warmup, ms_per_step=r["ms_per_step"], higher_is_better=True,
                     scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
                     impl="reference",
-                    config=dict(workload=f"chain n={args.layers} d={args.width} B={args.batch} "
-                                         f"sqrt(n) checkpointed step (BASELINE configs[1])",
-                                n_layers=args.layers, width=args.width, batch=args.batch,
-                                strategy="sqrt"),
+                    config=dict(workload=f"chain n={args.layers} d={args.width} B={args.batch}/GPU {args.strategy} "
+                                         f"checkpointed step (BASELINE configs[1])",
+                                n_layers=args.layers, width=args.width, batch_per_gpu=args.batch,
+                                global_batch=args.batch, strategy=args.strategy, parallelism="dp1"),
                     cpu_baseline=dict(value=r["value"], unit=UNIT, cores=r["cores"], kind="oracle",
                                       sample=r["sample"]),
                     e2e=dict(value=r["value"], unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
