@@ -196,6 +196,29 @@ def chain_graph(n_layers: int, batch: int, width: int, elem_bytes: int = 4) -> G
                  dims=dict(n_layers=n_layers, batch=batch, width=width))
 
 
+def preact_resnet_graph(depths, sizes) -> Graph:
+    """Op-granularity pre-activation residual network for the paper's strategy comparison
+    (Sec. 5.1 / Fig. 5): stage s has depths[s] layers whose
+    feature maps are sizes[s] bytes; a layer ("conv-bn-relu counted as one layer") is
+    BN(x) -> ReLU -> FC (the conv / GEMM stand-in) -> Add(x, .) = the next x.  Node 0 = Input
+    (sizes[0]); the last x feeds a SoftmaxCE (4-byte loss).  Stage transitions are a plain FC
+    to the next size (a projection)."""
+    nodes = [Node(INPUT, [], sizes[0])]
+    x = 0
+    for st, (dep, sz) in enumerate(zip(depths, sizes)):
+        if nodes[x].out_bytes != sz:
+            nodes.append(Node(FC, [x], sz))
+            x = len(nodes) - 1
+        for _ in range(dep):
+            nodes.append(Node(BN, [x], sz))
+            nodes.append(Node(RELU, [len(nodes) - 1], sz))
+            nodes.append(Node(FC, [len(nodes) - 1], sz))
+            nodes.append(Node(ADD, [x, len(nodes) - 1], sz))
+            x = len(nodes) - 1
+    nodes.append(Node(SOFTMAX_CE, [x], 4, F_NOT_CANDIDATE))
+    return Graph(nodes, [len(nodes) - 1], kind="dag", dims=dict(depths=list(depths)))
+
+
 def unit_chain(n: int, unit: int = 1) -> Graph:
     """n Block nodes of size ``unit`` after an Input of size ``unit`` — no loss node.
 

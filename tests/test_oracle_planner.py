@@ -512,3 +512,39 @@ def test_mirror_parity_lstm_segments_disjoint():
         assert not (st[j] & st[j - 1]), j
     plain = seg_tags(P.plan(g, P.S_EXPLICIT, m=m, alloc_flags=fl | P.A_GROUP_MIRRORS))
     assert any(plain[j] & plain[j - 1] for j in range(1, T // seg))
+
+
+def test_strategy_comparison_paper_claims():
+    """The paper's strategy comparison (Sec. 5) on op-granularity
+    pre-activation ResNets (BN -> ReLU -> FC -> Add per layer): the memory order no optimization
+    >= inplace >= sharing >= drop bn-relu; sharing saves at least the "factor of two" of P:416;
+    the system optimizations stay linear in depth while the sublinear plan's log-log slope is
+    well below 1.  C++ == oracle is checked by test_planner_parity."""
+    sizes = [4096, 2048, 1024, 512]
+    depths = (4, 8, 16, 32, 64)
+    peaks = {k: [] for k in ("none", "inplace", "sharing", "drop", "sub")}
+    for L in depths:
+        g = G.preact_resnet_graph([L] * 4, sizes)
+        assert G.validate(g) == []
+        p0 = P.plan(g, P.S_NONE, alloc_flags=0).alloc.exact_peak
+        p1 = P.plan(g, P.S_NONE, alloc_flags=P.A_INPLACE).alloc.exact_peak
+        p2 = P.plan(g, P.S_NONE, alloc_flags=P.A_INPLACE | P.A_SHARING).alloc.exact_peak
+        pd = P.plan(g, P.S_DROP_CHEAP)
+        ps = P.plan(g, P.S_SEARCH)
+        _simulate_interference(pd)
+        _simulate_interference(ps)
+        nop = P.plan(g, P.S_NONE, alloc_flags=0)
+        assert p0 == sum(nop.gg.nodes[v].out_bytes for v in nop.gg.order)   # no optimization = sum of sizes
+        assert p0 >= p1 >= p2 >= pd.alloc.exact_peak
+        assert p0 >= 2 * p2
+        for k, v in zip(peaks, (p0, p1, p2, pd.alloc.exact_peak, ps.alloc.exact_peak)):
+            peaks[k].append(v)
+
+    def slope(ys):   # log-log slope over the three deepest points (constant terms fade)
+        lx = [math.log(4 * L) for L in depths[-3:]]
+        ly = [math.log(y) for y in ys[-3:]]
+        mx, my = sum(lx) / len(lx), sum(ly) / len(ly)
+        return sum((a - mx) * (b - my) for a, b in zip(lx, ly)) / sum((a - mx) ** 2 for a in lx)
+
+    assert slope(peaks["none"]) > 0.95 and slope(peaks["sharing"]) > 0.85
+    assert slope(peaks["sub"]) < 0.75

@@ -101,6 +101,10 @@ def test_lstm_graph_plan():
     for strat, kw in ((P.S_SQRT, {}), (P.S_SEARCH, {}), (P.S_RECURSIVE, dict(k=1)), (P.S_RECURSIVE, dict(k=2))):
         assert_same_plan(G.chain_graph(40, 8, 64), strat, alloc_flags=par, **kw)
     assert_same_plan(g, P.S_SQRT, alloc_flags=grouped | P.A_MIRROR_PARITY)
+    rg = G.preact_resnet_graph([3, 5, 4, 2], [4096, 2048, 1024, 512])   # op-granularity ResNet (8(f) f1)
+    for strat, fl in ((P.S_NONE, 0), (P.S_NONE, P.A_INPLACE), (P.S_NONE, 3), (P.S_DROP_CHEAP, 3), (P.S_SEARCH, 3),
+                      (P.S_SQRT, 3), (P.S_SQRT, 3 | P.A_MIRROR_PARITY)):
+        assert_same_plan(rg, strat, alloc_flags=fl)
     assert_same_plan(g, P.S_SEARCH, alloc_flags=grouped)
     assert_same_plan(g, P.S_SQRT, alloc_flags=grouped)
     assert_same_plan(G.lstm_graph(4, 64, 64, 1024, 50), P.S_EXPLICIT,
