@@ -271,7 +271,10 @@ def run_lstm(args):
     # grouped sharing (reading A22): tags never cross layers -> less memory and no false
     # cross-layer dependencies for the layer wavefront
     AF = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_GROUPED | (slm.ALLOC_MIRROR_PARITY if args.lstm_parity else 0)
-    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg), alloc_flags=AF)
+    if args.lstm_strategy == "segments":
+        plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg), alloc_flags=AF)
+    else:   # the paper's general-DAG planners on the LSTM grid graph
+        plan = slm.Plan(graph, args.lstm_strategy, alloc_flags=AF)
     torch.cuda.synchronize()
     base_mem = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)
@@ -376,7 +379,7 @@ def run_lstm(args):
         ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
         data="synthetic (seeded NumPy, synth.lstm_inputs: PyTorch-default uniform LSTM init, x~N(0,1))",
         config=dict(workload=lstm_workload(args), n_layers=L, hidden=H, unroll=T, batch=B, n_in=I, classes=C,
-                    segment=args.seg, recompute="concurrent with the next segment's backward (A24 plan, mirror streams)" if args.lstm_parity else "sequential", parallelism=f"replicas{world}" if world > 1 else "single",
+                    segment=args.seg if args.lstm_strategy == "segments" else None, plan=args.lstm_strategy, recompute="concurrent with the next segment's backward (A24 plan, mirror streams)" if args.lstm_parity else "sequential", parallelism=f"replicas{world}" if world > 1 else "single",
                     l2="inputs > L2: 33 MB of bf16 weights + 24 GB of no-ckpt activations; the ckpt step re-reads "
                        "W every time step (L2-resident by design)"),
         roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches * args.steps), clocks=clocks,
@@ -408,6 +411,8 @@ def main():
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
     ap.add_argument("--mirror-parity", type=int, default=1,
                     help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
+    ap.add_argument("--lstm-strategy", default="segments",
+                    help="LSTM plan: segments (time segments of --seg steps) or a planner strategy (search, sqrt, ...)")
     ap.add_argument("--lstm-parity", type=int, default=1,
                     help="LSTM plan with SLM_ALLOC_MIRROR_PARITY (with --opt lstm_streams=2: recompute on its own streams)")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
