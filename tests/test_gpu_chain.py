@@ -121,11 +121,12 @@ def test_c2_full_size_bitwise_and_closed_form(slm):
     t = synth.chain_inputs_torch(n, B, d, dtype="bf16", seed=5)
     p = {k: t[k] for k in ("W", "b", "gamma", "beta")}
     out = {}
-    for s in ("none", "sqrt"):
+    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+    for s in ("none", "sqrt", "sqrt+A24"):   # sqrt+A24 = the bench's plan (overlapped recompute)
         g = dict(W=torch.empty_like(p["W"]), b=torch.empty_like(p["b"]), gamma=torch.empty_like(p["gamma"]),
                  beta=torch.empty_like(p["beta"]))
         model = slm.ChainModel(p, g, dtype="bf16", batch=B)
-        plan = slm.Plan(slm.Graph.chain(n, B, d), s)
+        plan = slm.Plan(slm.Graph.chain(n, B, d), s.split("+")[0], alloc_flags=par if "A24" in s else 3)
         strm = torch.cuda.Stream()
         with torch.cuda.stream(strm):
             loss = model.step(plan, t["x0"], t["labels"], stream=strm)
@@ -133,9 +134,10 @@ def test_c2_full_size_bitwise_and_closed_form(slm):
         torch.cuda.synchronize()
         out[s] = (loss.item(), {k: v.clone() for k, v in g.items()})
         del model, g
-    assert out["none"][0] == out["sqrt"][0]
-    for k in out["none"][1]:
-        assert torch.equal(out["none"][1][k], out["sqrt"][1][k]), k
+    for s in ("sqrt", "sqrt+A24"):
+        assert out["none"][0] == out[s][0], s
+        for k in out["none"][1]:
+            assert torch.equal(out["none"][1][k], out[s][1][k]), (s, k)
     # property that holds at any size: db_l = sum_b dx_{l+1} and BN backward conserves the
     # per-feature sum, so db is identical for every layer up to fp32 rounding
     db = out["sqrt"][1]["b"]
@@ -180,16 +182,19 @@ def test_comm_world1_equals_no_comm(slm):
     ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
     p, g, x0, y = _dev(inp, "bf16")
     model = slm.ChainModel(p, g, dtype="bf16", batch=B, batch_global=B)
-    plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt")
     comm = slm.Comm(0, 1, bucket_bytes=2 * d * d * 2)   # several buckets
-    s = torch.cuda.Stream()
-    with torch.cuda.stream(s):
-        for _ in range(2):
-            loss = model.step(plan, x0, y, stream=s, comm=comm)
-    torch.cuda.synchronize()
-    assert float(loss.item()) == ref_loss
-    for k in ref:
-        assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), k
+    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+    for af in (3, par):   # sequential recompute, and the bench's overlapped recompute (A24)
+        plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt", alloc_flags=af)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                loss = model.step(plan, x0, y, stream=s, comm=comm)
+        torch.cuda.synchronize()
+        assert model.get_option("last_overlap") == (af == par)
+        assert float(loss.item()) == ref_loss, af
+        for k in ref:
+            assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (af, k)
 
 
 @pytest.mark.parametrize("dtype,n,B,d", [("f32", 1, 8, 64), ("f32", 2, 5, 48), ("f32", 3, 33, 80),
