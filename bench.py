@@ -94,6 +94,26 @@ class Clocks:
 
 
 # ======================================================================= reference arm
+def _ncu_gemm_traffic(d, B):
+    """DRAM bytes per launch of the dX GEMM (dram__bytes_read.sum + write) from the committed
+    `ncu --set full` summary (profiles/*_ncu_full_backward.md, C2 shapes only), else None."""
+    import glob
+    if (d, B) != (2048, 256):
+        return None, None
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_full_backward.md")))
+    for f in reversed(files):
+        for line in open(f):
+            cells = [c.strip() for c in line.strip().strip("|").split("|")]
+            if len(cells) > 3 and cells[0].startswith("tc_gemm_kernel<128, 1, 0"):
+                try:
+                    return round((float(cells[2]) + float(cells[3])) * 1e6), (
+                        f"{os.path.basename(f)}: dX GEMM dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                        f"(algorithmic: 8.39 MB of W + 1.05 MB of bf16 upstream gradient)")
+                except ValueError:
+                    pass
+    return None, None
+
+
 def run_reference(args):
     """The CPU oracle as it stands (fp64 NumPy, bf16-operand emulation), timed on this box's
     host cores on a bounded sample of the same workload, scaled to samples/s of the full
@@ -614,6 +634,11 @@ def main():
                     gemm_share_of_step=round(crit_ms / prof_ms, 4) if prof_ms else None,
                     step_ms_instrumented=round(prof_ms, 3))
     step_flop = 2.0 * B * d * d * (4 * n - math.isqrt(max(0, n - 1)) - 1 if args.strategy == "sqrt" else 3 * n)
+    # whole-step tensor throughput (the launches of three streams overlap, so per-launch spans
+    # stretch under concurrency; this is the comparable figure) and the ncu DRAM traffic per GEMM
+    roofline["achieved_step"] = round(step_flop / (ms / 1e3) / 1e12, 2)
+    roofline["frac_step"] = round(roofline["achieved_step"] / peak, 4)
+    roofline["traffic"], roofline["traffic_source"] = _ncu_gemm_traffic(d, B)
 
     # ---- non-checkpointed step (the "vs no-ckpt" half of the metric)
     nock = None
