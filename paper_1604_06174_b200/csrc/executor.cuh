@@ -318,6 +318,7 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int tile_dx = 0, tile_mir = 0;              // N tiles of the dX / recompute-stream GEMMs (0 = fused_bn rule)
   int blk_cluster = 0;                        // forward Block as one cluster kernel (blk_cluster.cuh; B = 256;
                                               // measured 35.2 vs 35.3 ms/step at C2: within noise, default off)
   int dw_lag = 2;                             // dW ring depth: layers the dW stream may lag the dX chain (2..8)
@@ -409,6 +410,11 @@ bool fused_ok(const slm_model& m) {
 // N tile of the fused GEMMs: 128 (measured best at C2: 43.7 ms/step vs 45.1 with the full
 // batch of 256 per tile; profiles/README.md sweep), or the batch when smaller
 int fused_n(const slm_model& m) { return m.fused_bn > 0 ? m.fused_bn : std::min(m.d.batch, 128); }
+// N tiles of the dX GEMMs and of the recompute-stream mirror GEMMs (options tile_dx, tile_mir; 0 =
+// fused_n).  The N tile does not change any element's accumulation order (one tcgen05 MMA per
+// K = 16 step, K blocks in order), so mirrors with another tile reproduce the forward's bits.
+int dx_tile(const slm_model& m) { return m.tile_dx > 0 ? std::min(m.tile_dx, m.d.batch) : fused_n(m); }
+int mir_tile(const slm_model& m) { return m.tile_mir > 0 ? std::min(m.tile_mir, m.d.batch) : fused_n(m); }
 // split-K factor: as many K slices as keep <= ~148 CTAs and >= 64 of K per slice
 int auto_split(int M, int K, int req, int n_tiles = 1) {
   if (req > 0) return req;
@@ -520,7 +526,8 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 
 slm_status bind_maps(slm_model& m, void* ws) {
   const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.fused_bn * 1009 + m.cta_pair * 100003 + m.persist * 3 +
-                  m.overlap * 5 + m.dw_tma * 11 + m.dw_lag * 13 + m.blk_cluster * 17;
+                  m.overlap * 5 + m.dw_tma * 11 + m.dw_lag * 13 + m.blk_cluster * 17 + m.tile_dx * 19 +
+                  m.tile_mir * 23;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -528,7 +535,8 @@ slm_status bind_maps(slm_model& m, void* ws) {
   const bool fz = fused_ok(m);
   // fused: N tile fused_n() (K-major B box rows = tile / cta group)
   const uint32_t fb = (uint32_t)(fused_n(m) / (m.cta_pair ? 2 : 1));
-  const uint32_t bnf = fz ? fb : (uint32_t)m.bn_fwd, bnx = fz ? fb : (uint32_t)m.bn_dx;
+  const uint32_t cgd = m.cta_pair ? 2 : 1;
+  const uint32_t bnf = fz ? fb : (uint32_t)m.bn_fwd, bnx = fz ? (uint32_t)dx_tile(m) / cgd : (uint32_t)m.bn_dx;
   slm_status st;
   if ((st = make_map(&m.mW_K, m.d.W, d, n * d, 128)) != SLM_OK) return st;
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
@@ -536,7 +544,7 @@ slm_status bind_maps(slm_model& m, void* ws) {
   if (fz && (st = make_map(&m.mA_Kf, w + L.a, d, B, (uint32_t)B)) != SLM_OK) return st;
   if (fz && m.dw_tma && (st = make_map_bf16_store(&m.mdW_st, m.d.dW, d, n * d)) != SLM_OK) return st;
   if (fz && m.overlap) {
-    if ((st = make_map(&m.mA_K3, w + L.a3, d, B, bnf)) != SLM_OK) return st;
+    if ((st = make_map(&m.mA_K3, w + L.a3, d, B, (uint32_t)mir_tile(m) / cgd)) != SLM_OK) return st;
     if ((st = make_map_f32(&m.mP3, w + L.P3, d, (uint64_t)L.sk_fwd * B)) != SLM_OK) return st;
   }
   if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
@@ -837,7 +845,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         slmk::EpiPartialTma epi{B};
         pbeg(fs);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(
-                 fused_n(m), L.sk_fwd, m.mW_K, on3 ? m.mA_K3 : m.mA_K, d, B, d, l * d, 0, epi, fs, pdl,
+                 on3 ? mir_tile(m) : fused_n(m), L.sk_fwd, m.mW_K, on3 ? m.mA_K3 : m.mA_K, d, B, d, l * d, 0, epi, fs, pdl,
                  gdbg(SLM_K_GEMM_FWD), on3 ? &m.mP3 : &m.mP, m.cta_pair ? 2 : 1,
                  m.l2_prefetch && l + 1 < n ? (l + 1) * d : -1)) != SLM_OK)
           return s;
@@ -900,7 +908,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         slmk::EpiPartialTma e1{B};
         pbeg(st);
         if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(
-                 fused_n(m), L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d, l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX), &m.mP,
+                 dx_tile(m), L.sk_dx, m.mW_MN, m.mG_K[gcur], d, B, d, l * d, 0, e1, st, pdl, gdbg(SLM_K_GEMM_DX), &m.mP,
                  m.cta_pair ? 2 : 1, m.l2_prefetch && l > 0 ? (l - 1) * d : -1)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_DX, st);
