@@ -18,7 +18,8 @@ namespace slmk {
 
 constexpr int kFeat = 16;   // features per CTA
 constexpr int kThreads = 512;
-__device__ __forceinline__ float cta_feature_sum(float v, float (*red)[kFeat + 1], int rg, int fl) {
+template <int F = kFeat>
+__device__ __forceinline__ float cta_feature_sum(float v, float (*red)[F + 1], int rg, int fl) {
   red[rg][fl] = v;
   __syncthreads();
   float t = 0.f;
@@ -29,21 +30,21 @@ __device__ __forceinline__ float cta_feature_sum(float v, float (*red)[kFeat + 1
 }
 
 // mean (two-pass) and rstd of this thread's feature over the whole batch
-template <int R>
-__device__ __forceinline__ void feature_stats(const float (&v)[R], float (*red)[kFeat + 1], int w, int lane, float& mu,
+template <int R, int F = kFeat>
+__device__ __forceinline__ void feature_stats(const float (&v)[R], float (*red)[F + 1], int w, int lane, float& mu,
                                               float& rstd) {
   constexpr float invB = 1.0f / (32 * R);   // exact: B is a power of two
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < R; ++i) s = __fadd_rn(s, v[i]);
-  mu = __fmul_rn(cta_feature_sum(s, red, w, lane), invB);
+  mu = __fmul_rn(cta_feature_sum<F>(s, red, w, lane), invB);
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const float c = __fsub_rn(v[i], mu);
     q = __fmaf_rn(c, c, q);
   }
-  const float var = __fmul_rn(cta_feature_sum(q, red, w, lane), invB);
+  const float var = __fmul_rn(cta_feature_sum<F>(q, red, w, lane), invB);
   rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, kEps)));
 }
 
@@ -70,15 +71,17 @@ __device__ __forceinline__ void sum_slices(const float* __restrict__ p, unsigned
 
 // K1 (+ forward finalize).  NS > 0: x = xin + (sum_s P[s] + bias) is stored to xout (may alias
 // xin: element-wise).  Then, if gamma != null: stats[2][d] and a = ReLU(gamma xhat + beta) (T).
-template <class T, int R, int NS>
-__global__ void __launch_bounds__(kThreads) bn_act_rk(const float* xin, const float* __restrict__ P, unsigned pslice,
+// F = features per CTA (16: 512 threads, 8: 256 threads — option bn_feat); the per-feature
+// reduction order (32 row groups) does not depend on F.
+template <class T, int R, int NS, int F = kFeat>
+__global__ void __launch_bounds__(F * 32) bn_act_rk(const float* xin, const float* __restrict__ P, unsigned pslice,
                                                   const float* __restrict__ bias, float* xout,
                                                   const float* __restrict__ gamma, const float* __restrict__ beta,
                                                   int d, float* __restrict__ stats, T* __restrict__ a) {
-  __shared__ float red[32][kFeat + 1];
+  __shared__ float red[32][F + 1];
   pdl_wait();
-  const int lane = threadIdx.x % kFeat, w = threadIdx.x / kFeat;   // feature in CTA, row group
-  const int f = blockIdx.x * kFeat + lane;
+  const int lane = threadIdx.x % F, w = threadIdx.x / F;   // feature in CTA, row group
+  const int f = blockIdx.x * F + lane;
   const unsigned base = (unsigned)w * d + f, rs = 32u * d;
   float v[R];
 #pragma unroll
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) bn_act_rk(const float* xin, const fl
   pdl_launch();   // all inputs are loaded
   if (gamma == nullptr) return;
   float mu, rstd;
-  feature_stats<R>(v, red, w, lane, mu, rstd);
+  feature_stats<R, F>(v, red, w, lane, mu, rstd);
   if (w == 0) {
     stats[f] = mu;
     stats[d + f] = rstd;
@@ -111,24 +114,24 @@ __global__ void __launch_bounds__(kThreads) bn_act_rk(const float* xin, const fl
 //   dgamma = sum_b du xhat,  dbeta = sum_b du,  dx = g + gamma rstd (du - dbeta/B - xhat dgamma/B)
 //   -> dx (may alias g);  db_prev = sum_b dx;  gq = bf16(dx) (next dX / dW operand);
 //   a = ReLU(u) (this layer's dW operand; the same bits as the forward's a_l).
-template <class GQ, class TA, int R, int NS>
-__global__ void __launch_bounds__(kThreads) bn_bwd_rk(const float* __restrict__ P, unsigned pslice,
+template <class GQ, class TA, int R, int NS, int F = kFeat>
+__global__ void __launch_bounds__(F * 32) bn_bwd_rk(const float* __restrict__ P, unsigned pslice,
                                                   const float* __restrict__ x, const float* __restrict__ gamma,
                                                   const float* __restrict__ beta, const float* g, float* dx, int d,
                                                   float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                   float* __restrict__ db_prev, GQ* __restrict__ gq,
                                                   TA* __restrict__ a_out) {
-  __shared__ float red[32][kFeat + 1];
+  __shared__ float red[32][F + 1];
   pdl_wait();
-  const int lane = threadIdx.x % kFeat, w = threadIdx.x / kFeat;   // feature in CTA, row group
-  const int f = blockIdx.x * kFeat + lane;
+  const int lane = threadIdx.x % F, w = threadIdx.x / F;   // feature in CTA, row group
+  const int f = blockIdx.x * F + lane;
   const unsigned base = (unsigned)w * d + f, rs = 32u * d;
   float xv[R], du[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) xv[i] = x[base + i * rs];
   sum_slices<R, NS>(P + base, rs, pslice, du);   // du <- da
   float mu, rstd;
-  feature_stats<R>(xv, red, w, lane, mu, rstd);
+  feature_stats<R, F>(xv, red, w, lane, mu, rstd);
   const float ga = gamma[f], bt = beta[f];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -140,8 +143,8 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_rk(const float* __restrict__ 
     s1 = __fadd_rn(s1, du[i]);
     s2 = __fmaf_rn(du[i], xh, s2);
   }
-  const float S1 = cta_feature_sum(s1, red, w, lane);
-  const float S2 = cta_feature_sum(s2, red, w, lane);
+  const float S1 = cta_feature_sum<F>(s1, red, w, lane);
+  const float S2 = cta_feature_sum<F>(s2, red, w, lane);
   constexpr float invB = 1.0f / (32 * R);
   const float m1 = __fmul_rn(S1, invB), m2 = __fmul_rn(S2, invB);
   const float k = __fmul_rn(ga, rstd);
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_rk(const float* __restrict__ 
     gq[base + i * rs] = from_f32<GQ>(v);
     s3 = __fadd_rn(s3, v);
   }
-  const float S3 = cta_feature_sum(s3, red, w, lane);
+  const float S3 = cta_feature_sum<F>(s3, red, w, lane);
   if (w != 0) return;
   dgamma[f] = S2;
   dbeta[f] = S1;

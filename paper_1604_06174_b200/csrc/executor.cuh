@@ -203,42 +203,42 @@ slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint
   return SLM_OK;
 }
 
-// register-resident BN kernels: compile-time rows per warp R = B/32 and split count NS
-template <int R, int NS>
+// register-resident BN kernels: compile-time rows per warp R = B/32, split count NS and features
+// per CTA F (option bn_feat: 16 -> 512-thread CTAs, 8 -> 256-thread CTAs, same arithmetic)
+template <int R, int NS, int F>
 cudaError_t launch_act_rk(cudaStream_t st, bool pdl, int d, const float* xin, const float* P, unsigned pslice,
                           const float* bias, float* xout, const float* ga, const float* be, float* stats,
                           __nv_bfloat16* a) {
-  return launch_k(slmk::bn_act_rk<__nv_bfloat16, R, NS>, dim3(d / slmk::kFeat), dim3(slmk::kThreads), 0, st, pdl, xin,
-                  P, pslice, bias,
+  return launch_k(slmk::bn_act_rk<__nv_bfloat16, R, NS, F>, dim3(d / F), dim3(F * 32), 0, st, pdl, xin, P, pslice, bias,
                   xout, ga, be, d, stats, a);
 }
-cudaError_t act_rk(int R, int ns, cudaStream_t st, bool pdl, int d, const float* xin, const float* P,
+cudaError_t act_rk(int R, int ns, int F, cudaStream_t st, bool pdl, int d, const float* xin, const float* P,
                    unsigned pslice, const float* bias, float* xout, const float* ga, const float* be, float* stats,
                    __nv_bfloat16* a) {
-#define SLM_ACT(R_, NS_) \
-  if (R == R_ && ns == NS_) return launch_act_rk<R_, NS_>(st, pdl, d, xin, P, pslice, bias, xout, ga, be, stats, a);
-#define SLM_ACT_R(R_) SLM_ACT(R_, 0) SLM_ACT(R_, 1) SLM_ACT(R_, 2) SLM_ACT(R_, 4) SLM_ACT(R_, 8)
-  SLM_ACT_R(2) SLM_ACT_R(4) SLM_ACT_R(8)
+#define SLM_ACT(R_, NS_, F_)                                                                                 \
+  if (R == R_ && ns == NS_ && F == F_)                                                                      \
+    return launch_act_rk<R_, NS_, F_>(st, pdl, d, xin, P, pslice, bias, xout, ga, be, stats, a);
+#define SLM_ACT_R(R_, F_) SLM_ACT(R_, 0, F_) SLM_ACT(R_, 1, F_) SLM_ACT(R_, 2, F_) SLM_ACT(R_, 4, F_) SLM_ACT(R_, 8, F_)
+  SLM_ACT_R(2, 16) SLM_ACT_R(4, 16) SLM_ACT_R(8, 16) SLM_ACT_R(8, 8)
 #undef SLM_ACT_R
 #undef SLM_ACT
   return cudaErrorInvalidValue;
 }
-template <int R, int NS>
+template <int R, int NS, int F>
 cudaError_t launch_bwd_rk(cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice, const float* x,
                           const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe,
                           float* dbp, __nv_bfloat16* gq, __nv_bfloat16* a) {
-  return launch_k(slmk::bn_bwd_rk<__nv_bfloat16, __nv_bfloat16, R, NS>, dim3(d / slmk::kFeat), dim3(slmk::kThreads), 0,
-                  st, pdl, P,
+  return launch_k(slmk::bn_bwd_rk<__nv_bfloat16, __nv_bfloat16, R, NS, F>, dim3(d / F), dim3(F * 32), 0, st, pdl, P,
                   pslice, x, ga, be, g, dx, d, dga, dbe, dbp, gq, a);
 }
-cudaError_t bwd_rk(int R, int ns, cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice, const float* x,
-                   const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe, float* dbp,
-                   __nv_bfloat16* gq, __nv_bfloat16* a) {
-#define SLM_BWD(R_, NS_)                                                                                    \
-  if (R == R_ && ns == NS_)                                                                                  \
-    return launch_bwd_rk<R_, NS_>(st, pdl, d, P, pslice, x, ga, be, g, dx, dga, dbe, dbp, gq, a);
-#define SLM_BWD_R(R_) SLM_BWD(R_, 1) SLM_BWD(R_, 2) SLM_BWD(R_, 4) SLM_BWD(R_, 8)
-  SLM_BWD_R(2) SLM_BWD_R(4) SLM_BWD_R(8)
+cudaError_t bwd_rk(int R, int ns, int F, cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice,
+                   const float* x, const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe,
+                   float* dbp, __nv_bfloat16* gq, __nv_bfloat16* a) {
+#define SLM_BWD(R_, NS_, F_)                                                                                 \
+  if (R == R_ && ns == NS_ && F == F_)                                                                      \
+    return launch_bwd_rk<R_, NS_, F_>(st, pdl, d, P, pslice, x, ga, be, g, dx, dga, dbe, dbp, gq, a);
+#define SLM_BWD_R(R_, F_) SLM_BWD(R_, 1, F_) SLM_BWD(R_, 2, F_) SLM_BWD(R_, 4, F_) SLM_BWD(R_, 8, F_)
+  SLM_BWD_R(2, 16) SLM_BWD_R(4, 16) SLM_BWD_R(8, 16) SLM_BWD_R(8, 8)
 #undef SLM_BWD_R
 #undef SLM_BWD
   return cudaErrorInvalidValue;
@@ -318,6 +318,7 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int bn_feat = 16;                           // features per CTA of the BN kernels (16 | 8; same bits; 8 measured slower)
   int tile_dx = 0, tile_mir = 0;              // N tiles of the dX / recompute-stream GEMMs (0 = fused_bn rule)
   int blk_cluster = 0;                        // forward Block as one cluster kernel (blk_cluster.cuh; B = 256;
                                               // measured 35.2 vs 35.3 ms/step at C2: within noise, default off)
@@ -674,13 +675,15 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
     return launch_k(simt_gemm_kernel<TA, TB, TO, EPI_STORE>, grid, dim3(256), 0, st, pdl, M, N, K, A, sAm, sAk, Bp,
                     sBn, sBk, out, ldo, resid, bias);
   };
+  // features per CTA of the BN kernels (option bn_feat = 8 only at B = 256)
+  auto bnf_ = [&]() { return m.bn_feat == 8 && B == 256 ? 8 : 16; };
   // K1 (optionally fused with the forward finalize from split-K partials)
   auto bn_act = [&](const float* xin, const float* Pp, int nsplit, const float* bias, float* xout, int l,
                     cudaStream_t fs = nullptr, void* fa = nullptr, float* fstats = nullptr) -> cudaError_t {
     const float* ga = l < n ? gam + (size_t)l * d : nullptr;
     const float* be = l < n ? bet + (size_t)l * d : nullptr;
     if (fz)
-      return act_rk(B / 32, Pp ? nsplit : 0, fs ? fs : st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be,
+      return act_rk(B / 32, Pp ? nsplit : 0, bnf_(), fs ? fs : st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be,
                     fstats ? fstats : stats, (bf*)(fa ? fa : abuf));
     if (bf16)
       return launch_k(bn_act_kernel<bf>, colgrid, blk, 0, st, pdl, xin, ga, be, B, d, stats, (bf*)abuf);
@@ -915,7 +918,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         // bn_bwd(k) overwrites gq[(k+1)%NG] and ab[k%NA], last read by dW of backward k-NA
         if (side && kb >= NA && dw_event[kb - NA] >= 0) CK(cudaStreamWaitEvent(st, m.sync_ev[dw_event[kb - NA]], 0));
         pbeg(st);
-        CK(bwd_rk(B / 32, L.sk_dx, st, pdl, d, (const float*)P, (unsigned)pslice, xl, ga, be, g, dxl, dga, dbe, dbp,
+        CK(bwd_rk(B / 32, L.sk_dx, bnf_(), st, pdl, d, (const float*)P, (unsigned)pslice, xl, ga, be, g, dxl, dga, dbe, dbp,
                   gq[gnext], ab[abi]));
         pend(SLM_K_BN_BWD, st);
         // dW_l[f_out][f_in] = sum_b g[b][f_out] a[b][f_in]  (second stream)

@@ -374,3 +374,17 @@ def test_cluster_block_option(slm, sk, n, d):
             assert float(loss.item()) == ref_loss, (strategy, af)
             for k in ref:
                 assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (strategy, af, k)
+
+
+def test_bn_feat_option_same_bits(slm):
+    """Option bn_feat = 8 (256-thread BN CTAs of 8 features instead of 512-thread CTAs of 16):
+    the per-feature reductions keep their order (32 row groups), so the step's bits equal the
+    default's, checkpointed or not."""
+    n, B, d = 12, 256, 512
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=13)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+    for strategy in ("none", "sqrt"):
+        loss, g, _ = _run(slm, n, B, d, "bf16", strategy, inp, bn_feat=8)
+        assert loss == ref_loss, strategy
+        for k in ref:
+            assert np.array_equal(g[k], ref[k]), (strategy, k)
