@@ -146,6 +146,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// two 32-column loads (columns taddr .. taddr+63) behind one wait: one TMEM round trip per 64 columns
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+  uint32_t r[64];
+#define SLM_TLD(o, b)                                                                                         \
+  asm volatile(                                                                                               \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"           \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                         \
+      : "=r"(r[b + 0]), "=r"(r[b + 1]), "=r"(r[b + 2]), "=r"(r[b + 3]), "=r"(r[b + 4]), "=r"(r[b + 5]),         \
+        "=r"(r[b + 6]), "=r"(r[b + 7]), "=r"(r[b + 8]), "=r"(r[b + 9]), "=r"(r[b + 10]), "=r"(r[b + 11]),        \
+        "=r"(r[b + 12]), "=r"(r[b + 13]), "=r"(r[b + 14]), "=r"(r[b + 15]), "=r"(r[b + 16]), "=r"(r[b + 17]),    \
+        "=r"(r[b + 18]), "=r"(r[b + 19]), "=r"(r[b + 20]), "=r"(r[b + 21]), "=r"(r[b + 22]), "=r"(r[b + 23]),    \
+        "=r"(r[b + 24]), "=r"(r[b + 25]), "=r"(r[b + 26]), "=r"(r[b + 27]), "=r"(r[b + 28]), "=r"(r[b + 29]),    \
+        "=r"(r[b + 30]), "=r"(r[b + 31])                                                                      \
+      : "r"(taddr + o));
+  SLM_TLD(0, 0)
+  SLM_TLD(32, 32)
+#undef SLM_TLD
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // Shared-memory matrix descriptor (tcgen05 "smem descriptor"): start address, leading and
 // stride byte offsets (16-byte units), version 1 (sm_100), layout SWIZZLE_128B (= 2).
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -513,16 +535,11 @@ __global__ void __launch_bounds__(128, 1)
     // free after the MMAs.
     constexpr bool HALF = EpiHalf<Epi>::value;
     constexpr int BUF_BYTES = 32 * 128 * (HALF ? 2 : 4);
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      const int buf = (c >> 5) & 1;
-      if (c >= 64) {  // the store issued two chunks ago must have read this buffer
-        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncthreads();
-      }
-      float acc[32];
-      tmem_ld32(trow + c, acc);
-      uint8_t* sbuf = smem + buf * BUF_BYTES;
+    // one TMEM round trip per 64 columns (two staging boxes); 4 boxes in a ring, one bulk group
+    // per iteration, so iteration it reuses the boxes of iteration it - 2
+    constexpr int CW = BN >= 64 ? 64 : 32;
+    auto stage_box = [&](int box, const float* acc) {
+      uint8_t* sbuf = smem + box * BUF_BYTES;
       if constexpr (HALF) {
         __nv_bfloat16* sp = reinterpret_cast<__nv_bfloat16*>(sbuf) + warp * 32 + lane;
 #pragma unroll
@@ -532,18 +549,49 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) sp[j * 128] = acc[j];
       }
+    };
+    auto store_box = [&](int box, int c) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+              reinterpret_cast<uint64_t>(&tmC)),
+          "r"(smem_u32(smem + box * BUF_BYTES)), "r"(m0), "r"(epi.row0(ks) + n0 + c)
+          : "memory");
+    };
+#pragma unroll 1
+    for (int c = 0; c < BN; c += CW) {
+      const int it = c / CW;
+      const int b0 = (2 * it) & 3;
+      if (it >= 2) {  // the stores issued two iterations ago must have read these boxes
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+      }
+      if constexpr (CW == 64) {
+        float acc[64];
+        tmem_ld64(trow + c, acc);
+        stage_box(b0, acc);
+        stage_box(b0 + 1, acc + 32);
+      } else {
+        float acc[32];
+        tmem_ld32(trow + c, acc);
+        stage_box(b0, acc);
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (threadIdx.x == 0) {
-        asm volatile(
-            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&tmC)),
-            "r"(smem_u32(sbuf)), "r"(m0), "r"(epi.row0(ks) + n0 + c)
-            : "memory");
+        store_box(b0, c);
+        if constexpr (CW == 64) store_box(b0 + 1, c + 32);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  } else if constexpr (BN >= 64) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 64) {
+      float acc[64];
+      tmem_ld64(trow + c, acc);
+      epi(m, n0 + c, acc, ks);
+      epi(m, n0 + c + 32, acc + 32, ks);
+    }
   } else {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
