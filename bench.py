@@ -294,7 +294,11 @@ def run_lstm(args):
     if args.lstm_strategy == "segments":
         plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(args.seg), alloc_flags=AF)
     else:   # the paper's general-DAG planners on the LSTM grid graph
-        plan = slm.Plan(graph, args.lstm_strategy, alloc_flags=AF)
+        strat = args.lstm_strategy
+        if strat.endswith("-states"):   # reading A25: cell states are the only split points
+            graph.mark_not_candidate(slm.OP["lstm_gates"])
+            strat = strat[: -len("-states")]
+        plan = slm.Plan(graph, strat, alloc_flags=AF)
     torch.cuda.synchronize()
     base_mem = torch.cuda.memory_allocated(dev)
     torch.cuda.reset_peak_memory_stats(dev)

@@ -115,6 +115,12 @@ slm_status slm_graph_chain(int32_t n_layers, int32_t batch, int32_t width, slm_g
  * G^l_t (batch*4H*4) and S^l_t (batch*2H*4), a head H_t (4 bytes); final Sum (the loss). */
 slm_status slm_graph_lstm(int32_t n_layers, int32_t steps, int32_t batch, int32_t hidden,
                           int32_t n_in, slm_graph** out);
+/* Restricts Alg. 3's candidate set C (reading A19) on an existing graph: every
+ * node whose op is `op` (SLM_OP_*) gets SLM_NODE_NOT_CANDIDATE, so the budget / App. A search
+ * plans only split elsewhere — e.g. op = SLM_OP_LSTM_GATES leaves the LSTM's cell states as the
+ * only split points (reading A25).  *n_marked = nodes changed (may be NULL).
+ * SLM_E_ARG for a null graph or an unknown op. */
+slm_status slm_graph_mark_not_candidate(slm_graph* g, int32_t op, int32_t* n_marked);
 /* Time-segment mirror counts for a graph built by slm_graph_lstm (the LSTM
  * is checkpointed along time): m[v] = 1 for every gates/cell node except the cell states
  * S^l_t at segment ends (t % seg == seg - 1), which are kept; 0 elsewhere.  Feed the result

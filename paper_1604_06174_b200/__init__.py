@@ -48,6 +48,13 @@ class Graph:
         check(lib.slm_graph_lstm(n_layers, steps, batch, hidden, n_in, C.byref(h)), "slm_graph_lstm")
         return cls(h)
 
+    def mark_not_candidate(self, op):
+        """Removes every node of op `op` from Alg. 3's candidate set (slm_graph_mark_not_candidate);
+        returns the number of nodes changed."""
+        n = C.c_int32()
+        check(lib.slm_graph_mark_not_candidate(self._h, int(op), C.byref(n)), "slm_graph_mark_not_candidate")
+        return n.value
+
     def lstm_segment_mirrors(self, seg):
         """Time-segment mirror counts (slm_lstm_segment_mirrors) for Plan(..., 'explicit', m=...)."""
         n = len(self)

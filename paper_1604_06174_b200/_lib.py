@@ -82,6 +82,7 @@ _sig("slm_lstm_segment_mirrors", i32, vp, i32, i32p, i32)
 _sig("slm_model_destroy", None, vp)
 _sig("slm_model_set_option", i32, vp, C.c_char_p, i64)
 _sig("slm_model_get_option", i32, vp, C.c_char_p, i64p)
+_sig("slm_graph_mark_not_candidate", i32, vp, i32, i32p)
 _sig("slm_workspace_bytes", i32, vp, vp, C.POINTER(C.c_size_t))
 _sig("slm_step_launches", i32, vp, vp, i64p)
 _sig("slm_step", i32, vp, vp, vp, vp, vp, C.c_size_t, vp, C.c_size_t, vp, vp, vp)

@@ -813,6 +813,21 @@ slm_status slm_graph_topo(const slm_graph* g, int32_t* order, int32_t cap, int32
 
 void slm_graph_destroy(slm_graph* g) { delete g; }
 
+slm_status slm_graph_mark_not_candidate(slm_graph* g, int32_t op, int32_t* n_marked) {
+  if (!g || !op_meta(op)) {
+    set_error("slm_graph_mark_not_candidate: null graph or unknown op");
+    return SLM_E_ARG;
+  }
+  int32_t c = 0;
+  for (auto& nd : g->nodes)
+    if (nd.op == op && !(nd.flags & SLM_NODE_NOT_CANDIDATE)) {
+      nd.flags |= SLM_NODE_NOT_CANDIDATE;
+      ++c;
+    }
+  if (n_marked) *n_marked = c;
+  return SLM_OK;
+}
+
 slm_status slm_plan_create(const slm_graph* g, const slm_plan_opts* opts, slm_plan** out) {
   if (!g || !opts || !out) {
     set_error("null argument");

@@ -35,12 +35,14 @@ def _dev(inp, L, H, C):
     return p, g, torch.tensor(inp["x"]).cuda(), torch.tensor(inp["labels"]).cuda()
 
 
-def _run(slm, cfg, inp, strategy="none", m=None, alloc_flags=3, **opt):
+def _run(slm, cfg, inp, strategy="none", m=None, alloc_flags=3, state_candidates=False, **opt):
     L, T, B, H, I, C = cfg
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, **opt)
-    plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "explicit" if m is not None else strategy, m=m,
-                    alloc_flags=alloc_flags)
+    graph = slm.Graph.lstm(L, T, B, H, I)
+    if state_candidates:   # reading A25: only cell states are Alg. 3 split points
+        graph.mark_not_candidate(slm.OP["lstm_gates"])
+    plan = slm.Plan(graph, "explicit" if m is not None else strategy, m=m, alloc_flags=alloc_flags)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         loss = model.step(plan, x, y, stream=s)
@@ -222,3 +224,21 @@ def test_lstm_fused_cell_epilogue_matches_kernel_path(slm):
     assert res[(1, 1)][0] == res[(1, 0)][0]
     for k in res[(1, 1)][1]:
         assert np.array_equal(res[(1, 1)][1][k], res[(1, 0)][1][k]), k
+
+
+@pytest.mark.parametrize("cfg", [(2, 40, 64, 128, 50, 300), (3, 24, 64, 128, 50, 200)])
+def test_lstm_search_plans_bitwise(slm, cfg):
+    """The paper's App. A search over the LSTM grid graph, over all nodes and
+    over cell states only (reading A25), with and without the A24 recompute phases: the
+    checkpointed step equals the non-checkpointed one bit for bit, repeatedly."""
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=8)
+    ref_loss, ref, _ = _run(slm, cfg, inp)
+    for sc in (False, True):
+        for af in (7, 23):
+            for _ in range(2):
+                loss, g, plan = _run(slm, cfg, inp, strategy="search", alloc_flags=af, state_candidates=sc)
+                assert plan.extra_forward > 0
+                assert loss == ref_loss, (sc, af)
+                for k in ref:
+                    assert np.array_equal(g[k], ref[k]), (sc, af, k)

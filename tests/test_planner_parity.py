@@ -179,3 +179,26 @@ def test_validate_and_errors_match():
     assert e.value.code == -5
     for n, k in [(1024, 1), (81, 2), (1, 3), (10 ** 12, 1)]:
         assert slm.recursion_estimate(n, k) == P.recursion_estimate(n, k)
+
+
+def test_lstm_state_candidates_search():
+    """Reading A25: slm_graph_mark_not_candidate(LSTM_GATES) leaves the cell
+    states as Alg. 3's only split points on the LSTM grid; the C++ plan equals the oracle's on
+    the same flags (byte for byte), and no gates node is ever kept (m = 0)."""
+    import copy
+    g = G.lstm_graph(2, 24, 4, 8, 3)
+    go = copy.deepcopy(g)
+    for nd in go.nodes:
+        if nd.op == G.LSTM_GATES:
+            nd.flags |= G.F_NOT_CANDIDATE
+    cg = slm.Graph.lstm(2, 24, 4, 8, 3)
+    assert cg.mark_not_candidate(slm.OP["lstm_gates"]) == 48
+    assert cg.mark_not_candidate(slm.OP["lstm_gates"]) == 0
+    for strat, kw in ((P.S_SEARCH, {}), (P.S_BUDGET, dict(budget=4 * 8 * 4 * 6))):
+        for fl in (3, 7, 23):
+            po = P.plan(go, strat, alloc_flags=fl, **kw)
+            pc = slm.Plan(cg, {P.S_SEARCH: "search", P.S_BUDGET: "budget"}[strat], alloc_flags=fl, **kw)
+            assert po.m == pc.m and po.alloc.exact_peak == pc.exact_peak and po.alloc.offsets == pc.tags[2]
+            assert all(po.m[v] >= 1 for v, nd in enumerate(go.nodes) if nd.op == G.LSTM_GATES)
+    with pytest.raises(RuntimeError):
+        cg.mark_not_candidate(999)
