@@ -242,3 +242,19 @@ def test_lstm_search_plans_bitwise(slm, cfg):
                 assert loss == ref_loss, (sc, af)
                 for k in ref:
                     assert np.array_equal(g[k], ref[k]), (sc, af, k)
+
+
+def test_lstm_overlapped_recompute_race_midsize(slm):
+    """Race detection for the overlapped recompute at a mid size (4 layers, 130 steps, 32-step
+    segments: 4 recompute phases running under the next segment's backward on the mirror
+    streams): repeated steps reproduce the non-checkpointed step bit for bit."""
+    cfg = (4, 130, 64, 256, 50, 300)
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=12)
+    ref_loss, ref, _ = _run(slm, cfg, inp, alloc_flags=23)
+    m = slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(32)
+    for rep in range(3):
+        loss, g, plan = _run(slm, cfg, inp, m=m, alloc_flags=23, lstm_streams=2)
+        assert loss == ref_loss, rep
+        for k in ref:
+            assert np.array_equal(g[k], ref[k]), (rep, k)
