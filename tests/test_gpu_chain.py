@@ -296,7 +296,8 @@ def test_persistent_forward_option(slm, n, B, d):
 
 @pytest.mark.parametrize("n,B,d,opt", [(40, 64, 256, {}), (100, 128, 512, {}), (40, 256, 512, {}),
                                        (40, 256, 512, dict(tile_mir=256)), (40, 256, 512, dict(tile_dx=256)),
-                                       (40, 256, 512, dict(tile_mir=256, tile_dx=256))])
+                                       (40, 256, 512, dict(tile_mir=256, tile_dx=256)),
+                                       (40, 256, 512, dict(cta_pair=1)), (40, 256, 512, dict(dw_lag=5))])
 def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     """Option overlap (reading A24): with a SLM_ALLOC_MIRROR_PARITY plan each segment's recompute
     runs on its own stream, concurrent with the backward of the next segment.  The step must
@@ -304,7 +305,7 @@ def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     for bit, repeatedly (a race on a recycled pool slot would show up as a mismatch); plans
     without the flag fall back to the sequential schedule with the same bits."""
     inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=7)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, **{k: v for k, v in opt.items() if k == "tile_dx"})
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, **{k: v for k, v in opt.items() if k != "tile_mir"})
     par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
     p, g, x0, y = _dev(inp, "bf16")
     model = slm.ChainModel(p, g, dtype="bf16", batch=B, **opt)
