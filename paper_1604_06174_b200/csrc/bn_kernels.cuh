@@ -169,3 +169,118 @@ __global__ void __launch_bounds__(F * 32) bn_bwd_rk(const float* __restrict__ P,
 }
 
 }  // namespace slmk
+
+namespace slmk {
+
+// ---------------------------------------------------------------- vectorised K1 / finalize (option bn_vec)
+// CTA = 16 features x 128 row groups (512 threads): thread t holds features 4 (t % 4) .. +3 of
+// rows rg, rg + 128, ... (rg = t / 4, R4 = B / 128 rows), loaded as float4 (a warp covers 8 rows
+// x 64 contiguous bytes per instruction, 4x fewer memory instructions than bn_act_rk).  Per
+// feature reductions in a fixed order: serial over the thread's rows, xor-shuffle tree over the
+// 8 row groups of a warp (offsets 4, 8, 16), then the 16 warps' partials added in warp order.
+// The forward finalize and the K1 before a mirror run both use this kernel, so their statistics
+// are bit-identical; it is not bit-identical to bn_act_rk (another order).
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 f4_shfl_tree(float4 v) {
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    float4 u;
+    u.x = __shfl_xor_sync(0xffffffffu, v.x, o);
+    u.y = __shfl_xor_sync(0xffffffffu, v.y, o);
+    u.z = __shfl_xor_sync(0xffffffffu, v.z, o);
+    u.w = __shfl_xor_sync(0xffffffffu, v.w, o);
+    // fixed operand order (lower lane first) so every lane of the group computes the same bits
+    const bool lo = (threadIdx.x & o) == 0;
+    v = lo ? f4_add(v, u) : f4_add(u, v);
+  }
+  return v;
+}
+// sum over the CTA's 128 row groups of this thread's 4 features (result valid in every thread)
+__device__ __forceinline__ float4 cta_quad_sum(float4 v, float4 (*red)[4]) {
+  v = f4_shfl_tree(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane < 4) red[warp][lane] = v;
+  __syncthreads();
+  float4 t = red[0][lane & 3];
+#pragma unroll
+  for (int w = 1; w < 16; ++w) t = f4_add(t, red[w][lane & 3]);
+  __syncthreads();
+  return t;
+}
+
+template <int R4, int NS>
+__global__ void __launch_bounds__(512) bn_act_v4(const float* xin, const float* __restrict__ P, unsigned pslice,
+                                                 const float* __restrict__ bias, float* xout,
+                                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                 int d, float* __restrict__ stats, __nv_bfloat16* __restrict__ a) {
+  __shared__ float4 red[16][4];
+  pdl_wait();
+  const int fq = threadIdx.x & 3, rg = threadIdx.x >> 2;
+  const int f0 = blockIdx.x * 16 + 4 * fq;
+  const unsigned base = (unsigned)rg * d + f0, rs = 128u * d;
+  float4 v[R4];
+#pragma unroll
+  for (int i = 0; i < R4; ++i) v[i] = *reinterpret_cast<const float4*>(xin + base + i * rs);
+  if (NS > 0) {
+    float4 t[NS > 0 ? NS : 1][R4];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int i = 0; i < R4; ++i) t[s][i] = *reinterpret_cast<const float4*>(P + s * pslice + base + i * rs);
+    const float4 bf = *reinterpret_cast<const float4*>(bias + f0);
+#pragma unroll
+    for (int i = 0; i < R4; ++i) {
+      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) z = f4_add(z, t[s][i]);
+      v[i] = f4_add(v[i], f4_add(z, bf));
+      *reinterpret_cast<float4*>(xout + base + i * rs) = v[i];
+    }
+  }
+  pdl_launch();
+  if (gamma == nullptr) return;
+  constexpr float invB = 1.0f / (128 * R4);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < R4; ++i) s = f4_add(s, v[i]);
+  const float4 S = cta_quad_sum(s, red);
+  const float4 mu = make_float4(__fmul_rn(S.x, invB), __fmul_rn(S.y, invB), __fmul_rn(S.z, invB), __fmul_rn(S.w, invB));
+  float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < R4; ++i) {
+    const float cx = __fsub_rn(v[i].x, mu.x), cy = __fsub_rn(v[i].y, mu.y), cz = __fsub_rn(v[i].z, mu.z),
+                cw = __fsub_rn(v[i].w, mu.w);
+    q = make_float4(__fmaf_rn(cx, cx, q.x), __fmaf_rn(cy, cy, q.y), __fmaf_rn(cz, cz, q.z), __fmaf_rn(cw, cw, q.w));
+  }
+  const float4 Q = cta_quad_sum(q, red);
+  float rstd[4];
+  const float* Qp = &Q.x;
+  const float* mp = &mu.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) rstd[k] = __frcp_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(Qp[k], invB), kEps)));
+  if (rg == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      stats[f0 + k] = mp[k];
+      stats[d + f0 + k] = rstd[k];
+    }
+  }
+  const float4 g = *reinterpret_cast<const float4*>(gamma + f0), bt = *reinterpret_cast<const float4*>(beta + f0);
+  const float* gp = &g.x;
+  const float* bp = &bt.x;
+#pragma unroll
+  for (int i = 0; i < R4; ++i) {
+    const float* vp = &v[i].x;
+    __nv_bfloat16 o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = __float2bfloat16_rn(fmaxf(bn_u(bn_xhat(vp[k], mp[k], rstd[k]), gp[k], bp[k]), 0.f));
+    uint2 pk;
+    pk.x = (uint32_t)__bfloat16_as_ushort(o[0]) | ((uint32_t)__bfloat16_as_ushort(o[1]) << 16);
+    pk.y = (uint32_t)__bfloat16_as_ushort(o[2]) | ((uint32_t)__bfloat16_as_ushort(o[3]) << 16);
+    *reinterpret_cast<uint2*>(a + base + i * rs) = pk;
+  }
+}
+
+}  // namespace slmk

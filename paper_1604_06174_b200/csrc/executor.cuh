@@ -224,6 +224,21 @@ cudaError_t act_rk(int R, int ns, int F, cudaStream_t st, bool pdl, int d, const
 #undef SLM_ACT
   return cudaErrorInvalidValue;
 }
+// vectorised K1 / finalize (option bn_vec): B in {128, 256}
+cudaError_t act_v4(int B, int ns, cudaStream_t st, bool pdl, int d, const float* xin, const float* P,
+                   unsigned pslice, const float* bias, float* xout, const float* ga, const float* be, float* stats,
+                   __nv_bfloat16* a) {
+#define SLM_AV(R_, NS_)                                                                                      \
+  if (B == 128 * R_ && ns == NS_)                                                                           \
+    return launch_k(slmk::bn_act_v4<R_, NS_>, dim3(d / 16), dim3(512), 0, st, pdl, xin, P, pslice, bias, xout, ga, \
+                    be, d, stats, a);
+#define SLM_AV_R(R_) SLM_AV(R_, 0) SLM_AV(R_, 1) SLM_AV(R_, 2) SLM_AV(R_, 4) SLM_AV(R_, 8)
+  SLM_AV_R(1) SLM_AV_R(2)
+#undef SLM_AV_R
+#undef SLM_AV
+  return cudaErrorInvalidValue;
+}
+
 template <int R, int NS, int F>
 cudaError_t launch_bwd_rk(cudaStream_t st, bool pdl, int d, const float* P, unsigned pslice, const float* x,
                           const float* ga, const float* be, const float* g, float* dx, float* dga, float* dbe,
@@ -318,6 +333,8 @@ struct slm_model {
   int sk_fwd = 0, sk_dx = 0;                  // split-K of the fused forward / dX GEMMs (0 = auto)
   int fused_bn = 0;                           // N tile of the fused forward / dX GEMMs (0 = batch)
   int cta_pair = 0;                           // fused forward / dX GEMMs as CTA pairs (cta_group::2)
+  int bn_vec = 0;                             // vectorised forward BN kernel (bn_act_v4; another reduction order;
+                                              // measured slower at C2: 14.3 vs 13.1 us per forward Block)
   int bn_feat = 16;                           // features per CTA of the BN kernels (16 | 8; same bits; 8 measured slower)
   int tile_dx = 0, tile_mir = 0;              // N tiles of the dX / recompute-stream GEMMs (0 = fused_bn rule)
   int blk_cluster = 0;                        // forward Block as one cluster kernel (blk_cluster.cuh; B = 256;
@@ -682,6 +699,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
                     cudaStream_t fs = nullptr, void* fa = nullptr, float* fstats = nullptr) -> cudaError_t {
     const float* ga = l < n ? gam + (size_t)l * d : nullptr;
     const float* be = l < n ? bet + (size_t)l * d : nullptr;
+    if (fz && m.bn_vec && (B == 128 || B == 256))
+      return act_v4(B, Pp ? nsplit : 0, fs ? fs : st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be,
+                    fstats ? fstats : stats, (bf*)(fa ? fa : abuf));
     if (fz)
       return act_rk(B / 32, Pp ? nsplit : 0, bnf_(), fs ? fs : st, pdl, d, xin, Pp, (unsigned)pslice, bias, xout, ga, be,
                     fstats ? fstats : stats, (bf*)(fa ? fa : abuf));

@@ -229,6 +229,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "blk_cluster") m->blk_cluster = (int)value;
   else if (k == "tile_dx") m->tile_dx = (int)value;
   else if (k == "bn_feat") m->bn_feat = (int)value;
+  else if (k == "bn_vec") m->bn_vec = (int)value;
   else if (k == "tile_mir") m->tile_mir = (int)value;
   else if (k == "s3_prio") {
     if (m->s3) {

@@ -297,7 +297,8 @@ def test_persistent_forward_option(slm, n, B, d):
 @pytest.mark.parametrize("n,B,d,opt", [(40, 64, 256, {}), (100, 128, 512, {}), (40, 256, 512, {}),
                                        (40, 256, 512, dict(tile_mir=256)), (40, 256, 512, dict(tile_dx=256)),
                                        (40, 256, 512, dict(tile_mir=256, tile_dx=256)),
-                                       (40, 256, 512, dict(cta_pair=1)), (40, 256, 512, dict(dw_lag=5))])
+                                       (40, 256, 512, dict(cta_pair=1)), (40, 256, 512, dict(dw_lag=5)),
+                                       (40, 256, 512, dict(bn_vec=1)), (40, 128, 512, dict(bn_vec=1, sk_fwd=4))])
 def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     """Option overlap (reading A24): with a SLM_ALLOC_MIRROR_PARITY plan each segment's recompute
     runs on its own stream, concurrent with the backward of the next segment.  The step must
@@ -389,3 +390,15 @@ def test_bn_feat_option_same_bits(slm):
         assert loss == ref_loss, strategy
         for k in ref:
             assert np.array_equal(g[k], ref[k]), (strategy, k)
+
+
+@pytest.mark.parametrize("n,B,d", [(4, 128, 256), (3, 256, 256)])
+def test_bn_vec_option_vs_oracle(slm, n, B, d):
+    """Option bn_vec (bn_act_v4: float4 loads, shuffle-tree statistics in another fixed order):
+    within the bf16 tolerance of the fp64 oracle (ReLU-margin inputs)."""
+    inp = margin_inputs(n, B, d, "bf16")
+    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, bn_vec=1)
+    ol, og, _ = _oracle(n, B, d, "bf16", inp)
+    assert abs(loss - ol) <= 2e-2 * abs(ol)
+    for k in og:
+        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
