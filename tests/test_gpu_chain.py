@@ -402,3 +402,28 @@ def test_bn_vec_option_vs_oracle(slm, n, B, d):
     assert abs(loss - ol) <= 2e-2 * abs(ol)
     for k in og:
         assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
+
+
+@pytest.mark.parametrize("strategy,kw", [("recursive", dict(k=1)), ("recursive", dict(k=2)), ("budget", dict(budget=0)),
+                                         ("sqrt", {})])
+def test_overlap_soundness_check_other_plans(slm, strategy, kw):
+    """The executor re-checks A24's disjointness on every plan: recursive / budget plans built
+    with SLM_ALLOC_MIRROR_PARITY run overlapped only when the check holds, sequentially
+    otherwise, and give the non-checkpointed bits either way (n = 2: a single mirror run, no
+    overlap possible)."""
+    for n in (2, 33):
+        B, d = 64, 256
+        inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=17)
+        ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+        p, g, x0, y = _dev(inp, "bf16")
+        model = slm.ChainModel(p, g, dtype="bf16", batch=B)
+        par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+        plan = slm.Plan(slm.Graph.chain(n, B, d), strategy, alloc_flags=par, **kw)
+        for _ in range(2):
+            loss = model.step(plan, x0, y)
+            torch.cuda.synchronize()
+            assert float(loss.item()) == ref_loss, (n, strategy)
+            for k in ref:
+                assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (n, strategy, k)
+        if n == 2:
+            assert model.get_option("last_overlap") == 0
