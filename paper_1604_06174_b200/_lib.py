@@ -8,7 +8,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslm.so")
+# SLM_LIB: an alternative in-tree build of the same library (compile-time kernel experiments, e.g.
+# scripts that A/B two builds); default libslm.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("SLM_LIB", "libslm.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python paper_1604_06174_b200/build.py` "

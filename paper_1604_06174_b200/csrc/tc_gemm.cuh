@@ -293,7 +293,14 @@ struct TcCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // as many stages as fit in ~200 KiB (up to 8): the K loop is latency bound, bytes in
   // flight per SM set its bandwidth
-  static constexpr int STAGES = (200 * 1024 / STAGE) > 8 ? 8 : (200 * 1024 / STAGE);
+  // SLM_DW_STAGES (compile-time experiment knob): stage cap of the weight-gradient GEMMs (both
+  // operands MN-major, short K = batch); 2 stages let two CTAs share an SM so one's epilogue
+  // overlaps the other's main loop
+#ifndef SLM_DW_STAGES
+#define SLM_DW_STAGES 2
+#endif
+  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : 8;
+  static constexpr int STAGES = (200 * 1024 / STAGE) > CAP ? CAP : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
