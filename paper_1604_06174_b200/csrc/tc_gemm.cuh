@@ -299,7 +299,10 @@ struct TcCfg {
 #ifndef SLM_DW_STAGES
 #define SLM_DW_STAGES 2
 #endif
-  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : 8;
+#ifndef SLM_DX_STAGES
+#define SLM_DX_STAGES 8
+#endif
+  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : (A_MN ? SLM_DX_STAGES : 8);
   static constexpr int STAGES = (200 * 1024 / STAGE) > CAP ? CAP : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
