@@ -293,14 +293,16 @@ struct TcCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   // as many stages as fit in ~200 KiB (up to 8): the K loop is latency bound, bytes in
   // flight per SM set its bandwidth
-  // SLM_DW_STAGES (compile-time experiment knob): stage cap of the weight-gradient GEMMs (both
-  // operands MN-major, short K = batch); 2 stages let two CTAs share an SM so one's epilogue
-  // overlaps the other's main loop
+  // Stage caps by operand majorness (compile-time knobs, measured): the weight-gradient GEMMs
+  // (both operands MN-major, short K = batch) keep 2 stages and the dX GEMMs (A = W read
+  // MN-major) 4, so two CTAs share an SM and one's epilogue overlaps the other's main loop in
+  // the throughput-bound backward phase (C2 34.7 -> 34.1 ms, C3 342 -> 327-331 ms); the forward
+  // GEMMs keep the deep ring (their W prefetch before the dependency wait is on the critical path)
 #ifndef SLM_DW_STAGES
 #define SLM_DW_STAGES 2
 #endif
 #ifndef SLM_DX_STAGES
-#define SLM_DX_STAGES 8
+#define SLM_DX_STAGES 4
 #endif
   static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : (A_MN ? SLM_DX_STAGES : 8);
   static constexpr int STAGES = (200 * 1024 / STAGE) > CAP ? CAP : (200 * 1024 / STAGE);
