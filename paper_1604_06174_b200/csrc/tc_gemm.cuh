@@ -297,14 +297,18 @@ struct TcCfg {
   // (both operands MN-major, short K = batch) keep 2 stages and the dX GEMMs (A = W read
   // MN-major) 4, so two CTAs share an SM and one's epilogue overlaps the other's main loop in
   // the throughput-bound backward phase (C2 34.7 -> 34.1 ms, C3 342 -> 327-331 ms); the forward
-  // GEMMs keep the deep ring (their W prefetch before the dependency wait is on the critical path)
+  // GEMMs keep the deep ring (their W prefetch before the dependency wait is on the critical path),
+  // except the narrow ones (N tile <= 64: the LSTM gates / head GEMMs, 4 stages: C3 327 -> 321 ms)
 #ifndef SLM_DW_STAGES
 #define SLM_DW_STAGES 2
 #endif
 #ifndef SLM_DX_STAGES
 #define SLM_DX_STAGES 4
 #endif
-  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : (A_MN ? SLM_DX_STAGES : 8);
+#ifndef SLM_NARROW_STAGES
+#define SLM_NARROW_STAGES 4
+#endif
+  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : (A_MN ? SLM_DX_STAGES : (BN <= 64 ? SLM_NARROW_STAGES : 8));
   static constexpr int STAGES = (200 * 1024 / STAGE) > CAP ? CAP : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
