@@ -308,7 +308,11 @@ struct TcCfg {
 #ifndef SLM_NARROW_STAGES
 #define SLM_NARROW_STAGES 4
 #endif
-  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES : (A_MN ? SLM_DX_STAGES : (BN <= 64 ? SLM_NARROW_STAGES : 8));
+#ifndef SLM_WIDE_STAGES
+#define SLM_WIDE_STAGES 8
+#endif
+  static constexpr int CAP = (A_MN && B_MN) ? SLM_DW_STAGES
+                             : (A_MN ? SLM_DX_STAGES : (BN <= 64 ? SLM_NARROW_STAGES : SLM_WIDE_STAGES));
   static constexpr int STAGES = (200 * 1024 / STAGE) > CAP ? CAP : (200 * 1024 / STAGE);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
