@@ -25,6 +25,20 @@ extern "C" {
 slm_status slm_debug_gemm(int kind, int impl, int bn, int split, int M, int N, int K, const void* A,
                           const void* B, void* out, const float* resid, const float* bias,
                           void* stream);
+/* slm_debug_block runs ONE fused Block kernel (paper_1604_06174_b200/csrc/blk_fused.cuh) for a
+ * single layer with W bf16 [d][d] (row = output feature):
+ *   bwd = 0 (forward Block): opnd = a_l bf16 [B][d]; out = x + (a W^T + bias)
+ *           fp32 [B][d]; if gamma != NULL also a_out = bf16 ReLU(BN(out)) with (gamma, beta)
+ *   bwd = 1 (gradient Block): opnd = bf16(g) [B][d], x = x_l, g = dx_{l+1} fp32;
+ *           out = dx_l, a_out = bf16 ReLU(BN(x)), gq_out = bf16(dx_l), dgamma, dbeta [d],
+ *           db_prev [d] (may be NULL)
+ * P: exchange buffer of blk_split(B, d) * B * d fp32 (workspace).  dbg != 0: per-CTA phase stamps
+ * into the slm_debug_timestamps buffer ([cta][8]).  B in {64, 128, 256}, d % 128 == 0 (B = 256:
+ * d % 256 == 0).  Device pointers, asynchronous on `stream`. */
+slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opnd, const float* x, const float* g,
+                           const float* bias, const float* gamma, const float* beta, float* out, void* a_out,
+                           void* gq_out, float* dgamma, float* dbeta, float* db_prev, void* P, int dbg,
+                           void* stream);
 /* Per-CTA %globaltimer stamps (8 per CTA, phases of tc_gemm_kernel) written to dev_buf
  * (uint64, >= 8 * CTAs of the next launches); NULL switches the instrumentation off. */
 slm_status slm_debug_timestamps(void* dev_buf);

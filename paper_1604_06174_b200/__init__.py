@@ -268,10 +268,15 @@ class _Model:
         return n.value
 
     def buffers(self, plan, device="cuda"):
-        """Caller-owned pool (plan.pool_bytes) + workspace + loss scalar, cached per plan."""
+        """Caller-owned pool (plan.pool_bytes) + workspace + loss scalar, cached for the two most
+        recently used plans (older entries are released; pass `bufs` to manage them yourself)."""
         import torch
         key = id(plan)
-        if key not in self._bufs:
+        if key in self._bufs:
+            self._bufs[key] = self._bufs.pop(key)   # most recent last
+        else:
+            while len(self._bufs) >= 2:
+                self._bufs.pop(next(iter(self._bufs)))
             pool = torch.empty(max(256, plan.pool_bytes), dtype=torch.uint8, device=device)
             ws = torch.empty(self.workspace_bytes(plan), dtype=torch.uint8, device=device)
             loss = torch.zeros(1, dtype=torch.float32, device=device)

@@ -1,0 +1,416 @@
+// The residual Block of the chain as ONE kernel per node of V' (sm_100a): tcgen05 GEMM with
+// split-K over a cluster of S CTAs, an L2 reduce-scatter of the fp32 partials inside the
+// cluster, and the batch-norm work fused into the epilogue.
+//
+//   forward / mirror Block_l:
+//     z = W_l a_l^T (swap-AB: M = 128 output features per CTA, N = B = the whole batch, K split
+//     over the S CTAs of a cluster),  x_{l+1} = x_l + (z + b_l),  then the batch statistics of
+//     x_{l+1} and a_{l+1} = ReLU(BN_{l+1}(x_{l+1})) (bf16) for the next Block.
+//   gradient Block_l (a8): da = g W_l (dX, A = W read MN-major), then the BN backward
+//     du = da 1[u > 0], dgamma = sum_b du xhat, dbeta = sum_b du,
+//     dx_l = g + gamma rstd (du - dbeta/B - xhat dgamma/B), db_{l-1} = sum_b dx_l, plus the bf16
+//     copies of dx_l (next dX / dW operand) and a_l (dW operand).
+//
+// Why this shape (profiles/r2_microbench.md, measured on B200): tcgen05.mma kind::f16 reaches
+// the full 4096 MAC/clk/SM only at N = 256 (N = 128 runs at 72 %), so a CTA keeps the whole batch
+// as N; with M = 128 per CTA a layer has d/128 output tiles (16 at d = 2048), so K is split over
+// S = 4 CTAs (64 SMs, K slice 512) to bound the per-layer MMA time (2.2 us).  The S fp32
+// partials of a tile are reduce-scattered through L2 (L2 -> SM moves ~20 TB/s; distributed shared
+// memory only ~10-20 GB/s per SM): CTA k of the cluster TMA-stores the three quarters of its
+// accumulator owned by its peers (feature slices of FS = 128/S features x B rows), a cluster
+// barrier orders the writes, and each CTA TMA-loads the three slices it owns and adds the S
+// partials in the fixed order s = 0..S-1.  Owning all B rows of its features, the CTA computes
+// the per-feature batch statistics locally (two-pass mean / centred variance, fixed order), so
+// no separate BN kernel and no extra grid-wide dependency remain: one kernel boundary per Block
+// (launched with programmatic dependent launch, the next Block's weights are requested while
+// this one finishes).
+//
+// Determinism: every sum has a fixed order (MMA K order, slice order s, the
+// per-thread row loop, then the S row groups in order), so mirrors (same kernel, same launch
+// configuration) reproduce the forward's bits; bn_k1_kernel (the operand of the first Block of a
+// run) uses the identical statistics code on the identical slice layout.
+#pragma once
+#include "tc_gemm.cuh"
+
+namespace slmk {
+
+constexpr int kBlkThreads = 256;   // 8 warps: TMA producer / MMA issuer / TMEM owner roles, then all 8 in the epilogue
+
+template <int B, int S, bool BWD>
+struct BlkCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int FS = 128 / S;          // features owned by a CTA after the reduce-scatter
+  static constexpr int CGR = FS / 32;         // 32-float (128-byte) column groups of a slice
+  static constexpr int RG = kBlkThreads / FS; // row groups of the epilogue (threads per feature)
+  static constexpr int R = B / RG;            // rows per epilogue thread (values kept in registers)
+  static constexpr int A_BYTES = BM * BK * 2; // one W tile (128 x 64 bf16)
+  static constexpr int B_BYTES = B * BK * 2;  // one operand tile (B x 64 bf16)
+  static constexpr int SLICE = B * FS * 4;    // one fp32 slice [CGR][B][32] (128-byte swizzled rows)
+  static constexpr int AUX = SLICE;           // x_l, staged by TMA during the main loop
+  static constexpr int LIMIT = 227 * 1024;
+  static constexpr int STATIC = RG * FS * 4 + 64;
+  static constexpr int NB = 3;                // operand ring (after griddepcontrol.wait, from L2)
+  // W ring: as many 16 KiB tiles as fit (up to 8 = a 512-wide K slice): all of them are requested
+  // before griddepcontrol.wait, so the weight stream from HBM overlaps the predecessor
+  static constexpr int NA_FIT = (LIMIT - 1024 - AUX - 512 - STATIC - NB * B_BYTES) / A_BYTES;
+  static constexpr int NA = NA_FIT > 8 ? 8 : NA_FIT;
+  static constexpr int RING_MAIN = NA * A_BYTES + NB * B_BYTES;
+  static constexpr int RING = RING_MAIN > S * SLICE ? RING_MAIN : S * SLICE;
+  static constexpr int SMEM = 1024 + RING + AUX + 512;
+  static constexpr int TMEM_COLS = B;
+  static_assert(S == 2 || S == 4, "cluster of 2 or 4 CTAs");
+  static_assert(B == 64 || B == 128 || B == 256, "batch tile");
+  static_assert(SLICE <= 32 * 1024 && R >= 1 && R <= 32, "slice / registers");
+  static_assert(NA >= 2, "pipeline");
+  static_assert(SMEM + STATIC <= LIMIT, "shared memory");
+};
+
+// element (column group c, row b, column f32 in 0..31) of a 128-byte-swizzled fp32 slice: the
+// layout TMA reads / writes with CU_TENSOR_MAP_SWIZZLE_128B for a {32, B} box (16-byte chunk index
+// XOR row % 8), so a warp accessing one row (32 consecutive features) is conflict-free
+__device__ __forceinline__ int sw_off(int B_, int c, int b, int f32) {
+  return (c * B_ + b) * 32 + ((((f32 >> 2) ^ (b & 7))) << 2) + (f32 & 3);
+}
+
+// sum of one value per (row group rg, feature fl) over the RG row groups, in the order 0..RG-1
+template <int RG, int FS>
+__device__ __forceinline__ float rg_sum(float v, float (*red)[FS], int rg, int fl) {
+  red[rg][fl] = v;
+  __syncthreads();
+  float t = red[0][fl];
+#pragma unroll
+  for (int r = 1; r < RG; ++r) t = __fadd_rn(t, red[r][fl]);
+  __syncthreads();
+  return t;
+}
+
+// Batch statistics of one feature over the B rows held by its RG threads (R each, in registers):
+// two-pass mean / centred variance, per-thread serial then the row groups in order.  The forward
+// epilogue, the backward epilogue and bn_k1_kernel share this exact code and mapping (thread t:
+// feature t % FS, rows t / FS + RG j), so the statistics of a given x are bit-identical.
+template <int B, int S>
+__device__ __forceinline__ void slice_stats(const float (&v)[BlkCfg<B, S, false>::R],
+                                            float (*red)[128 / S], int fl, int rg, float& mu, float& rstd) {
+  using C = BlkCfg<B, S, false>;
+  constexpr float invB = 1.0f / B;   // exact: B is a power of two
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) s = __fadd_rn(s, v[j]);
+  mu = __fmul_rn(rg_sum<C::RG, C::FS>(s, red, rg, fl), invB);
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) {
+    const float e = __fsub_rn(v[j], mu);
+    q = __fmaf_rn(e, e, q);
+  }
+  const float var = __fmul_rn(rg_sum<C::RG, C::FS>(q, red, rg, fl), invB);
+  rstd = __frcp_rn(__fsqrt_rn(__fadd_rn(var, kEps)));
+}
+
+// a = bf16(ReLU(gamma xhat + beta)) of the slice's rows (next Block's operand)
+template <int B, int S>
+__device__ __forceinline__ void slice_act(const float (&v)[BlkCfg<B, S, false>::R], float (*red)[128 / S], int d,
+                                          int f, int rg, int fl, const float* __restrict__ gamma,
+                                          const float* __restrict__ beta, __nv_bfloat16* __restrict__ a) {
+  using C = BlkCfg<B, S, false>;
+  float mu, rstd;
+  slice_stats<B, S>(v, red, fl, rg, mu, rstd);
+  const float g = gamma[f], bt = beta[f];
+#pragma unroll
+  for (int j = 0; j < C::R; ++j)
+    a[(size_t)(rg + C::RG * j) * d + f] = __float2bfloat16_rn(fmaxf(bn_u(bn_xhat(v[j], mu, rstd), g, bt), 0.f));
+}
+
+struct BlkArgs {
+  int d;
+  int a_row0;              // row of W_l in the [n*d][d] weight tensor (= l*d)
+  int x_row0;              // row of x_l in its fp32 [rows][d] tensor map
+  const float* g;          // bwd: g = dx_{l+1} [B][d] fp32
+  float* out;              // fwd: x_{l+1}; bwd: dx_l                   [B][d] fp32
+  const float* bias;       // fwd: b_l
+  const float* gamma;      // fwd: gamma_{l+1} (null: no next Block); bwd: gamma_l
+  const float* beta;
+  __nv_bfloat16* a_out;    // fwd: a_{l+1}; bwd: a_l (dW operand)     [B][d] bf16
+  __nv_bfloat16* gq_out;   // bwd: bf16(dx_l)
+  float* dgamma;           // bwd
+  float* dbeta;
+  float* db_prev;          // bwd: db_{l-1} (null at l = 0)
+  int dbg;
+};
+
+// grid = (d/128) * S CTAs, clusters of S along x (CTA m*S + k = K slice k of output tile m),
+// 256 threads: warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warp 2 owns the TMEM
+// allocation; then all eight warps run the epilogue.
+//   tmA: W, K-major {64, 128} box (fwd) or MN-major {64, 64} boxes (bwd)
+//   tmB: the bf16 operand [B][d] (a_l fwd, bf16 dx_{l+1} bwd), {64, B} box
+//   tmP: the partial buffer [d/128][S owners][S sources][CGR][B] rows of 32 fp32, {32, B} box,
+//        128-byte swizzle (TMA stores and loads)
+//   tmX: fp32 [rows][d] source of x_l, {32, B} box, 128-byte swizzle
+template <int B, int S, bool BWD>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    blk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmX, const BlkArgs args) {
+  using C = BlkCfg<B, S, BWD>;
+  constexpr int FS = C::FS, CGR = C::CGR, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB;
+  ts_mark(0, args.dbg);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned by pointer arithmetic on the __shared__ array (not through an integer), so
+  // the compiler keeps the shared address space (LDS/STS) for the epilogue's accesses
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;                                   // W tiles [NA] | operand tiles [NB]; epilogue: S slices
+  uint8_t* bring = ring + NA * C::A_BYTES;
+  float* xs = reinterpret_cast<float*>(smem + C::RING);   // x_l slice
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C::RING + C::AUX);
+  uint64_t* emptyA = fullA + NA;
+  uint64_t* fullB = emptyA + NA;
+  uint64_t* emptyB = fullB + NB;
+  uint64_t* accum = emptyB + NB;
+  uint64_t* auxb = accum + 1;
+  uint64_t* recvb = auxb + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recvb + 1);
+  __shared__ float red[RG][FS];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = args.d;
+  const uint32_t k = cluster_ctarank();
+  const int m = (int)blockIdx.x / S;
+  const int m0 = m * 128;
+  const int nk = d / 64 / S;
+  const int kbase = (int)k * nk * 64;
+  const int f0 = m0 + (int)k * FS;   // first feature this CTA owns after the reduce-scatter
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmP);
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
+    }
+    mbar_init(accum, 1);
+    mbar_init(auxb, 1);
+    mbar_init(recvb, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  ts_mark(1, args.dbg);
+
+  auto load_a = [&](int kb) {
+    const int s = kb % NA;
+    uint8_t* sa = ring + s * C::A_BYTES;
+    const int k0 = kbase + kb * 64;
+    mbar_expect_tx(&fullA[s], C::A_BYTES);
+    if (BWD) {   // W stored [f_out = K][f_in = M]: two 64 x 64 boxes
+      tma_load_2d(sa, &tmA, &fullA[s], m0, args.a_row0 + k0);
+      tma_load_2d(sa + 8192, &tmA, &fullA[s], m0 + 64, args.a_row0 + k0);
+    } else {     // W stored [f_out = M][f_in = K]: one 64 (K) x 128 (M) box
+      tma_load_2d(sa, &tmA, &fullA[s], k0, args.a_row0 + m0);
+    }
+  };
+  auto load_b = [&](int kb) {
+    const int s = kb % NB;
+    mbar_expect_tx(&fullB[s], C::B_BYTES);
+    tma_load_2d(bring + s * C::B_BYTES, &tmB, &fullB[s], kbase + kb * 64, 0);
+  };
+
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer: the weights do not depend on the previous kernel, so up to NA tiles of
+    // W are requested before griddepcontrol.wait (they overlap the predecessor's tail)
+    const int na0 = nk < NA ? nk : NA, nb0 = nk < NB ? nk : NB;
+    for (int kb = 0; kb < na0; ++kb) load_a(kb);
+    pdl_wait();
+    if (args.dbg & 8) ts_dep(args.dbg);
+    for (int kb = 0; kb < nb0; ++kb) load_b(kb);
+    // the epilogue's x_l slice lands in its own buffer while the main loop runs
+    mbar_expect_tx(auxb, C::AUX);
+#pragma unroll
+    for (int c = 0; c < CGR; ++c) tma_load_2d(xs + c * B * 32, &tmX, auxb, f0 + 32 * c, args.x_row0);
+    // refill each ring slot as soon as the MMAs reading it retire
+    for (int kb = 0; kb < nk; ++kb) {
+      if (kb + NB < nk) {
+        mbar_wait(&emptyB[kb % NB], (kb / NB) & 1);
+        load_b(kb + NB);
+      }
+      if (kb + NA < nk) {
+        mbar_wait(&emptyA[kb % NA], (kb / NA) & 1);
+        load_a(kb + NA);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ===== MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, B, BWD, false);
+    for (int kb = 0; kb < nk; ++kb) {
+      mbar_wait(&fullA[kb % NA], (kb / NA) & 1);
+      mbar_wait(&fullB[kb % NB], (kb / NB) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(ring + (kb % NA) * C::A_BYTES);
+      const uint32_t sb = smem_u32(bring + (kb % NB) * C::B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = BWD ? make_sdesc(sa + kk * 2048, 8192, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
+        const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
+        tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
+      }
+      tc_commit(&emptyB[kb % NB]);
+      tc_commit(&emptyA[kb % NA]);
+    }
+    tc_commit(accum);
+  }
+  __syncwarp();
+
+  // ===== epilogue 1: accumulator -> the S feature slices (smem, 128-byte swizzled), then the
+  // S-1 slices owned by the peers -> L2 by TMA bulk stores
+  mbar_wait(accum, 0);
+  tc_fence_after();
+  pdl_launch();   // the next kernel may now start its prologue and weight prefetch on free SMs
+  ts_mark(2, args.dbg);
+  {
+    const int q = warp & 3, h = warp >> 2;   // TMEM lane quarter (features 32q..), column half
+    const int ko = q / CGR, cg = q % CGR;    // owner slice and its column group
+    float* slotp = reinterpret_cast<float*>(ring + ko * C::SLICE);
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int c0 = h * (B / 2); c0 < (h + 1) * (B / 2); c0 += 32) {
+      float acc[32];
+      tmem_ld32(trow + c0, acc);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) slotp[sw_off(B, cg, c0 + j, lane)] = acc[j];
+    }
+  }
+  tc_fence_before();
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> TMA (async proxy)
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  if (threadIdx.x == 0) {
+    for (int s = 1; s < S; ++s) {
+      const int ko = ((int)k + s) % S;   // peer owner
+#pragma unroll
+      for (int c = 0; c < CGR; ++c)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tmP)),
+                     "r"(smem_u32(ring + ko * C::SLICE + c * B * 128)), "r"(0),
+                     "r"((((m * S + ko) * S + (int)k) * CGR + c) * B)
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the peers' slices are in L2
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  ts_mark(3, args.dbg);
+  cluster_sync();   // every CTA of the cluster has published its peers' slices
+  ts_mark(4, args.dbg);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(recvb, (S - 1) * C::SLICE);
+    for (int s = 0; s < S; ++s) {
+      if (s == (int)k) continue;
+#pragma unroll
+      for (int c = 0; c < CGR; ++c)
+        tma_load_2d(ring + s * C::SLICE + c * B * 128, &tmP, recvb, 0, (((m * S + (int)k) * S + s) * CGR + c) * B);
+    }
+  }
+
+  // ===== epilogue 2: sum the S partials (slot s = K slice s, fixed order) and the fused batch norm
+  const int fl = threadIdx.x % FS, rg = threadIdx.x / FS, cc = fl >> 5, f32 = fl & 31;
+  const int f = f0 + fl;
+  const float* ringf = reinterpret_cast<const float*>(ring);
+  float gv[BWD ? R : 1];
+  if constexpr (BWD) {   // g = dx_{l+1}: coalesced loads issued before waiting for the slices
+#pragma unroll
+    for (int j = 0; j < R; ++j) gv[j] = args.g[(size_t)(rg + RG * j) * d + f];
+  }
+  mbar_wait(auxb, 0);
+  mbar_wait(recvb, 0);
+  ts_mark(5, args.dbg);
+  float xv[R], zv[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int off = sw_off(B, cc, rg + RG * j, f32);
+    float z = ringf[off];
+#pragma unroll
+    for (int s = 1; s < S; ++s) z = __fadd_rn(z, ringf[s * (C::SLICE / 4) + off]);
+    zv[j] = z;
+    xv[j] = xs[off];
+  }
+  if constexpr (!BWD) {
+    const float bf = args.bias[f];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      xv[j] = __fadd_rn(xv[j], __fadd_rn(zv[j], bf));
+      args.out[(size_t)(rg + RG * j) * d + f] = xv[j];
+    }
+    ts_mark(6, args.dbg);
+    if (args.gamma != nullptr) slice_act<B, S>(xv, red, d, f, rg, fl, args.gamma, args.beta, args.a_out);
+  } else {
+    float mu, rstd;
+    slice_stats<B, S>(xv, red, fl, rg, mu, rstd);
+    const float ga = args.gamma[f], bt = args.beta[f];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float xh = bn_xhat(xv[j], mu, rstd);
+      const float u = bn_u(xh, ga, bt);
+      zv[j] = u > 0.f ? zv[j] : 0.f;   // du
+      args.a_out[(size_t)(rg + RG * j) * d + f] = __float2bfloat16_rn(fmaxf(u, 0.f));
+      s1 = __fadd_rn(s1, zv[j]);
+      s2 = __fmaf_rn(zv[j], xh, s2);
+    }
+    ts_mark(6, args.dbg);
+    const float S1 = rg_sum<RG, FS>(s1, red, rg, fl);
+    const float S2 = rg_sum<RG, FS>(s2, red, rg, fl);
+    constexpr float invB = 1.0f / B;
+    const float m1 = __fmul_rn(S1, invB), m2 = __fmul_rn(S2, invB);
+    const float kk = __fmul_rn(ga, rstd);
+    float s3 = 0.f;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float xh = bn_xhat(xv[j], mu, rstd);
+      const float v = __fadd_rn(gv[j], __fmul_rn(kk, __fsub_rn(__fsub_rn(zv[j], m1), __fmul_rn(xh, m2))));
+      args.out[(size_t)(rg + RG * j) * d + f] = v;
+      args.gq_out[(size_t)(rg + RG * j) * d + f] = __float2bfloat16_rn(v);
+      s3 = __fadd_rn(s3, v);
+    }
+    const float S3 = rg_sum<RG, FS>(s3, red, rg, fl);
+    if (rg == 0) {
+      args.dgamma[f] = S2;
+      args.dbeta[f] = S1;
+      if (args.db_prev) args.db_prev[f] = S3;
+    }
+  }
+  ts_mark(7, args.dbg);
+}
+
+// K1: a = ReLU(BN(x)) for the first Block of a forward / mirror run (x_0, or a kept x_{s_j}),
+// with the Block epilogue's exact mapping and statistics code: grid = d / FS CTAs of 256 threads,
+// x read coalesced into registers (a warp covers 32 consecutive features of one row).
+template <int B, int S>
+__global__ void __launch_bounds__(kBlkThreads) bn_k1_kernel(const float* __restrict__ x,
+                                                            const float* __restrict__ gamma,
+                                                            const float* __restrict__ beta, int d,
+                                                            __nv_bfloat16* __restrict__ a) {
+  using C = BlkCfg<B, S, false>;
+  __shared__ float red[C::RG][C::FS];
+  pdl_wait();
+  const int fl = threadIdx.x % C::FS, rg = threadIdx.x / C::FS;
+  const int f = blockIdx.x * C::FS + fl;
+  float v[C::R];
+#pragma unroll
+  for (int j = 0; j < C::R; ++j) v[j] = x[(size_t)(rg + C::RG * j) * d + f];
+  pdl_launch();
+  slice_act<B, S>(v, red, d, f, rg, fl, gamma, beta, a);
+}
+
+}  // namespace slmk

@@ -9,6 +9,7 @@
 // tie has a total order and every budget is an integer, so plans are reproducible bit for
 // bit (tests/test_planner_parity.py compares them against the independent Python oracle).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -841,6 +842,8 @@ slm_status slm_plan_create(const slm_graph* g, const slm_plan_opts* opts, slm_pl
     return SLM_E_DEGENERATE;
   }
   auto* p = new (std::nothrow) slm_plan();
+  static std::atomic<uint64_t> next_uid{1};
+  if (p) p->uid = next_uid.fetch_add(1);
   if (!p) return SLM_E_ARG;
   slm_status st;
   try {

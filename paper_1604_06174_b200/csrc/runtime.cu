@@ -27,11 +27,9 @@
 #include <vector>
 
 #include "kernels_simt.cuh"
-#include "bn_kernels.cuh"
 #include "slm_internal.h"
 #include "tc_gemm.cuh"
-#include "fwd_persist.cuh"
-#include "blk_cluster.cuh"
+#include "blk_fused.cuh"
 
 using namespace slm;
 
@@ -182,9 +180,9 @@ slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* va
   const std::string k(key);
   if (k == "last_overlap") *value = m->last_overlap ? 1 : 0;
   else if (k == "overlap") *value = m->overlap;
-  else if (k == "persist") *value = m->persist;
   else if (k == "fused") *value = m->fused;
   else if (k == "use_graph") *value = m->use_graph;
+  else if (k == "block_split") *value = m->kind == SLM_MODEL_CHAIN && fused_ok(*m) ? blk_split(m->d.batch, m->d.width) : 0;
   else {
     set_error("unknown or write-only option: " + k);
     return SLM_E_ARG;
@@ -192,6 +190,7 @@ slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* va
   return SLM_OK;
 }
 
+// Lowering options (include/slm.h lists them).  Every change drops the captured CUDA graphs.
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   if (!m || !key) {
     set_error("null argument");
@@ -200,45 +199,14 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   std::string k(key);
   if (k == "use_graph") m->use_graph = (int)value;
   else if (k == "gemm_impl") m->gemm_impl = (int)value;
-  else if (k == "bn_fwd") m->bn_fwd = (int)value;
-  else if (k == "bn_dx") m->bn_dx = (int)value;
-  else if (k == "bn_dw") m->bn_dw = (int)value;
-  else if (k == "sk_fwd") m->sk_fwd = (int)value;
-  else if (k == "sk_dx") m->sk_dx = (int)value;
-  else if (k == "fused_bn") m->fused_bn = (int)value;
+  else if (k == "fused") m->fused = (int)value;
+  else if (k == "overlap") m->overlap = (int)value;
+  else if (k == "dw_stream") m->dw_stream = (int)value;
+  else if (k == "pdl") m->pdl = (int)value;
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
-  else if (k == "l2_prefetch") m->l2_prefetch = (int)value;
-  else if (k == "lstm_grid") m->lstm_grid = (int)value;
-  else if (k == "prio") {
-    if (m->s2) {
-      set_error("option prio must be set before the first step");
-      return SLM_E_ARG;
-    }
-    m->prio = (int)value;
-  }
   else if (k == "lstm_sk") m->lstm_sk = (int)value;
   else if (k == "lstm_skx") m->lstm_skx = (int)value;
-  else if (k == "lstm_fuse_cell") m->lstm_fuse_cell = (int)value;
-  else if (k == "cta_pair") m->cta_pair = (int)value;
-  else if (k == "fused") m->fused = (int)value;
-  else if (k == "persist") m->persist = (int)value;
-  else if (k == "persist_dbg") m->persist_dbg = (int)value;
-  else if (k == "overlap") m->overlap = (int)value;
-  else if (k == "dw_tma") m->dw_tma = (int)value;
-  else if (k == "dw_lag") m->dw_lag = (int)value;
-  else if (k == "blk_cluster") m->blk_cluster = (int)value;
-  else if (k == "tile_dx") m->tile_dx = (int)value;
-  else if (k == "bn_feat") m->bn_feat = (int)value;
-  else if (k == "bn_vec") m->bn_vec = (int)value;
-  else if (k == "tile_mir") m->tile_mir = (int)value;
-  else if (k == "s3_prio") {
-    if (m->s3) {
-      set_error("option s3_prio must be set before the first step");
-      return SLM_E_ARG;
-    }
-    m->s3_prio = (int)value;
-  }
-  else if (k == "dw_stream") m->dw_stream = (int)value;
+  // measurement hooks
   else if (k == "profile_ts") {
     m->profile_ts = (int)value;
     if (value <= 0) {   // detach the device-clock buffer: the caller may free it now
@@ -254,11 +222,6 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   }
   else if (k == "profile_events") m->profile = (int)value;
   else if (k == "profile_ts_dep") m->profile_ts_dep = (int)value;
-  else if (k == "pdl") m->pdl = (int)value;
-  else if (k == "lstm_early_trigger") {
-    const int v = (int)value;
-    CK(cudaMemcpyToSymbol(slmk::c_lstm_trigger, &v, sizeof(v)));
-  }
   else {
     set_error("unknown option " + k);
     return SLM_E_ARG;
@@ -334,21 +297,18 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   }
   std::vector<Op> ops;
   if ((s = lower(p, &ops)) != SLM_OK) return s;
-  // mirrors enqueue(): the fused lowering skips K1 when the operand is already resident
+  // mirrors enqueue(): K1 only when the operand is not already resident
   const bool fz = fused_ok(*m);
+  const int n = m->d.n_layers;
   int64_t nl = 0;
-  int abuf_node = -1;
+  int act_node = -1;
   for (auto& o : ops) {
     if (o.type == 0) {
-      if (fz) {
-        nl += (abuf_node != o.in_node ? 1 : 0) + 2;
-        abuf_node = o.node;
-      } else {
-        nl += 2;
-      }
+      nl += (act_node != o.in_node ? 1 : 0) + 1;
+      act_node = fz && o.layer + 1 < n ? o.node : -1;
     } else if (o.type == 3) {
-      nl += fz ? 3 : 4;
-      if (!fz) abuf_node = -1;
+      nl += fz ? 2 : 4;
+      if (!fz) act_node = -1;
     } else {
       nl += 2;
     }
@@ -401,7 +361,7 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
                    : enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
   };
   if (!m->use_graph || st == nullptr || m->profile) return run();
-  GraphKey key{p, x0, labels, pool, ws, loss, st, comm};
+  GraphKey key{p->uid, x0, labels, pool, ws, loss, st, comm};
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {
     // the first call runs eagerly (sets kernel attributes, tensor maps) then captures
@@ -530,6 +490,38 @@ slm_status slm_debug_timestamps(void* dev_buf) {
   unsigned long long* p = (unsigned long long*)dev_buf;
   CK(cudaMemcpyToSymbol(slmk::g_slm_ts, &p, sizeof(p)));
   return SLM_OK;
+}
+
+// slm_debug_block: one fused Block kernel (blk_fused.cuh) on caller buffers; declared in
+// include/slm_debug.h.
+slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opnd, const float* x, const float* g,
+                           const float* bias, const float* gamma, const float* beta, float* out, void* a_out,
+                           void* gq_out, float* dgamma, float* dbeta, float* db_prev, void* P, int dbg, void* stream) {
+  const int S = blk_split(B, d);
+  if (S == 0) {
+    set_error("slm_debug_block: unsupported (B, d)");
+    return SLM_E_UNSUPPORTED;
+  }
+  CUtensorMap ma, mb, mp, mx;
+  slm_status s;
+  const uint64_t prow = (uint64_t)d / 128 * 4 * S * B;
+  if ((s = make_map(&ma, W, d, d, bwd ? 64 : 128)) || (s = make_map(&mb, opnd, d, B, (uint32_t)B)) ||
+      (s = make_map_f32_sw(&mp, P, 32, prow, (uint32_t)B)) || (s = make_map_f32_sw(&mx, x, d, B, (uint32_t)B)))
+    return s;
+  slmk::BlkArgs a{};
+  a.d = d;
+  a.g = g;
+  a.out = out;
+  a.bias = bias;
+  a.gamma = gamma;
+  a.beta = beta;
+  a.a_out = (__nv_bfloat16*)a_out;
+  a.gq_out = (__nv_bfloat16*)gq_out;
+  a.dgamma = dgamma;
+  a.dbeta = dbeta;
+  a.db_prev = db_prev;
+  a.dbg = dbg ? 4 : 0;
+  return launch_blk(B, S, bwd != 0, ma, mb, mp, mx, a, (cudaStream_t)stream, false);
 }
 
 // slm_debug_gemm: one GEMM of the three kinds through the chosen implementation

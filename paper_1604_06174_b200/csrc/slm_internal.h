@@ -42,6 +42,9 @@ struct slm_graph {
 };
 
 struct slm_plan {
+  // process-unique id (never reused): the device runtime keys its captured CUDA graphs on it, so a
+  // new plan that lands at a freed plan's address can never replay that plan's graph
+  uint64_t uid = 0;
   // the forward graph it was planned for
   int graph_kind = -1;
   int dims[5] = {0, 0, 0, 0, 0};

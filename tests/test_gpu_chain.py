@@ -1,16 +1,20 @@
 """Device parity of the checkpointed training step through the C ABI (slm_step).
 
-  * GPU vs the fp64 oracle: <= 1e-4 relative (f32, C1) and <= 2e-2 (bf16, against the
-    bf16-operand-emulating oracle) per tensor, ||g_gpu - g_ref|| / ||g_ref|| (reading A12).
+  * GPU vs the fp64 oracle, element by element (reading A12): |g - ref| <= tol (|ref| + rms(ref))
+    for every element of the loss and of every gradient tensor, and the relative L2 error <= tol;
+    tol = 1e-4 (f32, C1) and 2e-2 (bf16, against the bf16-operand-emulating oracle).
   * checkpointed GPU step == non-checkpointed GPU step, bit for bit, for every strategy.
   * full C2 size (n=1024, d=2048, B=256): the same bit-exactness plus closed forms.
+Inputs with a ReLU-margin screen (reading A20) are used where the 1e-4 f32 bar needs it and at
+small bf16 sizes; the C2-width tests use plain seeded inputs (a rare flipped ReLU mask bit moves
+one term of one batch sum, far inside the bf16 bound).
 """
 import numpy as np
 import pytest
 import torch
 
 import synth
-from _util import margin_inputs
+from _util import assert_close, margin_inputs
 from oracle import chain as OC
 from oracle import graph as OG
 from oracle import planner as OP
@@ -48,6 +52,12 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
+def _parity(loss, grads, ol, og, tol, tag=""):
+    """loss and every gradient tensor element by element; returns {name: (max_abs, rms_ref, rel)}"""
+    assert abs(loss - ol) <= tol * abs(ol), (tag, loss, ol)
+    return {k: assert_close(grads[k], og[k], tol, f"{tag} {k}") for k in og}
+
+
 def _oracle(n, B, d, dtype, inp):
     Pm = OC.Params(inp["W"], inp["b"], inp["gamma"], inp["beta"])
     return OC.step_plain(Pm, inp["x0"], inp["labels"], "bf16" if dtype == "bf16" else "f64")
@@ -59,20 +69,24 @@ def test_c1_f32_vs_oracle(slm, strategy):
     inp = margin_inputs(n, B, d, "f32")
     loss, grads, _ = _run(slm, n, B, d, "f32", strategy, inp)
     ol, og, _ = _oracle(n, B, d, "f32", inp)
-    assert abs(loss - ol) / abs(ol) <= 1e-4
-    for k in og:
-        assert _rel(grads[k], og[k]) <= 1e-4, (k, _rel(grads[k], og[k]))
+    _parity(loss, grads, ol, og, 1e-4, strategy)
 
 
-@pytest.mark.parametrize("n,B,d", [(8, 64, 256), (5, 128, 384), (4, 256, 2048)])
+@pytest.mark.parametrize("n,B,d", [(3, 64, 256), (2, 64, 128), (2, 128, 384), (2, 128, 512), (2, 256, 512),
+                                   (2, 256, 2048)])
 @pytest.mark.parametrize("impl", [0, 1])
 def test_bf16_vs_oracle(slm, n, B, d, impl):
-    inp = margin_inputs(n, B, d, "bf16", seed=n + B + d)
-    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, gemm_impl=impl)
+    """The fused Block kernel (impl 0) at every cluster split it dispatches (block_split: S = 4 at
+    d % 256 == 0, S = 2 at B <= 128 with d = 128 / 384) and the SIMT path (impl 1), element by
+    element against the oracle.  Shallow chains: deeper ones drift from the oracle through
+    decision chaos for every implementation alike (test_bf16_depth_vs_oracle, reading A20)."""
+    inp = (margin_inputs(n, B, d, "bf16", seed=n + B + d) if n * B * d <= 300_000
+           else synth.chain_inputs(n, B, d, dtype="bf16", seed=n + B + d))
+    loss, grads, (model, *_rest) = _run(slm, n, B, d, "bf16", "sqrt", inp, gemm_impl=impl)
+    if impl == 0:
+        assert model.get_option("block_split") == (4 if d % 256 == 0 else 2)
     ol, og, _ = _oracle(n, B, d, "bf16", inp)
-    assert abs(loss - ol) / abs(ol) <= 2e-2
-    for k in og:
-        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
+    _parity(loss, grads, ol, og, 2e-2, f"impl{impl}")
 
 
 @pytest.mark.parametrize("dtype,n,B,d", [("f32", 16, 8, 64), ("bf16", 24, 64, 256), ("bf16", 9, 256, 512)])
@@ -145,16 +159,52 @@ def test_c2_full_size_bitwise_and_closed_form(slm):
     assert np.isfinite(out["sqrt"][0])
 
 
-@pytest.mark.slow
-def test_c2_width_depth4_vs_oracle(slm):
-    # full width and batch of C2 with 4 layers: the oracle finishes in seconds
-    n, B, d = 4, 256, 2048
-    inp = margin_inputs(n, B, d, "bf16", seed=11)
+def _norm_parity(loss, grads, ol, og, tol, tag):
+    """per-tensor relative L2 <= tol (north_star's bf16 bar) at depth; the element-wise statistics
+    are reported (a deep bf16 chain's rare decision flips make individual elements drift)"""
+    assert abs(loss - ol) <= tol * abs(ol), (tag, loss, ol)
+    out = {}
+    for k in og:
+        rel = _rel(grads[k], og[k])
+        err = np.abs(grads[k] - og[k])
+        frac = float((err > tol * (np.abs(og[k]) + np.sqrt(np.mean(og[k] ** 2)))).mean())
+        out[k] = (rel, float(err.max()), frac)
+        assert rel <= tol, (tag, k, rel)
+    print(tag, {k: f"rel {v[0]:.2e} max_abs {v[1]:.2e} frac_outside_elementwise {v[2]:.1e}" for k, v in out.items()})
+    return out
+
+
+@pytest.mark.parametrize("n,B,d", [(8, 64, 256), (8, 256, 2048)])
+def test_bf16_depth_vs_oracle(slm, n, B, d):
+    """Depth 8 (the C2 width and batch included): per-tensor relative L2 within 2e-2 of the oracle.
+    Element-wise agreement is checked per Block (test_gpu_block.py) and on shallow chains."""
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=16)
     loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp)
     ol, og, _ = _oracle(n, B, d, "bf16", inp)
-    assert abs(loss - ol) / abs(ol) <= 2e-2
-    for k in og:
-        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
+    _norm_parity(loss, grads, ol, og, 2e-2, f"depth n={n} B={B} d={d}")
+
+
+@pytest.mark.slow
+def test_c2_width_bench_plan_vs_oracle(slm):
+    """The bench's exact plan and launch configuration at C2 width and batch: sqrt(n) segments with
+    mirror-run parity (A24), the recompute overlapped with the backward on its own stream
+    (asserted through last_overlap), CUDA graph replay; against the oracle (n = 9: three segments
+    of three, so two recompute runs overlap the backward)."""
+    n, B, d = 9, 256, 2048
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=16)
+    p, g, x0, y = _dev(inp, "bf16")
+    model = slm.ChainModel(p, g, dtype="bf16", batch=B)
+    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
+    plan = slm.Plan(slm.Graph.chain(n, B, d), "sqrt", alloc_flags=par)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):   # eager + capture, then a replay
+            loss = model.step(plan, x0, y, stream=s)
+    torch.cuda.synchronize()
+    assert model.get_option("last_overlap") == 1
+    grads = {k: v.float().cpu().numpy().astype(np.float64) for k, v in g.items()}
+    ol, og, _ = _oracle(n, B, d, "bf16", inp)
+    _norm_parity(float(loss.item()), grads, ol, og, 2e-2, "bench plan")
 
 
 def test_zero_weights_closed_form(slm):
@@ -207,9 +257,7 @@ def test_edge_sizes_vs_oracle(slm, dtype, n, B, d):
     for strategy in ("none", "sqrt"):
         loss, grads, _ = _run(slm, n, B, d, dtype, strategy, inp)
         ol, og, _ = _oracle(n, B, d, dtype, inp)
-        assert abs(loss - ol) / abs(ol) <= tol
-        for k in og:
-            assert _rel(grads[k], og[k]) <= tol, (strategy, k, _rel(grads[k], og[k]))
+        _parity(loss, grads, ol, og, tol, strategy)
 
 
 @pytest.mark.parametrize("strategy,kw", [("budget", {"budget": 3 * 64 * 256 * 4}), ("recursive", {"k": 2}),
@@ -226,27 +274,6 @@ def test_other_plans_bitwise(slm, strategy, kw):
     assert float(loss.item()) == ref_loss
     for k in ref:
         assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), k
-
-
-def test_cta_pair_and_tile_options_bitwise(slm):
-    """The fused lowering's GEMM variants: CTA pairs keep the accumulation order (bitwise equal
-    to the default); other N tiles / split-K factors re-associate the fp32 partial sums (close
-    to the default); every variant keeps checkpointed == non-checkpointed bit for bit."""
-    n, B, d = 10, 256, 512
-    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=21)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
-    for opt in (dict(cta_pair=1), dict(fused_bn=256, sk_fwd=4, sk_dx=4), dict(cta_pair=1, fused_bn=256)):
-        l0, g0, _ = _run(slm, n, B, d, "bf16", "none", inp, **opt)
-        l1, g1, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, **opt)
-        assert l0 == l1, opt
-        for k in ref:
-            assert np.array_equal(g0[k], g1[k]), (opt, k)
-            if opt == dict(cta_pair=1):
-                assert np.array_equal(g0[k], ref[k]), (opt, k)
-            else:
-                assert _rel(g0[k], ref[k]) <= 2e-2, (opt, k, _rel(g0[k], ref[k]))   # bf16 dW rounding
-        if opt == dict(cta_pair=1):
-            assert l0 == ref_loss
 
 
 def test_sgd_training_reduces_loss(slm):
@@ -268,37 +295,8 @@ def test_sgd_training_reduces_loss(slm):
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
 
 
-@pytest.mark.parametrize("n,B,d", [(9, 64, 256), (7, 128, 1024), (6, 256, 2048), (70, 64, 512)])
-def test_persistent_forward_option(slm, n, B, d):
-    """Option persist=1 (fwd_persist.cuh: runs of forward / mirror Blocks as one persistent
-    kernel with split-K S = 4 / 16 / 8 / 8 at these widths; n = 70 spans two launches of <= 64
-    Blocks): within the bf16 tolerance of the fp64 oracle at the small size (ReLU-margin inputs,
-    reading A20) and of the default two-kernel lowering at all sizes, and checkpointed ==
-    non-checkpointed bit for bit for every strategy (mirrors re-run the same kernel)."""
-    small = n * B * d <= 200_000
-    inp = margin_inputs(n, B, d, "bf16") if small else synth.chain_inputs(n, B, d, dtype="bf16", seed=5)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, persist=1)
-    if small:
-        ol, og, _ = _oracle(n, B, d, "bf16", inp)
-        assert abs(ref_loss - ol) <= 2e-2 * abs(ol)
-        for k in og:
-            assert _rel(ref[k], og[k]) <= 2e-2, (k, _rel(ref[k], og[k]))
-    dl, dg, _ = _run(slm, n, B, d, "bf16", "none", inp, persist=0)
-    assert abs(ref_loss - dl) <= 2e-2 * abs(dl)
-    for k in dg:
-        assert _rel(ref[k], dg[k]) <= 2e-2, (k, _rel(ref[k], dg[k]))
-    for strategy in ("sqrt", "search", "recursive"):
-        l1, g1, _ = _run(slm, n, B, d, "bf16", strategy, inp, persist=1)
-        assert l1 == ref_loss, strategy
-        for k in ref:
-            assert np.array_equal(g1[k], ref[k]), (strategy, k)
-
-
 @pytest.mark.parametrize("n,B,d,opt", [(40, 64, 256, {}), (100, 128, 512, {}), (40, 256, 512, {}),
-                                       (40, 256, 512, dict(tile_mir=256)), (40, 256, 512, dict(tile_dx=256)),
-                                       (40, 256, 512, dict(tile_mir=256, tile_dx=256)),
-                                       (40, 256, 512, dict(cta_pair=1)), (40, 256, 512, dict(dw_lag=5)),
-                                       (40, 256, 512, dict(bn_vec=1)), (40, 128, 512, dict(bn_vec=1, sk_fwd=4))])
+                                       (33, 128, 384, {}), (40, 256, 2048, {}), (40, 256, 512, dict(pdl=0))])
 def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     """Option overlap (reading A24): with a SLM_ALLOC_MIRROR_PARITY plan each segment's recompute
     runs on its own stream, concurrent with the backward of the next segment.  The step must
@@ -306,7 +304,7 @@ def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     for bit, repeatedly (a race on a recycled pool slot would show up as a mismatch); plans
     without the flag fall back to the sequential schedule with the same bits."""
     inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=7)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, **{k: v for k, v in opt.items() if k != "tile_mir"})
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, **opt)
     par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
     p, g, x0, y = _dev(inp, "bf16")
     model = slm.ChainModel(p, g, dtype="bf16", batch=B, **opt)
@@ -324,84 +322,6 @@ def test_overlapped_recompute_bitwise(slm, n, B, d, opt):
     torch.cuda.synchronize()
     assert model.get_option("last_overlap") == 0
     assert float(loss.item()) == ref_loss
-
-
-def test_dw_lag_ring_bitwise(slm):
-    """Option dw_lag (ring of NA bf16 dW operands): only the schedule changes, so any depth gives
-    the default step's bits, with and without the overlapped recompute."""
-    n, B, d = 24, 64, 256
-    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=9)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
-    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
-    for lag in (3, 5, 8):
-        p, g, x0, y = _dev(inp, "bf16")
-        model = slm.ChainModel(p, g, dtype="bf16", batch=B, dw_lag=lag)
-        for af in (3, par):
-            loss = model.step(slm.Plan(slm.Graph.chain(n, B, d), "sqrt", alloc_flags=af), x0, y)
-            torch.cuda.synchronize()
-            assert float(loss.item()) == ref_loss, (lag, af)
-            for k in ref:
-                assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (lag, af, k)
-
-
-@pytest.mark.parametrize("sk,n,d", [(2, 4, 256), (2, 10, 512), (2, 4, 2048)])
-def test_cluster_block_option(slm, sk, n, d):
-    """Option blk_cluster = SK (blk_cluster.cuh: the forward Block as one kernel, split-K SK
-    partials reduced over DSMEM inside a 2 SK-CTA cluster, batch statistics exchanged between
-    the batch halves): within the bf16 tolerance of the oracle (small sizes, ReLU-margin inputs)
-    and of the default lowering (n = 10, like the tile options), and checkpointed ==
-    non-checkpointed bit for bit for every strategy and with the overlapped recompute (the K1
-    before a mirror run reproduces the kernel's statistics)."""
-    B = 256
-    small = n * B * d <= 300_000
-    inp = margin_inputs(n, B, d, "bf16") if small else synth.chain_inputs(n, B, d, dtype="bf16", seed=21)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp, blk_cluster=sk)
-    if small:
-        ol, og, _ = _oracle(n, B, d, "bf16", inp)
-        assert abs(ref_loss - ol) <= 2e-2 * abs(ol)
-        for k in og:
-            assert _rel(ref[k], og[k]) <= 2e-2, (k, _rel(ref[k], og[k]))
-    elif n <= 10:
-        dl, dg, _ = _run(slm, n, B, d, "bf16", "none", inp)
-        assert abs(ref_loss - dl) <= 2e-2 * abs(dl)
-        for k in dg:
-            assert _rel(ref[k], dg[k]) <= 2e-2, (k, _rel(ref[k], dg[k]))
-    par = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_MIRROR_PARITY
-    for strategy, af in (("sqrt", 3), ("search", 3), ("recursive", 3), ("sqrt", par)):
-        p, g, x0, y = _dev(inp, "bf16")
-        model = slm.ChainModel(p, g, dtype="bf16", batch=B, blk_cluster=sk)
-        for _ in range(2):
-            loss = model.step(slm.Plan(slm.Graph.chain(n, B, d), strategy, alloc_flags=af), x0, y)
-            torch.cuda.synchronize()
-            assert float(loss.item()) == ref_loss, (strategy, af)
-            for k in ref:
-                assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (strategy, af, k)
-
-
-def test_bn_feat_option_same_bits(slm):
-    """Option bn_feat = 8 (256-thread BN CTAs of 8 features instead of 512-thread CTAs of 16):
-    the per-feature reductions keep their order (32 row groups), so the step's bits equal the
-    default's, checkpointed or not."""
-    n, B, d = 12, 256, 512
-    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=13)
-    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
-    for strategy in ("none", "sqrt"):
-        loss, g, _ = _run(slm, n, B, d, "bf16", strategy, inp, bn_feat=8)
-        assert loss == ref_loss, strategy
-        for k in ref:
-            assert np.array_equal(g[k], ref[k]), (strategy, k)
-
-
-@pytest.mark.parametrize("n,B,d", [(4, 128, 256), (3, 256, 256)])
-def test_bn_vec_option_vs_oracle(slm, n, B, d):
-    """Option bn_vec (bn_act_v4: float4 loads, shuffle-tree statistics in another fixed order):
-    within the bf16 tolerance of the fp64 oracle (ReLU-margin inputs)."""
-    inp = margin_inputs(n, B, d, "bf16")
-    loss, grads, _ = _run(slm, n, B, d, "bf16", "sqrt", inp, bn_vec=1)
-    ol, og, _ = _oracle(n, B, d, "bf16", inp)
-    assert abs(loss - ol) <= 2e-2 * abs(ol)
-    for k in og:
-        assert _rel(grads[k], og[k]) <= 2e-2, (k, _rel(grads[k], og[k]))
 
 
 @pytest.mark.parametrize("strategy,kw", [("recursive", dict(k=1)), ("recursive", dict(k=2)), ("budget", dict(budget=0)),
