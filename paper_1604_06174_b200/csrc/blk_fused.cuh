@@ -3,7 +3,7 @@
 // cluster, and the batch-norm work fused into the epilogue.
 //
 //   forward / mirror Block_l:
-//     z = W_l a_l^T (swap-AB: M = 128 output features per CTA, N = B = the whole batch, K split
+//     z = W_l a_l^T (swap-AB: M = 64 output features per CTA, N = B = the whole batch, K split
 //     over the S CTAs of a cluster),  x_{l+1} = x_l + (z + b_l),  then the batch statistics of
 //     x_{l+1} and a_{l+1} = ReLU(BN_{l+1}(x_{l+1})) (bf16) for the next Block.
 //   gradient Block_l (a8): da = g W_l (dX, A = W read MN-major), then the BN backward
@@ -11,46 +11,43 @@
 //     dx_l = g + gamma rstd (du - dbeta/B - xhat dgamma/B), db_{l-1} = sum_b dx_l, plus the bf16
 //     copies of dx_l (next dX / dW operand) and a_l (dW operand).
 //
-// Why this shape (profiles/r2_microbench.md, measured on B200): tcgen05.mma kind::f16 reaches
-// the full 4096 MAC/clk/SM only at N = 256 (N = 128 runs at 72 %), so a CTA keeps the whole batch
-// as N; with M = 128 per CTA a layer has d/128 output tiles (16 at d = 2048), so K is split over
-// S = 4 CTAs (64 SMs, K slice 512) to bound the per-layer MMA time (2.2 us).  The S fp32
-// partials of a tile are reduce-scattered through L2 (L2 -> SM moves ~20 TB/s; distributed shared
-// memory only ~10-20 GB/s per SM): CTA k of the cluster TMA-stores the three quarters of its
-// accumulator owned by its peers (feature slices of FS = 128/S features x B rows), a cluster
-// barrier orders the writes, and each CTA TMA-loads the three slices it owns and adds the S
-// partials in the fixed order s = 0..S-1.  Owning all B rows of its features, the CTA computes
-// the per-feature batch statistics locally (two-pass mean / centred variance, fixed order), so
-// no separate BN kernel and no extra grid-wide dependency remain: one kernel boundary per Block
-// (launched with programmatic dependent launch, the next Block's weights are requested while
-// this one finishes).
+// Why this shape (measured on B200, profiles/r2_microbench.md):
+//  * the whole batch is the MMA's N (the per-feature batch statistics stay inside one CTA);
+//  * the layer's K is split over a cluster of S = 4 CTAs and the S fp32 partials are
+//    reduce-scattered through L2 (TMA stores / loads; distributed shared memory moves only
+//    ~10-20 GB/s per SM);
+//  * an SM stores only ~28 B/clk to L2 (loads ~100 B/clk), so the epilogue is bound by its
+//    writes: the peers' partial slices plus x_{l+1} and a_{l+1}.  M = 64 features per CTA (128
+//    CTAs at d = 2048) halves every SM's writes against M = 128 (64 CTAs) at the same per-layer
+//    MMA time: tcgen05 M = 64 runs at half the M = 128 rate on half the rows.
+// The M = 64 accumulator holds row r in TMEM lane 32 (r / 16) + r % 16 (measured,
+// scripts/mb_layout.cu): warp quarter q owns rows 16q..16q+15 in its lanes 0..15.
 //
 // Determinism: every sum has a fixed order (MMA K order, slice order s, the
-// per-thread row loop, then the S row groups in order), so mirrors (same kernel, same launch
+// per-thread row loop, then the row groups in order), so mirrors (same kernel, same launch
 // configuration) reproduce the forward's bits; bn_k1_kernel (the operand of the first Block of a
-// run) uses the identical statistics code on the identical slice layout.
+// run) uses the identical statistics code and thread mapping.
 #pragma once
 #include "tc_gemm.cuh"
 
 namespace slmk {
 
 constexpr int kBlkThreads = 256;   // 8 warps: TMA producer / MMA issuer / TMEM owner roles, then all 8 in the epilogue
-
-template <int B, int S, bool BWD>
+template <int B, int S, bool BWD, int BM_ = 64>
 struct BlkCfg {
-  static constexpr int BM = 128, BK = 64;
-  static constexpr int FS = 128 / S;          // features owned by a CTA after the reduce-scatter
-  static constexpr int CGR = FS / 32;         // 32-float (128-byte) column groups of a slice
+  static constexpr int BM = BM_, BK = 64;     // BM = output features per CTA (the MMA's M: 64 or 128)
+  static constexpr int FS = BM / S;           // features owned by a CTA after the reduce-scatter
+  static constexpr int CGR = FS / 16;         // 16-float (64-byte) column groups of a slice
   static constexpr int RG = kBlkThreads / FS; // row groups of the epilogue (threads per feature)
   static constexpr int R = B / RG;            // rows per epilogue thread (values kept in registers)
-  static constexpr int A_BYTES = BM * BK * 2; // one W tile (128 x 64 bf16)
+  static constexpr int A_BYTES = BM * BK * 2; // one W tile (BM x 64 bf16)
   static constexpr int B_BYTES = B * BK * 2;  // one operand tile (B x 64 bf16)
-  static constexpr int SLICE = B * FS * 4;    // one fp32 slice [CGR][B][32] (128-byte swizzled rows)
+  static constexpr int SLICE = B * FS * 4;    // one fp32 slice [CGR][B][16]
   static constexpr int AUX = SLICE;           // x_l, staged by TMA during the main loop
   static constexpr int LIMIT = 227 * 1024;
   static constexpr int STATIC = RG * FS * 4 + 64;
   static constexpr int NB = 3;                // operand ring (after griddepcontrol.wait, from L2)
-  // W ring: as many 16 KiB tiles as fit (up to 8 = a 512-wide K slice): all of them are requested
+  // W ring: as many tiles as fit (up to 8 = a 512-wide K slice): all of them are requested
   // before griddepcontrol.wait, so the weight stream from HBM overlaps the predecessor
   static constexpr int NA_FIT = (LIMIT - 1024 - AUX - 512 - STATIC - NB * B_BYTES) / A_BYTES;
   static constexpr int NA = NA_FIT > 8 ? 8 : NA_FIT;
@@ -59,18 +56,17 @@ struct BlkCfg {
   static constexpr int SMEM = 1024 + RING + AUX + 512;
   static constexpr int TMEM_COLS = B;
   static_assert(S == 2 || S == 4, "cluster of 2 or 4 CTAs");
+  static_assert(BM == 64 || BM == 128, "M tile");
   static_assert(B == 64 || B == 128 || B == 256, "batch tile");
-  static_assert(SLICE <= 32 * 1024 && R >= 1 && R <= 32, "slice / registers");
+  static_assert(FS % 16 == 0 && R >= 1 && R <= 32, "slice / registers");
   static_assert(NA >= 2, "pipeline");
   static_assert(SMEM + STATIC <= LIMIT, "shared memory");
 };
 
-// element (column group c, row b, column f32 in 0..31) of a 128-byte-swizzled fp32 slice: the
-// layout TMA reads / writes with CU_TENSOR_MAP_SWIZZLE_128B for a {32, B} box (16-byte chunk index
-// XOR row % 8), so a warp accessing one row (32 consecutive features) is conflict-free
-__device__ __forceinline__ int sw_off(int B_, int c, int b, int f32) {
-  return (c * B_ + b) * 32 + ((((f32 >> 2) ^ (b & 7))) << 2) + (f32 & 3);
-}
+// element (column group c, row b, column f16 in 0..15) of an fp32 slice [CGR][B][16]: the dense
+// layout of a {16, rows} TMA box (64-byte rows); a warp reading 2 rows x 16 features (FS = 16)
+// touches 128 consecutive bytes
+__device__ __forceinline__ int sl_off(int B_, int c, int b, int f16) { return (c * B_ + b) * 16 + f16; }
 
 // sum of one value per (row group rg, feature fl) over the RG row groups, in the order 0..RG-1
 template <int RG, int FS>
@@ -88,10 +84,11 @@ __device__ __forceinline__ float rg_sum(float v, float (*red)[FS], int rg, int f
 // two-pass mean / centred variance, per-thread serial then the row groups in order.  The forward
 // epilogue, the backward epilogue and bn_k1_kernel share this exact code and mapping (thread t:
 // feature t % FS, rows t / FS + RG j), so the statistics of a given x are bit-identical.
-template <int B, int S>
-__device__ __forceinline__ void slice_stats(const float (&v)[BlkCfg<B, S, false>::R],
-                                            float (*red)[128 / S], int fl, int rg, float& mu, float& rstd) {
-  using C = BlkCfg<B, S, false>;
+template <int B, int S, int BM>
+__device__ __forceinline__ void slice_stats(const float (&v)[BlkCfg<B, S, false, BM>::R],
+                                            float (*red)[BlkCfg<B, S, false, BM>::FS], int fl, int rg, float& mu,
+                                            float& rstd) {
+  using C = BlkCfg<B, S, false, BM>;
   constexpr float invB = 1.0f / B;   // exact: B is a power of two
   float s = 0.f;
 #pragma unroll
@@ -108,14 +105,13 @@ __device__ __forceinline__ void slice_stats(const float (&v)[BlkCfg<B, S, false>
 }
 
 // a = bf16(ReLU(gamma xhat + beta)) of the slice's rows (next Block's operand)
-template <int B, int S>
-__device__ __forceinline__ void slice_act(const float (&v)[BlkCfg<B, S, false>::R], float (*red)[128 / S], int d,
-                                          int f, int rg, int fl, const float* __restrict__ gamma,
-                                          const float* __restrict__ beta, __nv_bfloat16* __restrict__ a) {
-  using C = BlkCfg<B, S, false>;
+template <int B, int S, int BM>
+__device__ __forceinline__ void slice_act(const float (&v)[BlkCfg<B, S, false, BM>::R],
+                                          float (*red)[BlkCfg<B, S, false, BM>::FS], int d, int f, int rg, int fl,
+                                          float g, float bt, __nv_bfloat16* __restrict__ a) {
+  using C = BlkCfg<B, S, false, BM>;
   float mu, rstd;
-  slice_stats<B, S>(v, red, fl, rg, mu, rstd);
-  const float g = gamma[f], bt = beta[f];
+  slice_stats<B, S, BM>(v, red, fl, rg, mu, rstd);
 #pragma unroll
   for (int j = 0; j < C::R; ++j)
     a[(size_t)(rg + C::RG * j) * d + f] = __float2bfloat16_rn(fmaxf(bn_u(bn_xhat(v[j], mu, rstd), g, bt), 0.f));
@@ -138,21 +134,23 @@ struct BlkArgs {
   int dbg;
 };
 
-// grid = (d/128) * S CTAs, clusters of S along x (CTA m*S + k = K slice k of output tile m),
+// grid = (d/BM) * S CTAs, clusters of S along x (CTA m*S + k = K slice k of output tile m),
 // 256 threads: warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warp 2 owns the TMEM
 // allocation; then all eight warps run the epilogue.
-//   tmA: W, K-major {64, 128} box (fwd) or MN-major {64, 64} boxes (bwd)
-//   tmB: the bf16 operand [B][d] (a_l fwd, bf16 dx_{l+1} bwd), {64, B} box
-//   tmP: the partial buffer [d/128][S owners][S sources][CGR][B] rows of 32 fp32, {32, B} box,
-//        128-byte swizzle (TMA stores and loads)
-//   tmX: fp32 [rows][d] source of x_l, {32, B} box, 128-byte swizzle
-template <int B, int S, bool BWD>
+//   tmA: W, K-major {64, BM} box or MN-major {64, 64} boxes
+//   tmB: the bf16 operand [B][d] (a_l fwd, bf16 dx_{l+1} bwd), {64, B} box, 128-byte swizzle
+//   tmP / tmPs: the partial buffer [d/64][S owners][S sources][CGR][B] rows of 16 fp32, {16, B} box
+//        (the owner's loads) / {16, 32} box (a warp's chunk stores)
+//   tmX: fp32 [rows][d] source of x_l, {16, B} box
+template <int B, int S, bool BWD, int BM_>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     blk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmX, const BlkArgs args) {
-  using C = BlkCfg<B, S, BWD>;
-  constexpr int FS = C::FS, CGR = C::CGR, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB;
-  ts_mark(0, args.dbg);
+               const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmPs,
+               const __grid_constant__ CUtensorMap tmX, const BlkArgs args) {
+  using C = BlkCfg<B, S, BWD, BM_>;
+  constexpr int FS = C::FS, CGR = C::CGR, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB, BM = C::BM;
+  unsigned long long* const tsp = ts_buffer(args.dbg);
+  ts_mark(tsp, 0, args.dbg);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned by pointer arithmetic on the __shared__ array (not through an integer), so
   // the compiler keeps the shared address space (LDS/STS) for the epilogue's accesses
@@ -166,24 +164,33 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   uint64_t* emptyB = fullB + NB;
   uint64_t* accum = emptyB + NB;
   uint64_t* auxb = accum + 1;
-  uint64_t* recvb = auxb + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recvb + 1);
+  uint64_t* recvb = auxb + 1;    // remote arrivals: the peers' chunks of this owner's slice are in L2
+  uint64_t* recvb2 = recvb + 1;  // tx bytes of the incoming slices
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recvb2 + 1);
   __shared__ float red[RG][FS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = args.d;
   const uint32_t k = cluster_ctarank();
   const int m = (int)blockIdx.x / S;
-  const int m0 = m * 128;
+  const int m0 = m * BM;
   const int nk = d / 64 / S;
   const int kbase = (int)k * nk * 64;
   const int f0 = m0 + (int)k * FS;   // first feature this CTA owns after the reduce-scatter
+  // this thread's feature in the epilogue and its parameters, loaded now (they are constant during
+  // the step) so their latency hides under the main loop
+  const int fl = threadIdx.x % FS, rg = threadIdx.x / FS, cc = fl >> 4, f16 = fl & 15;
+  const int f = f0 + fl;
+  const float p_bias = BWD ? 0.f : args.bias[f];
+  const float p_gam = args.gamma ? args.gamma[f] : 0.f;
+  const float p_bet = args.gamma ? args.beta[f] : 0.f;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmP);
+    prefetch_tmap(&tmPs);
     for (int s = 0; s < NA; ++s) {
       mbar_init(&fullA[s], 1);
       mbar_init(&emptyA[s], 1);
@@ -194,7 +201,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
     mbar_init(accum, 1);
     mbar_init(auxb, 1);
-    mbar_init(recvb, 1);
+    mbar_init(recvb, 2 * (S - 1) * CGR);   // one arrival per (peer warp, 16-row group) of this owner's slice
+    mbar_init(recvb2, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -203,20 +211,19 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();   // every CTA's barriers are initialised before a peer can arrive on them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  ts_mark(1, args.dbg);
 
   auto load_a = [&](int kb) {
     const int s = kb % NA;
     uint8_t* sa = ring + s * C::A_BYTES;
     const int k0 = kbase + kb * 64;
     mbar_expect_tx(&fullA[s], C::A_BYTES);
-    if (BWD) {   // W stored [f_out = K][f_in = M]: two 64 x 64 boxes
-      tma_load_2d(sa, &tmA, &fullA[s], m0, args.a_row0 + k0);
-      tma_load_2d(sa + 8192, &tmA, &fullA[s], m0 + 64, args.a_row0 + k0);
-    } else {     // W stored [f_out = M][f_in = K]: one 64 (K) x 128 (M) box
+    if (BWD) {   // W stored [f_out = K][f_in = M]: 64 (M) x 64 (K) boxes
+#pragma unroll
+      for (int mm = 0; mm < BM; mm += 64) tma_load_2d(sa + mm * 128, &tmA, &fullA[s], m0 + mm, args.a_row0 + k0);
+    } else {     // W stored [f_out = M][f_in = K]: a 64 (K) x BM (M) box
       tma_load_2d(sa, &tmA, &fullA[s], k0, args.a_row0 + m0);
     }
   };
@@ -232,12 +239,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int na0 = nk < NA ? nk : NA, nb0 = nk < NB ? nk : NB;
     for (int kb = 0; kb < na0; ++kb) load_a(kb);
     pdl_wait();
-    if (args.dbg & 8) ts_dep(args.dbg);
+    ts_mark(tsp, 1, args.dbg);
+    if (args.dbg & 8) ts_dep(tsp, args.dbg);
     for (int kb = 0; kb < nb0; ++kb) load_b(kb);
     // the epilogue's x_l slice lands in its own buffer while the main loop runs
     mbar_expect_tx(auxb, C::AUX);
 #pragma unroll
-    for (int c = 0; c < CGR; ++c) tma_load_2d(xs + c * B * 32, &tmX, auxb, f0 + 32 * c, args.x_row0);
+    for (int c = 0; c < CGR; ++c) tma_load_2d(xs + c * B * 16, &tmX, auxb, f0 + 16 * c, args.x_row0);
     // refill each ring slot as soon as the MMAs reading it retire
     for (int kb = 0; kb < nk; ++kb) {
       if (kb + NB < nk) {
@@ -251,7 +259,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ===== MMA issuer
-    constexpr uint32_t idesc = make_idesc(128, B, BWD, false);
+    constexpr uint32_t idesc = make_idesc(BM, B, BWD, false);
     for (int kb = 0; kb < nk; ++kb) {
       mbar_wait(&fullA[kb % NA], (kb / NA) & 1);
       mbar_wait(&fullB[kb % NB], (kb / NB) & 1);
@@ -271,61 +279,79 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   }
   __syncwarp();
 
-  // ===== epilogue 1: accumulator -> the S feature slices (smem, 128-byte swizzled), then the
-  // S-1 slices owned by the peers -> L2 by TMA bulk stores
+  // ===== epilogue 1: accumulator -> the S feature slices (smem).  Warp (q, h) reads TMEM lane
+  // quarter q (rows 16q..16q+15 in lanes 0..15) for batch columns h*B/2..: it stages its 16
+  // features x 32 columns chunk by chunk and, when they belong to a peer, TMA-stores each chunk at
+  // once (stores overlap the TMEM reads), waits for its stores to complete and signals the owner
+  // through a remote mbarrier arrive; an owner loads its incoming slices once all its peers' warps
+  // have arrived (no cluster-wide barrier)
   mbar_wait(accum, 0);
   tc_fence_after();
-  pdl_launch();   // the next kernel may now start its prologue and weight prefetch on free SMs
-  ts_mark(2, args.dbg);
+  ts_mark(tsp, 2, args.dbg);
   {
-    const int q = warp & 3, h = warp >> 2;   // TMEM lane quarter (features 32q..), column half
-    const int ko = q / CGR, cg = q % CGR;    // owner slice and its column group
-    float* slotp = reinterpret_cast<float*>(ring + ko * C::SLICE);
+    // 16-row groups of the tile held by this warp's TMEM lane quarter: BM = 128 -> groups 2q, 2q+1
+    // (lanes 0..15, 16..31); BM = 64 -> group q (lanes 0..15, measured layout)
+    constexpr int GPW = BM / 64;
+    const int q = warp & 3, h = warp >> 2;
+    const int grp = GPW * q + (GPW == 2 ? (lane >> 4) : 0);   // this lane's group (BM = 64: lanes < 16)
+    const bool valid = GPW == 2 || lane < 16;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
     for (int c0 = h * (B / 2); c0 < (h + 1) * (B / 2); c0 += 32) {
       float acc[32];
       tmem_ld32(trow + c0, acc);
+      if (valid) {
+        const int ko = 16 * grp / FS, cg = (16 * grp % FS) / 16;
+        float* dst = reinterpret_cast<float*>(ring + ko * C::SLICE) + (cg * B + c0) * 16 + (lane & 15);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) slotp[sw_off(B, cg, c0 + j, lane)] = acc[j];
+        for (int j = 0; j < 32; ++j) dst[j * 16] = acc[j];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged smem -> TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {   // a peer's rows: store each 32 x 16 chunk now (stores overlap the TMEM reads)
+#pragma unroll
+        for (int gg = 0; gg < GPW; ++gg) {
+          const int g2 = GPW * q + gg, ko = 16 * g2 / FS, cg = (16 * g2 % FS) / 16;
+          if (ko == (int)k) continue;
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tmPs)),
+                       "r"(smem_u32(reinterpret_cast<float*>(ring + ko * C::SLICE) + (cg * B + c0) * 16)), "r"(0),
+                       "r"((((m * S + ko) * S + (int)k) * CGR + cg) * B + c0)
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // this warp's chunks are in L2
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+#pragma unroll
+      for (int gg = 0; gg < GPW; ++gg) {
+        const int ko = 16 * (GPW * q + gg) / FS;
+        if (ko != (int)k)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           cluster_map(smem_u32(recvb), (uint32_t)ko))
+                       : "memory");
+      }
     }
   }
   tc_fence_before();
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // smem writes -> TMA (async proxy)
   __syncthreads();
+  ts_mark(tsp, 3, args.dbg);
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
   if (threadIdx.x == 0) {
-    for (int s = 1; s < S; ++s) {
-      const int ko = ((int)k + s) % S;   // peer owner
-#pragma unroll
-      for (int c = 0; c < CGR; ++c)
-        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                         reinterpret_cast<uint64_t>(&tmP)),
-                     "r"(smem_u32(ring + ko * C::SLICE + c * B * 128)), "r"(0),
-                     "r"((((m * S + ko) * S + (int)k) * CGR + c) * B)
-                     : "memory");
-    }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // the peers' slices are in L2
+    mbar_wait(recvb, 0);   // every peer warp holding part of this owner's slice has stored it
     asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-  ts_mark(3, args.dbg);
-  cluster_sync();   // every CTA of the cluster has published its peers' slices
-  ts_mark(4, args.dbg);
-  if (threadIdx.x == 0) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    mbar_expect_tx(recvb, (S - 1) * C::SLICE);
+    mbar_expect_tx(recvb2, (S - 1) * C::SLICE);
     for (int s = 0; s < S; ++s) {
       if (s == (int)k) continue;
 #pragma unroll
       for (int c = 0; c < CGR; ++c)
-        tma_load_2d(ring + s * C::SLICE + c * B * 128, &tmP, recvb, 0, (((m * S + (int)k) * S + s) * CGR + c) * B);
+        tma_load_2d(ring + s * C::SLICE + c * B * 64, &tmP, recvb2, 0, (((m * S + (int)k) * S + s) * CGR + c) * B);
     }
   }
 
   // ===== epilogue 2: sum the S partials (slot s = K slice s, fixed order) and the fused batch norm
-  const int fl = threadIdx.x % FS, rg = threadIdx.x / FS, cc = fl >> 5, f32 = fl & 31;
-  const int f = f0 + fl;
   const float* ringf = reinterpret_cast<const float*>(ring);
   float gv[BWD ? R : 1];
   if constexpr (BWD) {   // g = dx_{l+1}: coalesced loads issued before waiting for the slices
@@ -333,12 +359,16 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     for (int j = 0; j < R; ++j) gv[j] = args.g[(size_t)(rg + RG * j) * d + f];
   }
   mbar_wait(auxb, 0);
-  mbar_wait(recvb, 0);
-  ts_mark(5, args.dbg);
+  mbar_wait(recvb2, 0);
+  // the next kernel may now start its prologue and weight prefetch: early enough to hide them under
+  // the batch-norm work, late enough that its waiting CTAs do not hold SMs the concurrent streams
+  // (recompute, dW) need during the backward phase
+  pdl_launch();
+  ts_mark(tsp, 4, args.dbg);
   float xv[R], zv[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const int off = sw_off(B, cc, rg + RG * j, f32);
+    const int off = sl_off(B, cc, rg + RG * j, f16);
     float z = ringf[off];
 #pragma unroll
     for (int s = 1; s < S; ++s) z = __fadd_rn(z, ringf[s * (C::SLICE / 4) + off]);
@@ -346,18 +376,17 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     xv[j] = xs[off];
   }
   if constexpr (!BWD) {
-    const float bf = args.bias[f];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      xv[j] = __fadd_rn(xv[j], __fadd_rn(zv[j], bf));
+      xv[j] = __fadd_rn(xv[j], __fadd_rn(zv[j], p_bias));
       args.out[(size_t)(rg + RG * j) * d + f] = xv[j];
     }
-    ts_mark(6, args.dbg);
-    if (args.gamma != nullptr) slice_act<B, S>(xv, red, d, f, rg, fl, args.gamma, args.beta, args.a_out);
+    ts_mark(tsp, 5, args.dbg);
+    if (args.gamma != nullptr) slice_act<B, S, BM>(xv, red, d, f, rg, fl, p_gam, p_bet, args.a_out);
   } else {
     float mu, rstd;
-    slice_stats<B, S>(xv, red, fl, rg, mu, rstd);
-    const float ga = args.gamma[f], bt = args.beta[f];
+    slice_stats<B, S, BM>(xv, red, fl, rg, mu, rstd);
+    const float ga = p_gam, bt = p_bet;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -368,7 +397,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       s1 = __fadd_rn(s1, zv[j]);
       s2 = __fmaf_rn(zv[j], xh, s2);
     }
-    ts_mark(6, args.dbg);
+    ts_mark(tsp, 5, args.dbg);
     const float S1 = rg_sum<RG, FS>(s1, red, rg, fl);
     const float S2 = rg_sum<RG, FS>(s2, red, rg, fl);
     constexpr float invB = 1.0f / B;
@@ -390,27 +419,28 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       if (args.db_prev) args.db_prev[f] = S3;
     }
   }
-  ts_mark(7, args.dbg);
+  ts_mark(tsp, 7, args.dbg);
 }
 
 // K1: a = ReLU(BN(x)) for the first Block of a forward / mirror run (x_0, or a kept x_{s_j}),
 // with the Block epilogue's exact mapping and statistics code: grid = d / FS CTAs of 256 threads,
-// x read coalesced into registers (a warp covers 32 consecutive features of one row).
-template <int B, int S>
+// x read coalesced into registers.
+template <int B, int S, int BM>
 __global__ void __launch_bounds__(kBlkThreads) bn_k1_kernel(const float* __restrict__ x,
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ beta, int d,
                                                             __nv_bfloat16* __restrict__ a) {
-  using C = BlkCfg<B, S, false>;
+  using C = BlkCfg<B, S, false, BM>;
   __shared__ float red[C::RG][C::FS];
   pdl_wait();
   const int fl = threadIdx.x % C::FS, rg = threadIdx.x / C::FS;
   const int f = blockIdx.x * C::FS + fl;
+  const float g = gamma[f], bt = beta[f];
   float v[C::R];
 #pragma unroll
   for (int j = 0; j < C::R; ++j) v[j] = x[(size_t)(rg + C::RG * j) * d + f];
   pdl_launch();
-  slice_act<B, S>(v, red, d, f, rg, fl, gamma, beta, a);
+  slice_act<B, S, BM>(v, red, d, f, rg, fl, g, bt, a);
 }
 
 }  // namespace slmk

@@ -149,9 +149,9 @@ slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint
   return SLM_OK;
 }
 
-// fp32 2-D tensor [rows][inner], box {32, box_rows}, 128-byte swizzle: the Block kernel's x / g
-// slices and its partial-exchange buffer (blk_fused.cuh)
-slm_status make_map_f32_sw(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+// fp32 2-D tensor [rows][inner], box {16, box_rows}, no swizzle: the Block kernel's x slices and its
+// partial-exchange buffer (blk_fused.cuh)
+slm_status make_map_f32_16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -159,58 +159,74 @@ slm_status make_map_f32_sw(CUtensorMap* map, const void* base, uint64_t inner, u
   }
   cuuint64_t dims[2] = {inner, rows};
   cuuint64_t strides[1] = {inner * 4};
-  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t box[2] = {16, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (f32, swizzled) failed: " + std::to_string((int)r));
+    set_error("cuTensorMapEncodeTiled (f32, 16-wide) failed: " + std::to_string((int)r));
     return SLM_E_CUDA;
   }
   return SLM_OK;
 }
+// rows of 16 floats in the Block kernel's partial buffer: [d/BM][S][S][CGR][B]
+uint64_t blk_prows(int B, int d, int S, int BM) { return (uint64_t)(d / BM) * S * S * (BM / S / 16) * B; }
 
-// cluster split S of the fused Block (blk_fused.cuh) for batch B and width d, 0 = not supported:
-// the largest S in {4, 2} with a K slice of whole 64-column blocks and a slice that fits
-// (S >= B / 64); d % 128 == 0 makes S = 2 always tile, so S = 1 is never needed
-int blk_split(int B, int d) {
-  if (!(B == 64 || B == 128 || B == 256) || d % 128) return 0;
-  for (int s : {4, 2})
-    if ((d / s) % 64 == 0 && s * 64 >= B) return s;
-  return 0;
+// Shape of the fused Block (blk_fused.cuh): BM output features per CTA (the MMA's M) and the
+// cluster split S of K; option block_cfg: 0 = default, 1 = (64, 4), 2 = (128, 4), 3 = (64, 2).
+// Default: (128, 4) at B = 256 (64 CTAs at d = 2048), (64, 4) below; (64, 2) when d % 256 != 0.
+// Measured at C2 (scripts/chain_timeline.py, profiles/r2_block_shapes.md): (128, 4) 29.9 ms/step,
+// (64, 2) 31.6, (64, 4) 35.1 — the 128-CTA Blocks run the forward pass faster (10.5 vs 11.4 us per
+// Block) but leave no room for the concurrent recompute and dW streams of the backward phase.
+// {0, 0} = not supported (basic lowering).
+struct BlkShape {
+  int BM, S;
+};
+BlkShape blk_shape(int B, int d, int cfg) {
+  if (!(B == 64 || B == 128 || B == 256) || d % 128) return {0, 0};
+  static const BlkShape tab[4] = {{128, 4}, {64, 4}, {128, 4}, {64, 2}};
+  BlkShape sh = tab[(cfg >= 0 && cfg <= 3) ? cfg : 0];
+  if (sh.BM == 128 && B != 256) sh.BM = 64;
+  if ((d / sh.S) % 64 || d % sh.BM) sh = {64, 2};   // K slice of whole 64-column blocks
+  if (d % sh.BM || (d / sh.S) % 64) return {0, 0};
+  return sh;
 }
+int blk_split(int B, int d) { return blk_shape(B, d, 0).S; }
 
-template <int B_, int S_, bool BWD>
-slm_status launch_blk_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& x,
-                        const slmk::BlkArgs& args, cudaStream_t st, bool pdl) {
-  using C = slmk::BlkCfg<B_, S_, BWD>;
-  auto kern = slmk::blk_kernel<B_, S_, BWD>;
+template <int B_, int S_, bool BWD, int BM_>
+slm_status launch_blk_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& ps,
+                        const CUtensorMap& x, const slmk::BlkArgs& args, cudaStream_t st, bool pdl) {
+  using C = slmk::BlkCfg<B_, S_, BWD, BM_>;
+  auto kern = slmk::blk_kernel<B_, S_, BWD, BM_>;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  CK(launch_kc(kern, dim3(args.d / 128 * S_), dim3(slmk::kBlkThreads), C::SMEM, st, pdl, S_, a, b, p, x, args));
+  CK(launch_kc(kern, dim3(args.d / BM_ * S_), dim3(slmk::kBlkThreads), C::SMEM, st, pdl, S_, a, b, p, ps, x, args));
   return SLM_OK;
 }
-slm_status launch_blk(int B, int S, bool bwd, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p,
+slm_status launch_blk(int B, BlkShape sh, bool bwd, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap* p,
                       const CUtensorMap& x, const slmk::BlkArgs& args, cudaStream_t st, bool pdl) {
-#define SLM_BLK(B_, S_)                                                \
-  if (B == B_ && S == S_)                                              \
-    return bwd ? launch_blk_t<B_, S_, true>(a, b, p, x, args, st, pdl) \
-               : launch_blk_t<B_, S_, false>(a, b, p, x, args, st, pdl);
-  SLM_BLK(64, 2) SLM_BLK(64, 4) SLM_BLK(128, 2) SLM_BLK(128, 4) SLM_BLK(256, 4)
+#define SLM_BLK(B_, S_, BM_)                                                               \
+  if (B == B_ && sh.S == S_ && sh.BM == BM_)                                               \
+    return bwd ? launch_blk_t<B_, S_, true, BM_>(a, b, p[0], p[1], x, args, st, pdl)       \
+               : launch_blk_t<B_, S_, false, BM_>(a, b, p[0], p[1], x, args, st, pdl);
+  SLM_BLK(64, 2, 64) SLM_BLK(64, 4, 64) SLM_BLK(128, 2, 64) SLM_BLK(128, 4, 64) SLM_BLK(256, 2, 64)
+  SLM_BLK(256, 4, 64) SLM_BLK(256, 4, 128)
 #undef SLM_BLK
   set_error("unsupported fused Block configuration");
   return SLM_E_UNSUPPORTED;
 }
-cudaError_t launch_k1(int B, int S, const float* x, const float* gam, const float* bet, int d, __nv_bfloat16* a,
+cudaError_t launch_k1(int B, BlkShape sh, const float* x, const float* gam, const float* bet, int d, __nv_bfloat16* a,
                       cudaStream_t st, bool pdl) {
-#define SLM_K1(B_, S_)       \
-  if (B == B_ && S == S_) \
-    return launch_k(slmk::bn_k1_kernel<B_, S_>, dim3(d / (128 / S_)), dim3(slmk::kBlkThreads), 0, st, pdl, x, gam, bet, d, a);
-  SLM_K1(64, 2) SLM_K1(64, 4) SLM_K1(128, 2) SLM_K1(128, 4) SLM_K1(256, 4)
+#define SLM_K1(B_, S_, BM_)                                                                                      \
+  if (B == B_ && sh.S == S_ && sh.BM == BM_)                                                                    \
+    return launch_k(slmk::bn_k1_kernel<B_, S_, BM_>, dim3(d / (BM_ / S_)), dim3(slmk::kBlkThreads), 0, st, pdl, x, \
+                    gam, bet, d, a);
+  SLM_K1(64, 2, 64) SLM_K1(64, 4, 64) SLM_K1(128, 2, 64) SLM_K1(128, 4, 64) SLM_K1(256, 2, 64) SLM_K1(256, 4, 64)
+  SLM_K1(256, 4, 128)
 #undef SLM_K1
   return cudaErrorInvalidValue;
 }
@@ -291,6 +307,7 @@ struct slm_model {
   int fused = 1;          // fused lowering (one Block kernel per node, blk_fused.cuh)
   int dw_stream = 1;      // dW GEMMs on a second stream
   int bn_fwd = 64, bn_dx = 64, bn_dw = 256;   // N tiles of the basic lowering's GEMMs (bn_dw: also the fused dW)
+  int block_cfg = 0;      // fused Block shape (blk_shape: 0 default, 1..4 explicit (BM, S))
   int overlap = 1;        // segment recompute on its own stream, concurrent with the backward of
                           // the next segment, when the plan allows it (SLM_ALLOC_MIRROR_PARITY)
   int lstm_streams = 2;   // LSTM: layer wavefront over L+1 streams (2: + L mirror streams)
@@ -301,7 +318,7 @@ struct slm_model {
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;
-  CUtensorMap mW_K, mW_MN, mdW_st, mA_K, mA_MN, mAct[2], mAct3[2], mPf, mPf3, mG_K[kNG], mG_MN[kNG], mAb_MN[kNA];
+  CUtensorMap mW_K, mW_K64, mW_MN, mdW_st, mA_K, mA_MN, mAct[2], mAct3[2], mPf[2], mPf3[2], mG_K[kNG], mG_MN[kNG], mAb_MN[kNA];
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int64_t last_launches = 0;
   bool last_overlap = false;           // the last enqueued step ran its recompute on s3
@@ -312,7 +329,8 @@ struct slm_model {
   // profile_ts: device-clock (%globaltimer) start/end of every CTA of the first profile_ts Block /
   // GEMM launches of a step, in the caller's buffer ts_buf ([slot][1024][2] uint64, zeroed)
   int profile_ts = 0;
-  int profile_ts_dep = 0;   // 1: stamp the start after the dependency wait (ts_dep)
+  int profile_ts_dep = 0;   // 1: stamp the start after the dependency wait (ts_dep); 2: all 8 phases
+                            // of every CTA, [slot][1024][8] (scripts/chain_timeline.py PHASES=1)
   void* ts_buf = nullptr;
   std::vector<int> ts_kind;
   std::vector<int> ts_aux;    // per slot: the LSTM stream of the launch (slm_debug_ts_meta)
@@ -360,8 +378,8 @@ bool tc_ok(const slm_model& m) {
          B % m.bn_fwd == 0 && B % m.bn_dx == 0 && d % m.bn_dw == 0;
 }
 // the fused lowering (blk_fused.cuh): the whole batch per Block CTA (N = B <= 256), K split over a
-// cluster of blk_split() CTAs
-bool fused_ok(const slm_model& m) { return tc_ok(m) && m.fused && blk_split(m.d.batch, m.d.width) > 0; }
+// cluster of blk_shape() CTAs
+bool fused_ok(const slm_model& m) { return tc_ok(m) && m.fused && blk_shape(m.d.batch, m.d.width, m.block_cfg).S > 0; }
 
 struct WsLayout {
   size_t act[2], act3[2], stats, gq[kNG], ab[kNA], P, P3, da, rowloss, a, total;
@@ -371,7 +389,7 @@ WsLayout ws_layout(const slm_model& m) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   WsLayout L{};
   const bool fz = fused_ok(m);
-  const size_t S = fz ? (size_t)blk_split((int)B, (int)d) : 0;
+  const size_t S = fz ? (size_t)blk_shape((int)B, (int)d, m.block_cfg).S : 0;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -383,7 +401,7 @@ WsLayout ws_layout(const slm_model& m) {
   for (int i = 0; i < kNG; ++i) L.gq[i] = take(B * d * 2);
   for (int i = 0; i < kNA; ++i) L.ab[i] = take(fz ? B * d * 2 : 0);
   for (int i = 0; i < 2; ++i) L.act[i] = take(fz ? B * d * 2 : 0);
-  L.P = take(S * B * d * 4);              // partial exchange of the Block kernels ([d/128][S][S][.][B][32])
+  L.P = take(S * B * d * 4);              // partial exchange of the Block kernels ([d/64][S][S][.][B][16])
   L.da = take(fz ? 0 : B * d * 4);
   L.rowloss = take(B * 4);
   // the recompute stream's own operands and partial buffer (option overlap)
@@ -428,7 +446,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
 }
 
 slm_status bind_maps(slm_model& m, void* ws) {
-  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.bn_dw * 1009 + m.overlap * 5;
+  const int key = m.bn_fwd * 7 + m.bn_dx * 131 + m.fused + m.bn_dw * 1009 + m.overlap * 5 + m.block_cfg * 100003;
   if (m.maps_ws == ws && m.maps_key == key) return SLM_OK;
   const uint64_t B = m.d.batch, d = m.d.width, n = m.d.n_layers;
   WsLayout L = ws_layout(m);
@@ -438,16 +456,20 @@ slm_status bind_maps(slm_model& m, void* ws) {
   if ((st = make_map(&m.mW_K, m.d.W, d, n * d, 128)) != SLM_OK) return st;
   if ((st = make_map(&m.mW_MN, m.d.W, d, n * d, 64)) != SLM_OK) return st;
   if (fz) {
-    const int S = blk_split((int)B, (int)d);
-    const uint64_t prow = d / 128 * 4 * (uint64_t)S * B;   // [d/128][S][S][128/S/32][B] rows of 32 floats
+    const BlkShape sh = blk_shape((int)B, (int)d, m.block_cfg);
+    const uint64_t prow = blk_prows((int)B, (int)d, sh.S, sh.BM);
+    if ((st = make_map(&m.mW_K64, m.d.W, d, n * d, (uint32_t)sh.BM)) != SLM_OK) return st;
     if ((st = make_map_bf16_store(&m.mdW_st, m.d.dW, d, n * d)) != SLM_OK) return st;
     for (int i = 0; i < 2; ++i)
       if ((st = make_map(&m.mAct[i], w + L.act[i], d, B, (uint32_t)B)) != SLM_OK) return st;
-    if ((st = make_map_f32_sw(&m.mPf, w + L.P, 32, prow, (uint32_t)B)) != SLM_OK) return st;
+    // partial exchange: {32, B} box for the owner's loads, {32, 32} for a warp's chunk stores
+    if ((st = make_map_f32_16(&m.mPf[0], w + L.P, 16, prow, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map_f32_16(&m.mPf[1], w + L.P, 16, prow, 32u)) != SLM_OK) return st;
     if (m.overlap) {
       for (int i = 0; i < 2; ++i)
         if ((st = make_map(&m.mAct3[i], w + L.act3[i], d, B, (uint32_t)B)) != SLM_OK) return st;
-      if ((st = make_map_f32_sw(&m.mPf3, w + L.P3, 32, prow, (uint32_t)B)) != SLM_OK) return st;
+      if ((st = make_map_f32_16(&m.mPf3[0], w + L.P3, 16, prow, (uint32_t)B)) != SLM_OK) return st;
+      if ((st = make_map_f32_16(&m.mPf3[1], w + L.P3, 16, prow, 32u)) != SLM_OK) return st;
     }
     for (int i = 0; i < kNA; ++i)
       if ((st = make_map(&m.mAb_MN[i], w + L.ab[i], d, B, 64)) != SLM_OK) return st;
@@ -485,7 +507,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   const bool bf16 = m.d.dtype == SLM_BF16;
   const bool tc = tc_ok(m);
   const bool fz = fused_ok(m);
-  const int S = fz ? blk_split(B, d) : 0;
+  const BlkShape bsh = fz ? blk_shape(B, d, m.block_cfg) : BlkShape{0, 0};
   const int Bg = m.d.batch_global > 0 ? m.d.batch_global : B;
   const float inv_bg = 1.0f / (float)Bg;
   const WsLayout L = ws_layout(m);
@@ -525,8 +547,8 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   const uint64_t row_bytes = (uint64_t)d * 4;
   if (fz) {
     const uint64_t prows = std::max<uint64_t>((uint64_t)p->pool_bytes / row_bytes, (uint64_t)B);
-    if ((s = make_map_f32_sw(&mx_pool, pool ? pool : x0, d, prows, (uint32_t)B)) != SLM_OK) return s;
-    if ((s = make_map_f32_sw(&mx_x0, x0, d, (uint64_t)B, (uint32_t)B)) != SLM_OK) return s;
+    if ((s = make_map_f32_16(&mx_pool, pool ? pool : x0, d, prows, (uint32_t)B)) != SLM_OK) return s;
+    if ((s = make_map_f32_16(&mx_x0, x0, d, (uint64_t)B, (uint32_t)B)) != SLM_OK) return s;
   }
   auto xsrc = [&](const float* ptr, const CUtensorMap** map, int* row) -> slm_status {
     if (ptr == (const float*)x0) {
@@ -592,7 +614,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock timing
     if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
     m.ts_kind[ts_slot] = kind;
-    return ((++ts_slot) << 8) | (m.profile_ts_dep ? 8 : 0);
+    return ((++ts_slot) << 8) | (m.profile_ts_dep == 1 ? 8 : 0) | (m.profile_ts_dep == 2 ? 16 : 0);
   };
   int kb = 0;             // backward index: the k-th gradient Block node
   int gcur = 0;           // gq buffer holding the bf16 copy of the current upstream gradient
@@ -682,7 +704,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         bf* const* ap = act_ptr[on3 ? 1 : 0];
         if (as.node != o.in_node) {   // K1: a_l from x_l (first Block of a run)
           pbeg(fs);
-          CK(launch_k1(B, S, xin, gam + (size_t)l * d, bet + (size_t)l * d, d, ap[as.cur], fs, pdl));
+          CK(launch_k1(B, bsh, xin, gam + (size_t)l * d, bet + (size_t)l * d, d, ap[as.cur], fs, pdl));
           pend(SLM_K_BN_ACT, fs);
           ++nl;
         }
@@ -700,7 +722,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         a.a_out = ap[as.cur ^ 1];
         a.dbg = gdbg(SLM_K_GEMM_FWD);
         pbeg(fs);
-        if ((s = launch_blk(B, S, false, m.mW_K, (on3 ? m.mAct3 : m.mAct)[as.cur], on3 ? m.mPf3 : m.mPf, *xm, a, fs,
+        if ((s = launch_blk(B, bsh, false, m.mW_K64, (on3 ? m.mAct3 : m.mAct)[as.cur], on3 ? m.mPf3 : m.mPf, *xm, a, fs,
                             pdl)) != SLM_OK)
           return s;
         pend(SLM_K_GEMM_FWD, fs);
@@ -782,7 +804,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         a.db_prev = dbp;
         a.dbg = gdbg(SLM_K_GEMM_DX);
         pbeg(st);
-        if ((s = launch_blk(B, S, true, m.mW_MN, m.mG_K[gcur], m.mPf, *xm, a, st, pdl)) != SLM_OK) return s;
+        if ((s = launch_blk(B, bsh, true, m.mW_MN, m.mG_K[gcur], m.mPf, *xm, a, st, pdl)) != SLM_OK) return s;
         pend(SLM_K_GEMM_DX, st);
         // dW_l[f_out][f_in] = sum_b g[b][f_out] a[b][f_in]  (second stream)
         cudaStream_t sw = st;

@@ -182,7 +182,8 @@ slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* va
   else if (k == "overlap") *value = m->overlap;
   else if (k == "fused") *value = m->fused;
   else if (k == "use_graph") *value = m->use_graph;
-  else if (k == "block_split") *value = m->kind == SLM_MODEL_CHAIN && fused_ok(*m) ? blk_split(m->d.batch, m->d.width) : 0;
+  else if (k == "block_split") *value = m->kind == SLM_MODEL_CHAIN && fused_ok(*m) ? blk_shape(m->d.batch, m->d.width, m->block_cfg).S : 0;
+  else if (k == "block_m") *value = m->kind == SLM_MODEL_CHAIN && fused_ok(*m) ? blk_shape(m->d.batch, m->d.width, m->block_cfg).BM : 0;
   else {
     set_error("unknown or write-only option: " + k);
     return SLM_E_ARG;
@@ -201,6 +202,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "gemm_impl") m->gemm_impl = (int)value;
   else if (k == "fused") m->fused = (int)value;
   else if (k == "overlap") m->overlap = (int)value;
+  else if (k == "block_cfg") m->block_cfg = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
@@ -249,7 +251,7 @@ slm_status slm_model_kernel_times(slm_model* m, float* ms, int64_t* count, int32
   }
   m->ev_live.clear();
   // device-clock GEMM spans of the last step (profile_ts): max end - min start over the CTAs
-  if (m->profile_ts > 0 && m->ts_buf && m->ts_used > 0) {
+  if (m->profile_ts > 0 && m->ts_buf && m->ts_used > 0 && m->profile_ts_dep != 2) {
     CK(cudaDeviceSynchronize());
     std::vector<unsigned long long> h((size_t)m->ts_used * 1024 * 2);
     CK(cudaMemcpy(h.data(), m->ts_buf, h.size() * 8, cudaMemcpyDeviceToHost));
@@ -497,16 +499,18 @@ slm_status slm_debug_timestamps(void* dev_buf) {
 slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opnd, const float* x, const float* g,
                            const float* bias, const float* gamma, const float* beta, float* out, void* a_out,
                            void* gq_out, float* dgamma, float* dbeta, float* db_prev, void* P, int dbg, void* stream) {
-  const int S = blk_split(B, d);
+  const BlkShape sh = blk_shape(B, d, dbg >> 4);   // dbg bits 4..: block_cfg
+  const int S = sh.S;
   if (S == 0) {
     set_error("slm_debug_block: unsupported (B, d)");
     return SLM_E_UNSUPPORTED;
   }
-  CUtensorMap ma, mb, mp, mx;
+  CUtensorMap ma, mb, mp[2], mx;
   slm_status s;
-  const uint64_t prow = (uint64_t)d / 128 * 4 * S * B;
-  if ((s = make_map(&ma, W, d, d, bwd ? 64 : 128)) || (s = make_map(&mb, opnd, d, B, (uint32_t)B)) ||
-      (s = make_map_f32_sw(&mp, P, 32, prow, (uint32_t)B)) || (s = make_map_f32_sw(&mx, x, d, B, (uint32_t)B)))
+  const uint64_t prow = blk_prows(B, d, S, sh.BM);
+  if ((s = make_map(&ma, W, d, d, bwd ? 64u : (uint32_t)sh.BM)) || (s = make_map(&mb, opnd, d, B, (uint32_t)B)) ||
+      (s = make_map_f32_16(&mp[0], P, 16, prow, (uint32_t)B)) || (s = make_map_f32_16(&mp[1], P, 16, prow, 32u)) ||
+      (s = make_map_f32_16(&mx, x, d, B, (uint32_t)B)))
     return s;
   slmk::BlkArgs a{};
   a.d = d;
@@ -520,8 +524,8 @@ slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opn
   a.dgamma = dgamma;
   a.dbeta = dbeta;
   a.db_prev = db_prev;
-  a.dbg = dbg ? 4 : 0;
-  return launch_blk(B, S, bwd != 0, ma, mb, mp, mx, a, (cudaStream_t)stream, false);
+  a.dbg = (dbg & 1) ? 4 : 0;
+  return launch_blk(B, sh, bwd != 0, ma, mb, mp, mx, a, (cudaStream_t)stream, false);
 }
 
 // slm_debug_gemm: one GEMM of the three kinds through the chosen implementation

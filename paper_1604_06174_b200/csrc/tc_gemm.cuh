@@ -99,6 +99,12 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+// address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t cluster_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -323,16 +329,21 @@ struct TcCfg {
 // launch's start (phase 0) and end (phase 7) per CTA at [slot][1024 CTAs][2] — used to time
 // every GEMM of a real step on the device clock (profile_ts option of the model).
 __device__ unsigned long long* g_slm_ts = nullptr;
-__device__ __forceinline__ void ts_mark(int phase, int dbg) {
-  unsigned long long* p = g_slm_ts;
+// the stamp buffer of this launch: the global pointer is read only when the launch is profiled
+// (dbg != 0), so production launches issue no memory access for their instrumentation
+__device__ __forceinline__ unsigned long long* ts_buffer(int dbg) { return dbg ? g_slm_ts : nullptr; }
+// dbg bit 4 (16): phase mode of the step profile, all 8 phases of every CTA at [slot][1024 CTAs][8]
+__device__ __forceinline__ void ts_mark(unsigned long long* p, int phase, int dbg) {
   if (p != nullptr && threadIdx.x == 0) {
     const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int slot = (dbg >> 8) - 1;
     if (slot < 0 && !(dbg & 4)) return;   // per-CTA phase mode only from the debug hook (bit 2)
-    if (slot >= 0 && phase != 0 && phase != 7) return;
+    if (slot >= 0 && !(dbg & 16) && phase != 0 && phase != 7) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (slot >= 0)
+    if (slot >= 0 && (dbg & 16))
+      p[((size_t)slot * 1024 + cta) * 8 + phase] = t;
+    else if (slot >= 0)
       p[((size_t)slot * 1024 + cta) * 2 + (phase == 7)] = t;
     else
       p[cta * 8 + phase] = t;
@@ -342,10 +353,9 @@ __device__ __forceinline__ void ts_mark(int phase, int dbg) {
 // profile mode "after dependency" (dbg bit 3): the launch's start stamp is replaced by the
 // moment this CTA's producer returns from griddepcontrol.wait (its inputs are ready), so the
 // span excludes time spent overlapping the predecessor under programmatic dependent launch
-__device__ __forceinline__ void ts_dep(int dbg) {
-  unsigned long long* p = g_slm_ts;
+__device__ __forceinline__ void ts_dep(unsigned long long* p, int dbg) {
   const int slot = (dbg >> 8) - 1;
-  if (p == nullptr || slot < 0) return;
+  if (p == nullptr || slot < 0 || (dbg & 16)) return;
   const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -372,7 +382,8 @@ __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg,
                    int pf_row0) {
-  ts_mark(0, dbg);
+  unsigned long long* const tsp = ts_buffer(dbg);
+  ts_mark(tsp, 0, dbg);
   using C = TcCfg<BN, A_MN, B_MN, CG>;
   uint32_t rank = 0;
   if constexpr (CG == 2) rank = cluster_ctarank();
@@ -419,7 +430,7 @@ __global__ void __launch_bounds__(128, 1)
   if constexpr (CG == 2) cluster_sync();   // the peer's barriers are initialised before use
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  ts_mark(1, dbg);
+  ts_mark(tsp, 1, dbg);
   // pf_row0 >= 0: pull this CTA's A tile of the NEXT GEMM of the chain (the next layer's
   // weights, rows a_row0 -> pf_row0) into L2 while this one runs
   if (pf_row0 >= 0 && warp == 2 && lane == 0) {
@@ -487,11 +498,11 @@ __global__ void __launch_bounds__(128, 1)
         load_a(kb, kb);
       }
       pdl_wait();
-      if (dbg & 8) ts_dep(dbg);
+      if (dbg & 8) ts_dep(tsp, dbg);
       for (int kb = 0; kb < kb0; ++kb) load_b(kb, kb);
     } else {
       pdl_wait();
-      if (dbg & 8) ts_dep(dbg);
+      if (dbg & 8) ts_dep(tsp, dbg);
     }
     for (int kb = kb0; kb < nk; ++kb) {
       const int s = kb % C::STAGES;
@@ -544,7 +555,7 @@ __global__ void __launch_bounds__(128, 1)
   // let the dependent kernel launch only now (its CTAs would otherwise sit on this kernel's SMs
   // waiting in griddepcontrol.wait for the whole main loop; measured: early trigger is slower)
   pdl_launch();
-  ts_mark(2, dbg);
+  ts_mark(tsp, 2, dbg);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const int m = m0 + warp * 32 + lane;
   if constexpr (EpiCell<Epi>::value) {
@@ -620,7 +631,7 @@ __global__ void __launch_bounds__(128, 1)
       epi(m, n0 + c, acc, ks);
     }
   }
-  ts_mark(7, dbg);
+  ts_mark(tsp, 7, dbg);
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) {

@@ -1,7 +1,7 @@
 """Per-phase device-clock breakdown of the fused Block kernel (slm_debug_block with per-CTA
-%globaltimer stamps): phase 0 start, 1 setup done (barriers, TMEM), 2 accumulator ready, 3 partial
-slices written, 4 cluster barrier passed, 5 incoming slices + x (g) landed, 6 first BN pass done,
-7 end.  Prints the median and max over CTAs of each phase's time since the earliest start."""
+%globaltimer stamps): phase 0 start, 1 griddepcontrol.wait returned (producer), 2 accumulator ready,
+3 own quarter-slices staged and stored (all warps), 4 incoming slices + x landed, 5 first BN pass
+done, 7 end.  Prints the median and max over CTAs of each phase's time since the earliest start."""
 import ctypes as C
 import os
 import sys

@@ -23,9 +23,13 @@ model = slm.ChainModel(params, grads, dtype="bf16", batch=B, **opts)
 af = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | (slm.ALLOC_MIRROR_PARITY if mp else 0)
 plan = slm.Plan(slm.Graph.chain(n, B, d), os.environ.get("STRATEGY", "sqrt"), alloc_flags=af)
 ngemm = 3 * n + plan.extra_forward
-ts = torch.zeros(ngemm * 1024 * 2, dtype=torch.int64, device=dev)
+PH = int(os.environ.get("PHASES", 0))   # 1: all 8 phase stamps of every CTA (profile_ts_dep = 2)
+W8 = 8 if PH else 2
+ts = torch.zeros(ngemm * 1024 * W8, dtype=torch.int64, device=dev)
 model.set_option("profile_ts", ngemm)
 model.set_option("profile_ts_buffer", ts.data_ptr())
+if PH:
+    model.set_option("profile_ts_dep", 2)
 st = torch.cuda.Stream()
 bufs = model.buffers(plan, dev)
 with torch.cuda.stream(st):
@@ -43,10 +47,19 @@ kind = (C.c_int32 * ngemm)()
 aux = (C.c_int32 * ngemm)()
 nn = C.c_int32()
 slm.check(slm.lib.slm_debug_ts_meta(model._h, kind, aux, ngemm, C.byref(nn)))
-t = ts.view(ngemm, 1024, 2).cpu().numpy()[:nn.value].astype(np.float64)
+t = ts.view(ngemm, 1024, W8).cpu().numpy()[:nn.value].astype(np.float64)
 t[t == 0] = np.nan
 s0 = np.nanmin(t[:, :, 0], axis=1)
-s1 = np.nanmax(t[:, :, 1], axis=1)
+s1 = np.nanmax(t[:, :, W8 - 1], axis=1)
+if PH:   # per kind: median over launches of the median over CTAs of (phase_i - the launch's first start)
+    kk_ = np.array(kind[:nn.value])
+    for kv, nm in ((1, "fwd Block"), (2, "dX Block"), (3, "dW GEMM")):
+        sel = np.where(kk_ == kv)[0]
+        if not len(sel):
+            continue
+        rel = (t[sel] - s0[sel, None, None]) / 1e3
+        med = np.nanmedian(np.nanmedian(rel, axis=1), axis=0)
+        print(f"  phases {nm:10s} (us from launch start): " + " ".join(f"{i}:{med[i]:.2f}" for i in range(8)))
 T0 = np.nanmin(s0)
 s0, s1 = (s0 - T0) / 1e3, (s1 - T0) / 1e3
 k = np.array(kind[:nn.value])

@@ -78,7 +78,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
 }
 
 // ================================================================ MMA issue rate
-template <int N, int CG>
+template <int N, int CG, int MC = 128>
 __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* o
   const uint32_t tmem = tslot;
   uint64_t t0 = 0, t1 = 0;
   if (threadIdx.x == 0 && rank == 0) {
-    constexpr uint32_t idesc = make_idesc(128 * CG, N);
+    constexpr uint32_t idesc = make_idesc(MC * CG, N);
     const uint32_t sa = smem_u32(sm), sb = sa + 16384;
     t0 = clk();
     for (int it = 0; it < iters; ++it) {
@@ -153,9 +153,9 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* o
   }
 }
 
-template <int N, int CG>
+template <int N, int CG, int MC = 128>
 void run_mma(int grid, int iters) {
-  auto k = k_mma<N, CG>;
+  auto k = k_mma<N, CG, MC>;
   const int smem = 64 * 1024;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   unsigned long long* d;
@@ -185,8 +185,8 @@ void run_mma(int grid, int iters) {
       ++cnt;
     }
   const double per = (sum / cnt) / (iters * 4.0);   // cycles per K=16 MMA
-  const double macs_sm = 128.0 * CG * N * 16 / per / CG;
-  printf("mma CG=%d M=%3d N=%3d grid=%3d: %.1f clk per K16 MMA (max %.1f), %.0f MAC/clk/SM (peak 4096)\n", CG, 128 * CG,
+  const double macs_sm = (double)MC * CG * N * 16 / per / CG;
+  printf("mma CG=%d M=%3d N=%3d grid=%3d: %.1f clk per K16 MMA (max %.1f), %.0f MAC/clk/SM (peak 4096)\n", CG, MC * CG,
          N, grid, per, mx / (iters * 4.0), macs_sm);
   cudaFree(d);
 }
@@ -265,6 +265,142 @@ __global__ void __launch_bounds__(128, 1) k_ingest(const __grid_constant__ CUten
   }
 }
 
+
+// ================================================================ epilogue components
+// mode 0: tcgen05.ld of the whole 128 x 256 fp32 accumulator into registers (8 warps, x32 loads)
+// mode 1: + stores into a 128-byte-swizzled [b][32] smem layout (the Block kernel's slices)
+// mode 2: + TMA bulk tensor stores of 3 of the 4 slices (96 KiB) to global and wait_group 0
+// mode 3: TMA loads of 3 slices (96 KiB) from global into smem only
+__device__ __forceinline__ int swo(int B_, int c, int b, int f32) {
+  return (c * B_ + b) * 32 + ((((f32 >> 2) ^ (b & 7))) << 2) + (f32 & 3);
+}
+__global__ void __launch_bounds__(256, 1) k_epi(const __grid_constant__ CUtensorMap tmP, int mode, int reps,
+                                                 unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  float sink = 0.f;
+  const uint64_t t0 = clk();
+  for (int r = 0; r < reps; ++r) {
+    if (mode <= 2) {
+      const int q = warp & 3, h = warp >> 2;
+      float* slot = reinterpret_cast<float*>(sm + q * 32768);
+      for (int c0 = h * 128; c0 < h * 128 + 128; c0 += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+            "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tmem + ((uint32_t)(q * 32) << 16) + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (mode == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sink += __uint_as_float(v[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) slot[swo(256, 0, c0 + j, lane)] = __uint_as_float(v[j]);
+        }
+      }
+      if (mode == 2) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int s = 1; s < 4; ++s)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             (uint64_t)&tmP),
+                         "r"(smem_u32(sm + s * 32768)), "r"(0), "r"((int)(blockIdx.x * 4 + s) * 256)
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+      }
+      __syncthreads();
+    } else {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, 3 * 32768);
+        for (int s = 1; s < 4; ++s)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+              "[%2];" ::"r"(smem_u32(sm + s * 32768)),
+              "l"((uint64_t)&tmP), "r"(smem_u32(&bar)), "r"(0), "r"((int)(blockIdx.x * 4 + s) * 256)
+              : "memory");
+      }
+      mbar_wait(&bar, r & 1);
+      __syncthreads();
+    }
+  }
+  const uint64_t t1 = clk();
+  if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / reps + (sink == 12345.f);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+
+// store-path variants for the 96 KiB partial exchange (per CTA), completion included:
+// mode 0: TMA bulk tensor store (3 boxes of 32 KiB), wait_group 0
+// mode 1: st.global.v4 from registers (256 threads, 24 x 16 B each), then fence.acq_rel.gpu
+// mode 2: st.global.b32 coalesced (a warp writes 128 B per instruction), then fence.acq_rel.gpu
+// mode 3: 1-D bulk copies cp.async.bulk.global.shared::cta (3 x 32 KiB), wait_group 0
+__global__ void __launch_bounds__(256, 1) k_store(const __grid_constant__ CUtensorMap tmP, float* P, int mode, int reps,
+                                                   unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+  float* dst = P + (size_t)blockIdx.x * 4 * 8192;
+  const uint64_t t0 = clk();
+  for (int r = 0; r < reps; ++r) {
+    if (mode == 0 || mode == 3) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int s = 1; s < 4; ++s) {
+          if (mode == 0)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             (uint64_t)&tmP),
+                         "r"(smem_u32(sm + s * 32768)), "r"(0), "r"((int)(blockIdx.x * 4 + s) * 256)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + s * 8192),
+                         "r"(smem_u32(sm + s * 32768)), "r"(32768)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+    } else if (mode == 1) {
+      float4 v = make_float4(r, 1, 2, 3);
+      float4* d4 = reinterpret_cast<float4*>(dst + 8192);
+      for (int i = threadIdx.x; i < 3 * 8192 / 4; i += 256) d4[i] = v;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      __syncthreads();
+    } else {
+      for (int i = threadIdx.x; i < 3 * 8192; i += 256) dst[8192 + i] = (float)r;
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      __syncthreads();
+    }
+  }
+  const uint64_t t1 = clk();
+  if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / reps;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -340,6 +476,11 @@ int main(int argc, char** argv) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   printf("SMs %d\n", sms);
   const int iters = 2048;
+  run_mma<256, 1, 64>(1, iters);
+  run_mma<256, 2, 64>(2, iters);
+  run_mma<128, 2, 64>(2, iters);
+  run_mma<256, 1, 64>(148, iters);
+  run_mma<256, 2, 64>(148, iters);
   run_mma<64, 1>(1, iters);
   run_mma<128, 1>(1, iters);
   run_mma<256, 1>(1, iters);
@@ -349,6 +490,48 @@ int main(int argc, char** argv) {
   run_mma<256, 1>(148, iters);
   run_mma<256, 2>(148, iters);
 
+
+  // epilogue components at 64 CTAs (the Block kernel's grid at C2)
+  {
+    float* Pb;
+    const int grid = 64;
+    CK(cudaMalloc(&Pb, (size_t)grid * 4 * 256 * 32 * 4));
+    CUtensorMap tp;
+    cuuint64_t dims[2] = {32, (cuuint64_t)grid * 4 * 256};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {32, 256};
+    cuuint32_t es[2] = {1, 1};
+    CUresult rr = enc()(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Pb, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rr != CUDA_SUCCESS) printf("encode P failed %d\n", (int)rr);
+    CK(cudaFuncSetAttribute(k_epi, cudaFuncAttributeMaxDynamicSharedMemorySize, 129 * 1024));
+    unsigned long long* dd;
+    CK(cudaMalloc(&dd, grid * 8));
+    const char* names[4] = {"TMEM ld 128 KiB (8 warps)", "+ STS swizzled", "+ TMA store 96 KiB + wait", "TMA load 96 KiB"};
+    for (int mode = 0; mode < 4; ++mode) {
+      k_epi<<<grid, 256, 129 * 1024>>>(tp, mode, 20, dd);
+      CK(cudaDeviceSynchronize());
+      std::vector<unsigned long long> h(grid);
+      CK(cudaMemcpy(h.data(), dd, grid * 8, cudaMemcpyDeviceToHost));
+      double sum = 0;
+      for (auto v : h) sum += v;
+      printf("epilogue %-28s: %.0f clk per rep (mean over %d CTAs) = %.2f us @1.9GHz\n", names[mode], sum / grid, grid,
+             sum / grid / 1900.0);
+    }
+    CK(cudaFuncSetAttribute(k_store, cudaFuncAttributeMaxDynamicSharedMemorySize, 129 * 1024));
+    const char* sn[4] = {"TMA tensor store 3x32KiB", "st.global.v4 + fence", "st.global.b32 + fence", "bulk 1-D store 3x32KiB"};
+    for (int g : {64, 16})
+      for (int mode = 0; mode < 4; ++mode) {
+        k_store<<<g, 256, 129 * 1024>>>(tp, Pb, mode, 20, dd);
+        CK(cudaDeviceSynchronize());
+        std::vector<unsigned long long> h(g);
+        CK(cudaMemcpy(h.data(), dd, g * 8, cudaMemcpyDeviceToHost));
+        double sum = 0;
+        for (auto v : h) sum += v;
+        printf("store %-26s grid %2d: %.0f clk per 96 KiB = %.2f us\n", sn[mode], g, sum / g, sum / g / 1900.0);
+      }
+
+  }
   const int d = 2048, nlay = 64;
   void *W, *X;
   CK(cudaMalloc(&W, (size_t)nlay * d * d * 2));

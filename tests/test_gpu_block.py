@@ -21,8 +21,10 @@ from oracle import chain as OC
 
 pytestmark = pytest.mark.gpu
 
-# (B, d): cluster split S = 4 (d % 256 == 0) and S = 2 (B <= 128)
-CASES = [(64, 256), (64, 128), (128, 384), (128, 512), (256, 512), (256, 2048)]
+# (B, d, block_cfg): the default shape (BM, S) = (64, 4) at d % 256 == 0, (64, 2) at d = 128 / 384 / 640;
+# at B = 256 also (128, 4) (cfg 2) and (64, 2) (cfg 3)
+CASES = [(64, 256, 0), (64, 128, 0), (128, 384, 0), (128, 512, 0), (256, 512, 0), (256, 640, 0), (256, 2048, 0),
+         (256, 512, 2), (256, 2048, 2), (256, 2048, 3)]
 
 
 @pytest.fixture(scope="module")
@@ -64,60 +66,66 @@ def _inputs(B, d, seed):
     return OC.Params(W, b, gam, bet), x, g
 
 
-def _launch(slm, bwd, B, d, W, opnd, x, g, bias, gam, bet):
+def _launch(slm, bwd, B, d, W, opnd, x, g, bias, gam, bet, cfg=0):
     t = lambda a, dt=torch.float32: torch.tensor(np.asarray(a), dtype=torch.float64).to(dt).cuda()
-    S = 4 if d % 256 == 0 else 2
     dev = dict(W=t(W, torch.bfloat16), opnd=t(opnd, torch.bfloat16), x=t(x), g=t(g), bias=t(bias), gam=t(gam),
                bet=t(bet))
-    P = torch.empty(S * B * d, device="cuda")
+    P = torch.empty(4 * B * d, device="cuda")
     out = torch.empty(B, d, device="cuda")
     aout = torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
     gq = torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
     dgam, dbet, dbp = (torch.empty(d, device="cuda") for _ in range(3))
     slm.check(slm.lib.slm_debug_block(bwd, B, d, _p(dev["W"]), _p(dev["opnd"]), _p(dev["x"]), _p(dev["g"]),
                                       _p(dev["bias"]), _p(dev["gam"]), _p(dev["bet"]), _p(out), _p(aout), _p(gq),
-                                      _p(dgam), _p(dbet), _p(dbp), _p(P), 0,
+                                      _p(dgam), _p(dbet), _p(dbp), _p(P), cfg << 4,
                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)), "slm_debug_block")
     torch.cuda.synchronize()
     return {k: v.double().cpu().numpy() for k, v in dict(out=out, a=aout, gq=gq, dgamma=dgam, dbeta=dbet,
                                                            db=dbp).items()}
 
 
-def _bf16_codes(got, ref_f64, name):
+def _bf16_codes(got, ref_f64, name, floor=0.0):
     """bf16 outputs are quantised codes: equal to the oracle's bf16 rounding, or one bf16 step away
-    where the fp32 (kernel) and fp64 (oracle) values straddle a rounding boundary"""
+    where the fp32 (kernel) and fp64 (oracle) values straddle a rounding boundary (plus an absolute
+    floor for values at the ReLU kink, where fp32 noise decides between 0 and a tiny code)"""
     ref = OC.bf16_round(ref_f64)
     big = np.maximum(np.maximum(np.abs(got), np.abs(ref)), 1e-30)
     ulp = 2.0 ** (np.floor(np.log2(big)) - 7)   # one bf16 step at the larger magnitude
     diff = np.abs(got - ref)
-    assert bool((diff <= ulp).all()), (name, float(diff.max()))
+    bad = diff > np.maximum(ulp, floor)
+    if bad.any():
+        i = np.unravel_index(int(np.argmax(diff - np.maximum(ulp, floor))), diff.shape)
+        raise AssertionError(f"{name}: {int(bad.sum())} codes off by more than one step; worst at {i}: got {got[i]!r} "
+                             f"ref {ref[i]!r} (fp64 {ref_f64[i]!r})")
     assert (diff > 0).mean() < 1e-3, (name, float((diff > 0).mean()))   # ties are rare
 
 
-@pytest.mark.parametrize("B,d", CASES)
-def test_forward_block_vs_oracle(slm, B, d):
+@pytest.mark.parametrize("B,d,cfg", CASES)
+def test_forward_block_vs_oracle(slm, B, d, cfg):
     P, x, _ = _inputs(B, d, B + d)
     u, _ = _u(x, P.gamma[0], P.beta[0])
     a = OC.bf16_round(np.maximum(u, 0.0))      # the operand oracle.block_forward builds from x
     ref = OC.block_forward(x, P, 0, "bf16")    # x + a W_0^T + b_0
-    got = _launch(slm, 0, B, d, P.W[0], a, x, np.zeros_like(x), P.b[0], P.gamma[1], P.beta[1])
+    got = _launch(slm, 0, B, d, P.W[0], a, x, np.zeros_like(x), P.b[0], P.gamma[1], P.beta[1], cfg)
     st = assert_close(got["out"], ref, 1e-5, "x_{l+1}")
     u1, _ = _u(ref, P.gamma[1], P.beta[1])
-    _bf16_codes(got["a"], np.maximum(u1, 0.0), "a_{l+1}")
-    print(f"forward B={B} d={d}: x_(l+1) max_abs {st[0]:.2e} rms_ref {st[1]:.2e} rel_l2 {st[2]:.2e}")
+    _bf16_codes(got["a"], np.maximum(u1, 0.0), "a_{l+1}", floor=1e-6)
+    print(f"forward B={B} d={d} cfg={cfg}: x_(l+1) max_abs {st[0]:.2e} rms_ref {st[1]:.2e} rel_l2 {st[2]:.2e}")
 
 
-@pytest.mark.parametrize("B,d", CASES)
-def test_backward_block_vs_oracle(slm, B, d):
+@pytest.mark.parametrize("B,d,cfg", CASES)
+def test_backward_block_vs_oracle(slm, B, d, cfg):
     P, x, g = _inputs(B, d, 7 * B + d)
     dx, (dW, db, dgam, dbet) = OC.block_backward(g, x, P, 0, "bf16")
-    got = _launch(slm, 1, B, d, P.W[0], OC.bf16_round(g), x, g, P.b[0], P.gamma[0], P.beta[0])
+    got = _launch(slm, 1, B, d, P.W[0], OC.bf16_round(g), x, g, P.b[0], P.gamma[0], P.beta[0], cfg)
     for k, ref in (("dbeta", dbet), ("dgamma", dgam), ("out", dx), ("db", dx.sum(axis=0))):
         st = assert_close(got[k], ref, 1e-4, k)
-        print(f"backward B={B} d={d} {k}: max_abs {st[0]:.2e} rms_ref {st[1]:.2e} rel_l2 {st[2]:.2e}")
-    _bf16_codes(got["gq"], dx, "bf16 dx")
+        print(f"backward B={B} d={d} cfg={cfg} {k}: max_abs {st[0]:.2e} rms_ref {st[1]:.2e} rel_l2 {st[2]:.2e}")
+    # the bf16 copy is the kernel's own fp32 dx rounded to nearest even (checked exactly); the fp32
+    # dx itself is compared with the oracle above
+    assert np.array_equal(got["gq"], OC.bf16_round(got["out"])), "bf16 dx is not RNE(dx)"
     u, _ = _u(x, P.gamma[0], P.beta[0])
-    _bf16_codes(got["a"], np.maximum(u, 0.0), "a_l")
+    _bf16_codes(got["a"], np.maximum(u, 0.0), "a_l", floor=1e-6)
 
 
 def test_block_deterministic(slm):

@@ -201,30 +201,6 @@ def test_lstm_alternating_plans_share_buffers(slm):
         assert torch.equal(a[1], b[1])
 
 
-def test_lstm_fused_cell_epilogue_matches_kernel_path(slm):
-    """lstm_fuse_cell = 1 runs the gates + cell in the GEMM epilogue, otherwise the GEMM (split-K 1
-    or 2) is followed by the gates/cell kernel.  All follow the oracle; each is ckpt == no-ckpt
-    bitwise, and the fused epilogue gives the same bits as the kernel path with one K slice."""
-    cfg = (2, 6, 64, 128, 50, 300)
-    L, T, B, H, I, C = cfg
-    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=23)
-    P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
-    ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
-    res = {}
-    for sk, fc in ((1, 1), (1, 0), (2, 0)):
-        l0, g0, _ = _run(slm, cfg, inp, "none", lstm_sk=sk, lstm_fuse_cell=fc)
-        l1, g1, _ = _run(slm, cfg, inp, m=slm.Graph.lstm(L, T, B, H, I).lstm_segment_mirrors(2), lstm_sk=sk,
-                         lstm_fuse_cell=fc)
-        assert l0 == l1
-        for k in g0:
-            assert np.array_equal(g0[k], g1[k]), (sk, fc, k)
-        assert abs(l0 - ol) / abs(ol) <= 2e-2
-        assert _rel(g0["W_o"][:C], og["W_o"]) <= 2e-2
-        res[(sk, fc)] = (l0, g0)
-    assert res[(1, 1)][0] == res[(1, 0)][0]
-    for k in res[(1, 1)][1]:
-        assert np.array_equal(res[(1, 1)][1][k], res[(1, 0)][1][k]), k
-
 
 @pytest.mark.parametrize("cfg", [(2, 40, 64, 128, 50, 300), (3, 24, 64, 128, 50, 200)])
 def test_lstm_search_plans_bitwise(slm, cfg):
