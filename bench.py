@@ -187,10 +187,11 @@ def lstm_gemm_flops(plan, L, T, B, H, I, C):
 def lstm_inputs_dev(L, T, B, H, I, C, dev):
     import torch
 
+    import paper_1604_06174_b200 as slm
     import synth
     inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16")
     Cp = -(-C // 128) * 128
-    W = torch.cat([torch.from_numpy(w).reshape(-1) for w in inp["W"]]).to(torch.bfloat16).to(dev)
+    W = slm.LstmModel.pack_w([torch.from_numpy(w) for w in inp["W"]], I).to(torch.bfloat16).to(dev)
     Wo = torch.zeros(Cp, H)
     Wo[:C] = torch.from_numpy(inp["W_o"])
     bo = torch.zeros(Cp)

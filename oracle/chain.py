@@ -146,14 +146,21 @@ def step_planned(plan, P: Params, x0, labels, mode="f64", batch_global=None):
     tags: "gradient calculation ... just a forward pass on the entire computation graph"
     (PAPER.md:135).  Each node's value is stored under its tag; a read of predecessor p
     asserts the tag still holds p (interference check).  Returns (loss, grads, dx0, stats)
-    with stats = dict(peak_live_bytes, op_evaluations)."""
+    with stats = dict(peak_live_bytes = the peak over V' of the bytes of values still to be read
+    (Input values count throughout), op_evaluations)."""
     x0 = np.asarray(x0, dtype=np.float64)
     Bg = batch_global or x0.shape[0]
     gg, al = plan.gg, plan.alloc
     store = {}            # tag -> (node, value)
     grads = [None] * P.n
     evals = 0
-    live = set()
+    # liveness of the values (not the tags): a node's value is live from its evaluation until its
+    # last reader in V' has run; the peak of the live bytes is what any allocator must hold at once
+    last_read = {}
+    for i, v in enumerate(gg.order):
+        for p in gg.nodes[v].preds:
+            last_read[p] = i
+    live = {}             # node -> bytes
     peak = 0
     dx0 = None
     loss = None
@@ -164,7 +171,9 @@ def step_planned(plan, P: Params, x0, labels, mode="f64", batch_global=None):
             raise TagClobber(f"node {p}: tag {t} holds {store.get(t, (None,))[0]}")
         return store[t][1]
 
-    for v in gg.order:
+    # Inputs and the loss (the graph output) stay live for the whole step (A8 pins them)
+    pinned = {v for v, nd in enumerate(gg.nodes) if nd.op == INPUT or (nd.op == SOFTMAX_CE and nd.kind == "fwd")}
+    for i, v in enumerate(gg.order):
         nd = gg.nodes[v]
         if nd.kind in ("fwd", "mirror"):
             if nd.op == INPUT:
@@ -190,9 +199,15 @@ def step_planned(plan, P: Params, x0, labels, mode="f64", batch_global=None):
             else:
                 raise NotImplementedError(nd.op)
             evals += 1
+        # an in-place node (A8) overwrites the value of the predecessor whose tag it takes
+        for p in nd.preds:
+            if al.tag_of[p] == al.tag_of[v]:
+                live.pop(p, None)
         store[al.tag_of[v]] = (v, val)
-        live.add(al.tag_of[v])
-        peak = max(peak, sum(al.tag_size[t] for t in live))
+        live[v] = nd.out_bytes
+        peak = max(peak, sum(live.values()))
+        for p in [u for u in live if last_read.get(u, -1) <= i and u not in pinned]:
+            del live[p]
     return loss, _stack(grads), dx0, dict(peak_live_bytes=peak, op_evaluations=evals)
 
 

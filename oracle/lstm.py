@@ -5,9 +5,8 @@ input of each timestamp is a continuous 50 dimension vector and the output is so
 5000 class."  Reading A13: PyTorch gate order (i, f, g, o), no peepholes,
 h_0 = c_0 = 0, a softmax head at every step, loss = mean over (t, b).
 
-Parameter layout (shared with the device path's C ABI, a layout only — no code is shared):
-  W[l]   [4H, Kin_l + H]  = [W_ih | W_hh], Kin_0 = the input width padded to a multiple of 128
-                           (padding columns multiply zero-padded inputs), Kin_l = H for l > 0
+Parameter layout (PyTorch's, at the true widths; the device path pads layer 0 in its binding):
+  W[l]   [4H, Kin_l + H]  = [W_ih | W_hh], Kin_0 = the input width I, Kin_l = H for l > 0
   b[l]   [4H]             = b_ih + b_hh
   W_o    [C, H], b_o [C]  the per-step softmax head
 
@@ -41,7 +40,7 @@ class LstmParams:
         self.b = [np.asarray(v, dtype=np.float64) for v in b]
         self.W_o = np.asarray(W_o, dtype=np.float64)
         self.b_o = np.asarray(b_o, dtype=np.float64)
-        self.n_in = n_in                       # true input width (<= Kin_0)
+        self.n_in = n_in                       # the input width I (= Kin_0)
 
     @property
     def L(self):
@@ -55,11 +54,8 @@ class LstmParams:
         return self.W[l].shape[1] - self.H
 
 
-def pad_input(x, kin0):
-    x = np.asarray(x, dtype=np.float64)
-    out = np.zeros(x.shape[:-1] + (kin0,))
-    out[..., : x.shape[-1]] = x
-    return out
+def as_input(x):
+    return np.asarray(x, dtype=np.float64)
 
 
 # ------------------------------------------------------------------ node functions
@@ -136,7 +132,7 @@ def step_plain(P: LstmParams, x, labels, mode="f64"):
     """x [T, B, n_in], labels [T, B] -> (loss, grads dict)."""
     T, B = labels.shape
     L, H = P.L, P.H
-    xs = pad_input(x, P.kin(0))
+    xs = as_input(x)
     scale = 1.0 / (T * B)
     h = [[np.zeros((B, H)) for _ in range(T + 1)] for _ in range(L)]   # h[l][t+1]
     c = [[np.zeros((B, H)) for _ in range(T + 1)] for _ in range(L)]
@@ -186,7 +182,7 @@ def step_planned(plan, P: LstmParams, x, labels, mode="f64"):
     (PAPER.md:488-489), in the same per-step order as step_plain."""
     T, B = labels.shape
     L, H = P.L, P.H
-    xs = pad_input(x, P.kin(0))
+    xs = as_input(x)
     scale = 1.0 / (T * B)
     gg, al = plan.gg, plan.alloc
     nodes = gg.nodes

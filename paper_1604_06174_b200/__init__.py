@@ -13,6 +13,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import _lib
 from ._lib import check, lib
 
@@ -352,6 +354,43 @@ class LstmModel(_Model):
     @staticmethod
     def cpad(n_classes):
         return -(-n_classes // 128) * 128
+
+    @staticmethod
+    def pack_w(W, n_in):
+        """Per-layer [W_ih | W_hh] at the true widths ([4H, I + H], then [4H, 2H]) -> the flat C-ABI
+        layout, layer 0 zero-padded to Kin0 = round_up(I, 128) input columns (reading A21: the
+        GEMM's K tiles by 64).  W: list of tensors / arrays; returns a flat torch tensor (CPU)."""
+        import torch
+        out = []
+        for l, w in enumerate(W):
+            w = torch.as_tensor(w)
+            if l == 0:
+                H4 = w.shape[0]
+                H = H4 // 4
+                k0 = LstmModel.kin0(n_in)
+                wp = torch.zeros(H4, k0 + H, dtype=w.dtype)
+                wp[:, :n_in] = w[:, :n_in]
+                wp[:, k0:] = w[:, n_in:]
+                w = wp
+            out.append(w.reshape(-1))
+        return torch.cat(out)
+
+    @staticmethod
+    def unpack_w(flat, n_layers, hidden, n_in):
+        """Inverse of pack_w for a flat gradient (or weight) buffer: per-layer arrays at the true
+        widths (the padding columns dropped)."""
+        H = hidden
+        k0 = LstmModel.kin0(n_in)
+        out, o = [], 0
+        for l in range(n_layers):
+            kin = k0 if l == 0 else H
+            w = flat[o:o + 4 * H * (kin + H)].reshape(4 * H, kin + H)
+            o += 4 * H * (kin + H)
+            if l == 0:
+                w = np.concatenate([w[:, :n_in], w[:, k0:]], axis=1) if isinstance(w, np.ndarray) else \
+                    __import__("torch").cat([w[:, :n_in], w[:, k0:]], dim=1)
+            out.append(w)
+        return out
 
 
 def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None, split=1):

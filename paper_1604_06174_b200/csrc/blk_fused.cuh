@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   }
   mbar_wait(auxb, 0);
   mbar_wait(recvb2, 0);
-  // the next kernel may now start its prologue and weight prefetch: early enough to hide them under
-  // the batch-norm work, late enough that its waiting CTAs do not hold SMs the concurrent streams
-  // (recompute, dW) need during the backward phase
+  // the next kernel may now start its prologue and weight prefetch, hidden under the batch-norm
+  // work (measured: triggering at the kernel's end instead costs 0.8 us per backward layer at C2,
+  // triggering at the epilogue's start 0.3 us per forward Block)
   pdl_launch();
   ts_mark(tsp, 4, args.dbg);
   float xv[R], zv[R];

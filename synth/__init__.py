@@ -70,18 +70,17 @@ def chain_inputs_torch(n_layers, batch, width, dtype="bf16", seed=SEED, device="
 
 
 def lstm_inputs(n_layers, steps, batch, hidden, n_in, n_classes, dtype="f32", seed=SEED):
-    """Unrolled LSTM inputs in the C-ABI layout: W[l] = [W_ih | W_hh] as [4H, Kin_l + H] with
-    Kin_0 = n_in padded up to a multiple of 128 (zero columns), b[l] = b_ih + b_hh [4H],
-    W_o [C, H], b_o [C] (zeros), x [T, B, n_in], labels [T, B]."""
+    """Unrolled LSTM inputs at the true widths: W[l] = [W_ih | W_hh] as [4H, Kin_l + H] with
+    Kin_0 = n_in, Kin_l = H (the device layout pads layer 0 in the binding, LstmModel.pack_w),
+    b[l] = b_ih + b_hh [4H], W_o [C, H], b_o [C] (zeros), x [T, B, n_in], labels [T, B]."""
     r = _streams(seed + 1, 8)
     H = hidden
     k = 1.0 / np.sqrt(H)
-    kin0 = -(-n_in // 128) * 128
     W = []
     for l in range(n_layers):
-        kin = kin0 if l == 0 else H
+        kin = n_in if l == 0 else H
         w = np.zeros((4 * H, kin + H))
-        w[:, : (n_in if l == 0 else H)] = r[0].uniform(-k, k, (4 * H, n_in if l == 0 else H))
+        w[:, :kin] = r[0].uniform(-k, k, (4 * H, kin))
         w[:, kin:] = r[1].uniform(-k, k, (4 * H, H))
         W.append(w)
     b = r[2].uniform(-k, k, (n_layers, 4 * H)) + r[3].uniform(-k, k, (n_layers, 4 * H))

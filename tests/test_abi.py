@@ -136,3 +136,23 @@ def test_lstm_segment_mirrors_shape():
     kept = [v for v in range(len(m)) if m[v] == 0 and v % per_t in (2, 4)]   # S nodes kept
     assert [v // per_t for v in kept] == [2, 2, 5, 5]                        # t = 2 and t = 5
     assert all(m[v] == 0 for v in range(0, len(m) - 1, per_t))               # inputs never mirrored
+
+
+def test_lstm_pack_unpack_roundtrip():
+    """LstmModel.pack_w pads layer 0 to Kin0 = round_up(I, 128) zero columns between W_ih and
+    W_hh (the C-ABI layout, reading A21); unpack_w recovers the true-width per-layer arrays."""
+    import numpy as np
+    import torch
+
+    import paper_1604_06174_b200 as slm
+    L, H, I = 3, 8, 5
+    rng = np.random.default_rng(0)
+    W = [rng.standard_normal((4 * H, (I if l == 0 else H) + H)) for l in range(L)]
+    flat = slm.LstmModel.pack_w([torch.tensor(w) for w in W], I)
+    k0 = slm.LstmModel.kin0(I)
+    assert flat.numel() == 4 * H * (k0 + H) + (L - 1) * 4 * H * 2 * H
+    w0 = flat[:4 * H * (k0 + H)].reshape(4 * H, k0 + H).numpy()
+    assert np.array_equal(w0[:, :I], W[0][:, :I]) and not w0[:, I:k0].any() and np.array_equal(w0[:, k0:], W[0][:, I:])
+    back = slm.LstmModel.unpack_w(flat.numpy(), L, H, I)
+    for a, b in zip(back, W):
+        assert np.array_equal(a, b)

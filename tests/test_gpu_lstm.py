@@ -1,7 +1,9 @@
 """Device parity of the unrolled-LSTM training step (C3) through the C ABI (slm_step).
 
   * GPU vs the bf16-operand-emulating fp64 oracle (oracle.lstm.step_plain): loss and every
-    gradient within 2e-2 relative norm (reading A12).
+    gradient element by element, |g - ref| <= 2e-2 (|ref| + rms(ref)), and within 2e-2 relative
+    norm (reading A12) — including the C3 shapes (L = 4, H = 1024, I = 50, C = 5000) with the
+    bench's plan.
   * checkpointed GPU step == non-checkpointed GPU step, bit for bit, for the generic
     strategies and the time-segment plan of PAPER.md:486-490.
 """
@@ -10,6 +12,7 @@ import pytest
 import torch
 
 import synth
+from _util import assert_close
 from oracle import lstm as OL
 
 pytestmark = pytest.mark.gpu
@@ -22,9 +25,11 @@ def slm():
 
 
 def _dev(inp, L, H, C):
-    """synth.lstm_inputs (bf16-valued) -> device tensors in the slm_lstm_desc layout."""
+    """synth.lstm_inputs (bf16-valued, true widths) -> device tensors in the slm_lstm_desc layout
+    (layer 0 padded to Kin0 by the binding's LstmModel.pack_w)."""
+    import paper_1604_06174_b200 as slm
     Cp = -(-C // 128) * 128
-    W = torch.cat([torch.tensor(w).reshape(-1) for w in inp["W"]]).to(torch.bfloat16).cuda()
+    W = slm.LstmModel.pack_w(inp["W"], inp["n_in"]).to(torch.bfloat16).cuda()
     Wo = torch.zeros(Cp, H)
     Wo[:C] = torch.tensor(inp["W_o"])
     bo = torch.zeros(Cp)
@@ -53,11 +58,9 @@ def _run(slm, cfg, inp, strategy="none", m=None, alloc_flags=3, state_candidates
 
 
 def _split_w(flat, inp):
-    out, o = [], 0
-    for w in inp["W"]:
-        out.append(flat[o:o + w.size].reshape(w.shape))
-        o += w.size
-    return out
+    import paper_1604_06174_b200 as slm
+    H = inp["W"][0].shape[0] // 4
+    return slm.LstmModel.unpack_w(flat, len(inp["W"]), H, inp["n_in"])
 
 
 def _rel(a, b):
@@ -75,15 +78,42 @@ def test_lstm_vs_oracle(slm, cfg):
     loss, g, _ = _run(slm, cfg, inp, "sqrt")
     P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
     ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
-    assert abs(loss - ol) / abs(ol) <= 2e-2, (loss, ol)
+    _lstm_parity(loss, g, ol, og, inp, L, C)
+
+
+def _lstm_parity(loss, g, ol, og, inp, L, C, tag="", max_frac=0.0):
+    """loss, every W_l, b_l, W_o, b_o element by element (padded classes get no gradient)"""
+    assert abs(loss - ol) / abs(ol) <= 2e-2, (tag, loss, ol)
+    stats = {}
     for l, w in enumerate(_split_w(g["W"], inp)):
-        assert _rel(w, og["W"][l]) <= 2e-2, ("W", l, _rel(w, og["W"][l]))
-    b = g["b"]
-    for l in range(L):
-        assert _rel(b[l], og["b"][l]) <= 2e-2, ("b", l)
-    assert _rel(g["W_o"][:C], og["W_o"]) <= 2e-2, _rel(g["W_o"][:C], og["W_o"])
-    assert _rel(g["b_o"][:C], og["b_o"]) <= 2e-2
+        stats[f"W{l}"] = assert_close(w, og["W"][l], 2e-2, f"{tag} W{l}", max_frac)
+        stats[f"b{l}"] = assert_close(g["b"][l], og["b"][l], 2e-2, f"{tag} b{l}", max_frac)
+    stats["W_o"] = assert_close(g["W_o"][:C], og["W_o"], 2e-2, f"{tag} W_o", max_frac)
+    stats["b_o"] = assert_close(g["b_o"][:C], og["b_o"], 2e-2, f"{tag} b_o", max_frac)
     assert not np.any(g["W_o"][C:]) and not np.any(g["b_o"][C:])   # padded classes get no gradient
+    return stats
+
+
+@pytest.mark.slow
+def test_lstm_c3_shapes_bench_plan_vs_oracle(slm):
+    """C3's layer shapes (L = 4, H = 1024, I = 50 padded to 128, C = 5000 padded to 5120 — the head's
+    class loops run 5 times) over T = 40 steps (one 32-step weight-gradient chunk plus a ragged 8),
+    with the bench's plan: time segments, grouped allocation and recompute phases (A22, A24),
+    the layer wavefront with mirror streams (lstm_streams = 2); element-wise against the oracle,
+    all but 0.1 % of each tensor's elements (the bf16 rounding decisions of 160 dependent steps
+    drift apart at the smallest elements of W_0: 0.02 % measured, relative L2 2.2e-3)."""
+    cfg = (4, 40, 64, 1024, 50, 5000)
+    L, T, B, H, I, C = cfg
+    inp = synth.lstm_inputs(L, T, B, H, I, C, dtype="bf16", seed=40)
+    graph = slm.Graph.lstm(L, T, B, H, I)
+    af = slm.ALLOC_INPLACE | slm.ALLOC_SHARING | slm.ALLOC_GROUPED | slm.ALLOC_MIRROR_PARITY
+    m = graph.lstm_segment_mirrors(8)
+    loss, g, plan = _run(slm, cfg, inp, m=m, alloc_flags=af, lstm_streams=2)
+    assert plan.extra_forward > 0
+    P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
+    ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
+    stats = _lstm_parity(loss, g, ol, og, inp, L, C, "C3 shapes", max_frac=1e-3)
+    print("C3-shape parity (max_abs, rms_ref, rel_l2):", {k: tuple(f"{x:.2e}" for x in v) for k, v in stats.items()})
 
 
 @pytest.mark.parametrize("cfg", [(2, 8, 64, 128, 50, 300), (1, 40, 64, 128, 50, 129)])
@@ -128,10 +158,7 @@ def test_lstm_edge_sizes(slm, cfg):
     loss, g, _ = _run(slm, cfg, inp, "sqrt")
     P = OL.LstmParams(inp["W"], inp["b"], inp["W_o"], inp["b_o"], I)
     ol, og = OL.step_plain(P, inp["x"], inp["labels"], mode="bf16")
-    assert abs(loss - ol) / abs(ol) <= 2e-2
-    for l, w in enumerate(_split_w(g["W"], inp)):
-        assert _rel(w, og["W"][l]) <= 2e-2, ("W", l)
-    assert _rel(g["W_o"][:C], og["W_o"]) <= 2e-2
+    _lstm_parity(loss, g, ol, og, inp, L, C, "edge")
     loss0, g0, _ = _run(slm, cfg, inp, "none")
     assert loss0 == loss
     for k in g0:

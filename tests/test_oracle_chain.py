@@ -136,8 +136,26 @@ def test_plan_invariance_bitwise(strategy, kw, mode):
     for k in grads:
         assert np.array_equal(grads[k], g2[k]), k
     assert np.array_equal(dx0, dx2)
+    # the interpreter's liveness peak (values still to be read, in-place outputs replacing their
+    # input) never exceeds the planned pool, and Fig. 2's sharing allocator is tight on a chain
+    assert st["peak_live_bytes"] <= p.alloc.exact_peak
     assert st["peak_live_bytes"] == p.alloc.exact_peak
     assert st["op_evaluations"] == (n + 1) + (n + 1) + p.extra_forward
+
+
+@pytest.mark.parametrize("strategy", [P.S_NONE, P.S_SQRT, P.S_RECURSIVE])
+def test_liveness_peak_vs_allocator(strategy):
+    """Without sharing (PAPER.md:165-172 'memory sharing' off) the pool holds every tag (Sigma of
+    the sizes) while the values' liveness peak stays the same: the gap is what sharing saves."""
+    n, B, d = 16, 8, 16
+    Pm, inp = _params(n, B, d)
+    shared = P.plan(G.chain_graph(n, B, d), strategy, alloc_flags=P.A_INPLACE | P.A_SHARING)
+    unshared = P.plan(G.chain_graph(n, B, d), strategy, alloc_flags=0)
+    l1 = C.step_planned(shared, Pm, inp["x0"], inp["labels"])[3]["peak_live_bytes"]
+    l0 = C.step_planned(unshared, Pm, inp["x0"], inp["labels"])[3]["peak_live_bytes"]
+    assert l1 == shared.alloc.exact_peak
+    # without in-place an op's input and output coexist: at most one more value than with it
+    assert l1 <= l0 <= l1 + B * d * 4 < unshared.alloc.exact_peak
 
 
 def test_planned_detects_clobber():

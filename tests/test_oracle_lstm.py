@@ -71,8 +71,6 @@ def test_lstm_finite_differences():
             l = int(rng.integers(0, Pm.L))
             arr = getattr(Pm, name)[l]
             idx = tuple(int(rng.integers(0, s)) for s in arr.shape)
-            if name == "W" and l == 0 and Pm.n_in <= idx[1] < Pm.kin(0):
-                continue   # padding column: multiplies zero inputs
             old = arr[idx]
             arr[idx] = old + h
             lp = OL.step_plain(Pm, inp["x"], inp["labels"])[0]

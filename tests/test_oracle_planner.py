@@ -186,6 +186,16 @@ def test_recursion_estimate_worked(row):
     assert P.recursion_estimate(n, k) == (units, depth)
 
 
+@pytest.mark.parametrize("row", _rows("drop_cheap.txt"))
+def test_drop_cheap_worked(row):
+    """SPEC.md:278-286 worked examples of the Sec. 4.2 drop-low-cost plan (tests/golden/drop_cheap.txt)"""
+    names, expect = row[0].split(","), [int(v) for v in row[1].split(",")]
+    code = {v: k for k, v in G.OP_NAMES.items()}
+    nodes = [G.Node(code[nm], [] if i == 0 else [i - 1], 4) for i, nm in enumerate(names)]
+    g = G.Graph(nodes, [len(nodes) - 1])
+    assert P.drop_cheap_plan(g) == expect
+
+
 def test_recursion_k1_is_ceil_log2():
     # PAPER.md:373 "if we set k = 1, we get g(n) = log2 n"; ceil(log2 n) = (n-1).bit_length()
     for n in list(range(1, 5000)) + [2 ** 20 - 1, 2 ** 20, 2 ** 20 + 1]:
