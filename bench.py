@@ -419,6 +419,60 @@ def run_lstm(args):
         torch.distributed.destroy_process_group()
 
 
+def _comm_ceiling(n, d, world, ms, probe):
+    """SURVEY 8(e) analysis next to the measurement: per rank n d^2 bf16 weight gradients (plus
+    the fp32 b / gamma / beta vectors) are all-reduced per step; a ring moves 2 (p-1)/p of them
+    over the measured bus bandwidth.  The ceiling assumes the backward phase (~60 % of the step,
+    profiles/r2_*timeline*) hides the buckets issued before its end."""
+    grad_bytes = n * d * d * 2 + 3 * n * d * 4
+    out = dict(grad_bytes_per_rank=grad_bytes, nccl_algo=os.environ.get("NCCL_ALGO"),
+               nccl_proto=os.environ.get("NCCL_PROTO"), bucket_mib=256,
+               reduction="bf16 dW summed by NCCL in bf16 (ring: p-1 roundings, <= (p-1) 2^-9 relative); "
+                         "b/gamma/beta fp32")
+    if probe:
+        t_comm = 2 * (world - 1) / world * grad_bytes / (probe["busbw_gbs"] * 1e9) * 1e3
+        out.update(probe=probe, ring_ms=round(t_comm, 3),
+                   ceiling_ms=round(max(ms, 0.4 * ms + t_comm), 3))
+    return out
+
+
+def _spawn(n):
+    """--gpus N without a launcher: re-run this command under torchrun, one process per GPU
+    (rendezvous on 127.0.0.1), and relay rank 0's output."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def _nccl_pins():
+    """Deterministic collectives: one algorithm and protocol for every bucket, so the
+    checkpointed and non-checkpointed steps reduce in the same order at every world size."""
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
+
+
+def _busbw_probe(dist, torch, dev, world, mib=256, reps=5):
+    """all_reduce(sum) bus bandwidth at start-up (nccl-tests definition: 2 (p-1)/p * bytes / time)"""
+    t = torch.ones(mib << 19, dtype=torch.bfloat16, device=dev)
+    for _ in range(2):
+        dist.all_reduce(t)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dist.all_reduce(t)
+    e1.record()
+    torch.cuda.synchronize()
+    s = e0.elapsed_time(e1) / reps / 1e3
+    return dict(bytes=t.numel() * 2, seconds=round(s, 6), busbw_gbs=round(2 * (world - 1) / world * t.numel() * 2 / s / 1e9, 1))
+
+
 # ======================================================================= our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -452,6 +506,10 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=4, help="LSTM time steps the CPU oracle runs")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn(args.gpus)
+    if args.gpus > 1 and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.model == "lstm":
         if args.batch == 256:
             args.batch = 64
@@ -499,8 +557,11 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    probe = None
     if world > 1:
+        _nccl_pins()
         dist.init_process_group("nccl", device_id=dev)
+        probe = _busbw_probe(dist, torch, dev, world)
     n, B, d = args.layers, args.batch, args.width
     Bg = B * world
     inp = synth.chain_inputs_torch(n, B * world, d, dtype="bf16", device=dev)
@@ -724,6 +785,7 @@ def main():
                            extra_forward=plan.extra_forward),
         nockpt=nock,
         ckpt_over_nockpt_time=round(ms / nock["ms_per_step"], 4) if nock else None,
+        comm=_comm_ceiling(n, d, world, ms, probe),
     )
     print(json.dumps(line), flush=True)
     if world > 1:
