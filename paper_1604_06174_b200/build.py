@@ -54,5 +54,24 @@ def build(force=False, verbose_ptxas=False):
     return LIB
 
 
+def build_variant(name, defines):
+    """An experimental in-tree variant of the library (compile-time kernel experiments), loaded by
+    setting SLM_LIB=<name> (paper_1604_06174_b200/_lib.py); not part of the product build."""
+    os.makedirs(BUILD, exist_ok=True)
+    po = os.path.join(BUILD, "planner.o")
+    if not os.path.exists(po):
+        _run(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", *INC, "-c", os.path.join(CSRC, "planner.cpp"), "-o", po])
+    o = os.path.join(BUILD, f"runtime_{name}.o")
+    _run([NVCC, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", *ARCH, *INC, *["-D" + d for d in defines],
+          "-c", os.path.join(CSRC, "runtime.cu"), "-o", o])
+    out = os.path.join(PKG, name)
+    _run([NVCC, "-shared", *ARCH, "-o", out, po, o, "-cudart", "static", "-ldl", "-lpthread"])
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    if "--variant" in sys.argv:   # --variant NAME.so DEF1 DEF2 ...
+        i = sys.argv.index("--variant")
+        build_variant(sys.argv[i + 1], sys.argv[i + 2:])
+    else:
+        build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -32,17 +32,19 @@
 
 namespace slmk {
 
-constexpr int kBlkThreads = 256;   // 8 warps: TMA producer / MMA issuer / TMEM owner roles, then all 8 in the epilogue
+// 16 warps: TMA producer / MMA issuer / TMEM owner roles, then all 16 in the epilogue (measured: the
+// epilogue's latency-bound passes ran 1.4 us with 8 warps, two per scheduler)
+constexpr int kBlkThreads = 512;
+constexpr int kBlkNH = kBlkThreads / 128;   // warps per TMEM lane quarter (column parts of the epilogue)
 template <int B, int S, bool BWD, int BM_ = 64>
 struct BlkCfg {
   static constexpr int BM = BM_, BK = 64;     // BM = output features per CTA (the MMA's M: 64 or 128)
   static constexpr int FS = BM / S;           // features owned by a CTA after the reduce-scatter
-  static constexpr int CGR = FS / 16;         // 16-float (64-byte) column groups of a slice
   static constexpr int RG = kBlkThreads / FS; // row groups of the epilogue (threads per feature)
   static constexpr int R = B / RG;            // rows per epilogue thread (values kept in registers)
   static constexpr int A_BYTES = BM * BK * 2; // one W tile (BM x 64 bf16)
   static constexpr int B_BYTES = B * BK * 2;  // one operand tile (B x 64 bf16)
-  static constexpr int SLICE = B * FS * 4;    // one fp32 slice [CGR][B][16]
+  static constexpr int SLICE = B * FS * 4;    // one fp32 slice [B][FS] (dense rows of FS floats)
   static constexpr int AUX = SLICE;           // x_l, staged by TMA during the main loop
   static constexpr int LIMIT = 227 * 1024;
   static constexpr int STATIC = RG * FS * 4 + 64;
@@ -63,10 +65,10 @@ struct BlkCfg {
   static_assert(SMEM + STATIC <= LIMIT, "shared memory");
 };
 
-// element (column group c, row b, column f16 in 0..15) of an fp32 slice [CGR][B][16]: the dense
-// layout of a {16, rows} TMA box (64-byte rows); a warp reading 2 rows x 16 features (FS = 16)
-// touches 128 consecutive bytes
-__device__ __forceinline__ int sl_off(int B_, int c, int b, int f16) { return (c * B_ + b) * 16 + f16; }
+// An fp32 slice is [B][FS] row-major: the dense layout of a {FS, rows} TMA box.  The epilogue's
+// thread t handles feature t % FS, so a warp touches 128 consecutive bytes (one row at FS = 32,
+// two at FS = 16): no shared-memory bank conflicts (a [FS/16][B][16] layout had two-way conflicts
+// at FS = 32 and doubled the epilogue's shared-memory time, measured with ncu stall_mio).
 
 // sum of one value per (row group rg, feature fl) over the RG row groups, in the order 0..RG-1
 template <int RG, int FS>
@@ -135,20 +137,20 @@ struct BlkArgs {
 };
 
 // grid = (d/BM) * S CTAs, clusters of S along x (CTA m*S + k = K slice k of output tile m),
-// 256 threads: warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warp 2 owns the TMEM
-// allocation; then all eight warps run the epilogue.
+// kBlkThreads threads: warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warp 2 owns the TMEM
+// allocation; then all warps run the epilogue.
 //   tmA: W, K-major {64, BM} box or MN-major {64, 64} boxes
 //   tmB: the bf16 operand [B][d] (a_l fwd, bf16 dx_{l+1} bwd), {64, B} box, 128-byte swizzle
-//   tmP / tmPs: the partial buffer [d/64][S owners][S sources][CGR][B] rows of 16 fp32, {16, B} box
-//        (the owner's loads) / {16, 32} box (a warp's chunk stores)
-//   tmX: fp32 [rows][d] source of x_l, {16, B} box
+//   tmP / tmPs: the partial buffer [d/BM][S owners][S sources][B] rows of FS fp32, {FS, B} box (the
+//        owner's loads) / {FS, 32} box (the chunk stores: FS features x 32 batch rows)
+//   tmX: fp32 [rows][d] source of x_l, {FS, B} box
 template <int B, int S, bool BWD, int BM_>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     blk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmPs,
                const __grid_constant__ CUtensorMap tmX, const BlkArgs args) {
   using C = BlkCfg<B, S, BWD, BM_>;
-  constexpr int FS = C::FS, CGR = C::CGR, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB, BM = C::BM;
+  constexpr int FS = C::FS, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB, BM = C::BM;
   unsigned long long* const tsp = ts_buffer(args.dbg);
   ts_mark(tsp, 0, args.dbg);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const int f0 = m0 + (int)k * FS;   // first feature this CTA owns after the reduce-scatter
   // this thread's feature in the epilogue and its parameters, loaded now (they are constant during
   // the step) so their latency hides under the main loop
-  const int fl = threadIdx.x % FS, rg = threadIdx.x / FS, cc = fl >> 4, f16 = fl & 15;
+  const int fl = threadIdx.x % FS, rg = threadIdx.x / FS;
   const int f = f0 + fl;
   const float p_bias = BWD ? 0.f : args.bias[f];
   const float p_gam = args.gamma ? args.gamma[f] : 0.f;
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
     mbar_init(accum, 1);
     mbar_init(auxb, 1);
-    mbar_init(recvb, 2 * (S - 1) * CGR);   // one arrival per (peer warp, 16-row group) of this owner's slice
+    mbar_init(recvb, kBlkNH * (S - 1));   // one arrival per storing peer warp (one per column part)
     mbar_init(recvb2, 1);
     fence_barrier_init();
   }
@@ -244,8 +246,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     for (int kb = 0; kb < nb0; ++kb) load_b(kb);
     // the epilogue's x_l slice lands in its own buffer while the main loop runs
     mbar_expect_tx(auxb, C::AUX);
-#pragma unroll
-    for (int c = 0; c < CGR; ++c) tma_load_2d(xs + c * B * 16, &tmX, auxb, f0 + 16 * c, args.x_row0);
+    tma_load_2d(xs, &tmX, auxb, f0, args.x_row0);
     // refill each ring slot as soon as the MMAs reading it retire
     for (int kb = 0; kb < nk; ++kb) {
       if (kb + NB < nk) {
@@ -289,50 +290,49 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   tc_fence_after();
   ts_mark(tsp, 2, args.dbg);
   {
-    // 16-row groups of the tile held by this warp's TMEM lane quarter: BM = 128 -> groups 2q, 2q+1
-    // (lanes 0..15, 16..31); BM = 64 -> group q (lanes 0..15, measured layout)
-    constexpr int GPW = BM / 64;
-    const int q = warp & 3, h = warp >> 2;
-    const int grp = GPW * q + (GPW == 2 ? (lane >> 4) : 0);   // this lane's group (BM = 64: lanes < 16)
-    const bool valid = GPW == 2 || lane < 16;
+    // TMEM lane quarter q of the tile: BM = 128 -> rows 32q..32q+31 (lanes 0..31); BM = 64 -> rows
+    // 16q..16q+15 (lanes 0..15, measured layout).  A quarter's rows belong to one owner slice;
+    // QPO quarters make up a slice (2 only for BM = 64, S = 2).
+    constexpr int QR = BM / 4;                 // tile rows per quarter
+    constexpr int QPO = FS / QR;               // quarters per owner slice
+    const int q = warp & 3, h = warp >> 2;     // lane quarter, column part h of kBlkNH
+    const bool valid = QR == 32 || lane < 16;
+    const int ft = QR * q + (lane & (QR - 1)); // tile row (feature) of this lane
+    const int ko = (QR * q) / FS;              // owner slice of this quarter
+    const bool leader = (q % QPO) == 0;        // the quarter that issues the slice's stores
+    float* slot = reinterpret_cast<float*>(ring + ko * C::SLICE);
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    // 32-column chunks dealt round-robin to the kBlkNH warps of a quarter (B = 64: two warps idle)
 #pragma unroll 1
-    for (int c0 = h * (B / 2); c0 < (h + 1) * (B / 2); c0 += 32) {
+    for (int c0 = h * 32; c0 < B; c0 += 32 * kBlkNH) {
       float acc[32];
       tmem_ld32(trow + c0, acc);
       if (valid) {
-        const int ko = 16 * grp / FS, cg = (16 * grp % FS) / 16;
-        float* dst = reinterpret_cast<float*>(ring + ko * C::SLICE) + (cg * B + c0) * 16 + (lane & 15);
+        float* dst = slot + c0 * FS + ft % FS;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) dst[j * 16] = acc[j];
+        for (int j = 0; j < 32; ++j) dst[j * FS] = acc[j];
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged smem -> TMA (async proxy)
-      __syncwarp();
-      if (lane == 0) {   // a peer's rows: store each 32 x 16 chunk now (stores overlap the TMEM reads)
-#pragma unroll
-        for (int gg = 0; gg < GPW; ++gg) {
-          const int g2 = GPW * q + gg, ko = 16 * g2 / FS, cg = (16 * g2 % FS) / 16;
-          if (ko == (int)k) continue;
+      if (ko != (int)k) {   // a peer's rows: store this {FS features, 32 rows} chunk now
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged smem -> TMA (async proxy)
+        if constexpr (QPO == 2)   // both quarters of the slice have staged their halves
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + ko * kBlkNH + h) : "memory");
+        else
+          __syncwarp();
+        if (leader && lane == 0) {
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                            reinterpret_cast<uint64_t>(&tmPs)),
-                       "r"(smem_u32(reinterpret_cast<float*>(ring + ko * C::SLICE) + (cg * B + c0) * 16)), "r"(0),
-                       "r"((((m * S + ko) * S + (int)k) * CGR + cg) * B + c0)
+                       "r"(smem_u32(slot + c0 * FS)), "r"(0), "r"(((m * S + ko) * S + (int)k) * B + c0)
                        : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
-    if (lane == 0) {
+    if (ko != (int)k && leader && lane == 0) {
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // this warp's chunks are in L2
       asm volatile("fence.proxy.async.global;" ::: "memory");
-#pragma unroll
-      for (int gg = 0; gg < GPW; ++gg) {
-        const int ko = 16 * (GPW * q + gg) / FS;
-        if (ko != (int)k)
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                           cluster_map(smem_u32(recvb), (uint32_t)ko))
-                       : "memory");
-      }
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                       cluster_map(smem_u32(recvb), (uint32_t)ko))
+                   : "memory");
     }
   }
   tc_fence_before();
@@ -346,8 +346,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     for (int s = 0; s < S; ++s) {
       if (s == (int)k) continue;
 #pragma unroll
-      for (int c = 0; c < CGR; ++c)
-        tma_load_2d(ring + s * C::SLICE + c * B * 64, &tmP, recvb2, 0, (((m * S + (int)k) * S + s) * CGR + c) * B);
+      tma_load_2d(ring + s * C::SLICE, &tmP, recvb2, 0, ((m * S + (int)k) * S + s) * B);
     }
   }
 
@@ -368,7 +367,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   float xv[R], zv[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const int off = sl_off(B, cc, rg + RG * j, f16);
+    const int off = (rg + RG * j) * FS + fl;
     float z = ringf[off];
 #pragma unroll
     for (int s = 1; s < S; ++s) z = __fadd_rn(z, ringf[s * (C::SLICE / 4) + off]);
@@ -379,7 +378,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       xv[j] = __fadd_rn(xv[j], __fadd_rn(zv[j], p_bias));
+#ifndef SLM_EXP_NO_XSTORE
       args.out[(size_t)(rg + RG * j) * d + f] = xv[j];
+#endif
     }
     ts_mark(tsp, 5, args.dbg);
     if (args.gamma != nullptr) slice_act<B, S, BM>(xv, red, d, f, rg, fl, p_gam, p_bet, args.a_out);
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 }
 
 // K1: a = ReLU(BN(x)) for the first Block of a forward / mirror run (x_0, or a kept x_{s_j}),
-// with the Block epilogue's exact mapping and statistics code: grid = d / FS CTAs of 256 threads,
+// with the Block epilogue's exact mapping and statistics code: grid = d / FS CTAs of kBlkThreads,
 // x read coalesced into registers.
 template <int B, int S, int BM>
 __global__ void __launch_bounds__(kBlkThreads) bn_k1_kernel(const float* __restrict__ x,

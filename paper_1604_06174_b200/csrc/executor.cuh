@@ -149,9 +149,10 @@ slm_status make_map_f32(CUtensorMap* map, const void* base, uint64_t inner, uint
   return SLM_OK;
 }
 
-// fp32 2-D tensor [rows][inner], box {16, box_rows}, no swizzle: the Block kernel's x slices and its
-// partial-exchange buffer (blk_fused.cuh)
-slm_status make_map_f32_16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+// fp32 2-D tensor [rows][inner], box {box_inner, box_rows}, no swizzle: the Block kernel's x slices
+// and its partial-exchange buffer (blk_fused.cuh)
+slm_status make_map_f32_box(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                            uint32_t box_rows) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -159,19 +160,19 @@ slm_status make_map_f32_16(CUtensorMap* map, const void* base, uint64_t inner, u
   }
   cuuint64_t dims[2] = {inner, rows};
   cuuint64_t strides[1] = {inner * 4};
-  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (f32, 16-wide) failed: " + std::to_string((int)r));
+    set_error("cuTensorMapEncodeTiled (f32 box) failed: " + std::to_string((int)r));
     return SLM_E_CUDA;
   }
   return SLM_OK;
 }
-// rows of 16 floats in the Block kernel's partial buffer: [d/BM][S][S][CGR][B]
-uint64_t blk_prows(int B, int d, int S, int BM) { return (uint64_t)(d / BM) * S * S * (BM / S / 16) * B; }
+// rows of FS = BM / S floats in the Block kernel's partial buffer: [d/BM][S][S][B]
+uint64_t blk_prows(int B, int d, int S, int BM) { return (uint64_t)(d / BM) * S * S * B; }
 
 // Shape of the fused Block (blk_fused.cuh): BM output features per CTA (the MMA's M) and the
 // cluster split S of K; option block_cfg: 0 = default, 1 = (64, 4), 2 = (128, 4), 3 = (64, 2).
@@ -463,13 +464,14 @@ slm_status bind_maps(slm_model& m, void* ws) {
     for (int i = 0; i < 2; ++i)
       if ((st = make_map(&m.mAct[i], w + L.act[i], d, B, (uint32_t)B)) != SLM_OK) return st;
     // partial exchange: {32, B} box for the owner's loads, {32, 32} for a warp's chunk stores
-    if ((st = make_map_f32_16(&m.mPf[0], w + L.P, 16, prow, (uint32_t)B)) != SLM_OK) return st;
-    if ((st = make_map_f32_16(&m.mPf[1], w + L.P, 16, prow, 32u)) != SLM_OK) return st;
+    const uint32_t FS = (uint32_t)(sh.BM / sh.S);
+    if ((st = make_map_f32_box(&m.mPf[0], w + L.P, FS, prow, FS, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map_f32_box(&m.mPf[1], w + L.P, FS, prow, FS, 32u)) != SLM_OK) return st;
     if (m.overlap) {
       for (int i = 0; i < 2; ++i)
         if ((st = make_map(&m.mAct3[i], w + L.act3[i], d, B, (uint32_t)B)) != SLM_OK) return st;
-      if ((st = make_map_f32_16(&m.mPf3[0], w + L.P3, 16, prow, (uint32_t)B)) != SLM_OK) return st;
-      if ((st = make_map_f32_16(&m.mPf3[1], w + L.P3, 16, prow, 32u)) != SLM_OK) return st;
+      if ((st = make_map_f32_box(&m.mPf3[0], w + L.P3, FS, prow, FS, (uint32_t)B)) != SLM_OK) return st;
+      if ((st = make_map_f32_box(&m.mPf3[1], w + L.P3, FS, prow, FS, 32u)) != SLM_OK) return st;
     }
     for (int i = 0; i < kNA; ++i)
       if ((st = make_map(&m.mAb_MN[i], w + L.ab[i], d, B, 64)) != SLM_OK) return st;
@@ -547,8 +549,9 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   const uint64_t row_bytes = (uint64_t)d * 4;
   if (fz) {
     const uint64_t prows = std::max<uint64_t>((uint64_t)p->pool_bytes / row_bytes, (uint64_t)B);
-    if ((s = make_map_f32_16(&mx_pool, pool ? pool : x0, d, prows, (uint32_t)B)) != SLM_OK) return s;
-    if ((s = make_map_f32_16(&mx_x0, x0, d, (uint64_t)B, (uint32_t)B)) != SLM_OK) return s;
+    const uint32_t FS = (uint32_t)(bsh.BM / bsh.S);
+    if ((s = make_map_f32_box(&mx_pool, pool ? pool : x0, d, prows, FS, (uint32_t)B)) != SLM_OK) return s;
+    if ((s = make_map_f32_box(&mx_x0, x0, d, (uint64_t)B, FS, (uint32_t)B)) != SLM_OK) return s;
   }
   auto xsrc = [&](const float* ptr, const CUtensorMap** map, int* row) -> slm_status {
     if (ptr == (const float*)x0) {

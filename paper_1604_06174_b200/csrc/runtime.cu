@@ -509,8 +509,9 @@ slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opn
   slm_status s;
   const uint64_t prow = blk_prows(B, d, S, sh.BM);
   if ((s = make_map(&ma, W, d, d, bwd ? 64u : (uint32_t)sh.BM)) || (s = make_map(&mb, opnd, d, B, (uint32_t)B)) ||
-      (s = make_map_f32_16(&mp[0], P, 16, prow, (uint32_t)B)) || (s = make_map_f32_16(&mp[1], P, 16, prow, 32u)) ||
-      (s = make_map_f32_16(&mx, x, d, B, (uint32_t)B)))
+      (s = make_map_f32_box(&mp[0], P, (uint32_t)(sh.BM / S), prow, (uint32_t)(sh.BM / S), (uint32_t)B)) ||
+      (s = make_map_f32_box(&mp[1], P, (uint32_t)(sh.BM / S), prow, (uint32_t)(sh.BM / S), 32u)) ||
+      (s = make_map_f32_box(&mx, x, d, B, (uint32_t)(sh.BM / S), (uint32_t)B)))
     return s;
   slmk::BlkArgs a{};
   a.d = d;

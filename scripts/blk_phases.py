@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 import paper_1604_06174_b200 as slm  # noqa: E402
 
 
-def run(bwd, B, d, reps=5):
+def run(bwd, B, d, reps=5, cfg=0):
     S = 4 if d % 256 == 0 else 2
     W = (torch.randn(d, d, device="cuda") / d ** 0.5).bfloat16()
     opnd = torch.randn(B, d, device="cuda").bfloat16()
@@ -23,8 +23,11 @@ def run(bwd, B, d, reps=5):
     out = torch.empty(B, d, device="cuda")
     a, gq = torch.empty(B, d, device="cuda", dtype=torch.bfloat16), torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
     dd = [torch.empty(d, device="cuda") for _ in range(3)]
-    P = torch.empty(S * B * d, device="cuda")
-    ncta = d // 128 * S
+    P = torch.empty(4 * B * d, device="cuda")
+    BM = 128 if (B == 256 and cfg in (0, 2)) else 64
+    if cfg == 3:
+        S = 2
+    ncta = d // BM * S
     ts = torch.zeros(ncta * 8, dtype=torch.int64, device="cuda")
     p = lambda t: C.c_void_p(t.data_ptr())
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -35,18 +38,19 @@ def run(bwd, B, d, reps=5):
         # flush L2 so W comes from HBM as in the chain (8.6 GB of weights)
         torch.empty(256 << 20, dtype=torch.uint8, device="cuda").fill_(1)
         slm.check(slm.lib.slm_debug_block(bwd, B, d, p(W), p(opnd), p(x), p(g), p(vec[0]), p(vec[1]), p(vec[2]),
-                                          p(out), p(a), p(gq), p(dd[0]), p(dd[1]), p(dd[2]), p(P), 1, st))
+                                          p(out), p(a), p(gq), p(dd[0]), p(dd[1]), p(dd[2]), p(P), 1 | (cfg << 4), st))
         torch.cuda.synchronize()
         t = ts.view(ncta, 8).cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
         res.append((t - t0) / 1000.0)
     slm.check(slm.lib.slm_debug_timestamps(None))
     r = np.median(np.stack(res[1:]), axis=0)
-    print(f"{'bwd' if bwd else 'fwd'} B={B} d={d} S={S} ({ncta} CTAs): phase median / max us:",
+    print(f"{os.environ.get('SLM_LIB', 'libslm.so')} cfg={cfg} {'bwd' if bwd else 'fwd'} B={B} d={d} S={S} ({ncta} CTAs): phase median / max us:",
           " | ".join(f"{i}:{np.median(r[:, i]):.2f}/{r[:, i].max():.2f}" for i in range(8)))
 
 
 if __name__ == "__main__":
-    for B, d in ((256, 2048), (256, 512), (64, 256)):
+    cfgs = [int(c) for c in sys.argv[1:]] or [0]
+    for cfg in cfgs:
         for bwd in (0, 1):
-            run(bwd, B, d)
+            run(bwd, 256, 2048, cfg=cfg)
