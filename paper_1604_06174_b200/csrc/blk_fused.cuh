@@ -36,19 +36,24 @@ namespace slmk {
 // epilogue's latency-bound passes ran 1.4 us with 8 warps, two per scheduler)
 constexpr int kBlkThreads = 512;
 constexpr int kBlkNH = kBlkThreads / 128;   // warps per TMEM lane quarter (column parts of the epilogue)
-template <int B, int S, bool BWD, int BM_ = 64>
+template <int B, int S, bool BWD, int BM_ = 64, int CG_ = 1>
 struct BlkCfg {
   static constexpr int BM = BM_, BK = 64;     // BM = output features per CTA (the MMA's M: 64 or 128)
+  static constexpr int CG = CG_;              // 2: CTA pairs (cta_group::2, M = 256 over two SMs; each
+                                              // SM stages half of the batch columns)
   static constexpr int FS = BM / S;           // features owned by a CTA after the reduce-scatter
   static constexpr int RG = kBlkThreads / FS; // row groups of the epilogue (threads per feature)
   static constexpr int R = B / RG;            // rows per epilogue thread (values kept in registers)
   static constexpr int A_BYTES = BM * BK * 2; // one W tile (BM x 64 bf16)
-  static constexpr int B_BYTES = B * BK * 2;  // one operand tile (B x 64 bf16)
+  static constexpr int B_BYTES = B / CG * BK * 2;   // one operand tile (this CTA's B / CG rows x 64 bf16)
   static constexpr int SLICE = B * FS * 4;    // one fp32 slice [B][FS] (dense rows of FS floats)
   static constexpr int AUX = SLICE;           // x_l, staged by TMA during the main loop
   static constexpr int LIMIT = 227 * 1024;
   static constexpr int STATIC = RG * FS * 4 + 64;
-  static constexpr int NB = 3;                // operand ring (after griddepcontrol.wait, from L2)
+#ifndef SLM_BLK_NB
+#define SLM_BLK_NB 3
+#endif
+  static constexpr int NB = SLM_BLK_NB;       // operand ring (after griddepcontrol.wait, from L2)
   // W ring: as many tiles as fit (up to 8 = a 512-wide K slice): all of them are requested
   // before griddepcontrol.wait, so the weight stream from HBM overlaps the predecessor
   static constexpr int NA_FIT = (LIMIT - 1024 - AUX - 512 - STATIC - NB * B_BYTES) / A_BYTES;
@@ -59,6 +64,7 @@ struct BlkCfg {
   static constexpr int TMEM_COLS = B;
   static_assert(S == 2 || S == 4, "cluster of 2 or 4 CTAs");
   static_assert(BM == 64 || BM == 128, "M tile");
+  static_assert(CG == 1 || (CG == 2 && BM == 128), "CTA pairs with 128 rows per CTA");
   static_assert(B == 64 || B == 128 || B == 256, "batch tile");
   static_assert(FS % 16 == 0 && R >= 1 && R <= 32, "slice / registers");
   static_assert(NA >= 2, "pipeline");
@@ -122,6 +128,7 @@ __device__ __forceinline__ void slice_act(const float (&v)[BlkCfg<B, S, false, B
 struct BlkArgs {
   int d;
   int a_row0;              // row of W_l in the [n*d][d] weight tensor (= l*d)
+  int pf_row0;             // row of the next Block's W (pulled into L2 during this one), -1 none
   int x_row0;              // row of x_l in its fp32 [rows][d] tensor map
   const float* g;          // bwd: g = dx_{l+1} [B][d] fp32
   float* out;              // fwd: x_{l+1}; bwd: dx_l                   [B][d] fp32
@@ -144,12 +151,12 @@ struct BlkArgs {
 //   tmP / tmPs: the partial buffer [d/BM][S owners][S sources][B] rows of FS fp32, {FS, B} box (the
 //        owner's loads) / {FS, 32} box (the chunk stores: FS features x 32 batch rows)
 //   tmX: fp32 [rows][d] source of x_l, {FS, B} box
-template <int B, int S, bool BWD, int BM_>
+template <int B, int S, bool BWD, int BM_, int CG>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     blk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmPs,
                const __grid_constant__ CUtensorMap tmX, const BlkArgs args) {
-  using C = BlkCfg<B, S, BWD, BM_>;
+  using C = BlkCfg<B, S, BWD, BM_, CG>;
   constexpr int FS = C::FS, RG = C::RG, R = C::R, NA = C::NA, NB = C::NB, BM = C::BM;
   unsigned long long* const tsp = ts_buffer(args.dbg);
   ts_mark(tsp, 0, args.dbg);
@@ -173,8 +180,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = args.d;
-  const uint32_t k = cluster_ctarank();
-  const int m = (int)blockIdx.x / S;
+  // cluster of S * CG CTAs: rank = K slice * CG + pair half
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t k = crank / CG, p = crank % CG;
+  const bool mma_cta = p == 0;   // the pair's leader issues the MMAs (CG = 1: every CTA)
+  const int m = ((int)blockIdx.x / (S * CG)) * CG + (int)p;
   const int m0 = m * BM;
   const int nk = d / 64 / S;
   const int kbase = (int)k * nk * 64;
@@ -208,31 +218,44 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   cluster_sync();   // every CTA's barriers are initialised before a peer can arrive on them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // CG = 2: both CTAs' loads complete on the leader's full barriers (it expects both halves' bytes)
+  auto tma = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    if constexpr (CG == 2)
+      tma_load_2d_cg2(dst, map, bar, c0, c1);
+    else
+      tma_load_2d(dst, map, bar, c0, c1);
+  };
   auto load_a = [&](int kb) {
     const int s = kb % NA;
     uint8_t* sa = ring + s * C::A_BYTES;
     const int k0 = kbase + kb * 64;
-    mbar_expect_tx(&fullA[s], C::A_BYTES);
+    if (mma_cta) mbar_expect_tx(&fullA[s], CG * C::A_BYTES);
     if (BWD) {   // W stored [f_out = K][f_in = M]: 64 (M) x 64 (K) boxes
 #pragma unroll
-      for (int mm = 0; mm < BM; mm += 64) tma_load_2d(sa + mm * 128, &tmA, &fullA[s], m0 + mm, args.a_row0 + k0);
+      for (int mm = 0; mm < BM; mm += 64) tma(sa + mm * 128, &tmA, &fullA[s], m0 + mm, args.a_row0 + k0);
     } else {     // W stored [f_out = M][f_in = K]: a 64 (K) x BM (M) box
-      tma_load_2d(sa, &tmA, &fullA[s], k0, args.a_row0 + m0);
+      tma(sa, &tmA, &fullA[s], k0, args.a_row0 + m0);
     }
   };
-  auto load_b = [&](int kb) {
+  auto load_b = [&](int kb) {   // this CTA's B / CG batch rows of the operand
     const int s = kb % NB;
-    mbar_expect_tx(&fullB[s], C::B_BYTES);
-    tma_load_2d(bring + s * C::B_BYTES, &tmB, &fullB[s], kbase + kb * 64, 0);
+    if (mma_cta) mbar_expect_tx(&fullB[s], CG * C::B_BYTES);
+    tma(bring + s * C::B_BYTES, &tmB, &fullB[s], kbase + kb * 64, (int)p * (B / CG));
   };
 
   if (warp == 0 && lane == 0) {
@@ -258,12 +281,37 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         load_a(kb + NA);
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ===== MMA issuer
-    constexpr uint32_t idesc = make_idesc(BM, B, BWD, false);
+    // the next Block's weight tiles of this CTA into L2 (HBM -> L2 off the critical path: the next
+    // kernel's requests, before and after its dependency wait, then hit L2)
+    if (args.pf_row0 >= 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int k0 = kbase + kb * 64;
+        if (BWD) {
+#pragma unroll
+          for (int mm = 0; mm < BM; mm += 64) tma_prefetch_l2(&tmA, m0 + mm, args.pf_row0 + k0);
+        } else {
+          tma_prefetch_l2(&tmA, k0, args.pf_row0 + m0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && mma_cta) {
+    // ===== MMA issuer (CG = 2: the pair's leader issues M = 256 MMAs for both CTAs and multicasts
+    // its commits to the pair's barriers)
+    constexpr uint32_t idesc = make_idesc(BM * CG, B, BWD, false);
+    const uint16_t pair = (uint16_t)(3u << (2 * k));
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (CG == 2)
+        tc_commit2(bar, pair);
+      else
+        tc_commit(bar);
+    };
     for (int kb = 0; kb < nk; ++kb) {
       mbar_wait(&fullA[kb % NA], (kb / NA) & 1);
       mbar_wait(&fullB[kb % NB], (kb / NB) & 1);
+#ifdef SLM_EXP_MAINLOOP
+      if (kb == 0) ts_mark(tsp, 5, args.dbg, 32);
+      if (kb == nk - 1) ts_mark(tsp, 6, args.dbg, 32);
+#endif
       tc_fence_after();
       const uint32_t sa = smem_u32(ring + (kb % NA) * C::A_BYTES);
       const uint32_t sb = smem_u32(bring + (kb % NB) * C::B_BYTES);
@@ -271,12 +319,15 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t ad = BWD ? make_sdesc(sa + kk * 2048, 8192, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
         const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
-        tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
+        if constexpr (CG == 2)
+          tc_mma2(tmem, ad, bd, idesc, (kb | kk) != 0);
+        else
+          tc_mma(tmem, ad, bd, idesc, (kb | kk) != 0);
       }
-      tc_commit(&emptyB[kb % NB]);
-      tc_commit(&emptyA[kb % NA]);
+      commit(&emptyB[kb % NB]);
+      commit(&emptyA[kb % NA]);
     }
-    tc_commit(accum);
+    commit(accum);
   }
   __syncwarp();
 
@@ -331,14 +382,16 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // this warp's chunks are in L2
       asm volatile("fence.proxy.async.global;" ::: "memory");
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                       cluster_map(smem_u32(recvb), (uint32_t)ko))
+                       cluster_map(smem_u32(recvb), (uint32_t)ko * CG + p))
                    : "memory");
     }
   }
   tc_fence_before();
   __syncthreads();
   ts_mark(tsp, 3, args.dbg);
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  if constexpr (CG == 1) {
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
   if (threadIdx.x == 0) {
     mbar_wait(recvb, 0);   // every peer warp holding part of this owner's slice has stored it
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -382,7 +435,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       args.out[(size_t)(rg + RG * j) * d + f] = xv[j];
 #endif
     }
+#ifndef SLM_EXP_MAINLOOP
     ts_mark(tsp, 5, args.dbg);
+#endif
     if (args.gamma != nullptr) slice_act<B, S, BM>(xv, red, d, f, rg, fl, p_gam, p_bet, args.a_out);
   } else {
     float mu, rstd;
@@ -419,6 +474,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       args.dbeta[f] = S1;
       if (args.db_prev) args.db_prev[f] = S3;
     }
+  }
+  if constexpr (CG == 2) {   // both CTAs of the pair are done with the pair's TMEM allocation
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
   }
   ts_mark(tsp, 7, args.dbg);
 }

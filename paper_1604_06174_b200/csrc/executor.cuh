@@ -175,47 +175,50 @@ slm_status make_map_f32_box(CUtensorMap* map, const void* base, uint64_t inner, 
 uint64_t blk_prows(int B, int d, int S, int BM) { return (uint64_t)(d / BM) * S * S * B; }
 
 // Shape of the fused Block (blk_fused.cuh): BM output features per CTA (the MMA's M) and the
-// cluster split S of K; option block_cfg: 0 = default, 1 = (64, 4), 2 = (128, 4), 3 = (64, 2).
+// cluster split S of K; option block_cfg: 0 = default, 1 = (64, 4), 2 = (128, 4), 3 = (64, 2),
+// 4 = (128, 4) as CTA pairs (cta_group::2: clusters of 8, each SM stages half of the batch).
 // Default: (128, 4) at B = 256 (64 CTAs at d = 2048), (64, 4) below; (64, 2) when d % 256 != 0.
 // Measured at C2 (scripts/chain_timeline.py, profiles/r2_block_shapes.md): (128, 4) 29.9 ms/step,
 // (64, 2) 31.6, (64, 4) 35.1 — the 128-CTA Blocks run the forward pass faster (10.5 vs 11.4 us per
 // Block) but leave no room for the concurrent recompute and dW streams of the backward phase.
 // {0, 0} = not supported (basic lowering).
 struct BlkShape {
-  int BM, S;
+  int BM, S, CG;   // CG = 2: CTA pairs (cta_group::2), clusters of S * CG
 };
 BlkShape blk_shape(int B, int d, int cfg) {
-  if (!(B == 64 || B == 128 || B == 256) || d % 128) return {0, 0};
-  static const BlkShape tab[4] = {{128, 4}, {64, 4}, {128, 4}, {64, 2}};
-  BlkShape sh = tab[(cfg >= 0 && cfg <= 3) ? cfg : 0];
-  if (sh.BM == 128 && B != 256) sh.BM = 64;
-  if ((d / sh.S) % 64 || d % sh.BM) sh = {64, 2};   // K slice of whole 64-column blocks
-  if (d % sh.BM || (d / sh.S) % 64) return {0, 0};
+  if (!(B == 64 || B == 128 || B == 256) || d % 128) return {0, 0, 1};
+  static const BlkShape tab[5] = {{128, 4, 1}, {64, 4, 1}, {128, 4, 1}, {64, 2, 1}, {128, 4, 2}};
+  BlkShape sh = tab[(cfg >= 0 && cfg <= 4) ? cfg : 0];
+  if (sh.BM == 128 && B != 256) sh = {64, sh.S, 1};
+  if (sh.CG == 2 && (d / sh.BM) % 2) sh.CG = 1;
+  if ((d / sh.S) % 64 || d % sh.BM) sh = {64, 2, 1};   // K slice of whole 64-column blocks
+  if (d % sh.BM || (d / sh.S) % 64) return {0, 0, 1};
   return sh;
 }
 int blk_split(int B, int d) { return blk_shape(B, d, 0).S; }
 
-template <int B_, int S_, bool BWD, int BM_>
+template <int B_, int S_, bool BWD, int BM_, int CG_ = 1>
 slm_status launch_blk_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& p, const CUtensorMap& ps,
                         const CUtensorMap& x, const slmk::BlkArgs& args, cudaStream_t st, bool pdl) {
-  using C = slmk::BlkCfg<B_, S_, BWD, BM_>;
-  auto kern = slmk::blk_kernel<B_, S_, BWD, BM_>;
+  using C = slmk::BlkCfg<B_, S_, BWD, BM_, CG_>;
+  auto kern = slmk::blk_kernel<B_, S_, BWD, BM_, CG_>;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  CK(launch_kc(kern, dim3(args.d / BM_ * S_), dim3(slmk::kBlkThreads), C::SMEM, st, pdl, S_, a, b, p, ps, x, args));
+  CK(launch_kc(kern, dim3(args.d / BM_ * S_), dim3(slmk::kBlkThreads), C::SMEM, st, pdl, S_ * CG_, a, b, p, ps, x,
+               args));
   return SLM_OK;
 }
 slm_status launch_blk(int B, BlkShape sh, bool bwd, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap* p,
                       const CUtensorMap& x, const slmk::BlkArgs& args, cudaStream_t st, bool pdl) {
-#define SLM_BLK(B_, S_, BM_)                                                               \
-  if (B == B_ && sh.S == S_ && sh.BM == BM_)                                               \
-    return bwd ? launch_blk_t<B_, S_, true, BM_>(a, b, p[0], p[1], x, args, st, pdl)       \
-               : launch_blk_t<B_, S_, false, BM_>(a, b, p[0], p[1], x, args, st, pdl);
-  SLM_BLK(64, 2, 64) SLM_BLK(64, 4, 64) SLM_BLK(128, 2, 64) SLM_BLK(128, 4, 64) SLM_BLK(256, 2, 64)
-  SLM_BLK(256, 4, 64) SLM_BLK(256, 4, 128)
+#define SLM_BLK(B_, S_, BM_, CG_)                                                              \
+  if (B == B_ && sh.S == S_ && sh.BM == BM_ && sh.CG == CG_)                                   \
+    return bwd ? launch_blk_t<B_, S_, true, BM_, CG_>(a, b, p[0], p[1], x, args, st, pdl)      \
+               : launch_blk_t<B_, S_, false, BM_, CG_>(a, b, p[0], p[1], x, args, st, pdl);
+  SLM_BLK(64, 2, 64, 1) SLM_BLK(64, 4, 64, 1) SLM_BLK(128, 2, 64, 1) SLM_BLK(128, 4, 64, 1) SLM_BLK(256, 2, 64, 1)
+  SLM_BLK(256, 4, 64, 1) SLM_BLK(256, 4, 128, 1) SLM_BLK(256, 4, 128, 2)
 #undef SLM_BLK
   set_error("unsupported fused Block configuration");
   return SLM_E_UNSUPPORTED;
@@ -460,16 +463,17 @@ slm_status bind_maps(slm_model& m, void* ws) {
     const BlkShape sh = blk_shape((int)B, (int)d, m.block_cfg);
     const uint64_t prow = blk_prows((int)B, (int)d, sh.S, sh.BM);
     if ((st = make_map(&m.mW_K64, m.d.W, d, n * d, (uint32_t)sh.BM)) != SLM_OK) return st;
+    const uint32_t brows = (uint32_t)(B / sh.CG);   // K-major operand box rows: this CTA's batch rows
     if ((st = make_map_bf16_store(&m.mdW_st, m.d.dW, d, n * d)) != SLM_OK) return st;
     for (int i = 0; i < 2; ++i)
-      if ((st = make_map(&m.mAct[i], w + L.act[i], d, B, (uint32_t)B)) != SLM_OK) return st;
+      if ((st = make_map(&m.mAct[i], w + L.act[i], d, B, brows)) != SLM_OK) return st;
     // partial exchange: {32, B} box for the owner's loads, {32, 32} for a warp's chunk stores
     const uint32_t FS = (uint32_t)(sh.BM / sh.S);
     if ((st = make_map_f32_box(&m.mPf[0], w + L.P, FS, prow, FS, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map_f32_box(&m.mPf[1], w + L.P, FS, prow, FS, 32u)) != SLM_OK) return st;
     if (m.overlap) {
       for (int i = 0; i < 2; ++i)
-        if ((st = make_map(&m.mAct3[i], w + L.act3[i], d, B, (uint32_t)B)) != SLM_OK) return st;
+        if ((st = make_map(&m.mAct3[i], w + L.act3[i], d, B, brows)) != SLM_OK) return st;
       if ((st = make_map_f32_box(&m.mPf3[0], w + L.P3, FS, prow, FS, (uint32_t)B)) != SLM_OK) return st;
       if ((st = make_map_f32_box(&m.mPf3[1], w + L.P3, FS, prow, FS, 32u)) != SLM_OK) return st;
     }
@@ -479,8 +483,9 @@ slm_status bind_maps(slm_model& m, void* ws) {
     if ((st = make_map(&m.mA_K, w + L.a, d, B, (uint32_t)m.bn_fwd)) != SLM_OK) return st;
     if ((st = make_map(&m.mA_MN, w + L.a, d, B, 64)) != SLM_OK) return st;
   }
+  const uint32_t grows = fz ? (uint32_t)(B / blk_shape((int)B, (int)d, m.block_cfg).CG) : (uint32_t)m.bn_dx;
   for (int i = 0; i < kNG; ++i) {
-    if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, fz ? (uint32_t)B : (uint32_t)m.bn_dx)) != SLM_OK) return st;
+    if ((st = make_map(&m.mG_K[i], w + L.gq[i], d, B, grows)) != SLM_OK) return st;
     if ((st = make_map(&m.mG_MN[i], w + L.gq[i], d, B, 64)) != SLM_OK) return st;
   }
   m.maps_ws = ws;
@@ -509,7 +514,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   const bool bf16 = m.d.dtype == SLM_BF16;
   const bool tc = tc_ok(m);
   const bool fz = fused_ok(m);
-  const BlkShape bsh = fz ? blk_shape(B, d, m.block_cfg) : BlkShape{0, 0};
+  const BlkShape bsh = fz ? blk_shape(B, d, m.block_cfg) : BlkShape{0, 0, 1};
   const int Bg = m.d.batch_global > 0 ? m.d.batch_global : B;
   const float inv_bg = 1.0f / (float)Bg;
   const WsLayout L = ws_layout(m);
@@ -717,6 +722,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         BlkArgs a{};
         a.d = d;
         a.a_row0 = l * d;
+        a.pf_row0 = l + 1 < n ? (l + 1) * d : -1;
         a.x_row0 = xrow;
         a.out = xout;
         a.bias = bvec + (size_t)l * d;
@@ -795,6 +801,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
         BlkArgs a{};
         a.d = d;
         a.a_row0 = l * d;
+        a.pf_row0 = l > 0 ? (l - 1) * d : -1;
         a.x_row0 = xrow;
         a.g = g;
         a.out = dxl;

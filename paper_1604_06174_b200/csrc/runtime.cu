@@ -508,13 +508,15 @@ slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opn
   CUtensorMap ma, mb, mp[2], mx;
   slm_status s;
   const uint64_t prow = blk_prows(B, d, S, sh.BM);
-  if ((s = make_map(&ma, W, d, d, bwd ? 64u : (uint32_t)sh.BM)) || (s = make_map(&mb, opnd, d, B, (uint32_t)B)) ||
+  if ((s = make_map(&ma, W, d, d, bwd ? 64u : (uint32_t)sh.BM)) ||
+      (s = make_map(&mb, opnd, d, B, (uint32_t)(B / sh.CG))) ||
       (s = make_map_f32_box(&mp[0], P, (uint32_t)(sh.BM / S), prow, (uint32_t)(sh.BM / S), (uint32_t)B)) ||
       (s = make_map_f32_box(&mp[1], P, (uint32_t)(sh.BM / S), prow, (uint32_t)(sh.BM / S), 32u)) ||
       (s = make_map_f32_box(&mx, x, d, B, (uint32_t)(sh.BM / S), (uint32_t)B)))
     return s;
   slmk::BlkArgs a{};
   a.d = d;
+  a.pf_row0 = -1;
   a.g = g;
   a.out = out;
   a.bias = bias;

@@ -333,8 +333,8 @@ __device__ unsigned long long* g_slm_ts = nullptr;
 // (dbg != 0), so production launches issue no memory access for their instrumentation
 __device__ __forceinline__ unsigned long long* ts_buffer(int dbg) { return dbg ? g_slm_ts : nullptr; }
 // dbg bit 4 (16): phase mode of the step profile, all 8 phases of every CTA at [slot][1024 CTAs][8]
-__device__ __forceinline__ void ts_mark(unsigned long long* p, int phase, int dbg) {
-  if (p != nullptr && threadIdx.x == 0) {
+__device__ __forceinline__ void ts_mark(unsigned long long* p, int phase, int dbg, int tid = 0) {
+  if (p != nullptr && threadIdx.x == tid) {
     const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     const int slot = (dbg >> 8) - 1;
     if (slot < 0 && !(dbg & 4)) return;   // per-CTA phase mode only from the debug hook (bit 2)

@@ -24,7 +24,7 @@ def run(bwd, B, d, reps=5, cfg=0):
     a, gq = torch.empty(B, d, device="cuda", dtype=torch.bfloat16), torch.empty(B, d, device="cuda", dtype=torch.bfloat16)
     dd = [torch.empty(d, device="cuda") for _ in range(3)]
     P = torch.empty(4 * B * d, device="cuda")
-    BM = 128 if (B == 256 and cfg in (0, 2)) else 64
+    BM = 128 if (B == 256 and cfg in (0, 2, 4)) else 64
     if cfg == 3:
         S = 2
     ncta = d // BM * S

@@ -22,9 +22,9 @@ from oracle import chain as OC
 pytestmark = pytest.mark.gpu
 
 # (B, d, block_cfg): the default shape (BM, S) = (64, 4) at d % 256 == 0, (64, 2) at d = 128 / 384 / 640;
-# at B = 256 also (128, 4) (cfg 2) and (64, 2) (cfg 3)
+# at B = 256 also (128, 4) (cfg 2), (64, 2) (cfg 3) and (128, 4) as CTA pairs (cfg 4)
 CASES = [(64, 256, 0), (64, 128, 0), (128, 384, 0), (128, 512, 0), (256, 512, 0), (256, 640, 0), (256, 2048, 0),
-         (256, 512, 2), (256, 2048, 2), (256, 2048, 3)]
+         (256, 512, 2), (256, 2048, 2), (256, 2048, 3), (256, 512, 4), (256, 2048, 4)]
 
 
 @pytest.fixture(scope="module")
@@ -137,5 +137,20 @@ def test_block_deterministic(slm):
     for bwd in (0, 1):
         args = (P.W[0], OC.bf16_round(g) if bwd else a, x, g, P.b[0], P.gamma[bwd ^ 1], P.beta[bwd ^ 1])
         r1, r2 = _launch(slm, bwd, B, d, *args), _launch(slm, bwd, B, d, *args)
-        for k in r1:
+        for k in (("out", "a", "gq", "dgamma", "dbeta", "db") if bwd else ("out", "a")):
             assert np.array_equal(r1[k], r2[k]), (bwd, k)
+
+
+def test_cta_pairs_same_bits_as_single_cta(slm):
+    """block_cfg 4 (cta_group::2 pairs, M = 256 over two SMs) and 2 (one CTA per 128 rows) have the
+    same K split and accumulation order per element, so they produce the same bits — the property
+    that lets a forward pass and its mirrors run with either shape."""
+    B, d = 256, 1024
+    P, x, g = _inputs(B, d, 5)
+    u, _ = _u(x, P.gamma[0], P.beta[0])
+    a = OC.bf16_round(np.maximum(u, 0.0))
+    for bwd in (0, 1):
+        args = (P.W[0], OC.bf16_round(g) if bwd else a, x, g, P.b[0], P.gamma[bwd ^ 1], P.beta[bwd ^ 1])
+        r2, r4 = _launch(slm, bwd, B, d, *args, cfg=2), _launch(slm, bwd, B, d, *args, cfg=4)
+        for k in (("out", "a", "gq", "dgamma", "dbeta", "db") if bwd else ("out", "a")):
+            assert np.array_equal(r2[k], r4[k]), (bwd, k)
