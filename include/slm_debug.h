@@ -39,6 +39,9 @@ slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opn
                            const float* bias, const float* gamma, const float* beta, float* out, void* a_out,
                            void* gq_out, float* dgamma, float* dbeta, float* db_prev, void* P, int dbg,
                            void* stream);
+/* slm_debug_plan_alias makes `node` of the plan's G' write into the pool tag of `onto` (test hook:
+ * a deliberately clobbering plan, for the poison option of slm_model_set_option). */
+slm_status slm_debug_plan_alias(slm_plan* p, int32_t node, int32_t onto);
 /* Per-CTA %globaltimer stamps (8 per CTA, phases of tc_gemm_kernel) written to dev_buf
  * (uint64, >= 8 * CTAs of the next launches); NULL switches the instrumentation off. */
 slm_status slm_debug_timestamps(void* dev_buf);

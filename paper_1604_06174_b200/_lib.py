@@ -117,5 +117,6 @@ def check(code, where=""):
 _sig("slm_model_kernel_times", i32, vp, f32p, i64p, i32, i32)
 K_KINDS = ["bn_act", "gemm_fwd", "gemm_dx", "gemm_dw", "bn_bwd", "ce"]
 _sig("slm_debug_timestamps", i32, vp)
+_sig("slm_debug_plan_alias", i32, vp, i32, i32)
 _sig("slm_debug_block", i32, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
      C.c_int, vp)

@@ -254,6 +254,7 @@ struct Op {
   int out_tag;
   int in_node;   // fwd block: the node whose value is x_l
   int node;      // this node of G'
+  int aux_node = -1;   // bwd block: the node whose value is g (in_node then holds x_l's node)
 };
 
 // CUDA-graph cache key: the plan's process-unique id (never reused, unlike its address), the
@@ -311,6 +312,7 @@ struct slm_model {
   int fused = 1;          // fused lowering (one Block kernel per node, blk_fused.cuh)
   int dw_stream = 1;      // dW GEMMs on a second stream
   int bn_fwd = 64, bn_dx = 64, bn_dw = 256;   // N tiles of the basic lowering's GEMMs (bn_dw: also the fused dW)
+  int poison = 0;         // debug: fill a pool tag with NaN once its value is dead (sequential schedule)
   int block_cfg = 0;      // fused Block shape (blk_shape: 0 default, 1..4 explicit (BM, S))
   int overlap = 1;        // segment recompute on its own stream, concurrent with the backward of
                           // the next segment, when the plan allows it (SLM_ALLOC_MIRROR_PARITY)
@@ -439,7 +441,7 @@ slm_status lower(const slm_plan* p, std::vector<Op>* ops) {
         ops->push_back({2, n, p->node_tag[pr[0]], -1, p->node_tag[v], pr[0], v});
       } else if (op == SLM_OP_BLOCK) {
         if (npr != 2) return SLM_E_UNSUPPORTED;
-        ops->push_back({3, orig - 1, p->node_tag[pr[0]], p->node_tag[pr[1]], p->node_tag[v], pr[1], v});
+        ops->push_back({3, orig - 1, p->node_tag[pr[0]], p->node_tag[pr[1]], p->node_tag[v], pr[1], v, pr[0]});
       } else {
         set_error("unsupported gradient op in chain plan");
         return SLM_E_UNSUPPORTED;
@@ -644,7 +646,7 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   std::vector<char> is_m(ops.size(), 0);
   bool ov = false;
   int n_runs = 0;
-  if (fz && side && m.overlap && m.s3) {
+  if (fz && side && m.overlap && m.s3 && !m.poison) {
     size_t i = 0;
     auto mir = [&](size_t k) { return ops[k].type == 0 && p->kind[ops[k].node] == SLM_KIND_MIRROR; };
     while (i < ops.size() && !mir(i)) ++i;
@@ -688,7 +690,33 @@ slm_status enqueue(const slm_plan* p, slm_model& m, const void* x0, const int32_
   bf* act_ptr[2][2] = {{(bf*)(w + L.act[0]), (bf*)(w + L.act[1])}, {(bf*)(w + L.act3[0]), (bf*)(w + L.act3[1])}};
   int abuf_node = -1;   // basic lowering: node whose operand is resident in abuf
 
+  // debug option poison ("ad hoc application ... can lead to errors"): after the op
+  // that reads a value for the last time in V', its pool tag is filled with NaN (0xFF bytes), so
+  // a plan that lets a later op read a recycled slot it should not see produces NaN instead of
+  // silently wrong numbers.  Runs with the sequential schedule (one stream).
+  std::vector<int> last_read;
+  if (m.poison) {
+    last_read.assign(p->kind.size(), -1);
+    for (size_t i = 0; i < ops.size(); ++i) {
+      last_read[ops[i].in_node] = (int)i;
+      if (ops[i].aux_node >= 0) last_read[ops[i].aux_node] = (int)i;
+    }
+  }
+  auto poison_after = [&](size_t oi) -> slm_status {
+    if (!m.poison) return SLM_OK;
+    const Op& o = ops[oi];
+    for (int v : {o.in_node, o.aux_node}) {
+      if (v < 0 || last_read[v] != (int)oi) continue;
+      const int t = p->node_tag[v];
+      if (t < 0 || p->tag_offset[t] < 0 || t == o.out_tag) continue;   // caller buffer or overwritten in place
+      CK(cudaMemsetAsync((uint8_t*)pool + p->tag_offset[t], 0xFF, (size_t)p->tag_size[t], st));
+      ++nl;
+    }
+    return SLM_OK;
+  };
+
   for (size_t oi = 0; oi < ops.size(); ++oi) {
+    if (oi > 0 && (s = poison_after(oi - 1)) != SLM_OK) return s;
     const Op& o = ops[oi];
     const int l = o.layer;
     if (ov && run_of[oi] >= 0 && (oi == 0 || run_of[oi - 1] != run_of[oi] || is_m[oi - 1] != is_m[oi])) {

@@ -203,6 +203,7 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "fused") m->fused = (int)value;
   else if (k == "overlap") m->overlap = (int)value;
   else if (k == "block_cfg") m->block_cfg = (int)value;
+  else if (k == "poison") m->poison = (int)value;
   else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
@@ -529,6 +530,23 @@ slm_status slm_debug_block(int bwd, int B, int d, const void* W, const void* opn
   a.db_prev = db_prev;
   a.dbg = (dbg & 1) ? 4 : 0;
   return launch_blk(B, sh, bwd != 0, ma, mb, mp, mx, a, (cudaStream_t)stream, false);
+}
+
+// slm_debug_plan_alias: make `node` write into `onto`'s tag (a deliberately clobbering plan for the
+// poison test); declared in include/slm_debug.h.
+slm_status slm_debug_plan_alias(slm_plan* p, int32_t node, int32_t onto) {
+  if (!p || node < 0 || onto < 0 || node >= (int)p->node_tag.size() || onto >= (int)p->node_tag.size()) {
+    set_error("slm_debug_plan_alias: bad node");
+    return SLM_E_ARG;
+  }
+  const int t = p->node_tag[onto];
+  if (t < 0 || p->node_tag[node] < 0 || p->tag_size[t] < p->tag_size[p->node_tag[node]]) {
+    set_error("slm_debug_plan_alias: nodes not in V' or tag too small");
+    return SLM_E_ARG;
+  }
+  p->node_tag[node] = t;
+  p->uid |= 1ull << 63;   // never matches a captured graph of the intact plan
+  return SLM_OK;
 }
 
 // slm_debug_gemm: one GEMM of the three kinds through the chosen implementation

@@ -352,3 +352,36 @@ def test_overlap_soundness_check_other_plans(slm, strategy, kw):
                 assert np.array_equal(g[k].float().cpu().numpy().astype(np.float64), ref[k]), (n, strategy, k)
         if n == 2:
             assert model.get_option("last_overlap") == 0
+
+
+def test_poison_turns_a_clobbering_plan_into_nan(slm):
+    """Debug option poison: every pool tag is filled with NaN once its value is
+    dead.  On an intact plan nothing changes (the step's bits equal the plain run's); on a plan
+    corrupted through slm_debug_plan_alias (the first gradient node written into x_1's slot, which
+    Block_1's backward still reads) the silent corruption becomes NaN."""
+    n, B, d = 6, 64, 256
+    inp = synth.chain_inputs(n, B, d, dtype="bf16", seed=2)
+    ref_loss, ref, _ = _run(slm, n, B, d, "bf16", "none", inp)
+    for strategy in ("none", "sqrt"):
+        loss_p, gp, _ = _run(slm, n, B, d, "bf16", strategy, inp, poison=1)
+        assert loss_p == ref_loss, strategy
+        for k in ref:
+            assert np.array_equal(gp[k], ref[k]), (strategy, k)
+
+    def corrupted(poison):
+        p, g, x0, y = _dev(inp, "bf16")
+        model = slm.ChainModel(p, g, dtype="bf16", batch=B, poison=poison)
+        plan = slm.Plan(slm.Graph.chain(n, B, d), "none")
+        nodes = plan.nodes
+        x1 = next(i for i, nd in enumerate(nodes) if nd["kind"] == 0 and nd["op"] == slm.OP["block"] and nd["orig"] == 1)
+        gn = next(i for i, nd in enumerate(nodes) if nd["kind"] == 2 and nd["op"] == slm.OP["block"] and nd["orig"] == n)
+        slm.check(slm.lib.slm_debug_plan_alias(plan._h, gn, x1), "slm_debug_plan_alias")
+        loss = model.step(plan, x0, y)
+        torch.cuda.synchronize()
+        return float(loss.item()), {k: v.float().cpu().numpy() for k, v in g.items()}
+
+    _, g0 = corrupted(0)
+    assert all(np.isfinite(g0[k]).all() for k in g0)                       # silent ...
+    assert not all(np.array_equal(g0[k], ref[k].astype(np.float32)) for k in g0)   # ... but wrong
+    _, g1 = corrupted(1)
+    assert np.isnan(g1["W"][0]).any() and np.isnan(g1["gamma"][0]).any()   # poisoned: NaN reaches layer 0
