@@ -275,8 +275,12 @@ struct GraphKey {
 struct LstmMaps {
   // per layer: W_l K-major / MN-major, forward operand [B][K_l], the time-chunk rings of the
   // backward operands (op K-major/MN-major, d_pre K-major/MN-major), the dX partials
-  std::vector<CUtensorMap> wK, wK32, wMN, opK, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
-  CUtensorMap woK, woMN, hopRK, hopRMN, dlRK, dlRMN, pL, pH, hfK[2][2], hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
+  std::vector<CUtensorMap> wK, wK32, wMN, opRK, opRMN, dpRK, dpRMN, pX, pG, pGm, pXd;   // partials of layer l's streams
+  CUtensorMap woK, woMN, hopRK, hopRMN, dlRK, dlRMN, pL, pH, hopRKb[3], dlRKb[3], pHB;            // pL / pH over the head's
+  // per forward lane (lstm_run.cuh): hx [2B][H] (box 64 x B), X [kRunMax B][4H] f32 (box 32 x 64),
+  // the chunk ring [2 CH B][H] and the packed operand [kRunMax B][Kin] as GEMM B operands (box
+  // rows 64 / 256)
+  std::vector<CUtensorMap> hxM, xpM, ringM[2], xopM[2];
   const void* ws = nullptr;
 };
 struct slm_lstm_state {
@@ -317,10 +321,11 @@ struct slm_model {
   int overlap = 1;        // segment recompute on its own stream, concurrent with the backward of
                           // the next segment, when the plan allows it (SLM_ALLOC_MIRROR_PARITY)
   int lstm_streams = 2;   // LSTM: layer wavefront over L+1 streams (2: + L mirror streams)
-  int lstm_grid = 1;      // LSTM element-wise grids sized to the work
   int lstm_sk = 1;        // LSTM: split-K of the gates GEMMs (0 = auto; 1 measured best with the wavefront)
-  int lstm_fuse_cell = 0; // LSTM: gates + cell in the GEMM epilogue (needs lstm_sk = 1; measured slower)
   int lstm_skx = 4;       // LSTM: split-K of the dX GEMMs (0 = auto; 4 measured best with the wavefront)
+  int lstm_fuse_runs = 1; // LSTM: forward / recompute phases as chunk x layer runs (0: node by node in V' order)
+  void* lstm_run_ts = nullptr;   // debug: per-step device clock of CTA 0 of the first runs ([run][kRunMax][4] u64)
+  int lstm_run_ts_n = 0;
   // tensor maps bound to the current workspace / weights
   const void* maps_ws = nullptr;
   int maps_key = -1;

@@ -8,12 +8,26 @@
 //   Sum      loss   scalar  (caller buffer)
 // and one gradient node per non-Input node holding d(inputs) concatenated in pred order (A17).
 //
-// Lowering:
-//   gates (fwd/mirror)  pack [x | h] bf16 -> tcgen05 GEMM, split-K fp32 partials (N = B = 64
-//                       would leave 32 of 148 SMs busy) -> lstm_gates_cell_kernel (partials +
-//                       bias + activations -> G; fused with the cell S when S^l_t is the next
-//                       node of V', which it is in forward and recompute order)
-//   head  (fwd)         pack h -> logits GEMM (split-K) -> softmax-CE rows -> row sum
+// Forward / re-computed (mirror) gates + cell nodes run as RUNS of up to
+// kRunMax consecutive steps of one layer (lstm_run.cuh): the input projection of the run as one
+// batched GEMM (N = n B), then ONE persistent launch for the n steps of the recurrence with the
+// gates and the cell fused into its epilogue.  A run's recurrent state (bf16 h, fp32 c) stays in
+// per-(layer, kind) side buffers, so consecutive runs of a layer continue without touching the
+// pool; the bf16 h of every step also lands in the layer's chunk ring, which the next layer's
+// input projection and the head read.  Only values some other unit reads through the pool are
+// written to their tags ("materialised": kept checkpoints, mirrors, anything a gradient node
+// reads); the dropped forward values of a segment never leave the chip.
+//
+// Scheduling: V' is split into phases (maximal ranges without gradient nodes).  In a phase whose
+// gates/cell nodes all come in (G, S) pairs, the runs are issued chunk by chunk, layer by layer
+// (a legal topological reorder of V': every value is produced before it is read, and the phase
+// writes each of its tags once -- checked, else the phase runs node by node in V' order with runs
+// of one step; both give the same bits).  Across streams, happens-before edges come from
+// per-resource last-writer / reader tracking (option lstm_streams).
+//
+// The backward:
+//   head  (fwd)         batched per 32-step chunk: logits GEMM over the chunk's ring rows ->
+//                       softmax-CE rows -> per-step losses
 //   grad head           pack h -> logits GEMM -> CE + dlogits -> dh GEMM (split-K) -> (dh | 0)
 //   grad cell           sum of successor slices -> d(acts) | (0 | dc_prev)
 //   grad gates          d_pre (+ db) -> dX GEMM (split-K) -> scatter into d(inputs)
@@ -21,17 +35,20 @@
 //                       steps; once per chunk (in time order, independent of the plan)
 //                       dW_l += opᵀ d_pre runs as ONE GEMM with K = B * CH (PAPER.md:488-489
 //                       "in-place accumulation"), instead of CH GEMMs with K = B.
-// Re-computed (mirror) nodes run the same kernels with the same configuration and every
-// reduction has a fixed order, so the checkpointed step is bit-identical to the plain one.
+// Every reduction has a fixed order, so the checkpointed step is bit-identical to the plain one.
 
 namespace {
 
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
 struct LstmWs {
-  size_t logits, dlog_f, rowloss, offs, cnt, hopR, dlR, hf, logitsF, rowlossF, dhR, PH, total;
+  size_t logits, dlog_f, rowloss, offs, cnt, hopR, dlR, logitsF, rowlossF, dhR, PH, bar, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
-  std::vector<size_t> opL, opR, dpR, dpF, PX;   // per layer: forward operand, backward rings, dX partials
+  std::vector<size_t> opR, dpR, dpF, PX;     // per layer: backward rings, dX partials
+  // per lane (layer l, kind k: lane l + L k) of the forward runs: recurrent state hx [2][B][H]
+  // bf16 and c [B][H] fp32, the chunk ring [2][CH B][H] bf16 of h, the packed input-projection
+  // operand [kRunMax B][Kin] bf16 and the projection X [kRunMax B][4H] fp32
+  std::vector<size_t> hx, cst, ring, xop, xp;
 };
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
@@ -98,15 +115,22 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
   L.offs = off;     off += al(T * 4);   // per-step losses (loss_t)
   L.cnt = off;      off += 256;
   L.hopR = off;     off += al(CH * B * H * 2);
-  L.hf = off;       off += 2 * al(CH * B * H * 2);   // forward head operands, chunk-parity double buffer
   L.logitsF = off;  off += al(CH * B * Cp * 4);
   L.rowlossF = off; off += al(CH * B * 4);
   L.dhR = off;      off += 2 * al(CH * B * 2 * H * 4);          // (dh | 0) of batched head steps, chunk parity
   L.PH = off;       off += al((size_t)sp.hd * CH * B * H * 4);  // split-K partials of the batched dh GEMM
   L.dlR = off;      off += al(CH * B * Cp * 2);
+  L.bar = off;      off += al(2 * d.n_layers * 4);
+  const size_t RM = slmk::kRunMax;
+  for (int ln = 0; ln < 2 * d.n_layers; ++ln) {
+    const size_t kin = (ln % d.n_layers) == 0 ? (size_t)lstm_kin0(d.n_in) : H;
+    L.hx.push_back(off);   off += al(2 * B * H * 2);
+    L.cst.push_back(off);  off += al(B * H * 4);
+    L.ring.push_back(off); off += al(2 * CH * B * H * 2);
+    L.xop.push_back(off);  off += al(RM * B * kin * 2);
+    L.xp.push_back(off);   off += al(RM * B * 4 * H * 4);
+  }
   for (int l = 0; l < d.n_layers; ++l) {
-    L.opL.push_back(off);
-    off += 2 * al(B * lstm_K(d, l) * 2);   // time-parity double buffer
     L.opR.push_back(off);
     off += al(CH * B * lstm_K(d, l) * 2);
     L.dpR.push_back(off);
@@ -136,7 +160,6 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   M.wK.resize(nl);
   M.wMN.resize(nl);
   M.wK32.resize(nl);
-  M.opK.resize(2 * nl);
   M.opRMN.resize(nl);
   M.dpRK.resize(nl);
   M.dpRMN.resize(nl);
@@ -151,10 +174,6 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
     if ((st = make_map(&M.wK[l], W + lstm_w_offset(d, l), K, 4 * H, 128)) != SLM_OK) return st;
     if ((st = make_map(&M.wK32[l], W + lstm_w_offset(d, l), K, 4 * H, 32)) != SLM_OK) return st;
     if ((st = make_map(&M.wMN[l], W + lstm_w_offset(d, l), K, 4 * H, 64)) != SLM_OK) return st;
-    for (int par = 0; par < 2; ++par)
-      if ((st = make_map(&M.opK[2 * l + par], w + L.opL[l] + par * ((B * K * 2 + 255) / 256 * 256), K, B,
-                         (uint32_t)B)) != SLM_OK)
-        return st;
     if ((st = make_map(&M.opRK[l], w + L.opR[l], K, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
@@ -173,11 +192,22 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   if ((st = make_map(&M.woK, d.W_o, H, Cp, 128)) != SLM_OK) return st;
   if ((st = make_map(&M.woMN, d.W_o, H, Cp, 64)) != SLM_OK) return st;
   if ((st = make_map(&M.hopRK, w + L.hopR, H, CH * B, (uint32_t)B)) != SLM_OK) return st;
-  for (int par = 0; par < 2; ++par)
-    for (int bi = 0; bi < 2; ++bi)
-      if ((st = make_map(&M.hfK[par][bi], w + L.hf + par * ((CH * B * H * 2 + 255) / 256 * 256), H, CH * B,
-                         bi ? 256u : 64u)) != SLM_OK)
-        return st;
+  const uint64_t RM = slmk::kRunMax;
+  M.hxM.resize(2 * nl);
+  M.xpM.resize(2 * nl);
+  for (int bi = 0; bi < 2; ++bi) {
+    M.ringM[bi].resize(2 * nl);
+    M.xopM[bi].resize(2 * nl);
+  }
+  for (int ln = 0; ln < 2 * nl; ++ln) {
+    const uint64_t kin = (ln % nl) == 0 ? (uint64_t)lstm_kin0(d.n_in) : H;
+    if ((st = make_map(&M.hxM[ln], w + L.hx[ln], H, 2 * B, (uint32_t)B)) != SLM_OK) return st;
+    if ((st = make_map_f32_box(&M.xpM[ln], w + L.xp[ln], 4 * H, RM * B, 32, 64)) != SLM_OK) return st;
+    for (int bi = 0; bi < 2; ++bi) {
+      if ((st = make_map(&M.ringM[bi][ln], w + L.ring[ln], H, 2 * CH * B, bi ? 256u : 64u)) != SLM_OK) return st;
+      if ((st = make_map(&M.xopM[bi][ln], w + L.xop[ln], kin, RM * B, bi ? 256u : 64u)) != SLM_OK) return st;
+    }
+  }
   for (int bi = 0; bi < 3; ++bi) {   // batched head backward: N tiles 64 / 128 / 256
     if ((st = make_map(&M.hopRKb[bi], w + L.hopR, H, CH * B, 64u << bi)) != SLM_OK) return st;
     if ((st = make_map(&M.dlRKb[bi], w + L.dlR, Cp, CH * B, 64u << bi)) != SLM_OK) return st;
@@ -196,51 +226,271 @@ struct LstmNode {
   int t, l;     // time, layer (-1 for X_t, L for H_t / Sum)
 };
 
-// Which V' node's value currently sits (as bf16) in each forward GEMM operand: the x and h
-// halves of layer l's operand [x | h_{t-1}] and the head operand.  Cell-state kernels write
-// their h (and, at layer 0, the next input) straight into the operands of their consumers;
-// a gates / head node re-packs only when its operand does not already hold its inputs.
-// kZeros marks the all-zero h of t = 0.  Used identically by enqueue_lstm and lstm_launches.
-// Operands are double-buffered by time parity (G^l_t reads buffer t % 2), so a producer for
-// step t+1 never waits for the consumer of step t.
-struct OperandTracker {
-  static constexpr int kZeros = -2;
-  std::vector<int> wx, wh;   // [2 l + parity]
-  explicit OperandTracker(int L) : wx(2 * L, -1), wh(2 * L, -1) {}
-  bool gates_needs_pack(int l, int t, int xnode, int hnode) const {
-    return wx[2 * l + t % 2] != xnode || wh[2 * l + t % 2] != hnode;
-  }
-  void packed(int l, int t, int xnode, int hnode) {
-    wx[2 * l + t % 2] = xnode;
-    wh[2 * l + t % 2] = hnode;
-  }
-  // cell state node u = S^l_t produced: h -> layer l's h half for t+1, layer l+1's x half
-  // (step t) or the head operand (step t); layer 0 also writes x_{t+1} (Input node xnext_node)
-  void cell(int u, int l, int t, int L, int T, int xnext_node) {
-    if (t + 1 < T) wh[2 * l + (t + 1) % 2] = u;
-    if (l + 1 < L) wx[2 * (l + 1) + t % 2] = u;
-    if (l == 0 && t + 1 < T) wx[(t + 1) % 2] = xnext_node;
-  }
+// ---- schedule (see the header): launch units in issue order and the materialised set
+struct LstmUnit {
+  int type = 0;                       // 0 = the V' node at order index oi (+ fused successor), 1 = run
+  int oi = -1;
+  int l = 0, k = 0, t0 = 0, n = 0;    // run: layer, kind (0 forward, 1 mirror), first step, steps
+  int g[slmk::kRunMax], s[slmk::kRunMax];   // the run's gates / cell nodes (s = -1: gates only)
+};
+struct LstmSched {
+  std::vector<LstmUnit> units;
+  std::vector<char> mat;   // per G' node: its value is written to its tag
+  int fused = 0;           // phases issued chunk by chunk, layer by layer
 };
 
+LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse) {
+  const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, CH = kLstmChunk, RM = slmk::kRunMax;
+  const std::vector<int>& order = p->order;
+  const int nn = (int)p->kind.size();
+  LstmSched S;
+  S.mat.assign(nn, 1);
+  auto op = [&](int v) { return p->op[v]; };
+  auto pred0 = [&](int v) { return p->preds[p->pred_ptr[v]]; };
+  auto pred1 = [&](int v) { return p->pred_ptr[v + 1] - p->pred_ptr[v] > 1 ? p->preds[p->pred_ptr[v] + 1] : -1; };
+  auto tof = [&](int v) { return p->orig[v] / per_t; };
+  auto lof = [&](int v) { return (p->orig[v] % per_t - 1) / 2; };
+  std::vector<std::vector<int>> readers(nn);
+  for (int v : order)
+    for (int i = p->pred_ptr[v]; i < p->pred_ptr[v + 1]; ++i) readers[p->preds[i]].push_back(v);
+  struct Item {
+    int oi, g, s;   // g >= 0: a forward / mirror gates node and its fused cell s (-1: none)
+  };
+  std::vector<Item> items;
+  for (size_t oi = 0; oi < order.size(); ++oi) {
+    const int v = order[oi];
+    if (p->kind[v] != SLM_KIND_GRAD && op(v) == SLM_OP_LSTM_GATES) {
+      int c = -1;
+      if (oi + 1 < order.size()) {
+        const int u = order[oi + 1];
+        if (op(u) == SLM_OP_LSTM_CELL && p->kind[u] == p->kind[v] && pred0(u) == v) c = u;
+      }
+      items.push_back({(int)oi, v, c});
+      if (c >= 0) ++oi;
+    } else {
+      items.push_back({(int)oi, -1, -1});
+    }
+  }
+  auto node_unit = [&](int oi) {
+    LstmUnit u;
+    u.oi = oi;
+    S.units.push_back(u);
+  };
+  auto kind01 = [&](int v) { return p->kind[v] == SLM_KIND_MIRROR ? 1 : 0; };
+  std::vector<char> inph(nn, 0);
+  auto is_grad = [&](const Item& it) { return it.g < 0 && p->kind[order[it.oi]] == SLM_KIND_GRAD; };
+  size_t a0 = 0;
+  while (a0 < items.size()) {
+    if (is_grad(items[a0])) {
+      node_unit(items[a0].oi);
+      ++a0;
+      continue;
+    }
+    size_t a1 = a0;
+    while (a1 < items.size() && !is_grad(items[a1])) ++a1;
+    // ---- phase [a0, a1): fusable when every gates / cell node is paired and the forward heads
+    // come in whole chunks
+    bool ok = fuse;
+    std::vector<int> pn;
+    for (size_t i = a0; i < a1; ++i) {
+      const Item& it = items[i];
+      if (it.g >= 0) {
+        pn.push_back(it.g);
+        if (it.s >= 0) pn.push_back(it.s);
+        continue;
+      }
+      const int v = order[it.oi], o = op(v);
+      pn.push_back(v);
+      if (o == SLM_OP_LSTM_CELL || (o == SLM_OP_HEAD_CE && p->kind[v] != SLM_KIND_FWD) ||
+          (o != SLM_OP_HEAD_CE && o != SLM_OP_INPUT && o != SLM_OP_SUM))
+        ok = false;
+    }
+    for (int v : pn) inph[v] = 1;
+    // a gates node without its cell must be the last step of its lane in the phase (the run computes
+    // that step's cell into its side buffers only; e.g. the kept state closing a time segment)
+    for (size_t i = a0; i < a1 && ok; ++i) {
+      const Item& it = items[i];
+      if (it.g < 0 || it.s >= 0) continue;
+      for (size_t i2 = i + 1; i2 < a1; ++i2)
+        if (items[i2].g >= 0 && lof(items[i2].g) == lof(it.g) && kind01(items[i2].g) == kind01(it.g)) ok = false;
+    }
+    if (ok)
+      for (int v : pn)
+        if (op(v) == SLM_OP_HEAD_CE) {
+          const int t = tof(v), te = std::min(T - 1, t - t % CH + CH - 1);
+          if (!inph[te * per_t + per_t - 1]) ok = false;   // forward nodes: G' id == forward id
+        }
+    if (ok) {
+      // materialise a value iff some reader does not get it on chip / from a side buffer
+      for (int v : pn) {
+        const int o = op(v);
+        if (o != SLM_OP_LSTM_GATES && o != SLM_OP_LSTM_CELL) continue;
+        bool need = false;
+        for (int r : readers[v]) {
+          bool cov = false;
+          if (o == SLM_OP_LSTM_GATES) {
+            cov = inph[r] && op(r) == SLM_OP_LSTM_CELL && pred0(r) == v;
+          } else if (inph[r] && p->kind[r] == p->kind[v]) {
+            const int dr = p->orig[r] - p->orig[v];
+            cov = (dr == per_t - 1 && op(r) == SLM_OP_LSTM_GATES) || (dr == per_t && op(r) == SLM_OP_LSTM_CELL) ||
+                  (dr == 1 && op(r) == SLM_OP_LSTM_GATES) ||
+                  (dr == 1 && op(r) == SLM_OP_HEAD_CE && p->kind[v] == SLM_KIND_FWD);
+          }
+          if (!cov) {
+            need = true;
+            break;
+          }
+        }
+        S.mat[v] = need;
+      }
+      // the reordered phase must write each tag once and read no tag it writes
+      std::vector<int> wt;
+      for (int v : pn)
+        if (((op(v) == SLM_OP_LSTM_GATES || op(v) == SLM_OP_LSTM_CELL) && S.mat[v]) || op(v) == SLM_OP_HEAD_CE)
+          wt.push_back(p->node_tag[v]);
+      std::sort(wt.begin(), wt.end());
+      if (std::adjacent_find(wt.begin(), wt.end()) != wt.end()) ok = false;
+      for (int v : pn) {
+        if (!ok || op(v) != SLM_OP_LSTM_GATES) continue;
+        const int sp = pred1(v), xn = pred0(v);
+        for (int r : {sp, lof(v) > 0 ? xn : -1})
+          if (r >= 0 && !(inph[r] && p->kind[r] == p->kind[v]) &&
+              std::binary_search(wt.begin(), wt.end(), p->node_tag[r]))
+            ok = false;
+      }
+      if (!ok)
+        for (int v : pn) S.mat[v] = 1;
+    }
+    if (!ok) {   // node by node in V' order, runs of one step (a lone gates node: gates only)
+      for (size_t i = a0; i < a1; ++i) {
+        const Item& it = items[i];
+        if (it.g < 0) {
+          node_unit(it.oi);
+          continue;
+        }
+        LstmUnit u;
+        u.type = 1;
+        u.l = lof(it.g);
+        u.k = kind01(it.g);
+        u.t0 = tof(it.g);
+        u.n = 1;
+        u.g[0] = it.g;
+        u.s[0] = it.s;
+        S.units.push_back(u);
+      }
+    } else {
+      ++S.fused;
+      // runs per lane (consecutive steps of one chunk, at most kRunMax), issued by (chunk, layer, kind)
+      std::vector<LstmUnit> runs;
+      std::vector<std::vector<std::pair<int, int>>> lane(2 * L);
+      for (size_t i = a0; i < a1; ++i)
+        if (items[i].g >= 0) lane[lof(items[i].g) + L * kind01(items[i].g)].push_back({items[i].g, items[i].s});
+      for (int ln = 0; ln < 2 * L; ++ln) {
+        LstmUnit u;
+        u.type = 1;
+        u.l = ln % L;
+        u.k = ln / L;
+        for (auto& gs : lane[ln]) {
+          const int t = tof(gs.first);
+          if (u.n > 0 && (t != u.t0 + u.n || t / CH != u.t0 / CH || u.n == RM)) {
+            runs.push_back(u);
+            u.n = 0;
+          }
+          if (u.n == 0) u.t0 = t;
+          u.g[u.n] = gs.first;
+          u.s[u.n] = gs.second;
+          ++u.n;
+        }
+        if (u.n > 0) runs.push_back(u);
+      }
+      std::stable_sort(runs.begin(), runs.end(), [&](const LstmUnit& x, const LstmUnit& y) {
+        return std::make_tuple(x.t0 / CH, x.l, x.k, x.t0) < std::make_tuple(y.t0 / CH, y.l, y.k, y.t0);
+      });
+      std::vector<int> head_oi(T / CH + 2, -1);   // V' index of each chunk's last forward head
+      int sum_oi = -1;
+      for (size_t i = a0; i < a1; ++i) {
+        if (items[i].g >= 0) continue;
+        const int v = order[items[i].oi];
+        if (op(v) == SLM_OP_HEAD_CE) {
+          const int t = tof(v);
+          if (t % CH == CH - 1 || t == T - 1) head_oi[t / CH] = items[i].oi;
+        } else if (op(v) == SLM_OP_SUM) {
+          sum_oi = items[i].oi;
+        }
+      }
+      for (size_t r = 0; r < runs.size(); ++r) {
+        S.units.push_back(runs[r]);
+        const int c = runs[r].t0 / CH;
+        const bool last_top = r + 1 == runs.size() || runs[r + 1].t0 / CH != c;
+        if (last_top && head_oi[c] >= 0) {
+          node_unit(head_oi[c]);
+          head_oi[c] = -1;
+        }
+      }
+      for (int c = 0; c < (int)head_oi.size(); ++c)
+        if (head_oi[c] >= 0) node_unit(head_oi[c]);
+      if (sum_oi >= 0) node_unit(sum_oi);
+    }
+    for (int v : pn) inph[v] = 0;
+    a0 = a1;
+  }
+  return S;
+}
+
+// Launch a persistent run kernel (its CTAs wait on each other every step, so all of them must be
+// resident at once).  Not a cooperative launch: cooperative grids were measured to serialise
+// across streams (the four layer runs of the wavefront ran one after the other).  Residency holds
+// by construction instead: the runs that can be in flight together (one per forward or mirror
+// lane: 2 L H / 32 <= 128 CTAs at C3 with one of the two kinds active) fit on the 148 SMs, every
+// other kernel of the step finishes without waiting on a run, and a PDL successor of a run is
+// only released by the run's final griddepcontrol.launch_dependents.
+template <class... KArgs, class... Args>
+cudaError_t launch_run(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                       Args... args) {
+  return launch_kc(k, grid, block, smem, st, pdl, 1, args...);
+}
+
+template <int B>
+slm_status launch_fwd_run(const CUtensorMap& w, const CUtensorMap& h, const CUtensorMap& x, const slmk::FwdRun& a,
+                          cudaStream_t st, bool pdl) {
+  using C = slmk::FwdRunCfg<B>;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(slmk::lstm_fwd_run_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CK(launch_run(slmk::lstm_fwd_run_kernel<B>, dim3(a.H / 32), dim3(slmk::kRunThreads), C::SMEM, st, pdl, w, h, x, a));
+  return SLM_OK;
+}
+
+// dry = true: no CUDA call, only the launch count (slm_step_launches)
 slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const int32_t* labels, void* pool,
-                        void* ws, float* loss, cudaStream_t st, int64_t* launches) {
+                        void* ws, float* loss, cudaStream_t st, int64_t* launches, bool dry = false) {
   using namespace slmk;
   using bf = __nv_bfloat16;
   const slm_lstm_desc& d = m.ld;
   slm_lstm_state& S = m.lst;
   const bool pdl = m.pdl != 0;
   int ts_slot = 0;
-  if (m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) {
+  if (!dry && m.profile_ts > 0 && (int)m.ts_kind.size() < m.profile_ts) {
     m.ts_kind.resize(m.profile_ts);
     m.ts_aux.resize(m.profile_ts);
   }
   auto gdbg = [&](int kind) -> int {   // launch slot for the device-clock GEMM timing
-    if (m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
+    if (dry || m.profile_ts <= 0 || m.ts_buf == nullptr || ts_slot >= m.profile_ts) return 0;
     m.ts_kind[ts_slot] = kind;
     m.ts_aux[ts_slot] = m.ts_cur_aux;
     return ((++ts_slot) << 8) | (m.profile_ts_dep ? 8 : 0);
   };
+  // every CUDA call of the step goes through these (skipped in a dry run)
+#define LK(call)      \
+  do {                \
+    if (!dry) CK(call); \
+  } while (0)
+#define LT(call)                                            \
+  do {                                                      \
+    if (!dry && (s = (call)) != SLM_OK) return s;           \
+  } while (0)
   const int L = d.n_layers, T = d.steps, B = d.batch, H = d.hidden, I = d.n_in, C = d.n_classes;
   const int Cp = lstm_cpad(C), K0 = lstm_kin0(I), CH = kLstmChunk;
   const LstmWs W = lstm_ws_layout(d, m.lstm_sk, m.lstm_skx);
@@ -253,8 +503,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   bf* hopR = (bf*)(w + W.hopR);
   bf* dlR = (bf*)(w + W.dlR);
   const float scale = 1.0f / ((float)T * (float)B);
-  slm_status s;
-  if ((s = lstm_bind_maps(d, S.maps, ws, m.lstm_sk, m.lstm_skx)) != SLM_OK) return s;
+  slm_status s = SLM_OK;
+  if (!dry && (s = lstm_bind_maps(d, S.maps, ws, m.lstm_sk, m.lstm_skx)) != SLM_OK) return s;
   const LstmMaps& M = S.maps;
 
   const int N = p->n_fwd;
@@ -279,95 +529,73 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto V = [&](int node) -> float* { return node < 0 ? nullptr : (float*)tp[p->node_tag[node]]; };
   const int* pred = p->preds.data();
   auto preds_of = [&](int v) { return std::make_pair(pred + p->pred_ptr[v], p->pred_ptr[v + 1] - p->pred_ptr[v]); };
-  const dim3 eg(592), eb(256);
+  const dim3 eb(256);
   // element-wise grids sized to the work (one element per thread, at most 4 CTAs per SM) so
-  // the kernels of concurrent layer streams share the SMs (option lstm_grid = 0: 592 CTAs)
-  auto gsz = [&](size_t n) {
-    if (!m.lstm_grid) return eg;
-    return dim3((unsigned)std::max<size_t>(1, std::min<size_t>(592, (n + 255) / 256)));
-  };
+  // the kernels of concurrent layer streams share the SMs
+  auto gsz = [&](size_t n) { return dim3((unsigned)std::max<size_t>(1, std::min<size_t>(592, (n + 255) / 256))); };
   int64_t nl = 0;
   // gradients are overwritten by every step: zero the in-place accumulators first
-  CK(cudaMemsetAsync(d.dW, 0, lstm_w_offset(d, L) * 4, st));
-  CK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
-  CK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
-  CK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
+  LK(cudaMemsetAsync(d.dW, 0, lstm_w_offset(d, L) * 4, st));
+  LK(cudaMemsetAsync(d.db, 0, (size_t)L * 4 * H * 4, st));
+  LK(cudaMemsetAsync(d.dW_o, 0, (size_t)Cp * H * 4, st));
+  LK(cudaMemsetAsync(d.db_o, 0, (size_t)Cp * 4, st));
+  // the run kernels' step counters (monotone within a step; the host tracks each one's value)
+  unsigned* bar = (unsigned*)(w + W.bar);
+  LK(cudaMemsetAsync(bar, 0, (size_t)2 * L * 4, st));
+  std::vector<unsigned> bar_val(2 * L, 0u);
   // weight-gradient chunk of time t: slot in the ring and whether t closes the chunk (the
   // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
 
-  OperandTracker trk(L);
-  auto opl = [&](int l, int par) {
-    return (bf*)(w + W.opL[l] + par * (((size_t)B * lstm_K(d, l) * 2 + 255) / 256 * 256));
-  };
-  // forward head operands: a ring of CH steps per chunk parity, consumed by one batched head
-  auto hfb = [&](int t) {
-    return (bf*)(w + W.hf + ((t / CH) % 2) * (((size_t)CH * B * H * 2 + 255) / 256 * 256)) + (size_t)(t % CH) * B * H;
-  };
-  // the operand side outputs of the kernel producing S^l_t (V' node u); the top layer's h
-  // goes to the forward head ring only for forward (not re-computed) states
-  auto op_out = [&](int u, int l, int t, int knd) {
-    slmk::OpOut o{};
-    if (t + 1 < T) {
-      o.h_self = opl(l, (t + 1) % 2) + (l == 0 ? K0 : H);
-      o.ld_self = lstm_K(d, l);
-    }
-    o.h_up = l + 1 < L ? opl(l + 1, t % 2) : (knd == SLM_KIND_FWD ? hfb(t) : nullptr);
-    o.ld_up = l + 1 < L ? lstm_K(d, l + 1) : H;
-    if (l == 0 && t + 1 < T) {
-      o.xnext = (const float*)((const uint8_t*)xin + (size_t)(t + 1) * B * I * 4);
-      o.I = I;
-      o.Kin0 = K0;
-      o.x0 = opl(0, (t + 1) % 2);
-      o.ld0 = lstm_K(d, 0);
-    }
-    trk.cell(u, l, t, L, T, (t + 1) * per_t);
-    return o;
-  };
+  // ---- forward lanes (layer l, kind k): side state and which V' node each holds
+  auto lane_of = [&](int l, int k) { return l + L * k; };
+  std::vector<int> hx_node(2 * L, -1), cs_node(2 * L, -1);
+  std::vector<int> ring_node((size_t)2 * L * 2 * CH, -1);   // [lane][chunk parity][slot]
+  auto rslot = [&](int t) { return ((t / CH) % 2) * CH + t % CH; };
+  auto ring_ptr = [&](int ln, int t) { return (bf*)(w + W.ring[ln]) + (size_t)rslot(t) * B * H; };
 
   // ---- layer wavefront (option lstm_streams): every launch unit runs on the stream of its
   // layer (the head and the loss on stream L); happens-before edges come from tracking, per
-  // resource (pool tag, forward operand half), the last writer and the latest reader on each
+  // resource (pool tag, ring buffer), the last writer and the latest reader on each
   // stream, so concurrent units never touch a buffer out of V' order.  A dependency is a
   // (stream, unit sequence number); it is skipped when the waiting stream is already ordered
   // after that unit (same stream, or an earlier wait on a later unit of that stream).  Events
   // live in a per-stream ring large enough to hold a step's units; a re-recorded slot only
   // makes a (very old) wait more conservative, never wrong.
-  const bool msm = m.lstm_streams != 0 && st != nullptr;
+  const bool msm = m.lstm_streams != 0 && (st != nullptr || dry);
   // lstm_streams = 2: re-computed (mirror) units get streams of their own (L+1+l), so the
   // recompute of segment j-1 can overlap the backward of segment j
   const int NSTR = m.lstm_streams >= 2 ? 2 * L + 1 : L + 1;
   constexpr int kRing = 16384;
   const int ntag = (int)p->tag_size.size();
-  auto OPX = [&](int l, int par) { return ntag + 4 * l + par; };
-  auto OPH = [&](int l, int par) { return ntag + 4 * l + 2 + par; };
-  auto HFR = [&](int par) { return ntag + 4 * L + par; };       // forward head ring, chunk parity
-  auto DHR = [&](int par) { return ntag + 4 * L + 2 + par; };   // batched (dh | 0) ring, chunk parity
-  auto PXR = [&](int l, int par) { return ntag + 4 * L + 4 + 2 * l + par; };   // dX partials of layer l
-  const int HOP = ntag + 6 * L + 3;   // the highest resource id
+  auto DHR = [&](int par) { return ntag + par; };                       // batched (dh | 0) ring, chunk parity
+  auto PXR = [&](int l, int par) { return ntag + 2 + 2 * l + par; };    // dX partials of layer l
+  auto RNG = [&](int ln, int par) { return ntag + 2 + 2 * L + 2 * ln + par; };   // forward chunk ring
+  const int HOP = ntag + 2 + 6 * L;   // the number of resources
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
   std::vector<long> seqn(NSTR, 0), waits;
   std::vector<long> known((size_t)NSTR * NSTR, -1);   // [a][s]: latest seq of s stream a is ordered after
   if (msm) {
-    while ((int)S.streams.size() < NSTR) {
-      cudaStream_t x;
-      CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
-      S.streams.push_back(x);
+    if (!dry) {
+      while ((int)S.streams.size() < NSTR) {
+        cudaStream_t x;
+        CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        S.streams.push_back(x);
+      }
+      if ((int)S.ev.size() < NSTR * kRing) S.ev.resize((size_t)NSTR * kRing, nullptr);
+      while ((int)S.join.size() < NSTR) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        S.join.push_back(e);
+      }
+      if (!S.fork) CK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
+      CK(cudaEventRecord(S.fork, st));
+      for (int i = 0; i < NSTR; ++i) CK(cudaStreamWaitEvent(S.streams[i], S.fork, 0));
     }
-    if ((int)S.ev.size() < NSTR * kRing) S.ev.resize((size_t)NSTR * kRing, nullptr);
-    while ((int)S.join.size() < NSTR) {
-      cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      S.join.push_back(e);
-    }
-    if (!S.fork) CK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
-    res_w.assign(HOP + 1, -1);
-    res_r.assign((size_t)(HOP + 1) * NSTR, -1);
-    // events are created lazily up to the ring size
-    CK(cudaEventRecord(S.fork, st));
-    for (int i = 0; i < NSTR; ++i) CK(cudaStreamWaitEvent(S.streams[i], S.fork, 0));
+    res_w.assign(HOP, -1);
+    res_r.assign((size_t)HOP * NSTR, -1);
   }
   auto evt = [&](long u) -> cudaEvent_t& { return S.ev[(size_t)(u % NSTR) * kRing + (size_t)((u / NSTR) % kRing)]; };
   auto unit_begin = [&](int sid, cudaStream_t* out) -> slm_status {
@@ -384,17 +612,19 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     for (long u : waits) need[u % NSTR] = std::max(need[u % NSTR], u / NSTR);
     for (int s2 = 0; s2 < NSTR; ++s2) {
       if (s2 == sid || need[s2] < 0 || known[(size_t)sid * NSTR + s2] >= need[s2]) continue;
-      CK(cudaStreamWaitEvent(S.streams[sid], evt(need[s2] * NSTR + s2), 0));
+      LK(cudaStreamWaitEvent(S.streams[sid], evt(need[s2] * NSTR + s2), 0));
       known[(size_t)sid * NSTR + s2] = need[s2];
     }
-    *out = S.streams[sid];
+    if (!dry) *out = S.streams[sid];
     return SLM_OK;
   };
   auto unit_end = [&](int sid) -> slm_status {
     const long u = seqn[sid]++ * NSTR + sid;
-    cudaEvent_t& e = evt(u);
-    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaEventRecord(e, S.streams[sid]));
+    if (!dry) {
+      cudaEvent_t& e = evt(u);
+      if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, S.streams[sid]));
+    }
     for (int r : rd) res_r[(size_t)r * NSTR + sid] = u;
     for (int r : wr) {
       res_w[r] = u;
@@ -403,8 +633,8 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     return SLM_OK;
   };
 
-  // which V' node's value each pool tag holds (host view of V' order), for the batched head
-  // backward: a chunk of g[H_t] runs as one unit when every a[S^{L-1}_t] it reads is resident
+  // which V' node's value each pool tag holds (host view of the issue order), for the batched
+  // head backward: a chunk of g[H_t] runs as one unit when every a[S^{L-1}_t] it reads is resident
   std::vector<int> owner(p->tag_size.size(), -1);
   std::vector<char> hb_batched(T, 0);
   auto dh_ring = [&](int t) {
@@ -427,8 +657,104 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     return lo;
   };
 
+  const LstmSched sched = lstm_schedule(p, d, m.lstm_fuse_runs != 0);
+  int run_idx = 0;
   const std::vector<int>& order = p->order;
-  for (size_t oi = 0; oi < order.size(); ++oi) {
+  int skip_oi = -1;
+  for (const LstmUnit& U : sched.units) {
+    if (U.type == 1) {
+      // ===== forward / mirror run of layer l, steps t0 .. t0 + n - 1 (lstm_run.cuh)
+      const int l = U.l, k = U.k, ln = lane_of(l, k), t0 = U.t0, n = U.n;
+      // cell = false: a lone gates node (n = 1, node by node); a fused run may end with a gates
+      // node whose cell is not in the phase: its cell goes to the side buffers only
+      const bool cell = n > 1 || U.s[0] >= 0;
+      const int sid = (k == 1 && NSTR > L + 1) ? L + 1 + l : l;
+      const int Kin = l == 0 ? K0 : H;
+      const int sprev = t0 > 0 ? preds_of(U.g[0]).first[1] : -1;
+      const int init = sprev < 0 ? 1 : (hx_node[ln] == sprev && cs_node[ln] == sprev ? 0 : 2);
+      // x operand rows of the input projection: the lower layer's ring when it holds the inputs
+      bool xring = l > 0;
+      for (int i = 0; i < n && xring; ++i)
+        xring = ring_node[(size_t)lane_of(l - 1, k) * 2 * CH + rslot(t0 + i)] == preds_of(U.g[i]).first[0];
+      rd.clear();
+      wr.clear();
+      if (init == 2) rd.push_back(p->node_tag[sprev]);
+      if (l > 0 && xring) rd.push_back(RNG(lane_of(l - 1, k), (t0 / CH) % 2));
+      if (l > 0 && !xring)
+        for (int i = 0; i < n; ++i) rd.push_back(p->node_tag[preds_of(U.g[i]).first[0]]);
+      for (int i = 0; i < n; ++i) {
+        if (sched.mat[U.g[i]]) wr.push_back(p->node_tag[U.g[i]]);
+        if (U.s[i] >= 0 && sched.mat[U.s[i]]) wr.push_back(p->node_tag[U.s[i]]);
+      }
+      if (cell) wr.push_back(RNG(ln, (t0 / CH) % 2));
+      cudaStream_t cs = st;
+      if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
+      m.ts_cur_aux = sid * 4 + k;
+      bf* xop = (bf*)(w + W.xop[ln]);
+      // the projection always runs with 256-column tiles over n B rows rounded up to 256 (the
+      // extra rows read neighbouring ring / operand rows, or zeros past the end, and land in unread
+      // rows of X): tcgen05 results are not invariant to the MMA's N, so one tile shape for every
+      // run length keeps runs of different lengths -- forward vs re-computed segments -- bit-identical
+      const int bi = 1, bn = 256, npad = (n * B + 255) / 256 * 256;
+      const CUtensorMap* bmap = &M.xopM[bi][ln];
+      int brow = 0;
+      if (l == 0) {
+        LK(launch_k(lstm_xpack_kernel, gsz((size_t)n * B * K0), eb, 0, cs, pdl,
+                    (const float*)((const uint8_t*)xin + (size_t)t0 * B * I * 4), I, K0, B, n, xop));
+        ++nl;
+      } else if (xring) {
+        bmap = &M.ringM[bi][lane_of(l - 1, k)];
+        brow = rslot(t0) * B;
+      } else {
+        StepIn in{};
+        for (int i = 0; i < n; ++i) in.p[i] = V(preds_of(U.g[i]).first[0]);
+        LK(launch_k(lstm_hpack_multi_kernel, gsz((size_t)n * B * H), eb, 0, cs, pdl, in, n, H, B, xop));
+        ++nl;
+      }
+      float* xp = (float*)(w + W.xp[ln]);
+      EpiBiasF32 e{xp, 4 * H, d.b + (size_t)l * 4 * H};
+      LT((launch_tc_bn<EpiBiasF32, false, false, true>(bn, 1, M.wK[l], *bmap, 4 * H, npad, Kin, 0, brow, e, cs, pdl,
+                                                        gdbg(SLM_K_GEMM_FWD))));
+      FwdRun a{};
+      a.H = H;
+      a.n = n;
+      a.t0 = t0;
+      a.Kin = Kin;
+      a.init = init;
+      a.cell = cell ? 1 : 0;
+      a.s_init = init == 2 ? V(sprev) : nullptr;
+      a.hx = (bf*)(w + W.hx[ln]);
+      a.cstate = (float*)(w + W.cst[ln]);
+      a.hring = cell ? ring_ptr(ln, t0) : nullptr;
+      a.bar = bar + ln;
+      a.ts = (m.lstm_run_ts && run_idx < m.lstm_run_ts_n)
+                 ? (unsigned long long*)m.lstm_run_ts + (size_t)run_idx * slmk::kRunMax * 16
+                 : nullptr;
+      ++run_idx;
+      a.base = bar_val[ln];
+      for (int i = 0; i < n; ++i) {
+        a.g_out[i] = sched.mat[U.g[i]] ? V(U.g[i]) : nullptr;
+        a.s_out[i] = U.s[i] >= 0 && sched.mat[U.s[i]] ? V(U.s[i]) : nullptr;
+      }
+      bar_val[ln] += (unsigned)(H / 32) * (unsigned)(n + 1);
+      switch (B) {
+        case 64: LT((launch_fwd_run<64>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
+        case 128: LT((launch_fwd_run<128>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
+        default: LT((launch_fwd_run<256>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
+      }
+      nl += 2;
+      if (msm && (s = unit_end(sid)) != SLM_OK) return s;
+      // side state: -1 where the run computed a cell that is not a node of V' (or none)
+      hx_node[ln] = cs_node[ln] = cell ? U.s[n - 1] : -1;
+      for (int i = 0; i < n && cell; ++i) ring_node[(size_t)ln * 2 * CH + rslot(t0 + i)] = U.s[i];
+      for (int i = 0; i < n; ++i) {
+        if (sched.mat[U.g[i]]) owner[p->node_tag[U.g[i]]] = U.g[i];
+        if (U.s[i] >= 0 && sched.mat[U.s[i]]) owner[p->node_tag[U.s[i]]] = U.s[i];
+      }
+      continue;
+    }
+    const int oi = U.oi;
+    if (oi == skip_oi) continue;   // the gradient gates node fused into the previous unit
     const int v = order[oi];
     const int kind = p->kind[v], opk = p->op[v], orig = p->orig[v];
     auto pp = preds_of(v);
@@ -439,11 +765,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     const bool lay = opk == SLM_OP_LSTM_GATES || opk == SLM_OP_LSTM_CELL;
     const int sid = !lay ? L : (kind == SLM_KIND_MIRROR && NSTR > L + 1 ? L + 1 + l : l);
     int partner = -1;
-    if (oi + 1 < order.size()) {
+    if (oi + 1 < (int)order.size()) {
       const int u = order[oi + 1];
       const bool pu0 = p->pred_ptr[u + 1] > p->pred_ptr[u] && p->preds[p->pred_ptr[u]] == v;
-      if (kind != SLM_KIND_GRAD && opk == SLM_OP_LSTM_GATES && p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu0)
-        partner = u;
       if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL && p->op[u] == SLM_OP_LSTM_GATES &&
           p->kind[u] == SLM_KIND_GRAD && pu0)
         partner = u;
@@ -457,31 +781,18 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         if (pn.first[i] != v) rd.push_back(p->node_tag[pn.first[i]]);
       wr.push_back(p->node_tag[node]);
     }
-    auto cell_writes = [&]() {
-      if (t + 1 < T) wr.push_back(OPH(l, (t + 1) % 2));
-      if (l + 1 < L) wr.push_back(OPX(l + 1, t % 2));
-      else if (kind == SLM_KIND_FWD) wr.push_back(HFR((t / CH) % 2));
-      if (l == 0 && t + 1 < T) wr.push_back(OPX(0, (t + 1) % 2));
-    };
+    const int lane_top = lane_of(L - 1, 0);
     if (kind != SLM_KIND_GRAD) {
-      if (opk == SLM_OP_LSTM_GATES) {
-        const int hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, t, pp.first[0], hn)) {
-          wr.push_back(OPX(l, t % 2));
-          wr.push_back(OPH(l, t % 2));
-        } else {
-          rd.push_back(OPX(l, t % 2));
-          rd.push_back(OPH(l, t % 2));
-        }
-        if (partner >= 0) cell_writes();
-      } else if (opk == SLM_OP_LSTM_CELL) {
-        cell_writes();
+      if (opk == SLM_OP_LSTM_CELL) {
+        // an isolated cell node (its gates node not right before it in V'): h into the ring of
+        // its lane, the lane's recurrent state becomes stale
+        wr.push_back(RNG(lane_of(l, kind == SLM_KIND_MIRROR ? 1 : 0), (t / CH) % 2));
       } else if (opk == SLM_OP_HEAD_CE) {
         // one batched unit per chunk of forward heads, at the chunk's last step
         wr.clear();
         rd.clear();
         if (t % CH == CH - 1 || t == T - 1) {
-          rd.push_back(HFR((t / CH) % 2));
+          rd.push_back(RNG(lane_top, (t / CH) % 2));
           for (int t2 = t - t % CH; t2 <= t; ++t2) wr.push_back(p->node_tag[t2 * per_t + per_t - 1]);
         }
       }
@@ -511,76 +822,40 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
     m.ts_cur_aux = sid * 4 + (kind == SLM_KIND_GRAD ? 2 : kind == SLM_KIND_MIRROR ? 1 : 0);
     if (kind != SLM_KIND_GRAD) {
-      if (opk == SLM_OP_LSTM_GATES) {
-        const bool lower_state = l > 0;
-        const float* x = V(pp.first[0]);
-        const float* sprev = pp.second > 1 ? V(pp.first[1]) : nullptr;
-        const int Kin = l == 0 ? K0 : H, sk = l == 0 ? sp.g0 : sp.g1;
-        const int xn = pp.first[0], hn = pp.second > 1 ? pp.first[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, t, xn, hn)) {
-          CK(launch_k(lstm_pack_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, x, lower_state ? H : I, lower_state ? 2 * H : I, Kin, sprev,
-                      H, B, opl(l, t % 2)));
-          trk.packed(l, t, xn, hn);
-          ++nl;
-        }
-        // fuse the cell when V' runs S^l_t (same kind) right after G^l_t
-        float* s_out = nullptr;
-        const float* s_prev = nullptr;
-        slmk::OpOut oo{};
-        if (oi + 1 < order.size()) {
-          const int u = order[oi + 1];
-          auto pu = preds_of(u);
-          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && pu.first[0] == v) {
-            s_out = V(u);
-            s_prev = pu.second > 1 ? V(pu.first[1]) : nullptr;
-            oo = op_out(u, l, t, kind);
-            ++oi;
-          }
-        }
-        if (sk == 1 && m.lstm_fuse_cell) {   // one kernel: GEMM with the activations and the cell in its epilogue
-          slmk::EpiGatesCell e{V(v), s_out, s_prev, d.b + (size_t)l * 4 * H, H, B, oo};
-          if ((s = launch_tc_bn<slmk::EpiGatesCell, false, false, true>(B, 1, M.wK32[l], M.opK[2 * l + t % 2], 4 * H, B,
-                                                                        Kin + H, 0, 0, e, cs, pdl,
-                                                                        gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
-            return s;
-          nl += 1;
-        } else {
-          slmk::EpiPartialTma e{B};
-          if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(
-                   B, sk, M.wK[l], M.opK[2 * l + t % 2], 4 * H, B, Kin + H, 0, 0, e, cs, pdl, gdbg(SLM_K_GEMM_FWD),
-                   sid > L ? &M.pGm[l] : &M.pG[l])) != SLM_OK)
-            return s;
-          CK(launch_k(lstm_gates_cell_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, Pb(sid), sk, d.b + (size_t)l * 4 * H,
-                      H, B, V(v), s_prev, s_out, oo));
-          nl += 2;
-        }
-      } else if (opk == SLM_OP_LSTM_CELL) {
-        CK(launch_k(lstm_cell_fwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, (const float*)V(pp.first[0]),
-                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), op_out(v, l, t, kind)));
+      if (opk == SLM_OP_LSTM_CELL) {
+        const int ln = lane_of(l, kind == SLM_KIND_MIRROR ? 1 : 0);
+        LK(launch_k(lstm_cell_fwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, (const float*)V(pp.first[0]),
+                    (const float*)(pp.second > 1 ? V(pp.first[1]) : nullptr), H, B, V(v), ring_ptr(ln, t)));
         ++nl;
+        hx_node[ln] = cs_node[ln] = -1;
+        ring_node[(size_t)ln * 2 * CH + rslot(t)] = v;
       } else if (opk == SLM_OP_HEAD_CE) {
         // batched forward heads of steps t0..t (the chunk ends here): logits for n*B rows in one
-        // GEMM, the softmax-CE rows, then the per-step losses into the H_t tags
+        // GEMM over the top layer's ring, the softmax-CE rows, then the per-step losses into the H_t tags
         if (t % CH == CH - 1 || t == T - 1) {
-          const int t0 = t - t % CH, n = t - t0 + 1, N = n * B, bi = N % 256 == 0 ? 1 : 0;
+          const int t0 = t - t % CH, n = t - t0 + 1, Nr = n * B, bi = Nr % 256 == 0 ? 1 : 0;
+          for (int t2 = t0; t2 <= t; ++t2)
+            if (ring_node[(size_t)lane_top * 2 * CH + rslot(t2)] != t2 * per_t + per_t - 2) {
+              set_error("lstm: forward head inputs not in the top layer's ring (unsupported V' order)");
+              return SLM_E_UNSUPPORTED;
+            }
           float* lgF = (float*)(w + W.logitsF);
           float* rlF = (float*)(w + W.rowlossF);
           slmk::EpiStoreF32 e{lgF, Cp};
-          if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bi ? 256 : 64, 1, M.woK, M.hfK[(t / CH) % 2][bi],
-                                                                       Cp, N, H, 0, 0, e, cs, pdl,
-                                                                       gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
-            return s;
-          CK(launch_k(lstm_head_ce_kernel, dim3(N), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
-                      labels + (size_t)t0 * B, C, Cp, N, scale, rlF, (bf*)nullptr, (float*)nullptr, (unsigned*)nullptr,
+          LT((launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bi ? 256 : 64, 1, M.woK, M.ringM[bi][lane_top], Cp,
+                                                                  Nr, H, 0, rslot(t0) * B, e, cs, pdl,
+                                                                  gdbg(SLM_K_GEMM_FWD))));
+          LK(launch_k(lstm_head_ce_kernel, dim3(Nr), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
+                      labels + (size_t)t0 * B, C, Cp, Nr, scale, rlF, (bf*)nullptr, (float*)nullptr, (unsigned*)nullptr,
                       (float*)nullptr));
           slmk::StepOut so{};
           for (int i = 0; i < n; ++i) so.p[i] = V((t0 + i) * per_t + per_t - 1);
-          CK(launch_k(lstm_step_loss_kernel, dim3(n), dim3(1024), 0, cs, pdl, (const float*)rlF, B, scale, so,
+          LK(launch_k(lstm_step_loss_kernel, dim3(n), dim3(1024), 0, cs, pdl, (const float*)rlF, B, scale, so,
                       loss_t + t0));
           nl += 3;
         }
       } else if (opk == SLM_OP_SUM) {
-        CK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const float*)loss_t, T, V(v)));
+        LK(launch_k(lstm_sum_kernel, dim3(1), dim3(32), 0, cs, pdl, (const float*)loss_t, T, V(v)));
         ++nl;
       } else {
         set_error("unsupported op in lstm plan");
@@ -590,7 +865,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       const int slot = t % CH;
       const bool flush = slot == 0;
       if (opk == SLM_OP_SUM) {
-        CK(launch_k(fill_kernel, dim3(1), eb, 0, cs, pdl, V(v), T, 1.0f));
+        LK(launch_k(fill_kernel, dim3(1), eb, 0, cs, pdl, V(v), T, 1.0f));
         ++nl;
       } else if (opk == SLM_OP_HEAD_CE && hb_now) {
         // batched head backward of steps t0..t: h operands, logits GEMM (N = n B), CE rows ->
@@ -600,55 +875,49 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         const int bi = N % 256 == 0 ? 2 : N % 128 == 0 ? 1 : 0, bnb = 64 << bi;
         slmk::StepIn in{};
         for (int i = 0; i < n; ++i) in.p[i] = V(head_state(t0 + i));
-        CK(launch_k(lstm_hpack_multi_kernel, gsz((size_t)n * B * H), eb, 0, cs, pdl, in, n, H, B, hopR + (size_t)r0 * H));
+        LK(launch_k(lstm_hpack_multi_kernel, gsz((size_t)n * B * H), eb, 0, cs, pdl, in, n, H, B, hopR + (size_t)r0 * H));
         float* lgF = (float*)(w + W.logitsF);
         slmk::EpiStoreF32 e{lgF, Cp};
-        if ((s = launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bnb, 1, M.woK, M.hopRKb[bi], Cp, N, H, 0, r0, e, cs,
-                                                                     pdl, gdbg(SLM_K_GEMM_FWD))) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(N), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
+        LT((launch_tc_bn<slmk::EpiStoreF32, false, false, true>(bnb, 1, M.woK, M.hopRKb[bi], Cp, N, H, 0, r0, e, cs,
+                                                                     pdl, gdbg(SLM_K_GEMM_FWD))));
+        LK(launch_k(lstm_head_ce_kernel, dim3(N), dim3(1024), 0, cs, pdl, (const float*)lgF, 1, lgF, d.b_o,
                     labels + (size_t)t0 * B, C, Cp, N, scale, (float*)nullptr, dlR + (size_t)r0 * Cp, dlog_f,
                     (unsigned*)nullptr, (float*)nullptr));
         slmk::EpiPartialTma e2{N};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(bnb, sp.hd, M.woMN, M.dlRKb[bi], H, N, Cp, 0, r0,
-                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pHB)) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl,
+        LT((launch_tc_bn<slmk::EpiPartialTma, true, false, true>(bnb, sp.hd, M.woMN, M.dlRKb[bi], H, N, Cp, 0, r0,
+                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pHB)));
+        LK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl,
                     (const float*)(w + W.PH), sp.hd, H, N, dh_ring(t0), (const float*)dlog_f, Cp, B, n, d.db_o));
         nl += 5;
         if (t0 % CH == 0) {   // the chunk is complete: dW_o over all its rows
           slmk::EpiAccF32 e3{d.dW_o, H};
-          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp,
+          LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp,
                                                                     chunk_rows(t0), 0, 0, e3, cs, pdl,
-                                                                    gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-            return s;
+                                                                    gdbg(SLM_K_GEMM_DW))));
           ++nl;
         }
         for (int t2 = t0; t2 <= t; ++t2) hb_batched[t2] = 1;
       } else if (opk == SLM_OP_HEAD_CE) {
         // preds = [g[Sum], a[S^{L-1}_t]]: recompute logits (the head reads only its input, A6)
         const float* sL = V(pp.first[pp.second - 1]);
-        CK(launch_k(lstm_hpack_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, sL, H, B, hopR + (size_t)slot * B * H));
+        LK(launch_k(lstm_hpack_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, sL, H, B, hopR + (size_t)slot * B * H));
         slmk::EpiPartialTma e{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
-                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
+        LT((launch_tc_bn<slmk::EpiPartialTma, false, false, true>(B, sp.lg, M.woK, M.hopRK, Cp, B, H, 0, slot * B,
+                                                                       e, cs, pdl, gdbg(SLM_K_GEMM_FWD), &M.pL)));
+        LK(launch_k(lstm_head_ce_kernel, dim3(B), dim3(1024), 0, cs, pdl, Pb(sid), sp.lg, logits, d.b_o,
                     labels + (size_t)t * B, C, Cp, B, scale, (float*)nullptr, dlR + (size_t)slot * B * Cp, dlog_f,
                     (unsigned*)nullptr, (float*)nullptr));
         // dh[b][h] = sum_c dlog[b][c] W_o[c][h]  (split-K partials) -> (dh | 0)
         slmk::EpiPartialTma e2{B};
-        if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
-                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)) != SLM_OK)
-          return s;
-        CK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl, Pb(sid),
+        LT((launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
+                                                                      e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)));
+        LK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl, Pb(sid),
                     sp.hd, H, B, V(v), (const float*)dlog_f, Cp, B, 1, d.db_o));
         nl += 5;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};
-          if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp, chunk_rows(t), 0,
-                                                                    0, e3, cs, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-            return s;
+          LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>(Cp % 256 ? 128 : 256, 1, M.hopRMN, M.dlRMN, H, Cp, chunk_rows(t), 0,
+                                                                    0, e3, cs, pdl, gdbg(SLM_K_GEMM_DW))));
           ++nl;
         }
       } else if (opk == SLM_OP_LSTM_CELL || opk == SLM_OP_LSTM_GATES) {
@@ -695,15 +964,15 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
             if (p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && pu.first[0] == v) {
               const int nf = has_prev ? 2 : 1;
               const float* x = V(pu.first[pu.second - nf]);
-              CK(launch_k(lstm_cell_bwd_dpre_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, src, act, sprev, H, B,
+              LK(launch_k(lstm_cell_bwd_dpre_kernel, gsz((size_t)B * (Kin + H)), eb, 0, cs, pdl, src, act, sprev, H, B,
                           V(v), dpS, dpFS, x, l > 0 ? H : I, l > 0 ? 2 * H : I, Kin, opS));
               ++nl;
               vg = u;
-              ++oi;
+              skip_oi = oi + 1;
             }
           }
           if (vg < 0) {
-            CK(launch_k(lstm_cell_bwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, src, act, sprev, H, B, V(v)));
+            LK(launch_k(lstm_cell_bwd_kernel, gsz((size_t)B * H), eb, 0, cs, pdl, src, act, sprev, H, B, V(v)));
             ++nl;
           }
         } else {
@@ -714,7 +983,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           const float* x = V(pp.first[pp.second - nf]);
           const float* sprev = has_prev ? V(pp.first[pp.second - 1]) : nullptr;
           const int drow = 4 * H + (has_prev ? 2 * H : 0);
-          CK(launch_k(lstm_dpre_kernel, gsz((size_t)B * 4 * H), eb, 0, cs, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
+          LK(launch_k(lstm_dpre_kernel, gsz((size_t)B * 4 * H), eb, 0, cs, pdl, dact, drow, act, H, B, dpS, dpFS, x, l > 0 ? H : I,
                       l > 0 ? 2 * H : I, Kin, sprev, opS));
           ++nl;
         }
@@ -722,19 +991,17 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           // d[x | h] = d_pre W_l:  D[m = k_in][n = b], K = 4H, split-K partials kept (time-parity
           // double buffer) and read in place by the two cell gradients that consume them
           slmk::EpiPartialTma e{B};
-          if ((s = launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
+          LT((launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, skx, M.wMN[l], M.dpRK[l], K, B, 4 * H, 0,
                                                                         slot * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX),
-                                                                        &M.pXd[2 * l + t % 2])) != SLM_OK)
-            return s;
+                                                                        &M.pXd[2 * l + t % 2])));
           ++nl;
           if (flush) {   // dW_l[gate][k_in] += sum over the chunk's rows of op[r][k_in] d_pre[r][gate]
             slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
-            if ((s = launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l],
+            LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l],
                                                                       M.dpRMN[l], K, 4 * H, chunk_rows(t), 0, 0, e2,
-                                                                      cs, pdl, gdbg(SLM_K_GEMM_DW))) != SLM_OK)
-              return s;
+                                                                      cs, pdl, gdbg(SLM_K_GEMM_DW))));
             // db_l += column sums of the chunk's fp32 d_pre rows (time order, plan-independent)
-            CK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, cs, pdl, (const float*)(w + W.dpF[l]),
+            LK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, cs, pdl, (const float*)(w + W.dpF[l]),
                         chunk_rows(t), 4 * H, d.db + (size_t)l * 4 * H));
             nl += 2;
           }
@@ -752,103 +1019,24 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   }
   if (msm) {   // join every stream back into the caller's
     for (int i = 0; i < NSTR; ++i) {
-      CK(cudaEventRecord(S.join[i], S.streams[i]));
-      CK(cudaStreamWaitEvent(st, S.join[i], 0));
+      LK(cudaEventRecord(S.join[i], S.streams[i]));
+      LK(cudaStreamWaitEvent(st, S.join[i], 0));
     }
   }
-  CK(cudaGetLastError());
-  m.ts_used = ts_slot;
+  LK(cudaGetLastError());
+  if (!dry) m.ts_used = ts_slot;
   if (launches) *launches = nl;
   return SLM_OK;
 }
 
-// kernels enqueue_lstm launches for this plan (the memsets are not counted); mirrors its
-// fusion and operand-residency decisions
-int64_t lstm_launches(const slm_plan* p, const slm_lstm_desc& d, int gates_sk, int fuse_cell) {
-  int64_t nl = 0;
-  const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, N = p->n_fwd, CH = kLstmChunk;
-  OperandTracker trk(L);
-  auto tl = [&](int o) {
-    if (o == N - 1) return std::make_pair(T - 1, L);
-    return std::make_pair(o / per_t, (o % per_t - 1) / 2);
-  };
-  std::vector<int> owner(p->tag_size.size(), -1);
-  std::vector<char> hb_batched(T, 0);
-  const LstmSplits sp = lstm_splits(d, gates_sk);
-  auto head_state = [&](int t) {
-    const int gh = p->gnode[t * per_t + per_t - 1];
-    return gh < 0 ? -1 : p->preds[p->pred_ptr[gh + 1] - 1];
-  };
-  const std::vector<int>& order = p->order;
-  for (size_t oi = 0; oi < order.size(); ++oi) {
-    const int v = order[oi], opk = p->op[v], kind = p->kind[v];
-    if (opk == SLM_OP_INPUT) continue;
-    const auto [t, l] = tl(p->orig[v]);
-    const int* pr = p->preds.data() + p->pred_ptr[v];
-    const int np = p->pred_ptr[v + 1] - p->pred_ptr[v];
-    int partner = -1;
-    if (kind != SLM_KIND_GRAD) {
-      if (opk == SLM_OP_LSTM_GATES) {
-        const int xn = pr[0], hn = np > 1 ? pr[1] : OperandTracker::kZeros;
-        if (trk.gates_needs_pack(l, t, xn, hn)) {
-          ++nl;
-          trk.packed(l, t, xn, hn);
-        }
-        nl += ((l == 0 ? sp.g0 : sp.g1) == 1 && fuse_cell) ? 1 : 2;   // GEMM with the cell epilogue, or + gates/cell kernel
-        if (oi + 1 < order.size()) {
-          const int u = order[oi + 1];
-          if (p->op[u] == SLM_OP_LSTM_CELL && p->kind[u] == kind && p->preds[p->pred_ptr[u]] == v) {
-            trk.cell(u, l, t, L, T, (t + 1) * per_t);
-            partner = u;
-            ++oi;
-          }
-        }
-      } else if (opk == SLM_OP_LSTM_CELL) {
-        trk.cell(v, l, t, L, T, (t + 1) * per_t);
-        ++nl;
-      } else if (opk == SLM_OP_HEAD_CE) {
-        if (t % CH == CH - 1 || t == T - 1) {   // batched forward heads
-          nl += 3;
-          for (int t2 = t - t % CH; t2 <= t; ++t2) owner[p->node_tag[t2 * per_t + per_t - 1]] = t2 * per_t + per_t - 1;
-        }
-      } else {
-        ++nl;
-      }
-    } else {
-      const bool flush = t % CH == 0;
-      if (opk == SLM_OP_HEAD_CE) {
-        if (hb_batched[t]) continue;
-        int lo = t + 1;
-        for (int t2 = t; t2 >= t - t % CH; --t2) {
-          const int a = head_state(t2);
-          if (a < 0 || owner[p->node_tag[a]] != a) break;
-          lo = t2;
-        }
-        if (lo < t) {   // batched head backward of steps lo..t
-          nl += 5 + (lo % CH == 0);
-          for (int t2 = lo; t2 <= t; ++t2) hb_batched[t2] = 1;
-        } else {
-          nl += 5 + flush;
-        }
-      } else if (opk == SLM_OP_LSTM_GATES) {
-        nl += 2 + 2 * flush;   // d_pre/pack, dX GEMM (+ dW GEMM and db column sums)
-      } else if (opk == SLM_OP_LSTM_CELL) {
-        const int u = oi + 1 < order.size() ? order[oi + 1] : -1;
-        if (u >= 0 && p->op[u] == SLM_OP_LSTM_GATES && p->kind[u] == SLM_KIND_GRAD && p->preds[p->pred_ptr[u]] == v) {
-          nl += 2 + 2 * flush;   // fused cell/d_pre/pack + dX GEMM
-          partner = u;
-          ++oi;
-        } else {
-          nl += 1;
-        }
-      } else {
-        nl += 1;
-      }
-    }
-    for (int node : {v, partner})
-      if (node >= 0) owner[p->node_tag[node]] = node;
-  }
-  return nl;
+#undef LK
+#undef LT
+
+// kernels enqueue_lstm launches for this plan (the memsets are not counted): a dry run
+int64_t lstm_launches(const slm_plan* p, const slm_model& m) {
+  int64_t n = 0;
+  enqueue_lstm(p, const_cast<slm_model&>(m), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &n, true);
+  return n;
 }
 
 }  // namespace

@@ -12,131 +12,40 @@
 
 namespace slmk {
 
-// 1 = every LSTM SIMT kernel signals griddepcontrol.launch_dependents right after its own
-// griddepcontrol.wait, so the next kernel of the chain is scheduled (and runs its prologue)
-// while this one works; the dependent still waits for this grid's completion before reading
-// its outputs (option lstm_early_trigger, default 1).
-__constant__ int c_lstm_trigger = 1;
+// every LSTM SIMT kernel waits for its predecessor (griddepcontrol.wait) and then releases its
+// dependent launch, so the next kernel of the chain is scheduled and runs its prologue while this
+// one works (the dependent still waits for this grid's completion before reading its outputs)
 __device__ __forceinline__ void lstm_entry() {
   pdl_wait();
-  if (c_lstm_trigger) pdl_launch();
+  pdl_launch();
 }
 
-// bf16 GEMM-operand side outputs of a cell-state kernel (S^l_t = (h, c)): the executor keeps
-// the next consumers' operands resident instead of re-packing them (executor_lstm.cuh):
-//   h_self  -> h part of layer l's operand (read by G^l_{t+1}),      row stride ld_self
-//   h_up    -> x part of layer l+1's operand, or the head operand,   row stride ld_up
-//   xnext   -> (layer 0) the next step's input x_{t+1} [B][I] fp32, written zero-padded to
-//              Kin0 columns into x0 (row stride ld0)
-struct OpOut {
-  __nv_bfloat16* h_self;
-  int ld_self;
-  __nv_bfloat16* h_up;
-  int ld_up;
-  const float* xnext;
-  int I, Kin0;
-  __nv_bfloat16* x0;
-  int ld0;
-};
-__device__ __forceinline__ void op_out_h(const OpOut& o, int b, int j, float h) {
-  const __nv_bfloat16 hb = __float2bfloat16_rn(h);
-  if (o.h_self) o.h_self[(size_t)b * o.ld_self + j] = hb;
-  if (o.h_up) o.h_up[(size_t)b * o.ld_up + j] = hb;
-}
-__device__ __forceinline__ void op_out_x(const OpOut& o, int B) {
-  if (!o.xnext) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * o.Kin0; i += gridDim.x * blockDim.x) {
-    const int b = i / o.Kin0, k = i % o.Kin0;
-    o.x0[(size_t)b * o.ld0 + k] = __float2bfloat16_rn(k < o.I ? o.xnext[(size_t)b * o.I + k] : 0.f);
-  }
+// tanh on the SFU (tanh.approx.f32, MUFU.TANH: relative error <= 2^-10.99): the forward cell and
+// gate activations (lstm_run.cuh) -- reading A26 in DESIGN.md
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-
-// op[b][0:Kin] = x (width xw, zero padded to Kin, source row stride xs), op[b][Kin:Kin+H] = h_prev
-// (h part of S_{t-1}: row stride 2H; null = zeros).  bf16 GEMM operand [B][Kin+H].
-__global__ void __launch_bounds__(256) lstm_pack_kernel(const float* __restrict__ x, int xw, int xs, int Kin,
-                                                        const float* __restrict__ sprev, int H, int B,
-                                                        __nv_bfloat16* __restrict__ op) {
-  lstm_entry();
-  const int K = Kin + H;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * K; i += gridDim.x * blockDim.x) {
-    const int b = i / K, k = i % K;
-    float v;
-    if (k < Kin)
-      v = k < xw ? x[(size_t)b * xs + k] : 0.f;
-    else
-      v = sprev ? sprev[(size_t)b * 2 * H + (k - Kin)] : 0.f;
-    op[i] = __float2bfloat16_rn(v);
-  }
-}
-
-// S = (h, c): c = f c_prev + i g, h = o tanh(c)   (sprev null: c_prev = 0)
+// S = (h, c): c = f c_prev + i g, h = o tanh(c)   (sprev null: c_prev = 0) -- an isolated cell
+// node (node by node); the same arithmetic as the run kernel's cell (lstm_run.cuh).  h also goes
+// as bf16 into hring [B][H] (the lane's chunk ring slot).
 __global__ void __launch_bounds__(256) lstm_cell_fwd_kernel(const float* __restrict__ act,
                                                             const float* __restrict__ sprev, int H, int B,
-                                                            float* __restrict__ s, OpOut oo) {
+                                                            float* __restrict__ s, __nv_bfloat16* __restrict__ hring) {
   lstm_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
     const int b = i / H, j = i % H;
     const float* a = act + (size_t)b * 4 * H;
     const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
     const float c = __fadd_rn(__fmul_rn(a[H + j], cp), __fmul_rn(a[j], a[2 * H + j]));
-    const float h = __fmul_rn(a[3 * H + j], tanhf(c));
+    const float h = __fmul_rn(a[3 * H + j], tanh_fast(c));
     s[(size_t)b * 2 * H + j] = h;
     s[(size_t)b * 2 * H + H + j] = c;
-    op_out_h(oo, b, j, h);
+    hring[i] = __float2bfloat16_rn(h);
   }
-  op_out_x(oo, B);
 }
-
-// tcgen05 GEMM epilogue of a gates node computed without split-K (tc_gemm.cuh, EpiCell): the
-// CTA's tile holds gate q = warp of 32 hidden units (TMEM lane = unit) for BN batch columns;
-// each warp activates its gate (pre = acc + b, sigmoid / tanh) and writes G, the four gates
-// meet in shared memory, and -- when the cell S^l_t is fused (s_out) -- the CTA computes
-// c = f c_prev + i g, h = o tanh c for its units and writes S and the operand side outputs.
-// The arithmetic is lstm_gates_cell_kernel's with one K slice, so both give identical bits.
-struct EpiGatesCell {
-  static constexpr bool kTma = false;
-  static constexpr bool kCell = true;
-  float* g_out;
-  float* s_out;
-  const float* sprev;
-  const float* bias;
-  int H, B;
-  OpOut oo;
-  __device__ __forceinline__ void operator()(int, int, const float*, int) const {}
-  template <int BN>
-  __device__ __forceinline__ void cell(uint32_t trow, int m0, int n0, int warp, int lane, float* sm) const {
-    constexpr int LD = BN + 1;   // padded rows: conflict-free in both passes
-    const int q = warp, j = (m0 >> 2) + lane;
-    const float bq = bias[q * H + j];
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float acc[32];
-      tmem_ld32(trow + c, acc);
-#pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
-        const float pre = __fadd_rn(acc[jj], bq);
-        const float a = q == 2 ? tanhf(pre) : __frcp_rn(__fadd_rn(1.f, expf(-pre)));
-        g_out[(size_t)(n0 + c + jj) * 4 * H + q * H + j] = a;
-        sm[(q * 32 + lane) * LD + c + jj] = a;
-      }
-    }
-    __syncthreads();
-    if (!s_out) return;
-    for (int idx = threadIdx.x; idx < 32 * BN; idx += blockDim.x) {
-      const int u = idx % 32, nl = idx / 32, n = n0 + nl, ju = (m0 >> 2) + u;
-      const float ig = sm[u * LD + nl], fg = sm[(32 + u) * LD + nl], gg = sm[(64 + u) * LD + nl],
-                  og = sm[(96 + u) * LD + nl];
-      const float cp = sprev ? sprev[(size_t)n * 2 * H + H + ju] : 0.f;
-      const float cc = __fadd_rn(__fmul_rn(fg, cp), __fmul_rn(ig, gg));
-      const float h = __fmul_rn(og, tanhf(cc));
-      s_out[(size_t)n * 2 * H + ju] = h;
-      s_out[(size_t)n * 2 * H + H + ju] = cc;
-      op_out_h(oo, n, ju, h);
-    }
-    op_out_x(oo, B);
-  }
-};
 
 // Back through S: dS = sum of up to 3 successor slices (dh | dc), each [B][2H] with row stride
 // ld_k (null = absent), added in the fixed order 0, 1, 2.  Output rows (pred order, reading
@@ -214,40 +123,6 @@ __global__ void __launch_bounds__(256) lstm_dpre_kernel(const float* __restrict_
     dpre_f[i] = dv;
   }
   pack_op(x, xw, xs, Kin, sprev, H, B, op);
-}
-
-// G = act(sum_s P[s] + b) from the split-K partials P [sk][B][4H] (fixed slice order), and —
-// when s_out is given — the fused cell S = (h, c) = (o tanh(c), f c_prev + i g) (same
-// arithmetic as lstm_cell_fwd_kernel, so fused and separate runs are bit-identical).
-__global__ void __launch_bounds__(256) lstm_gates_cell_kernel(const float* __restrict__ P, int sk,
-                                                              const float* __restrict__ bias, int H, int B,
-                                                              float* __restrict__ g_out,
-                                                              const float* __restrict__ sprev,
-                                                              float* __restrict__ s_out, OpOut oo) {
-  lstm_entry();
-  const size_t slice = (size_t)B * 4 * H;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * H; i += gridDim.x * blockDim.x) {
-    const int b = i / H, j = i % H;
-    float a[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const size_t e = (size_t)b * 4 * H + q * H + j;
-      float acc = P[e];
-      for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, P[s * slice + e]);
-      const float pre = __fadd_rn(acc, bias[q * H + j]);
-      a[q] = q == 2 ? tanhf(pre) : __frcp_rn(__fadd_rn(1.f, expf(-pre)));
-      g_out[e] = a[q];
-    }
-    if (s_out) {
-      const float cp = sprev ? sprev[(size_t)b * 2 * H + H + j] : 0.f;
-      const float c = __fadd_rn(__fmul_rn(a[1], cp), __fmul_rn(a[0], a[2]));
-      const float h = __fmul_rn(a[3], tanhf(c));
-      s_out[(size_t)b * 2 * H + j] = h;
-      s_out[(size_t)b * 2 * H + H + j] = c;
-      op_out_h(oo, b, j, h);
-    }
-  }
-  if (s_out) op_out_x(oo, B);
 }
 
 __device__ __forceinline__ float dpre_of(int q, float da, float a) {   // d_pre = d(act) * act'

@@ -115,6 +115,7 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 
 #include "executor.cuh"
 #include "lstm_kernels.cuh"
+#include "lstm_run.cuh"
 #include "executor_lstm.cuh"
 
 extern "C" {
@@ -209,6 +210,9 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
   else if (k == "lstm_sk") m->lstm_sk = (int)value;
   else if (k == "lstm_skx") m->lstm_skx = (int)value;
+  else if (k == "lstm_fuse_runs") m->lstm_fuse_runs = (int)value;
+  else if (k == "lstm_run_ts") m->lstm_run_ts = reinterpret_cast<void*>(value);
+  else if (k == "lstm_run_ts_n") m->lstm_run_ts_n = (int)value;
   // measurement hooks
   else if (k == "profile_ts") {
     m->profile_ts = (int)value;
@@ -295,7 +299,7 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (m->kind == SLM_MODEL_LSTM) {
-    *launches = lstm_launches(p, m->ld, m->lstm_sk, m->lstm_fuse_cell);
+    *launches = lstm_launches(p, *m);
     return SLM_OK;
   }
   std::vector<Op> ops;

@@ -243,7 +243,6 @@ struct EpiPartial {
   }
 };
 
-// LSTM gates: out[n*4H + m] = act_m(acc + b[m]), sigmoid for the i, f, o blocks, tanh for g
 // gradient accumulation in place across time steps: out[n*ld+m] += acc
 struct EpiAccF32 {
   static constexpr bool kTma = false;
@@ -280,14 +279,6 @@ template <class E, class = void>
 struct EpiHalf : std::false_type {};
 template <class E>
 struct EpiHalf<E, std::void_t<decltype(E::kHalf)>> : std::bool_constant<E::kHalf> {};
-
-// Epilogues with kCell = true (the LSTM gates + cell epilogue, lstm_kernels.cuh) load A as four
-// 32-row boxes, rows q*H + m0/4 .. +32 of gate q (one tile = 32 hidden units x 4 gates), and
-// run their own cell(...) epilogue with the whole CTA.
-template <class E, class = void>
-struct EpiCell : std::false_type {};
-template <class E>
-struct EpiCell<E, std::void_t<decltype(E::kCell)>> : std::bool_constant<E::kCell> {};
 
 // ---------------------------------------------------------------- the kernel
 template <int BN, bool A_MN, bool B_MN, int CG = 1>
@@ -457,9 +448,6 @@ __global__ void __launch_bounds__(128, 1)
     if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
       tma(sa, &tmA, s, m0, a_row0 + k0);
       tma(sa + 8192, &tmA, s, m0 + 64, a_row0 + k0);
-    } else if constexpr (EpiCell<Epi>::value) {   // gate-interleaved tile: four 64(K) x 32 boxes
-#pragma unroll
-      for (int q = 0; q < 4; ++q) tma(sa + q * 4096, &tmA, s, k0, a_row0 + q * epi.H + (m0 >> 2));
     } else {     // A stored [M][K]: one box of 64(K) x 128(M)
       tma(sa, &tmA, s, k0, a_row0 + m0);
     }
@@ -558,9 +546,7 @@ __global__ void __launch_bounds__(128, 1)
   ts_mark(tsp, 2, dbg);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const int m = m0 + warp * 32 + lane;
-  if constexpr (EpiCell<Epi>::value) {
-    epi.template cell<BN>(trow, m0, n0, warp, lane, reinterpret_cast<float*>(smem));
-  } else if constexpr (Epi::kTma) {
+  if constexpr (Epi::kTma) {
     // fp32 (or bf16, EpiHalf) tile -> smem box [32 n][128 m] (a warp writes 128 (64) contiguous
     // bytes: conflict-free) -> cp.async.bulk.tensor store, double-buffered; the pipeline smem is
     // free after the MMAs.

@@ -139,15 +139,14 @@ def test_lstm_launch_count(slm):
     p, g, x, y = _dev(inp, L, H, C)
     model = slm.LstmModel(p, g, L, T, B, H, I, C, use_graph=0)
     plan = slm.Plan(slm.Graph.lstm(L, T, B, H, I), "none")
-    # forward: per t, per layer the gates GEMM and the fused gates/cell kernel; the operands are
-    # packed only at t = 0
-    # (afterwards the cell kernels write them); the heads run batched per 32-step chunk
-    # (logits GEMM, CE rows, per-step losses); Sum 1.
+    # forward (one fused phase, lstm_run.cuh): per layer one run of the T = 4 steps (the input
+    # projection GEMM and the persistent run kernel; layer 0 also packs its input); the heads run
+    # batched per 32-step chunk (logits GEMM, CE rows, per-step losses); Sum 1.
     # backward: fill 1; the head gradients batched per 32-step chunk (pack, logits GEMM, CE,
     # dh GEMM, dh + db_o, dW_o GEMM); per t and layer 2 (fused cell / d_pre / pack, dX GEMM whose
     # partials the next cell gradients read in place); per chunk one weight-gradient GEMM + db
     # column sum per layer (T = 4: one chunk)
-    assert model.launches(plan) == T * 2 * L + L + 3 + 1 + 1 + 6 + T * 2 * L + 2 * L
+    assert model.launches(plan) == 2 * L + 1 + 3 + 1 + 1 + 6 + T * 2 * L + 2 * L
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
