@@ -281,6 +281,8 @@ struct LstmMaps {
   // the chunk ring [2 CH B][H] and the packed operand [kRunMax B][Kin] as GEMM B operands (box
   // rows 64 / 256)
   std::vector<CUtensorMap> hxM, xpM, ringM[2], xopM[2];
+  // backward runs: the d_pre ring as a 256-row B operand, the d_pre exchange (box 64 x B)
+  std::vector<CUtensorMap> dpR256, dpxM;
   const void* ws = nullptr;
 };
 struct slm_lstm_state {

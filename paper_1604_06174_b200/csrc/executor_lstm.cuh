@@ -49,7 +49,14 @@ struct LstmWs {
   // bf16 and c [B][H] fp32, the chunk ring [2][CH B][H] bf16 of h, the packed input-projection
   // operand [kRunMax B][Kin] bf16 and the projection X [kRunMax B][4H] fp32
   std::vector<size_t> hx, cst, ring, xop, xp;
+  // per layer, backward runs (batch 64): d_pre exchange [2][B][4H] bf16, dc state [B][H], the
+  // partial exchange [H/128][4][4][B][32] fp32, the gradient from the layer above [2][CH B + 256][H]
+  // fp32 (chunk parity; 256 rows of slack for the padded projection), step / exchange counters
+  std::vector<size_t> dpx, dcst, xch, dxa;
+  size_t bbar;
 };
+// the backward runs (lstm_run.cuh) serve batch 64; other batches keep the node-by-node backward
+inline bool lstm_bwd_runs(const slm_lstm_desc& d) { return d.batch == 64; }
 
 inline int lstm_kin0(int n_in) { return (n_in + 127) / 128 * 128; }   // keeps K_0 = Kin0 + H a multiple of 128
 inline int lstm_cpad(int C) { return (C + 127) / 128 * 128; }
@@ -121,6 +128,14 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
   L.PH = off;       off += al((size_t)sp.hd * CH * B * H * 4);  // split-K partials of the batched dh GEMM
   L.dlR = off;      off += al(CH * B * Cp * 2);
   L.bar = off;      off += al(2 * d.n_layers * 4);
+  L.bbar = off;     off += al((size_t)d.n_layers * (1 + H / 128) * 4);
+  if (lstm_bwd_runs(d))
+    for (int l = 0; l < d.n_layers; ++l) {
+      L.dpx.push_back(off);  off += al(2 * B * 4 * H * 2);
+      L.dcst.push_back(off); off += al(B * H * 4);
+      L.xch.push_back(off);  off += al((H / 128) * 16 * B * 32 * 4);
+      L.dxa.push_back(off);  off += 2 * al((CH * B + 256) * H * 4);
+    }
   const size_t RM = slmk::kRunMax;
   for (int ln = 0; ln < 2 * d.n_layers; ++ln) {
     const size_t kin = (ln % d.n_layers) == 0 ? (size_t)lstm_kin0(d.n_in) : H;
@@ -163,6 +178,8 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   M.opRMN.resize(nl);
   M.dpRK.resize(nl);
   M.dpRMN.resize(nl);
+  M.dpR256.resize(nl);
+  M.dpxM.resize(nl);
   M.pX.resize(nl);
   M.pG.resize(nl);
   M.pGm.resize(nl);
@@ -178,6 +195,8 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
     if ((st = make_map(&M.opRMN[l], w + L.opR[l], K, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
+    if ((st = make_map(&M.dpR256[l], w + L.dpR[l], 4 * H, CH * B, 256)) != SLM_OK) return st;
+    if (lstm_bwd_runs(d) && (st = make_map(&M.dpxM[l], w + L.dpx[l], 4 * H, 2 * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pX[l], w + L.P[l], K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
     for (int par = 0; par < 2; ++par) {
       const size_t bytes = ((size_t)(l == 0 ? sp.x0 : sp.x1) * B * K * 4 + 255) / 256 * 256;
@@ -228,7 +247,9 @@ struct LstmNode {
 
 // ---- schedule (see the header): launch units in issue order and the materialised set
 struct LstmUnit {
-  int type = 0;                       // 0 = the V' node at order index oi (+ fused successor), 1 = run
+  int type = 0;                       // 0 = the V' node at order index oi (+ fused successor), 1 = run,
+                                      // 2 = backward run (steps t0, t0-1, .. t0-n+1; g = the g[S] nodes),
+                                      // 3 = input gradient + weight-gradient flush of steps t0 .. t0+n-1
   int oi = -1;
   int l = 0, k = 0, t0 = 0, n = 0;    // run: layer, kind (0 forward, 1 mirror), first step, steps
   int g[slmk::kRunMax], s[slmk::kRunMax];   // the run's gates / cell nodes (s = -1: gates only)
@@ -239,7 +260,7 @@ struct LstmSched {
   int fused = 0;           // phases issued chunk by chunk, layer by layer
 };
 
-LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse) {
+LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse, bool bwd_runs) {
   const int L = d.n_layers, T = d.steps, per_t = 2 * L + 2, CH = kLstmChunk, RM = slmk::kRunMax;
   const std::vector<int>& order = p->order;
   const int nn = (int)p->kind.size();
@@ -279,11 +300,91 @@ LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse) {
   auto kind01 = [&](int v) { return p->kind[v] == SLM_KIND_MIRROR ? 1 : 0; };
   std::vector<char> inph(nn, 0);
   auto is_grad = [&](const Item& it) { return it.g < 0 && p->kind[order[it.oi]] == SLM_KIND_GRAD; };
+  auto grad_op = [&](const Item& it, int o) { return is_grad(it) && op(order[it.oi]) == o; };
   size_t a0 = 0;
   while (a0 < items.size()) {
-    if (is_grad(items[a0])) {
+    if (is_grad(items[a0]) && !bwd_runs) {
       node_unit(items[a0].oi);
       ++a0;
+      continue;
+    }
+    if (is_grad(items[a0])) {
+      // ---- gradient phase [a0, a1): g[S^l_t] -> backward runs, g[G^l_t] -> input gradient /
+      // weight-gradient flush units.  Fused (chunk by chunk descending, layer by layer from the top)
+      // when every g[S^l_t] of the phase has its g[G^l_t] in the phase and vice versa; else node by
+      // node in V' order with runs of one step.
+      size_t a1 = a0;
+      while (a1 < items.size() && is_grad(items[a1])) ++a1;
+      bool ok = fuse;
+      for (size_t i = a0; i < a1; ++i) inph[order[items[i].oi]] = 1;
+      auto gnode_of = [&](int gv, int dlt) { return p->gnode[p->orig[gv] + dlt]; };   // g[S^l_t] -> g[G^l_t]: orig - 1
+      for (size_t i = a0; i < a1 && ok; ++i) {
+        const int v = order[items[i].oi];
+        if (op(v) == SLM_OP_LSTM_CELL) ok = gnode_of(v, -1) >= 0 && inph[gnode_of(v, -1)];
+        else if (op(v) == SLM_OP_LSTM_GATES) ok = gnode_of(v, 1) >= 0 && inph[gnode_of(v, 1)];
+      }
+      auto bunit = [&](int type, int l, int t0, int n, const int* gs) {
+        LstmUnit u;
+        u.type = type;
+        u.l = l;
+        u.t0 = t0;
+        u.n = n;
+        for (int i = 0; i < n && gs; ++i) u.g[i] = gs[i];
+        S.units.push_back(u);
+      };
+      if (!ok) {
+        for (size_t i = a0; i < a1; ++i) {
+          const int v = order[items[i].oi];
+          if (op(v) == SLM_OP_LSTM_CELL) bunit(2, lof(v), tof(v), 1, &v);
+          else if (op(v) == SLM_OP_LSTM_GATES) bunit(3, lof(v), tof(v), 1, nullptr);
+          else node_unit(items[i].oi);
+        }
+      } else {
+        ++S.fused;
+        for (size_t i = a0; i < a1; ++i)   // g[Sum] and other non-step nodes first, in V' order
+          if (!grad_op(items[i], SLM_OP_LSTM_CELL) && !grad_op(items[i], SLM_OP_LSTM_GATES) &&
+              !grad_op(items[i], SLM_OP_HEAD_CE))
+            node_unit(items[i].oi);
+        // per chunk (descending): its head gradients in V' order, then per layer (top first) the
+        // runs of its g[S] nodes, each followed by its input-gradient / flush unit
+        std::vector<std::vector<int>> byc((T + CH - 1) / CH), lay((size_t)L * ((T + CH - 1) / CH));
+        for (size_t i = a0; i < a1; ++i) {
+          const int v = order[items[i].oi];
+          if (op(v) == SLM_OP_HEAD_CE) byc[tof(v) / CH].push_back(items[i].oi);
+          else if (op(v) == SLM_OP_LSTM_CELL) lay[(size_t)(tof(v) / CH) * L + lof(v)].push_back(v);
+        }
+        for (int c = (int)byc.size() - 1; c >= 0; --c) {
+          for (int oi : byc[c]) node_unit(oi);
+          // the chunk's runs: RM-step blocks descending, inside a block the layers from the top
+          // (a wavefront with a lag of one block between neighbouring layers)
+          std::vector<std::vector<LstmUnit>> blk((CH + RM - 1) / RM);
+          for (int l = L - 1; l >= 0; --l) {
+            std::vector<int>& gsv = lay[(size_t)c * L + l];
+            std::sort(gsv.begin(), gsv.end(), [&](int x, int y) { return tof(x) > tof(y); });
+            size_t k0 = 0;
+            while (k0 < gsv.size()) {
+              size_t k1 = k0 + 1;
+              while (k1 < gsv.size() && tof(gsv[k1]) == tof(gsv[k1 - 1]) - 1 && tof(gsv[k1]) / RM == tof(gsv[k0]) / RM) ++k1;
+              const int n = (int)(k1 - k0), th = tof(gsv[k0]);
+              LstmUnit u2, u3;
+              u2.type = 2;
+              u2.l = u3.l = l;
+              u2.t0 = th;
+              u2.n = u3.n = n;
+              for (int i = 0; i < n; ++i) u2.g[i] = gsv[k0 + i];
+              u3.type = 3;
+              u3.t0 = th - n + 1;
+              blk[(th % CH) / RM].push_back(u2);
+              blk[(th % CH) / RM].push_back(u3);
+              k0 = k1;
+            }
+          }
+          for (int b = (int)blk.size() - 1; b >= 0; --b)
+            for (const LstmUnit& u : blk[b]) S.units.push_back(u);
+        }
+      }
+      for (size_t i = a0; i < a1; ++i) inph[order[items[i].oi]] = 0;
+      a0 = a1;
       continue;
     }
     size_t a1 = a0;
@@ -392,7 +493,7 @@ LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse) {
         u.k = ln / L;
         for (auto& gs : lane[ln]) {
           const int t = tof(gs.first);
-          if (u.n > 0 && (t != u.t0 + u.n || t / CH != u.t0 / CH || u.n == RM)) {
+          if (u.n > 0 && (t != u.t0 + u.n || t / RM != u.t0 / RM)) {   // runs stay inside an RM-step block
             runs.push_back(u);
             u.n = 0;
           }
@@ -403,8 +504,10 @@ LstmSched lstm_schedule(const slm_plan* p, const slm_lstm_desc& d, bool fuse) {
         }
         if (u.n > 0) runs.push_back(u);
       }
+      // block by block, layer by layer inside a block: layer l's run of a block waits only for
+      // layer l-1's run of the same block (a wavefront with a lag of one block)
       std::stable_sort(runs.begin(), runs.end(), [&](const LstmUnit& x, const LstmUnit& y) {
-        return std::make_tuple(x.t0 / CH, x.l, x.k, x.t0) < std::make_tuple(y.t0 / CH, y.l, y.k, y.t0);
+        return std::make_tuple(x.t0 / RM, x.l, x.k, x.t0) < std::make_tuple(y.t0 / RM, y.l, y.k, y.t0);
       });
       std::vector<int> head_oi(T / CH + 2, -1);   // V' index of each chunk's last forward head
       int sum_oi = -1;
@@ -448,6 +551,18 @@ template <class... KArgs, class... Args>
 cudaError_t launch_run(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
                        Args... args) {
   return launch_kc(k, grid, block, smem, st, pdl, 1, args...);
+}
+
+slm_status launch_bwd_run(const CUtensorMap& w, const CUtensorMap& dpx, const slmk::BwdRun& a, cudaStream_t st,
+                          bool pdl) {
+  using C = slmk::BwdRunCfg;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(slmk::lstm_bwd_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CK(launch_run(slmk::lstm_bwd_run_kernel, dim3(a.H / 32), dim3(slmk::kRunThreads), C::SMEM, st, pdl, w, dpx, a));
+  return SLM_OK;
 }
 
 template <int B>
@@ -547,6 +662,16 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   // backward visits each layer's steps in descending t, so the chunk's lowest t comes last)
   auto chunk_rows = [&](int t) { return std::min(CH, T - (t / CH) * CH) * B; };
 
+  // backward runs: step / exchange counters, the lowest step each layer's state belongs to
+  const bool bwdr = lstm_bwd_runs(d);
+  unsigned* bbar = (unsigned*)(w + W.bbar);
+  if (bwdr) LK(cudaMemsetAsync(bbar, 0, (size_t)L * (1 + H / 128) * 4, st));
+  std::vector<unsigned> bbar_val(L, 0u), bxbar_val(L, 0u);
+  std::vector<int> bstate(L, -1);
+  auto dxa_ptr = [&](int l, int t) {   // rows of step t in the gradient layer l receives from layer l+1
+    return (float*)(w + W.dxa[l] + ((t / CH) % 2) * (((size_t)(CH * B + 256) * H * 4 + 255) / 256 * 256)) +
+           (size_t)(t % CH) * B * H;
+  };
   // ---- forward lanes (layer l, kind k): side state and which V' node each holds
   auto lane_of = [&](int l, int k) { return l + L * k; };
   std::vector<int> hx_node(2 * L, -1), cs_node(2 * L, -1);
@@ -570,8 +695,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const int ntag = (int)p->tag_size.size();
   auto DHR = [&](int par) { return ntag + par; };                       // batched (dh | 0) ring, chunk parity
   auto PXR = [&](int l, int par) { return ntag + 2 + 2 * l + par; };    // dX partials of layer l
-  auto RNG = [&](int ln, int par) { return ntag + 2 + 2 * L + 2 * ln + par; };   // forward chunk ring
-  const int HOP = ntag + 2 + 6 * L;   // the number of resources
+  // the chunk ring of a forward lane and the gradient layer l receives from layer l+1 are tracked
+  // per RM-step block (rows of different blocks are disjoint): block id (t / RM) mod NBK
+  constexpr int NBK = 2 * kLstmChunk / slmk::kRunMax;
+  auto bk = [&](int t) { return (t / slmk::kRunMax) % NBK; };
+  auto RNG = [&](int ln, int t) { return ntag + 2 + 2 * L + NBK * ln + bk(t); };            // forward ring
+  auto DXA = [&](int l, int t) { return ntag + 2 + 2 * L + NBK * 2 * L + NBK * l + bk(t); };  // from layer l+1
+  const int HOP = ntag + 2 + 2 * L + 3 * NBK * L;   // the number of resources
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -657,7 +787,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     return lo;
   };
 
-  const LstmSched sched = lstm_schedule(p, d, m.lstm_fuse_runs != 0);
+  const LstmSched sched = lstm_schedule(p, d, m.lstm_fuse_runs != 0, bwdr);
   int run_idx = 0;
   const std::vector<int>& order = p->order;
   int skip_oi = -1;
@@ -668,7 +798,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       // cell = false: a lone gates node (n = 1, node by node); a fused run may end with a gates
       // node whose cell is not in the phase: its cell goes to the side buffers only
       const bool cell = n > 1 || U.s[0] >= 0;
-      const int sid = (k == 1 && NSTR > L + 1) ? L + 1 + l : l;
+      // with backward runs, re-computed runs share the layer's stream: at most one persistent
+      // kernel per layer stream (<= L H / 32 resident CTAs), so every run's CTAs can be resident
+      const int sid = (k == 1 && NSTR > L + 1 && !bwdr) ? L + 1 + l : l;
       const int Kin = l == 0 ? K0 : H;
       const int sprev = t0 > 0 ? preds_of(U.g[0]).first[1] : -1;
       const int init = sprev < 0 ? 1 : (hx_node[ln] == sprev && cs_node[ln] == sprev ? 0 : 2);
@@ -679,14 +811,16 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       rd.clear();
       wr.clear();
       if (init == 2) rd.push_back(p->node_tag[sprev]);
-      if (l > 0 && xring) rd.push_back(RNG(lane_of(l - 1, k), (t0 / CH) % 2));
+      if (l > 0 && xring)
+        for (int i = 0; i < n; ++i) rd.push_back(RNG(lane_of(l - 1, k), t0 + i));
       if (l > 0 && !xring)
         for (int i = 0; i < n; ++i) rd.push_back(p->node_tag[preds_of(U.g[i]).first[0]]);
       for (int i = 0; i < n; ++i) {
         if (sched.mat[U.g[i]]) wr.push_back(p->node_tag[U.g[i]]);
         if (U.s[i] >= 0 && sched.mat[U.s[i]]) wr.push_back(p->node_tag[U.s[i]]);
       }
-      if (cell) wr.push_back(RNG(ln, (t0 / CH) % 2));
+      if (cell)
+        for (int i = 0; i < n; ++i) wr.push_back(RNG(ln, t0 + i));
       cudaStream_t cs = st;
       if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
       m.ts_cur_aux = sid * 4 + k;
@@ -727,6 +861,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       a.cstate = (float*)(w + W.cst[ln]);
       a.hring = cell ? ring_ptr(ln, t0) : nullptr;
       a.bar = bar + ln;
+      a.dbg = gdbg(SLM_K_BN_ACT);   // profile_ts: forward runs counted under kind 0
       a.ts = (m.lstm_run_ts && run_idx < m.lstm_run_ts_n)
                  ? (unsigned long long*)m.lstm_run_ts + (size_t)run_idx * slmk::kRunMax * 16
                  : nullptr;
@@ -751,6 +886,102 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         if (sched.mat[U.g[i]]) owner[p->node_tag[U.g[i]]] = U.g[i];
         if (U.s[i] >= 0 && sched.mat[U.s[i]]) owner[p->node_tag[U.s[i]]] = U.s[i];
       }
+      continue;
+    }
+    if (U.type == 2 || U.type == 3) {
+      // ===== backward runs (lstm_run.cuh): type 2 = steps t0, t0-1, .., t0-n+1 of layer l; type 3 =
+      // the input gradient of steps t0 .. t0+n-1 for the layer below (one GEMM over their d_pre
+      // ring rows) and, when the chunk is complete, its weight-gradient GEMM and db column sums
+      const int l = U.l, n = U.n, sid = l;
+      const int K = lstm_K(d, l), Kin = l == 0 ? K0 : H;
+      rd.clear();
+      wr.clear();
+      cudaStream_t cs = st;
+      if (U.type == 2) {
+        const int t1 = U.t0;
+        BwdRun a{};
+        a.H = H;
+        a.n = n;
+        a.t1 = t1;
+        a.Kin = Kin;
+        a.first = t1 == T - 1 ? 1 : 0;
+        if (!a.first && bstate[l] != t1 + 1) {
+          set_error("lstm: backward steps of a layer out of order");
+          return SLM_E_UNSUPPORTED;
+        }
+        a.ldh = l == L - 1 ? 2 * H : H;
+        a.dpx = (bf*)(w + W.dpx[l]);
+        a.dcstate = (float*)(w + W.dcst[l]);
+        a.xch = (float*)(w + W.xch[l]);
+        a.bar = bbar + l;
+        a.base = bbar_val[l];
+        a.xbar = bbar + L + l * (H / 128);
+        a.xbase = bxbar_val[l];
+        a.ts = (m.lstm_run_ts && run_idx < m.lstm_run_ts_n)
+                   ? (unsigned long long*)m.lstm_run_ts + (size_t)run_idx * slmk::kRunMax * 16
+                   : nullptr;
+        ++run_idx;
+        for (int i = 0; i < n; ++i) {
+          const int t = t1 - i, gs = U.g[i];
+          auto pp2 = preds_of(gs);
+          const int actn = pp2.first[pp2.second - (t > 0 ? 2 : 1)], spn = t > 0 ? pp2.first[pp2.second - 1] : -1;
+          a.act[i] = V(actn);
+          a.sprev[i] = spn >= 0 ? V(spn) : nullptr;
+          rd.push_back(p->node_tag[actn]);
+          if (spn >= 0) rd.push_back(p->node_tag[spn]);
+          a.dh_in[i] = l == L - 1 ? dh_ring(t) : dxa_ptr(l, t);
+          const int slot = t % CH;
+          a.dpr[i] = (bf*)(w + W.dpR[l]) + (size_t)slot * B * 4 * H;
+          a.dpf[i] = (float*)(w + W.dpF[l]) + (size_t)slot * B * 4 * H;
+        }
+        for (int t = t1 - n + 1; t <= t1; ++t) rd.push_back(l == L - 1 ? DHR((t / CH) % 2) : DXA(l, t));
+        if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
+        m.ts_cur_aux = sid * 4 + 2;
+        bbar_val[l] += (unsigned)(H / 32) * (unsigned)(n + 1);
+        bxbar_val[l] += 4u * (unsigned)(n - a.first);
+        a.dbg = gdbg(SLM_K_BN_BWD);   // profile_ts: backward runs counted under kind 4
+        LT((launch_bwd_run(M.wMN[l], M.dpxM[l], a, cs, pdl)));
+        ++nl;
+        bstate[l] = t1 - n + 1;
+      } else {
+        const int t0 = U.t0, slot0 = t0 % CH;
+        // the weight-gradient operand rows [x_t | h_{t-1}] of the steps, from the tags of a[x]
+        // and a[S_{t-1}] (the preds of g[G^l_t]: [g[S], a[G], a[x], a[S_{t-1}]?])
+        StepPtrs xsp{}, hsp{};
+        for (int i = 0; i < n; ++i) {
+          const int t = t0 + i, gg = p->gnode[t * per_t + 1 + 2 * l];
+          auto pg = preds_of(gg);
+          const int xn = pg.first[pg.second - (t > 0 ? 2 : 1)], hn = t > 0 ? pg.first[pg.second - 1] : -1;
+          xsp.p[i] = V(xn);
+          hsp.p[i] = hn >= 0 ? V(hn) : nullptr;
+          rd.push_back(p->node_tag[xn]);
+          if (hn >= 0) rd.push_back(p->node_tag[hn]);
+        }
+        if (l > 0)
+          for (int t = t0; t < t0 + n; ++t) wr.push_back(DXA(l - 1, t));
+        if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
+        m.ts_cur_aux = sid * 4 + 2;
+        LK(launch_k(lstm_oppack_kernel, gsz((size_t)n * B * K), eb, 0, cs, pdl, xsp, hsp, n, B, l == 0 ? I : H,
+                    l == 0 ? I : 2 * H, Kin, H, (bf*)(w + W.opR[l]) + (size_t)slot0 * B * K));
+        ++nl;
+        if (l > 0) {   // d x_t (the h of layer l-1) = d_pre W_ih over the run's ring rows (N padded to 256)
+          const int npad = (n * B + 255) / 256 * 256;
+          EpiStoreF32Lim e{dxa_ptr(l - 1, t0), H, n * B};
+          LT((launch_tc_bn<EpiStoreF32Lim, true, false, true>(256, 1, M.wMN[l], M.dpR256[l], H, npad, 4 * H, 0,
+                                                              slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
+          ++nl;
+        }
+        if (slot0 == 0) {   // the chunk is complete: dW_l += op^T d_pre over its rows, db_l += column sums
+          slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
+          LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l], M.dpRMN[l], K,
+                                                               4 * H, chunk_rows(t0), 0, 0, e2, cs, pdl,
+                                                               gdbg(SLM_K_GEMM_DW))));
+          LK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, cs, pdl, (const float*)(w + W.dpF[l]),
+                      chunk_rows(t0), 4 * H, d.db + (size_t)l * 4 * H));
+          nl += 2;
+        }
+      }
+      if (msm && (s = unit_end(sid)) != SLM_OK) return s;
       continue;
     }
     const int oi = U.oi;
@@ -786,13 +1017,13 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       if (opk == SLM_OP_LSTM_CELL) {
         // an isolated cell node (its gates node not right before it in V'): h into the ring of
         // its lane, the lane's recurrent state becomes stale
-        wr.push_back(RNG(lane_of(l, kind == SLM_KIND_MIRROR ? 1 : 0), (t / CH) % 2));
+        wr.push_back(RNG(lane_of(l, kind == SLM_KIND_MIRROR ? 1 : 0), t));
       } else if (opk == SLM_OP_HEAD_CE) {
         // one batched unit per chunk of forward heads, at the chunk's last step
         wr.clear();
         rd.clear();
         if (t % CH == CH - 1 || t == T - 1) {
-          rd.push_back(RNG(lane_top, (t / CH) % 2));
+          for (int t2 = t - t % CH; t2 <= t; ++t2) rd.push_back(RNG(lane_top, t2));
           for (int t2 = t - t % CH; t2 <= t; ++t2) wr.push_back(p->node_tag[t2 * per_t + per_t - 1]);
         }
       }
@@ -809,6 +1040,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         wr.push_back(DHR((t / CH) % 2));
       }
     }
+    if (bwdr && kind == SLM_KIND_GRAD && opk == SLM_OP_HEAD_CE && !hb_now) wr.push_back(DHR((t / CH) % 2));
     if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL && l == L - 1 && hb_batched[t]) rd.push_back(DHR((t / CH) % 2));
     if (kind == SLM_KIND_GRAD && opk == SLM_OP_LSTM_CELL) {   // reads dX partials of its gates successors
       if (l + 1 < L) rd.push_back(PXR(l + 1, t % 2));
@@ -912,7 +1144,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         LT((launch_tc_bn<slmk::EpiPartialTma, true, false, true>(B, sp.hd, M.woMN, M.dlRK, H, B, Cp, 0, slot * B,
                                                                       e2, cs, pdl, gdbg(SLM_K_GEMM_DX), &M.pH)));
         LK(launch_k(lstm_head_bwd_finish_kernel, dim3(std::max((Cp + 31) / 32, 148)), dim3(512), 0, cs, pdl, Pb(sid),
-                    sp.hd, H, B, V(v), (const float*)dlog_f, Cp, B, 1, d.db_o));
+                    sp.hd, H, B, bwdr ? dh_ring(t) : V(v), (const float*)dlog_f, Cp, B, 1, d.db_o));
         nl += 5;
         if (flush) {   // dW_o[c][h] += sum over the chunk's rows of dlog[r][c] h[r][h]
           slmk::EpiAccF32 e3{d.dW_o, H};

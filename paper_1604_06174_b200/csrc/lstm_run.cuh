@@ -48,6 +48,7 @@ struct FwdRun {
   unsigned* bar;         // step counter of this (layer, stream)
   unsigned base;         // its value when this launch starts (host-tracked)
   unsigned long long* ts; // debug (option lstm_run_ts): CTA 0's %globaltimer per step [n][16], or null
+  int dbg;               // profile_ts slot (tc_gemm.cuh ts_mark): launch start / end per CTA
   float* g_out[kRunMax]; // G_t tags (null = not materialised)
   float* s_out[kRunMax]; // S_t tags
 };
@@ -102,6 +103,8 @@ __global__ void __launch_bounds__(kRunThreads, 1)
                         const __grid_constant__ CUtensorMap tmX, const __grid_constant__ FwdRun a) {
   static_assert(B == 64 || B == 128 || B == 256, "batch");
   using C = FwdRunCfg<B>;
+  unsigned long long* const tsp = ts_buffer(a.dbg);
+  ts_mark(tsp, 0, a.dbg);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -341,8 +344,322 @@ __global__ void __launch_bounds__(kRunThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  ts_mark(tsp, 7, a.dbg);
   if (warp == kRunEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(B));
 }
+
+// ============================================================================ backward runs
+// lstm_bwd_run_kernel: the backward of one layer over n consecutive steps t1, t1-1, ..., t1-n+1
+// (descending) in one launch.  Per step t:
+//   dR_t = d_pre_{t+1} W_hh  ([B] x [H], K = 4H): the recurrent part of dh_t.  32 CTAs = 8 unit
+//          tiles (m: 128 hidden units) x 4 K slices (q: the 1024 gate rows of gate q); CTA (m, q)
+//          computes D[128 units][B] = W_hh(q rows, m units)^T . d_pre_{t+1}(:, q rows)^T with
+//          tcgen05 (A = W read MN-major, B = d_pre K-major from the exchange buffer dpx), then
+//          the four K-slice partials of a tile are summed in the fixed order q = 0..3 by the
+//          unit's owner through an L2 exchange buffer (per-tile counter)
+//   cell   CTA (m, q) owns units 128 m + 32 q .. +31: dh = fl(dR + dh_in) (dh_in: the gradient
+//          from the layer above / the head, precomputed per chunk), the cell backward with the
+//          forward's arithmetic (c re-derived from G_t and c_{t-1}, tanh on the SFU) and the dc
+//          state in shared memory, d_pre_t of the 4 gates -> dpx (bf16, the next step's B
+//          operand), then -- after the step barrier is released -- the chunk rings (bf16 d_pre for
+//          the weight / input gradient GEMMs, fp32 d_pre for db)
+// dR of the first step of the whole backward (t = T-1) is 0.
+struct BwdRun {
+  int H, n, t1, Kin;
+  int first;                    // 1: no state yet (t1 = T - 1): dR = 0, dc = 0
+  int ldh;                      // row stride of dh_in
+  __nv_bfloat16* dpx;           // [2][B][4H] bf16: d_pre_t at parity t % 2
+  float* dcstate;               // [B][H] fp32: dc carried into the step before the run
+  float* xch;                   // [8][4][4][B][32] fp32 partial exchange
+  unsigned* bar;                // step counter
+  unsigned base;
+  unsigned* xbar;               // [8] per-tile exchange counters
+  unsigned xbase;
+  unsigned long long* ts;       // debug stamps (option lstm_run_ts) or null
+  int dbg;                      // profile_ts slot (tc_gemm.cuh ts_mark)
+  const float* dh_in[kRunMax];  // [B] rows of step t1 - i
+  const float* act[kRunMax];    // G_t tags
+  const float* sprev[kRunMax];  // S_{t-1} tags (null at t = 0)
+  __nv_bfloat16* dpr[kRunMax];  // d_pre ring rows [B][4H] bf16
+  float* dpf[kRunMax];          // d_pre ring rows [B][4H] fp32
+};
+
+struct BwdRunCfg {
+  static constexpr int B = 64;
+  static constexpr int NS = 6;
+  static constexpr int A_BYTES = 128 * 64 * 2;     // W: 64 gate rows (K) x 128 units, two 64-unit boxes
+  static constexpr int B_BYTES = B * 64 * 2;       // d_pre: 64 batch rows x 64 gate rows
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int C_BYTES = 32 * B * 4;       // dc of the 32 owned units
+  static constexpr int OFF_C = NS * STAGE;
+  static constexpr int OFF_BAR = OFF_C + C_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
+};
+
+__device__ __forceinline__ void bwd_stamp(const BwdRun& a, int i, int k) {
+  if (a.ts != nullptr && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.ts[i * 16 + k] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kRunThreads, 1)
+    lstm_bwd_run_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmD,
+                        const __grid_constant__ BwdRun a) {
+  using C = BwdRunCfg;
+  constexpr int B = C::B, ET = 32 * kRunEpiWarps;
+  unsigned long long* const tsp = ts_buffer(a.dbg);
+  ts_mark(tsp, 0, a.dbg);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* empty = full + C::NS;
+  uint64_t* accum = empty + C::NS;
+  uint64_t* tfree = accum + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfree + 1);
+  float* dcs = reinterpret_cast<float*>(smem + C::OFF_C);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int H = a.H, m = (int)blockIdx.x >> 2, q = (int)blockIdx.x & 3;
+  const int u0 = 128 * m, j0 = u0 + 32 * q;   // the tile's units, this CTA's own units
+  const int nk = H / 64;                       // K blocks of the gate-q slice
+  const unsigned ncta = gridDim.x;
+  const int mma0 = a.first ? 1 : 0;            // steps before mma0 have dR = 0
+
+  if (warp == kRunEpiWarps + 1) {
+    if (lane == 0) {
+      prefetch_tmap(&tmW);
+      prefetch_tmap(&tmD);
+      for (int s = 0; s < C::NS; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+      }
+      mbar_init(accum, 1);
+      mbar_init(tfree, ET);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(B));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kRunEpiWarps) {
+    if (lane == 0) {
+      // ===== TMA producer: W_hh (gate-q rows, tile units; constant) ahead of the step barrier,
+      // d_pre_{t+1} (gate-q columns) after it
+      auto load_w = [&](int kb, int s) {
+        uint8_t* sa = smem + s * C::STAGE;
+        tma_load_2d(sa, &tmW, &full[s], a.Kin + u0, q * H + kb * 64);
+        tma_load_2d(sa + 8192, &tmW, &full[s], a.Kin + u0 + 64, q * H + kb * 64);
+      };
+      auto load_d = [&](int kb, int s, int t) {
+        tma_load_2d(smem + s * C::STAGE + C::A_BYTES, &tmD, &full[s], q * H + kb * 64, ((t + 1) & 1) * B);
+      };
+      pdl_wait();
+      int g = 0;
+      for (int i = mma0; i < a.n; ++i) {
+        const int t = a.t1 - i;
+        const int pre = nk < C::NS ? nk : C::NS;
+        for (int kb = 0; kb < pre; ++kb) {
+          const int gg = g + kb, s = gg % C::NS;
+          if (gg >= C::NS) mbar_wait(&empty[s], ((gg / C::NS) - 1) & 1);
+          mbar_expect_tx(&full[s], C::STAGE);
+          load_w(kb, s);
+        }
+        const unsigned target = a.base + ncta * (unsigned)(i + 1);   // d_pre_{t+1} published by every CTA
+        while ((int)(ld_acquire_gpu(a.bar) - target) < 0) {
+        }
+        bwd_stamp(a, i, 0);
+        fence_proxy_async_global();
+        for (int kb = 0; kb < pre; ++kb) load_d(kb, (g + kb) % C::NS, t);
+        for (int kb = pre; kb < nk; ++kb) {
+          const int gg = g + kb, s = gg % C::NS;
+          if (gg >= C::NS) mbar_wait(&empty[s], ((gg / C::NS) - 1) & 1);
+          mbar_expect_tx(&full[s], C::STAGE);
+          load_w(kb, s);
+          load_d(kb, s, t);
+        }
+        g += nk;
+      }
+    }
+  } else if (warp == kRunEpiWarps + 1) {
+    if (lane == 0) {
+      // ===== MMA issuer: D[128 units][B] += W(k, unit) . d_pre(b, k), A MN-major, B K-major
+      constexpr uint32_t idesc = make_idesc(128, B, true, false);
+      int g = 0;
+      for (int i = mma0; i < a.n; ++i) {
+        if (i > mma0) mbar_wait(tfree, (i - mma0 - 1) & 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % C::NS;
+          mbar_wait(&full[s], (g / C::NS) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * C::STAGE), sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma(tmem, make_sdesc(sa + kk * 2048, 8192, 1024), make_sdesc(sb + kk * 32, 16, 1024), idesc,
+                   (kb | kk) != 0);
+          tc_commit(&empty[s]);
+        }
+        tc_commit(accum);
+      }
+    }
+  } else {
+    // ===== epilogue (warps 0-7): warp w reads TMEM lanes 32 (w % 4) = tile units 32 (w % 4) ..,
+    // batch columns hf*32 .. hf*32+31; the cell is per owned (unit, batch row)
+    pdl_wait();
+    const int qq = warp & 3, hf = warp >> 2;
+    for (int idx = tid; idx < 32 * B; idx += ET) {
+      const int uu = idx & 31, b = idx >> 5;
+      dcs[b * 32 + uu] = a.first ? 0.f : a.dcstate[(size_t)b * H + j0 + uu];
+    }
+    epi_bar();
+    if (tid == 0) red_release_gpu(a.bar, 1u);
+    unsigned xcount = a.xbase;
+    for (int i = 0; i < a.n; ++i) {
+      const int t = a.t1 - i;
+      const bool mma = i >= mma0;
+      // ---- the step's inputs (written by earlier kernels: read-only here), loaded before waiting
+      // for the MMA so their latency hides behind it
+      const float* dhi = a.dh_in[i];
+      const float* act = a.act[i];
+      const float* sp = a.sprev[i];
+      float in[8][6];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = tid + ET * k, uu = idx & 31, b = idx >> 5, j = j0 + uu;
+        const float* ar = act + (size_t)b * 4 * H;
+        in[k][0] = __ldg(ar + j);
+        in[k][1] = __ldg(ar + H + j);
+        in[k][2] = __ldg(ar + 2 * H + j);
+        in[k][3] = __ldg(ar + 3 * H + j);
+        in[k][4] = sp ? __ldg(sp + (size_t)b * 2 * H + H + j) : 0.f;
+        in[k][5] = __ldg(dhi + (size_t)b * a.ldh + j);
+      }
+      if (mma) {
+        // ---- partial of K slice q for the tile's 128 units -> the exchange, slot (owner, q)
+        mbar_wait(accum, (i - mma0) & 1);
+        tc_fence_after();
+        if (tid == 0) bwd_stamp(a, i, 2);
+        float acc[32];
+        tmem_ld32(tmem + ((uint32_t)(qq * 32) << 16) + hf * 32, acc);
+        tc_fence_before();
+        mbar_arrive(tfree);
+        float* xo = a.xch + ((((size_t)m * 4 + qq) * 4 + q) * B + hf * 32) * 32 + lane;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) __stcg(xo + jj * 32, acc[jj]);
+        epi_bar();
+        xcount += 4;
+        if (tid == 0) {
+          red_release_gpu(a.xbar + m, 1u);
+          while ((int)(ld_acquire_gpu(a.xbar + m) - xcount) < 0) {
+          }
+          bwd_stamp(a, i, 4);
+        }
+        epi_bar();
+      }
+      // ---- cell backward of the owned units
+      __nv_bfloat16* dpo = a.dpx + (size_t)(t & 1) * B * 4 * H;
+      float dp[8][4];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = tid + ET * k, uu = idx & 31, b = idx >> 5;
+        float dr = 0.f;
+        if (mma) {
+          const float* xi = a.xch + (((size_t)m * 4 + q) * 4 * B + b) * 32 + uu;
+          dr = __ldcg(xi);
+#pragma unroll
+          for (int s2 = 1; s2 < 4; ++s2) dr = __fadd_rn(dr, __ldcg(xi + (size_t)s2 * B * 32));
+        }
+        const float dh = __fadd_rn(dr, in[k][5]);
+        const float ig = in[k][0], fg = in[k][1], gg = in[k][2], og = in[k][3], cp = in[k][4];
+        const float c = __fadd_rn(__fmul_rn(fg, cp), __fmul_rn(ig, gg));
+        const float tc = tanh_fast(c);
+        const float dct = __fadd_rn(dcs[b * 32 + uu], __fmul_rn(__fmul_rn(dh, og), __fsub_rn(1.f, __fmul_rn(tc, tc))));
+        dcs[b * 32 + uu] = __fmul_rn(dct, fg);
+        dp[k][0] = dpre_of(0, __fmul_rn(dct, gg), ig);
+        dp[k][1] = dpre_of(1, __fmul_rn(dct, cp), fg);
+        dp[k][2] = dpre_of(2, __fmul_rn(dct, ig), gg);
+        dp[k][3] = dpre_of(3, __fmul_rn(dh, tc), og);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = tid + ET * k, uu = idx & 31, b = idx >> 5, j = j0 + uu;
+#pragma unroll
+        for (int g2 = 0; g2 < 4; ++g2) dpo[(size_t)b * 4 * H + g2 * H + j] = __float2bfloat16_rn(dp[k][g2]);
+      }
+      if (tid == 0) bwd_stamp(a, i, 8);
+      fence_proxy_async_global();
+      epi_bar();
+      if (tid == 0) {
+        red_release_gpu(a.bar, 1u);
+        bwd_stamp(a, i, 3);
+      }
+      // ---- off the critical path: the chunk rings and the weight-gradient operand slice
+      __nv_bfloat16* dr = a.dpr[i];
+      float* df = a.dpf[i];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = tid + ET * k, uu = idx & 31, b = idx >> 5, j = j0 + uu;
+#pragma unroll
+        for (int g2 = 0; g2 < 4; ++g2) {
+          dr[(size_t)b * 4 * H + g2 * H + j] = __float2bfloat16_rn(dp[k][g2]);
+          df[(size_t)b * 4 * H + g2 * H + j] = dp[k][g2];
+        }
+      }
+    }
+    for (int idx = tid; idx < 32 * B; idx += ET) {
+      const int uu = idx & 31, b = idx >> 5;
+      a.dcstate[(size_t)b * H + j0 + uu] = dcs[b * 32 + uu];
+    }
+    pdl_launch();
+  }
+  tc_fence_before();
+  __syncthreads();
+  ts_mark(tsp, 7, a.dbg);
+  if (warp == kRunEpiWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(B));
+}
+
+// weight-gradient operand rows of n steps: out rows (i B + b) = bf16([x_t | h_{t-1}]), x_t =
+// xs.p[i] (width xw, row stride xrs, zero-padded to Kin), h_{t-1} = the h half of hs.p[i] (null: 0)
+struct StepPtrs {
+  const float* p[kRunMax];
+};
+__global__ void __launch_bounds__(256) lstm_oppack_kernel(StepPtrs xs, StepPtrs hs, int n, int B, int xw, int xrs, int Kin,
+                                                          int H, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  const int K = Kin + H;
+  const size_t tot = (size_t)n * B * K;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % K);
+    const size_t r = e / K;
+    const int i = (int)(r / B), b = (int)(r % B);
+    float v;
+    if (c < Kin) v = c < xw ? xs.p[i][(size_t)b * xrs + c] : 0.f;
+    else v = hs.p[i] ? hs.p[i][(size_t)b * 2 * H + (c - Kin)] : 0.f;
+    out[e] = __float2bfloat16_rn(v);
+  }
+}
+
+// input gradient of a run: out[n ld + m] = acc for the first nmax columns n (the projection runs
+// over a 256-column padded N; the padding columns are not stored)
+struct EpiStoreF32Lim {
+  static constexpr bool kTma = false;
+  float* out;
+  long ld;
+  int nmax;
+  __device__ __forceinline__ void operator()(int m, int n0, const float* acc, int) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < nmax) out[(long)(n0 + j) * ld + m] = acc[j];
+  }
+};
 
 // X_t = x_t W_ih^T + b of a run: the tcgen05 GEMM epilogue out[n ld + m] = fl(acc + bias[m])
 struct EpiBiasF32 {

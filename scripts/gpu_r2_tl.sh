@@ -1,4 +1,3 @@
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
-PHASES=1 timeout -s KILL 300 python scripts/chain_timeline.py > gpurun_out/r2_timeline.txt 2>&1
-STRATEGY=none MP=0 PHASES=1 timeout -s KILL 300 python scripts/chain_timeline.py >> gpurun_out/r2_timeline.txt 2>&1
+T=256 DUMP=0 DUMPN=2000 timeout -s KILL 300 python scripts/lstm_timeline.py lstm_streams=2 > gpurun_out/r2_lstm_tl4.txt 2>&1

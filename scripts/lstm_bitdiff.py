@@ -53,12 +53,20 @@ with torch.cuda.stream(s):
 torch.cuda.synchronize()
 t = ts.view(nr, 16, 16).cpu().numpy().astype(np.float64)
 names = {1: "mma issued", 2: "accum", 4: "tmem ld", 5: "x ready", 6: "acts", 7: "bar1", 8: "cell", 9: "fence", 10: "bar2", 3: "released"}
-for r in range(min(nr, 8)):
+bnames = {2: "accum", 4: "exchanged", 8: "cell", 3: "released"}
+for r in range(nr):
     v = t[r]
-    ok = v[:, 0] > 0
+    ok = v[:, 3] > 0
     v = v[ok]
     if len(v) < 2:
         continue
-    step = np.diff(v[:, 0]).mean()
-    print(f"run {r}: steps {ok.sum()} period {step / 1e3:.2f} us; from the barrier: " +
-          "  ".join(f"{names[k]} {np.mean(v[:, k] - v[:, 0]) / 1e3:.2f}" for k in (1, 2, 4, 5, 6, 7, 8, 9, 10, 3)))
+    bwd = v[0, 1] == 0   # the forward run stamps k = 1 (MMA issued), the backward run does not
+    step = np.abs(np.diff(v[:, 3])).mean()
+    ref = v[:, 0]
+    if bwd:
+        if r % 4 == 0 or r > nr - 5:
+            print(f"bwd run {r}: steps {ok.sum()} period {step / 1e3:.2f} us; from the barrier: " +
+                  "  ".join(f"{bnames[k]} {np.mean(v[1:, k] - ref[1:]) / 1e3:.2f}" for k in (2, 4, 8, 3)))
+    elif r < 4:
+        print(f"fwd run {r}: steps {ok.sum()} period {step / 1e3:.2f} us; from the barrier: " +
+              "  ".join(f"{names[k]} {np.mean(v[:, k] - ref) / 1e3:.2f}" for k in (1, 2, 4, 5, 6, 7, 8, 9, 10, 3)))

@@ -1,5 +1,5 @@
-"""Device-clock timeline of the LSTM step's GEMM launches (profile_ts + slm_debug_ts_meta):
-per stream busy time, concurrency and the gaps between consecutive GEMMs of a stream."""
+"""Device-clock timeline of the LSTM step's GEMM and persistent-run launches (profile_ts +
+slm_debug_ts_meta): per stream busy time, concurrency and the gaps between consecutive launches."""
 import ctypes as C
 import os
 import sys
@@ -19,6 +19,7 @@ plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(int(os.environ.g
 opts = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[1:])}
 model = slm.LstmModel(p, g, L, T, B, H, I, Cn, **opts)
 ngemm = 4 * T * (L + 2) + 64
+KIND = {0: 'fwd run', 1: 'gemm fwd', 2: 'gemm dx', 3: 'gemm dw', 4: 'bwd run'}
 ts = torch.zeros(ngemm * 1024 * 2, dtype=torch.int64, device=dev)
 model.set_option("profile_ts", ngemm)
 model.set_option("profile_ts_buffer", ts.data_ptr())
@@ -48,6 +49,10 @@ ends = t[:, :, 1].max(1)
 t0 = starts.min()
 s_us, e_us = (starts - t0) / 1e3, (ends - t0) / 1e3
 aux = np.array(aux[:])
+kinds = np.array(kind[:])
+for kd in sorted(set(kinds.tolist())):
+    sel = kinds == kd
+    print(f"{KIND.get(kd, kd):9s}: {sel.sum():6d} launches, busy {(e_us - s_us)[sel].sum() / 1e3:8.2f} ms, mean {(e_us - s_us)[sel].mean():8.2f} us")
 print(f"T={T} step {step_ms:.2f} ms, {n.value} GEMM launches, first..last GEMM {e_us.max() / 1e3:.2f} ms")
 streams = sorted(set(aux // 4))
 for s in streams:
@@ -85,3 +90,10 @@ for kd, name in ((0, "forward"), (1, "recompute"), (2, "backward")):
     busy += cur_e - cur_s
     print(f"{name:9s}: {sel.sum():6d} GEMMs, first {ss.min() / 1e3:8.2f} ms  last end {ee.max() / 1e3:8.2f} ms  "
           f"GEMM-busy union {busy / 1e3:8.2f} ms")
+if os.environ.get("DUMP"):
+    # a window of the launch list: start, end (us), stream, kind
+    order = np.argsort(s_us)
+    lo = float(os.environ.get("DUMP"))
+    rows = [(s_us[i], e_us[i], aux[i] // 4, aux[i] % 4, KIND.get(kinds[i], kinds[i])) for i in order if s_us[i] >= lo * 1e3][:int(os.environ.get("DUMPN", 120))]
+    for r in rows:
+        print(f"{r[0]:10.1f} {r[1]:10.1f} {r[1] - r[0]:8.1f}  stream {r[2]} k{r[3]}  {r[4]}")
