@@ -35,7 +35,7 @@
 
 namespace slmk {
 
-constexpr int kRunMax = 16;   // steps per run launch (two runs per 32-step weight-gradient chunk)
+constexpr int kRunMax = 8;    // steps per run launch (four runs per 32-step weight-gradient chunk)
 
 struct FwdRun {
   int H, n, t0, Kin;     // Kin: first column of W_hh inside the layer's [W_ih | W_hh] rows
