@@ -222,7 +222,7 @@ slm_status slm_recursion_estimate(int64_t n, int64_t k, int64_t* units, int64_t*
  * call returns SLM_E_CUDA / SLM_E_UNSUPPORTED.
  */
 enum { SLM_F32 = 0, SLM_BF16 = 1 };
-enum { SLM_MODEL_CHAIN = 0, SLM_MODEL_LSTM = 1 };
+enum { SLM_MODEL_CHAIN = 0, SLM_MODEL_LSTM = 1, SLM_MODEL_OPS = 2 };
 
 /* Chain parameters, all device pointers, row-major, caller-owned:
  *   W      [n][d][d]  (out, in)  fp32 (SLM_F32) or bf16 (SLM_BF16)
@@ -261,6 +261,27 @@ typedef struct {
   float* dW; float* db; float* dW_o; float* db_o;
 } slm_lstm_desc;
 slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out);
+/* Op-granularity graphs: any DAG built with
+ * slm_graph_create from Input, BN, ReLU, FC, Add and SoftmaxCE nodes (e.g. the pre-activation
+ * network of oracle.graph.preact_resnet_graph: per layer BN(x) -> ReLU -> FC -> Add(x, .)), so
+ * that the DROP_CHEAP plan ("drop bn-relu") really re-computes BN and ReLU outputs.  Every node's
+ * value is [batch][w] fp32 with w = out_bytes / (4 batch) (the loss: 4 bytes).  Node semantics
+ * (oracle/opgraph.py): BN with batch statistics (biased variance, eps 1e-5), ReLU'(0) = 0,
+ * FC y = x W^T + b, Add, SoftmaxCE = mean CE over batch_global (0 = batch) with labels in [0, w).
+ * Per-node parameter arrays of n_nodes entries (host arrays of DEVICE pointers, copied; entries of
+ * other ops ignored):
+ *   FC  W bf16 [dout][din], b fp32 [dout]; grads dW bf16 (rounded from fp32), db fp32
+ *   BN  gamma, beta fp32 [w]; grads dgamma, dbeta fp32
+ * Gradients are overwritten by every step.  Constraints of the tcgen05 path: batch % 64 == 0,
+ * every width % 128 == 0.  Step inputs: x0 [batch][w_input] fp32, labels int32 [batch].
+ * Runs replicas-only (comm must be NULL).  SLM_E_ARG / SLM_E_UNSUPPORTED (message in
+ * slm_last_error) for an unsupported op, a bad width or a missing parameter. */
+typedef struct {
+  int32_t batch, batch_global, n_nodes;
+  const void* const* W; const float* const* b; const float* const* gamma; const float* const* beta;
+  void* const* dW; float* const* db; float* const* dgamma; float* const* dbeta;
+} slm_ops_desc;
+slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model** out);
 void slm_model_destroy(slm_model* m);
 /* Options (int64 values):
  *   use_graph       capture the whole step in a CUDA graph per buffer set (default 1)

@@ -393,6 +393,53 @@ class LstmModel(_Model):
         return out
 
 
+class OpsModel(_Model):
+    """slm_model for an op-granularity graph (slm_model_ops).  graph: a Graph built
+    with Graph.from_nodes from Input / BN / ReLU / FC / Add / SoftmaxCE nodes; params / grads:
+    {node id: {"W": bf16 [dout, din], "b": f32 [dout]}} for FC nodes and {"gamma", "beta"} (f32)
+    for BN nodes (grads: the same keys, W bf16)."""
+
+    def __init__(self, graph, params, grads, batch, batch_global=0, **options):
+        n = len(graph)
+        self.params, self.grads, self.graph = params, grads, graph
+        arrs = {k: (C.c_void_p * max(1, n))() for k in ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")}
+        for v in range(n):
+            pv, gv = params.get(v, {}), grads.get(v, {})
+            for k in ("W", "b", "gamma", "beta"):
+                if k in pv:
+                    arrs[k][v] = _ptr(pv[k]).value
+            for k in ("W", "b", "gamma", "beta"):
+                if k in gv:
+                    arrs["d" + k][v] = _ptr(gv[k]).value
+        self._arrs = arrs
+        vpp = C.POINTER(C.c_void_p)
+        desc = _lib.OpsDesc(batch, batch_global, n, *(C.cast(arrs[k], vpp) for k in
+                                                       ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")))
+        h = C.c_void_p()
+        check(lib.slm_model_ops(graph._h, C.byref(desc), C.byref(h)), "slm_model_ops")
+        self._init(h, options)
+
+    @staticmethod
+    def preact_nodes(depths, widths, batch):
+        """Node list (op, preds, out_bytes, flags) of the pre-activation network of SURVEY 8(f) f1:
+        per layer BN(x) -> ReLU -> FC -> Add(x, .), an FC projection where the width changes, a
+        SoftmaxCE loss (the same graph as oracle.graph.preact_resnet_graph)."""
+        nodes = [(OP["input"], [], batch * widths[0] * 4, 0)]
+        x = 0
+        for dep, w in zip(depths, widths):
+            if nodes[x][2] != batch * w * 4:
+                nodes.append((OP["fc"], [x], batch * w * 4, 0))
+                x = len(nodes) - 1
+            for _ in range(dep):
+                nodes.append((OP["bn"], [x], batch * w * 4, 0))
+                nodes.append((OP["relu"], [len(nodes) - 1], batch * w * 4, 0))
+                nodes.append((OP["fc"], [len(nodes) - 1], batch * w * 4, 0))
+                nodes.append((OP["add"], [x, len(nodes) - 1], batch * w * 4, 0))
+                x = len(nodes) - 1
+        nodes.append((OP["softmax_ce"], [x], 4, 1))
+        return nodes
+
+
 def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None, split=1):
     """Test hook (include/slm_debug.h)."""
     import torch

@@ -52,6 +52,12 @@ class LstmDesc(C.Structure):
                 ("dW", vp), ("db", vp), ("dW_o", vp), ("db_o", vp)]
 
 
+class OpsDesc(C.Structure):
+    _fields_ = [("batch", i32), ("batch_global", i32), ("n_nodes", i32),
+                ("W", C.POINTER(vp)), ("b", C.POINTER(vp)), ("gamma", C.POINTER(vp)), ("beta", C.POINTER(vp)),
+                ("dW", C.POINTER(vp)), ("db", C.POINTER(vp)), ("dgamma", C.POINTER(vp)), ("dbeta", C.POINTER(vp))]
+
+
 def _sig(name, res, *args):
     f = getattr(lib, name)
     f.restype = res
@@ -79,6 +85,7 @@ _sig("slm_plan_destroy", None, vp)
 _sig("slm_recursion_estimate", i32, i64, i64, i64p, i64p)
 _sig("slm_model_chain", i32, C.POINTER(ChainDesc), C.POINTER(vp))
 _sig("slm_model_lstm", i32, C.POINTER(LstmDesc), C.POINTER(vp))
+_sig("slm_model_ops", i32, vp, C.POINTER(OpsDesc), C.POINTER(vp))
 _sig("slm_debug_ts_meta", i32, vp, i32p, i32p, i32, i32p)
 _sig("slm_lstm_segment_mirrors", i32, vp, i32, i32p, i32)
 _sig("slm_model_destroy", None, vp)

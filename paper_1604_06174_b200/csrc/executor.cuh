@@ -307,9 +307,22 @@ struct slm_lstm_state {
 // backward k - kNA: kNA layers of slack between the dX chain and the dW stream
 constexpr int kNA = 2, kNG = kNA + 1;
 
+// op-granularity model (executor_ops.cuh): per forward node parameters, the graph it was built for
+struct slm_ops_model {
+  int batch = 0, batch_global = 0;
+  std::vector<const void*> W;
+  std::vector<const float*> b, gamma, beta;
+  std::vector<void*> dW;
+  std::vector<float*> db, dgamma, dbeta;
+  std::vector<int> op;
+  std::vector<int64_t> out_bytes;
+};
+
 struct slm_model {
   slm_chain_desc d{};
   slm_lstm_desc ld{};
+  slm_ops_model od;
+  int ops_maxw = 0;
   slm_lstm_state lst;
   int kind = SLM_MODEL_CHAIN;
   int use_graph = 1;
@@ -978,6 +991,16 @@ slm_status check_plan_model(const slm_plan* p, const slm_model* m) {
   if (!p || !m) {
     set_error("null plan/model");
     return SLM_E_ARG;
+  }
+  if (m->kind == SLM_MODEL_OPS) {
+    const slm_ops_model& o = m->od;
+    bool ok = p->graph_kind == -1 && p->n_fwd == (int)o.op.size();
+    for (int v = 0; ok && v < p->n_fwd; ++v) ok = p->op[v] == o.op[v] && p->out_bytes[v] == o.out_bytes[v];
+    if (!ok) {
+      set_error("plan was not built for this op graph");
+      return SLM_E_SHAPE;
+    }
+    return SLM_OK;
   }
   if (m->kind == SLM_MODEL_LSTM) {
     const slm_lstm_desc& d = m->ld;

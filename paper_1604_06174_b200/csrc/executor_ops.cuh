@@ -1,0 +1,234 @@
+// Executor of V' for op-granularity graphs (included by runtime.cu).
+//
+// The graph is any DAG of Input, BN, ReLU, FC, Add and SoftmaxCE nodes (e.g. oracle.graph.
+// preact_resnet_graph: per layer BN(x) -> ReLU -> FC -> Add(x, .), FC projections between stages;
+// PAPER.md:431-446 and "conv-bn-relu counted as one layer", :437), with per-node parameters
+// (slm_ops_desc).  The step runs V' node by node on one stream: every node -- forward,
+// re-computed (mirror) or gradient -- reads its inputs from and writes its value to its pool tag,
+// exactly as the plan allocated them, so a "drop bn-relu" plan (Sec. 4.2)
+// really re-computes BN and ReLU outputs from the kept FC / Add values.  Node semantics are
+// oracle/opgraph.py's; FC operands (x, W, dy) are bf16 (reading A11), everything else fp32.
+//
+// Lowering per node (B = batch, w = width = out_bytes / (4 B)):
+//   BN / ReLU / Add     ops_kernels.cuh (element-wise, fixed-order per-feature reductions)
+//   FC forward          x -> bf16 operand, tcgen05 GEMM D[dout][B] = W x^T (+ bias epilogue)
+//   FC backward         dy -> bf16, dx = dy W (GEMM, W read MN-major), dW = dy^T x (GEMM over
+//                       K = B, bf16 output), db = column sums of dy
+//   SoftmaxCE           kernels_simt.cuh ce_fwd / ce_reduce / ce_bwd (loss = mean over B_global)
+//   gradient node g[v]  upstream dy = the sum of g[s]'s slice for v over v's successors s in
+//                       successor order (reading A17) -- used in place when it is one whole slice
+#pragma once
+#include "ops_kernels.cuh"
+
+namespace {
+
+bool ops_supported(int op) {
+  return op == SLM_OP_INPUT || op == SLM_OP_BN || op == SLM_OP_RELU || op == SLM_OP_FC || op == SLM_OP_ADD ||
+         op == SLM_OP_SOFTMAX_CE;
+}
+
+struct OpsWs {
+  size_t xq, gq, dy, rowloss, total;
+};
+OpsWs ops_ws_layout(const slm_model& m) {
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t B = m.od.batch, W = m.ops_maxw;
+  OpsWs L{};
+  size_t off = 0;
+  L.xq = off;      off += al(B * W * 2);
+  L.gq = off;      off += al(B * W * 2);
+  L.dy = off;      off += al(B * W * 4);
+  L.rowloss = off; off += al(B * 4);
+  L.total = off;
+  return L;
+}
+
+slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const int32_t* labels, void* pool, void* ws,
+                       float* loss, cudaStream_t st, int64_t* launches, bool dry = false) {
+  using namespace slmk;
+  using bf = __nv_bfloat16;
+#define OK_(call)       \
+  do {                  \
+    if (!dry) CK(call); \
+  } while (0)
+#define OT_(call)                                  \
+  do {                                             \
+    if (!dry && (s = (call)) != SLM_OK) return s;  \
+  } while (0)
+  const slm_ops_model& d = m.od;
+  const int B = d.batch, N = p->n_fwd;
+  const float inv_bg = 1.0f / (float)(d.batch_global > 0 ? d.batch_global : B);
+  const bool pdl = m.pdl != 0;
+  const OpsWs W = ops_ws_layout(m);
+  uint8_t* w8 = (uint8_t*)ws;
+  bf* xq = (bf*)(w8 + W.xq);
+  bf* gq = (bf*)(w8 + W.gq);
+  float* dyw = (float*)(w8 + W.dy);
+  float* rowloss = (float*)(w8 + W.rowloss);
+  slm_status s = SLM_OK;
+  int64_t nl = 0;
+  auto width = [&](int node) { return (int)(p->out_bytes[node] / (4 * (int64_t)B)); };
+  std::vector<void*> tp(p->tag_size.size(), nullptr);
+  for (size_t t = 0; t < tp.size(); ++t)
+    if (p->tag_offset[t] >= 0) tp[t] = (uint8_t*)pool + p->tag_offset[t];
+  for (int v = 0; v < N; ++v) {
+    const int t = p->node_tag[v];
+    if (t < 0 || p->tag_offset[t] >= 0) continue;
+    if (p->op[v] == SLM_OP_INPUT) tp[t] = const_cast<void*>(x0);
+    else if (p->op[v] == SLM_OP_SOFTMAX_CE) tp[t] = loss;
+  }
+  auto V = [&](int node) -> float* { return (float*)tp[p->node_tag[node]]; };
+  const int* pred = p->preds.data();
+  auto ew = [&](size_t n) { return dim3((unsigned)std::max<size_t>(1, std::min<size_t>(1184, (n + 255) / 256))); };
+  const dim3 eb(256);
+  // tensor maps of one GEMM operand (encoded per launch: host work only, captured into the graph)
+  CUtensorMap ma, mb;
+  auto kmap = [&](CUtensorMap* mp, const void* base, int inner, int rows, int box_rows) -> slm_status {
+    return dry ? SLM_OK : make_map(mp, base, (uint64_t)inner, (uint64_t)rows, (uint32_t)box_rows);
+  };
+  const int bnB = B % 256 == 0 ? 256 : B % 128 == 0 ? 128 : 64;   // N tile over the batch
+  // FC x -> y = x W^T + b   (W [dout][din] bf16)
+  auto fc_fwd = [&](int v, const float* x, int din, int dout, float* y) -> slm_status {
+    OK_(launch_k(op_pack_kernel, ew((size_t)B * din), eb, 0, st, pdl, x, B, din, din, xq));
+    if ((s = kmap(&ma, d.W[p->orig[v]], din, dout, 128)) != SLM_OK) return s;
+    if ((s = kmap(&mb, xq, din, B, bnB)) != SLM_OK) return s;
+    EpiBiasF32 e{y, dout, d.b[p->orig[v]]};
+    OT_((launch_tc_bn<EpiBiasF32, false, false, true>(bnB, 1, ma, mb, dout, B, din, 0, 0, e, st, pdl)));
+    nl += 2;
+    return SLM_OK;
+  };
+
+  for (int v : p->order) {
+    const int kind = p->kind[v], op = p->op[v], u = p->orig[v];
+    const int* pv = pred + p->pred_ptr[v];
+    const int np = p->pred_ptr[v + 1] - p->pred_ptr[v];
+    if (kind != SLM_KIND_GRAD) {
+      const int w = width(v);
+      switch (op) {
+        case SLM_OP_INPUT:
+          break;
+        case SLM_OP_BN:
+          OK_(launch_k(op_bn_fwd_kernel, dim3((w + 31) / 32), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
+                       d.beta[u], B, w, V(v)));
+          ++nl;
+          break;
+        case SLM_OP_RELU:
+          OK_(launch_k(op_relu_fwd_kernel, ew((size_t)B * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
+                       (size_t)B * w / 4, (float4*)V(v)));
+          ++nl;
+          break;
+        case SLM_OP_ADD:
+          OK_(launch_k(op_add_fwd_kernel, ew((size_t)B * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
+                       (const float4*)V(pv[1]), (size_t)B * w / 4, (float4*)V(v)));
+          ++nl;
+          break;
+        case SLM_OP_FC:
+          if ((s = fc_fwd(v, V(pv[0]), width(pv[0]), w, V(v))) != SLM_OK) return s;
+          break;
+        case SLM_OP_SOFTMAX_CE: {
+          const int wi = width(pv[0]);
+          OK_(launch_k(ce_fwd_kernel, dim3(B), eb, 0, st, pdl, (const float*)V(pv[0]), labels, wi, rowloss));
+          OK_(launch_k(ce_reduce_kernel, dim3(1), eb, 0, st, pdl, (const float*)rowloss, B, inv_bg, V(v)));
+          nl += 2;
+          break;
+        }
+        default:
+          set_error("op graph executor: unsupported op " + std::to_string(op));
+          return SLM_E_UNSUPPORTED;
+      }
+      continue;
+    }
+    // ---- gradient node of u: preds = [successor gradient nodes (successor order)..., the forward
+    // values its backward reads (op metadata, reading A6)]
+    const int wu = width(u);
+    int k = 0;
+    GradSlices gs{};
+    while (k < np && p->kind[pv[k]] == SLM_KIND_GRAD) {
+      const int sg = pv[k], so = p->orig[sg];
+      const int* sp = pred + p->pred_ptr[so];
+      const int ns = p->pred_ptr[so + 1] - p->pred_ptr[so];
+      int off = 0, ld = 0;
+      for (int i = 0; i < ns; ++i) ld += width(sp[i]);
+      for (int i = 0; i < ns; ++i) {
+        if (sp[i] == u) {
+          if (gs.n == 8) {
+            set_error("op graph executor: more than 8 gradient slices");
+            return SLM_E_UNSUPPORTED;
+          }
+          gs.p[gs.n] = V(sg) + off;
+          gs.ld[gs.n] = ld;
+          ++gs.n;
+        }
+        off += width(sp[i]);
+      }
+      ++k;
+    }
+    const int* rest = pv + k;
+    const float* dy = nullptr;
+    if (op != SLM_OP_SOFTMAX_CE) {
+      if (gs.n == 0) {
+        set_error("op graph executor: gradient node without an upstream gradient");
+        return SLM_E_UNSUPPORTED;
+      }
+      if (gs.n == 1 && gs.ld[0] == wu) {
+        dy = gs.p[0];   // one whole slice in the node's own layout (an in-place output aliases it element for element)
+      } else {
+        OK_(launch_k(op_gsum_kernel, ew((size_t)B * wu), eb, 0, st, pdl, gs, B, wu, dyw));
+        ++nl;
+        dy = dyw;
+      }
+    }
+    switch (op) {
+      case SLM_OP_RELU:   // rest = [output]
+        OK_(launch_k(op_relu_bwd_kernel, ew((size_t)B * wu / 4), eb, 0, st, pdl, (const float4*)dy,
+                     (const float4*)V(rest[0]), (size_t)B * wu / 4, (float4*)V(v)));
+        ++nl;
+        break;
+      case SLM_OP_BN:   // rest = [x]
+        OK_(launch_k(op_bn_bwd_kernel, dim3((wu + 31) / 32), eb, 0, st, pdl, dy, (const float*)V(rest[0]), d.gamma[u],
+                     B, wu, V(v), d.dgamma[u], d.dbeta[u]));
+        ++nl;
+        break;
+      case SLM_OP_ADD:   // [dy | dy]
+        OK_(launch_k(op_add_bwd_kernel, ew((size_t)B * wu / 4), eb, 0, st, pdl, (const float4*)dy, B, wu / 4,
+                     (float4*)V(v)));
+        ++nl;
+        break;
+      case SLM_OP_SOFTMAX_CE:   // rest = [x]; dx may alias x
+        OK_(launch_k(ce_bwd_kernel<bf>, dim3(B), eb, 0, st, pdl, (const float*)V(rest[0]), labels, width(rest[0]),
+                     inv_bg, V(v), (bf*)nullptr));
+        ++nl;
+        break;
+      case SLM_OP_FC: {   // rest = [x]
+        const int din = width(rest[0]), dout = wu;
+        // bf16 dy and x (the GEMM operands), db = column sums of dy -- all before dx may overwrite dy
+        OK_(launch_k(op_pack_kernel, ew((size_t)B * dout), eb, 0, st, pdl, dy, B, dout, dout, gq));
+        OK_(launch_k(op_pack_kernel, ew((size_t)B * din), eb, 0, st, pdl, (const float*)V(rest[0]), B, din, din, xq));
+        OK_(launch_k(colsum_kernel, dim3((dout + 31) / 32), eb, 0, st, pdl, dy, B, dout, d.db[u]));
+        // dW[dout][din] = sum_b dy[b][dout] x[b][din]: D[m = din][n = dout], both operands MN-major, K = B
+        if ((s = kmap(&ma, xq, din, B, 64)) != SLM_OK) return s;
+        if ((s = kmap(&mb, gq, dout, B, 64)) != SLM_OK) return s;
+        EpiStoreBF16 e1{(bf*)d.dW[u], din};
+        OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(dout % 256 == 0 ? 256 : 128, 1, ma, mb, din, dout, B, 0, 0,
+                                                          e1, st, pdl)));
+        // dx[b][din] = sum_o dy[b][o] W[o][din]: D[m = din][n = b], W MN-major (K = dout rows)
+        if ((s = kmap(&ma, d.W[u], din, dout, 64)) != SLM_OK) return s;
+        if ((s = kmap(&mb, gq, dout, B, bnB)) != SLM_OK) return s;
+        EpiStoreF32 e2{V(v), din};
+        OT_((launch_tc_bn<EpiStoreF32, true, false, true>(bnB, 1, ma, mb, din, B, dout, 0, 0, e2, st, pdl)));
+        nl += 5;
+        break;
+      }
+      default:
+        set_error("op graph executor: unsupported gradient op " + std::to_string(op));
+        return SLM_E_UNSUPPORTED;
+    }
+  }
+  OK_(cudaGetLastError());
+  if (launches) *launches = nl;
+  return SLM_OK;
+#undef OK_
+#undef OT_
+}
+
+}  // namespace

@@ -117,6 +117,7 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 #include "lstm_kernels.cuh"
 #include "lstm_run.cuh"
 #include "executor_lstm.cuh"
+#include "executor_ops.cuh"
 
 extern "C" {
 
@@ -171,7 +172,74 @@ slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out) {
   return SLM_OK;
 }
 
+slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model** out) {
+  if (!g || !desc || !out) {
+    set_error("null argument");
+    return SLM_E_ARG;
+  }
+  *out = nullptr;
+  const slm_ops_desc& d = *desc;
+  const int n = (int)g->nodes.size();
+  if (d.n_nodes != n || d.batch <= 0 || d.batch % 64) {
+    set_error("slm_model_ops: n_nodes must match the graph, batch % 64 == 0");
+    return SLM_E_ARG;
+  }
+  if (!d.W || !d.b || !d.gamma || !d.beta || !d.dW || !d.db || !d.dgamma || !d.dbeta) {
+    set_error("slm_model_ops: null parameter array");
+    return SLM_E_ARG;
+  }
+  auto m = std::make_unique<slm_model>();
+  m->kind = SLM_MODEL_OPS;
+  slm_ops_model& o = m->od;
+  o.batch = d.batch;
+  o.batch_global = d.batch_global;
+  for (int v = 0; v < n; ++v) {
+    const slm::Node& nd = g->nodes[v];
+    if (!ops_supported(nd.op)) {
+      set_error("slm_model_ops: node " + std::to_string(v) + ": unsupported op " + std::to_string(nd.op));
+      return SLM_E_UNSUPPORTED;
+    }
+    const bool loss = nd.op == SLM_OP_SOFTMAX_CE;
+    if (!loss && (nd.out_bytes % (4 * (int64_t)d.batch) || (nd.out_bytes / (4 * (int64_t)d.batch)) % 128)) {
+      set_error("slm_model_ops: node " + std::to_string(v) + ": width must be a multiple of 128");
+      return SLM_E_UNSUPPORTED;
+    }
+    if (loss && nd.out_bytes != 4) {
+      set_error("slm_model_ops: the SoftmaxCE node's output is the 4-byte loss");
+      return SLM_E_ARG;
+    }
+    if (nd.op == SLM_OP_FC && (!d.W[v] || !d.b[v] || !d.dW[v] || !d.db[v])) {
+      set_error("slm_model_ops: FC node " + std::to_string(v) + " without W / b / dW / db");
+      return SLM_E_ARG;
+    }
+    if (nd.op == SLM_OP_BN && (!d.gamma[v] || !d.beta[v] || !d.dgamma[v] || !d.dbeta[v])) {
+      set_error("slm_model_ops: BN node " + std::to_string(v) + " without gamma / beta / dgamma / dbeta");
+      return SLM_E_ARG;
+    }
+    o.W.push_back(d.W[v]);
+    o.b.push_back(d.b[v]);
+    o.gamma.push_back(d.gamma[v]);
+    o.beta.push_back(d.beta[v]);
+    o.dW.push_back(d.dW[v]);
+    o.db.push_back(d.db[v]);
+    o.dgamma.push_back(d.dgamma[v]);
+    o.dbeta.push_back(d.dbeta[v]);
+    o.op.push_back(nd.op);
+    o.out_bytes.push_back(nd.out_bytes);
+    if (!loss) m->ops_maxw = std::max(m->ops_maxw, (int)(nd.out_bytes / (4 * (int64_t)d.batch)));
+  }
+  *out = m.release();
+  return SLM_OK;
+}
+
 void slm_model_destroy(slm_model* m) { delete m; }
+
+// workspace bytes of a model's step
+size_t model_ws_bytes(const slm_model& m) {
+  if (m.kind == SLM_MODEL_LSTM) return lstm_ws_layout(m.ld, m.lstm_sk, m.lstm_skx).total;
+  if (m.kind == SLM_MODEL_OPS) return ops_ws_layout(m).total;
+  return ws_layout(m).total;
+}
 
 slm_status slm_model_get_option(const slm_model* m, const char* key, int64_t* value) {
   if (!m || !key || !value) {
@@ -291,7 +359,7 @@ slm_status slm_workspace_bytes(const slm_plan* p, const slm_model* m, size_t* by
   slm_status s = check_plan_model(p, m);
   if (s != SLM_OK) return s;
   if (!bytes) return SLM_E_ARG;
-  *bytes = m->kind == SLM_MODEL_LSTM ? lstm_ws_layout(m->ld, m->lstm_sk, m->lstm_skx).total : ws_layout(*m).total;
+  *bytes = model_ws_bytes(*m);
   return SLM_OK;
 }
 
@@ -301,6 +369,12 @@ slm_status slm_step_launches(const slm_plan* p, const slm_model* m, int64_t* lau
   if (m->kind == SLM_MODEL_LSTM) {
     *launches = lstm_launches(p, *m);
     return SLM_OK;
+  }
+  if (m->kind == SLM_MODEL_OPS) {   // a dry run of the executor
+    int64_t n = 0;
+    s = enqueue_ops(p, const_cast<slm_model&>(*m), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &n, true);
+    *launches = n;
+    return s;
   }
   std::vector<Op> ops;
   if ((s = lower(p, &ops)) != SLM_OK) return s;
@@ -332,8 +406,8 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("null device buffer");
     return SLM_E_ARG;
   }
-  const bool is_lstm = m->kind == SLM_MODEL_LSTM;
-  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < (is_lstm ? lstm_ws_layout(m->ld, m->lstm_sk, m->lstm_skx).total : ws_layout(*m).total)) {
+  const bool is_lstm = m->kind == SLM_MODEL_LSTM, is_ops = m->kind == SLM_MODEL_OPS;
+  if ((int64_t)pool_bytes < p->pool_bytes || ws_bytes < model_ws_bytes(*m)) {
     set_error("pool or workspace smaller than required");
     return SLM_E_BUFFER_TOO_SMALL;
   }
@@ -341,8 +415,8 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("pool and workspace must be 256-byte aligned");
     return SLM_E_ARG;
   }
-  if (is_lstm && comm) {
-    set_error("the LSTM step runs replicas-only (comm must be NULL)");
+  if ((is_lstm || is_ops) && comm) {
+    set_error("the LSTM and op-graph steps run replicas-only (comm must be NULL)");
     return SLM_E_UNSUPPORTED;
   }
   int dev = 0;
@@ -354,16 +428,17 @@ slm_status slm_step(const slm_plan* p, slm_model* m, const void* x0, const int32
     set_error("slm kernels are built for sm_100a only");
     return SLM_E_UNSUPPORTED;
   }
-  if (!is_lstm && m->d.dtype == SLM_BF16 && m->gemm_impl == 0 && !tc_ok(*m)) {
+  if (!is_lstm && !is_ops && m->d.dtype == SLM_BF16 && m->gemm_impl == 0 && !tc_ok(*m)) {
     set_error("bf16 tcgen05 path needs width % 128 == 0 and batch % 64 == 0 (or gemm_impl=1)");
     return SLM_E_UNSUPPORTED;
   }
-  if (!is_lstm && comm && comm->world > 1 && m->d.batch_global <= 0) {
+  if (!is_lstm && !is_ops && comm && comm->world > 1 && m->d.batch_global <= 0) {
     set_error("data parallel step needs batch_global");
     return SLM_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
   auto run = [&]() {
+    if (is_ops) return enqueue_ops(p, *m, x0, labels, pool, ws, loss, st, &m->last_launches);
     return is_lstm ? enqueue_lstm(p, *m, x0, labels, pool, ws, loss, st, &m->last_launches)
                    : enqueue(p, *m, x0, labels, pool, ws, loss, st, comm, &m->last_launches);
   };
@@ -411,6 +486,14 @@ slm_status slm_step_host(const slm_plan* p, slm_model* m, const float* x0_host, 
   if (m->kind == SLM_MODEL_LSTM) {
     xb = (size_t)m->ld.steps * m->ld.batch * m->ld.n_in * 4;
     lb = (size_t)m->ld.steps * m->ld.batch * 4;
+  } else if (m->kind == SLM_MODEL_OPS) {
+    xb = (size_t)m->od.out_bytes[0];   // node 0 is the input (slm_graph_create keeps ids)
+    for (size_t v = 0; v < m->od.op.size(); ++v)
+      if (m->od.op[v] == SLM_OP_INPUT) {
+        xb = (size_t)m->od.out_bytes[v];
+        break;
+      }
+    lb = (size_t)m->od.batch * 4;
   } else {
     xb = (size_t)m->d.batch * m->d.width * 4;
     lb = (size_t)m->d.batch * 4;

@@ -1,0 +1,53 @@
+"""Host-side checks of the op-granularity model (slm_model_ops): what it accepts
+and rejects.  No GPU: model creation only records device pointers."""
+import ctypes as C
+
+import pytest
+
+import paper_1604_06174_b200 as slm
+from paper_1604_06174_b200 import _lib
+
+
+def _desc(n, B, fc=(), bn=()):
+    arrs = {k: (C.c_void_p * n)() for k in ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")}
+    for v in fc:
+        for k in ("W", "b", "dW", "db"):
+            arrs[k][v] = 0x1000 + v
+    for v in bn:
+        for k in ("gamma", "beta", "dgamma", "dbeta"):
+            arrs[k][v] = 0x2000 + v
+    vpp = C.POINTER(C.c_void_p)
+    d = _lib.OpsDesc(B, 0, n, *(C.cast(arrs[k], vpp) for k in ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")))
+    return d, arrs
+
+
+def _create(nodes, B, fc, bn):
+    g = slm.Graph.from_nodes(nodes, [len(nodes) - 1])
+    d, keep = _desc(len(nodes), B, fc, bn)
+    h = C.c_void_p()
+    rc = slm.lib.slm_model_ops(g._h, C.byref(d), C.byref(h))
+    if rc == 0:
+        slm.lib.slm_model_destroy(h)
+    return rc
+
+
+def test_preact_graph_accepted():
+    B = 64
+    nodes = slm.OpsModel.preact_nodes([2, 1], [128, 256], B)
+    fc = [v for v, n in enumerate(nodes) if n[0] == slm.OP["fc"]]
+    bn = [v for v, n in enumerate(nodes) if n[0] == slm.OP["bn"]]
+    assert _create(nodes, B, fc, bn) == 0
+
+
+def test_rejections():
+    B = 64
+    nodes = slm.OpsModel.preact_nodes([1], [128], B)
+    fc = [v for v, n in enumerate(nodes) if n[0] == slm.OP["fc"]]
+    bn = [v for v, n in enumerate(nodes) if n[0] == slm.OP["bn"]]
+    assert _create(nodes, B, fc[:0], bn) != 0            # FC without parameters
+    assert _create(nodes, B, fc, bn[:0]) != 0            # BN without parameters
+    assert _create(nodes, 96, fc, bn) != 0               # batch not a multiple of 64
+    bad = slm.OpsModel.preact_nodes([1], [192], B)       # width not a multiple of 128
+    assert _create(bad, B, fc, bn) != 0
+    sig = [(0, [], B * 128 * 4, 0), (slm.OP["sigmoid"], [0], B * 128 * 4, 0), (slm.OP["softmax_ce"], [1], 4, 1)]
+    assert _create(sig, B, [], []) != 0                  # unsupported op
