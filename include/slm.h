@@ -286,7 +286,26 @@ void slm_model_destroy(slm_model* m);
 /* Options (int64 values):
  *   use_graph       capture the whole step in a CUDA graph per buffer set (default 1)
  *   gemm_impl       0 = tcgen05/TMA tensor-core GEMMs (bf16, default), 1 = SIMT FFMA GEMMs
- *   bn_fwd, bn_dx, bn_dw   N tile of the forward / dX / dW tcgen05 GEMMs (32|64|128|256)
+ *   fused           1 (default) = chain: one fused Block kernel per node of V' (blk_fused.cuh:
+ *                   split-K tcgen05 GEMM over a cluster + batch norm in the epilogue);
+ *                   0 = the basic lowering (separate BN kernels)
+ *   block_cfg       fused Block shape: 0 = default for the batch, 1..4 = explicit (BM, S)
+ *   overlap         1 (default) = chain: each segment's recompute on its own stream, concurrent
+ *                   with the backward of the next segment, when the plan makes that sound
+ *                   (SLM_ALLOC_MIRROR_PARITY plans); other plans run sequentially
+ *   dw_stream       1 (default) = chain weight-gradient GEMMs on a second stream
+ *   pdl             1 (default) = programmatic dependent launch between the step's kernels
+ *   poison          debug: 1 = fill a pool tag with NaN once its value is dead (forces the
+ *                   sequential schedule); a plan that clobbers a live value then yields NaN
+ *   lstm_streams    1 = LSTM layer wavefront: one stream per layer + one for the head, ordered
+ *                   by per-buffer last-writer / reader events (0 = the caller's stream);
+ *                   2 (default) = plus one stream per layer for re-computed (mirror) units, so
+ *                   with a SLM_ALLOC_MIRROR_PARITY plan the recompute of a time segment runs
+ *                   concurrently with the backward of the next one
+ *   lstm_sk         split-K of the LSTM gates GEMMs (default 1, 0 = one wave of CTAs)
+ *   lstm_skx        split-K of the LSTM dX GEMMs (default 4, 0 = one wave of CTAs)
+ *   lstm_fuse_runs  1 (default) = LSTM forward / recompute phases as persistent chunk x layer
+ *                   runs (lstm_run.cuh); 0 = node by node in V' order
  *   profile_events  1 = record a CUDA event pair around every kernel of the step, by kind
  *                   (read with slm_model_kernel_times after the stream is synchronised)
  *   profile_ts      N > 0: the first N tcgen05 GEMM launches of a step record the device clock
@@ -294,23 +313,9 @@ void slm_model_destroy(slm_model* m);
  *                   (caller-owned, zeroed device buffer of N*1024*2 uint64, passed as an int64
  *                   pointer value); slm_model_kernel_times then adds each launch's span
  *                   (latest end - earliest start) to its GEMM kind.  Works inside the CUDA graph.
- *   fused, dw_stream, pdl   lowering switches of the chain
- *   sk_fwd, sk_dx   split-K of the fused forward / dX GEMMs (0 = auto, ~64 CTAs)
- *   fused_bn        N tile of the fused GEMMs (0 = min(batch, 128))
- *   cta_pair        1 = fused GEMMs as CTA pairs (tcgen05 cta_group::2, clusters of 2)
- *   overlap         1 (default) = chain: each segment's recompute on its own stream, concurrent
- *                   with the backward of the next segment, when the plan makes that sound
- *                   (SLM_ALLOC_MIRROR_PARITY plans); other plans run sequentially
- *   persist         1 = chain: runs of forward / mirror Blocks as one persistent kernel
- *                   (default 0: measured slower at the bench configuration)
- *   lstm_early_trigger  1 (default) = LSTM element-wise kernels release their dependent launch
- *                   (griddepcontrol.launch_dependents) right after their own dependency wait
- *   lstm_streams    1 = LSTM layer wavefront: one stream per layer + one for the head, ordered
- *                   by per-buffer last-writer / reader events (0 = the caller's stream);
- *                   2 (default) = plus one stream per layer for re-computed (mirror) units, so
- *                   with a SLM_ALLOC_MIRROR_PARITY plan the recompute of a time segment runs
- *                   concurrently with the backward of the next one
- *   lstm_sk         split-K of the LSTM gates GEMMs (default 2, 0 = one wave of CTAs) */
+ *   profile_ts_dep  1 = a CTA's span starts when it returns from its dependency wait
+ *   lstm_run_ts, lstm_run_ts_n   debug: per-step device clocks of the first persistent LSTM runs
+ * Every change drops the captured CUDA graphs.  SLM_E_ARG for an unknown key. */
 slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value);
 /* Reads an option back, or the read-only state "last_overlap" (1 = the last enqueued chain step
  * ran its segment recomputes on the recompute stream, concurrently with the backward; option
