@@ -94,21 +94,22 @@ class Clocks:
 
 
 # ======================================================================= reference arm
-def _ncu_gemm_traffic(d, B):
-    """DRAM bytes per launch of the dX GEMM (dram__bytes_read.sum + write) from the committed
-    `ncu --set full` summary (profiles/*_ncu_full_backward.md, C2 shapes only), else None."""
+def _ncu_block_traffic(d, B):
+    """DRAM bytes per launch of the forward Block kernel (dram__bytes_read.sum + write) from the
+    committed `ncu --set full` summary (profiles/*_ncu_full_block.md, C2 shapes only), else None."""
     import glob
     if (d, B) != (2048, 256):
         return None, None
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_full_backward.md")))
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_ncu_full_block.md")))
     for f in reversed(files):
         for line in open(f):
             cells = [c.strip() for c in line.strip().strip("|").split("|")]
-            if len(cells) > 3 and cells[0].startswith("tc_gemm_kernel<128, 1, 0"):
+            if len(cells) > 3 and cells[0].startswith("blk_kernel<256, 4, 0"):
                 try:
                     return round((float(cells[2]) + float(cells[3])) * 1e6), (
-                        f"{os.path.basename(f)}: dX GEMM dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                        f"(algorithmic: 8.39 MB of W + 1.05 MB of bf16 upstream gradient)")
+                        f"{os.path.basename(f)}: forward Block dram__bytes_read.sum + dram__bytes_write.sum per "
+                        f"launch (cold L2); algorithmic 11.5 MB (W 8.39 + a 1.05 + x 2.10) plus the by-design L2 "
+                        f"prefetch of the next layer's W (8.39 MB)")
                 except ValueError:
                     pass
     return None, None
@@ -350,7 +351,8 @@ def run_lstm(args):
                     flop_per_step={k: fl[k] for k in kinds},
                     timing="device clock per launch (%globaltimer) inside the graph; achieved = "
                            "algorithmic GEMM FLOPs of the step / summed launch spans",
-                    per_kind=per_kind, gemm_share_of_step=round(gemm_ms / prof_ms, 4) if prof_ms else None,
+                    per_kind=per_kind,
+                    summed_spans_over_step=round(gemm_ms / prof_ms, 4) if prof_ms else None,
                     step_ms_instrumented=round(prof_ms, 3))
 
     nock = None
@@ -670,41 +672,48 @@ def main():
     model.set_option("profile_ts_dep", 0)
     model.set_option("profile_ts", 0)
     pk = _peaks()
-    gemm_flop = 2.0 * B * d * d          # every GEMM kind: 2*B*d^2 per launch
+    gemm_flop = 2.0 * B * d * d          # every launch kind: 2*B*d^2 per launch
     kinds = ("gemm_fwd", "gemm_dx", "gemm_dw")
-    gemm_ms = sum(kt[k][0] for k in kinds)
-    gemm_cnt = sum(kt[k][1] for k in kinds)
-    avg_ms = gemm_ms / max(1, gemm_cnt)
-    achieved = gemm_flop / (avg_ms / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    fused = model.get_option("fused") == 1 and model.get_option("block_m") > 0
+    # dominant kernel: the forward / mirror Block (fused lowering: blk_kernel<.., BWD=0>, one
+    # launch per forward or mirror node, 2 B d^2 FLOP each; the largest share of the ncu launch
+    # list, profiles/r2_launches_summary.txt)
+    dom = "gemm_fwd"
+    avg_ms = kt[dom][0] / max(1, kt[dom][1])
+    achieved = gemm_flop / (avg_ms / 1e3) / 1e12
+    dep_avg = kt_dep[dom][0] / max(1, kt_dep[dom][1]) if kt_dep[dom][1] else None
+    achieved_dep = gemm_flop / (dep_avg / 1e3) / 1e12 if dep_avg else None
     per_kind = {k: {"avg_us": round(1e3 * kt[k][0] / max(1, kt[k][1]), 3),
+                    "avg_us_after_dependency": round(1e3 * kt_dep[k][0] / max(1, kt_dep[k][1]), 3),
                     "launches_per_step": kt[k][1] // prof_steps,
                     "tflops": round(gemm_flop / (kt[k][0] / max(1, kt[k][1]) / 1e3) / 1e12, 1) if kt[k][1] else None}
                 for k in kinds}
-    crit_ms = (kt["gemm_fwd"][0] + kt["gemm_dx"][0]) / prof_steps   # dW runs on a second stream
-    dep_ms = sum(kt_dep[k][0] for k in kinds)
-    dep_cnt = sum(kt_dep[k][1] for k in kinds)
-    achieved_dep = gemm_flop / (dep_ms / max(1, dep_cnt) / 1e3) / 1e12 if dep_ms else None
+    # share of the summed (after-dependency) launch spans of the step, the live counterpart of the
+    # ncu launch list's per-kernel share (which is serialised and cold-cache)
+    dep_tot = sum(kt_dep[k][0] for k in kinds)
+    for k in kinds:
+        per_kind[k]["share_of_launch_time"] = round(kt_dep[k][0] / dep_tot, 4) if dep_tot else None
     roofline = dict(bound="tensor", achieved=round(achieved, 2), peak=peak, unit="TFLOP/s",
                     frac=round(achieved / peak, 4), traffic=None,
                     achieved_after_dependency=round(achieved_dep, 2) if achieved_dep else None,
                     frac_after_dependency=round(achieved_dep / peak, 4) if achieved_dep else None,
-                    avg_us_after_dependency={k: round(1e3 * kt_dep[k][0] / max(1, kt_dep[k][1]), 3) for k in kinds},
-                    kernel="tc_gemm_kernel (forward, dX, dW GEMMs; 2*B*d^2 FLOP per launch)",
+                    kernel=("blk_kernel<B,S,BWD=0> fused forward / mirror Block (tcgen05 split-K GEMM + BN epilogue; "
+                            "2*B*d^2 FLOP per launch)") if fused else
+                           "tc_gemm_kernel forward GEMM (2*B*d^2 FLOP per launch)",
                     peak_source="MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)"
                     if "_fallback" not in pk else "fallback (B200_PROFILING.md)",
                     timing="device clock per launch (%globaltimer, CTA min start .. max end) inside the graph; "
                            "frac uses the span from launch, *_after_dependency from each CTA's return from "
                            "griddepcontrol.wait (excludes the PDL overlap with the predecessor)",
                     per_kind=per_kind,
-                    gemm_share_of_step=round(crit_ms / prof_ms, 4) if prof_ms else None,
                     step_ms_instrumented=round(prof_ms, 3))
     step_flop = 2.0 * B * d * d * (4 * n - math.isqrt(max(0, n - 1)) - 1 if args.strategy == "sqrt" else 3 * n)
     # whole-step tensor throughput (the launches of three streams overlap, so per-launch spans
-    # stretch under concurrency; this is the comparable figure) and the ncu DRAM traffic per GEMM
+    # stretch under concurrency; this is the comparable figure) and the ncu DRAM traffic
     roofline["achieved_step"] = round(step_flop / (ms / 1e3) / 1e12, 2)
     roofline["frac_step"] = round(roofline["achieved_step"] / peak, 4)
-    roofline["traffic"], roofline["traffic_source"] = _ncu_gemm_traffic(d, B)
+    roofline["traffic"], roofline["traffic_source"] = _ncu_block_traffic(d, B)
 
     # ---- non-checkpointed step (the "vs no-ckpt" half of the metric)
     nock = None
