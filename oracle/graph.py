@@ -17,12 +17,13 @@ from dataclasses import dataclass, field
 # ---- op kinds (numbering is part of the C ABI, include/slm.h mirrors it independently) ----
 INPUT, BLOCK, SOFTMAX_CE, FC, SIGMOID, RELU, BN, ADD, MUL, IDENTITY = range(10)
 LSTM_GATES, LSTM_CELL, HEAD_CE, SUM = 10, 11, 12, 13
+CONV, POOL = 14, 15   # convolution (NHWC, "same" padding) and global average pool
 
 OP_NAMES = {
     INPUT: "Input", BLOCK: "Block", SOFTMAX_CE: "SoftmaxCE", FC: "FullyConnected",
     SIGMOID: "Sigmoid", RELU: "ReLU", BN: "BatchNormLite", ADD: "Add", MUL: "ElemMul",
     IDENTITY: "Identity", LSTM_GATES: "LstmGates", LSTM_CELL: "LstmCell",
-    HEAD_CE: "HeadCE", SUM: "Sum",
+    HEAD_CE: "HeadCE", SUM: "Sum", CONV: "Convolution", POOL: "GlobalAvgPool",
 }
 
 
@@ -71,6 +72,10 @@ OPS = {
     LSTM_CELL:  OpMeta(1, 2, -1, False, 0b11, G_NONE, False),
     HEAD_CE:    OpMeta(1, 1, -1, False, 0b01, G_NONE, False),
     SUM:        OpMeta(1, ANY, -1, False, 0b00, G_NONE, False),
+    # convolution y = conv(x, W) + b: like FC, the backward reads its input only
+    CONV:       OpMeta(1, 1, -1, False, 0b01, G_NONE, False),
+    # global average pool over the spatial positions: the backward needs only the shapes
+    POOL:       OpMeta(1, 1, -1, False, 0b00, G_NONE, False),
 }
 
 # node flags (mirrored in include/slm.h)
@@ -217,6 +222,51 @@ def preact_resnet_graph(depths, sizes) -> Graph:
             x = len(nodes) - 1
     nodes.append(Node(SOFTMAX_CE, [x], 4, F_NOT_CANDIDATE))
     return Graph(nodes, [len(nodes) - 1], kind="dag", dims=dict(depths=list(depths)))
+
+
+def preact_resnet_conv_graph(batch, hw, stages, classes):
+    """Convolutional pre-activation ResNet (the network of the
+    paper's Fig. 5/6 experiments at synthetic size).  Values are NHWC fp32, stored as
+    [batch*H*W][C] rows; ``shapes[v] = (H, W, C, k, s)`` (k, s: kernel and stride of a CONV node,
+    0 otherwise).  The Input is the stem output [batch, hw, hw, C_0].  Stage i (C_i, depth_i) has
+    depth_i basic pre-activation blocks (He et al. 2016 "identity mappings"):
+        r = ReLU(BN(x));  y = Conv3x3(ReLU(BN(Conv3x3_s(r)))) ;  x' = Add(y, x)
+    where the first block of every stage after the first has stride 2 and a projection shortcut
+    Conv1x1_s2(r) in place of x (the stage transitions of P:437-441).  Head: ReLU(BN(x)) ->
+    GlobalAvgPool -> FC(classes) -> SoftmaxCE (4-byte loss)."""
+    c0 = stages[0][0]
+    nodes = [Node(INPUT, [], batch * hw * hw * c0 * 4)]
+    shapes = [(hw, hw, c0, 0, 0)]
+
+    def add(op, preds, H, W, C, k=0, s=0, flags=0):
+        nodes.append(Node(op, list(preds), (batch * H * W * C * 4) if op != SOFTMAX_CE else 4, flags))
+        shapes.append((H, W, C, k, s))
+        return len(nodes) - 1
+
+    x, H = 0, hw
+    for i, (C, depth) in enumerate(stages):
+        for j in range(depth):
+            s = 2 if (i > 0 and j == 0) else 1
+            Cin = shapes[x][2]
+            Ho = (H - 1) // s + 1
+            bn = add(BN, [x], H, H, Cin)
+            r = add(RELU, [bn], H, H, Cin)
+            c1 = add(CONV, [r], Ho, Ho, C, 3, s)
+            bn2 = add(BN, [c1], Ho, Ho, C)
+            r2 = add(RELU, [bn2], Ho, Ho, C)
+            c2 = add(CONV, [r2], Ho, Ho, C, 3, 1)
+            short = add(CONV, [r], Ho, Ho, C, 1, s) if (s != 1 or Cin != C) else x
+            x = add(ADD, [c2, short], Ho, Ho, C)
+            H = Ho
+    C = shapes[x][2]
+    bn = add(BN, [x], H, H, C)
+    r = add(RELU, [bn], H, H, C)
+    gp = add(POOL, [r], 1, 1, C)
+    fc = add(FC, [gp], 1, 1, classes)
+    add(SOFTMAX_CE, [fc], 1, 1, 1, flags=F_NOT_CANDIDATE)
+    g = Graph(nodes, [len(nodes) - 1], kind="dag",
+              dims=dict(batch=batch, hw=hw, stages=[list(t) for t in stages], classes=classes))
+    return g, shapes
 
 
 def unit_chain(n: int, unit: int = 1) -> Graph:

@@ -16,6 +16,14 @@ Node semantics (every value is [B, width] with width = out_bytes / (4 B); readin
 bf16 mode (reading A11) rounds exactly the GEMM operands the device rounds: the FC input x and W
 (forward), the upstream gradient dy (both backward GEMMs), and the dW output; the rest is fp64.
 
+Convolutional graphs (oracle.graph.preact_resnet_conv_graph) carry per-node shapes
+(H, W, C, k, s); a value is then the NHWC tensor [B, H, W, C] stored as [B*H*W, C] rows (BN's
+statistics run over all B*H*W rows of a channel: per-channel batch norm):
+  Conv        y[b,i,j,o] = b_o + sum_{u,v,c} W[o, (u k + v) C_in + c] x[b, i s + u - p, j s + v - p, c]
+              ("same" zero padding p = k // 2, stride s, W [C_out, k*k*C_in]) -- the definition,
+              summed tap by tap; bf16 mode rounds x, W, dy and dW like FC
+  GlobalAvgPool  y[b,c] = (1 / (H W)) sum_{h,w} x[b,h,w,c]
+
 Two executors, as for the chain: step_plain (ordinary back-propagation: the definition) and
 step_planned (interprets V' of a plan node by node through the allocator's tags with the
 interference check; gradient nodes hold the gradient w.r.t. all of v's inputs, concatenated in
@@ -27,17 +35,70 @@ from __future__ import annotations
 import numpy as np
 
 from .chain import EPS, TagClobber, _q, bf16_round
-from .graph import ADD, BN, FC, INPUT, RELU, SOFTMAX_CE, Graph
+from .graph import ADD, BN, CONV, FC, INPUT, POOL, RELU, SOFTMAX_CE, Graph
 
 
 class OpParams:
-    """Per-node parameters: FC -> (W, b), BN -> (gamma, beta); float64 arrays."""
+    """Per-node parameters: FC / Conv -> (W, b), BN -> (gamma, beta); float64 arrays.
+    Convolutional graphs also give ``shapes`` (node -> (H, W, C, k, s)) and the graph, from which
+    every Conv / Pool node's input shape is taken (in_shape)."""
 
-    def __init__(self, W=None, b=None, gamma=None, beta=None):
+    def __init__(self, W=None, b=None, gamma=None, beta=None, shapes=None, graph=None):
         self.W = {k: np.asarray(v, np.float64) for k, v in (W or {}).items()}
         self.b = {k: np.asarray(v, np.float64) for k, v in (b or {}).items()}
         self.gamma = {k: np.asarray(v, np.float64) for k, v in (gamma or {}).items()}
         self.beta = {k: np.asarray(v, np.float64) for k, v in (beta or {}).items()}
+        self.shapes = shapes
+        self.in_shape = {}
+        if shapes is not None and graph is not None:
+            for v, nd in enumerate(graph.nodes):
+                if nd.preds:
+                    self.in_shape[v] = shapes[nd.preds[0]]
+
+    def width(self, v, out_bytes, batch):
+        """Row width of node v's value: C of its shape, else out_bytes / (4 batch)."""
+        if self.shapes is not None:
+            return self.shapes[v][2]
+        return out_bytes // (4 * batch)
+
+
+def conv_forward(x, W, b, in_shape, k, s, mode):
+    """Conv (definition above) of x [B*H*W, C_in] -> [B*Ho*Wo, C_out]."""
+    H, Wd, Cin = in_shape[0], in_shape[1], in_shape[2]
+    B = x.shape[0] // (H * Wd)
+    p = k // 2
+    Ho, Wo = (H + 2 * p - k) // s + 1, (Wd + 2 * p - k) // s + 1
+    Cout = W.shape[0]
+    xp = np.pad(_q(x, mode).reshape(B, H, Wd, Cin), ((0, 0), (p, p), (p, p), (0, 0)))
+    Wt = _q(W, mode).reshape(Cout, k, k, Cin)
+    y = np.zeros((B, Ho, Wo, Cout)) + b
+    for u in range(k):
+        for v in range(k):
+            xs = xp[:, u:u + s * (Ho - 1) + 1:s, v:v + s * (Wo - 1) + 1:s, :]
+            y += xs @ Wt[:, u, v, :].T
+    return y.reshape(B * Ho * Wo, Cout)
+
+
+def conv_backward(dy, x, W, in_shape, k, s, mode):
+    """(dx, dW, db) of the Conv: dW[o, (u,v,c)] = sum_{b,i,j} dy[b,i,j,o] x[b, i s+u-p, j s+v-p, c],
+    dx[b,h,w,c] = sum over the taps that read x[b,h,w] of dy[b,i,j,:] . W[:, (u,v,c)]."""
+    H, Wd, Cin = in_shape[0], in_shape[1], in_shape[2]
+    B = x.shape[0] // (H * Wd)
+    p = k // 2
+    Ho, Wo = (H + 2 * p - k) // s + 1, (Wd + 2 * p - k) // s + 1
+    Cout = W.shape[0]
+    dq = _q(dy, mode).reshape(B, Ho, Wo, Cout)
+    xp = np.pad(_q(x, mode).reshape(B, H, Wd, Cin), ((0, 0), (p, p), (p, p), (0, 0)))
+    Wt = _q(W, mode).reshape(Cout, k, k, Cin)
+    dW = np.zeros((Cout, k, k, Cin))
+    dxp = np.zeros_like(xp)
+    for u in range(k):
+        for v in range(k):
+            sl = (slice(None), slice(u, u + s * (Ho - 1) + 1, s), slice(v, v + s * (Wo - 1) + 1, s), slice(None))
+            dW[:, u, v, :] = dq.reshape(-1, Cout).T @ xp[sl].reshape(-1, Cin)
+            dxp[sl] += dq @ Wt[:, u, v, :]
+    dx = dxp[:, p:p + H, p:p + Wd, :].reshape(B * H * Wd, Cin)
+    return dx, _q(dW.reshape(Cout, k * k * Cin), mode), dy.sum(axis=0)
 
 
 def forward_node(op, v, ins, P: OpParams, mode, labels=None, Bg=None):
@@ -52,11 +113,16 @@ def forward_node(op, v, ins, P: OpParams, mode, labels=None, Bg=None):
         return _q(ins[0], mode) @ _q(P.W[v], mode).T + P.b[v]
     if op == ADD:
         return ins[0] + ins[1]
+    if op == CONV:
+        return conv_forward(ins[0], P.W[v], P.b[v], P.in_shape[v], P.shapes[v][3], P.shapes[v][4], mode)
+    if op == POOL:
+        H, Wd, C = P.in_shape[v][:3]
+        return ins[0].reshape(-1, H * Wd, C).mean(axis=1)
     if op == SOFTMAX_CE:
         x = ins[0]
         mx = x.max(axis=1, keepdims=True)
         lse = np.log(np.exp(x - mx).sum(axis=1)) + mx[:, 0]
-        return float((lse - x[np.arange(x.shape[0]), labels]).sum() / Bg)
+        return float((lse - x[np.arange(x.shape[0]), labels]).sum() / (Bg or x.shape[0]))
     raise NotImplementedError(op)
 
 
@@ -81,13 +147,20 @@ def backward_node(op, v, dy, ins, out, P: OpParams, mode, grads, labels=None, Bg
         return [dq @ _q(P.W[v], mode)]
     if op == ADD:
         return [dy, dy]
+    if op == CONV:
+        dx, grads["W"][v], grads["b"][v] = conv_backward(dy, ins[0], P.W[v], P.in_shape[v], P.shapes[v][3],
+                                                          P.shapes[v][4], mode)
+        return [dx]
+    if op == POOL:
+        H, Wd, C = P.in_shape[v][:3]
+        return [np.repeat(dy[:, None, :] / (H * Wd), H * Wd, axis=1).reshape(-1, C)]
     if op == SOFTMAX_CE:
         x = ins[0]
         mx = x.max(axis=1, keepdims=True)
         e = np.exp(x - mx)
         p = e / e.sum(axis=1, keepdims=True)
         p[np.arange(x.shape[0]), labels] -= 1.0
-        return [p / Bg]
+        return [p / (Bg or x.shape[0])]
     raise NotImplementedError(op)
 
 
@@ -98,7 +171,7 @@ def _empty_grads():
 def step_plain(g: Graph, P: OpParams, x0, labels, mode="f64", batch_global=None):
     """Ordinary back-propagation over the graph (the definition the plans must reproduce)."""
     x0 = np.asarray(x0, np.float64)
-    Bg = batch_global or x0.shape[0]
+    Bg = batch_global   # None: the loss input's rows (the batch)
     val = {}
     for v, nd in enumerate(g.nodes):
         val[v] = x0 if nd.op == INPUT else forward_node(nd.op, v, [val[u] for u in nd.preds], P, mode, labels, Bg)
@@ -124,7 +197,7 @@ def step_plain(g: Graph, P: OpParams, x0, labels, mode="f64", batch_global=None)
 def step_planned(plan, g: Graph, P: OpParams, x0, labels, mode="f64", batch_global=None):
     """Interpret V' of `plan` (oracle.planner.plan on g) node by node through the tags."""
     x0 = np.asarray(x0, np.float64)
-    Bg = batch_global or x0.shape[0]
+    Bg = batch_global   # None: the loss input's rows (the batch)
     gg, al = plan.gg, plan.alloc
     store = {}
     grads = _empty_grads()
@@ -158,7 +231,7 @@ def step_planned(plan, g: Graph, P: OpParams, x0, labels, mode="f64", batch_glob
                 spreds = g.nodes[s.orig].preds
                 off = 0
                 for u in spreds:
-                    w = g.nodes[u].out_bytes // (4 * x0.shape[0])
+                    w = P.width(u, g.nodes[u].out_bytes, x0.shape[0])
                     if u == orig:
                         sl = sg[:, off:off + w]
                         dy = sl if dy is None else dy + sl

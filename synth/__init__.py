@@ -93,25 +93,38 @@ def lstm_inputs(n_layers, steps, batch, hidden, n_in, n_classes, dtype="f32", se
                 n_in=n_in)
 
 
-def opgraph_inputs(nodes, batch, seed=SEED):
+def opgraph_inputs(nodes, batch, seed=SEED, shapes=None):
     """Inputs of an op-granularity graph: nodes = [(op, preds, out_bytes, flags)]
     with the slm op codes (FC = 3, BN = 6).  Per FC node W [dout, din] ~ N(0, 1/din) (bf16-valued
     f32) and b ~ N(0, 0.01^2); per BN node gamma ~ 1 + N(0, 0.1^2), beta ~ N(0, 0.1^2) (the chain's
     recipe); x0 [B, w_in] ~ N(0, 1); labels ~ U{0 .. w_out - 1} (w_out = the width of the
-    loss's input).  Returns dict(params={node: {..}}, x0, labels)."""
+    loss's input).  Returns dict(params={node: {..}}, x0, labels).
+    Convolutional graphs pass shapes[v] = (H, W, C, k, s): widths are the channel
+    counts, x0 is [B*H*W, C_0] (NHWC rows), and a Conv node (op 14) gets W [C_out, k*k*C_in] ~
+    N(0, 1/(k*k*C_in)) (fan-in scaling, as FC) and b ~ N(0, 0.01^2)."""
     r = _streams(seed, 2 + 2 * len(nodes))
-    width = [ob // (4 * batch) for (_, _, ob, _) in nodes]
+    if shapes is not None:
+        width = [sh[2] for sh in shapes]
+        rows0 = batch * shapes[0][0] * shapes[0][1]
+    else:
+        width = [ob // (4 * batch) for (_, _, ob, _) in nodes]
+        rows0 = batch
     params = {}
     for v, (op, preds, ob, _) in enumerate(nodes):
         ra, rb = r[2 + 2 * v], r[3 + 2 * v]
-        if op == 3:
+        if op == 14:
+            k, cin, cout = shapes[v][3], width[preds[0]], width[v]
+            fan = k * k * cin
+            params[v] = dict(W=bf16_values(ra.standard_normal((cout, fan)) / np.sqrt(fan)),
+                             b=(0.01 * rb.standard_normal(cout)).astype(np.float32))
+        elif op == 3:
             din, dout = width[preds[0]], width[v]
             params[v] = dict(W=bf16_values(ra.standard_normal((dout, din)) / np.sqrt(din)),
                              b=(0.01 * rb.standard_normal(dout)).astype(np.float32))
         elif op == 6:
             params[v] = dict(gamma=(1.0 + 0.1 * ra.standard_normal(width[v])).astype(np.float32),
                              beta=(0.1 * rb.standard_normal(width[v])).astype(np.float32))
-    x0 = r[0].standard_normal((batch, width[0])).astype(np.float32)
+    x0 = r[0].standard_normal((rows0, width[0])).astype(np.float32)
     loss_in = nodes[-1][1][0]
     labels = r[1].integers(0, width[loss_in], size=batch).astype(np.int32)
     return dict(params=params, x0=x0, labels=labels)
