@@ -80,7 +80,9 @@ enum {
   SLM_OP_LSTM_GATES = 10, /* (x_or_lower_state[, prev_state]); bwd reads output and inputs    */
   SLM_OP_LSTM_CELL = 11,  /* (gates[, prev_state]); bwd reads both inputs                     */
   SLM_OP_HEAD_CE = 12,    /* per-step softmax head + CE; bwd reads its input                  */
-  SLM_OP_SUM = 13         /* scalar sum of any number of inputs                               */
+  SLM_OP_SUM = 13,        /* scalar sum of any number of inputs                               */
+  SLM_OP_CONV = 14,       /* convolution (NHWC, "same" padding); bwd reads its input          */
+  SLM_OP_POOL = 15        /* global average pool over the spatial positions; bwd reads nothing */
 };
 enum {
   SLM_NODE_NOT_CANDIDATE = 1, /* exclude from Alg. 3's candidate set C         */
@@ -275,11 +277,22 @@ slm_status slm_model_lstm(const slm_lstm_desc* desc, slm_model** out);
  * Gradients are overwritten by every step.  Constraints of the tcgen05 path: batch % 64 == 0,
  * every width % 128 == 0.  Step inputs: x0 [batch][w_input] fp32, labels int32 [batch].
  * Runs replicas-only (comm must be NULL).  SLM_E_ARG / SLM_E_UNSUPPORTED (message in
- * slm_last_error) for an unsupported op, a bad width or a missing parameter. */
+ * slm_last_error) for an unsupported op, a bad width or a missing parameter.
+ * Convolutional graphs (oracle.graph.preact_resnet_conv_graph):
+ * `shape` = 5 int32 per node (H, W, C, k, s); a node's value is then the NHWC tensor
+ * [batch][H][W][C] fp32 (rows = batch H W of width C; out_bytes must equal 4 batch H W C), BN
+ * normalises each channel over all rows, and two more ops are available:
+ *   Conv (SLM_OP_CONV)  k x k ("same" zero padding k / 2), stride s, k in {1, 3}, s in {1, 2}:
+ *       W bf16 [C_out][k k C_in] (K index (u k + v) C_in + c), b fp32 [C_out]; the output H, W
+ *       must be (H_in - 1) / s + 1; C_in % 128 == 0.  Lowered as im2col + tcgen05 GEMM (forward:
+ *       y = col W^T + b; backward: dW = dy^T col, dcol = dy W, col2im gather), db = sum dy.
+ *   Pool (SLM_OP_POOL)  global average over the H W positions -> [batch][C] (H = W = 1).
+ * FC nodes then need an input with H = W = 1.  shape = NULL: H = W = 1, C = out_bytes / (4 batch). */
 typedef struct {
   int32_t batch, batch_global, n_nodes;
   const void* const* W; const float* const* b; const float* const* gamma; const float* const* beta;
   void* const* dW; float* const* db; float* const* dgamma; float* const* dbeta;
+  const int32_t* shape;   /* n_nodes x (H, W, C, k, s), or NULL (copied) */
 } slm_ops_desc;
 slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model** out);
 void slm_model_destroy(slm_model* m);

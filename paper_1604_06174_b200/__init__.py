@@ -23,7 +23,7 @@ __all__ = ["Graph", "Plan", "ChainModel", "LstmModel", "Comm", "recursion_estima
 STRATEGY = {"none": 0, "sqrt": 1, "budget": 2, "search": 3, "recursive": 4, "explicit": 5,
             "drop_cheap": 6}
 OP = dict(input=0, block=1, softmax_ce=2, fc=3, sigmoid=4, relu=5, bn=6, add=7, mul=8,
-          identity=9, lstm_gates=10, lstm_cell=11, head_ce=12, sum=13)
+          identity=9, lstm_gates=10, lstm_cell=11, head_ce=12, sum=13, conv=14, pool=15)
 ALLOC_INPLACE, ALLOC_SHARING, ALLOC_GROUPED, ALLOC_GROUP_MIRRORS, ALLOC_MIRROR_PARITY = 1, 2, 4, 8, 16
 NODE_NOT_CANDIDATE, NODE_PIN, NODE_REQUEST_GRAD = 1, 2, 4
 
@@ -399,7 +399,9 @@ class OpsModel(_Model):
     {node id: {"W": bf16 [dout, din], "b": f32 [dout]}} for FC nodes and {"gamma", "beta"} (f32)
     for BN nodes (grads: the same keys, W bf16)."""
 
-    def __init__(self, graph, params, grads, batch, batch_global=0, **options):
+    def __init__(self, graph, params, grads, batch, batch_global=0, shapes=None, **options):
+        """shapes: per node (H, W, C, k, s) for convolutional graphs (Conv params
+        {"W": bf16 [C_out, k*k*C_in], "b": f32 [C_out]}), None for [batch][w] graphs."""
         n = len(graph)
         self.params, self.grads, self.graph = params, grads, graph
         arrs = {k: (C.c_void_p * max(1, n))() for k in ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")}
@@ -413,8 +415,13 @@ class OpsModel(_Model):
                     arrs["d" + k][v] = _ptr(gv[k]).value
         self._arrs = arrs
         vpp = C.POINTER(C.c_void_p)
+        self._shape = None
+        if shapes is not None:
+            flat = [int(x) for sh in shapes for x in sh]
+            self._shape = (C.c_int32 * len(flat))(*flat)
         desc = _lib.OpsDesc(batch, batch_global, n, *(C.cast(arrs[k], vpp) for k in
-                                                       ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")))
+                                                       ("W", "b", "gamma", "beta", "dW", "db", "dgamma", "dbeta")),
+                            C.cast(self._shape, C.POINTER(C.c_int32)) if self._shape is not None else None)
         h = C.c_void_p()
         check(lib.slm_model_ops(graph._h, C.byref(desc), C.byref(h)), "slm_model_ops")
         self._init(h, options)
@@ -438,6 +445,39 @@ class OpsModel(_Model):
                 x = len(nodes) - 1
         nodes.append((OP["softmax_ce"], [x], 4, 1))
         return nodes
+
+    @staticmethod
+    def preact_conv_nodes(batch, hw, stages, classes):
+        """(nodes, shapes) of the convolutional pre-activation ResNet of SURVEY 8(f) f4 (the graph of
+        oracle.graph.preact_resnet_conv_graph): stages [(C, depth)], basic blocks
+        BN -> ReLU -> Conv3x3_s -> BN -> ReLU -> Conv3x3 -> Add, the first block of every later stage
+        with stride 2 and a Conv1x1_s2 projection shortcut of the pre-activated input; head
+        BN -> ReLU -> Pool -> FC(classes) -> SoftmaxCE.  shapes[v] = (H, W, C, k, s)."""
+        c0 = stages[0][0]
+        nodes, shapes = [(OP["input"], [], batch * hw * hw * c0 * 4, 0)], [(hw, hw, c0, 0, 0)]
+
+        def add(op, preds, H, C, k=0, s=0, flags=0):
+            nodes.append((OP[op], list(preds), batch * H * H * C * 4 if op != "softmax_ce" else 4, flags))
+            shapes.append((H, H, C, k, s))
+            return len(nodes) - 1
+
+        x, H = 0, hw
+        for i, (C_, depth) in enumerate(stages):
+            for j in range(depth):
+                s = 2 if (i > 0 and j == 0) else 1
+                cin = shapes[x][2]
+                Ho = (H - 1) // s + 1
+                r = add("relu", [add("bn", [x], H, cin)], H, cin)
+                c1 = add("conv", [r], Ho, C_, 3, s)
+                c2 = add("conv", [add("relu", [add("bn", [c1], Ho, C_)], Ho, C_)], Ho, C_, 3, 1)
+                short = add("conv", [r], Ho, C_, 1, s) if (s != 1 or cin != C_) else x
+                x = add("add", [c2, short], Ho, C_)
+                H = Ho
+        C_ = shapes[x][2]
+        r = add("relu", [add("bn", [x], H, C_)], H, C_)
+        fc = add("fc", [add("pool", [r], 1, C_)], 1, classes)
+        add("softmax_ce", [fc], 1, 1, flags=1)
+        return nodes, shapes
 
 
 def debug_gemm(kind, impl, bn, M, N, K, A, B, out, resid=None, bias=None, stream=None, split=1):

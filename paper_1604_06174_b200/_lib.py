@@ -55,7 +55,8 @@ class LstmDesc(C.Structure):
 class OpsDesc(C.Structure):
     _fields_ = [("batch", i32), ("batch_global", i32), ("n_nodes", i32),
                 ("W", C.POINTER(vp)), ("b", C.POINTER(vp)), ("gamma", C.POINTER(vp)), ("beta", C.POINTER(vp)),
-                ("dW", C.POINTER(vp)), ("db", C.POINTER(vp)), ("dgamma", C.POINTER(vp)), ("dbeta", C.POINTER(vp))]
+                ("dW", C.POINTER(vp)), ("db", C.POINTER(vp)), ("dgamma", C.POINTER(vp)), ("dbeta", C.POINTER(vp)),
+                ("shape", C.POINTER(i32))]
 
 
 def _sig(name, res, *args):

@@ -316,6 +316,10 @@ struct slm_ops_model {
   std::vector<float*> db, dgamma, dbeta;
   std::vector<int> op;
   std::vector<int64_t> out_bytes;
+  // per node: rows (batch H W) and (H, W, C, k, s) (convolutional graphs)
+  std::vector<int64_t> rows;
+  std::vector<std::array<int, 5>> shape;
+  int64_t max_elems = 0, max_col = 0, max_parts = 0;   // workspace sizing
 };
 
 struct slm_model {

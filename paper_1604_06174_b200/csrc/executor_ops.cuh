@@ -24,20 +24,24 @@ namespace {
 
 bool ops_supported(int op) {
   return op == SLM_OP_INPUT || op == SLM_OP_BN || op == SLM_OP_RELU || op == SLM_OP_FC || op == SLM_OP_ADD ||
-         op == SLM_OP_SOFTMAX_CE;
+         op == SLM_OP_SOFTMAX_CE || op == SLM_OP_CONV || op == SLM_OP_POOL;
 }
 
+// workspace: bf16 GEMM operands (x / im2col columns, dy), the summed upstream gradient, the conv
+// column gradient dcol (fp32), the chunk partials of the many-row reductions, CE row losses
 struct OpsWs {
-  size_t xq, gq, dy, rowloss, total;
+  size_t xq, gq, dy, dcol, parts, rowloss, total;
 };
 OpsWs ops_ws_layout(const slm_model& m) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  const size_t B = m.od.batch, W = m.ops_maxw;
+  const size_t B = m.od.batch, E = (size_t)m.od.max_elems, Kc = (size_t)m.od.max_col;
   OpsWs L{};
   size_t off = 0;
-  L.xq = off;      off += al(B * W * 2);
-  L.gq = off;      off += al(B * W * 2);
-  L.dy = off;      off += al(B * W * 4);
+  L.xq = off;      off += al(std::max(E, Kc) * 2);
+  L.gq = off;      off += al(E * 2);
+  L.dy = off;      off += al(E * 4);
+  L.dcol = off;    off += al(Kc * 4);
+  L.parts = off;   off += al((size_t)m.od.max_parts * 4 * 4);
   L.rowloss = off; off += al(B * 4);
   L.total = off;
   return L;
@@ -65,9 +69,15 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   bf* gq = (bf*)(w8 + W.gq);
   float* dyw = (float*)(w8 + W.dy);
   float* rowloss = (float*)(w8 + W.rowloss);
+  float* dcol = (float*)(w8 + W.dcol);
+  float* parts = (float*)(w8 + W.parts);
+  const size_t PS = (size_t)d.max_parts;   // one partial array: chunks x C floats
   slm_status s = SLM_OK;
   int64_t nl = 0;
-  auto width = [&](int node) { return (int)(p->out_bytes[node] / (4 * (int64_t)B)); };
+  // rows (batch H W) and width (C) of a node's value; mirrors / gradient nodes use their forward node's
+  auto rows = [&](int node) { return (int)d.rows[p->orig[node]]; };
+  auto width = [&](int node) { return (int)(p->out_bytes[node] / (4 * (int64_t)rows(node))); };
+  auto shp = [&](int node) { return d.shape[p->orig[node]]; };
   std::vector<void*> tp(p->tag_size.size(), nullptr);
   for (size_t t = 0; t < tp.size(); ++t)
     if (p->tag_offset[t] >= 0) tp[t] = (uint8_t*)pool + p->tag_offset[t];
@@ -87,6 +97,38 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     return dry ? SLM_OK : make_map(mp, base, (uint64_t)inner, (uint64_t)rows, (uint32_t)box_rows);
   };
   const int bnB = B % 256 == 0 ? 256 : B % 128 == 0 ? 128 : 64;   // N tile over the batch
+  auto ntile = [](int64_t R) { return R % 256 == 0 ? 256 : R % 128 == 0 ? 128 : 64; };
+  // per-channel sums over R rows: the original one-CTA-per-32-channels kernels up to kRowChunk
+  // rows (the f1 graphs' bits), the chunked kernels beyond
+  auto nchunk = [](int64_t R) { return (int)((R + kRowChunk - 1) / kRowChunk); };
+  auto colsum = [&](const float* x, int64_t R, int C, float* out) -> slm_status {
+    if (R <= kRowChunk) {
+      OK_(launch_k(colsum_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, x, (int)R, C, out));
+      ++nl;
+    } else {
+      OK_(launch_k(op_colpart_kernel, dim3((C + 31) / 32, nchunk(R)), eb, 0, st, pdl, x, (int)R, C, parts));
+      OK_(launch_k(op_colfin_kernel, dim3((C + 255) / 256), eb, 0, st, pdl, (const float*)parts, nchunk(R), C, out));
+      nl += 2;
+    }
+    return SLM_OK;
+  };
+  auto geom = [&](int v, int in_node) {
+    const auto so = shp(v), si = shp(in_node);
+    return ConvGeom{si[0], si[1], si[2], so[3], so[4], so[0], so[1]};
+  };
+  // Conv forward: col = im2col(x) (bf16), y = col W^T + b (tcgen05, M = C_out, N = rows, K = k k C_in)
+  auto conv_fwd = [&](int v, int in_node, const float* x, float* y) -> slm_status {
+    const ConvGeom g = geom(v, in_node);
+    const int64_t R = rows(v);
+    const int K = g.k * g.k * g.Cin, Cout = width(v);
+    OK_(launch_k(op_im2col_kernel, ew((size_t)R * K / 8), eb, 0, st, pdl, x, g, (size_t)R, xq));
+    if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
+    if ((s = kmap(&mb, xq, K, (int)R, ntile(R))) != SLM_OK) return s;
+    EpiBiasF32 e{y, Cout, d.b[p->orig[v]]};
+    OT_((launch_tc_bn<EpiBiasF32, false, false, true>(ntile(R), 1, ma, mb, Cout, (int)R, K, 0, 0, e, st, pdl)));
+    nl += 2;
+    return SLM_OK;
+  };
   // FC x -> y = x W^T + b   (W [dout][din] bf16)
   auto fc_fwd = [&](int v, const float* x, int din, int dout, float* y) -> slm_status {
     OK_(launch_k(op_pack_kernel, ew((size_t)B * din), eb, 0, st, pdl, x, B, din, din, xq));
@@ -107,24 +149,46 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
       switch (op) {
         case SLM_OP_INPUT:
           break;
-        case SLM_OP_BN:
-          OK_(launch_k(op_bn_fwd_kernel, dim3((w + 31) / 32), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
-                       d.beta[u], B, w, V(v)));
-          ++nl;
+        case SLM_OP_BN: {
+          const int R = rows(v);
+          if (R <= kRowChunk) {
+            OK_(launch_k(op_bn_fwd_kernel, dim3((w + 31) / 32), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
+                         d.beta[u], R, w, V(v)));
+            ++nl;
+          } else {   // chunked two-pass statistics, then the affine map
+            const dim3 gr((w + 31) / 32, nchunk(R));
+            OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, parts));
+            OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)parts,
+                         parts + PS));
+            OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)parts,
+                         (const float*)(parts + PS), d.gamma[u], d.beta[u], V(v)));
+            nl += 3;
+          }
           break;
+        }
         case SLM_OP_RELU:
-          OK_(launch_k(op_relu_fwd_kernel, ew((size_t)B * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
-                       (size_t)B * w / 4, (float4*)V(v)));
+          OK_(launch_k(op_relu_fwd_kernel, ew((size_t)rows(v) * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
+                       (size_t)rows(v) * w / 4, (float4*)V(v)));
           ++nl;
           break;
         case SLM_OP_ADD:
-          OK_(launch_k(op_add_fwd_kernel, ew((size_t)B * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
-                       (const float4*)V(pv[1]), (size_t)B * w / 4, (float4*)V(v)));
+          OK_(launch_k(op_add_fwd_kernel, ew((size_t)rows(v) * w / 4), eb, 0, st, pdl, (const float4*)V(pv[0]),
+                       (const float4*)V(pv[1]), (size_t)rows(v) * w / 4, (float4*)V(v)));
           ++nl;
           break;
         case SLM_OP_FC:
           if ((s = fc_fwd(v, V(pv[0]), width(pv[0]), w, V(v))) != SLM_OK) return s;
           break;
+        case SLM_OP_CONV:
+          if ((s = conv_fwd(v, pv[0], V(pv[0]), V(v))) != SLM_OK) return s;
+          break;
+        case SLM_OP_POOL: {
+          const auto si = shp(pv[0]);
+          OK_(launch_k(op_pool_fwd_kernel, ew((size_t)B * w), eb, 0, st, pdl, (const float*)V(pv[0]), B, si[0] * si[1],
+                       w, V(v)));
+          ++nl;
+          break;
+        }
         case SLM_OP_SOFTMAX_CE: {
           const int wi = width(pv[0]);
           OK_(launch_k(ce_fwd_kernel, dim3(B), eb, 0, st, pdl, (const float*)V(pv[0]), labels, wi, rowloss));
@@ -173,27 +237,75 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
       if (gs.n == 1 && gs.ld[0] == wu) {
         dy = gs.p[0];   // one whole slice in the node's own layout (an in-place output aliases it element for element)
       } else {
-        OK_(launch_k(op_gsum_kernel, ew((size_t)B * wu), eb, 0, st, pdl, gs, B, wu, dyw));
+        OK_(launch_k(op_gsum_kernel, ew((size_t)rows(u) * wu), eb, 0, st, pdl, gs, rows(u), wu, dyw));
         ++nl;
         dy = dyw;
       }
     }
+    const int Ru = rows(u);
     switch (op) {
       case SLM_OP_RELU:   // rest = [output]
-        OK_(launch_k(op_relu_bwd_kernel, ew((size_t)B * wu / 4), eb, 0, st, pdl, (const float4*)dy,
-                     (const float4*)V(rest[0]), (size_t)B * wu / 4, (float4*)V(v)));
+        OK_(launch_k(op_relu_bwd_kernel, ew((size_t)Ru * wu / 4), eb, 0, st, pdl, (const float4*)dy,
+                     (const float4*)V(rest[0]), (size_t)Ru * wu / 4, (float4*)V(v)));
         ++nl;
         break;
       case SLM_OP_BN:   // rest = [x]
-        OK_(launch_k(op_bn_bwd_kernel, dim3((wu + 31) / 32), eb, 0, st, pdl, dy, (const float*)V(rest[0]), d.gamma[u],
-                     B, wu, V(v), d.dgamma[u], d.dbeta[u]));
-        ++nl;
+        if (Ru <= kRowChunk) {
+          OK_(launch_k(op_bn_bwd_kernel, dim3((wu + 31) / 32), eb, 0, st, pdl, dy, (const float*)V(rest[0]),
+                       d.gamma[u], Ru, wu, V(v), d.dgamma[u], d.dbeta[u]));
+          ++nl;
+        } else {
+          const dim3 gr((wu + 31) / 32, nchunk(Ru));
+          const float* xr = V(rest[0]);
+          OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, parts));
+          OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, (const float*)parts, parts + PS));
+          OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)parts,
+                       (const float*)(parts + PS), parts + 2 * PS, parts + 3 * PS));
+          OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)parts,
+                       (const float*)(parts + PS), (const float*)(parts + 2 * PS), (const float*)(parts + 3 * PS),
+                       d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));
+          nl += 4;
+        }
         break;
       case SLM_OP_ADD:   // [dy | dy]
-        OK_(launch_k(op_add_bwd_kernel, ew((size_t)B * wu / 4), eb, 0, st, pdl, (const float4*)dy, B, wu / 4,
+        OK_(launch_k(op_add_bwd_kernel, ew((size_t)Ru * wu / 4), eb, 0, st, pdl, (const float4*)dy, Ru, wu / 4,
                      (float4*)V(v)));
         ++nl;
         break;
+      case SLM_OP_POOL: {   // rest = []; dx[b][q][c] = dy[b][c] / HW
+        const auto si = shp(pred[p->pred_ptr[u]]);
+        OK_(launch_k(op_pool_bwd_kernel, ew((size_t)B * si[0] * si[1] * wu), eb, 0, st, pdl, dy, B, si[0] * si[1], wu,
+                     V(v)));
+        ++nl;
+        break;
+      }
+      case SLM_OP_CONV: {   // rest = [x]
+        const int xin = rest[0];
+        const ConvGeom g = geom(u, xin);
+        const int K = g.k * g.k * g.Cin, Cout = wu;
+        const int64_t Rin = rows(xin);
+        // bf16 dy and the im2col columns of x (the GEMM operands), db = column sums of dy
+        OK_(launch_k(op_pack_kernel, ew((size_t)Ru * Cout), eb, 0, st, pdl, dy, Ru, Cout, Cout, gq));
+        OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * K / 8), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
+        nl += 2;
+        if ((s = colsum(dy, Ru, Cout, d.db[u])) != SLM_OK) return s;
+        // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows
+        if ((s = kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
+        if ((s = kmap(&mb, gq, Cout, Ru, 64)) != SLM_OK) return s;
+        EpiStoreBF16 e1{(bf*)d.dW[u], K};
+        OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(Cout % 256 == 0 ? 256 : 128, 1, ma, mb, K, Cout, Ru, 0, 0,
+                                                          e1, st, pdl)));
+        // dcol[r][k] = sum_o dy[r][o] W[o][k]: D[m = K][n = r], W MN-major (K = C_out rows)
+        if ((s = kmap(&ma, d.W[u], K, Cout, 64)) != SLM_OK) return s;
+        if ((s = kmap(&mb, gq, Cout, Ru, ntile(Ru))) != SLM_OK) return s;
+        EpiStoreF32 e2{dcol, K};
+        OT_((launch_tc_bn<EpiStoreF32, true, false, true>(ntile(Ru), 1, ma, mb, K, Ru, Cout, 0, 0, e2, st, pdl)));
+        // dx = col2im(dcol) (gather over the taps in order)
+        OK_(launch_k(op_col2im_kernel, ew((size_t)Rin * g.Cin / 4), eb, 0, st, pdl, (const float*)dcol, g,
+                     (size_t)Rin, V(v)));
+        nl += 3;
+        break;
+      }
       case SLM_OP_SOFTMAX_CE:   // rest = [x]; dx may alias x
         OK_(launch_k(ce_bwd_kernel<bf>, dim3(B), eb, 0, st, pdl, (const float*)V(rest[0]), labels, width(rest[0]),
                      inv_bg, V(v), (bf*)nullptr));

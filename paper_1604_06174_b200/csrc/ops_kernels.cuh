@@ -181,4 +181,247 @@ __global__ void __launch_bounds__(256) op_pack_kernel(const float* __restrict__ 
     out[i] = __float2bfloat16_rn(x[(i / w) * ld + i % w]);
 }
 
+// ---------------------------------------------------------------- many-row reductions
+// Values of convolutional graphs have rows = B*H*W (NHWC) up to ~10^4-10^5 per channel: the
+// per-channel sums run over row chunks of kRowChunk rows in parallel CTAs (grid (C/32, chunks)),
+// each chunk's partial in a fixed order (8 row groups), then the chunk partials in chunk order.
+// Batch statistics are two-pass (mean, then the centred sum of squares), as bn_stats32.
+constexpr int kRowChunk = 256;
+__device__ __forceinline__ float chunk_colsum(const float* __restrict__ x, int R, int C, int f, int r0, int r1,
+                                              float (*red)[33]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float s = 0.f;
+  if (f < C)
+    for (int r = r0 + w; r < r1; r += 8) s = __fadd_rn(s, x[(size_t)r * C + f]);
+  red[w][lane] = s;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t = __fadd_rn(t, red[i][lane]);
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ float parts_sum(const float* __restrict__ part, int nch, int C, int f) {
+  float t = 0.f;
+  for (int ch = 0; ch < nch; ++ch) t = __fadd_rn(t, part[(size_t)ch * C + f]);
+  return t;
+}
+// part[ch][f] = sum of x[r][f] over the rows of chunk ch
+__global__ void __launch_bounds__(256) op_colpart_kernel(const float* __restrict__ x, int R, int C,
+                                                         float* __restrict__ part) {
+  __shared__ float red[8][33];
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * 32 + (threadIdx.x & 31), ch = blockIdx.y;
+  const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
+  const float t = chunk_colsum(x, R, C, f, r0, r1, red);
+  if (threadIdx.x < 32 && f < C) part[(size_t)ch * C + f] = t;
+}
+// out[f] = sum of the chunk partials in chunk order
+__global__ void __launch_bounds__(256) op_colfin_kernel(const float* __restrict__ part, int nch, int C,
+                                                        float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < C) out[f] = parts_sum(part, nch, C, f);
+}
+// mean and rstd of channel f from the chunk partials (sum, centred squares)
+__device__ __forceinline__ void parts_stats(const float* __restrict__ psum, const float* __restrict__ psq, int nch,
+                                            int R, int C, int f, float& mu, float& rstd) {
+  const float invR = __frcp_rn((float)R);
+  mu = __fmul_rn(parts_sum(psum, nch, C, f), invR);
+  if (psq) rstd = __frsqrt_rn(__fadd_rn(__fmul_rn(parts_sum(psq, nch, C, f), invR), kEps));
+}
+// psq[ch][f] = sum over chunk ch of (x - mu)^2, mu from psum
+__global__ void __launch_bounds__(256) op_bn_sq_kernel(const float* __restrict__ x, int R, int C,
+                                                       const float* __restrict__ psum, float* __restrict__ psq) {
+  __shared__ float red[8][33];
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
+  float mu = 0.f, dummy;
+  if (f < C) parts_stats(psum, nullptr, nch, R, C, f, mu, dummy);
+  float v = 0.f;
+  if (f < C)
+    for (int r = r0 + w; r < r1; r += 8) {
+      const float e = __fsub_rn(x[(size_t)r * C + f], mu);
+      v = __fmaf_rn(e, e, v);
+    }
+  red[w][lane] = v;
+  __syncthreads();
+  if (w != 0 || f >= C) return;
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t = __fadd_rn(t, red[i][lane]);
+  psq[(size_t)ch * C + f] = t;
+}
+// y = gamma xhat + beta over chunk ch (y may alias x)
+__global__ void __launch_bounds__(256) op_bn_apply_kernel(const float* x, int R, int C, const float* __restrict__ psum,
+                                                          const float* __restrict__ psq, const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta, float* y) {
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  if (f >= C) return;
+  const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
+  float mu, rstd;
+  parts_stats(psum, psq, nch, R, C, f, mu, rstd);
+  const float g = gamma[f], bt = beta[f];
+  for (int r = r0 + w; r < r1; r += 8) {
+    const size_t i = (size_t)r * C + f;
+    y[i] = bn_u(bn_xhat(x[i], mu, rstd), g, bt);
+  }
+}
+// backward chunk partials: ps1 = sum dy, ps2 = sum dy xhat
+__global__ void __launch_bounds__(256) op_bn_bpart_kernel(const float* dy, const float* __restrict__ x, int R, int C,
+                                                          const float* __restrict__ psum, const float* __restrict__ psq,
+                                                          float* __restrict__ ps1, float* __restrict__ ps2) {
+  __shared__ float red[8][33];
+  __shared__ float red2[8][33];
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
+  float mu = 0.f, rstd = 0.f, s1 = 0.f, s2 = 0.f;
+  if (f < C) {
+    parts_stats(psum, psq, nch, R, C, f, mu, rstd);
+    for (int r = r0 + w; r < r1; r += 8) {
+      const size_t i = (size_t)r * C + f;
+      const float g = dy[i];
+      s1 = __fadd_rn(s1, g);
+      s2 = __fmaf_rn(g, bn_xhat(x[i], mu, rstd), s2);
+    }
+  }
+  red[w][lane] = s1;
+  red2[w][lane] = s2;
+  __syncthreads();
+  if (w != 0 || f >= C) return;
+  float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    t1 = __fadd_rn(t1, red[i][lane]);
+    t2 = __fadd_rn(t2, red2[i][lane]);
+  }
+  ps1[(size_t)ch * C + f] = t1;
+  ps2[(size_t)ch * C + f] = t2;
+}
+// dx = gamma rstd (dy - mean dy - xhat mean(dy xhat)) over chunk ch (dx may alias dy); chunk 0
+// writes dgamma / dbeta
+__global__ void __launch_bounds__(256) op_bn_bapply_kernel(const float* dy, const float* __restrict__ x, int R, int C,
+                                                           const float* __restrict__ psum, const float* __restrict__ psq,
+                                                           const float* __restrict__ ps1, const float* __restrict__ ps2,
+                                                           const float* __restrict__ gamma, float* dx,
+                                                           float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  pdl_wait();
+  pdl_launch();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  if (f >= C) return;
+  const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
+  float mu, rstd;
+  parts_stats(psum, psq, nch, R, C, f, mu, rstd);
+  const float S1 = parts_sum(ps1, nch, C, f), S2 = parts_sum(ps2, nch, C, f);
+  const float invR = __frcp_rn((float)R);
+  const float m1 = __fmul_rn(S1, invR), m2 = __fmul_rn(S2, invR), k = __fmul_rn(gamma[f], rstd);
+  for (int r = r0 + w; r < r1; r += 8) {
+    const size_t i = (size_t)r * C + f;
+    const float xh = bn_xhat(x[i], mu, rstd);
+    dx[i] = __fmul_rn(k, __fsub_rn(__fsub_rn(dy[i], m1), __fmul_rn(xh, m2)));
+  }
+  if (ch == 0 && w == 0) {
+    dgamma[f] = S2;
+    dbeta[f] = S1;
+  }
+}
+
+// ---------------------------------------------------------------- convolution
+// NHWC fp32 values [B*H*W][C]; "same" padding p = k / 2, stride s; the GEMM's K index of tap (u, v)
+// and channel c is (u k + v) C_in + c (W [C_out][k k C_in]).
+struct ConvGeom {
+  int H, W, Cin, k, s, Ho, Wo;
+};
+// col[r][K] (bf16, r = (b, i, j) output position) = x at the tap's input position, 0 in the padding;
+// 8 consecutive K columns (one tap, C_in % 8 == 0) per thread: two float4 loads, one 16-byte store
+__global__ void __launch_bounds__(256) op_im2col_kernel(const float* __restrict__ x, ConvGeom g, size_t R,
+                                                        __nv_bfloat16* __restrict__ col) {
+  pdl_wait();
+  pdl_launch();
+  const int K = g.k * g.k * g.Cin, K8 = K / 8, p = g.k / 2;
+  const size_t n = R * (size_t)K8;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / K8;
+    const int q = (int)(i % K8) * 8, tap = q / g.Cin, c = q % g.Cin, u = tap / g.k, v = tap % g.k;
+    const int hw = g.Ho * g.Wo, b = (int)(r / hw), rem = (int)(r % hw), oi = rem / g.Wo, oj = rem % g.Wo;
+    const int h = oi * g.s + u - p, w = oj * g.s + v - p;
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
+      const float4* src = reinterpret_cast<const float4*>(x + ((size_t)(b * g.H + h) * g.W + w) * g.Cin + c);
+      const float4 a = src[0], e = src[1];
+      __nv_bfloat162 t0 = __floats2bfloat162_rn(a.x, a.y), t1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(e.x, e.y), t3 = __floats2bfloat162_rn(e.z, e.w);
+      o = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                     *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+    }
+    reinterpret_cast<uint4*>(col)[i] = o;
+  }
+}
+// dx[b][h][w][c] = sum over the taps (u, v) in order whose output position reads x[b][h][w] of
+// dcol[(b, i, j)][(u k + v) C_in + c]: the gather form of col2im (no atomics; fixed order)
+__global__ void __launch_bounds__(256) op_col2im_kernel(const float* __restrict__ dcol, ConvGeom g, size_t Rin,
+                                                        float* __restrict__ dx) {
+  pdl_wait();
+  pdl_launch();
+  const int K = g.k * g.k * g.Cin, C4 = g.Cin / 4, p = g.k / 2;
+  const size_t n = Rin * (size_t)C4;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / C4;
+    const int c = (int)(i % C4) * 4;
+    const int hw = g.H * g.W, b = (int)(r / hw), rem = (int)(r % hw), h = rem / g.W, w = rem % g.W;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < g.k; ++u) {
+      const int ih = h + p - u;
+      if (ih < 0 || ih % g.s) continue;
+      const int oi = ih / g.s;
+      if (oi >= g.Ho) continue;
+      for (int v = 0; v < g.k; ++v) {
+        const int iw = w + p - v;
+        if (iw < 0 || iw % g.s) continue;
+        const int oj = iw / g.s;
+        if (oj >= g.Wo) continue;
+        const float4 d = *reinterpret_cast<const float4*>(dcol + ((size_t)(b * g.Ho + oi) * g.Wo + oj) * K +
+                                                          (u * g.k + v) * g.Cin + c);
+        acc = make_float4(__fadd_rn(acc.x, d.x), __fadd_rn(acc.y, d.y), __fadd_rn(acc.z, d.z), __fadd_rn(acc.w, d.w));
+      }
+    }
+    reinterpret_cast<float4*>(dx)[i] = acc;
+  }
+}
+// global average pool: y[b][c] = (sum over the HW positions in order) / HW; backward dx = dy / HW
+__global__ void __launch_bounds__(256) op_pool_fwd_kernel(const float* __restrict__ x, int B, int HW, int C,
+                                                          float* __restrict__ y) {
+  pdl_wait();
+  pdl_launch();
+  const int n = B * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int b = i / C, c = i % C;
+    float s = 0.f;
+    for (int q = 0; q < HW; ++q) s = __fadd_rn(s, x[((size_t)b * HW + q) * C + c]);
+    y[i] = __fdiv_rn(s, (float)HW);
+  }
+}
+__global__ void __launch_bounds__(256) op_pool_bwd_kernel(const float* __restrict__ dy, int B, int HW, int C,
+                                                          float* __restrict__ dx) {
+  pdl_wait();
+  pdl_launch();
+  const size_t n = (size_t)B * HW * C;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t c = i % C, b = i / ((size_t)HW * C);
+    dx[i] = __fdiv_rn(dy[b * C + c], (float)HW);
+  }
+}
+
 }  // namespace slmk

@@ -44,6 +44,8 @@ static const OpMeta kOps[] = {
     {1, 2, -1, false, 0x3, GI_NONE, false},          // LSTM_CELL
     {1, 1, -1, false, 0x1, GI_NONE, false},          // HEAD_CE
     {1, 1 << 30, -1, false, 0x0, GI_NONE, false},    // SUM
+    {1, 1, -1, false, 0x1, GI_NONE, false},          // CONV        (bwd reads input, as FC)
+    {1, 1, -1, false, 0x0, GI_NONE, false},          // POOL        (bwd needs the shapes only)
 };
 
 const OpMeta* op_meta(int op) {

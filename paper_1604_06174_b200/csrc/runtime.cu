@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <type_traits>
 #include <cstring>
@@ -56,10 +57,21 @@ struct Nccl {
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
+  int (*GetVersion)(int*) = nullptr;
+  int version = 0;
+  // SLM_NCCL_LIB (an explicit path) first, else the process's libnccl.so.2 (the one torch loaded,
+  // NCCL 2.28.9 in this image); NCCL >= 2.27 is required (ncclGetVersion)
   bool load() {
     if (h) return true;
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    const char* env = getenv("SLM_NCCL_LIB");
+    h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return false;
+    GetVersion = (decltype(GetVersion))dlsym(h, "ncclGetVersion");
+    if (!GetVersion || GetVersion(&version) != 0 || version < 22700) {
+      dlclose(h);
+      h = nullptr;
+      return false;
+    }
     GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
     CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
     AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
@@ -193,16 +205,49 @@ slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model
   slm_ops_model& o = m->od;
   o.batch = d.batch;
   o.batch_global = d.batch_global;
+  auto bad = [&](int v, const std::string& why) {
+    set_error("slm_model_ops: node " + std::to_string(v) + ": " + why);
+    return SLM_E_UNSUPPORTED;
+  };
   for (int v = 0; v < n; ++v) {
     const slm::Node& nd = g->nodes[v];
-    if (!ops_supported(nd.op)) {
-      set_error("slm_model_ops: node " + std::to_string(v) + ": unsupported op " + std::to_string(nd.op));
-      return SLM_E_UNSUPPORTED;
-    }
+    if (!ops_supported(nd.op)) return bad(v, "unsupported op " + std::to_string(nd.op));
     const bool loss = nd.op == SLM_OP_SOFTMAX_CE;
-    if (!loss && (nd.out_bytes % (4 * (int64_t)d.batch) || (nd.out_bytes / (4 * (int64_t)d.batch)) % 128)) {
-      set_error("slm_model_ops: node " + std::to_string(v) + ": width must be a multiple of 128");
-      return SLM_E_UNSUPPORTED;
+    std::array<int, 5> sh{1, 1, 0, 0, 0};
+    if (d.shape) {
+      for (int i = 0; i < 5; ++i) sh[i] = d.shape[5 * v + i];
+      if (sh[0] <= 0 || sh[1] <= 0 || (!loss && sh[2] <= 0)) return bad(v, "bad shape");
+    } else if (!loss) {
+      if (nd.out_bytes % (4 * (int64_t)d.batch)) return bad(v, "out_bytes is not a multiple of 4 batch");
+      sh[2] = (int)(nd.out_bytes / (4 * (int64_t)d.batch));
+    }
+    const int64_t rows = (int64_t)d.batch * sh[0] * sh[1];
+    if (!loss && (sh[2] % 128 || (int64_t)sh[2] * rows * 4 != nd.out_bytes))
+      return bad(v, "width must be a multiple of 128 and out_bytes = 4 batch H W C");
+    const bool has_in = !nd.preds.empty();
+    const std::array<int, 5> in = has_in && d.shape ? std::array<int, 5>{d.shape[5 * nd.preds[0]], d.shape[5 * nd.preds[0] + 1],
+                                                                            d.shape[5 * nd.preds[0] + 2], 0, 0}
+                                                    : std::array<int, 5>{1, 1, 0, 0, 0};
+    if (nd.op == SLM_OP_CONV) {
+      if (!d.shape) return bad(v, "Conv needs shapes");
+      const int k = sh[3], st = sh[4];
+      if (!(k == 1 || k == 3) || !(st == 1 || st == 2)) return bad(v, "Conv k in {1, 3}, stride in {1, 2}");
+      if (sh[0] != (in[0] - 1) / st + 1 || sh[1] != (in[1] - 1) / st + 1 || in[2] % 128)
+        return bad(v, "Conv output size / input channels");
+      if (!d.W[v] || !d.b[v] || !d.dW[v] || !d.db[v]) return bad(v, "Conv without W / b / dW / db");
+      m->od.max_col = std::max(m->od.max_col, rows * (int64_t)k * k * in[2]);
+    }
+    if (nd.op == SLM_OP_POOL && (sh[0] != 1 || sh[1] != 1 || sh[2] != in[2])) return bad(v, "Pool output [batch][C]");
+    if ((nd.op == SLM_OP_FC || nd.op == SLM_OP_SOFTMAX_CE) && (in[0] != 1 || in[1] != 1))
+      return bad(v, "FC / SoftmaxCE need an input with H = W = 1");
+    if ((nd.op == SLM_OP_ADD) && d.shape &&
+        (d.shape[5 * nd.preds[1]] != in[0] || d.shape[5 * nd.preds[1] + 1] != in[1] || d.shape[5 * nd.preds[1] + 2] != in[2]))
+      return bad(v, "Add of different shapes");
+    m->od.rows.push_back(rows);
+    m->od.shape.push_back(sh);
+    if (!loss) {
+      m->od.max_elems = std::max(m->od.max_elems, rows * sh[2]);
+      m->od.max_parts = std::max(m->od.max_parts, ((rows + slmk::kRowChunk - 1) / slmk::kRowChunk) * sh[2]);
     }
     if (loss && nd.out_bytes != 4) {
       set_error("slm_model_ops: the SoftmaxCE node's output is the 4-byte loss");
@@ -226,7 +271,7 @@ slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model
     o.dbeta.push_back(d.dbeta[v]);
     o.op.push_back(nd.op);
     o.out_bytes.push_back(nd.out_bytes);
-    if (!loss) m->ops_maxw = std::max(m->ops_maxw, (int)(nd.out_bytes / (4 * (int64_t)d.batch)));
+    if (!loss) m->ops_maxw = std::max(m->ops_maxw, sh[2]);
   }
   *out = m.release();
   return SLM_OK;
@@ -511,7 +556,7 @@ slm_status slm_step_host(const slm_plan* p, slm_model* m, const float* x0_host, 
 slm_status slm_comm_unique_id(void* id128) {
   if (!id128) return SLM_E_ARG;
   if (!g_nccl.load()) {
-    set_error("libnccl.so.2 not loadable");
+    set_error("libnccl.so.2 (or SLM_NCCL_LIB) not loadable or older than NCCL 2.27");
     return SLM_E_NCCL;
   }
   nccl_uid u;
@@ -530,7 +575,7 @@ slm_status slm_comm_init(int32_t rank, int32_t world, const void* id128, int64_t
   }
   *out = nullptr;
   if (!g_nccl.load()) {
-    set_error("libnccl.so.2 not loadable");
+    set_error("libnccl.so.2 (or SLM_NCCL_LIB) not loadable or older than NCCL 2.27");
     return SLM_E_NCCL;
   }
   auto* c = new slm_comm();

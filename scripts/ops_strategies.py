@@ -17,9 +17,15 @@ depths = [int(x) for x in os.environ.get("DEPTHS", "16,16,16").split(",")]
 widths = [int(x) for x in os.environ.get("WIDTHS", "512,1024,2048").split(",")]
 B = int(os.environ.get("B", 256))
 steps = int(os.environ.get("STEPS", 10))
+CONV = int(os.environ.get("CONV", 0))   # 1: the convolutional ResNet of SURVEY 8(f) f4 (HW, DEPTHS, WIDTHS)
+HW = int(os.environ.get("HW", 32))
 dev = torch.device("cuda", 0)
-nodes = slm.OpsModel.preact_nodes(depths, widths, B)
-inp = synth.opgraph_inputs(nodes, B, seed=11)
+shapes = None
+if CONV:
+    nodes, shapes = slm.OpsModel.preact_conv_nodes(B, HW, list(zip(widths, depths)), 128)
+else:
+    nodes = slm.OpsModel.preact_nodes(depths, widths, B)
+inp = synth.opgraph_inputs(nodes, B, seed=11, shapes=shapes)
 params, grads = {}, {}
 for v, pv in inp["params"].items():
     params[v] = {k: torch.tensor(a, device=dev, dtype=torch.bfloat16 if k == "W" else torch.float32) for k, a in pv.items()}
@@ -27,11 +33,12 @@ for v, pv in inp["params"].items():
 x = torch.tensor(inp["x0"], device=dev)
 y = torch.tensor(inp["labels"], device=dev)
 graph = slm.Graph.from_nodes(nodes, [len(nodes) - 1])
-model = slm.OpsModel(graph, params, grads, B)
+model = slm.OpsModel(graph, params, grads, B, shapes=shapes)
 # the paper's five strategies (Fig. 5): no optimisation, in-place, sharing, drop bn-relu, sublinear
 strategies = [("no-opt", "none", 0), ("inplace", "none", 1), ("sharing", "none", 3),
               ("drop bn-relu", "drop_cheap", 3), ("sublinear (sqrt)", "sqrt", 3), ("sublinear (search)", "search", 3)]
-out = dict(graph=dict(depths=depths, widths=widths, batch=B, nodes=len(nodes)), strategies={})
+out = dict(graph=dict(depths=depths, widths=widths, batch=B, nodes=len(nodes), conv=CONV, hw=HW if CONV else None),
+           strategies={})
 ref = None
 for name, strat, af in strategies:
     plan = slm.Plan(graph, strat, alloc_flags=af)

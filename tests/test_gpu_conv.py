@@ -1,0 +1,159 @@
+"""GPU convolutional ResNet through the op-granularity executor:
+pre-activation basic blocks with stride-2 stage transitions and 1x1 projection shortcuts, global
+average pool, FC head -- Conv lowered as im2col + tcgen05 GEMM (col2im gather backward), BN over
+all batch*H*W rows of a channel (chunked fixed-order reductions).  Element-wise parity with the
+op-graph oracle (oracle.opgraph, bf16 operand rounding), checkpointed plans (sqrt, drop bn-relu,
+App. A search) bit-identical to the plain step, drop bn-relu below the sharing plan's memory."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import graph as OGR
+from oracle import opgraph as OG
+from _util import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def slm():
+    import paper_1604_06174_b200 as m
+    return m
+
+
+def _setup(slm, B, hw, stages, classes, seed=5):
+    import torch
+    nodes, shapes = slm.OpsModel.preact_conv_nodes(B, hw, stages, classes)
+    inp = synth.opgraph_inputs(nodes, B, seed=seed, shapes=shapes)
+    dev = torch.device("cuda", 0)
+    params, grads = {}, {}
+    for v, pv in inp["params"].items():
+        params[v] = {k: torch.tensor(a, device=dev, dtype=torch.bfloat16 if k == "W" else torch.float32)
+                     for k, a in pv.items()}
+        grads[v] = {k: torch.zeros_like(t) for k, t in params[v].items()}
+    x = torch.tensor(inp["x0"], device=dev)
+    y = torch.tensor(inp["labels"], device=dev)
+    return nodes, shapes, inp, params, grads, x, y
+
+
+def _run(slm, nodes, shapes, params, grads, x, y, B, strategy, af=3):
+    import torch
+    graph = slm.Graph.from_nodes(nodes, [len(nodes) - 1])
+    model = slm.OpsModel(graph, params, grads, B, shapes=shapes)
+    plan = slm.Plan(graph, strategy, alloc_flags=af)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        loss = model.step(plan, x, y, stream=s)
+        loss = model.step(plan, x, y, stream=s)   # CUDA-graph replay
+    torch.cuda.synchronize()
+    g = {(v, k): t.float().cpu().numpy().astype(np.float64) for v, gv in grads.items() for k, t in gv.items()}
+    return float(loss.item()), g, plan, model
+
+
+def _oparams(inp, shapes, og):
+    pr = inp["params"]
+    return OG.OpParams({v: p["W"] for v, p in pr.items() if "W" in p}, {v: p["b"] for v, p in pr.items() if "b" in p},
+                       {v: p["gamma"] for v, p in pr.items() if "gamma" in p},
+                       {v: p["beta"] for v, p in pr.items() if "beta" in p}, shapes=shapes, graph=og)
+
+
+def _small_graph(slm, B, spec):
+    """Input [B, H, H, 128] -> the ops of spec -> Pool -> FC(128) -> SoftmaxCE; spec = list of
+    ("conv", C, k, s) / ("bn",) / ("relu",)."""
+    OP = slm.OP
+    H = spec[0][1] if spec[0][0] == "input" else 8
+    nodes, shapes = [(OP["input"], [], B * H * H * 128 * 4, 0)], [(H, H, 128, 0, 0)]
+    for op in spec[1:]:
+        h, _, c = shapes[-1][:3]
+        if op[0] == "conv":
+            _, c, k, s = op
+            h = (h - 1) // s + 1
+            shapes.append((h, h, c, k, s))
+        else:
+            shapes.append((h, h, c, 0, 0))
+        nodes.append((OP[op[0]], [len(nodes) - 1], B * h * h * c * 4, 0))
+    c = shapes[-1][2]
+    nodes.append((OP["pool"], [len(nodes) - 1], B * c * 4, 0))
+    shapes.append((1, 1, c, 0, 0))
+    nodes.append((OP["fc"], [len(nodes) - 1], B * 128 * 4, 0))
+    shapes.append((1, 1, 128, 0, 0))
+    nodes.append((OP["softmax_ce"], [len(nodes) - 1], 4, 1))
+    shapes.append((1, 1, 1, 0, 0))
+    return nodes, shapes
+
+
+@pytest.mark.parametrize("spec", [
+    [("input", 8), ("conv", 256, 3, 2)],                                    # 3x3 stride 2, channel change
+    [("input", 7), ("conv", 128, 3, 1)],                                    # odd size, ragged rows
+    [("input", 8), ("conv", 256, 1, 2), ("bn",), ("relu",)],                # projection + chunked BN
+    [("input", 6), ("bn",), ("relu",), ("conv", 128, 3, 1), ("conv", 128, 3, 1)],
+])
+def test_conv_ops_vs_oracle_strict(slm, spec):
+    """Single conv / BN stages (little depth for bf16 rounding decisions to amplify): every element
+    within 2e-2 (|ref| + rms(ref)) of the oracle (reading A12), conv bias gradients included."""
+    import torch
+    B = 64
+    nodes, shapes = _small_graph(slm, B, spec)
+    inp = synth.opgraph_inputs(nodes, B, seed=3, shapes=shapes)
+    dev = torch.device("cuda", 0)
+    params = {v: {k: torch.tensor(a, device=dev, dtype=torch.bfloat16 if k == "W" else torch.float32)
+                  for k, a in pv.items()} for v, pv in inp["params"].items()}
+    grads = {v: {k: torch.zeros_like(t) for k, t in pv.items()} for v, pv in params.items()}
+    x, y = torch.tensor(inp["x0"], device=dev), torch.tensor(inp["labels"], device=dev)
+    loss, g, _, _ = _run(slm, nodes, shapes, params, grads, x, y, B, "none")
+    og = OGR.Graph([OGR.Node(o, list(p), ob, f) for o, p, ob, f in nodes], [len(nodes) - 1])
+    ol, ogr = OG.step_plain(og, _oparams(inp, shapes, og), inp["x0"].astype(np.float64), inp["labels"], "bf16")
+    assert abs(loss - ol) <= 2e-2 * abs(ol), (loss, ol)
+    for (v, k), a in g.items():
+        if k == "b" and og.nodes[v].op == OGR.CONV and og.nodes[v + 1].op == OGR.BN:
+            continue   # identically zero (reading A26); checked in the ResNet test
+        assert_close(a, ogr[k][v], 2e-2, f"node {v} d{k}")
+
+
+@pytest.mark.parametrize("B,hw,stages", [(64, 8, [(128, 1), (256, 1)]), (64, 6, [(128, 2)]), (64, 5, [(128, 1), (256, 1)])])
+def test_conv_resnet_vs_oracle(slm, B, hw, stages):
+    """Whole ResNet (reading A26): the device is held to the bf16 oracle at the resolution the bf16
+    rounding decisions allow -- per tensor, relative L2 <= max(2e-2, S) and the fraction of elements
+    outside 2e-2 (|ref| + rms(ref)) <= max(1e-2, F), where S and F are how far the ORACLE's own
+    result moves when its input is perturbed by a seeded 1e-6 relative (the fp32-vs-fp64 arithmetic
+    gap); conv biases feeding a BN (gradient identically 0) stay below 1e-2 rms(dW)."""
+    classes = 128
+    nodes, shapes, inp, params, grads, x, y = _setup(slm, B, hw, stages, classes)
+    loss, g, _, _ = _run(slm, nodes, shapes, params, grads, x, y, B, "sqrt")
+    og, oshapes = OGR.preact_resnet_conv_graph(B, hw, stages, classes)
+    assert [(nd.op, list(nd.preds), nd.out_bytes) for nd in og.nodes] == [(o, list(p), ob) for o, p, ob, _ in nodes]
+    assert [tuple(s) for s in oshapes] == [tuple(s) for s in shapes]
+    P = _oparams(inp, oshapes, og)
+    x0 = inp["x0"].astype(np.float64)
+    ol, ogr = OG.step_plain(og, P, x0, inp["labels"], "bf16")
+    rng = np.random.default_rng(0)
+    _, opert = OG.step_plain(og, P, x0 * (1 + 1e-6 * rng.standard_normal(x0.shape)), inp["labels"], "bf16")
+    assert abs(loss - ol) <= 2e-2 * abs(ol), (loss, ol)
+
+    def stats(a, r):
+        rms = np.sqrt(np.mean(r * r))
+        return (np.linalg.norm(a - r) / np.linalg.norm(r), float((np.abs(a - r) > 2e-2 * (np.abs(r) + rms)).mean()))
+
+    for (v, k), a in g.items():
+        ref = ogr[k][v]
+        if k == "b" and og.nodes[v].op == OGR.CONV:   # every conv feeds a BN here
+            wrms = np.sqrt(np.mean(ogr["W"][v] ** 2))
+            assert np.abs(a).max() <= 1e-2 * wrms and np.abs(ref).max() <= 1e-2 * wrms, (v, np.abs(a).max(), wrms)
+            continue
+        rel, out = stats(a, ref)
+        s_rel, s_out = stats(opert[k][v], ref)
+        assert rel <= max(2e-2, s_rel) and out <= max(1e-2, s_out), (v, k, rel, s_rel, out, s_out)
+
+
+def test_conv_plans_bitwise_and_drop_saves_memory(slm):
+    B, hw, stages, classes = 64, 8, [(128, 2), (256, 2)], 128
+    nodes, shapes, inp, params, grads, x, y = _setup(slm, B, hw, stages, classes, seed=9)
+    ref_loss, ref, share, _ = _run(slm, nodes, shapes, params, grads, x, y, B, "none")
+    runs = {s: _run(slm, nodes, shapes, params, grads, x, y, B, s) for s in ("sqrt", "drop_cheap", "search")}
+    for s, (loss, g, plan, _) in runs.items():
+        assert loss == ref_loss, s
+        for k in ref:
+            assert np.array_equal(g[k], ref[k]), (s, k)
+    drop = runs["drop_cheap"][2]
+    assert drop.extra_forward > 0
+    assert drop.exact_peak < share.exact_peak

@@ -105,6 +105,10 @@ def test_lstm_graph_plan():
     for strat, fl in ((P.S_NONE, 0), (P.S_NONE, P.A_INPLACE), (P.S_NONE, 3), (P.S_DROP_CHEAP, 3), (P.S_SEARCH, 3),
                       (P.S_SQRT, 3), (P.S_SQRT, 3 | P.A_MIRROR_PARITY)):
         assert_same_plan(rg, strat, alloc_flags=fl)
+    cg, _ = G.preact_resnet_conv_graph(16, 16, [(128, 3), (256, 3), (512, 2)], 128)   # conv ResNet (8(f) f4)
+    for strat, fl in ((P.S_NONE, 0), (P.S_NONE, 3), (P.S_DROP_CHEAP, 3), (P.S_SEARCH, 3), (P.S_SQRT, 3),
+                      (P.S_SQRT, 3 | P.A_MIRROR_PARITY)):
+        assert_same_plan(cg, strat, alloc_flags=fl)
     assert_same_plan(g, P.S_SEARCH, alloc_flags=grouped)
     assert_same_plan(g, P.S_SQRT, alloc_flags=grouped)
     assert_same_plan(G.lstm_graph(4, 64, 64, 1024, 50), P.S_EXPLICIT,
@@ -202,3 +206,13 @@ def test_lstm_state_candidates_search():
             assert all(po.m[v] >= 1 for v, nd in enumerate(go.nodes) if nd.op == G.LSTM_GATES)
     with pytest.raises(RuntimeError):
         cg.mark_not_candidate(999)
+
+
+def test_binding_conv_builder_matches_oracle():
+    """The binding's node list for the conv ResNet is oracle.graph's graph."""
+    for B, hw, stages in ((64, 8, [(128, 1), (256, 2)]), (16, 16, [(128, 3), (256, 3), (512, 2)])):
+        nodes, shapes = slm.OpsModel.preact_conv_nodes(B, hw, stages, 128)
+        og, osh = G.preact_resnet_conv_graph(B, hw, stages, 128)
+        assert [(nd.op, list(nd.preds), nd.out_bytes, nd.flags) for nd in og.nodes] == \
+            [(o, list(p), ob, f) for o, p, ob, f in nodes]
+        assert [tuple(s) for s in osh] == [tuple(s) for s in shapes]
