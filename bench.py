@@ -494,7 +494,7 @@ def main():
                     help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
     ap.add_argument("--lstm-strategy", default="segments",
                     help="LSTM plan: segments (time segments of --seg steps) or a planner strategy (search, sqrt, ...)")
-    ap.add_argument("--lstm-parity", type=int, default=1,
+    ap.add_argument("--lstm-parity", type=int, default=0,
                     help="LSTM plan with SLM_ALLOC_MIRROR_PARITY (with --opt lstm_streams=2: recompute on its own streams)")
     ap.add_argument("--opt", action="append", default=[], help="model option key=value (slm_model_set_option)")
     ap.add_argument("--model", default="chain", choices=["chain", "lstm"],

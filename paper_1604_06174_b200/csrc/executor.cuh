@@ -305,7 +305,10 @@ struct slm_lstm_state {
 // dW ring (fused lowering): the dW GEMM of backward k reads ab[k % kNA] and gq[k % kNG]; the
 // gradient Block of backward k overwrites gq[(k+1) % kNG] and ab[k % kNA], so it waits for dW of
 // backward k - kNA: kNA layers of slack between the dX chain and the dW stream
-constexpr int kNA = 2, kNG = kNA + 1;
+#ifndef SLM_KNA
+#define SLM_KNA 2
+#endif
+constexpr int kNA = SLM_KNA, kNG = kNA + 1;
 
 // op-granularity model (executor_ops.cuh): per forward node parameters, the graph it was built for
 struct slm_ops_model {

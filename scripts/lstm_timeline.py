@@ -15,7 +15,11 @@ L, T, B, H, I, Cn = 4, int(os.environ.get("T", 1024)), 64, 1024, 50, 5000
 dev = torch.device("cuda", 0)
 p, g, x, y = bench.lstm_inputs_dev(L, T, B, H, I, Cn, dev)
 graph = slm.Graph.lstm(L, T, B, H, I)
-plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(int(os.environ.get("SEG", 32))), alloc_flags=int(os.environ.get("AF", 7)))
+if os.environ.get("PLAN") == "none":
+    plan = slm.Plan(graph, "none", alloc_flags=int(os.environ.get("AF", 7)))
+else:
+    plan = slm.Plan(graph, "explicit", m=graph.lstm_segment_mirrors(int(os.environ.get("SEG", 32))),
+                    alloc_flags=int(os.environ.get("AF", 7)))
 opts = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[1:])}
 model = slm.LstmModel(p, g, L, T, B, H, I, Cn, **opts)
 ngemm = 4 * T * (L + 2) + 64
