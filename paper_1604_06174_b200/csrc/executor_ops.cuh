@@ -289,12 +289,25 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * K / 8), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
         nl += 2;
         if ((s = colsum(dy, Ru, Cout, d.db[u])) != SLM_OK) return s;
-        // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows
+        // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows.
+        // Few output tiles and a long K (batch H W): split K over ~one wave of CTAs, fp32 partials in
+        // the dcol workspace (not yet in use), summed in split order into the bf16 dW
         if ((s = kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
         if ((s = kmap(&mb, gq, Cout, Ru, 64)) != SLM_OK) return s;
-        EpiStoreBF16 e1{(bf*)d.dW[u], K};
-        OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(Cout % 256 == 0 ? 256 : 128, 1, ma, mb, K, Cout, Ru, 0, 0,
-                                                          e1, st, pdl)));
+        const int bnw = Cout % 256 == 0 ? 256 : 128;
+        const int tiles = (K / 128) * (Cout / bnw);
+        int split = 1;
+        while (split * 2 * tiles <= 148 && Ru % (64 * split * 2) == 0 && (int64_t)split * 2 * Cout <= Ru) split *= 2;
+        if (split == 1) {
+          EpiStoreBF16 e1{(bf*)d.dW[u], K};
+          OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(bnw, 1, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl)));
+        } else {
+          EpiPartial e1{dcol, (long)K, (long)K * Cout};
+          OT_((launch_tc_bn<EpiPartial, true, true, false>(bnw, split, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl)));
+          OK_(launch_k(op_splitk_bf16_kernel, ew((size_t)K * Cout), eb, 0, st, pdl, (const float*)dcol, split,
+                       (size_t)K * Cout, (bf*)d.dW[u]));
+          ++nl;
+        }
         // dcol[r][k] = sum_o dy[r][o] W[o][k]: D[m = K][n = r], W MN-major (K = C_out rows)
         if ((s = kmap(&ma, d.W[u], K, Cout, 64)) != SLM_OK) return s;
         if ((s = kmap(&mb, gq, Cout, Ru, ntile(Ru))) != SLM_OK) return s;

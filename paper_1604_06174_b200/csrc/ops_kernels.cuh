@@ -400,6 +400,17 @@ __global__ void __launch_bounds__(256) op_col2im_kernel(const float* __restrict_
     reinterpret_cast<float4*>(dx)[i] = acc;
   }
 }
+// split-K partial sums -> bf16: out[i] = bf16(sum_{ks < split} P[ks * n + i]) in ks order
+__global__ void __launch_bounds__(256) op_splitk_bf16_kernel(const float* __restrict__ P, int split, size_t n,
+                                                             __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float v = P[i];
+    for (int ks = 1; ks < split; ++ks) v = __fadd_rn(v, P[(size_t)ks * n + i]);
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
 // global average pool: y[b][c] = (sum over the HW positions in order) / HW; backward dx = dy / HW
 __global__ void __launch_bounds__(256) op_pool_fwd_kernel(const float* __restrict__ x, int B, int HW, int C,
                                                           float* __restrict__ y) {
