@@ -306,7 +306,6 @@ void slm_model_destroy(slm_model* m);
  *   overlap         1 (default) = chain: each segment's recompute on its own stream, concurrent
  *                   with the backward of the next segment, when the plan makes that sound
  *                   (SLM_ALLOC_MIRROR_PARITY plans); other plans run sequentially
- *   dw_stream       1 (default) = chain weight-gradient GEMMs on a second stream
  *   pdl             1 (default) = programmatic dependent launch between the step's kernels
  *   poison          debug: 1 = fill a pool tag with NaN once its value is dead (forces the
  *                   sequential schedule); a plan that clobbers a live value then yields NaN
@@ -315,8 +314,6 @@ void slm_model_destroy(slm_model* m);
  *                   2 (default) = plus one stream per layer for re-computed (mirror) units, so
  *                   with a SLM_ALLOC_MIRROR_PARITY plan the recompute of a time segment runs
  *                   concurrently with the backward of the next one
- *   lstm_sk         split-K of the LSTM gates GEMMs (default 1, 0 = one wave of CTAs)
- *   lstm_skx        split-K of the LSTM dX GEMMs (default 4, 0 = one wave of CTAs)
  *   lstm_fuse_runs  1 (default) = LSTM forward / recompute phases as persistent chunk x layer
  *                   runs (lstm_run.cuh); 0 = node by node in V' order
  *   profile_events  1 = record a CUDA event pair around every kernel of the step, by kind

@@ -336,7 +336,7 @@ struct slm_model {
   int gemm_impl = 0;      // 0 tcgen05 (bf16), 1 SIMT
   int pdl = 1;            // programmatic dependent launch between the step's kernels
   int fused = 1;          // fused lowering (one Block kernel per node, blk_fused.cuh)
-  int dw_stream = 1;      // dW GEMMs on a second stream
+  int dw_stream = 1;      // dW GEMMs on a second stream (fixed; measured: serial dW 41 vs 27.9 ms/step)
   int bn_fwd = 64, bn_dx = 64, bn_dw = 256;   // N tiles of the basic lowering's GEMMs (bn_dw: also the fused dW)
   int poison = 0;         // debug: fill a pool tag with NaN once its value is dead (sequential schedule)
   int block_cfg = 0;      // fused Block shape (blk_shape: 0 default, 1..4 explicit (BM, S))

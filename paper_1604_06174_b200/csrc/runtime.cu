@@ -318,11 +318,8 @@ slm_status slm_model_set_option(slm_model* m, const char* key, int64_t value) {
   else if (k == "overlap") m->overlap = (int)value;
   else if (k == "block_cfg") m->block_cfg = (int)value;
   else if (k == "poison") m->poison = (int)value;
-  else if (k == "dw_stream") m->dw_stream = (int)value;
   else if (k == "pdl") m->pdl = (int)value;
   else if (k == "lstm_streams") m->lstm_streams = (int)value;
-  else if (k == "lstm_sk") m->lstm_sk = (int)value;
-  else if (k == "lstm_skx") m->lstm_skx = (int)value;
   else if (k == "lstm_fuse_runs") m->lstm_fuse_runs = (int)value;
   else if (k == "lstm_run_ts") m->lstm_run_ts = reinterpret_cast<void*>(value);
   else if (k == "lstm_run_ts_n") m->lstm_run_ts_n = (int)value;
