@@ -41,9 +41,14 @@ namespace {
 
 constexpr int kLstmChunk = 32;   // time steps per weight-gradient GEMM
 
+// split-K of a backward run's input-gradient GEMM d x = d_pre W_ih (M = H, N = 8 B, K = 4 H): without
+// it 16 CTAs each run the whole K = 4H (35 us per run at C3); four K slices give 64 CTAs whose
+// fp32 partials are summed in slice order (deterministic, the same in every plan)
+constexpr int kDxSplit = 4;
 struct LstmWs {
   size_t logits, dlog_f, rowloss, offs, cnt, hopR, dlR, logitsF, rowlossF, dhR, PH, bar, total;
   std::vector<size_t> P;                     // split-K partials, one buffer per stream (layers, head)
+  std::vector<size_t> pdx;                   // per layer: split-K partials of the runs' input gradient
   std::vector<size_t> opR, dpR, dpF, PX;     // per layer: backward rings, dX partials
   // per lane (layer l, kind k: lane l + L k) of the forward runs: recurrent state hx [2][B][H]
   // bf16 and c [B][H] fp32, the chunk ring [2][CH B][H] bf16 of h, the packed input-projection
@@ -135,6 +140,8 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
       L.dcst.push_back(off); off += al(B * H * 4);
       L.xch.push_back(off);  off += al((H / 128) * 16 * B * 32 * 4);
       L.dxa.push_back(off);  off += 2 * al((CH * B + 256) * H * 4);
+      // split-K partials of the run's input-gradient GEMM (kDxSplit x [run rows padded to 256][H])
+      L.pdx.push_back(off);  off += al((size_t)kDxSplit * ((slmk::kRunMax * B + 255) / 256 * 256) * H * 4);
     }
   const size_t RM = slmk::kRunMax;
   for (int ln = 0; ln < 2 * d.n_layers; ++ln) {
@@ -966,10 +973,20 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         ++nl;
         if (l > 0) {   // d x_t (the h of layer l-1) = d_pre W_ih over the run's ring rows (N padded to 256)
           const int npad = (n * B + 255) / 256 * 256;
-          EpiStoreF32Lim e{dxa_ptr(l - 1, t0), H, n * B};
-          LT((launch_tc_bn<EpiStoreF32Lim, true, false, true>(256, 1, M.wMN[l], M.dpR256[l], H, npad, 4 * H, 0,
-                                                              slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
-          ++nl;
+          if ((4 * H) % (64 * kDxSplit) == 0 && npad <= (slmk::kRunMax * B + 255) / 256 * 256) {
+            float* pdx = (float*)(w + W.pdx[l]);
+            slmk::EpiPartial e{pdx, (long)H, (long)npad * H};
+            LT((launch_tc_bn<slmk::EpiPartial, true, false, true>(256, kDxSplit, M.wMN[l], M.dpR256[l], H, npad, 4 * H,
+                                                                  0, slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
+            LK(launch_k(splitk_sum_kernel, gsz((size_t)n * B * H / 4), eb, 0, cs, pdl, (const float4*)pdx, kDxSplit,
+                        (size_t)npad * H / 4, (size_t)n * B * H / 4, (float4*)dxa_ptr(l - 1, t0)));
+            nl += 2;
+          } else {
+            EpiStoreF32Lim e{dxa_ptr(l - 1, t0), H, n * B};
+            LT((launch_tc_bn<EpiStoreF32Lim, true, false, true>(256, 1, M.wMN[l], M.dpR256[l], H, npad, 4 * H, 0,
+                                                                slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
+            ++nl;
+          }
         }
         if (slot0 == 0) {   // the chunk is complete: dW_l += op^T d_pre over its rows, db_l += column sums
           slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};

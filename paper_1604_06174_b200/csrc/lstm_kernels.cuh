@@ -337,6 +337,20 @@ __global__ void __launch_bounds__(32) lstm_sum_kernel(const float* __restrict__ 
   *out = s;
 }
 
+// split-K partial sums in slice order: out[i] = sum_{ks < split} P[ks * slice + i], i < n (float4)
+__global__ void __launch_bounds__(256) splitk_sum_kernel(const float4* __restrict__ P, int split, size_t slice, size_t n,
+                                                         float4* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float4 v = P[i];
+    for (int ks = 1; ks < split; ++ks) {
+      const float4 q = P[(size_t)ks * slice + i];
+      v = make_float4(__fadd_rn(v.x, q.x), __fadd_rn(v.y, q.y), __fadd_rn(v.z, q.z), __fadd_rn(v.w, q.w));
+    }
+    out[i] = v;
+  }
+}
 __global__ void __launch_bounds__(256) fill_kernel(float* __restrict__ p, int n, float v) {
   lstm_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;

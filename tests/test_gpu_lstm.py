@@ -145,8 +145,9 @@ def test_lstm_launch_count(slm):
     # backward: fill 1; the head gradients batched per 32-step chunk (pack, logits GEMM, CE,
     # dh GEMM, dh + db_o, dW_o GEMM); per t and layer 2 (fused cell / d_pre / pack, dX GEMM whose
     # partials the next cell gradients read in place); per chunk one weight-gradient GEMM + db
-    # column sum per layer (T = 4: one chunk)
-    assert model.launches(plan) == 2 * L + 1 + 3 + 1 + 1 + 6 + (1 + 4) * (L - 1) + (1 + 3)
+    # column sum per layer (T = 4: one chunk); the input gradient of a layer above 0 is a split-K
+    # GEMM plus the slice-order sum of its partials (executor_lstm.cuh kDxSplit)
+    assert model.launches(plan) == 2 * L + 1 + 3 + 1 + 1 + 6 + (1 + 5) * (L - 1) + (1 + 3)
 
 
 @pytest.mark.parametrize("cfg", [(1, 1, 64, 128, 50, 129), (1, 2, 256, 128, 7, 128), (2, 33, 64, 128, 50, 200)])
