@@ -283,6 +283,9 @@ struct LstmMaps {
   std::vector<CUtensorMap> hxM, xpM, ringM[2], xopM[2];
   // backward runs: the d_pre ring as a 256-row B operand, the d_pre exchange (box 64 x B)
   std::vector<CUtensorMap> dpR256, dpxM;
+  // the second (odd-chunk) half of the backward rings when the weight gradients run on their own
+  // stream (executor_lstm.cuh: chunk-parity double buffering)
+  std::vector<CUtensorMap> opRMN1, dpRMN1, dpR2561;
   const void* ws = nullptr;
 };
 struct slm_lstm_state {

@@ -152,13 +152,16 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
     L.xop.push_back(off);  off += al(RM * B * kin * 2);
     L.xp.push_back(off);   off += al(RM * B * 4 * H * 4);
   }
+  // backward rings of one chunk; with backward runs two of them (chunk parity), so the chunk's
+  // weight-gradient GEMM can run on its own stream while the next chunk's runs fill the other
+  const size_t nring = lstm_bwd_runs(d) ? 2 : 1;
   for (int l = 0; l < d.n_layers; ++l) {
     L.opR.push_back(off);
-    off += al(CH * B * lstm_K(d, l) * 2);
+    off += nring * al(CH * B * lstm_K(d, l) * 2);
     L.dpR.push_back(off);
-    off += al(CH * B * 4 * H * 2);
+    off += nring * al(CH * B * 4 * H * 2);
     L.dpF.push_back(off);
-    off += al(CH * B * 4 * H * 4);
+    off += nring * al(CH * B * 4 * H * 4);
     L.PX.push_back(off);   // dX partials [sk][B][K_l], double-buffered by time parity
     off += 2 * al((size_t)(l == 0 ? sp.x0 : sp.x1) * B * lstm_K(d, l) * 4);
   }
@@ -186,6 +189,9 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   M.dpRK.resize(nl);
   M.dpRMN.resize(nl);
   M.dpR256.resize(nl);
+  M.opRMN1.resize(nl);
+  M.dpRMN1.resize(nl);
+  M.dpR2561.resize(nl);
   M.dpxM.resize(nl);
   M.pX.resize(nl);
   M.pG.resize(nl);
@@ -203,6 +209,12 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
     if ((st = make_map(&M.dpRK[l], w + L.dpR[l], 4 * H, CH * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map(&M.dpRMN[l], w + L.dpR[l], 4 * H, CH * B, 64)) != SLM_OK) return st;
     if ((st = make_map(&M.dpR256[l], w + L.dpR[l], 4 * H, CH * B, 256)) != SLM_OK) return st;
+    if (lstm_bwd_runs(d)) {   // the odd-chunk halves
+      const size_t ob = (CH * B * K * 2 + 255) / 256 * 256, db = (CH * B * 4 * H * 2 + 255) / 256 * 256;
+      if ((st = make_map(&M.opRMN1[l], w + L.opR[l] + ob, K, CH * B, 64)) != SLM_OK) return st;
+      if ((st = make_map(&M.dpRMN1[l], w + L.dpR[l] + db, 4 * H, CH * B, 64)) != SLM_OK) return st;
+      if ((st = make_map(&M.dpR2561[l], w + L.dpR[l] + db, 4 * H, CH * B, 256)) != SLM_OK) return st;
+    }
     if (lstm_bwd_runs(d) && (st = make_map(&M.dpxM[l], w + L.dpx[l], 4 * H, 2 * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map_f32(&M.pX[l], w + L.P[l], K, (uint64_t)(l == 0 ? sp.x0 : sp.x1) * B)) != SLM_OK) return st;
     for (int par = 0; par < 2; ++par) {
@@ -697,7 +709,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   const bool msm = m.lstm_streams != 0 && (st != nullptr || dry);
   // lstm_streams = 2: re-computed (mirror) units get streams of their own (L+1+l), so the
   // recompute of segment j-1 can overlap the backward of segment j
-  const int NSTR = m.lstm_streams >= 2 ? 2 * L + 1 : L + 1;
+  // + one stream for the weight-gradient GEMMs of the backward runs (WST)
+  const int WST = m.lstm_streams >= 2 ? 2 * L + 1 : L + 1;
+  const int NSTR = WST + 1;
   constexpr int kRing = 16384;
   const int ntag = (int)p->tag_size.size();
   auto DHR = [&](int par) { return ntag + par; };                       // batched (dh | 0) ring, chunk parity
@@ -708,7 +722,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto bk = [&](int t) { return (t / slmk::kRunMax) % NBK; };
   auto RNG = [&](int ln, int t) { return ntag + 2 + 2 * L + NBK * ln + bk(t); };            // forward ring
   auto DXA = [&](int l, int t) { return ntag + 2 + 2 * L + NBK * 2 * L + NBK * l + bk(t); };  // from layer l+1
-  const int HOP = ntag + 2 + 2 * L + 3 * NBK * L;   // the number of resources
+  // the backward rings (op / d_pre) of layer l, chunk parity
+  auto WGR = [&](int l, int par) { return ntag + 2 + 2 * L + 3 * NBK * L + 2 * l + par; };
+  const int HOP = ntag + 2 + 2 * L + 3 * NBK * L + 2 * L;   // the number of resources
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -807,7 +823,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       const bool cell = n > 1 || U.s[0] >= 0;
       // with backward runs, re-computed runs share the layer's stream: at most one persistent
       // kernel per layer stream (<= L H / 32 resident CTAs), so every run's CTAs can be resident
-      const int sid = (k == 1 && NSTR > L + 1 && !bwdr) ? L + 1 + l : l;
+      const int sid = (k == 1 && WST > L + 1 && !bwdr) ? L + 1 + l : l;
       const int Kin = l == 0 ? K0 : H;
       const int sprev = t0 > 0 ? preds_of(U.g[0]).first[1] : -1;
       const int init = sprev < 0 ? 1 : (hx_node[ln] == sprev && cs_node[ln] == sprev ? 0 : 2);
@@ -904,6 +920,10 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       rd.clear();
       wr.clear();
       cudaStream_t cs = st;
+      // chunk-parity halves of the backward rings (op / d_pre bf16 / d_pre fp32)
+      const size_t ob = ((size_t)CH * B * K * 2 + 255) / 256 * 256;
+      const size_t db2 = ((size_t)CH * B * 4 * H * 2 + 255) / 256 * 256;
+      const size_t df4 = ((size_t)CH * B * 4 * H * 4 + 255) / 256 * 256;
       if (U.type == 2) {
         const int t1 = U.t0;
         BwdRun a{};
@@ -937,11 +957,12 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           rd.push_back(p->node_tag[actn]);
           if (spn >= 0) rd.push_back(p->node_tag[spn]);
           a.dh_in[i] = l == L - 1 ? dh_ring(t) : dxa_ptr(l, t);
-          const int slot = t % CH;
-          a.dpr[i] = (bf*)(w + W.dpR[l]) + (size_t)slot * B * 4 * H;
-          a.dpf[i] = (float*)(w + W.dpF[l]) + (size_t)slot * B * 4 * H;
+          const int slot = t % CH, cp = (t / CH) % 2;
+          a.dpr[i] = (bf*)(w + W.dpR[l] + cp * db2) + (size_t)slot * B * 4 * H;
+          a.dpf[i] = (float*)(w + W.dpF[l] + cp * df4) + (size_t)slot * B * 4 * H;
         }
         for (int t = t1 - n + 1; t <= t1; ++t) rd.push_back(l == L - 1 ? DHR((t / CH) % 2) : DXA(l, t));
+        wr.push_back(WGR(l, (t1 / CH) % 2));
         if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
         m.ts_cur_aux = sid * 4 + 2;
         bbar_val[l] += (unsigned)(H / 32) * (unsigned)(n + 1);
@@ -964,38 +985,56 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
           rd.push_back(p->node_tag[xn]);
           if (hn >= 0) rd.push_back(p->node_tag[hn]);
         }
+        const int cp = (t0 / CH) % 2;
         if (l > 0)
           for (int t = t0; t < t0 + n; ++t) wr.push_back(DXA(l - 1, t));
+        wr.push_back(WGR(l, cp));
         if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
         m.ts_cur_aux = sid * 4 + 2;
         LK(launch_k(lstm_oppack_kernel, gsz((size_t)n * B * K), eb, 0, cs, pdl, xsp, hsp, n, B, l == 0 ? I : H,
-                    l == 0 ? I : 2 * H, Kin, H, (bf*)(w + W.opR[l]) + (size_t)slot0 * B * K));
+                    l == 0 ? I : 2 * H, Kin, H, (bf*)(w + W.opR[l] + cp * ob) + (size_t)slot0 * B * K));
         ++nl;
         if (l > 0) {   // d x_t (the h of layer l-1) = d_pre W_ih over the run's ring rows (N padded to 256)
           const int npad = (n * B + 255) / 256 * 256;
           if ((4 * H) % (64 * kDxSplit) == 0 && npad <= (slmk::kRunMax * B + 255) / 256 * 256) {
             float* pdx = (float*)(w + W.pdx[l]);
             slmk::EpiPartial e{pdx, (long)H, (long)npad * H};
-            LT((launch_tc_bn<slmk::EpiPartial, true, false, true>(256, kDxSplit, M.wMN[l], M.dpR256[l], H, npad, 4 * H,
+            LT((launch_tc_bn<slmk::EpiPartial, true, false, true>(256, kDxSplit, M.wMN[l], cp ? M.dpR2561[l] : M.dpR256[l], H, npad, 4 * H,
                                                                   0, slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
             LK(launch_k(splitk_sum_kernel, gsz((size_t)n * B * H / 4), eb, 0, cs, pdl, (const float4*)pdx, kDxSplit,
                         (size_t)npad * H / 4, (size_t)n * B * H / 4, (float4*)dxa_ptr(l - 1, t0)));
             nl += 2;
           } else {
             EpiStoreF32Lim e{dxa_ptr(l - 1, t0), H, n * B};
-            LT((launch_tc_bn<EpiStoreF32Lim, true, false, true>(256, 1, M.wMN[l], M.dpR256[l], H, npad, 4 * H, 0,
-                                                                slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
+            LT((launch_tc_bn<EpiStoreF32Lim, true, false, true>(256, 1, M.wMN[l], cp ? M.dpR2561[l] : M.dpR256[l], H, npad,
+                                                                4 * H, 0, slot0 * B, e, cs, pdl, gdbg(SLM_K_GEMM_DX))));
             ++nl;
           }
         }
         if (slot0 == 0) {   // the chunk is complete: dW_l += op^T d_pre over its rows, db_l += column sums
+          // as a unit of its own on the weight-gradient stream (it reads the chunk's ring half; the
+          // runs of the chunk after next, which refill that half, wait for it), in issue order, so
+          // every layer's chunks still accumulate in descending time (reading A23)
+          cudaStream_t ws_ = cs;
+          if (msm) {
+            if ((s = unit_end(sid)) != SLM_OK) return s;
+            rd.clear();
+            wr.clear();
+            rd.push_back(WGR(l, cp));
+            if ((s = unit_begin(WST, &ws_)) != SLM_OK) return s;
+          }
           slmk::EpiAccF32 e2{d.dW + lstm_w_offset(d, l), K};
-          LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1, M.opRMN[l], M.dpRMN[l], K,
-                                                               4 * H, chunk_rows(t0), 0, 0, e2, cs, pdl,
-                                                               gdbg(SLM_K_GEMM_DW))));
-          LK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, cs, pdl, (const float*)(w + W.dpF[l]),
-                      chunk_rows(t0), 4 * H, d.db + (size_t)l * 4 * H));
+          LT((launch_tc_bn<slmk::EpiAccF32, true, true, false>((4 * H) % 256 ? 128 : 256, 1,
+                                                               cp ? M.opRMN1[l] : M.opRMN[l],
+                                                               cp ? M.dpRMN1[l] : M.dpRMN[l], K, 4 * H, chunk_rows(t0), 0,
+                                                               0, e2, ws_, pdl && !msm, gdbg(SLM_K_GEMM_DW))));
+          LK(launch_k(colsum_acc_kernel, dim3(4 * H / 32), dim3(512), 0, ws_, pdl && !msm,
+                      (const float*)(w + W.dpF[l] + cp * df4), chunk_rows(t0), 4 * H, d.db + (size_t)l * 4 * H));
           nl += 2;
+          if (msm) {
+            if ((s = unit_end(WST)) != SLM_OK) return s;
+            continue;
+          }
         }
       }
       if (msm && (s = unit_end(sid)) != SLM_OK) return s;
@@ -1011,7 +1050,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
     if (opk == SLM_OP_INPUT) continue;
     // ---- the launch unit: this node, plus the next one when the two are fused
     const bool lay = opk == SLM_OP_LSTM_GATES || opk == SLM_OP_LSTM_CELL;
-    const int sid = !lay ? L : (kind == SLM_KIND_MIRROR && NSTR > L + 1 ? L + 1 + l : l);
+    const int sid = !lay ? L : (kind == SLM_KIND_MIRROR && WST > L + 1 ? L + 1 + l : l);
     int partner = -1;
     if (oi + 1 < (int)order.size()) {
       const int u = order[oi + 1];
