@@ -286,6 +286,7 @@ struct LstmMaps {
   // the second (odd-chunk) half of the backward rings when the weight gradients run on their own
   // stream (executor_lstm.cuh: chunk-parity double buffering)
   std::vector<CUtensorMap> opRMN1, dpRMN1, dpR2561;
+  std::vector<CUtensorMap> xpM1;   // the second half of each lane's double-buffered projection X
   const void* ws = nullptr;
 };
 struct slm_lstm_state {

@@ -150,7 +150,7 @@ LstmWs lstm_ws_layout(const slm_lstm_desc& d, int gates_sk = 0, int dx_sk = 0) {
     L.cst.push_back(off);  off += al(B * H * 4);
     L.ring.push_back(off); off += al(2 * CH * B * H * 2);
     L.xop.push_back(off);  off += al(RM * B * kin * 2);
-    L.xp.push_back(off);   off += al(RM * B * 4 * H * 4);
+    L.xp.push_back(off);   off += 2 * al(RM * B * 4 * H * 4);   // double-buffered (run parity)
   }
   // backward rings of one chunk; with backward runs two of them (chunk parity), so the chunk's
   // weight-gradient GEMM can run on its own stream while the next chunk's runs fill the other
@@ -233,6 +233,7 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
   const uint64_t RM = slmk::kRunMax;
   M.hxM.resize(2 * nl);
   M.xpM.resize(2 * nl);
+  M.xpM1.resize(2 * nl);
   for (int bi = 0; bi < 2; ++bi) {
     M.ringM[bi].resize(2 * nl);
     M.xopM[bi].resize(2 * nl);
@@ -241,6 +242,9 @@ slm_status lstm_bind_maps(const slm_lstm_desc& d, LstmMaps& M, void* ws, int gat
     const uint64_t kin = (ln % nl) == 0 ? (uint64_t)lstm_kin0(d.n_in) : H;
     if ((st = make_map(&M.hxM[ln], w + L.hx[ln], H, 2 * B, (uint32_t)B)) != SLM_OK) return st;
     if ((st = make_map_f32_box(&M.xpM[ln], w + L.xp[ln], 4 * H, RM * B, 32, 64)) != SLM_OK) return st;
+    if ((st = make_map_f32_box(&M.xpM1[ln], w + L.xp[ln] + (RM * B * 4 * H * 4 + 255) / 256 * 256, 4 * H, RM * B, 32,
+                               64)) != SLM_OK)
+      return st;
     for (int bi = 0; bi < 2; ++bi) {
       if ((st = make_map(&M.ringM[bi][ln], w + L.ring[ln], H, 2 * CH * B, bi ? 256u : 64u)) != SLM_OK) return st;
       if ((st = make_map(&M.xopM[bi][ln], w + L.xop[ln], kin, RM * B, bi ? 256u : 64u)) != SLM_OK) return st;
@@ -711,7 +715,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   // recompute of segment j-1 can overlap the backward of segment j
   // + one stream for the weight-gradient GEMMs of the backward runs (WST)
   const int WST = m.lstm_streams >= 2 ? 2 * L + 1 : L + 1;
-  const int NSTR = WST + 1;
+  // + one stream per layer for the input projections of the forward / recompute runs (PST + l)
+  const int PST = WST + 1;
+  const int NSTR = PST + L;
   constexpr int kRing = 16384;
   const int ntag = (int)p->tag_size.size();
   auto DHR = [&](int par) { return ntag + par; };                       // batched (dh | 0) ring, chunk parity
@@ -724,7 +730,10 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
   auto DXA = [&](int l, int t) { return ntag + 2 + 2 * L + NBK * 2 * L + NBK * l + bk(t); };  // from layer l+1
   // the backward rings (op / d_pre) of layer l, chunk parity
   auto WGR = [&](int l, int par) { return ntag + 2 + 2 * L + 3 * NBK * L + 2 * l + par; };
-  const int HOP = ntag + 2 + 2 * L + 3 * NBK * L + 2 * L;   // the number of resources
+  // the projection X of lane ln, run parity
+  auto XPR = [&](int ln, int par) { return ntag + 2 + 2 * L + 3 * NBK * L + 2 * L + 2 * ln + par; };
+  const int HOP = ntag + 2 + 2 * L + 3 * NBK * L + 2 * L + 4 * L;   // the number of resources
+  std::vector<int> xp_cnt(2 * L, 0);   // runs issued per lane (parity of the X half)
   std::vector<int> rd, wr;
   // dependencies are unit ids u = seq * NSTR + stream (seq = per-stream unit counter)
   std::vector<long> res_w, res_r;   // [resource] last writer unit; [resource][stream] latest reader
@@ -831,21 +840,18 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       bool xring = l > 0;
       for (int i = 0; i < n && xring; ++i)
         xring = ring_node[(size_t)lane_of(l - 1, k) * 2 * CH + rslot(t0 + i)] == preds_of(U.g[i]).first[0];
+      // unit 1: the input projection into the lane's X half (its own stream per layer, so it runs
+      // while the layer's previous run is still stepping); unit 2: the run
+      const int xpar = xp_cnt[ln]++ % 2;
       rd.clear();
       wr.clear();
-      if (init == 2) rd.push_back(p->node_tag[sprev]);
       if (l > 0 && xring)
         for (int i = 0; i < n; ++i) rd.push_back(RNG(lane_of(l - 1, k), t0 + i));
       if (l > 0 && !xring)
         for (int i = 0; i < n; ++i) rd.push_back(p->node_tag[preds_of(U.g[i]).first[0]]);
-      for (int i = 0; i < n; ++i) {
-        if (sched.mat[U.g[i]]) wr.push_back(p->node_tag[U.g[i]]);
-        if (U.s[i] >= 0 && sched.mat[U.s[i]]) wr.push_back(p->node_tag[U.s[i]]);
-      }
-      if (cell)
-        for (int i = 0; i < n; ++i) wr.push_back(RNG(ln, t0 + i));
+      wr.push_back(XPR(ln, xpar));
       cudaStream_t cs = st;
-      if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
+      if (msm && (s = unit_begin(PST + l, &cs)) != SLM_OK) return s;
       m.ts_cur_aux = sid * 4 + k;
       bf* xop = (bf*)(w + W.xop[ln]);
       // the projection always runs with 256-column tiles over n B rows rounded up to 256 (the
@@ -868,10 +874,25 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         LK(launch_k(lstm_hpack_multi_kernel, gsz((size_t)n * B * H), eb, 0, cs, pdl, in, n, H, B, xop));
         ++nl;
       }
-      float* xp = (float*)(w + W.xp[ln]);
+      float* xp = (float*)(w + W.xp[ln] + xpar * (((size_t)slmk::kRunMax * B * 4 * H * 4 + 255) / 256 * 256));
       EpiBiasF32 e{xp, 4 * H, d.b + (size_t)l * 4 * H};
       LT((launch_tc_bn<EpiBiasF32, false, false, true>(bn, 1, M.wK[l], *bmap, 4 * H, npad, Kin, 0, brow, e, cs, pdl,
                                                         gdbg(SLM_K_GEMM_FWD))));
+      if (msm) {
+        if ((s = unit_end(PST + l)) != SLM_OK) return s;
+        rd.clear();
+        wr.clear();
+        if (init == 2) rd.push_back(p->node_tag[sprev]);
+        rd.push_back(XPR(ln, xpar));
+        for (int i = 0; i < n; ++i) {
+          if (sched.mat[U.g[i]]) wr.push_back(p->node_tag[U.g[i]]);
+          if (U.s[i] >= 0 && sched.mat[U.s[i]]) wr.push_back(p->node_tag[U.s[i]]);
+        }
+        if (cell)
+          for (int i = 0; i < n; ++i) wr.push_back(RNG(ln, t0 + i));
+        if ((s = unit_begin(sid, &cs)) != SLM_OK) return s;
+      }
+      const CUtensorMap& xpm = xpar ? M.xpM1[ln] : M.xpM[ln];
       FwdRun a{};
       a.H = H;
       a.n = n;
@@ -896,9 +917,9 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
       }
       bar_val[ln] += (unsigned)(H / 32) * (unsigned)(n + 1);
       switch (B) {
-        case 64: LT((launch_fwd_run<64>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
-        case 128: LT((launch_fwd_run<128>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
-        default: LT((launch_fwd_run<256>(M.wK32[l], M.hxM[ln], M.xpM[ln], a, cs, pdl))); break;
+        case 64: LT((launch_fwd_run<64>(M.wK32[l], M.hxM[ln], xpm, a, cs, pdl))); break;
+        case 128: LT((launch_fwd_run<128>(M.wK32[l], M.hxM[ln], xpm, a, cs, pdl))); break;
+        default: LT((launch_fwd_run<256>(M.wK32[l], M.hxM[ln], xpm, a, cs, pdl))); break;
       }
       nl += 2;
       if (msm && (s = unit_end(sid)) != SLM_OK) return s;
