@@ -1012,7 +1012,7 @@ slm_status enqueue_lstm(const slm_plan* p, slm_model& m, const void* xin, const 
         wr.push_back(WGR(l, cp));
         if (msm && (s = unit_begin(sid, &cs)) != SLM_OK) return s;
         m.ts_cur_aux = sid * 4 + 2;
-        LK(launch_k(lstm_oppack_kernel, gsz((size_t)n * B * K), eb, 0, cs, pdl, xsp, hsp, n, B, l == 0 ? I : H,
+        LK(launch_k(lstm_oppack_kernel, gsz((size_t)n * B * K / 8), eb, 0, cs, pdl, xsp, hsp, n, B, l == 0 ? I : H,
                     l == 0 ? I : 2 * H, Kin, H, (bf*)(w + W.opR[l] + cp * ob) + (size_t)slot0 * B * K));
         ++nl;
         if (l > 0) {   // d x_t (the h of layer l-1) = d_pre W_ih over the run's ring rows (N padded to 256)
