@@ -217,14 +217,40 @@ __global__ void __launch_bounds__(512) lstm_head_bwd_finish_kernel(const float* 
                                                                    int nsteps, float* __restrict__ acc) {
   __shared__ float red[kColGroups][33];
   lstm_entry();
+  // (dh | 0) rows first (the top layer's backward waits for them): the split-K partials summed in
+  // slice order, four columns per thread
+  const int H4 = H / 4;
+  const int slice4 = N * H4;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < slice4; i += gridDim.x * blockDim.x) {
+    const int row = i / H4, j4 = i % H4;
+    float4 a = P4[i];
+    for (int s2 = 1; s2 < sk; ++s2) {
+      const float4 q = P4[(size_t)s2 * slice4 + i];
+      a = make_float4(__fadd_rn(a.x, q.x), __fadd_rn(a.y, q.y), __fadd_rn(a.z, q.z), __fadd_rn(a.w, q.w));
+    }
+    float4* o = reinterpret_cast<float4*>(out + (size_t)row * 2 * H);
+    o[j4] = a;
+    o[H4 + j4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // db_o += the per-step column sums in descending step order; every step's row sums are loaded
+  // up front (independent loads), then reduced over the row groups step by step
   if ((int)blockIdx.x * 32 < Cp) {
     const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
     const int j = blockIdx.x * 32 + c;
-    for (int i = nsteps - 1; i >= 0; --i) {
+    constexpr int kMaxSteps = 32;   // kLstmChunk
+    float sv[kMaxSteps];
+#pragma unroll
+    for (int i = 0; i < kMaxSteps; ++i) {
       float sum = 0.f;
-      if (j < Cp)
+      if (i < nsteps && j < Cp)
         for (int b = rg; b < B; b += kColGroups) sum = __fadd_rn(sum, g[((size_t)i * B + b) * Cp + j]);
-      red[rg][c] = sum;
+      sv[i] = sum;
+    }
+#pragma unroll
+    for (int i = kMaxSteps - 1; i >= 0; --i) {
+      if (i >= nsteps) continue;
+      red[rg][c] = sv[i];
       __syncthreads();
       if (rg == 0 && j < Cp) {
         float t = red[0][c];
@@ -234,14 +260,6 @@ __global__ void __launch_bounds__(512) lstm_head_bwd_finish_kernel(const float* 
       }
       __syncthreads();
     }
-  }
-  const size_t slice = (size_t)N * H;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < slice; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t row = i / H, jj = i % H;
-    float a = P[i];
-    for (int s2 = 1; s2 < sk; ++s2) a = __fadd_rn(a, P[s2 * slice + i]);
-    out[row * 2 * H + jj] = a;
-    out[row * 2 * H + H + jj] = 0.f;
   }
 }
 
