@@ -280,17 +280,48 @@ __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restr
   const size_t slice = (size_t)B * Cp;
   float* lr = logits + (size_t)blockIdx.x * Cp;
   const float* pr = P + (size_t)blockIdx.x * Cp;
+  // a row's logits and exponentials stay in registers (kPer per thread, the same element order as
+  // the strided loops, so the same bits); rows wider than kPer * blockDim fall back to re-reading
+  constexpr int kPer = 8;
+  const bool regs = Cp <= kPer * (int)blockDim.x;
+  float vv[kPer], ev[kPer];
   float mx = -INFINITY;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float acc = pr[c];
-    for (int s = 1; s < sk; ++s) acc = __fadd_rn(acc, pr[s * slice + c]);
-    const float v = __fadd_rn(acc, bo[c]);
-    lr[c] = v;
-    mx = fmaxf(mx, v);
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) vv[k] = ev[k] = 0.f;
+  if (regs) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      if (c < C) {
+        float acc = pr[c];
+        for (int s2 = 1; s2 < sk; ++s2) acc = __fadd_rn(acc, pr[s2 * slice + c]);
+        const float v = __fadd_rn(acc, bo[c]);
+        lr[c] = v;
+        vv[k] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+  } else {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      float acc = pr[c];
+      for (int s2 = 1; s2 < sk; ++s2) acc = __fadd_rn(acc, pr[s2 * slice + c]);
+      const float v = __fadd_rn(acc, bo[c]);
+      lr[c] = v;
+      mx = fmaxf(mx, v);
+    }
   }
   mx = block_reduce_max(mx, sh);   // (block_reduce_* synchronise the block: the row is visible)
   float s = 0.f;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) s = __fadd_rn(s, expf(__fsub_rn(lr[c], mx)));
+  if (regs) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if ((int)threadIdx.x + k * (int)blockDim.x < C) {
+        ev[k] = expf(__fsub_rn(vv[k], mx));
+        s = __fadd_rn(s, ev[k]);
+      }
+  } else {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) s = __fadd_rn(s, expf(__fsub_rn(lr[c], mx)));
+  }
   s = block_reduce_sum(s, sh);
   const int yy = y[blockIdx.x];
   if (rowloss && done) {
@@ -316,6 +347,18 @@ __global__ void __launch_bounds__(1024) lstm_head_ce_kernel(const float* __restr
   if (threadIdx.x == 0 && rowloss) rowloss[blockIdx.x] = __fsub_rn(__fadd_rn(logf(s), mx), lr[yy]);
   if (!dlog) return;
   const float inv = __frcp_rn(s);
+  if (regs) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      if (c >= Cp) continue;
+      float v = 0.f;
+      if (c < C) v = __fmul_rn(__fsub_rn(__fmul_rn(ev[k], inv), c == yy ? 1.f : 0.f), scale);
+      dlog[(size_t)blockIdx.x * Cp + c] = __float2bfloat16_rn(v);
+      dlog_f[(size_t)blockIdx.x * Cp + c] = v;
+    }
+    return;
+  }
   for (int c = threadIdx.x; c < Cp; c += blockDim.x) {
     float v = 0.f;
     if (c < C) v = __fmul_rn(__fsub_rn(__fmul_rn(expf(__fsub_rn(lr[c], mx)), inv), c == yy ? 1.f : 0.f), scale);
