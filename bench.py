@@ -421,6 +421,25 @@ def run_lstm(args):
         torch.distributed.destroy_process_group()
 
 
+def _lstm_subrun():
+    """BASELINE configs[2] (C3 LSTM) measured in the same bench run, in a child process (its own
+    device memory), so the driver's round-end run records both workloads; a summary of its line."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--model", "lstm", "--steps", "3", "--warmup", "3",
+           "--no-baseline"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout.strip().splitlines()
+        d = json.loads(out[-1])
+        keep = ("workload",)
+        return dict(value=d["value"], unit=d["unit"], ms_per_step=d["ms_per_step"],
+                    ckpt_over_nockpt_time=d.get("ckpt_over_nockpt_time"),
+                    nockpt_ms_per_step=(d.get("nockpt") or {}).get("ms_per_step"),
+                    activation_gb=d.get("activation_gb"), roofline_frac=d["roofline"].get("frac"),
+                    e2e=d.get("e2e", {}).get("value"), gpu_launches=d.get("gpu_launches"),
+                    clocks=d.get("clocks"), config={k: d["config"][k] for k in keep})
+    except Exception as exc:   # reported, never fatal for the chain line
+        return dict(error=f"{type(exc).__name__}: {exc}"[:300])
+
+
 def _comm_ceiling(n, d, world, ms, probe):
     """SURVEY 8(e) analysis next to the measurement: per rank n d^2 bf16 weight gradients (plus
     the fp32 b / gamma / beta vectors) are all-reduced per step; a ring moves 2 (p-1)/p of them
@@ -489,6 +508,8 @@ def main():
     ap.add_argument("--ref-layers", type=int, default=16)
     ap.add_argument("--no-baseline", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-nockpt", action="store_true", help="skip the non-checkpointed comparison")
+    ap.add_argument("--no-lstm", action="store_true",
+                    help="chain run: skip the C3 LSTM measurement appended as lstm_c3 (N = 1 only)")
     ap.add_argument("--bn", type=str, default="", help="fwd,dx,dw GEMM N tiles")
     ap.add_argument("--mirror-parity", type=int, default=1,
                     help="chain plan with SLM_ALLOC_MIRROR_PARITY (overlapped recompute; 0 = sequential)")
@@ -796,6 +817,8 @@ def main():
         ckpt_over_nockpt_time=round(ms / nock["ms_per_step"], 4) if nock else None,
         comm=_comm_ceiling(n, d, world, ms, probe),
     )
+    if world == 1 and not args.no_lstm:
+        line["lstm_c3"] = _lstm_subrun()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
