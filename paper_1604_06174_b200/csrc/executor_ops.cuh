@@ -30,7 +30,7 @@ bool ops_supported(int op) {
 // workspace: bf16 GEMM operands (x / im2col columns, dy), the summed upstream gradient, the conv
 // column gradient dcol (fp32), the chunk partials of the many-row reductions, CE row losses
 struct OpsWs {
-  size_t xq, gq, dy, dcol, parts, rowloss, total;
+  size_t xq, gq, dy, dcol, parts, stat, rowloss, total;
 };
 OpsWs ops_ws_layout(const slm_model& m) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -42,6 +42,7 @@ OpsWs ops_ws_layout(const slm_model& m) {
   L.dy = off;      off += al(E * 4);
   L.dcol = off;    off += al(Kc * 4);
   L.parts = off;   off += al((size_t)m.od.max_parts * 4 * 4);
+  L.stat = off;    off += al((size_t)m.ops_maxw * 4 * 4);   // per-channel mean, rstd, S1, S2
   L.rowloss = off; off += al(B * 4);
   L.total = off;
   return L;
@@ -71,6 +72,9 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   float* rowloss = (float*)(w8 + W.rowloss);
   float* dcol = (float*)(w8 + W.dcol);
   float* parts = (float*)(w8 + W.parts);
+  float* stat = (float*)(w8 + W.stat);
+  const int MW = m.ops_maxw;
+  float *smu = stat, *srs = stat + MW, *ss1 = stat + 2 * MW, *ss2 = stat + 3 * MW;
   const size_t PS = (size_t)d.max_parts;   // one partial array: chunks x C floats
   slm_status s = SLM_OK;
   int64_t nl = 0;
@@ -106,8 +110,8 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
       OK_(launch_k(colsum_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, x, (int)R, C, out));
       ++nl;
     } else {
-      OK_(launch_k(op_colpart_kernel, dim3((C + 31) / 32, nchunk(R)), eb, 0, st, pdl, x, (int)R, C, parts));
-      OK_(launch_k(op_colfin_kernel, dim3((C + 255) / 256), eb, 0, st, pdl, (const float*)parts, nchunk(R), C, out));
+      OK_(launch_k(op_colpart_kernel, dim3(C / 128, nchunk(R)), eb, 0, st, pdl, x, (int)R, C, parts));
+      OK_(launch_k(op_colfin_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, (const float*)parts, nchunk(R), C, out));
       nl += 2;
     }
     return SLM_OK;
@@ -121,7 +125,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     const ConvGeom g = geom(v, in_node);
     const int64_t R = rows(v);
     const int K = g.k * g.k * g.Cin, Cout = width(v);
-    OK_(launch_k(op_im2col_kernel, ew((size_t)R * K / 8), eb, 0, st, pdl, x, g, (size_t)R, xq));
+    OK_(launch_k(op_im2col_kernel, ew((size_t)R * 32), eb, 0, st, pdl, x, g, (size_t)R, xq));
     if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
     if ((s = kmap(&mb, xq, K, (int)R, ntile(R))) != SLM_OK) return s;
     EpiBiasF32 e{y, Cout, d.b[p->orig[v]]};
@@ -156,13 +160,17 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
                          d.beta[u], R, w, V(v)));
             ++nl;
           } else {   // chunked two-pass statistics, then the affine map
-            const dim3 gr((w + 31) / 32, nchunk(R));
+            const dim3 gr(w / 128, nchunk(R)), gf((w + 31) / 32);
             OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, parts));
-            OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)parts,
+            OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(R), R,
+                         w, smu, srs));
+            OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)smu,
                          parts + PS));
-            OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)parts,
-                         (const float*)(parts + PS), d.gamma[u], d.beta[u], V(v)));
-            nl += 3;
+            OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
+                         nchunk(R), R, w, (float*)nullptr, srs));
+            OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)smu,
+                         (const float*)srs, d.gamma[u], d.beta[u], V(v)));
+            nl += 5;
           }
           break;
         }
@@ -255,16 +263,21 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
                        d.gamma[u], Ru, wu, V(v), d.dgamma[u], d.dbeta[u]));
           ++nl;
         } else {
-          const dim3 gr((wu + 31) / 32, nchunk(Ru));
+          const dim3 gr(wu / 128, nchunk(Ru)), gf((wu + 31) / 32);
           const float* xr = V(rest[0]);
           OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, parts));
-          OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, (const float*)parts, parts + PS));
-          OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)parts,
-                       (const float*)(parts + PS), parts + 2 * PS, parts + 3 * PS));
-          OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)parts,
-                       (const float*)(parts + PS), (const float*)(parts + 2 * PS), (const float*)(parts + 3 * PS),
-                       d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));
-          nl += 4;
+          OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(Ru), Ru,
+                       wu, smu, srs));
+          OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, (const float*)smu, parts + PS));
+          OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
+                       nchunk(Ru), Ru, wu, (float*)nullptr, srs));
+          OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)smu, (const float*)srs,
+                       parts + 2 * PS, parts + 3 * PS));
+          OK_(launch_k(op_parts2_kernel, gf, eb, 0, st, pdl, (const float*)(parts + 2 * PS),
+                       (const float*)(parts + 3 * PS), nchunk(Ru), wu, ss1, ss2));
+          OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)smu, (const float*)srs,
+                       (const float*)ss1, (const float*)ss2, d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));
+          nl += 7;
         }
         break;
       case SLM_OP_ADD:   // [dy | dy]
@@ -286,7 +299,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         const int64_t Rin = rows(xin);
         // bf16 dy and the im2col columns of x (the GEMM operands), db = column sums of dy
         OK_(launch_k(op_pack_kernel, ew((size_t)Ru * Cout), eb, 0, st, pdl, dy, Ru, Cout, Cout, gq));
-        OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * K / 8), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
+        OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * 32), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
         nl += 2;
         if ((s = colsum(dy, Ru, Cout, d.db[u])) != SLM_OK) return s;
         // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows.
@@ -314,7 +327,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         EpiStoreF32 e2{dcol, K};
         OT_((launch_tc_bn<EpiStoreF32, true, false, true>(ntile(Ru), 1, ma, mb, K, Ru, Cout, 0, 0, e2, st, pdl)));
         // dx = col2im(dcol) (gather over the taps in order)
-        OK_(launch_k(op_col2im_kernel, ew((size_t)Rin * g.Cin / 4), eb, 0, st, pdl, (const float*)dcol, g,
+        OK_(launch_k(op_col2im_kernel, ew((size_t)Rin * 32), eb, 0, st, pdl, (const float*)dcol, g,
                      (size_t)Rin, V(v)));
         nl += 3;
         break;

@@ -183,16 +183,28 @@ __global__ void __launch_bounds__(256) op_pack_kernel(const float* __restrict__ 
 
 // ---------------------------------------------------------------- many-row reductions
 // Values of convolutional graphs have rows = B*H*W (NHWC) up to ~10^4-10^5 per channel: the
-// per-channel sums run over row chunks of kRowChunk rows in parallel CTAs (grid (C/32, chunks)),
-// each chunk's partial in a fixed order (8 row groups), then the chunk partials in chunk order.
+// per-channel sums run over row chunks of kRowChunk rows in parallel CTAs (grid (C/128, chunks)),
+// each chunk's partial in a fixed order (8 row groups), then the chunk partials (block_parts_sum)
+// into per-channel statistics, computed once per channel.
 // Batch statistics are two-pass (mean, then the centred sum of squares), as bn_stats32.
 constexpr int kRowChunk = 256;
-__device__ __forceinline__ float chunk_colsum(const float* __restrict__ x, int R, int C, int f, int r0, int r1,
-                                              float (*red)[33]) {
+// Total over the chunk partials of channel f = blockIdx.x * 32 + lane, by a 256-thread CTA: warp w
+// sums chunks w, w + 8, ... (loads of consecutive channels coalesced, 4 in flight per thread), the
+// eight warp sums are added in warp order.  A fixed order, so deterministic; every thread returns
+// the total.
+__device__ __forceinline__ float block_parts_sum(const float* __restrict__ part, int nch, int C, int f,
+                                                 float (*red)[33]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float s = 0.f;
-  if (f < C)
-    for (int r = r0 + w; r < r1; r += 8) s = __fadd_rn(s, x[(size_t)r * C + f]);
+  if (f < C) {
+    int ch = w;
+    for (; ch + 24 < nch; ch += 32) {
+      const float a = part[(size_t)ch * C + f], b = part[(size_t)(ch + 8) * C + f];
+      const float c = part[(size_t)(ch + 16) * C + f], d = part[(size_t)(ch + 24) * C + f];
+      s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, a), b), c), d);
+    }
+    for (; ch < nch; ch += 8) s = __fadd_rn(s, part[(size_t)ch * C + f]);
+  }
   red[w][lane] = s;
   __syncthreads();
   float t = 0.f;
@@ -201,140 +213,176 @@ __device__ __forceinline__ float chunk_colsum(const float* __restrict__ x, int R
   __syncthreads();
   return t;
 }
-__device__ __forceinline__ float parts_sum(const float* __restrict__ part, int nch, int C, int f) {
-  float t = 0.f;
-  for (int ch = 0; ch < nch; ++ch) t = __fadd_rn(t, part[(size_t)ch * C + f]);
+// The chunk kernels: grid (C / 128, chunks), 256 threads; lane l of warp w holds channels
+// blockIdx.x * 128 + 4 l .. + 3 (float4: a warp reads 512 contiguous bytes of a row) and rows
+// r0 + w, r0 + w + 8, ... of the chunk; the eight warp partials are added in warp order.
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 ld_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st_f4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+// total over the 8 warps (warp order), valid in warp 0
+__device__ __forceinline__ float4 warps_sum4(float4 v, float4 (*red)[32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  red[w][lane] = v;
+  __syncthreads();
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t = f4_add(t, red[i][lane]);
+  }
   return t;
 }
 // part[ch][f] = sum of x[r][f] over the rows of chunk ch
 __global__ void __launch_bounds__(256) op_colpart_kernel(const float* __restrict__ x, int R, int C,
                                                          float* __restrict__ part) {
-  __shared__ float red[8][33];
+  __shared__ float4 red[8][32];
   pdl_wait();
   pdl_launch();
-  const int f = blockIdx.x * 32 + (threadIdx.x & 31), ch = blockIdx.y;
+  const int f = blockIdx.x * 128 + (threadIdx.x & 31) * 4, w = threadIdx.x >> 5, ch = blockIdx.y;
   const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
-  const float t = chunk_colsum(x, R, C, f, r0, r1, red);
-  if (threadIdx.x < 32 && f < C) part[(size_t)ch * C + f] = t;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int r = r0 + w; r < r1; r += 8) s = f4_add(s, ld_f4(x + (size_t)r * C + f));
+  const float4 t = warps_sum4(s, red);
+  if (w == 0) st_f4(part + (size_t)ch * C + f, t);
 }
-// out[f] = sum of the chunk partials in chunk order
+// out[f] = total of the chunk partials (block_parts_sum); grid (C + 31) / 32, 256 threads
 __global__ void __launch_bounds__(256) op_colfin_kernel(const float* __restrict__ part, int nch, int C,
                                                         float* __restrict__ out) {
-  pdl_wait();
-  pdl_launch();
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < C) out[f] = parts_sum(part, nch, C, f);
-}
-// mean and rstd of channel f from the chunk partials (sum, centred squares)
-__device__ __forceinline__ void parts_stats(const float* __restrict__ psum, const float* __restrict__ psq, int nch,
-                                            int R, int C, int f, float& mu, float& rstd) {
-  const float invR = __frcp_rn((float)R);
-  mu = __fmul_rn(parts_sum(psum, nch, C, f), invR);
-  if (psq) rstd = __frsqrt_rn(__fadd_rn(__fmul_rn(parts_sum(psq, nch, C, f), invR), kEps));
-}
-// psq[ch][f] = sum over chunk ch of (x - mu)^2, mu from psum
-__global__ void __launch_bounds__(256) op_bn_sq_kernel(const float* __restrict__ x, int R, int C,
-                                                       const float* __restrict__ psum, float* __restrict__ psq) {
   __shared__ float red[8][33];
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  const int f = blockIdx.x * 32 + (threadIdx.x & 31);
+  const float t = block_parts_sum(part, nch, C, f, red);
+  if (threadIdx.x < 32 && f < C) out[f] = t;
+}
+// per-channel statistics from the chunk partials, once per channel (reading A10): mean = total(psum)
+// / R and, with psq (centred squares), rstd = 1 / sqrt(total(psq) / R + eps)
+__global__ void __launch_bounds__(256) op_bn_fin_kernel(const float* __restrict__ psum, const float* __restrict__ psq,
+                                                        int nch, int R, int C, float* __restrict__ mu_out,
+                                                        float* __restrict__ rstd_out) {
+  __shared__ float red[8][33];
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * 32 + (threadIdx.x & 31);
+  const float invR = __frcp_rn((float)R);
+  if (mu_out) {
+    const float t = block_parts_sum(psum, nch, C, f, red);
+    if (threadIdx.x < 32 && f < C) mu_out[f] = __fmul_rn(t, invR);
+  }
+  if (psq) {
+    const float t = block_parts_sum(psq, nch, C, f, red);
+    if (threadIdx.x < 32 && f < C) rstd_out[f] = __frsqrt_rn(__fadd_rn(__fmul_rn(t, invR), kEps));
+  }
+}
+// totals of two partial arrays (the backward sums S1, S2)
+__global__ void __launch_bounds__(256) op_parts2_kernel(const float* __restrict__ p1, const float* __restrict__ p2,
+                                                        int nch, int C, float* __restrict__ s1, float* __restrict__ s2) {
+  __shared__ float red[8][33];
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * 32 + (threadIdx.x & 31);
+  const float a = block_parts_sum(p1, nch, C, f, red);
+  const float b = block_parts_sum(p2, nch, C, f, red);
+  if (threadIdx.x < 32 && f < C) {
+    s1[f] = a;
+    s2[f] = b;
+  }
+}
+// psq[ch][f] = sum over chunk ch of (x - mu)^2
+__global__ void __launch_bounds__(256) op_bn_sq_kernel(const float* __restrict__ x, int R, int C,
+                                                       const float* __restrict__ mean, float* __restrict__ psq) {
+  __shared__ float4 red[8][32];
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * 128 + (threadIdx.x & 31) * 4, w = threadIdx.x >> 5, ch = blockIdx.y;
   const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
-  float mu = 0.f, dummy;
-  if (f < C) parts_stats(psum, nullptr, nch, R, C, f, mu, dummy);
-  float v = 0.f;
-  if (f < C)
-    for (int r = r0 + w; r < r1; r += 8) {
-      const float e = __fsub_rn(x[(size_t)r * C + f], mu);
-      v = __fmaf_rn(e, e, v);
-    }
-  red[w][lane] = v;
-  __syncthreads();
-  if (w != 0 || f >= C) return;
-  float t = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) t = __fadd_rn(t, red[i][lane]);
-  psq[(size_t)ch * C + f] = t;
+  const float4 mu = ld_f4(mean + f);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int r = r0 + w; r < r1; r += 8) {
+    const float4 a = ld_f4(x + (size_t)r * C + f);
+    const float ex = __fsub_rn(a.x, mu.x), ey = __fsub_rn(a.y, mu.y), ez = __fsub_rn(a.z, mu.z), ew = __fsub_rn(a.w, mu.w);
+    v = make_float4(__fmaf_rn(ex, ex, v.x), __fmaf_rn(ey, ey, v.y), __fmaf_rn(ez, ez, v.z), __fmaf_rn(ew, ew, v.w));
+  }
+  const float4 t = warps_sum4(v, red);
+  if (w == 0) st_f4(psq + (size_t)ch * C + f, t);
 }
 // y = gamma xhat + beta over chunk ch (y may alias x)
-__global__ void __launch_bounds__(256) op_bn_apply_kernel(const float* x, int R, int C, const float* __restrict__ psum,
-                                                          const float* __restrict__ psq, const float* __restrict__ gamma,
+__global__ void __launch_bounds__(256) op_bn_apply_kernel(const float* x, int R, int C, const float* __restrict__ mean,
+                                                          const float* __restrict__ rstdv, const float* __restrict__ gamma,
                                                           const float* __restrict__ beta, float* y) {
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
-  if (f >= C) return;
+  const int f = blockIdx.x * 128 + (threadIdx.x & 31) * 4, w = threadIdx.x >> 5, ch = blockIdx.y;
   const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
-  float mu, rstd;
-  parts_stats(psum, psq, nch, R, C, f, mu, rstd);
-  const float g = gamma[f], bt = beta[f];
+  const float4 mu = ld_f4(mean + f), rs = ld_f4(rstdv + f), g = ld_f4(gamma + f), bt = ld_f4(beta + f);
+#pragma unroll 4
   for (int r = r0 + w; r < r1; r += 8) {
     const size_t i = (size_t)r * C + f;
-    y[i] = bn_u(bn_xhat(x[i], mu, rstd), g, bt);
+    const float4 a = ld_f4(x + i);
+    st_f4(y + i, make_float4(bn_u(bn_xhat(a.x, mu.x, rs.x), g.x, bt.x), bn_u(bn_xhat(a.y, mu.y, rs.y), g.y, bt.y),
+                             bn_u(bn_xhat(a.z, mu.z, rs.z), g.z, bt.z), bn_u(bn_xhat(a.w, mu.w, rs.w), g.w, bt.w)));
   }
 }
 // backward chunk partials: ps1 = sum dy, ps2 = sum dy xhat
 __global__ void __launch_bounds__(256) op_bn_bpart_kernel(const float* dy, const float* __restrict__ x, int R, int C,
-                                                          const float* __restrict__ psum, const float* __restrict__ psq,
+                                                          const float* __restrict__ mean, const float* __restrict__ rstdv,
                                                           float* __restrict__ ps1, float* __restrict__ ps2) {
-  __shared__ float red[8][33];
-  __shared__ float red2[8][33];
+  __shared__ float4 red[8][32];
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
+  const int f = blockIdx.x * 128 + (threadIdx.x & 31) * 4, w = threadIdx.x >> 5, ch = blockIdx.y;
   const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
-  float mu = 0.f, rstd = 0.f, s1 = 0.f, s2 = 0.f;
-  if (f < C) {
-    parts_stats(psum, psq, nch, R, C, f, mu, rstd);
-    for (int r = r0 + w; r < r1; r += 8) {
-      const size_t i = (size_t)r * C + f;
-      const float g = dy[i];
-      s1 = __fadd_rn(s1, g);
-      s2 = __fmaf_rn(g, bn_xhat(x[i], mu, rstd), s2);
-    }
+  const float4 mu = ld_f4(mean + f), rs = ld_f4(rstdv + f);
+  float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), s2 = s1;
+#pragma unroll 4
+  for (int r = r0 + w; r < r1; r += 8) {
+    const size_t i = (size_t)r * C + f;
+    const float4 g = ld_f4(dy + i), a = ld_f4(x + i);
+    s1 = f4_add(s1, g);
+    s2 = make_float4(__fmaf_rn(g.x, bn_xhat(a.x, mu.x, rs.x), s2.x), __fmaf_rn(g.y, bn_xhat(a.y, mu.y, rs.y), s2.y),
+                     __fmaf_rn(g.z, bn_xhat(a.z, mu.z, rs.z), s2.z), __fmaf_rn(g.w, bn_xhat(a.w, mu.w, rs.w), s2.w));
   }
-  red[w][lane] = s1;
-  red2[w][lane] = s2;
+  const float4 t1 = warps_sum4(s1, red);
   __syncthreads();
-  if (w != 0 || f >= C) return;
-  float t1 = 0.f, t2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    t1 = __fadd_rn(t1, red[i][lane]);
-    t2 = __fadd_rn(t2, red2[i][lane]);
+  const float4 t2 = warps_sum4(s2, red);
+  if (w == 0) {
+    st_f4(ps1 + (size_t)ch * C + f, t1);
+    st_f4(ps2 + (size_t)ch * C + f, t2);
   }
-  ps1[(size_t)ch * C + f] = t1;
-  ps2[(size_t)ch * C + f] = t2;
 }
 // dx = gamma rstd (dy - mean dy - xhat mean(dy xhat)) over chunk ch (dx may alias dy); chunk 0
 // writes dgamma / dbeta
+__device__ __forceinline__ float bn_dx1(float g, float a, float mu, float rs, float m1, float m2, float k) {
+  return __fmul_rn(k, __fsub_rn(__fsub_rn(g, m1), __fmul_rn(bn_xhat(a, mu, rs), m2)));
+}
 __global__ void __launch_bounds__(256) op_bn_bapply_kernel(const float* dy, const float* __restrict__ x, int R, int C,
-                                                           const float* __restrict__ psum, const float* __restrict__ psq,
-                                                           const float* __restrict__ ps1, const float* __restrict__ ps2,
+                                                           const float* __restrict__ mean, const float* __restrict__ rstdv,
+                                                           const float* __restrict__ S1v, const float* __restrict__ S2v,
                                                            const float* __restrict__ gamma, float* dx,
                                                            float* __restrict__ dgamma, float* __restrict__ dbeta) {
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane, ch = blockIdx.y, nch = gridDim.y;
-  if (f >= C) return;
+  const int f = blockIdx.x * 128 + (threadIdx.x & 31) * 4, w = threadIdx.x >> 5, ch = blockIdx.y;
   const int r0 = ch * kRowChunk, r1 = min(R, r0 + kRowChunk);
-  float mu, rstd;
-  parts_stats(psum, psq, nch, R, C, f, mu, rstd);
-  const float S1 = parts_sum(ps1, nch, C, f), S2 = parts_sum(ps2, nch, C, f);
   const float invR = __frcp_rn((float)R);
-  const float m1 = __fmul_rn(S1, invR), m2 = __fmul_rn(S2, invR), k = __fmul_rn(gamma[f], rstd);
+  const float4 mu = ld_f4(mean + f), rs = ld_f4(rstdv + f), S1 = ld_f4(S1v + f), S2 = ld_f4(S2v + f),
+               gm = ld_f4(gamma + f);
+  const float4 m1 = make_float4(__fmul_rn(S1.x, invR), __fmul_rn(S1.y, invR), __fmul_rn(S1.z, invR), __fmul_rn(S1.w, invR));
+  const float4 m2 = make_float4(__fmul_rn(S2.x, invR), __fmul_rn(S2.y, invR), __fmul_rn(S2.z, invR), __fmul_rn(S2.w, invR));
+  const float4 k = make_float4(__fmul_rn(gm.x, rs.x), __fmul_rn(gm.y, rs.y), __fmul_rn(gm.z, rs.z), __fmul_rn(gm.w, rs.w));
+#pragma unroll 4
   for (int r = r0 + w; r < r1; r += 8) {
     const size_t i = (size_t)r * C + f;
-    const float xh = bn_xhat(x[i], mu, rstd);
-    dx[i] = __fmul_rn(k, __fsub_rn(__fsub_rn(dy[i], m1), __fmul_rn(xh, m2)));
+    const float4 g = ld_f4(dy + i), a = ld_f4(x + i);
+    st_f4(dx + i, make_float4(bn_dx1(g.x, a.x, mu.x, rs.x, m1.x, m2.x, k.x), bn_dx1(g.y, a.y, mu.y, rs.y, m1.y, m2.y, k.y),
+                              bn_dx1(g.z, a.z, mu.z, rs.z, m1.z, m2.z, k.z), bn_dx1(g.w, a.w, mu.w, rs.w, m1.w, m2.w, k.w)));
   }
   if (ch == 0 && w == 0) {
-    dgamma[f] = S2;
-    dbeta[f] = S1;
+    st_f4(dgamma + f, S2);
+    st_f4(dbeta + f, S1);
   }
 }
 
@@ -350,54 +398,64 @@ __global__ void __launch_bounds__(256) op_im2col_kernel(const float* __restrict_
                                                         __nv_bfloat16* __restrict__ col) {
   pdl_wait();
   pdl_launch();
-  const int K = g.k * g.k * g.Cin, K8 = K / 8, p = g.k / 2;
-  const size_t n = R * (size_t)K8;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = i / K8;
-    const int q = (int)(i % K8) * 8, tap = q / g.Cin, c = q % g.Cin, u = tap / g.k, v = tap % g.k;
-    const int hw = g.Ho * g.Wo, b = (int)(r / hw), rem = (int)(r % hw), oi = rem / g.Wo, oj = rem % g.Wo;
-    const int h = oi * g.s + u - p, w = oj * g.s + v - p;
-    uint4 o = make_uint4(0u, 0u, 0u, 0u);
-    if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
-      const float4* src = reinterpret_cast<const float4*>(x + ((size_t)(b * g.H + h) * g.W + w) * g.Cin + c);
-      const float4 a = src[0], e = src[1];
-      __nv_bfloat162 t0 = __floats2bfloat162_rn(a.x, a.y), t1 = __floats2bfloat162_rn(a.z, a.w);
-      __nv_bfloat162 t2 = __floats2bfloat162_rn(e.x, e.y), t3 = __floats2bfloat162_rn(e.z, e.w);
-      o = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
-                     *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+  // one warp per output row (position): the row's coordinates once, the lanes over its K / 8
+  // 16-byte column groups (consecutive lanes write consecutive 16 B); 32-bit index arithmetic
+  const int K8 = g.k * g.k * g.Cin / 8, C8 = g.Cin / 8, p = g.k / 2, hw = g.Ho * g.Wo;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  uint4* out = reinterpret_cast<uint4*>(col);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < (int)R; r += nw) {
+    const int b = r / hw, rem = r - b * hw, oi = rem / g.Wo, oj = rem - oi * g.Wo;
+    const int h0 = oi * g.s - p, w0 = oj * g.s - p;
+    for (int j = lane; j < K8; j += 32) {
+      const int tap = j / C8, c = (j - tap * C8) * 8, u = tap / g.k, v = tap - u * g.k;
+      const int h = h0 + u, w = w0 + v;
+      uint4 o = make_uint4(0u, 0u, 0u, 0u);
+      if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
+        const float4* src = reinterpret_cast<const float4*>(x + ((size_t)(b * g.H + h) * g.W + w) * g.Cin + c);
+        const float4 a = src[0], e = src[1];
+        __nv_bfloat162 t0 = __floats2bfloat162_rn(a.x, a.y), t1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(e.x, e.y), t3 = __floats2bfloat162_rn(e.z, e.w);
+        o = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                       *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+      }
+      out[(size_t)r * K8 + j] = o;
     }
-    reinterpret_cast<uint4*>(col)[i] = o;
   }
 }
 // dx[b][h][w][c] = sum over the taps (u, v) in order whose output position reads x[b][h][w] of
-// dcol[(b, i, j)][(u k + v) C_in + c]: the gather form of col2im (no atomics; fixed order)
+// dcol[(b, i, j)][(u k + v) C_in + c]: the gather form of col2im (no atomics; fixed order).  One
+// warp per input row, the lanes over its C_in / 4 float4 groups.
 __global__ void __launch_bounds__(256) op_col2im_kernel(const float* __restrict__ dcol, ConvGeom g, size_t Rin,
                                                         float* __restrict__ dx) {
   pdl_wait();
   pdl_launch();
-  const int K = g.k * g.k * g.Cin, C4 = g.Cin / 4, p = g.k / 2;
-  const size_t n = Rin * (size_t)C4;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = i / C4;
-    const int c = (int)(i % C4) * 4;
-    const int hw = g.H * g.W, b = (int)(r / hw), rem = (int)(r % hw), h = rem / g.W, w = rem % g.W;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int u = 0; u < g.k; ++u) {
-      const int ih = h + p - u;
-      if (ih < 0 || ih % g.s) continue;
-      const int oi = ih / g.s;
-      if (oi >= g.Ho) continue;
-      for (int v = 0; v < g.k; ++v) {
-        const int iw = w + p - v;
-        if (iw < 0 || iw % g.s) continue;
-        const int oj = iw / g.s;
-        if (oj >= g.Wo) continue;
-        const float4 d = *reinterpret_cast<const float4*>(dcol + ((size_t)(b * g.Ho + oi) * g.Wo + oj) * K +
-                                                          (u * g.k + v) * g.Cin + c);
-        acc = make_float4(__fadd_rn(acc.x, d.x), __fadd_rn(acc.y, d.y), __fadd_rn(acc.z, d.z), __fadd_rn(acc.w, d.w));
+  const int K = g.k * g.k * g.Cin, C4 = g.Cin / 4, p = g.k / 2, hw = g.H * g.W;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < (int)Rin; r += nw) {
+    const int b = r / hw, rem = r - b * hw, h = rem / g.W, w = rem - h * g.W;
+    for (int c4 = lane; c4 < C4; c4 += 32) {
+      const int c = c4 * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < g.k; ++u) {
+        const int ih = h + p - u;
+        if (ih < 0 || ih % g.s) continue;
+        const int oi = ih / g.s;
+        if (oi >= g.Ho) continue;
+        for (int v = 0; v < g.k; ++v) {
+          const int iw = w + p - v;
+          if (iw < 0 || iw % g.s) continue;
+          const int oj = iw / g.s;
+          if (oj >= g.Wo) continue;
+          const float4 d = *reinterpret_cast<const float4*>(dcol + ((size_t)(b * g.Ho + oi) * g.Wo + oj) * K +
+                                                            (u * g.k + v) * g.Cin + c);
+          acc = make_float4(__fadd_rn(acc.x, d.x), __fadd_rn(acc.y, d.y), __fadd_rn(acc.z, d.z),
+                            __fadd_rn(acc.w, d.w));
+        }
       }
+      reinterpret_cast<float4*>(dx)[(size_t)r * C4 + c4] = acc;
     }
-    reinterpret_cast<float4*>(dx)[i] = acc;
   }
 }
 // split-K partial sums -> bf16: out[i] = bf16(sum_{ks < split} P[ks * n + i]) in ks order

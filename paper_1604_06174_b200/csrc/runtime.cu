@@ -243,6 +243,7 @@ slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model
     if ((nd.op == SLM_OP_ADD) && d.shape &&
         (d.shape[5 * nd.preds[1]] != in[0] || d.shape[5 * nd.preds[1] + 1] != in[1] || d.shape[5 * nd.preds[1] + 2] != in[2]))
       return bad(v, "Add of different shapes");
+    if (rows >= (int64_t)1 << 31) return bad(v, "more than 2^31 - 1 rows (batch * H * W)");
     m->od.rows.push_back(rows);
     m->od.shape.push_back(sh);
     if (!loss) {
