@@ -326,7 +326,7 @@ struct slm_ops_model {
   // per node: rows (batch H W) and (H, W, C, k, s) (convolutional graphs)
   std::vector<int64_t> rows;
   std::vector<std::array<int, 5>> shape;
-  int64_t max_elems = 0, max_col = 0, max_parts = 0;   // workspace sizing
+  int64_t max_elems = 0, max_col = 0, max_parts = 0, max_colT = 0, max_wt = 0;   // workspace sizing
 };
 
 struct slm_model {

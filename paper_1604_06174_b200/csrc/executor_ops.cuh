@@ -30,7 +30,7 @@ bool ops_supported(int op) {
 // workspace: bf16 GEMM operands (x / im2col columns, dy), the summed upstream gradient, the conv
 // column gradient dcol (fp32), the chunk partials of the many-row reductions, CE row losses
 struct OpsWs {
-  size_t xq, gq, dy, dcol, parts, stat, rowloss, total;
+  size_t xq, gq, dy, dcol, wt, parts, stat, rowloss, total;
 };
 OpsWs ops_ws_layout(const slm_model& m) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -40,7 +40,8 @@ OpsWs ops_ws_layout(const slm_model& m) {
   L.xq = off;      off += al(std::max(E, Kc) * 2);
   L.gq = off;      off += al(E * 2);
   L.dy = off;      off += al(E * 4);
-  L.dcol = off;    off += al(Kc * 4);
+  L.dcol = off;    off += al(std::max(Kc * 4, (size_t)m.od.max_colT * 2));   // or the bf16 im2col of dy
+  L.wt = off;      off += al((size_t)m.od.max_wt * 2);                       // flipped kernel, bf16
   L.parts = off;   off += al((size_t)m.od.max_parts * 4 * 4);
   L.stat = off;    off += al((size_t)m.ops_maxw * 4 * 4);   // per-channel mean, rstd, S1, S2
   L.rowloss = off; off += al(B * 4);
@@ -320,6 +321,28 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           OK_(launch_k(op_splitk_bf16_kernel, ew((size_t)K * Cout), eb, 0, st, pdl, (const float*)dcol, split,
                        (size_t)K * Cout, (bf*)d.dW[u]));
           ++nl;
+        }
+        if (g.k == 3 && g.s == 1) {
+          // dx = im2col(dy) Wt^T with Wt the flipped, transposed kernel (op_wflip_kernel): one
+          // GEMM of the forward's shape (M = C_in, N = rows, K = k k C_out) instead of the fp32
+          // column gradient and its col2im gather
+          const ConvGeom gt{g.Ho, g.Wo, Cout, g.k, 1, g.Ho, g.Wo};
+          const int Kt = g.k * g.k * Cout;
+          bf* colT = (bf*)dcol;
+          bf* wt = (bf*)(w8 + W.wt);
+          // Wt before the im2col: the GEMM requests its A (Wt) tiles before griddepcontrol.wait
+          // (PREFETCH_A), which is safe only if A's producer is not the immediately preceding
+          // kernel (im2col waits for the flip before it lets the GEMM launch)
+          OK_(launch_k(op_wflip_kernel, dim3(g.Cin / 32, Cout / 32, g.k * g.k), eb, 0, st, pdl, (const bf*)d.W[u], g.k,
+                       g.Cin, Cout, wt));
+          OK_(launch_k(op_im2col_kernel, ew((size_t)Rin * 32), eb, 0, st, pdl, dy, gt, (size_t)Rin, colT));
+          if ((s = kmap(&ma, wt, Kt, g.Cin, 128)) != SLM_OK) return s;
+          if ((s = kmap(&mb, colT, Kt, (int)Rin, ntile(Rin))) != SLM_OK) return s;
+          EpiStoreF32 e3{V(v), g.Cin};
+          OT_((launch_tc_bn<EpiStoreF32, false, false, true>(ntile(Rin), 1, ma, mb, g.Cin, (int)Rin, Kt, 0, 0, e3, st,
+                                                            pdl)));
+          nl += 3;
+          break;
         }
         // dcol[r][k] = sum_o dy[r][o] W[o][k]: D[m = K][n = r], W MN-major (K = C_out rows)
         if ((s = kmap(&ma, d.W[u], K, Cout, 64)) != SLM_OK) return s;

@@ -458,6 +458,23 @@ __global__ void __launch_bounds__(256) op_col2im_kernel(const float* __restrict_
     }
   }
 }
+// The flipped, transposed kernel of a k x k stride-1 convolution: Wt[c][t' C_out + o] =
+// W[o][(k k - 1 - t') C_in + c] (tap t' = u' k + v' reads tap (k-1-u', k-1-v')), so that
+// dx = im2col(dy) Wt^T -- the input gradient of a stride-1 "same" convolution is the same
+// convolution of dy with the spatially flipped kernel, input and output channels exchanged.
+// 32 x 32 tiles through shared memory per tap: grid (C_in / 32, C_out / 32, k k), 256 threads.
+__global__ void __launch_bounds__(256) op_wflip_kernel(const __nv_bfloat16* __restrict__ W, int k, int Cin, int Cout,
+                                                       __nv_bfloat16* __restrict__ Wt) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  pdl_wait();
+  pdl_launch();
+  const int c0 = blockIdx.x * 32, o0 = blockIdx.y * 32, tp = blockIdx.z, t = k * k - 1 - tp;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const size_t K = (size_t)k * k * Cin, Kt = (size_t)k * k * Cout;
+  for (int i = ty; i < 32; i += 8) tile[i][tx] = W[(size_t)(o0 + i) * K + (size_t)t * Cin + c0 + tx];   // [o][c]
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) Wt[(size_t)(c0 + i) * Kt + (size_t)tp * Cout + o0 + tx] = tile[tx][i];
+}
 // split-K partial sums -> bf16: out[i] = bf16(sum_{ks < split} P[ks * n + i]) in ks order
 __global__ void __launch_bounds__(256) op_splitk_bf16_kernel(const float* __restrict__ P, int split, size_t n,
                                                              __nv_bfloat16* __restrict__ out) {

@@ -236,6 +236,10 @@ slm_status slm_model_ops(const slm_graph* g, const slm_ops_desc* desc, slm_model
         return bad(v, "Conv output size / input channels");
       if (!d.W[v] || !d.b[v] || !d.dW[v] || !d.db[v]) return bad(v, "Conv without W / b / dW / db");
       m->od.max_col = std::max(m->od.max_col, rows * (int64_t)k * k * in[2]);
+      if (k == 3 && st == 1) {   // dx as the convolution of dy with the flipped kernel (executor_ops.cuh)
+        m->od.max_colT = std::max(m->od.max_colT, rows * (int64_t)k * k * sh[2]);
+        m->od.max_wt = std::max(m->od.max_wt, (int64_t)k * k * in[2] * sh[2]);
+      }
     }
     if (nd.op == SLM_OP_POOL && (sh[0] != 1 || sh[1] != 1 || sh[2] != in[2])) return bad(v, "Pool output [batch][C]");
     if ((nd.op == SLM_OP_FC || nd.op == SLM_OP_SOFTMAX_CE) && (in[0] != 1 || in[1] != 1))
