@@ -61,7 +61,8 @@ enum GemmKind { G_FWD = 0, G_DX = 1, G_DW = 2 };
 
 template <int BN, bool AMN, bool BMN, bool PRE, class Epi, int CG = 1>
 slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, int M, int N, int K, int split,
-                     int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg, int pf_row0 = -1) {
+                     int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg, int pf_row0 = -1,
+                     slmk::ConvB cb = {}) {
   using C = slmk::TcCfg<BN, AMN, BMN, CG>;
   auto kern = slmk::tc_gemm_kernel<BN, AMN, BMN, PRE, Epi, CG>;
   static bool attr = false;
@@ -74,7 +75,7 @@ slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
     return SLM_E_UNSUPPORTED;
   }
   CK(launch_kc(kern, dim3(M / 128, N / BN, split), dim3(128), C::SMEM, st, pdl, CG, a, b, c, K, a_row0, b_row0, epi,
-               dbg, pf_row0));
+               dbg, pf_row0, cb));
   return SLM_OK;
 }
 
@@ -83,25 +84,25 @@ slm_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorM
 template <class Epi, bool AMN, bool BMN, bool PRE>
 slm_status launch_tc_bn(int bn, int split, const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                         int a_row0, int b_row0, Epi epi, cudaStream_t st, bool pdl, int dbg = 0,
-                        const CUtensorMap* c = nullptr, int cg = 1, int pf = -1) {
+                        const CUtensorMap* c = nullptr, int cg = 1, int pf = -1, slmk::ConvB cb = {}) {
   const CUtensorMap& cm = c ? *c : a;
   if (cg == 2) {
     switch (bn) {
       case 128:
-        return launch_tc<128, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+        return launch_tc<128, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
       case 256:
-        return launch_tc<256, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+        return launch_tc<256, AMN, BMN, PRE, Epi, 2>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
     }
     set_error("unsupported CTA-pair GEMM N tile " + std::to_string(bn));
     return SLM_E_UNSUPPORTED;
   }
   switch (bn) {
     case 32:
-      if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+      if (!BMN) return launch_tc<32, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
       break;
-    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
-    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
-    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf);
+    case 64: return launch_tc<64, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
+    case 128: return launch_tc<128, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
+    case 256: return launch_tc<256, AMN, BMN, PRE>(a, b, cm, M, N, K, split, a_row0, b_row0, epi, st, pdl, dbg, pf, cb);
   }
   set_error("unsupported GEMM N tile " + std::to_string(bn));
   return SLM_E_UNSUPPORTED;

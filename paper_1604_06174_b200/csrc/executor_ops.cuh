@@ -121,11 +121,41 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     const auto so = shp(v), si = shp(in_node);
     return ConvGeom{si[0], si[1], si[2], so[3], so[4], so[0], so[1]};
   };
+  // Implicit GEMM (slmk::ConvB): a stride-1 convolution whose positions tile into whole image
+  // rows reads its im2col operand as 4-D TMA boxes of the bf16 NHWC tensor -- the columns are
+  // never written.  conv_tile: the largest N tile (positions) of whole image rows that also
+  // divides an image, else 0 (explicit im2col).
+  auto conv_tile = [](const ConvGeom& g, int64_t R) {
+    if (g.s != 1 || g.W > 256) return 0;
+    for (int bn = 256; bn >= 64; bn /= 2)
+      if (R % bn == 0 && (g.H * g.W) % bn == 0 && bn % g.W == 0) return bn;
+    return 0;
+  };
+  auto kmap4 = [&](CUtensorMap* mp, const void* base, const ConvGeom& g, int64_t R, int box_pos) -> slm_status {
+    return dry ? SLM_OK
+               : make_map4(mp, base, (uint64_t)g.Cin, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)(R / (g.H * g.W)),
+                           (uint32_t)(box_pos / g.W));
+  };
+  auto cvt = [&](const float* x, int64_t n, bf* out) -> slm_status {
+    OK_(launch_k(op_cvt_bf16_kernel, ew((size_t)n / 8), eb, 0, st, pdl, (const float4*)x, (size_t)n / 8, (uint4*)out));
+    ++nl;
+    return SLM_OK;
+  };
   // Conv forward: col = im2col(x) (bf16), y = col W^T + b (tcgen05, M = C_out, N = rows, K = k k C_in)
   auto conv_fwd = [&](int v, int in_node, const float* x, float* y) -> slm_status {
     const ConvGeom g = geom(v, in_node);
     const int64_t R = rows(v);
     const int K = g.k * g.k * g.Cin, Cout = width(v);
+    if (const int bn = conv_tile(g, R)) {   // implicit GEMM over bf16(x)
+      if ((s = cvt(x, R * g.Cin, xq)) != SLM_OK) return s;
+      if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
+      if ((s = kmap4(&mb, xq, g, R, bn)) != SLM_OK) return s;
+      EpiBiasF32 e{y, Cout, d.b[p->orig[v]]};
+      OT_((launch_tc_bn<EpiBiasF32, false, false, true>(bn, 1, ma, mb, Cout, (int)R, K, 0, 0, e, st, pdl, 0, nullptr, 1,
+                                                       -1, ConvB{1, g.Cin, g.k, g.H * g.W, g.W})));
+      ++nl;
+      return SLM_OK;
+    }
     OK_(launch_k(op_im2col_kernel, ew((size_t)R * 32), eb, 0, st, pdl, x, g, (size_t)R, xq));
     if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
     if ((s = kmap(&mb, xq, K, (int)R, ntile(R))) != SLM_OK) return s;
@@ -298,15 +328,28 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         const ConvGeom g = geom(u, xin);
         const int K = g.k * g.k * g.Cin, Cout = wu;
         const int64_t Rin = rows(xin);
-        // bf16 dy and the im2col columns of x (the GEMM operands), db = column sums of dy
-        OK_(launch_k(op_pack_kernel, ew((size_t)Ru * Cout), eb, 0, st, pdl, dy, Ru, Cout, Cout, gq));
-        OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * 32), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
-        nl += 2;
+        const bool flip = g.k == 3 && g.s == 1;   // dx by the flipped kernel (below)
+        bf* wt = (bf*)(w8 + W.wt);
+        if (flip)   // first: the dx GEMM prefetches Wt before its dependency wait (PREFETCH_A)
+          OK_(launch_k(op_wflip_kernel, dim3(g.Cin / 32, Cout / 32, g.k * g.k), eb, 0, st, pdl, (const bf*)d.W[u], g.k,
+                       g.Cin, Cout, wt));
+        nl += flip;
+        // bf16 dy and the im2col columns of x (the GEMM operands; implicit: bf16 x), db = column
+        // sums of dy
+        if ((s = cvt(dy, Ru * Cout, gq)) != SLM_OK) return s;
+        const bool implicit_a = g.s == 1 && 64 % g.W == 0 && (g.H * g.W) % 64 == 0;
+        if (implicit_a) {
+          if ((s = cvt(V(xin), Rin * g.Cin, xq)) != SLM_OK) return s;
+        } else {
+          OK_(launch_k(op_im2col_kernel, ew((size_t)Ru * 32), eb, 0, st, pdl, (const float*)V(xin), g, (size_t)Ru, xq));
+          ++nl;
+        }
         if ((s = colsum(dy, Ru, Cout, d.db[u])) != SLM_OK) return s;
         // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows.
         // Few output tiles and a long K (batch H W): split K over ~one wave of CTAs, fp32 partials in
         // the dcol workspace (not yet in use), summed in split order into the bf16 dW
-        if ((s = kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
+        const ConvB cbw = implicit_a ? ConvB{2, g.Cin, g.k, g.H * g.W, g.W} : ConvB{};
+        if ((s = implicit_a ? kmap4(&ma, xq, g, Rin, 64) : kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
         if ((s = kmap(&mb, gq, Cout, Ru, 64)) != SLM_OK) return s;
         const int bnw = Cout % 256 == 0 ? 256 : 128;
         const int tiles = (K / 128) * (Cout / bnw);
@@ -314,34 +357,41 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         while (split * 2 * tiles <= 148 && Ru % (64 * split * 2) == 0 && (int64_t)split * 2 * Cout <= Ru) split *= 2;
         if (split == 1) {
           EpiStoreBF16 e1{(bf*)d.dW[u], K};
-          OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(bnw, 1, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl)));
+          OT_((launch_tc_bn<EpiStoreBF16, true, true, false>(bnw, 1, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl, 0, nullptr,
+                                                            1, -1, cbw)));
         } else {
           EpiPartial e1{dcol, (long)K, (long)K * Cout};
-          OT_((launch_tc_bn<EpiPartial, true, true, false>(bnw, split, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl)));
+          OT_((launch_tc_bn<EpiPartial, true, true, false>(bnw, split, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl, 0, nullptr,
+                                                          1, -1, cbw)));
           OK_(launch_k(op_splitk_bf16_kernel, ew((size_t)K * Cout), eb, 0, st, pdl, (const float*)dcol, split,
                        (size_t)K * Cout, (bf*)d.dW[u]));
           ++nl;
         }
-        if (g.k == 3 && g.s == 1) {
-          // dx = im2col(dy) Wt^T with Wt the flipped, transposed kernel (op_wflip_kernel): one
-          // GEMM of the forward's shape (M = C_in, N = rows, K = k k C_out) instead of the fp32
-          // column gradient and its col2im gather
+        ++nl;   // the dW GEMM
+        if (flip) {
+          // dx = im2col(dy) Wt^T with Wt the flipped, transposed kernel (op_wflip_kernel, launched
+          // first -- the GEMM requests its A (Wt) tiles before griddepcontrol.wait, so Wt's producer
+          // must not be the immediately preceding kernel): one GEMM of the forward's shape (M = C_in,
+          // N = rows, K = k k C_out) instead of the fp32 column gradient and its col2im gather;
+          // implicit over bf16(dy) when the positions tile into whole image rows
           const ConvGeom gt{g.Ho, g.Wo, Cout, g.k, 1, g.Ho, g.Wo};
           const int Kt = g.k * g.k * Cout;
+          const int bn = conv_tile(gt, Rin);
           bf* colT = (bf*)dcol;
-          bf* wt = (bf*)(w8 + W.wt);
-          // Wt before the im2col: the GEMM requests its A (Wt) tiles before griddepcontrol.wait
-          // (PREFETCH_A), which is safe only if A's producer is not the immediately preceding
-          // kernel (im2col waits for the flip before it lets the GEMM launch)
-          OK_(launch_k(op_wflip_kernel, dim3(g.Cin / 32, Cout / 32, g.k * g.k), eb, 0, st, pdl, (const bf*)d.W[u], g.k,
-                       g.Cin, Cout, wt));
-          OK_(launch_k(op_im2col_kernel, ew((size_t)Rin * 32), eb, 0, st, pdl, dy, gt, (size_t)Rin, colT));
+          if (bn) {
+            if ((s = kmap4(&mb, gq, gt, Rin, bn)) != SLM_OK) return s;
+          } else {
+            OK_(launch_k(op_im2col_kernel, ew((size_t)Rin * 32), eb, 0, st, pdl, dy, gt, (size_t)Rin, colT));
+            ++nl;
+            if ((s = kmap(&mb, colT, Kt, (int)Rin, ntile(Rin))) != SLM_OK) return s;
+          }
           if ((s = kmap(&ma, wt, Kt, g.Cin, 128)) != SLM_OK) return s;
-          if ((s = kmap(&mb, colT, Kt, (int)Rin, ntile(Rin))) != SLM_OK) return s;
           EpiStoreF32 e3{V(v), g.Cin};
-          OT_((launch_tc_bn<EpiStoreF32, false, false, true>(ntile(Rin), 1, ma, mb, g.Cin, (int)Rin, Kt, 0, 0, e3, st,
-                                                            pdl)));
-          nl += 3;
+          const int bnx = bn ? bn : ntile(Rin);
+          OT_((launch_tc_bn<EpiStoreF32, false, false, true>(bnx, 1, ma, mb, g.Cin, (int)Rin, Kt, 0, 0, e3, st, pdl, 0,
+                                                            nullptr, 1, -1,
+                                                            bn ? ConvB{1, Cout, g.k, g.Ho * g.Wo, g.Wo} : ConvB{})));
+          ++nl;
           break;
         }
         // dcol[r][k] = sum_o dy[r][o] W[o][k]: D[m = K][n = r], W MN-major (K = C_out rows)
@@ -352,7 +402,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         // dx = col2im(dcol) (gather over the taps in order)
         OK_(launch_k(op_col2im_kernel, ew((size_t)Rin * 32), eb, 0, st, pdl, (const float*)dcol, g,
                      (size_t)Rin, V(v)));
-        nl += 3;
+        nl += 2;
         break;
       }
       case SLM_OP_SOFTMAX_CE:   // rest = [x]; dx may alias x

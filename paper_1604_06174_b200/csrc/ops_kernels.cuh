@@ -181,6 +181,20 @@ __global__ void __launch_bounds__(256) op_pack_kernel(const float* __restrict__ 
     out[i] = __float2bfloat16_rn(x[(i / w) * ld + i % w]);
 }
 
+// contiguous fp32 -> bf16 (RN), 8 elements per thread (n8 = elements / 8)
+__global__ void __launch_bounds__(256) op_cvt_bf16_kernel(const float4* __restrict__ x, size_t n8,
+                                                          uint4* __restrict__ out) {
+  pdl_wait();
+  pdl_launch();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = x[2 * i], e = x[2 * i + 1];
+    __nv_bfloat162 t0 = __floats2bfloat162_rn(a.x, a.y), t1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(e.x, e.y), t3 = __floats2bfloat162_rn(e.z, e.w);
+    out[i] = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                        *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+  }
+}
+
 // ---------------------------------------------------------------- many-row reductions
 // Values of convolutional graphs have rows = B*H*W (NHWC) up to ~10^4-10^5 per channel: the
 // per-channel sums run over row chunks of kRowChunk rows in parallel CTAs (grid (C/128, chunks)),

@@ -123,6 +123,30 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
   return SLM_OK;
 }
 
+// bf16 NHWC tensor [images][h][w][c] as a 4-D map {c, w, h, images}, box {64, w, box_h, 1},
+// 128-byte swizzle: one box = box_h whole image rows of 64 channels, laid out in shared memory as
+// the 2-D box {64, w box_h} (the implicit-GEMM convolution operand, slmk::ConvB)
+slm_status make_map4(CUtensorMap* map, const void* base, uint64_t c, uint64_t w, uint64_t h, uint64_t imgs,
+                     uint32_t box_h) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SLM_E_CUDA;
+  }
+  cuuint64_t dims[4] = {c, w, h, imgs};
+  cuuint64_t strides[3] = {c * 2, w * c * 2, h * w * c * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)w, box_h, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (4-D conv operand) failed: " + std::to_string((int)r));
+    return SLM_E_CUDA;
+  }
+  return SLM_OK;
+}
+
 }  // namespace
 
 #include "executor.cuh"

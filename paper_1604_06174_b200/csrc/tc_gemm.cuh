@@ -63,6 +63,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 4-D tile load (the implicit-GEMM convolution operand: {C, W, H, image} of an NHWC tensor;
+// coordinates may be negative / past the end -- those elements are zero-filled, which is the
+// convolution's "same" padding)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// Implicit-GEMM convolution operand (stride 1, "same" padding p = k / 2): the im2col matrix
+// col[position][(u k + v) cin + c] = x[img][i + u - p][j + v - p][c] is never stored; its tiles
+// are 4-D TMA boxes of the bf16 NHWC tensor x (map {cin, w, h, images}).  on = 1: it is the
+// K-major B operand (rows = positions, a tile = BN / w whole image rows); on = 2: the MN-major A
+// operand of the weight gradient (K = positions, a 64-position K block = 64 / w image rows).
+struct ConvB {
+  int on = 0, cin = 0, k = 0, hw = 0, w = 0;
+};
 // bulk prefetch of one tensor-map box into L2 (no smem, no barrier)
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
@@ -372,7 +391,7 @@ template <int BN, bool A_MN, bool B_MN, bool PREFETCH_A, class Epi, int CG = 1>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, int K, int a_row0, int b_row0, Epi epi, int dbg,
-                   int pf_row0) {
+                   int pf_row0, ConvB cb) {
   unsigned long long* const tsp = ts_buffer(dbg);
   ts_mark(tsp, 0, dbg);
   using C = TcCfg<BN, A_MN, B_MN, CG>;
@@ -442,10 +461,20 @@ __global__ void __launch_bounds__(128, 1)
     else
       tma_load_2d(dst, map, &full[s], c0, c1);
   };
+  // tap (u, v) and channel offset of im2col column kk, as 4-D box coordinates (c, j0, i0, img) of
+  // the positions starting at q (whole image rows)
+  auto conv_load = [&](void* dst, const CUtensorMap* map, int s, int kk, int q) {
+    const int tap = kk / cb.cin, c0 = kk - tap * cb.cin, u = tap / cb.k, v = tap - u * cb.k, p = cb.k / 2;
+    const int img = q / cb.hw, i0 = (q - img * cb.hw) / cb.w;
+    tma_load_4d(dst, map, &full[s], c0, v - p, i0 + u - p, img);
+  };
   auto load_a = [&](int kb, int s) {
     uint8_t* sa = smem + s * C::STAGE;
     const int k0 = kbase + kb * C::BK;
-    if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
+    if (A_MN && cb.on == 2) {   // implicit im2col, A = col [positions = K][M = (tap, c)]
+      conv_load(sa, &tmA, s, m0, k0);
+      conv_load(sa + 8192, &tmA, s, m0 + 64, k0);
+    } else if (A_MN) {  // A stored [K][M]: boxes of 64(M) x 64(K)
       tma(sa, &tmA, s, m0, a_row0 + k0);
       tma(sa + 8192, &tmA, s, m0 + 64, a_row0 + k0);
     } else {     // A stored [M][K]: one box of 64(K) x 128(M)
@@ -459,6 +488,8 @@ __global__ void __launch_bounds__(128, 1)
     if (B_MN) {
 #pragma unroll
       for (int j = 0; j < C::BNC / 64; ++j) tma(sb + j * 8192, &tmB, s, nb0 + 64 * j, b_row0 + k0);
+    } else if (CG == 1 && cb.on == 1) {   // implicit im2col, B = col [N = positions][K = (tap, c)]
+      conv_load(sb, &tmB, s, k0, nb0);
     } else {     // box rows = BN / CG
       tma(sb, &tmB, s, k0, b_row0 + nb0);
     }

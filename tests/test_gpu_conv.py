@@ -87,6 +87,10 @@ def _small_graph(slm, B, spec):
     [("input", 7), ("conv", 128, 3, 1)],                                    # odd size, ragged rows
     [("input", 8), ("conv", 256, 1, 2), ("bn",), ("relu",)],                # projection + chunked BN
     [("input", 6), ("bn",), ("relu",), ("conv", 128, 3, 1), ("conv", 128, 3, 1)],
+    # implicit GEMM (4-D TMA boxes of whole image rows): N tile 256 = 16 / 8 rows, W-gradient
+    # K blocks of 4 / 2 rows, dx through the flipped kernel over bf16 dy
+    [("input", 16), ("conv", 128, 3, 1), ("bn",), ("relu",), ("conv", 256, 3, 1)],
+    [("input", 32), ("conv", 128, 3, 1)],
 ])
 def test_conv_ops_vs_oracle_strict(slm, spec):
     """Single conv / BN stages (little depth for bf16 rounding decisions to amplify): every element
