@@ -32,6 +32,18 @@ bool ops_supported(int op) {
 struct OpsWs {
   size_t xq, gq, dy, dcol, wt, parts, stat, rowloss, total;
 };
+// float offsets (after the 4 x max-width scratch) of each node's kept BN statistics (mean[C],
+// rstd[C]); the last entry is the total.  Only the chunked (many-row) BNs keep them: their
+// gradient reads them instead of re-reducing x (the values are the forward's bit for bit, as a
+// re-computed BN produces the same statistics).  2 C floats per BN node -- workspace, not part of
+// the plan's activation memory (like the saved mean / inverse std of library BN layers).
+std::vector<size_t> bn_stat_slots(const slm_model& m) {
+  const size_t n = m.od.rows.size();
+  std::vector<size_t> off(n + 1, 0);
+  for (size_t u = 0; u < n; ++u)
+    off[u + 1] = off[u] + (m.od.op[u] == SLM_OP_BN && m.od.rows[u] > slmk::kRowChunk ? 2 * (size_t)m.od.shape[u][2] : 0);
+  return off;
+}
 OpsWs ops_ws_layout(const slm_model& m) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t B = m.od.batch, E = (size_t)m.od.max_elems, Kc = (size_t)m.od.max_col;
@@ -43,7 +55,9 @@ OpsWs ops_ws_layout(const slm_model& m) {
   L.dcol = off;    off += al(std::max(Kc * 4, (size_t)m.od.max_colT * 2));   // or the bf16 im2col of dy
   L.wt = off;      off += al((size_t)m.od.max_wt * 2);                       // flipped kernel, bf16
   L.parts = off;   off += al((size_t)m.od.max_parts * 4 * 4);
-  L.stat = off;    off += al((size_t)m.ops_maxw * 4 * 4);   // per-channel mean, rstd, S1, S2
+  // per-channel mean, rstd, S1, S2 of the current BN, then every BN node's (mean, rstd) kept from
+  // its forward for its gradient node (bn_stat_slots)
+  L.stat = off;    off += al(((size_t)m.ops_maxw * 4 + bn_stat_slots(m).back()) * 4);
   L.rowloss = off; off += al(B * 4);
   L.total = off;
   return L;
@@ -75,7 +89,9 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   float* parts = (float*)(w8 + W.parts);
   float* stat = (float*)(w8 + W.stat);
   const int MW = m.ops_maxw;
-  float *smu = stat, *srs = stat + MW, *ss1 = stat + 2 * MW, *ss2 = stat + 3 * MW;
+  float *ss1 = stat + 2 * MW, *ss2 = stat + 3 * MW;   // stat[0, 2 MW): spare
+  const std::vector<size_t> bnslot = bn_stat_slots(m);
+  auto bn_mu = [&](int u) { return stat + 4 * (size_t)MW + bnslot[u]; };   // then rstd at + C
   const size_t PS = (size_t)d.max_parts;   // one partial array: chunks x C floats
   slm_status s = SLM_OK;
   int64_t nl = 0;
@@ -192,15 +208,16 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
             ++nl;
           } else {   // chunked two-pass statistics, then the affine map
             const dim3 gr(w / 128, nchunk(R)), gf((w + 31) / 32);
+            float *mu = bn_mu(u), *rs = mu + w;
             OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, parts));
             OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(R), R,
-                         w, smu, srs));
-            OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)smu,
+                         w, mu, rs));
+            OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)mu,
                          parts + PS));
             OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
-                         nchunk(R), R, w, (float*)nullptr, srs));
-            OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)smu,
-                         (const float*)srs, d.gamma[u], d.beta[u], V(v)));
+                         nchunk(R), R, w, (float*)nullptr, rs));
+            OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)mu,
+                         (const float*)rs, d.gamma[u], d.beta[u], V(v)));
             nl += 5;
           }
           break;
@@ -276,7 +293,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
       if (gs.n == 1 && gs.ld[0] == wu) {
         dy = gs.p[0];   // one whole slice in the node's own layout (an in-place output aliases it element for element)
       } else {
-        OK_(launch_k(op_gsum_kernel, ew((size_t)rows(u) * wu), eb, 0, st, pdl, gs, rows(u), wu, dyw));
+        OK_(launch_k(op_gsum_kernel, ew((size_t)rows(u) * wu / 4), eb, 0, st, pdl, gs, rows(u), wu, dyw));
         ++nl;
         dy = dyw;
       }
@@ -296,19 +313,13 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         } else {
           const dim3 gr(wu / 128, nchunk(Ru)), gf((wu + 31) / 32);
           const float* xr = V(rest[0]);
-          OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, parts));
-          OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(Ru), Ru,
-                       wu, smu, srs));
-          OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, xr, Ru, wu, (const float*)smu, parts + PS));
-          OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
-                       nchunk(Ru), Ru, wu, (float*)nullptr, srs));
-          OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)smu, (const float*)srs,
-                       parts + 2 * PS, parts + 3 * PS));
+          const float *mu = bn_mu(u), *rs = mu + wu;   // the forward's statistics
+          OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, mu, rs, parts + 2 * PS, parts + 3 * PS));
           OK_(launch_k(op_parts2_kernel, gf, eb, 0, st, pdl, (const float*)(parts + 2 * PS),
                        (const float*)(parts + 3 * PS), nchunk(Ru), wu, ss1, ss2));
-          OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, (const float*)smu, (const float*)srs,
-                       (const float*)ss1, (const float*)ss2, d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));
-          nl += 7;
+          OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, mu, rs, (const float*)ss1,
+                       (const float*)ss2, d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));
+          nl += 3;
         }
         break;
       case SLM_OP_ADD:   // [dy | dy]

@@ -159,15 +159,21 @@ struct GradSlices {
   int ld[8];
   int n;
 };
+// (widths, strides and offsets are multiples of 128 floats: float4 per thread)
 __global__ void __launch_bounds__(256) op_gsum_kernel(GradSlices s, int B, int w, float* __restrict__ out) {
   pdl_wait();
   pdl_launch();
-  const size_t n = (size_t)B * w;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = i / w, c = i % w;
-    float v = s.p[0][b * s.ld[0] + c];
-    for (int k = 1; k < s.n; ++k) v = __fadd_rn(v, s.p[k][b * s.ld[k] + c]);
-    out[i] = v;
+  const int w4 = w / 4;
+  const size_t n4 = (size_t)B * w4;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / w4;
+    const int c = (int)(i - b * w4) * 4;
+    float4 v = *reinterpret_cast<const float4*>(s.p[0] + b * s.ld[0] + c);
+    for (int k = 1; k < s.n; ++k) {
+      const float4 t = *reinterpret_cast<const float4*>(s.p[k] + b * s.ld[k] + c);
+      v = make_float4(__fadd_rn(v.x, t.x), __fadd_rn(v.y, t.y), __fadd_rn(v.z, t.z), __fadd_rn(v.w, t.w));
+    }
+    reinterpret_cast<float4*>(out)[i] = v;
   }
 }
 
