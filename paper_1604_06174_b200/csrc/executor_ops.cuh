@@ -41,7 +41,7 @@ std::vector<size_t> bn_stat_slots(const slm_model& m) {
   const size_t n = m.od.rows.size();
   std::vector<size_t> off(n + 1, 0);
   for (size_t u = 0; u < n; ++u)
-    off[u + 1] = off[u] + (m.od.op[u] == SLM_OP_BN && m.od.rows[u] > slmk::kRowChunk ? 2 * (size_t)m.od.shape[u][2] : 0);
+    off[u + 1] = off[u] + (m.od.op[u] == SLM_OP_BN && m.od.rows[u] > slmk::kSmallRows ? 2 * (size_t)m.od.shape[u][2] : 0);
   return off;
 }
 OpsWs ops_ws_layout(const slm_model& m) {
@@ -111,7 +111,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   auto V = [&](int node) -> float* { return (float*)tp[p->node_tag[node]]; };
   const int* pred = p->preds.data();
   auto ew = [&](size_t n) { return dim3((unsigned)std::max<size_t>(1, std::min<size_t>(1184, (n + 255) / 256))); };
-  const dim3 eb(256);
+  const dim3 eb(256), ebf(kFinThreads);
   // tensor maps of one GEMM operand (encoded per launch: host work only, captured into the graph)
   CUtensorMap ma, mb;
   auto kmap = [&](CUtensorMap* mp, const void* base, int inner, int rows, int box_rows) -> slm_status {
@@ -119,16 +119,16 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   };
   const int bnB = B % 256 == 0 ? 256 : B % 128 == 0 ? 128 : 64;   // N tile over the batch
   auto ntile = [](int64_t R) { return R % 256 == 0 ? 256 : R % 128 == 0 ? 128 : 64; };
-  // per-channel sums over R rows: the original one-CTA-per-32-channels kernels up to kRowChunk
+  // per-channel sums over R rows: the original one-CTA-per-32-channels kernels up to kSmallRows
   // rows (the f1 graphs' bits), the chunked kernels beyond
   auto nchunk = [](int64_t R) { return (int)((R + kRowChunk - 1) / kRowChunk); };
   auto colsum = [&](const float* x, int64_t R, int C, float* out) -> slm_status {
-    if (R <= kRowChunk) {
+    if (R <= kSmallRows) {
       OK_(launch_k(colsum_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, x, (int)R, C, out));
       ++nl;
     } else {
       OK_(launch_k(op_colpart_kernel, dim3(C / 128, nchunk(R)), eb, 0, st, pdl, x, (int)R, C, parts));
-      OK_(launch_k(op_colfin_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, (const float*)parts, nchunk(R), C, out));
+      OK_(launch_k(op_colfin_kernel, dim3((C + 31) / 32), ebf, 0, st, pdl, (const float*)parts, nchunk(R), C, out));
       nl += 2;
     }
     return SLM_OK;
@@ -202,7 +202,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           break;
         case SLM_OP_BN: {
           const int R = rows(v);
-          if (R <= kRowChunk) {
+          if (R <= kSmallRows) {
             OK_(launch_k(op_bn_fwd_kernel, dim3((w + 31) / 32), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
                          d.beta[u], R, w, V(v)));
             ++nl;
@@ -210,11 +210,11 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
             const dim3 gr(w / 128, nchunk(R)), gf((w + 31) / 32);
             float *mu = bn_mu(u), *rs = mu + w;
             OK_(launch_k(op_colpart_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, parts));
-            OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(R), R,
+            OK_(launch_k(op_bn_fin_kernel, gf, ebf, 0, st, pdl, (const float*)parts, (const float*)nullptr, nchunk(R), R,
                          w, mu, rs));
             OK_(launch_k(op_bn_sq_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)mu,
                          parts + PS));
-            OK_(launch_k(op_bn_fin_kernel, gf, eb, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
+            OK_(launch_k(op_bn_fin_kernel, gf, ebf, 0, st, pdl, (const float*)parts, (const float*)(parts + PS),
                          nchunk(R), R, w, (float*)nullptr, rs));
             OK_(launch_k(op_bn_apply_kernel, gr, eb, 0, st, pdl, (const float*)V(pv[0]), R, w, (const float*)mu,
                          (const float*)rs, d.gamma[u], d.beta[u], V(v)));
@@ -306,7 +306,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         ++nl;
         break;
       case SLM_OP_BN:   // rest = [x]
-        if (Ru <= kRowChunk) {
+        if (Ru <= kSmallRows) {
           OK_(launch_k(op_bn_bwd_kernel, dim3((wu + 31) / 32), eb, 0, st, pdl, dy, (const float*)V(rest[0]),
                        d.gamma[u], Ru, wu, V(v), d.dgamma[u], d.dbeta[u]));
           ++nl;
@@ -315,7 +315,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           const float* xr = V(rest[0]);
           const float *mu = bn_mu(u), *rs = mu + wu;   // the forward's statistics
           OK_(launch_k(op_bn_bpart_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, mu, rs, parts + 2 * PS, parts + 3 * PS));
-          OK_(launch_k(op_parts2_kernel, gf, eb, 0, st, pdl, (const float*)(parts + 2 * PS),
+          OK_(launch_k(op_parts2_kernel, gf, ebf, 0, st, pdl, (const float*)(parts + 2 * PS),
                        (const float*)(parts + 3 * PS), nchunk(Ru), wu, ss1, ss2));
           OK_(launch_k(op_bn_bapply_kernel, gr, eb, 0, st, pdl, dy, xr, Ru, wu, mu, rs, (const float*)ss1,
                        (const float*)ss2, d.gamma[u], V(v), d.dgamma[u], d.dbeta[u]));

@@ -207,29 +207,31 @@ __global__ void __launch_bounds__(256) op_cvt_bf16_kernel(const float4* __restri
 // each chunk's partial in a fixed order (8 row groups), then the chunk partials (block_parts_sum)
 // into per-channel statistics, computed once per channel.
 // Batch statistics are two-pass (mean, then the centred sum of squares), as bn_stats32.
-constexpr int kRowChunk = 256;
-// Total over the chunk partials of channel f = blockIdx.x * 32 + lane, by a 256-thread CTA: warp w
-// sums chunks w, w + 8, ... (loads of consecutive channels coalesced, 4 in flight per thread), the
-// eight warp sums are added in warp order.  A fixed order, so deterministic; every thread returns
-// the total.
+constexpr int kRowChunk = 128;   // rows per chunk CTA (C = 128 at 64 x 32 x 32 rows: 512 CTAs)
+constexpr int kSmallRows = 256;  // up to this many rows: the one-CTA-per-32-channels kernels
+// Total over the chunk partials of channel f = blockIdx.x * 32 + lane, by a 1024-thread CTA (the
+// partials are few KB to a few hundred KB: latency, not bandwidth): warp w sums chunks w, w + 32,
+// ... (loads of consecutive channels coalesced, 4 in flight per thread), the 32 warp sums are
+// added in warp order.  A fixed order, so deterministic; every thread returns the total.
+constexpr int kFinThreads = 1024;
 __device__ __forceinline__ float block_parts_sum(const float* __restrict__ part, int nch, int C, int f,
                                                  float (*red)[33]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float s = 0.f;
   if (f < C) {
     int ch = w;
-    for (; ch + 24 < nch; ch += 32) {
-      const float a = part[(size_t)ch * C + f], b = part[(size_t)(ch + 8) * C + f];
-      const float c = part[(size_t)(ch + 16) * C + f], d = part[(size_t)(ch + 24) * C + f];
+    for (; ch + 96 < nch; ch += 128) {
+      const float a = part[(size_t)ch * C + f], b = part[(size_t)(ch + 32) * C + f];
+      const float c = part[(size_t)(ch + 64) * C + f], d = part[(size_t)(ch + 96) * C + f];
       s = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(s, a), b), c), d);
     }
-    for (; ch < nch; ch += 8) s = __fadd_rn(s, part[(size_t)ch * C + f]);
+    for (; ch < nch; ch += 32) s = __fadd_rn(s, part[(size_t)ch * C + f]);
   }
   red[w][lane] = s;
   __syncthreads();
   float t = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) t = __fadd_rn(t, red[i][lane]);
+  for (int i = 0; i < 32; ++i) t = __fadd_rn(t, red[i][lane]);
   __syncthreads();
   return t;
 }
@@ -267,10 +269,10 @@ __global__ void __launch_bounds__(256) op_colpart_kernel(const float* __restrict
   const float4 t = warps_sum4(s, red);
   if (w == 0) st_f4(part + (size_t)ch * C + f, t);
 }
-// out[f] = total of the chunk partials (block_parts_sum); grid (C + 31) / 32, 256 threads
-__global__ void __launch_bounds__(256) op_colfin_kernel(const float* __restrict__ part, int nch, int C,
+// out[f] = total of the chunk partials (block_parts_sum); grid (C + 31) / 32, kFinThreads threads
+__global__ void __launch_bounds__(kFinThreads) op_colfin_kernel(const float* __restrict__ part, int nch, int C,
                                                         float* __restrict__ out) {
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   pdl_wait();
   pdl_launch();
   const int f = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -279,10 +281,10 @@ __global__ void __launch_bounds__(256) op_colfin_kernel(const float* __restrict_
 }
 // per-channel statistics from the chunk partials, once per channel (reading A10): mean = total(psum)
 // / R and, with psq (centred squares), rstd = 1 / sqrt(total(psq) / R + eps)
-__global__ void __launch_bounds__(256) op_bn_fin_kernel(const float* __restrict__ psum, const float* __restrict__ psq,
+__global__ void __launch_bounds__(kFinThreads) op_bn_fin_kernel(const float* __restrict__ psum, const float* __restrict__ psq,
                                                         int nch, int R, int C, float* __restrict__ mu_out,
                                                         float* __restrict__ rstd_out) {
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   pdl_wait();
   pdl_launch();
   const int f = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -297,9 +299,9 @@ __global__ void __launch_bounds__(256) op_bn_fin_kernel(const float* __restrict_
   }
 }
 // totals of two partial arrays (the backward sums S1, S2)
-__global__ void __launch_bounds__(256) op_parts2_kernel(const float* __restrict__ p1, const float* __restrict__ p2,
+__global__ void __launch_bounds__(kFinThreads) op_parts2_kernel(const float* __restrict__ p1, const float* __restrict__ p2,
                                                         int nch, int C, float* __restrict__ s1, float* __restrict__ s2) {
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   pdl_wait();
   pdl_launch();
   const int f = blockIdx.x * 32 + (threadIdx.x & 31);
