@@ -141,17 +141,21 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   // rows reads its im2col operand as 4-D TMA boxes of the bf16 NHWC tensor -- the columns are
   // never written.  conv_tile: the largest N tile (positions) of whole image rows that also
   // divides an image, else 0 (explicit im2col).
-  auto conv_tile = [](const ConvGeom& g, int64_t R) {
-    if (g.s != 1 || g.W > 256) return 0;
+  // (R = output positions; a box spans s wo x s rows input elements, each <= 256)
+  auto tiles_rows = [](const ConvGeom& g, int64_t R, int bn) {
+    return R % bn == 0 && (g.Ho * g.Wo) % bn == 0 && bn % g.Wo == 0 && g.s * g.Wo <= 256 && g.s * (bn / g.Wo) <= 256;
+  };
+  auto conv_tile = [&](const ConvGeom& g, int64_t R) {
     for (int bn = 256; bn >= 64; bn /= 2)
-      if (R % bn == 0 && (g.H * g.W) % bn == 0 && bn % g.W == 0) return bn;
+      if (tiles_rows(g, R, bn)) return bn;
     return 0;
   };
   auto kmap4 = [&](CUtensorMap* mp, const void* base, const ConvGeom& g, int64_t R, int box_pos) -> slm_status {
     return dry ? SLM_OK
-               : make_map4(mp, base, (uint64_t)g.Cin, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)(R / (g.H * g.W)),
-                           (uint32_t)(box_pos / g.W));
+               : make_map4(mp, base, (uint64_t)g.Cin, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)(R / (g.Ho * g.Wo)),
+                           (uint32_t)g.Wo, (uint32_t)(box_pos / g.Wo), (uint32_t)g.s);
   };
+  auto convb = [](int on, const ConvGeom& g) { return ConvB{on, g.Cin, g.k, g.Ho * g.Wo, g.Wo, g.s}; };
   auto cvt = [&](const float* x, int64_t n, bf* out) -> slm_status {
     OK_(launch_k(op_cvt_bf16_kernel, ew((size_t)n / 8), eb, 0, st, pdl, (const float4*)x, (size_t)n / 8, (uint4*)out));
     ++nl;
@@ -163,12 +167,12 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     const int64_t R = rows(v);
     const int K = g.k * g.k * g.Cin, Cout = width(v);
     if (const int bn = conv_tile(g, R)) {   // implicit GEMM over bf16(x)
-      if ((s = cvt(x, R * g.Cin, xq)) != SLM_OK) return s;
+      if ((s = cvt(x, rows(in_node) * (int64_t)g.Cin, xq)) != SLM_OK) return s;
       if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
       if ((s = kmap4(&mb, xq, g, R, bn)) != SLM_OK) return s;
       EpiBiasF32 e{y, Cout, d.b[p->orig[v]]};
       OT_((launch_tc_bn<EpiBiasF32, false, false, true>(bn, 1, ma, mb, Cout, (int)R, K, 0, 0, e, st, pdl, 0, nullptr, 1,
-                                                       -1, ConvB{1, g.Cin, g.k, g.H * g.W, g.W})));
+                                                       -1, convb(1, g))));
       ++nl;
       return SLM_OK;
     }
@@ -348,7 +352,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         // bf16 dy and the im2col columns of x (the GEMM operands; implicit: bf16 x), db = column
         // sums of dy
         if ((s = cvt(dy, Ru * Cout, gq)) != SLM_OK) return s;
-        const bool implicit_a = g.s == 1 && 64 % g.W == 0 && (g.H * g.W) % 64 == 0;
+        const bool implicit_a = 64 % g.Wo == 0 && tiles_rows(g, Ru, 64);
         if (implicit_a) {
           if ((s = cvt(V(xin), Rin * g.Cin, xq)) != SLM_OK) return s;
         } else {
@@ -359,8 +363,8 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         // dW[C_out][K] = sum_r dy[r][o] col[r][k]: D[m = K][n = C_out], both operands MN-major, K = rows.
         // Few output tiles and a long K (batch H W): split K over ~one wave of CTAs, fp32 partials in
         // the dcol workspace (not yet in use), summed in split order into the bf16 dW
-        const ConvB cbw = implicit_a ? ConvB{2, g.Cin, g.k, g.H * g.W, g.W} : ConvB{};
-        if ((s = implicit_a ? kmap4(&ma, xq, g, Rin, 64) : kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
+        const ConvB cbw = implicit_a ? convb(2, g) : ConvB{};
+        if ((s = implicit_a ? kmap4(&ma, xq, g, Ru, 64) : kmap(&ma, xq, K, Ru, 64)) != SLM_OK) return s;
         if ((s = kmap(&mb, gq, Cout, Ru, 64)) != SLM_OK) return s;
         const int bnw = Cout % 256 == 0 ? 256 : 128;
         const int tiles = (K / 128) * (Cout / bnw);
@@ -401,7 +405,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           const int bnx = bn ? bn : ntile(Rin);
           OT_((launch_tc_bn<EpiStoreF32, false, false, true>(bnx, 1, ma, mb, g.Cin, (int)Rin, Kt, 0, 0, e3, st, pdl, 0,
                                                             nullptr, 1, -1,
-                                                            bn ? ConvB{1, Cout, g.k, g.Ho * g.Wo, g.Wo} : ConvB{})));
+                                                            bn ? convb(1, gt) : ConvB{})));
           ++nl;
           break;
         }

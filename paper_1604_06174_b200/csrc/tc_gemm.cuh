@@ -74,13 +74,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-// Implicit-GEMM convolution operand (stride 1, "same" padding p = k / 2): the im2col matrix
-// col[position][(u k + v) cin + c] = x[img][i + u - p][j + v - p][c] is never stored; its tiles
-// are 4-D TMA boxes of the bf16 NHWC tensor x (map {cin, w, h, images}).  on = 1: it is the
-// K-major B operand (rows = positions, a tile = BN / w whole image rows); on = 2: the MN-major A
-// operand of the weight gradient (K = positions, a 64-position K block = 64 / w image rows).
+// Implicit-GEMM convolution operand (stride s, "same" padding p = k / 2): the im2col matrix
+// col[position (i, j)][(u k + v) cin + c] = x[img][s i + u - p][s j + v - p][c] is never stored;
+// its tiles are 4-D TMA boxes of the bf16 NHWC input x (map {cin, W, H, images}, element strides
+// {1, s, s, 1}: a box of s wo x s rows elements loads wo x rows of them).  hw, w: the OUTPUT
+// positions per image and per row.  on = 1: the K-major B operand (rows = positions, a tile = BN
+// / w whole output rows); on = 2: the MN-major A operand of the weight gradient (K = positions, a
+// 64-position K block = 64 / w output rows).
 struct ConvB {
-  int on = 0, cin = 0, k = 0, hw = 0, w = 0;
+  int on = 0, cin = 0, k = 0, hw = 0, w = 0, s = 1;
 };
 // bulk prefetch of one tensor-map box into L2 (no smem, no barrier)
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(128, 1)
   auto conv_load = [&](void* dst, const CUtensorMap* map, int s, int kk, int q) {
     const int tap = kk / cb.cin, c0 = kk - tap * cb.cin, u = tap / cb.k, v = tap - u * cb.k, p = cb.k / 2;
     const int img = q / cb.hw, i0 = (q - img * cb.hw) / cb.w;
-    tma_load_4d(dst, map, &full[s], c0, v - p, i0 + u - p, img);
+    tma_load_4d(dst, map, &full[s], c0, v - p, cb.s * i0 + u - p, img);
   };
   auto load_a = [&](int kb, int s) {
     uint8_t* sa = smem + s * C::STAGE;

@@ -91,6 +91,9 @@ def _small_graph(slm, B, spec):
     # K blocks of 4 / 2 rows, dx through the flipped kernel over bf16 dy
     [("input", 16), ("conv", 128, 3, 1), ("bn",), ("relu",), ("conv", 256, 3, 1)],
     [("input", 32), ("conv", 128, 3, 1)],
+    # stride 2 implicit (element-strided 4-D boxes): 3x3 and the 1x1 projection, 16x16 -> 8x8
+    [("input", 16), ("conv", 256, 3, 2)],
+    [("input", 16), ("conv", 256, 1, 2), ("bn",), ("relu",)],
 ])
 def test_conv_ops_vs_oracle_strict(slm, spec):
     """Single conv / BN stages (little depth for bf16 rounding decisions to amplify): every element
