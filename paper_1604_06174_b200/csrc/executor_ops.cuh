@@ -117,7 +117,14 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   auto kmap = [&](CUtensorMap* mp, const void* base, int inner, int rows, int box_rows) -> slm_status {
     return dry ? SLM_OK : make_map(mp, base, (uint64_t)inner, (uint64_t)rows, (uint32_t)box_rows);
   };
-  const int bnB = B % 256 == 0 ? 256 : B % 128 == 0 ? 128 : 64;   // N tile over the batch
+  // N tile over the batch of an FC GEMM with M output rows: the largest that still gives >= 64
+  // CTAs (M = 2048, B = 256: 64-column tiles, 64 CTAs instead of 16; every output element's
+  // K accumulation is the same whatever the tile, so the bits do not depend on it)
+  auto fc_bn = [&](int M) {
+    int bn = B % 256 == 0 ? 256 : B % 128 == 0 ? 128 : 64;
+    while (bn > 64 && (int64_t)(M / 128) * (B / bn) < 64) bn /= 2;
+    return bn;
+  };
   auto ntile = [](int64_t R) { return R % 256 == 0 ? 256 : R % 128 == 0 ? 128 : 64; };
   // per-channel sums over R rows: the original one-CTA-per-32-channels kernels up to kSmallRows
   // rows (the f1 graphs' bits), the chunked kernels beyond
@@ -186,12 +193,13 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   };
   // FC x -> y = x W^T + b   (W [dout][din] bf16)
   auto fc_fwd = [&](int v, const float* x, int din, int dout, float* y) -> slm_status {
-    OK_(launch_k(op_pack_kernel, ew((size_t)B * din), eb, 0, st, pdl, x, B, din, din, xq));
+    if ((s = cvt(x, (int64_t)B * din, xq)) != SLM_OK) return s;
+    const int bn = fc_bn(dout);
     if ((s = kmap(&ma, d.W[p->orig[v]], din, dout, 128)) != SLM_OK) return s;
-    if ((s = kmap(&mb, xq, din, B, bnB)) != SLM_OK) return s;
+    if ((s = kmap(&mb, xq, din, B, bn)) != SLM_OK) return s;
     EpiBiasF32 e{y, dout, d.b[p->orig[v]]};
-    OT_((launch_tc_bn<EpiBiasF32, false, false, true>(bnB, 1, ma, mb, dout, B, din, 0, 0, e, st, pdl)));
-    nl += 2;
+    OT_((launch_tc_bn<EpiBiasF32, false, false, true>(bn, 1, ma, mb, dout, B, din, 0, 0, e, st, pdl)));
+    ++nl;
     return SLM_OK;
   };
 
@@ -207,7 +215,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         case SLM_OP_BN: {
           const int R = rows(v);
           if (R <= kSmallRows) {
-            OK_(launch_k(op_bn_fwd_kernel, dim3((w + 31) / 32), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
+            OK_(launch_k(op_bn_fwd_kernel, dim3(w / 8), eb, 0, st, pdl, (const float*)V(pv[0]), d.gamma[u],
                          d.beta[u], R, w, V(v)));
             ++nl;
           } else {   // chunked two-pass statistics, then the affine map
@@ -311,7 +319,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         break;
       case SLM_OP_BN:   // rest = [x]
         if (Ru <= kSmallRows) {
-          OK_(launch_k(op_bn_bwd_kernel, dim3((wu + 31) / 32), eb, 0, st, pdl, dy, (const float*)V(rest[0]),
+          OK_(launch_k(op_bn_bwd_kernel, dim3(wu / 8), eb, 0, st, pdl, dy, (const float*)V(rest[0]),
                        d.gamma[u], Ru, wu, V(v), d.dgamma[u], d.dbeta[u]));
           ++nl;
         } else {
@@ -428,8 +436,8 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
       case SLM_OP_FC: {   // rest = [x]
         const int din = width(rest[0]), dout = wu;
         // bf16 dy and x (the GEMM operands), db = column sums of dy -- all before dx may overwrite dy
-        OK_(launch_k(op_pack_kernel, ew((size_t)B * dout), eb, 0, st, pdl, dy, B, dout, dout, gq));
-        OK_(launch_k(op_pack_kernel, ew((size_t)B * din), eb, 0, st, pdl, (const float*)V(rest[0]), B, din, din, xq));
+        if ((s = cvt(dy, (int64_t)B * dout, gq)) != SLM_OK) return s;
+        if ((s = cvt(V(rest[0]), (int64_t)B * din, xq)) != SLM_OK) return s;
         OK_(launch_k(colsum_kernel, dim3((dout + 31) / 32), eb, 0, st, pdl, dy, B, dout, d.db[u]));
         // dW[dout][din] = sum_b dy[b][dout] x[b][din]: D[m = din][n = dout], both operands MN-major, K = B
         if ((s = kmap(&ma, xq, din, B, 64)) != SLM_OK) return s;
@@ -439,10 +447,11 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
                                                           e1, st, pdl)));
         // dx[b][din] = sum_o dy[b][o] W[o][din]: D[m = din][n = b], W MN-major (K = dout rows)
         if ((s = kmap(&ma, d.W[u], din, dout, 64)) != SLM_OK) return s;
-        if ((s = kmap(&mb, gq, dout, B, bnB)) != SLM_OK) return s;
+        const int bnx = fc_bn(din);
+        if ((s = kmap(&mb, gq, dout, B, bnx)) != SLM_OK) return s;
         EpiStoreF32 e2{V(v), din};
-        OT_((launch_tc_bn<EpiStoreF32, true, false, true>(bnB, 1, ma, mb, din, B, dout, 0, 0, e2, st, pdl)));
-        nl += 5;
+        OT_((launch_tc_bn<EpiStoreF32, true, false, true>(bnx, 1, ma, mb, din, B, dout, 0, 0, e2, st, pdl)));
+        nl += 3;   // colsum, dW, dx (the converts count themselves)
         break;
       }
       default:

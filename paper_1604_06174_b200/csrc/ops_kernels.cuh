@@ -13,52 +13,51 @@
 namespace slmk {
 
 // BN with batch statistics (reading A10: biased variance, eps 1e-5), no ReLU:
-// y = gamma (x - mu) rstd + beta.  Block = 32 features x 8 row groups (the bn_act_kernel order).
-__device__ __forceinline__ void bn_stats32(const float* __restrict__ x, int B, int d, int f, bool ok, float (*red)[33],
-                                           float& mu, float& rstd) {
+// y = gamma (x - mu) rstd + beta.
+// Few-row BN (rows <= kSmallRows, e.g. the batch of an FC network): a CTA of 256 threads owns 8
+// features; thread t holds feature t % 8 and rows t / 8, t / 8 + 32, ... (a warp reads 4 rows x 32
+// contiguous bytes per load).  Per-feature totals: the 4 row groups of a warp by an xor-shuffle
+// tree (a + b == b + a, so every lane holding the feature gets the same bits), then the 8 warps in
+// warp order.  Fixed order: deterministic.  Grid d / 8.
+__device__ __forceinline__ float bn8_total(float v, float (*red)[8]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float s = 0.f;
-  if (ok)
-    for (int b = w; b < B; b += 8) s = __fadd_rn(s, x[(size_t)b * d + f]);
-  red[w][lane] = s;
+  v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 8));
+  v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 16));
+  if (lane < 8) red[w][lane] = v;
   __syncthreads();
-  float tot = 0.f;
+  float t = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) tot = __fadd_rn(tot, red[i][lane]);
-  mu = __fmul_rn(tot, __frcp_rn((float)B));
+  for (int i = 0; i < 8; ++i) t = __fadd_rn(t, red[i][lane & 7]);
   __syncthreads();
-  float v = 0.f;
-  if (ok)
-    for (int b = w; b < B; b += 8) {
-      const float dx = __fsub_rn(x[(size_t)b * d + f], mu);
-      v = __fmaf_rn(dx, dx, v);
-    }
-  red[w][lane] = v;
-  __syncthreads();
-  float var = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) var = __fadd_rn(var, red[i][lane]);
-  var = __fmul_rn(var, __frcp_rn((float)B));
-  rstd = __frsqrt_rn(__fadd_rn(var, kEps));
-  __syncthreads();
+  return t;
 }
-
-__global__ void __launch_bounds__(256) op_bn_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
-                                                        const float* __restrict__ beta, int B, int d,
-                                                        float* __restrict__ y) {
-  __shared__ float red[8][33];
+// two-pass batch statistics of feature f (mean, then the centred sum of squares; reading A10)
+__device__ __forceinline__ void bn_stats8(const float* __restrict__ x, int B, int d, int f, float (*red)[8],
+                                          float& mu, float& rstd) {
+  const int rg = threadIdx.x >> 3;
+  const float invB = __frcp_rn((float)B);
+  float s = 0.f;
+  for (int b = rg; b < B; b += 32) s = __fadd_rn(s, x[(size_t)b * d + f]);
+  mu = __fmul_rn(bn8_total(s, red), invB);
+  float v = 0.f;
+  for (int b = rg; b < B; b += 32) {
+    const float e = __fsub_rn(x[(size_t)b * d + f], mu);
+    v = __fmaf_rn(e, e, v);
+  }
+  rstd = __frsqrt_rn(__fadd_rn(__fmul_rn(bn8_total(v, red), invB), kEps));
+}
+__global__ void __launch_bounds__(256) op_bn_fwd_kernel(const float* x, const float* __restrict__ gamma,
+                                                        const float* __restrict__ beta, int B, int d, float* y) {
+  __shared__ float red[8][8];
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  const bool ok = f < d;
+  const int f = blockIdx.x * 8 + (threadIdx.x & 7), rg = threadIdx.x >> 3;
   float mu, rstd;
-  bn_stats32(x, B, d, f, ok, red, mu, rstd);
-  if (!ok) return;
+  bn_stats8(x, B, d, f, red, mu, rstd);
   const float g = gamma[f], bt = beta[f];
-  for (int b = w; b < B; b += 8) {
+  for (int b = rg; b < B; b += 32) {
     const size_t i = (size_t)b * d + f;
-    y[i] = bn_u(bn_xhat(x[i], mu, rstd), g, bt);   // y may alias x: each element is read once before
+    y[i] = bn_u(bn_xhat(x[i], mu, rstd), g, bt);   // y may alias x: each element is read before it is written
   }
 }
 
@@ -67,41 +66,28 @@ __global__ void __launch_bounds__(256) op_bn_fwd_kernel(const float* __restrict_
 __global__ void __launch_bounds__(256) op_bn_bwd_kernel(const float* dy, const float* __restrict__ x,
                                                         const float* __restrict__ gamma, int B, int d, float* dx,
                                                         float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  __shared__ float red[8][33];
-  __shared__ float red2[8][33];
+  __shared__ float red[8][8];
   pdl_wait();
   pdl_launch();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int f = blockIdx.x * 32 + lane;
-  const bool ok = f < d;
+  const int f = blockIdx.x * 8 + (threadIdx.x & 7), rg = threadIdx.x >> 3;
   float mu, rstd;
-  bn_stats32(x, B, d, f, ok, red, mu, rstd);
+  bn_stats8(x, B, d, f, red, mu, rstd);
   float s1 = 0.f, s2 = 0.f;
-  if (ok)
-    for (int b = w; b < B; b += 8) {
-      const size_t i = (size_t)b * d + f;
-      const float g = dy[i];
-      s1 = __fadd_rn(s1, g);
-      s2 = __fmaf_rn(g, bn_xhat(x[i], mu, rstd), s2);
-    }
-  red[w][lane] = s1;
-  red2[w][lane] = s2;
-  __syncthreads();
-  float S1 = 0.f, S2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    S1 = __fadd_rn(S1, red[i][lane]);
-    S2 = __fadd_rn(S2, red2[i][lane]);
+  for (int b = rg; b < B; b += 32) {
+    const size_t i = (size_t)b * d + f;
+    const float g = dy[i];
+    s1 = __fadd_rn(s1, g);
+    s2 = __fmaf_rn(g, bn_xhat(x[i], mu, rstd), s2);
   }
-  if (!ok) return;
+  const float S1 = bn8_total(s1, red), S2 = bn8_total(s2, red);
   const float invB = __frcp_rn((float)B);
   const float m1 = __fmul_rn(S1, invB), m2 = __fmul_rn(S2, invB), k = __fmul_rn(gamma[f], rstd);
-  for (int b = w; b < B; b += 8) {
+  for (int b = rg; b < B; b += 32) {
     const size_t i = (size_t)b * d + f;
     const float xh = bn_xhat(x[i], mu, rstd);
     dx[i] = __fmul_rn(k, __fsub_rn(__fsub_rn(dy[i], m1), __fmul_rn(xh, m2)));
   }
-  if (w == 0) {
+  if (threadIdx.x < 8) {
     dgamma[f] = S2;
     dbeta[f] = S1;
   }
