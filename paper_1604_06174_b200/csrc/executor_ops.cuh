@@ -126,12 +126,12 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     return bn;
   };
   auto ntile = [](int64_t R) { return R % 256 == 0 ? 256 : R % 128 == 0 ? 128 : 64; };
-  // per-channel sums over R rows: the original one-CTA-per-32-channels kernels up to kSmallRows
-  // rows (the f1 graphs' bits), the chunked kernels beyond
+  // per-channel sums over R rows: the 8-feature few-row kernels up to kSmallRows rows, the
+  // chunked kernels beyond
   auto nchunk = [](int64_t R) { return (int)((R + kRowChunk - 1) / kRowChunk); };
   auto colsum = [&](const float* x, int64_t R, int C, float* out) -> slm_status {
     if (R <= kSmallRows) {
-      OK_(launch_k(colsum_kernel, dim3((C + 31) / 32), eb, 0, st, pdl, x, (int)R, C, out));
+      OK_(launch_k(op_colsum8_kernel, dim3(C / 8), eb, 0, st, pdl, x, (int)R, C, out));
       ++nl;
     } else {
       OK_(launch_k(op_colpart_kernel, dim3(C / 128, nchunk(R)), eb, 0, st, pdl, x, (int)R, C, parts));
@@ -438,7 +438,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
         // bf16 dy and x (the GEMM operands), db = column sums of dy -- all before dx may overwrite dy
         if ((s = cvt(dy, (int64_t)B * dout, gq)) != SLM_OK) return s;
         if ((s = cvt(V(rest[0]), (int64_t)B * din, xq)) != SLM_OK) return s;
-        OK_(launch_k(colsum_kernel, dim3((dout + 31) / 32), eb, 0, st, pdl, dy, B, dout, d.db[u]));
+        OK_(launch_k(op_colsum8_kernel, dim3(dout / 8), eb, 0, st, pdl, dy, B, dout, d.db[u]));
         // dW[dout][din] = sum_b dy[b][dout] x[b][din]: D[m = din][n = dout], both operands MN-major, K = B
         if ((s = kmap(&ma, xq, din, B, 64)) != SLM_OK) return s;
         if ((s = kmap(&mb, gq, dout, B, 64)) != SLM_OK) return s;

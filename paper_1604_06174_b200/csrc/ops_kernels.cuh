@@ -46,6 +46,18 @@ __device__ __forceinline__ void bn_stats8(const float* __restrict__ x, int B, in
   }
   rstd = __frsqrt_rn(__fadd_rn(__fmul_rn(bn8_total(v, red), invB), kEps));
 }
+// out[f] = sum of g[b][f] over the B rows (bias gradients), 8 features per CTA as above
+__global__ void __launch_bounds__(256) op_colsum8_kernel(const float* __restrict__ g, int B, int d,
+                                                         float* __restrict__ out) {
+  __shared__ float red[8][8];
+  pdl_wait();
+  pdl_launch();
+  const int f = blockIdx.x * 8 + (threadIdx.x & 7), rg = threadIdx.x >> 3;
+  float s = 0.f;
+  for (int b = rg; b < B; b += 32) s = __fadd_rn(s, g[(size_t)b * d + f]);
+  const float t = bn8_total(s, red);
+  if (threadIdx.x < 8) out[f] = t;
+}
 __global__ void __launch_bounds__(256) op_bn_fwd_kernel(const float* x, const float* __restrict__ gamma,
                                                         const float* __restrict__ beta, int B, int d, float* y) {
   __shared__ float red[8][8];
