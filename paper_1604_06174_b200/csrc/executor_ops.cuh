@@ -386,7 +386,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           EpiPartial e1{dcol, (long)K, (long)K * Cout};
           OT_((launch_tc_bn<EpiPartial, true, true, false>(bnw, split, ma, mb, K, Cout, Ru, 0, 0, e1, st, pdl, 0, nullptr,
                                                           1, -1, cbw)));
-          OK_(launch_k(op_splitk_bf16_kernel, ew((size_t)K * Cout), eb, 0, st, pdl, (const float*)dcol, split,
+          OK_(launch_k(op_splitk_bf16_kernel, ew((size_t)K * Cout / 4), eb, 0, st, pdl, (const float*)dcol, split,
                        (size_t)K * Cout, (bf*)d.dW[u]));
           ++nl;
         }

@@ -496,14 +496,22 @@ __global__ void __launch_bounds__(256) op_wflip_kernel(const __nv_bfloat16* __re
   for (int i = ty; i < 32; i += 8) Wt[(size_t)(c0 + i) * Kt + (size_t)tp * Cout + o0 + tx] = tile[tx][i];
 }
 // split-K partial sums -> bf16: out[i] = bf16(sum_{ks < split} P[ks * n + i]) in ks order
+// (n % 4 == 0: 4 elements per thread, float4 loads, 8-byte stores)
 __global__ void __launch_bounds__(256) op_splitk_bf16_kernel(const float* __restrict__ P, int split, size_t n,
                                                              __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_launch();
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    float v = P[i];
-    for (int ks = 1; ks < split; ++ks) v = __fadd_rn(v, P[(size_t)ks * n + i]);
-    out[i] = __float2bfloat16_rn(v);
+  const size_t n4 = n / 4;
+  const float4* P4 = reinterpret_cast<const float4*>(P);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 v = P4[i];
+#pragma unroll 4
+    for (int ks = 1; ks < split; ++ks) {
+      const float4 t = P4[(size_t)ks * n4 + i];
+      v = make_float4(__fadd_rn(v.x, t.x), __fadd_rn(v.y, t.y), __fadd_rn(v.z, t.z), __fadd_rn(v.w, t.w));
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    reinterpret_cast<uint2*>(out)[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
   }
 }
 // global average pool: y[b][c] = (sum over the HW positions in order) / HW; backward dx = dy / HW
