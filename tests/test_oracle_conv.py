@@ -145,3 +145,20 @@ def test_conv_plan_invariance_bitwise(strategy, mode):
             assert np.array_equal(grads[kind][v], g2[kind][v]), (strategy, kind, v)
     if strategy == P.S_DROP_CHEAP:
         assert plan.extra_forward > 0
+
+
+@pytest.mark.parametrize("H", [5, 6])
+def test_stride1_input_gradient_is_flipped_kernel_convolution(H):
+    """The identity the device's 3x3 stride-1 input gradient uses (op_wflip_kernel):
+    dx = conv(dy, Wt) with Wt[c][(u' k + v') C_out + o] = W[o][((k-1-u') k + (k-1-v')) C_in + c],
+    stride 1, "same" padding -- checked on the oracle's conv_backward (itself pinned to torch above)."""
+    rng = np.random.default_rng(H)
+    B, Cin, Cout, k = 2, 3, 4, 3
+    x = rng.standard_normal((B * H * H, Cin))
+    W = rng.standard_normal((Cout, k * k * Cin))
+    dy = rng.standard_normal((B * H * H, Cout))
+    dx, _, _ = OG.conv_backward(dy, x, W, (H, H, Cin), k, 1, "f64")
+    Wr = W.reshape(Cout, k * k, Cin)
+    Wt = np.transpose(Wr[:, ::-1, :], (2, 1, 0)).reshape(Cin, k * k * Cout)   # [c][t'][o], t' = 8 - t
+    dx2 = OG.conv_forward(dy, Wt, np.zeros(Cin), (H, H, Cout), k, 1, "f64")
+    assert np.allclose(dx, dx2, rtol=1e-12, atol=1e-12)
