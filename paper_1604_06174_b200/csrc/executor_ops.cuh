@@ -149,18 +149,30 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
   // never written.  conv_tile: the largest N tile (positions) of whole image rows that also
   // divides an image, else 0 (explicit im2col).
   // (R = output positions; a box spans s wo x s rows input elements, each <= 256)
+  // a tile of bn positions = whole output rows of one image, or whole images (small maps: 8 x 8 at
+  // bn = 256 is 4 images, where row tiles would stop at bn = 64 and re-read the weights 4x as often)
   auto tiles_rows = [](const ConvGeom& g, int64_t R, int bn) {
-    return R % bn == 0 && (g.Ho * g.Wo) % bn == 0 && bn % g.Wo == 0 && g.s * g.Wo <= 256 && g.s * (bn / g.Wo) <= 256;
+    const int hw = g.Ho * g.Wo;
+    if (R % bn || g.s * g.Wo > 256) return false;
+    if (hw % bn == 0) return bn % g.Wo == 0 && g.s * (bn / g.Wo) <= 256;
+    return bn % hw == 0 && g.s * g.Ho <= 256;
   };
-  auto conv_tile = [&](const ConvGeom& g, int64_t R) {
+  // N tile of an implicit conv GEMM with M output rows: the largest valid tile that still gives
+  // >= 128 CTAs, else the smallest valid one (0: none, explicit im2col)
+  auto conv_tile = [&](const ConvGeom& g, int64_t R, int M) {
+    int pick = 0;
     for (int bn = 256; bn >= 64; bn /= 2)
-      if (tiles_rows(g, R, bn)) return bn;
-    return 0;
+      if (tiles_rows(g, R, bn)) {
+        pick = bn;
+        if ((int64_t)(M / 128) * (R / bn) >= 128) break;
+      }
+    return pick;
   };
   auto kmap4 = [&](CUtensorMap* mp, const void* base, const ConvGeom& g, int64_t R, int box_pos) -> slm_status {
     return dry ? SLM_OK
                : make_map4(mp, base, (uint64_t)g.Cin, (uint64_t)g.W, (uint64_t)g.H, (uint64_t)(R / (g.Ho * g.Wo)),
-                           (uint32_t)g.Wo, (uint32_t)(box_pos / g.Wo), (uint32_t)g.s);
+                           (uint32_t)g.Wo, (uint32_t)std::min(box_pos / g.Wo, g.Ho), (uint32_t)g.s,
+                           (uint32_t)std::max(1, box_pos / (g.Ho * g.Wo)));
   };
   auto convb = [](int on, const ConvGeom& g) { return ConvB{on, g.Cin, g.k, g.Ho * g.Wo, g.Wo, g.s}; };
   auto cvt = [&](const float* x, int64_t n, bf* out) -> slm_status {
@@ -173,7 +185,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
     const ConvGeom g = geom(v, in_node);
     const int64_t R = rows(v);
     const int K = g.k * g.k * g.Cin, Cout = width(v);
-    if (const int bn = conv_tile(g, R)) {   // implicit GEMM over bf16(x)
+    if (const int bn = conv_tile(g, R, Cout)) {   // implicit GEMM over bf16(x)
       if ((s = cvt(x, rows(in_node) * (int64_t)g.Cin, xq)) != SLM_OK) return s;
       if ((s = kmap(&ma, d.W[p->orig[v]], K, Cout, 128)) != SLM_OK) return s;
       if ((s = kmap4(&mb, xq, g, R, bn)) != SLM_OK) return s;
@@ -399,7 +411,7 @@ slm_status enqueue_ops(const slm_plan* p, slm_model& m, const void* x0, const in
           // implicit over bf16(dy) when the positions tile into whole image rows
           const ConvGeom gt{g.Ho, g.Wo, Cout, g.k, 1, g.Ho, g.Wo};
           const int Kt = g.k * g.k * Cout;
-          const int bn = conv_tile(gt, Rin);
+          const int bn = conv_tile(gt, Rin, g.Cin);
           bf* colT = (bf*)dcol;
           if (bn) {
             if ((s = kmap4(&mb, gq, gt, Rin, bn)) != SLM_OK) return s;

@@ -124,11 +124,13 @@ slm_status make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 }
 
 // bf16 NHWC tensor [images][h][w][c] as a 4-D map {c, w, h, images}, element strides {1, s, s, 1},
-// box {64, s wo, s rows, 1}, 128-byte swizzle: one box = `rows` whole output rows of wo positions
-// (every s-th input column / row) of 64 channels, laid out in shared memory as the 2-D box
-// {64, wo rows} (the implicit-GEMM convolution operand, slmk::ConvB)
+// box {64, s wo, s rows, nimg}, 128-byte swizzle: one box = `rows` whole output rows of wo
+// positions (every s-th input column / row) of 64 channels -- or nimg whole images (rows = the
+// output height) -- laid out in shared memory as the 2-D box {64, wo rows nimg} (the
+// implicit-GEMM convolution operand, slmk::ConvB; rows of a box never wrap into the next image:
+// out-of-bounds rows are zero-filled)
 slm_status make_map4(CUtensorMap* map, const void* base, uint64_t c, uint64_t w, uint64_t h, uint64_t imgs,
-                     uint32_t wo, uint32_t rows, uint32_t s) {
+                     uint32_t wo, uint32_t rows, uint32_t s, uint32_t nimg) {
   EncodeTiledFn enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -136,7 +138,7 @@ slm_status make_map4(CUtensorMap* map, const void* base, uint64_t c, uint64_t w,
   }
   cuuint64_t dims[4] = {c, w, h, imgs};
   cuuint64_t strides[3] = {c * 2, w * c * 2, h * w * c * 2};
-  cuuint32_t box[4] = {64, s * wo, s * rows, 1};
+  cuuint32_t box[4] = {64, s * wo, s * rows, nimg};
   cuuint32_t es[4] = {1, s, s, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -79,8 +79,8 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 // its tiles are 4-D TMA boxes of the bf16 NHWC input x (map {cin, W, H, images}, element strides
 // {1, s, s, 1}: a box of s wo x s rows elements loads wo x rows of them).  hw, w: the OUTPUT
 // positions per image and per row.  on = 1: the K-major B operand (rows = positions, a tile = BN
-// / w whole output rows); on = 2: the MN-major A operand of the weight gradient (K = positions, a
-// 64-position K block = 64 / w output rows).
+// / w whole output rows, or BN / hw whole images); on = 2: the MN-major A operand of the weight
+// gradient (K = positions, a 64-position K block = 64 / w output rows, or 64 / hw images).
 struct ConvB {
   int on = 0, cin = 0, k = 0, hw = 0, w = 0, s = 1;
 };
