@@ -94,6 +94,10 @@ def _small_graph(slm, B, spec):
     # stride 2 implicit (element-strided 4-D boxes): 3x3 and the 1x1 projection, 16x16 -> 8x8
     [("input", 16), ("conv", 256, 3, 2)],
     [("input", 16), ("conv", 256, 1, 2), ("bn",), ("relu",)],
+    # tiles of whole images (4x4 maps: a 256-position tile = 16 images, a 64-position weight-gradient
+    # K block = 4 images), stride 1 and 2
+    [("input", 4), ("conv", 128, 3, 1), ("bn",), ("relu",), ("conv", 256, 3, 1)],
+    [("input", 8), ("conv", 128, 3, 2), ("conv", 128, 3, 1)],
 ])
 def test_conv_ops_vs_oracle_strict(slm, spec):
     """Single conv / BN stages (little depth for bf16 rounding decisions to amplify): every element
