@@ -175,16 +175,6 @@ __global__ void __launch_bounds__(256) op_gsum_kernel(GradSlices s, int B, int w
   }
 }
 
-// bf16 GEMM operand (round to nearest even): rows of width w from a source of row stride ld
-__global__ void __launch_bounds__(256) op_pack_kernel(const float* __restrict__ x, int B, int w, int ld,
-                                                      __nv_bfloat16* __restrict__ out) {
-  pdl_wait();
-  pdl_launch();
-  const size_t n = (size_t)B * w;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16_rn(x[(i / w) * ld + i % w]);
-}
-
 // contiguous fp32 -> bf16 (RN), 8 elements per thread (n8 = elements / 8)
 __global__ void __launch_bounds__(256) op_cvt_bf16_kernel(const float4* __restrict__ x, size_t n8,
                                                           uint4* __restrict__ out) {
