@@ -98,3 +98,16 @@ def test_conv_resnet_accepted_and_rejections():
     n2 = list(nodes)
     n2[fc] = (slm.OP["fc"], [pool - 1], nodes[fc][2], 0)
     assert _create_shaped(n2, shapes, B) != 0
+
+
+def test_rows_beyond_int32_rejected():
+    """The op kernels index rows (batch H W) in 32 bits: a value with >= 2^31 rows is refused at
+    model creation (runtime.cu), not overflowed at run time."""
+    B, C_ = 64, 128
+    big = 8192                                           # 64 * 8192 * 8192 = 2^32 rows
+    nodes = [(slm.OP["input"], [], B * big * big * C_ * 4, 0), (slm.OP["pool"], [0], B * C_ * 4, 0),
+             (slm.OP["fc"], [1], B * 128 * 4, 0), (slm.OP["softmax_ce"], [2], 4, 1)]
+    shapes = [(big, big, C_, 0, 0), (1, 1, C_, 0, 0), (1, 1, 128, 0, 0), (1, 1, 1, 0, 0)]
+    assert _create_shaped(nodes, shapes, B) != 0
+    small = [(slm.OP["input"], [], B * 8 * 8 * C_ * 4, 0)] + nodes[1:]
+    assert _create_shaped(small, [(8, 8, C_, 0, 0)] + shapes[1:], B) == 0
