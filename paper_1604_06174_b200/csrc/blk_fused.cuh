@@ -398,7 +398,6 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     mbar_expect_tx(recvb2, (S - 1) * C::SLICE);
     for (int s = 0; s < S; ++s) {
       if (s == (int)k) continue;
-#pragma unroll
       tma_load_2d(ring + s * C::SLICE, &tmP, recvb2, 0, ((m * S + (int)k) * S + s) * B);
     }
   }
